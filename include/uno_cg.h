@@ -1,0 +1,163 @@
+/*
+ * uno_cg.h — C ABI of libunocg.so, the B200 (sm_100a) hot path of UNO-CG
+ * (Herb & Fritzen, arXiv 2508.02681; PAPER.md in the reference tree).
+ *
+ * What the library computes
+ * -------------------------
+ * The UNO-CG hybrid solver, Alg 2: preconditioned CG on the
+ * Q1 voxel finite-element system A u = f of a two-phase periodic RVE
+ * (§3.1 Eq 20-22; thermal §5.1 Eq 74-77, elastic §5.2 Eq 78-84),
+ * preconditioned by the Unitary-Neural-Operator apply s = T^H Q T r (Eq 46-49,
+ * P:458-490) with T the orthonormal DFT (Table 1 row "Periodic") and Q
+ * the per-frequency c x c symbol G_hat(k).  Because no trained weights exist,
+ * G_hat is the FANS reference-medium Green's operator (§3.3.4 Eq 33-37)
+ * times (c = 1) / plus (c = 3) a seeded SPD perturbation.
+ *
+ * Conventions (all calls)
+ * -----------------------
+ *  - fp64 everywhere; phase fields are uint8 (0 = matrix, 1 = inclusion, §5).
+ *  - Grid: N1 (x, fastest) x N2 (y) x N3 (z) voxels, N3 = 1 in 2D; cubic voxels of
+ *    edge h.  Periodic boundaries on every axis (bc[] must be 0 in this version;
+ *    Dirichlet/mixed axes return UNO_ERR_UNSUPPORTED).  N1, N2 in {8..1024},
+ *    N3 in {1} U {4..1024}, all powers of two.
+ *  - Field layout (device): component-planar C order [nrhs][c][N3][N2][N1]; node
+ *    (i,j,k) at h*(i,j,k); voxel (i,j,k) has corners (i+a1, j+a2, k+a3) mod N.
+ *    The paper's interleaved vec() (§1.6 Eq 1) is a fixed permutation of this.
+ *  - c = 1 (thermal) or c = dim (elastic).  nrhs load cases are iterated together,
+ *    each with its own CG scalars (a converged load is frozen, so its iterates equal
+ *    an unbatched solve).
+ *  - Loads (host): thermal macroscopic gradient g_bar in R^dim; elastic macroscopic
+ *    strain eps_bar as a Mandel vector (App. A Eq A2-A4), length 3 (2D)
+ *    or 6 (3D), order (11,22,[33],sqrt2*12,[sqrt2*13,sqrt2*23]).
+ *  - Streams: every call is stream-ordered on desc.stream (a cudaStream_t owned by
+ *    the caller, e.g. torch.cuda.current_stream().cuda_stream); calls that return
+ *    host scalars synchronise that stream.
+ *  - Ownership: all field buffers (phase, u, f, r, z, ...) are caller-owned device
+ *    memory.  The handle owns its workspace (CG vectors r,d,p, one spectrum buffer,
+ *    the tabulated symbol, reduction scratch) and frees it in uno_cg_destroy.
+ *  - Errors: every call returns uno_status; on error nothing is written to the
+ *    outputs unless stated, and uno_cg_last_error() returns a thread-local message.
+ *    No C++ exception crosses the ABI.  Calls on one handle are not thread-safe.
+ */
+#ifndef UNO_CG_H
+#define UNO_CG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define UNO_API __attribute__((visibility("default")))
+#else
+#define UNO_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct uno_cg_handle uno_cg_handle; /* opaque */
+
+typedef enum {
+  UNO_OK = 0,
+  UNO_ERR_ARG = 1,         /* NULL pointer or invalid scalar argument                    */
+  UNO_ERR_SHAPE = 2,       /* grid size not supported (see Conventions)                   */
+  UNO_ERR_CUDA = 3,        /* a CUDA runtime call failed (message in uno_cg_last_error)   */
+  UNO_ERR_UNSUPPORTED = 4, /* valid per the paper but not built yet (non-periodic bc)     */
+  UNO_ERR_NOT_SPD = 5,     /* Eq 55 safety check failed at create            */
+  UNO_ERR_BREAKDOWN = 6,   /* d.p <= 0 or gamma_1 <= 0 during solve           */
+  UNO_ERR_NONFINITE = 7    /* NaN/Inf residual during solve                               */
+} uno_status;
+
+enum { UNO_THERMAL = 0, UNO_ELASTIC = 1 };
+
+typedef struct {
+  int32_t dim;        /* 2 or 3                                                          */
+  int32_t n[3];       /* voxel counts N1, N2, N3 (N3 = 1 when dim == 2)                  */
+  double h;           /* voxel edge; <= 0 means 1/N1 (unit cell)              */
+  int32_t physics;    /* UNO_THERMAL (c = 1) or UNO_ELASTIC (c = dim)                    */
+  int32_t bc[3];      /* per axis: 0 periodic (only value accepted in this version)      */
+  double mat[2][2];   /* phase 0 / phase 1: thermal {kappa, unused}; elastic {lambda, mu} */
+  double ref[2];      /* reference medium (kappa_r | lambda_r, mu_r); ref[0] <= 0 means the
+                         arithmetic mean of the phases          */
+  uint64_t seed;      /* perturbation seed; 0 = unperturbed FANS symbol                  */
+  double amp;         /* perturbation amplitude: c=1 rho in [1-amp, 1+amp];
+                         c=3 G = Phi + amp*tr(Phi)/3*psi(theta) (Eq B5)                  */
+  int32_t nrhs;       /* load cases iterated together, 1..8                              */
+  void* stream;       /* cudaStream_t (NULL = legacy default stream)                     */
+} uno_cg_desc;
+
+typedef struct {
+  int32_t iterations;  /* Alg 2 iterations performed (K applications)                      */
+  int32_t converged;   /* 1 if ||r||_inf <= rel_tol * ||r0||_inf was reached               */
+  int32_t status;      /* uno_status of this load case (BREAKDOWN / NONFINITE per load)   */
+  int32_t pad_;
+  double r0_inf;       /* ||r0||_inf = ||f||_inf                                           */
+  double rel_res;      /* final recursive ||r||_inf / ||r0||_inf                           */
+  double gamma_last;   /* last gamma_1 = r.s (Alg 2 l.7)                                   */
+} uno_cg_report;
+
+/* Create a solver for one microstructure.  Computes the reference medium, tabulates
+ * G_hat(k)/n on the R2C half spectrum (Eq 46/49/51: the unique entries v, C = c(c+1)/2
+ * planes) and runs the Eq 55 check (every block with k != 0 SPD with lambda_min > 1e-14;
+ * G_hat(0) = 0 shares the periodic null space).
+ *   d_phase: device uint8 [N3][N2][N1], caller-owned, must outlive the handle.
+ * Returns UNO_ERR_NOT_SPD (and no handle) if Eq 55 fails.                             */
+UNO_API uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_phase, uno_cg_handle** out);
+
+UNO_API uno_status uno_cg_destroy(uno_cg_handle* h);
+
+/* Galerkin right-hand side f = l(phi_i) of the decomposition Eq 76 / Eq 81:
+ *   thermal f_i = -sum_{e ni i} kappa_e (s(a).g_bar) h^(d-1)/2^(d-1)
+ *   elastic f_(i,alpha) = -sum_e sum_j s(a)_j sigma_bar^e_(alpha j) h^(d-1)/2^(d-1),
+ *           sigma_bar^e = lambda_e tr(eps_bar) I + 2 mu_e eps_bar
+ *   h_loads: host [nrhs][dim] (thermal) or [nrhs][D] (elastic, Mandel).
+ *   d_f: device [nrhs][c][N3][N2][N1].                                                  */
+UNO_API uno_status uno_cg_rhs(uno_cg_handle* h, const double* h_loads, double* d_f);
+
+/* p = A u (Alg 2 l.9) for all nrhs vectors; optional u.Au per vector.
+ *   d_u, d_Au: device [nrhs][c][N3][N2][N1] (must not alias).  h_uAu: host [nrhs] or NULL. */
+UNO_API uno_status uno_cg_apply_K(uno_cg_handle* h, const double* d_u, double* d_Au, double* h_uAu);
+
+/* z = T^H Q T r (Alg 2 l.4-6) for all nrhs vectors; optional r.z per vector (Alg 2 l.7,
+ * evaluated in the transformed space by Parseval).
+ *   d_r, d_z: device [nrhs][c][N3][N2][N1] (may alias).  h_rz: host [nrhs] or NULL.     */
+UNO_API uno_status uno_cg_apply_precond(uno_cg_handle* h, const double* d_r, double* d_z, double* h_rz);
+
+/* Alg 2 from u0 = 0 for the nrhs loads: r = f; d = 0; gamma_1 = 1; iterate while
+ * ||r||_inf > rel_tol * ||r0||_inf (relative stop on the recursive residual)
+ * and iterations < max_iter.  fixed_iters > 0 runs exactly that many iterations instead
+ * (parity protocol).  An RHS with ||f||_inf <= 1e-13 * max modulus *
+ * h^(d-1) * ||load||_inf is a zero RHS: 0 iterations, u = 0.  On return u holds the
+ * per-component mean-free solution.
+ *   h_loads: as uno_cg_rhs.  d_u: device [nrhs][c][N3][N2][N1] (output).
+ *   rep: host [nrhs] reports (may be NULL).  h_hist: host [nrhs][max_iter+1] residual
+ *   history ||r_m||_inf/||r0||_inf or NULL.
+ * Returns UNO_ERR_BREAKDOWN / UNO_ERR_NONFINITE if any load broke down (rep says which). */
+UNO_API uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, double rel_tol, int32_t max_iter,
+                        int32_t fixed_iters, double* d_u, uno_cg_report* rep, double* h_hist);
+
+/* Effective property from the nrhs solutions:
+ *   out_ij = <C>_ij - f^(i) . u^(j) / |Omega|,  |Omega| = N1 N2 N3 h^dim,
+ * thermal <C>_ij = <kappa> delta_ij (g_bar loads), elastic <C>_ij = B^(i):<D>:B^(j)
+ * evaluated for the given loads (Mandel).  f^(i) is recomputed from the phase field.
+ *   d_u: device [nrhs][c][N3][N2][N1]; h_loads as uno_cg_rhs; h_out: host [nrhs][nrhs]. */
+UNO_API uno_status uno_cg_effective_property(uno_cg_handle* h, const double* d_u, const double* h_loads, double* h_out);
+
+/* Timing of the most recent uno_cg_solve (CUDA events on desc.stream, ms), and the number
+ * of library kernels it launched.                                                       */
+UNO_API uno_status uno_cg_last_solve_stats(uno_cg_handle* h, double* ms, int64_t* kernel_launches);
+
+/* Kernel-level timing hook for bench.py: per-kernel-class accumulated device time (ms)
+ * and launch counts since create or the last reset, measured with CUDA events on
+ * desc.stream when enabled (adds an event pair per launch; off by default).
+ *   which: 0 = K apply, 1 = x-pass forward, 2 = y-pass, 3 = G pass, 4 = x-pass inverse,
+ *   5 = other.                                                                          */
+UNO_API uno_status uno_cg_kernel_timing(uno_cg_handle* h, int32_t enable, int32_t reset, double* ms6, int64_t* count6);
+
+UNO_API const char* uno_cg_last_error(void);
+UNO_API const char* uno_cg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UNO_CG_H */

@@ -131,13 +131,14 @@ class Grid:
     """Regular grid: N = (N1, N2[, N3]) elements per physical axis, bc per axis
     (0 periodic, 1 Dirichlet), c components, edge h_i = L0/N_i."""
 
-    def __init__(self, N, bc=None, c=1, L0=1.0):
+    def __init__(self, N, bc=None, c=1, L0=1.0, h=None):
         self.N = tuple(int(v) for v in N)
         self.d = len(self.N)
         self.bc = tuple(bc) if bc is not None else (0,) * self.d
         self.c = c
         self.L0 = L0
-        self.h = tuple(L0 / n for n in self.N)
+        # cubic voxels of edge h (domain N_i h per axis) when h is given, else h_i = L0 / N_i
+        self.h = tuple(float(h) for _ in self.N) if h is not None else tuple(L0 / n for n in self.N)
 
     def nax(self, i: int) -> int:
         """numpy axis (in a (c, ...) field) of physical axis i."""
@@ -160,7 +161,7 @@ class Grid:
         return (self.c,) + self.node_shape
 
     def volume(self) -> float:
-        return float(self.L0 ** self.d)
+        return float(np.prod([n * hh for n, hh in zip(self.N, self.h)]))
 
 
 def _pad_full(g: Grid, u: np.ndarray) -> np.ndarray:

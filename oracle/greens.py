@@ -126,8 +126,18 @@ def ghat(g: fem.Grid, physics: str, mat, seed: int, amp: float, ref=None) -> np.
     nz[0] = False
     Phi[nz] = np.linalg.inv(Am[nz])
     Phi = 0.5 * (Phi + np.transpose(Phi, (0, 2, 1)))
-    if seed:
-        assert c == 3, "perturbation defined for c = 3 (Eq B5)"
+    if seed and c == 2:
+        # c = 2 analogue with the Eq 45 parametrisation: theta_1,2 in [0.5,1], theta_3 in [-0.5,0.5]
+        base = (8 * can.reshape(-1)).astype(np.uint64)
+        t1 = 0.5 + 0.5 * u01(seed, 2, base)
+        t2 = 0.5 + 0.5 * u01(seed, 2, base + np.uint64(1))
+        t3 = u01(seed, 2, base + np.uint64(2)) - 0.5
+        P = np.moveaxis(np.array([[t1 * t1, t1 * t3], [t1 * t3, t2 * t2 + t3 * t3]]), -1, 0)
+        tr = np.trace(Phi, axis1=1, axis2=2) / 2.0
+        Phi = Phi + amp * tr[:, None, None] * P
+        Phi[0] = 0.0
+    elif seed:
+        assert c == 3, "perturbation defined for c = 2 (Eq 45) and c = 3 (Eq B5)"
         base = (8 * can.reshape(-1)).astype(np.uint64)
         th = np.stack([u01(seed, 2, base + np.uint64(t)) for t in range(6)])
         for t in (0, 1, 3):

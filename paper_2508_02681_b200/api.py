@@ -1,0 +1,104 @@
+"""Python-level API over the C ABI: one `UnoCG` object per microstructure.
+
+PyTorch is used only for device memory and the stream (`torch.cuda.current_stream()`);
+the solve itself is the library's.  Mirrors PAPER.md Alg 2 as exposed by
+include/uno_cg.h.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import binding as B
+
+KERNEL_CLASSES = ("K", "xfwd", "ypass", "gpass", "xinv", "other")
+
+
+@dataclass
+class SolveResult:
+    u: torch.Tensor          # [nrhs][c][N3][N2][N1] (mean-free)
+    reports: list
+    hist: np.ndarray | None
+    ms: float                # device time of the solve (CUDA events in the library)
+    launches: int            # library kernels launched by the solve
+
+
+class UnoCG:
+    def __init__(self, phase: torch.Tensor, physics: str, mat, nrhs: int, seed: int = 0, amp: float | None = None,
+                 h: float = 0.0, ref=None, stream: torch.cuda.Stream | None = None):
+        assert phase.is_cuda and phase.dtype == torch.uint8 and phase.is_contiguous()
+        self.phase = phase
+        self.dim = phase.dim()
+        shp = tuple(phase.shape)
+        self.N = tuple(reversed(shp))  # (N1, N2[, N3])
+        self.physics = physics
+        self.c = 1 if physics == "thermal" else self.dim
+        self.nrhs = nrhs
+        self.stream = stream or torch.cuda.current_stream()
+        d = B.UnoCgDesc()
+        d.dim = self.dim
+        d.n[0], d.n[1] = self.N[0], self.N[1]
+        d.n[2] = self.N[2] if self.dim == 3 else 1
+        d.h = float(h)
+        d.physics = B.UNO_THERMAL if physics == "thermal" else B.UNO_ELASTIC
+        if physics == "thermal":
+            d.mat[0][0], d.mat[1][0] = float(mat[0]), float(mat[1])
+        else:
+            (l0, m0), (l1, m1) = mat
+            d.mat[0][0], d.mat[0][1], d.mat[1][0], d.mat[1][1] = l0, m0, l1, m1
+        if ref is not None:
+            r = (ref, 0.0) if physics == "thermal" else tuple(ref)
+            d.ref[0], d.ref[1] = float(r[0]), float(r[1])
+        d.seed = int(seed)
+        d.amp = float(amp if amp is not None else (0.1 if physics == "thermal" else 0.05))
+        d.nrhs = int(nrhs)
+        d.stream = self.stream.cuda_stream
+        self.desc = d
+        self.handle = B.uno_cg_create(d, phase)
+        self.field_shape = (nrhs, self.c) + shp
+
+    def close(self):
+        if getattr(self, "handle", None):
+            B.uno_cg_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def empty(self) -> torch.Tensor:
+        return torch.empty(self.field_shape, dtype=torch.float64, device=self.phase.device)
+
+    def rhs(self, loads) -> torch.Tensor:
+        f = self.empty()
+        B.uno_cg_rhs(self.handle, loads, f)
+        return f
+
+    def apply_K(self, u: torch.Tensor, want_dot: bool = False):
+        out = self.empty()
+        dot = B.uno_cg_apply_K(self.handle, u.contiguous(), out, self.nrhs if want_dot else None)
+        return (out, dot) if want_dot else out
+
+    def apply_precond(self, r: torch.Tensor, want_dot: bool = False):
+        out = self.empty()
+        dot = B.uno_cg_apply_precond(self.handle, r.contiguous(), out, self.nrhs if want_dot else None)
+        return (out, dot) if want_dot else out
+
+    def solve(self, loads, rel_tol: float = 1e-8, max_iter: int = 1000, fixed_iters: int = 0,
+              hist: bool = False, out: torch.Tensor | None = None, raise_on_breakdown: bool = True) -> SolveResult:
+        u = out if out is not None else self.empty()
+        reps, hh = B.uno_cg_solve(self.handle, loads, rel_tol, max_iter, fixed_iters, u, self.nrhs, hist,
+                                  raise_on_breakdown)
+        ms, n = B.uno_cg_last_solve_stats(self.handle)
+        return SolveResult(u, reps, hh, ms, n)
+
+    def effective_property(self, u: torch.Tensor, loads) -> np.ndarray:
+        return B.uno_cg_effective_property(self.handle, u.contiguous(), loads, self.nrhs)
+
+    def kernel_timing(self, enable: int = -1, reset: int = 0):
+        ms, cnt = B.uno_cg_kernel_timing(self.handle, enable, reset)
+        return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(KERNEL_CLASSES)}

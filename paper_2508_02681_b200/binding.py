@@ -1,0 +1,156 @@
+"""Thin ctypes binding of libunocg.so (include/uno_cg.h) — argument marshalling only.
+
+Every function here has the name of the C entry point it wraps and does nothing but
+convert arguments; all arithmetic of the hot path runs in the CUDA kernels.  The
+library is loaded from the package's `lib/` directory (built in-tree by
+`__graft_entry__.build()`); if it is missing this module raises at import: there is
+no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libunocg.so")
+
+UNO_OK, UNO_ERR_ARG, UNO_ERR_SHAPE, UNO_ERR_CUDA, UNO_ERR_UNSUPPORTED, UNO_ERR_NOT_SPD, UNO_ERR_BREAKDOWN, \
+    UNO_ERR_NONFINITE = range(8)
+UNO_THERMAL, UNO_ELASTIC = 0, 1
+
+EXPORTS = ("uno_cg_create", "uno_cg_destroy", "uno_cg_rhs", "uno_cg_apply_K", "uno_cg_apply_precond",
+           "uno_cg_solve", "uno_cg_effective_property", "uno_cg_last_solve_stats", "uno_cg_kernel_timing",
+           "uno_cg_last_error", "uno_cg_version")
+
+
+class UnoCgDesc(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("n", C.c_int32 * 3), ("h", C.c_double), ("physics", C.c_int32),
+                ("bc", C.c_int32 * 3), ("mat", (C.c_double * 2) * 2), ("ref", C.c_double * 2),
+                ("seed", C.c_uint64), ("amp", C.c_double), ("nrhs", C.c_int32), ("stream", C.c_void_p)]
+
+
+class UnoCgReport(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("status", C.c_int32), ("pad_", C.c_int32),
+                ("r0_inf", C.c_double), ("rel_res", C.c_double), ("gamma_last", C.c_double)]
+
+
+class UnoError(RuntimeError):
+    def __init__(self, status: int, where: str, msg: str):
+        super().__init__(f"{where}: status {status}: {msg}")
+        self.status = status
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libunocg.so not built ({LIB_PATH}); run __graft_entry__.build() — no CPU fallback exists")
+    lib = C.CDLL(LIB_PATH)
+    P, D, I32, I64 = C.c_void_p, C.c_double, C.c_int32, C.c_int64
+    lib.uno_cg_create.argtypes = [C.POINTER(UnoCgDesc), P, C.POINTER(P)]
+    lib.uno_cg_destroy.argtypes = [P]
+    lib.uno_cg_rhs.argtypes = [P, P, P]
+    lib.uno_cg_apply_K.argtypes = [P, P, P, P]
+    lib.uno_cg_apply_precond.argtypes = [P, P, P, P]
+    lib.uno_cg_solve.argtypes = [P, P, D, I32, I32, P, P, P]
+    lib.uno_cg_effective_property.argtypes = [P, P, P, P]
+    lib.uno_cg_last_solve_stats.argtypes = [P, C.POINTER(D), C.POINTER(I64)]
+    lib.uno_cg_kernel_timing.argtypes = [P, I32, I32, P, P]
+    for f in EXPORTS[:-2]:
+        getattr(lib, f).restype = C.c_int
+    lib.uno_cg_last_error.restype = C.c_char_p
+    lib.uno_cg_version.restype = C.c_char_p
+    return lib
+
+
+_lib = _load()
+
+
+def _check(st: int, where: str):
+    if st != UNO_OK:
+        raise UnoError(st, where, _lib.uno_cg_last_error().decode())
+
+
+def _ptr(x) -> int | None:
+    """Device/host pointer of a torch tensor, numpy array, or int (None -> NULL)."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if isinstance(x, np.ndarray):
+        assert x.flags.c_contiguous
+        return x.ctypes.data
+    if hasattr(x, "data_ptr"):
+        assert x.is_contiguous()
+        return x.data_ptr()
+    raise TypeError(type(x))
+
+
+def _host_f64(a) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+
+
+def uno_cg_create(desc: UnoCgDesc, d_phase) -> int:
+    h = C.c_void_p()
+    _check(_lib.uno_cg_create(C.byref(desc), _ptr(d_phase), C.byref(h)), "uno_cg_create")
+    return h.value
+
+
+def uno_cg_destroy(h: int):
+    _check(_lib.uno_cg_destroy(h), "uno_cg_destroy")
+
+
+def uno_cg_rhs(h: int, loads, d_f):
+    L = _host_f64(loads)
+    _check(_lib.uno_cg_rhs(h, _ptr(L), _ptr(d_f)), "uno_cg_rhs")
+
+
+def uno_cg_apply_K(h: int, d_u, d_Au, nrhs: int | None = None):
+    out = np.zeros(nrhs) if nrhs else None
+    _check(_lib.uno_cg_apply_K(h, _ptr(d_u), _ptr(d_Au), _ptr(out)), "uno_cg_apply_K")
+    return out
+
+
+def uno_cg_apply_precond(h: int, d_r, d_z, nrhs: int | None = None):
+    out = np.zeros(nrhs) if nrhs else None
+    _check(_lib.uno_cg_apply_precond(h, _ptr(d_r), _ptr(d_z), _ptr(out)), "uno_cg_apply_precond")
+    return out
+
+
+def uno_cg_solve(h: int, loads, rel_tol: float, max_iter: int, fixed_iters: int, d_u, nrhs: int,
+                 want_hist: bool = False, raise_on_breakdown: bool = True):
+    L = _host_f64(loads)
+    reps = (UnoCgReport * nrhs)()
+    cap = fixed_iters if fixed_iters > 0 else max_iter
+    hist = np.zeros((nrhs, cap + 1)) if want_hist else None
+    st = _lib.uno_cg_solve(h, _ptr(L), float(rel_tol), int(max_iter), int(fixed_iters), _ptr(d_u), reps, _ptr(hist))
+    if st != UNO_OK and (raise_on_breakdown or st not in (UNO_ERR_BREAKDOWN, UNO_ERR_NONFINITE)):
+        _check(st, "uno_cg_solve")
+    out = [dict(iterations=r.iterations, converged=bool(r.converged), status=r.status, r0_inf=r.r0_inf,
+                rel_res=r.rel_res, gamma_last=r.gamma_last) for r in reps]
+    return out, hist
+
+
+def uno_cg_effective_property(h: int, d_u, loads, nrhs: int) -> np.ndarray:
+    L = _host_f64(loads)
+    out = np.zeros((nrhs, nrhs))
+    _check(_lib.uno_cg_effective_property(h, _ptr(d_u), _ptr(L), _ptr(out)), "uno_cg_effective_property")
+    return out
+
+
+def uno_cg_last_solve_stats(h: int):
+    ms = C.c_double()
+    n = C.c_int64()
+    _check(_lib.uno_cg_last_solve_stats(h, C.byref(ms), C.byref(n)), "uno_cg_last_solve_stats")
+    return ms.value, n.value
+
+
+def uno_cg_kernel_timing(h: int, enable: int = -1, reset: int = 0):
+    ms = np.zeros(6)
+    cnt = np.zeros(6, dtype=np.int64)
+    _check(_lib.uno_cg_kernel_timing(h, int(enable), int(reset), _ptr(ms), _ptr(cnt)), "uno_cg_kernel_timing")
+    return ms, cnt
+
+
+def uno_cg_version() -> str:
+    return _lib.uno_cg_version().decode()

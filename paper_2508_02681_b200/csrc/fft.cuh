@@ -1,0 +1,168 @@
+// fft.cuh — fp64 complex FFT of 8 interleaved sequences held in shared memory (Stockham
+// autosort, radix 4/8/16 butterflies in registers).  Used by every transform pass of the
+// UNO apply T^H Q T (Eq 47-48; cost model Eq 54).  Unnormalised: forward uses
+// e^{-2 pi i jk/L}, inverse e^{+2 pi i jk/L}; the 1/n of the unitary pair is folded into
+// the tabulated symbol.
+//
+// Shared-memory tile: element j (0..L-1) of column c (0..7) lives at
+//     idx(j, c) = 8*j + (c ^ (j & 7))
+// The XOR swizzle makes both the column-contiguous accesses of the butterflies and the
+// row-contiguous (transposing) global<->smem copies bank-conflict free for 16-byte
+// double2 elements.
+#pragma once
+#include "common.cuh"
+
+namespace uno {
+
+__device__ __forceinline__ int tidx(int j, int c) { return (j << 3) + (c ^ (j & 7)); }
+
+constexpr double kR2 = 0.70710678118654752440;   // cos(pi/4)
+constexpr double kC8 = 0.92387953251128675613;   // cos(pi/8)
+constexpr double kS8 = 0.38268343236508977173;   // sin(pi/8)
+
+template <int R> struct Dft;
+
+template <> struct Dft<2> {
+  static __device__ __forceinline__ void run(double2* v) {
+    double2 a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  }
+};
+
+template <> struct Dft<4> {
+  static __device__ __forceinline__ void run(double2* v) {
+    double2 a0 = cadd(v[0], v[2]), a1 = csub(v[0], v[2]);
+    double2 a2 = cadd(v[1], v[3]), a3 = csub(v[1], v[3]);
+    v[0] = cadd(a0, a2);
+    v[2] = csub(a0, a2);
+    v[1] = cadd(a1, mul_mi(a3));
+    v[3] = csub(a1, mul_mi(a3));
+  }
+};
+
+// w8^1 * o, w8^3 * o with w8 = e^{-i pi/4}
+__device__ __forceinline__ double2 mul_w8_1(double2 o) { return make_double2((o.x + o.y) * kR2, (o.y - o.x) * kR2); }
+__device__ __forceinline__ double2 mul_w8_3(double2 o) { return make_double2((o.y - o.x) * kR2, -(o.x + o.y) * kR2); }
+
+template <> struct Dft<8> {
+  static __device__ __forceinline__ void run(double2* v) {
+    double2 e[4] = {v[0], v[2], v[4], v[6]};
+    double2 o[4] = {v[1], v[3], v[5], v[7]};
+    Dft<4>::run(e);
+    Dft<4>::run(o);
+    double2 t1 = mul_w8_1(o[1]), t2 = mul_mi(o[2]), t3 = mul_w8_3(o[3]);
+    v[0] = cadd(e[0], o[0]);
+    v[4] = csub(e[0], o[0]);
+    v[1] = cadd(e[1], t1);
+    v[5] = csub(e[1], t1);
+    v[2] = cadd(e[2], t2);
+    v[6] = csub(e[2], t2);
+    v[3] = cadd(e[3], t3);
+    v[7] = csub(e[3], t3);
+  }
+};
+
+template <> struct Dft<16> {
+  // 4 x 4: X[k1 + 4 k2] = sum_{n2} w16^{n2 k1} w4^{n2 k2} sum_{n1} v[4 n1 + n2] w4^{n1 k1}
+  static __device__ __forceinline__ void run(double2* v) {
+    double2 a[4][4];
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) {
+      double2 t[4] = {v[n2], v[4 + n2], v[8 + n2], v[12 + n2]};
+      Dft<4>::run(t);
+#pragma unroll
+      for (int k1 = 0; k1 < 4; ++k1) a[n2][k1] = t[k1];
+    }
+    // twiddles w16^{n2 k1}
+    const double2 w1 = make_double2(kC8, -kS8), w3 = make_double2(kS8, -kC8), w9 = make_double2(-kC8, kS8);
+    a[1][1] = cmul(a[1][1], w1);
+    a[1][2] = mul_w8_1(a[1][2]);
+    a[1][3] = cmul(a[1][3], w3);
+    a[2][1] = mul_w8_1(a[2][1]);
+    a[2][2] = mul_mi(a[2][2]);
+    a[2][3] = mul_w8_3(a[2][3]);
+    a[3][1] = cmul(a[3][1], w3);
+    a[3][2] = mul_w8_3(a[3][2]);
+    a[3][3] = cmul(a[3][3], w9);
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+      double2 t[4] = {a[0][k1], a[1][k1], a[2][k1], a[3][k1]};
+      Dft<4>::run(t);
+#pragma unroll
+      for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = t[k2];
+    }
+  }
+};
+
+__host__ __device__ constexpr int pick_radix(int rem) {
+  return (rem == 32 || rem == 64 || rem == 512) ? 8 : (rem >= 16 ? 16 : rem);
+}
+__host__ __device__ constexpr int min_radix(int L, int ns = 1) {
+  return ns >= L ? 1 << 30
+                 : (pick_radix(L / ns) < min_radix(L, ns * pick_radix(L / ns)) ? pick_radix(L / ns)
+                                                                                : min_radix(L, ns * pick_radix(L / ns)));
+}
+// threads needed so that every Stockham stage has one butterfly per thread
+__host__ __device__ constexpr int fft_threads(int L) { return (8 * L / min_radix(L)) < 64 ? 64 : 8 * L / min_radix(L); }
+
+// One Stockham stage (radix R, span NS) over the 8 columns of the tile, in place.
+template <int L, int R, int NS, bool INV>
+__device__ __forceinline__ void fft_stage(double2* s, const double2* __restrict__ tw) {
+  constexpr int NJ = L / R;
+  constexpr int ITEMS = NJ * kTile;
+  const int t = threadIdx.x;
+  const bool act = t < ITEMS;
+  const int c = t & 7, j = t >> 3;
+  const int k = j % NS;
+  double2 v[R];
+  if (act) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = s[tidx(j + r * NJ, c)];
+    if (NS > 1) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        double2 w = tw[r * k * (L / (NS * R))];
+        if (INV) w.y = -w.y;
+        v[r] = cmul(v[r], w);
+      }
+    }
+    if (INV) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r].y = -v[r].y;
+    }
+    Dft<R>::run(v);
+    if (INV) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r].y = -v[r].y;
+    }
+  }
+  __syncthreads();
+  if (act) {
+    const int base = (j / NS) * NS * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) s[tidx(base + r * NS, c)] = v[r];
+  }
+  __syncthreads();
+}
+
+template <int L, int NS, bool INV>
+struct FftStages {
+  static __device__ __forceinline__ void run(double2* s, const double2* tw) {
+    constexpr int R = pick_radix(L / NS);
+    fft_stage<L, R, NS, INV>(s, tw);
+    FftStages<L, NS * R, INV>::run(s, tw);
+  }
+};
+template <int L, bool INV>
+struct FftStages<L, L, INV> {
+  static __device__ __forceinline__ void run(double2*, const double2*) {}
+};
+
+// Full length-L transform of the 8 tile columns.  Caller syncs before (data in smem).
+template <int L, bool INV>
+__device__ __forceinline__ void fft_tile(double2* s, const double2* tw) {
+  FftStages<L, 1, INV>::run(s, tw);
+}
+
+}  // namespace uno

@@ -1,0 +1,1325 @@
+// kernels.cu — the UNO-CG hot path on B200 (sm_100a), fp64.
+//
+// Per PCG iteration (Alg 2) five transform passes and one stencil
+// kernel run, with the CG vector updates fused into them:
+//   F1 xfwd  (CG):  r -= alpha p ; ||r||_inf ; x-axis R2C FFT           (Alg 2 l.11, l.3, l.4)
+//   F2 ypass (fwd): y-axis complex FFT                                   (l.4)
+//   F3 gpass:       z FFT -> s_hat = G_hat r_hat, gamma_1 (Parseval) -> inverse z FFT
+//                                                                        (l.4-7, Eq 46/49)
+//   F4 ypass (inv): y-axis inverse FFT                                   (l.6)
+//   F5 xinv  (CG):  x-axis C2R -> s ; u += alpha_prev d_old ; d = s + beta d   (l.6, 8, 12)
+//   K  kapply (CG): p = A d (matrix-free Q1 gather, no atomics) ; d.p ; alpha  (l.9-10)
+// Scalars (alpha, beta, gamma, ||r||) are produced on the device by the last CTA of the
+// reducing kernel (deterministic fixed-order combine), so the host never waits inside the
+// loop.  In 2D the G pass runs along y directly after F1 (3 passes).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <type_traits>
+
+#include "common.cuh"
+#include "fft.cuh"
+#include "kernels.cuh"
+
+namespace uno {
+
+enum { ST_OK = 0, ST_BREAKDOWN = 6, ST_NONFINITE = 7 };
+
+__device__ __forceinline__ double* red_partials(const Scratch& sc, int slot, int load) {
+  return sc.partials + ((long long)slot * kMaxRhs + load) * sc.max_blocks;
+}
+__device__ __forceinline__ unsigned* red_counter(const Scratch& sc, int slot, int load) {
+  return sc.counters + slot * kMaxRhs + load;
+}
+
+// ------------------------------------------------------------------------------ scalar logic
+// F1 last CTA: stopping test of Alg 2 l.3 with the relative reading.
+__device__ void scalar_after_rnorm(LoadState* st, double rn, double* hist, int hist_stride, int load) {
+  st->rn = rn;
+  if (!isfinite(rn)) {
+    st->status = ST_NONFINITE;
+    st->active = 0;
+    return;
+  }
+  const int it = st->iters;
+  if (it == 0) {
+    st->r0 = rn;
+    st->tol_abs = st->rel_tol * rn;
+    if (rn <= st->zero_floor) {  // all-zero RHS up to assembly round-off
+      st->active = 0;
+      st->converged = 1;
+    } else if (st->fixed_iters <= 0 && st->max_iter <= 0) {
+      st->active = 0;
+    }
+  } else if (st->fixed_iters > 0) {
+    if (it >= st->fixed_iters) {
+      st->active = 0;
+      st->converged = rn <= st->tol_abs;
+    }
+  } else {
+    if (rn <= st->tol_abs) {
+      st->active = 0;
+      st->converged = 1;
+    } else if (it >= st->max_iter) {
+      st->active = 0;
+    }
+  }
+  if (hist && it < hist_stride) hist[(long long)load * hist_stride + it] = st->r0 > 0 ? rn / st->r0 : 0.0;
+}
+
+// G-pass last CTA: gamma_0 <- gamma_1 ; gamma_1 <- r.s ; beta = gamma_1 / gamma_0 (Alg 2 l.7-8).
+__device__ void scalar_after_gamma(LoadState* st, double g1) {
+  if (!isfinite(g1)) {
+    st->status = ST_NONFINITE;
+    st->active = 0;
+    return;
+  }
+  if (!(g1 > 0.0)) {
+    st->status = ST_BREAKDOWN;
+    st->active = 0;
+    return;
+  }
+  const double g0 = st->iters == 0 ? 1.0 : st->gamma1;
+  st->gamma0 = g0;
+  st->gamma1 = g1;
+  st->beta = st->iters == 0 ? 0.0 : g1 / g0;
+}
+
+// K last CTA: alpha = gamma_1 / (d.p) (Alg 2 l.10).
+__device__ void scalar_after_dp(LoadState* st, double dp) {
+  st->dp = dp;
+  if (!isfinite(dp)) {
+    st->status = ST_NONFINITE;
+    st->active = 0;
+    st->pending_u = 0;
+    return;
+  }
+  if (!(dp > 0.0)) {
+    st->status = ST_BREAKDOWN;
+    st->active = 0;
+    st->pending_u = 0;
+    return;
+  }
+  st->alpha = st->gamma1 / dp;
+  st->iters += 1;
+  st->pending_u = 1;
+}
+
+// ============================================================================== x passes
+template <int M>
+__host__ __device__ constexpr int xsmem_bytes() {
+  return (8 * M + M + (M + 1)) * (int)sizeof(double2);
+}
+
+// F1 / standalone forward: real rows of length N1 = 2M -> half spectrum [kx][z][y].
+template <int M, int MODE>
+__global__ void __launch_bounds__(fft_threads(M)) xfwd_kernel(Ctx cx, const double* __restrict__ src) {
+  const Geo g = cx.g;
+  const int load = blockIdx.y;
+  LoadState* st = cx.st + load;
+  if (MODE == CG && !st->active) return;
+  extern __shared__ double2 smem[];
+  double2* tile = smem;
+  double2* tw = smem + 8 * M;
+  double2* twp = tw + M;
+  __shared__ double red_sh[32];
+  const int T = blockDim.x, t = threadIdx.x;
+  for (int i = t; i < M; i += T) tw[i] = cx.tw.x[i];
+  for (int i = t; i <= M; i += T) twp[i] = cx.tw.xpost[i];
+
+  const long long row0 = (long long)blockIdx.x * 8;  // row = (comp, z, y) within the load
+  const long long voff = (long long)load * g.c * g.n + row0 * g.N1;
+  const double2* src2 = reinterpret_cast<const double2*>(src + voff);
+  double2* r2 = reinterpret_cast<double2*>(cx.r + voff);
+  const double2* p2 = reinterpret_cast<const double2*>(cx.p + voff);
+  bool upd = false;
+  double alpha = 0.0;
+  if (MODE == CG) {
+    upd = st->iters > 0;
+    alpha = st->alpha;
+  }
+  double mx = 0.0;
+  for (int e = t; e < 8 * M; e += T) {
+    const int row = e / M, j = e & (M - 1);
+    double2 v = src2[e];
+    if (MODE == CG && upd) {  // r <- r - alpha p   (Alg 2 l.11)
+      const double2 pv = p2[e];
+      v.x = fma(-alpha, pv.x, v.x);
+      v.y = fma(-alpha, pv.y, v.y);
+      r2[e] = v;
+    }
+    mx = fmax(mx, fmax(fabs(v.x), fabs(v.y)));
+    tile[tidx(j, row)] = v;
+  }
+  __syncthreads();
+  fft_tile<M, false>(tile, tw);
+
+  const int y0 = (int)(row0 % g.N2);
+  const long long zc = row0 / g.N2;
+  const int z = (int)(zc % g.N3);
+  const int comp = (int)(zc / g.N3);
+  double2* out = cx.spec + ((long long)load * g.c + comp) * g.nspec + (long long)z * g.N2 + y0;
+  const long long plane = (long long)g.N3 * g.N2;
+  for (int it = t; it < (M / 2 + 1) * 8; it += T) {
+    const int row = it & 7, k = it >> 3;
+    const double2 a = tile[tidx(k, row)];
+    const double2 b = cconj(tile[tidx((M - k) & (M - 1), row)]);
+    const double2 E = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
+    const double2 O = mul_mi(make_double2(0.5 * (a.x - b.x), 0.5 * (a.y - b.y)));
+    out[(long long)k * plane + row] = cadd(E, cmul(twp[k], O));
+    if (k != M - k) out[(long long)(M - k) * plane + row] = cadd(cconj(E), cmul(twp[M - k], cconj(O)));
+  }
+  if (MODE == CG) {
+    double tot;
+    if (grid_reduce<true>(mx, red_partials(cx.sc, RED_RNORM, load), red_counter(cx.sc, RED_RNORM, load), gridDim.x,
+                          blockIdx.x, &tot, red_sh)) {
+      if (threadIdx.x == 0) scalar_after_rnorm(st, tot, cx.hist, cx.hist_stride, load);
+    }
+  }
+}
+
+// F5 / standalone inverse: half spectrum -> real rows; CG epilogue d = s + beta d, u += alpha d_old.
+template <int M, int MODE>
+__global__ void __launch_bounds__(fft_threads(M)) xinv_kernel(Ctx cx, double* __restrict__ dst) {
+  const Geo g = cx.g;
+  const int load = blockIdx.y;
+  LoadState* st = cx.st + load;
+  if (MODE == CG && !st->active) return;
+  extern __shared__ double2 smem[];
+  double2* tile = smem;
+  double2* tw = smem + 8 * M;
+  double2* twp = tw + M;
+  const int T = blockDim.x, t = threadIdx.x;
+  for (int i = t; i < M; i += T) tw[i] = cx.tw.x[i];
+  for (int i = t; i <= M; i += T) twp[i] = cx.tw.xpost[i];
+  __syncthreads();
+
+  const long long row0 = (long long)blockIdx.x * 8;
+  const int y0 = (int)(row0 % g.N2);
+  const long long zc = row0 / g.N2;
+  const int z = (int)(zc % g.N3);
+  const int comp = (int)(zc / g.N3);
+  const double2* in = cx.spec + ((long long)load * g.c + comp) * g.nspec + (long long)z * g.N2 + y0;
+  const long long plane = (long long)g.N3 * g.N2;
+  for (int it = t; it < (M / 2 + 1) * 8; it += T) {
+    const int row = it & 7, k = it >> 3;
+    if (k == 0) {
+      const double X0 = in[row].x, XM = in[(long long)M * plane + row].x;
+      tile[tidx(0, row)] = make_double2(X0 + XM, X0 - XM);
+    } else {
+      const double2 a = in[(long long)k * plane + row];
+      const double2 bm = in[(long long)(M - k) * plane + row];
+      const double2 b = cconj(bm);
+      const double2 E = cadd(a, b);
+      const double2 O = cmul(csub(a, b), cconj(twp[k]));
+      tile[tidx(k, row)] = cadd(E, mul_pi(O));
+      if (k != M - k) {
+        const double2 a2 = bm, b2 = cconj(a);
+        const double2 E2 = cadd(a2, b2);
+        const double2 O2 = cmul(csub(a2, b2), cconj(twp[M - k]));
+        tile[tidx(M - k, row)] = cadd(E2, mul_pi(O2));
+      }
+    }
+  }
+  __syncthreads();
+  fft_tile<M, true>(tile, tw);
+
+  const long long voff = (long long)load * g.c * g.n + row0 * g.N1;
+  if (MODE == STANDALONE) {
+    double2* o2 = reinterpret_cast<double2*>(dst + voff);
+    for (int e = t; e < 8 * M; e += T) o2[e] = tile[tidx(e & (M - 1), e / M)];
+  } else {
+    double2* d2 = reinterpret_cast<double2*>(cx.d + voff);
+    double2* u2 = reinterpret_cast<double2*>(cx.u + voff);
+    const int it0 = st->iters;
+    const double beta = st->beta, alpha = st->alpha;
+    for (int e = t; e < 8 * M; e += T) {
+      const double2 s = tile[tidx(e & (M - 1), e / M)];
+      if (it0 == 0) {
+        d2[e] = s;  // d = s + (gamma1/gamma0) * 0   (Alg 2 l.2, l.8)
+      } else {
+        const double2 dold = d2[e];
+        double2 uu = u2[e];  // deferred u += alpha_{m-1} d_{m-1}  (Alg 2 l.12)
+        uu.x = fma(alpha, dold.x, uu.x);
+        uu.y = fma(alpha, dold.y, uu.y);
+        u2[e] = uu;
+        d2[e] = make_double2(fma(beta, dold.x, s.x), fma(beta, dold.y, s.y));
+      }
+    }
+  }
+}
+
+// ============================================================================== y pass (3D)
+template <int L>
+__host__ __device__ constexpr int ysmem_bytes() {
+  return (8 * L + L) * (int)sizeof(double2);
+}
+
+template <int L, bool INV, int MODE>
+__global__ void __launch_bounds__(fft_threads(L)) ypass_kernel(Ctx cx) {
+  const Geo g = cx.g;
+  const int load = blockIdx.y;
+  if (MODE == CG && !cx.st[load].active) return;
+  extern __shared__ double2 smem[];
+  double2* tile = smem;
+  double2* tw = smem + 8 * L;
+  const int T = blockDim.x, t = threadIdx.x;
+  for (int i = t; i < L; i += T) tw[i] = cx.tw.y[i];
+  const long long nrows = (long long)g.c * g.H1 * g.N3;
+  const long long row0 = (long long)blockIdx.x * 8;
+  double2* base = cx.spec + (long long)load * g.c * g.nspec + row0 * L;
+  for (int e = t; e < 8 * L; e += T) {
+    const int row = e / L, j = e & (L - 1);
+    tile[tidx(j, row)] = (row0 + row < nrows) ? base[e] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  fft_tile<L, INV>(tile, tw);
+  for (int e = t; e < 8 * L; e += T) {
+    const int row = e / L, j = e & (L - 1);
+    if (row0 + row < nrows) base[e] = tile[tidx(j, row)];
+  }
+}
+
+// ============================================================================== G multiply
+// s_hat(k) = G_hat(k) r_hat(k) on one bin; returns w_k Re(r_hat^H G_hat r_hat) (Parseval term).
+// gtab holds the unique entries in Eq B7 order: v1=G11 v2=G22 v3=G12 v4=G33 v5=G23 v6=G13.
+template <int NC>
+__device__ __forceinline__ double gmul_bin(double2* const* tiles, int ti, const double* __restrict__ gtab,
+                                           long long nspec, long long b, double w) {
+  if (NC == 1) {
+    const double gv = __ldg(gtab + b);
+    double2 X = tiles[0][ti];
+    const double q = w * gv * fma(X.x, X.x, X.y * X.y);
+    tiles[0][ti] = make_double2(gv * X.x, gv * X.y);
+    return q;
+  } else if (NC == 2) {
+    const double v1 = __ldg(gtab + b), v2 = __ldg(gtab + nspec + b), v3 = __ldg(gtab + 2 * nspec + b);
+    const double2 X1 = tiles[0][ti], X2 = tiles[1][ti];
+    const double2 Y1 = make_double2(fma(v1, X1.x, v3 * X2.x), fma(v1, X1.y, v3 * X2.y));
+    const double2 Y2 = make_double2(fma(v3, X1.x, v2 * X2.x), fma(v3, X1.y, v2 * X2.y));
+    tiles[0][ti] = Y1;
+    tiles[1][ti] = Y2;
+    return w * (X1.x * Y1.x + X1.y * Y1.y + X2.x * Y2.x + X2.y * Y2.y);
+  } else {
+    const double v1 = __ldg(gtab + b), v2 = __ldg(gtab + nspec + b), v3 = __ldg(gtab + 2 * nspec + b);
+    const double v4 = __ldg(gtab + 3 * nspec + b), v5 = __ldg(gtab + 4 * nspec + b), v6 = __ldg(gtab + 5 * nspec + b);
+    const double2 X1 = tiles[0][ti], X2 = tiles[1][ti], X3 = tiles[2][ti];
+    double2 Y1, Y2, Y3;
+    Y1.x = fma(v1, X1.x, fma(v3, X2.x, v6 * X3.x));
+    Y1.y = fma(v1, X1.y, fma(v3, X2.y, v6 * X3.y));
+    Y2.x = fma(v3, X1.x, fma(v2, X2.x, v5 * X3.x));
+    Y2.y = fma(v3, X1.y, fma(v2, X2.y, v5 * X3.y));
+    Y3.x = fma(v6, X1.x, fma(v5, X2.x, v4 * X3.x));
+    Y3.y = fma(v6, X1.y, fma(v5, X2.y, v4 * X3.y));
+    tiles[0][ti] = Y1;
+    tiles[1][ti] = Y2;
+    tiles[2][ti] = Y3;
+    return w * (X1.x * Y1.x + X1.y * Y1.y + X2.x * Y2.x + X2.y * Y2.y + X3.x * Y3.x + X3.y * Y3.y);
+  }
+}
+
+__device__ __forceinline__ double parseval_w(int kx, int M) { return (kx == 0 || kx == M) ? 1.0 : 2.0; }
+
+__device__ void gamma_finish(const Ctx& cx, int load, double part, double* red_sh, int mode) {
+  double tot;
+  if (grid_reduce<false>(part, red_partials(cx.sc, RED_GAMMA, load), red_counter(cx.sc, RED_GAMMA, load),
+                         gridDim.x, blockIdx.x, &tot, red_sh)) {
+    if (threadIdx.x == 0) {
+      if (mode == CG)
+        scalar_after_gamma(cx.st + load, tot);
+      else
+        cx.sc.results[RED_GAMMA * kMaxRhs + load] = tot;
+    }
+  }
+}
+
+template <int L, int NC>
+__host__ __device__ constexpr int gsmem_bytes() {
+  return (NC * 8 * L + L) * (int)sizeof(double2);
+}
+
+// 3D G pass: sequences along z (stride N2), tile = 8 consecutive y of one kx plane.
+template <int L, int NC, int MODE>
+__global__ void __launch_bounds__(fft_threads(L)) gpass_z_kernel(Ctx cx) {
+  const Geo g = cx.g;
+  const int load = blockIdx.y;
+  if (MODE == CG && !cx.st[load].active) return;
+  extern __shared__ double2 smem[];
+  double2* tiles[NC];
+#pragma unroll
+  for (int q = 0; q < NC; ++q) tiles[q] = smem + q * 8 * L;
+  double2* tw = smem + NC * 8 * L;
+  __shared__ double red_sh[32];
+  const int T = blockDim.x, t = threadIdx.x;
+  for (int i = t; i < L; i += T) tw[i] = cx.tw.z[i];
+  const int ntile_y = g.N2 >> 3;
+  const int kx = blockIdx.x / ntile_y;
+  const int y0 = (blockIdx.x - kx * ntile_y) * 8;
+  const long long boff = (long long)kx * g.N3 * g.N2 + y0;
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    const double2* base = cx.spec + ((long long)load * g.c + q) * g.nspec + boff;
+    for (int e = t; e < 8 * L; e += T) {
+      const int j = e >> 3, c = e & 7;
+      tiles[q][tidx(j, c)] = base[(long long)j * g.N2 + c];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NC; ++q) fft_tile<L, false>(tiles[q], tw);
+  const double w = parseval_w(kx, g.M);
+  double part = 0.0;
+  for (int e = t; e < 8 * L; e += T) {
+    const int j = e >> 3, c = e & 7;
+    part += gmul_bin<NC>(tiles, tidx(j, c), cx.gtab, g.nspec, boff + (long long)j * g.N2 + c, w);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NC; ++q) fft_tile<L, true>(tiles[q], tw);
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    double2* base = cx.spec + ((long long)load * g.c + q) * g.nspec + boff;
+    for (int e = t; e < 8 * L; e += T) {
+      const int j = e >> 3, c = e & 7;
+      base[(long long)j * g.N2 + c] = tiles[q][tidx(j, c)];
+    }
+  }
+  gamma_finish(cx, load, part, red_sh, MODE);
+}
+
+// 2D G pass: sequences along y (contiguous), tile = 8 consecutive kx rows.
+template <int L, int NC, int MODE>
+__global__ void __launch_bounds__(fft_threads(L)) gpass_y2d_kernel(Ctx cx) {
+  const Geo g = cx.g;
+  const int load = blockIdx.y;
+  if (MODE == CG && !cx.st[load].active) return;
+  extern __shared__ double2 smem[];
+  double2* tiles[NC];
+#pragma unroll
+  for (int q = 0; q < NC; ++q) tiles[q] = smem + q * 8 * L;
+  double2* tw = smem + NC * 8 * L;
+  __shared__ double red_sh[32];
+  const int T = blockDim.x, t = threadIdx.x;
+  for (int i = t; i < L; i += T) tw[i] = cx.tw.y[i];
+  const int kx0 = blockIdx.x * 8;
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    const double2* base = cx.spec + ((long long)load * g.c + q) * g.nspec + (long long)kx0 * L;
+    for (int e = t; e < 8 * L; e += T) {
+      const int row = e / L, j = e & (L - 1);
+      tiles[q][tidx(j, row)] = (kx0 + row < g.H1) ? base[e] : make_double2(0.0, 0.0);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NC; ++q) fft_tile<L, false>(tiles[q], tw);
+  double part = 0.0;
+  for (int e = t; e < 8 * L; e += T) {
+    const int row = e & 7, j = e >> 3;
+    const int kx = kx0 + row;
+    if (kx < g.H1) part += gmul_bin<NC>(tiles, tidx(j, row), cx.gtab, g.nspec, (long long)kx * L + j, parseval_w(kx, g.M));
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NC; ++q) fft_tile<L, true>(tiles[q], tw);
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    double2* base = cx.spec + ((long long)load * g.c + q) * g.nspec + (long long)kx0 * L;
+    for (int e = t; e < 8 * L; e += T) {
+      const int row = e / L, j = e & (L - 1);
+      if (kx0 + row < g.H1) base[e] = tiles[q][tidx(j, row)];
+    }
+  }
+  gamma_finish(cx, load, part, red_sh, MODE);
+}
+
+// ============================================================================== K apply
+__device__ void dp_finish(const Ctx& cx, int load, int nblk, int my, double part, double* red_sh, int mode) {
+  double tot;
+  if (grid_reduce<false>(part, red_partials(cx.sc, RED_DP, load), red_counter(cx.sc, RED_DP, load), nblk, my, &tot,
+                         red_sh)) {
+    if (threadIdx.x == 0) {
+      if (mode == CG)
+        scalar_after_dp(cx.st + load, tot);
+      else
+        cx.sc.results[RED_DP * kMaxRhs + load] = tot;
+    }
+  }
+}
+
+// Thermal 3D, cubic voxels.  For node i with octant elements o (conductivity k_o), the Q1
+// element row (App. A1: h{1/3, 0, -1/12, -1/12}) gives
+//   p_i = h/12 [ 5 d_i sum_o k_o + sum_{6 axis nbrs j} d_j (sum of k over the 4 octants
+//         sharing edge ij) - sum_o k_o S_o ],   S_o = sum of the 8 corner values of o.
+// CTA = TX x 8 nodes marching over ZC z-planes with a 3-plane smem ring (2.5D blocking).
+constexpr int KT_TY = 8;
+__global__ void __launch_bounds__(256) kp_thermal3d_kernel(Ctx cx, int mode, const double* __restrict__ src,
+                                                           double* __restrict__ dst, int TX, int ZC) {
+  const Geo g = cx.g;
+  const int nzc = g.N3 / ZC;
+  const int load = blockIdx.z / nzc;
+  const int zcI = blockIdx.z - load * nzc;
+  if (mode == CG && !cx.st[load].active) return;
+  extern __shared__ double ksm[];
+  const int DW = TX + 2, EW = TX + 1;
+  double* D = ksm;                       // [3][10][DW]
+  double* Kp = D + 3 * 10 * DW;          // [2][9][EW]
+  double* Q = Kp + 2 * 9 * EW;           // [3][9][EW]
+  __shared__ double red_sh[32];
+  const int t = threadIdx.x, T = blockDim.x;
+  const int tx = t % TX, ty = t / TX;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * KT_TY, zs = zcI * ZC;
+  const double* dv = src + (long long)load * g.n;
+  const double k0 = cx.mat[0][0], k1 = cx.mat[1][0];
+  const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
+
+  auto load_plane = [&](int zz, int slot) {
+    const int zw = (zz + N3) % N3;
+    double* Ds = D + slot * 10 * DW;
+    for (int i = t; i < 10 * DW; i += T) {
+      const int ly = i / DW, lx = i - ly * DW;
+      const int gx = (x0 - 1 + lx + N1) & (N1 - 1), gy = (y0 - 1 + ly + N2) & (N2 - 1);
+      Ds[i] = __ldg(dv + ((long long)zw * N2 + gy) * N1 + gx);
+    }
+  };
+  auto load_kappa = [&](int layer, int slot) {
+    const int zw = (layer + N3) % N3;
+    double* Ks = Kp + slot * 9 * EW;
+    for (int i = t; i < 9 * EW; i += T) {
+      const int ly = i / EW, lx = i - ly * EW;
+      const int gx = (x0 - 1 + lx + N1) & (N1 - 1), gy = (y0 - 1 + ly + N2) & (N2 - 1);
+      Ks[i] = __ldg(cx.phase + ((long long)zw * N2 + gy) * N1 + gx) ? k1 : k0;
+    }
+  };
+  auto compute_Q = [&](int slot) {
+    const double* Ds = D + slot * 10 * DW;
+    double* Qs = Q + slot * 9 * EW;
+    for (int i = t; i < 9 * EW; i += T) {
+      const int ly = i / EW, lx = i - ly * EW;
+      const double* r0 = Ds + ly * DW + lx;
+      Qs[i] = (r0[0] + r0[1]) + (r0[DW] + r0[DW + 1]);
+    }
+  };
+  // prologue: node planes zs-1, zs ; element layer zs-1
+  load_plane(zs - 1, 0);
+  load_plane(zs, 1);
+  load_kappa(zs - 1, 0);
+  __syncthreads();
+  compute_Q(0);
+  compute_Q(1);
+  double part = 0.0;
+  const double hc = g.h / 12.0;
+  for (int k = zs; k < zs + ZC; ++k) {
+    const int q = k - zs;                       // plane k-1 -> slot q%3, k -> (q+1)%3, k+1 -> (q+2)%3
+    const int sm1 = q % 3, s0 = (q + 1) % 3, sp1 = (q + 2) % 3;
+    const int klo = q & 1, khi = (q + 1) & 1;   // layers k-1, k
+    load_plane(k + 1, sp1);
+    load_kappa(k, khi);
+    __syncthreads();
+    compute_Q(sp1);
+    __syncthreads();
+    {
+      const double* Klo = Kp + klo * 9 * EW + ty * EW + tx;
+      const double* Khi = Kp + khi * 9 * EW + ty * EW + tx;
+      const double a000 = Klo[0], a001 = Klo[1], a010 = Klo[EW], a011 = Klo[EW + 1];  // [oz][oy][ox]
+      const double a100 = Khi[0], a101 = Khi[1], a110 = Khi[EW], a111 = Khi[EW + 1];
+      const double* Qm = Q + sm1 * 9 * EW + ty * EW + tx;
+      const double* Q0 = Q + s0 * 9 * EW + ty * EW + tx;
+      const double* Qp = Q + sp1 * 9 * EW + ty * EW + tx;
+      const double S000 = Qm[0] + Q0[0], S001 = Qm[1] + Q0[1], S010 = Qm[EW] + Q0[EW], S011 = Qm[EW + 1] + Q0[EW + 1];
+      const double S100 = Q0[0] + Qp[0], S101 = Q0[1] + Qp[1], S110 = Q0[EW] + Qp[EW], S111 = Q0[EW + 1] + Qp[EW + 1];
+      const double Kxp = (a001 + a011) + (a101 + a111);
+      const double Kyp = (a010 + a011) + (a110 + a111);
+      const double Kzp = (a100 + a101) + (a110 + a111);
+      const double Ksum = (a000 + a001) + (a010 + a011) + (a100 + a101) + (a110 + a111);
+      double KS = a000 * S000;
+      KS = fma(a001, S001, KS);
+      KS = fma(a010, S010, KS);
+      KS = fma(a011, S011, KS);
+      KS = fma(a100, S100, KS);
+      KS = fma(a101, S101, KS);
+      KS = fma(a110, S110, KS);
+      KS = fma(a111, S111, KS);
+      const double* Dc = D + s0 * 10 * DW + (ty + 1) * DW + (tx + 1);
+      const double di = Dc[0];
+      const double dzm = D[sm1 * 10 * DW + (ty + 1) * DW + (tx + 1)];
+      const double dzp = D[sp1 * 10 * DW + (ty + 1) * DW + (tx + 1)];
+      double EE = Kxp * Dc[1];
+      EE = fma(Ksum - Kxp, Dc[-1], EE);
+      EE = fma(Kyp, Dc[DW], EE);
+      EE = fma(Ksum - Kyp, Dc[-DW], EE);
+      EE = fma(Kzp, dzp, EE);
+      EE = fma(Ksum - Kzp, dzm, EE);
+      const double pv = hc * (fma(5.0 * di, Ksum, EE) - KS);
+      const int gx = x0 + tx, gy = y0 + ty;
+      if (gx < N1) {
+        dst[(long long)load * g.n + ((long long)k * N2 + gy) * N1 + gx] = pv;
+        part = fma(di, pv, part);
+      }
+    }
+    __syncthreads();
+  }
+  const int nblk = gridDim.x * gridDim.y * nzc;
+  const int my = (zcI * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  dp_finish(cx, load, nblk, my, part, red_sh, mode);
+}
+
+// Thermal 2D: element row (App. A1: {2/3, -1/6, -1/3}) ->
+//   p_i = 1/6 [ 6 d_i sum_o k_o + sum_{4 axis nbrs} d_j (k of the 2 octants on edge ij) - 2 sum_o k_o S_o ].
+__global__ void __launch_bounds__(256) kp_thermal2d_kernel(Ctx cx, int mode, const double* __restrict__ src,
+                                                           double* __restrict__ dst) {
+  const Geo g = cx.g;
+  const int load = blockIdx.y;
+  if (mode == CG && !cx.st[load].active) return;
+  __shared__ double red_sh[32];
+  const int N1 = g.N1, N2 = g.N2;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  double part = 0.0;
+  if (i < g.n) {
+    const int x = (int)(i % N1), y = (int)(i / N1);
+    const double* dv = src + (long long)load * g.n;
+    const int xm = (x - 1 + N1) & (N1 - 1), xp = (x + 1) & (N1 - 1), ym = (y - 1 + N2) & (N2 - 1), yp = (y + 1) & (N2 - 1);
+    auto D = [&](int xx, int yy) { return __ldg(dv + (long long)yy * N1 + xx); };
+    auto KAP = [&](int xx, int yy) { return __ldg(cx.phase + (long long)yy * N1 + xx) ? cx.mat[1][0] : cx.mat[0][0]; };
+    const double a00 = KAP(xm, ym), a01 = KAP(x, ym), a10 = KAP(xm, y), a11 = KAP(x, y);  // [oy][ox]
+    const double dmm = D(xm, ym), d0m = D(x, ym), dpm = D(xp, ym);
+    const double dm0 = D(xm, y), d00 = D(x, y), dp0 = D(xp, y);
+    const double dmp = D(xm, yp), d0p = D(x, yp), dpp = D(xp, yp);
+    const double S00 = (dmm + d0m) + (dm0 + d00), S01 = (d0m + dpm) + (d00 + dp0);
+    const double S10 = (dm0 + d00) + (dmp + d0p), S11 = (d00 + dp0) + (d0p + dpp);
+    const double Ksum = (a00 + a01) + (a10 + a11);
+    const double KS = fma(a00, S00, fma(a01, S01, fma(a10, S10, a11 * S11)));
+    double EE = (a01 + a11) * dp0;
+    EE = fma(a00 + a10, dm0, EE);
+    EE = fma(a10 + a11, d0p, EE);
+    EE = fma(a00 + a01, d0m, EE);
+    const double pv = (fma(6.0 * d00, Ksum, EE) - 2.0 * KS) * (1.0 / 6.0);
+    dst[(long long)load * g.n + i] = pv;
+    part = d00 * pv;
+  }
+  dp_finish(cx, load, gridDim.x, blockIdx.x, part, red_sh, mode);
+}
+
+// Elastic (c = dim): node-centric gather with the two phase element matrices
+// K^(ph) = lambda_ph K_lambda + mu_ph K_mu (Eq 80) resident in shared memory.
+//   p_(i,alpha) = sum_o sum_(b,beta) K^(ph_o)[(a_o,alpha),(b,beta)] d_(i-1+o+b, beta),  a_o = 1 - o.
+// (v1: direct 576-FMA gather; the Walsh-Hadamard modal form is the planned faster variant.)
+
+constexpr int KE_TX = 16, KE_TY = 8;
+__global__ void __launch_bounds__(128) kp_elastic3d_kernel(Ctx cx, int mode, const double* __restrict__ src,
+                                                           double* __restrict__ dst, int ZC) {
+  const Geo g = cx.g;
+  const int nzc = g.N3 / ZC;
+  const int load = blockIdx.z / nzc;
+  const int zcI = blockIdx.z - load * nzc;
+  if (mode == CG && !cx.st[load].active) return;
+  constexpr int DW = KE_TX + 2, DH = KE_TY + 2, EW = KE_TX + 1, EH = KE_TY + 1;
+  __shared__ double D[3][3][DH * DW];        // [slot][comp][...]
+  __shared__ unsigned char P[2][EH * EW];     // phase of element layers
+  __shared__ double Ks[2][24 * 24];
+  __shared__ double red_sh[32];
+  const int t = threadIdx.x, T = blockDim.x;
+  for (int i = t; i < 2 * 576; i += T) Ks[i / 576][i % 576] = __ldg(cx.kel + i);
+  const int tx = t % KE_TX, ty = t / KE_TX;
+  const int x0 = blockIdx.x * KE_TX, y0 = blockIdx.y * KE_TY, zs = zcI * ZC;
+  const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
+  const long long n = g.n;
+  const double* dv = src + (long long)load * 3 * n;
+  auto load_plane = [&](int zz, int slot) {
+    const int zw = (zz + N3) % N3;
+    for (int i = t; i < 3 * DH * DW; i += T) {
+      const int comp = i / (DH * DW), r = i - comp * DH * DW;
+      const int ly = r / DW, lx = r - ly * DW;
+      const int gx = (x0 - 1 + lx + N1) & (N1 - 1), gy = (y0 - 1 + ly + N2) & (N2 - 1);
+      D[slot][comp][r] = __ldg(dv + comp * n + ((long long)zw * N2 + gy) * N1 + gx);
+    }
+  };
+  auto load_phase = [&](int layer, int slot) {
+    const int zw = (layer + N3) % N3;
+    for (int i = t; i < EH * EW; i += T) {
+      const int ly = i / EW, lx = i - ly * EW;
+      const int gx = (x0 - 1 + lx + N1) & (N1 - 1), gy = (y0 - 1 + ly + N2) & (N2 - 1);
+      P[slot][i] = __ldg(cx.phase + ((long long)zw * N2 + gy) * N1 + gx) ? 1 : 0;
+    }
+  };
+  load_plane(zs - 1, 0);
+  load_plane(zs, 1);
+  load_phase(zs - 1, 0);
+  double part = 0.0;
+  for (int k = zs; k < zs + ZC; ++k) {
+    const int q = k - zs;
+    const int sl[3] = {q % 3, (q + 1) % 3, (q + 2) % 3};  // planes k-1, k, k+1
+    const int pl[2] = {q & 1, (q + 1) & 1};                // layers k-1, k
+    load_plane(k + 1, sl[2]);
+    load_phase(k, pl[1]);
+    __syncthreads();
+    double acc[3] = {0.0, 0.0, 0.0};
+#pragma unroll 1
+    for (int o = 0; o < 8; ++o) {
+      const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
+      const int a = (1 - ox) + 2 * (1 - oy) + 4 * (1 - oz);
+      const int ph = P[pl[oz]][(ty + oy) * EW + tx + ox];
+      const double* Km = &Ks[ph][0];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const int bx = b & 1, by = (b >> 1) & 1, bz = b >> 2;
+        const int slot = sl[oz + bz];
+        const int off = (ty + oy + by) * DW + (tx + ox + bx);
+        const double u0 = D[slot][0][off], u1 = D[slot][1][off], u2 = D[slot][2][off];
+#pragma unroll
+        for (int al = 0; al < 3; ++al) {
+          const double* row = Km + (3 * a + al) * 24 + 3 * b;
+          acc[al] = fma(row[0], u0, fma(row[1], u1, fma(row[2], u2, acc[al])));
+        }
+      }
+    }
+    const int gx = x0 + tx, gy = y0 + ty;
+    const int offc = (ty + 1) * DW + tx + 1;
+    const long long gi = ((long long)k * N2 + gy) * N1 + gx;
+#pragma unroll
+    for (int al = 0; al < 3; ++al) {
+      dst[(long long)load * 3 * n + al * n + gi] = acc[al];
+      part = fma(D[sl[1]][al][offc], acc[al], part);
+    }
+    __syncthreads();
+  }
+  const int nblk = gridDim.x * gridDim.y * nzc;
+  const int my = (zcI * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  dp_finish(cx, load, nblk, my, part, red_sh, mode);
+}
+
+__global__ void __launch_bounds__(256) kp_elastic2d_kernel(Ctx cx, int mode, const double* __restrict__ src,
+                                                           double* __restrict__ dst) {
+  const Geo g = cx.g;
+  const int load = blockIdx.y;
+  if (mode == CG && !cx.st[load].active) return;
+  __shared__ double red_sh[32];
+  const int N1 = g.N1, N2 = g.N2;
+  const long long n = g.n;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  double part = 0.0;
+  if (i < n) {
+    const int x = (int)(i % N1), y = (int)(i / N1);
+    const double* dv = src + (long long)load * 2 * n;
+    double acc[2] = {0.0, 0.0};
+    for (int o = 0; o < 4; ++o) {
+      const int ox = o & 1, oy = o >> 1;
+      const int a = (1 - ox) + 2 * (1 - oy);
+      const int ex = (x - 1 + ox + N1) & (N1 - 1), ey = (y - 1 + oy + N2) & (N2 - 1);
+      const int ph = __ldg(cx.phase + (long long)ey * N1 + ex) ? 1 : 0;
+      for (int b = 0; b < 4; ++b) {
+        const int bx = b & 1, by = b >> 1;
+        const int nx = (ex + bx) & (N1 - 1), ny = (ey + by) & (N2 - 1);
+        const double u0 = __ldg(dv + (long long)ny * N1 + nx), u1 = __ldg(dv + n + (long long)ny * N1 + nx);
+        for (int al = 0; al < 2; ++al) {
+          const double* row = cx.kel + ph * 64 + (2 * a + al) * 8 + 2 * b;
+          acc[al] = fma(__ldg(row), u0, fma(__ldg(row + 1), u1, acc[al]));
+        }
+      }
+    }
+    for (int al = 0; al < 2; ++al) {
+      dst[(long long)load * 2 * n + al * n + i] = acc[al];
+      part = fma(__ldg(dv + al * n + i), acc[al], part);
+    }
+  }
+  dp_finish(cx, load, gridDim.x, blockIdx.x, part, red_sh, mode);
+}
+
+// ============================================================================== RHS (Eq 76 / 81)
+// f_(i,alpha) = -(h^(d-1)/2^(d-1)) sum_o sum_j s_j(o) sigma^o_(alpha j),  s_j(o) = +1 if o_j = 0 else -1,
+// sigma^o = kappa_o g_bar (thermal, alpha = 0) or lambda_o tr(eps) I + 2 mu_o eps (elastic).
+__global__ void rhs_kernel(Ctx cx, LoadParams lp, double* __restrict__ f) {
+  const Geo g = cx.g;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.n) return;
+  const int N1 = g.N1, N2 = g.N2, N3 = g.N3, d = g.dim;
+  const int x = (int)(i % N1);
+  const int y = (int)((i / N1) % N2);
+  const int z = (int)(i / ((long long)N1 * N2));
+  const double scale = (d == 3 ? g.h * g.h / 4.0 : g.h / 2.0);
+  int ph[8];
+  const int no = 1 << d;
+  for (int o = 0; o < no; ++o) {
+    const int ox = o & 1, oy = (o >> 1) & 1, oz = (o >> 2) & 1;
+    const int ex = (x - 1 + ox + N1) & (N1 - 1), ey = (y - 1 + oy + N2) & (N2 - 1);
+    const int ez = d == 3 ? (z - 1 + oz + N3) % N3 : 0;
+    ph[o] = __ldg(cx.phase + ((long long)ez * N2 + ey) * N1 + ex) ? 1 : 0;
+  }
+  const double rt2 = 0.70710678118654752440;
+  for (int l = 0; l < g.nrhs; ++l) {
+    if (g.c == 1) {
+      double acc = 0.0;
+      for (int o = 0; o < no; ++o) {
+        double sg = 0.0;
+        for (int j = 0; j < d; ++j) sg += ((o >> j) & 1) ? -lp.v[l][j] : lp.v[l][j];
+        acc += cx.mat[ph[o]][0] * sg;
+      }
+      f[(long long)l * g.n + i] = -scale * acc;
+    } else {
+      double e[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+      if (d == 3) {
+        e[0][0] = lp.v[l][0]; e[1][1] = lp.v[l][1]; e[2][2] = lp.v[l][2];
+        e[0][1] = e[1][0] = lp.v[l][3] * rt2;
+        e[0][2] = e[2][0] = lp.v[l][4] * rt2;
+        e[1][2] = e[2][1] = lp.v[l][5] * rt2;
+      } else {
+        e[0][0] = lp.v[l][0]; e[1][1] = lp.v[l][1];
+        e[0][1] = e[1][0] = lp.v[l][2] * rt2;
+      }
+      const double tr = e[0][0] + e[1][1] + e[2][2];
+      for (int al = 0; al < d; ++al) {
+        double acc = 0.0;
+        for (int o = 0; o < no; ++o) {
+          const double lam = cx.mat[ph[o]][0], mu = cx.mat[ph[o]][1];
+          for (int j = 0; j < d; ++j) {
+            const double sig = (al == j ? lam * tr : 0.0) + 2.0 * mu * e[al][j];
+            acc += ((o >> j) & 1) ? -sig : sig;
+          }
+        }
+        f[((long long)l * g.c + al) * g.n + i] = -scale * acc;
+      }
+    }
+  }
+}
+
+// ============================================================================== finalize / means
+__global__ void finalize_kernel(Ctx cx) {
+  const Geo g = cx.g;
+  const int load = blockIdx.y;
+  const LoadState* st = cx.st + load;
+  if (!st->pending_u || st->iters < 1) return;
+  const double a = st->alpha;
+  const long long cnt = (long long)g.c * g.n;
+  double* u = cx.u + (long long)load * cnt;
+  const double* d = cx.d + (long long)load * cnt;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (long long)gridDim.x * blockDim.x)
+    u[i] = fma(a, d[i], u[i]);
+}
+
+// per (load, comp) partial sums over fixed chunks, then a fixed-order combine + subtract
+__global__ void mean_partial_kernel(const double* __restrict__ u, long long n, double* partials, int nblk) {
+  __shared__ double sh[32];
+  const int lc = blockIdx.y;
+  const double* v = u + (long long)lc * n;
+  double acc = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)nblk * blockDim.x)
+    acc += v[i];
+  const double b = block_reduce<false>(acc, sh);
+  if (threadIdx.x == 0) partials[(long long)lc * nblk + blockIdx.x] = b;
+}
+__global__ void mean_combine_kernel(const double* partials, int nblk, long long n, double* means) {
+  __shared__ double sh[32];
+  const int lc = blockIdx.x;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) acc += partials[(long long)lc * nblk + i];
+  const double b = block_reduce<false>(acc, sh);
+  if (threadIdx.x == 0) means[lc] = b / (double)n;
+}
+__global__ void mean_subtract_kernel(const double* __restrict__ src, double* __restrict__ dst, long long n,
+                                     const double* means) {
+  const int lc = blockIdx.y;
+  const double m = means[lc];
+  const double* v = src + (long long)lc * n;
+  double* o = dst + (long long)lc * n;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    o[i] = v[i] - m;
+}
+
+// ============================================================================== effective property
+// acc[i][j] = f^(i) . u^(j); plus the count of phase-1 voxels for <C>.
+constexpr int EFF_T = 256;
+__global__ void __launch_bounds__(EFF_T) effective_kernel(Ctx cx, LoadParams lp, const double* __restrict__ u,
+                                                          double* partials) {
+  const Geo g = cx.g;
+  const int nl = g.nrhs;
+  const int nacc = nl * nl + 1;
+  __shared__ double sh[32];
+  double acc[kMaxRhs * kMaxRhs + 1];
+  for (int a = 0; a < nacc; ++a) acc[a] = 0.0;
+  const int N1 = g.N1, N2 = g.N2, N3 = g.N3, d = g.dim;
+  const double scale = (d == 3 ? g.h * g.h / 4.0 : g.h / 2.0);
+  const double rt2 = 0.70710678118654752440;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += (long long)gridDim.x * blockDim.x) {
+    const int x = (int)(i % N1), y = (int)((i / N1) % N2), z = (int)(i / ((long long)N1 * N2));
+    int ph[8];
+    const int no = 1 << d;
+    for (int o = 0; o < no; ++o) {
+      const int ox = o & 1, oy = (o >> 1) & 1, oz = (o >> 2) & 1;
+      const int ex = (x - 1 + ox + N1) & (N1 - 1), ey = (y - 1 + oy + N2) & (N2 - 1);
+      const int ez = d == 3 ? (z - 1 + oz + N3) % N3 : 0;
+      ph[o] = __ldg(cx.phase + ((long long)ez * N2 + ey) * N1 + ex) ? 1 : 0;
+    }
+    acc[nl * nl] += ph[no - 1];  // voxel i itself is octant (1,1,1) of node i: count each voxel once
+    for (int li = 0; li < nl; ++li) {
+      double fi[3] = {0.0, 0.0, 0.0};
+      if (g.c == 1) {
+        double s = 0.0;
+        for (int o = 0; o < no; ++o) {
+          double sg = 0.0;
+          for (int j = 0; j < d; ++j) sg += ((o >> j) & 1) ? -lp.v[li][j] : lp.v[li][j];
+          s += cx.mat[ph[o]][0] * sg;
+        }
+        fi[0] = -scale * s;
+      } else {
+        double e[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+        if (d == 3) {
+          e[0][0] = lp.v[li][0]; e[1][1] = lp.v[li][1]; e[2][2] = lp.v[li][2];
+          e[0][1] = e[1][0] = lp.v[li][3] * rt2;
+          e[0][2] = e[2][0] = lp.v[li][4] * rt2;
+          e[1][2] = e[2][1] = lp.v[li][5] * rt2;
+        } else {
+          e[0][0] = lp.v[li][0]; e[1][1] = lp.v[li][1];
+          e[0][1] = e[1][0] = lp.v[li][2] * rt2;
+        }
+        const double tr = e[0][0] + e[1][1] + e[2][2];
+        for (int al = 0; al < d; ++al) {
+          double s = 0.0;
+          for (int o = 0; o < no; ++o) {
+            const double lam = cx.mat[ph[o]][0], mu = cx.mat[ph[o]][1];
+            for (int j = 0; j < d; ++j) {
+              const double sig = (al == j ? lam * tr : 0.0) + 2.0 * mu * e[al][j];
+              s += ((o >> j) & 1) ? -sig : sig;
+            }
+          }
+          fi[al] = -scale * s;
+        }
+      }
+      for (int lj = 0; lj < nl; ++lj) {
+        double s = 0.0;
+        for (int al = 0; al < g.c; ++al) s = fma(fi[al], u[((long long)lj * g.c + al) * g.n + i], s);
+        acc[li * nl + lj] += s;
+      }
+    }
+  }
+  for (int a = 0; a < nacc; ++a) {
+    const double b = block_reduce<false>(acc[a], sh);
+    if (threadIdx.x == 0) partials[(long long)a * gridDim.x + blockIdx.x] = b;
+    __syncthreads();
+  }
+}
+
+__global__ void combine_rows_kernel(const double* partials, int nblk, double* out) {
+  __shared__ double sh[32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) acc += partials[(long long)blockIdx.x * nblk + i];
+  const double b = block_reduce<false>(acc, sh);
+  if (threadIdx.x == 0) out[blockIdx.x] = b;
+}
+
+// ============================================================================== symbol (a0)
+// G_hat(k)/n on the half spectrum, layout [C][H1][N3][N2].
+// Reference symbol (closed form of the Q1 stencil's DFT, App./SURVEY A3 — the oracle probes
+// it instead):  S_ii = (2/h)(1-cos t_i) prod_{j!=i} (h/3)(2+cos t_j);
+//               S_ij = sin t_i sin t_j prod_{l!=i,j} (h/3)(2+cos t_l).
+// thermal A = kappa_r tr S ; elastic A = (lam_r + mu_r) S + mu_r tr(S) I  (Eq 36 symbol).
+// Perturbation: c=1 rho = 1-amp+2 amp u01(seed,2,canon(k));
+//   c=3 G = Phi + amp tr(Phi)/3 psi(theta), theta_t = u01(seed,2,8 canon(k)+t) (Eq B5);
+//   c=2 analogous with Eq 45.  canon(k) = min(flat(k), flat(-k)).  G(0) = 0.
+__device__ __forceinline__ void axis_trig(int k, int N, double& cs, double& sn) {
+  const int ks = (2 * k <= N) ? k : k - N;  // signed frequency: cos even, sin odd -> G(-k)=G(k) bitwise
+  const int ka = ks < 0 ? -ks : ks;
+  double s, c;
+  sincospi(2.0 * (double)ka / (double)N, &s, &c);
+  cs = c;
+  sn = ks < 0 ? -s : s;
+}
+
+__global__ void build_symbol_kernel(Ctx cx, double* gtab, double ref0, double ref1, unsigned long long seed, double amp) {
+  const Geo g = cx.g;
+  const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= g.nspec) return;
+  const int N1 = g.N1, N2 = g.N2, N3 = g.N3, d = g.dim;
+  const int ky = (int)(b % N2);
+  const int kz = (int)((b / N2) % N3);
+  const int kx = (int)(b / ((long long)N2 * N3));
+  double cs[3], sn[3];
+  axis_trig(kx, N1, cs[0], sn[0]);
+  axis_trig(ky, N2, cs[1], sn[1]);
+  axis_trig(kz, N3, cs[2], sn[2]);
+  const double h = g.h;
+  const double inv_n = 1.0 / (double)g.n;
+  const long long ns = g.nspec;
+  const unsigned long long flat = ((unsigned long long)kz * N2 + ky) * N1 + kx;
+  const unsigned long long flatm =
+      ((unsigned long long)((N3 - kz) % N3) * N2 + (unsigned long long)((N2 - ky) % N2)) * N1 + (unsigned long long)((N1 - kx) % N1);
+  const unsigned long long canon = flat < flatm ? flat : flatm;
+  const bool zero = (kx == 0 && ky == 0 && kz == 0);
+  double mass[3], S[3][3];
+  for (int i = 0; i < d; ++i) mass[i] = (h / 3.0) * (2.0 + cs[i]);
+  for (int i = 0; i < d; ++i) {
+    double v = (2.0 / h) * (1.0 - cs[i]);
+    for (int j = 0; j < d; ++j)
+      if (j != i) v *= mass[j];
+    S[i][i] = v;
+    for (int j = 0; j < d; ++j) {
+      if (j == i) continue;
+      double w = sn[i] * sn[j];
+      for (int l = 0; l < d; ++l)
+        if (l != i && l != j) w *= mass[l];
+      S[i][j] = w;
+    }
+  }
+  if (g.c == 1) {
+    double a = 0.0;
+    for (int i = 0; i < d; ++i) a += S[i][i];
+    a *= ref0;
+    double gv = 0.0;
+    if (!zero) {
+      const double rho = seed ? (1.0 - amp + 2.0 * amp * u01(seed, 2, canon)) : 1.0;
+      gv = rho / a * inv_n;
+    }
+    gtab[b] = gv;
+    return;
+  }
+  const double lr = ref0, mr = ref1;
+  double tr = 0.0;
+  for (int i = 0; i < d; ++i) tr += S[i][i];
+  double A[3][3];
+  for (int i = 0; i < d; ++i)
+    for (int j = 0; j < d; ++j) A[i][j] = (lr + mr) * S[i][j] + (i == j ? mr * tr : 0.0);
+  double P[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  if (!zero) {
+    if (d == 3) {
+      // symmetric A: inverse from cofactors (A is symmetric by construction)
+      const double i00 = A[1][1] * A[2][2] - A[1][2] * A[1][2];
+      const double i01 = A[0][2] * A[1][2] - A[0][1] * A[2][2];
+      const double i02 = A[0][1] * A[1][2] - A[0][2] * A[1][1];
+      const double i11 = A[0][0] * A[2][2] - A[0][2] * A[0][2];
+      const double i12 = A[0][2] * A[0][1] - A[0][0] * A[1][2];
+      const double i22 = A[0][0] * A[1][1] - A[0][1] * A[0][1];
+      const double id = 1.0 / (A[0][0] * i00 + A[0][1] * i01 + A[0][2] * i02);
+      P[0][0] = i00 * id;
+      P[1][1] = i11 * id;
+      P[2][2] = i22 * id;
+      P[0][1] = P[1][0] = i01 * id;
+      P[0][2] = P[2][0] = i02 * id;
+      P[1][2] = P[2][1] = i12 * id;
+      if (seed) {
+        double th[6];
+        for (int tt = 0; tt < 6; ++tt) th[tt] = u01(seed, 2, 8ULL * canon + tt);
+        th[0] = 0.5 + 0.5 * th[0];
+        th[1] = 0.5 + 0.5 * th[1];
+        th[3] = 0.5 + 0.5 * th[3];
+        th[2] -= 0.5;
+        th[4] -= 0.5;
+        th[5] -= 0.5;
+        const double t1 = th[0], t2 = th[1], t3 = th[2], t4 = th[3], t5 = th[4], t6 = th[5];
+        const double s = amp * (P[0][0] + P[1][1] + P[2][2]) / 3.0;
+        const double psi[3][3] = {{t1 * t1, t1 * t3, t1 * t6},
+                                  {t1 * t3, t2 * t2 + t3 * t3, t2 * t5 + t3 * t6},
+                                  {t1 * t6, t2 * t5 + t3 * t6, t4 * t4 + t5 * t5 + t6 * t6}};
+        for (int i = 0; i < 3; ++i)
+          for (int j = 0; j < 3; ++j) P[i][j] += s * psi[i][j];
+      }
+    } else {
+      const double det = A[0][0] * A[1][1] - A[0][1] * A[1][0];
+      P[0][0] = A[1][1] / det;
+      P[1][1] = A[0][0] / det;
+      P[0][1] = P[1][0] = -0.5 * (A[0][1] + A[1][0]) / det;
+      if (seed) {
+        double t1 = 0.5 + 0.5 * u01(seed, 2, 8ULL * canon + 0);
+        double t2 = 0.5 + 0.5 * u01(seed, 2, 8ULL * canon + 1);
+        double t3 = u01(seed, 2, 8ULL * canon + 2) - 0.5;
+        const double s = amp * (P[0][0] + P[1][1]) / 2.0;
+        P[0][0] += s * t1 * t1;
+        P[0][1] += s * t1 * t3;
+        P[1][0] += s * t1 * t3;
+        P[1][1] += s * (t2 * t2 + t3 * t3);
+      }
+    }
+  }
+  if (g.c == 3) {
+    gtab[0 * ns + b] = P[0][0] * inv_n;
+    gtab[1 * ns + b] = P[1][1] * inv_n;
+    gtab[2 * ns + b] = P[0][1] * inv_n;
+    gtab[3 * ns + b] = P[2][2] * inv_n;
+    gtab[4 * ns + b] = P[1][2] * inv_n;
+    gtab[5 * ns + b] = P[0][2] * inv_n;
+  } else {
+    gtab[0 * ns + b] = P[0][0] * inv_n;
+    gtab[1 * ns + b] = P[1][1] * inv_n;
+    gtab[2 * ns + b] = P[0][1] * inv_n;
+  }
+}
+
+// Eq 55: min / max block eigenvalue of n*G_hat(k) over k != 0 (2x2 / 3x3 closed forms).
+__device__ void eig_sym3(double a, double b, double c, double d, double e, double f, double& lmin, double& lmax) {
+  // matrix [[a,d,f],[d,b,e],[f,e,c]]
+  const double p1 = d * d + e * e + f * f;
+  const double q = (a + b + c) / 3.0;
+  const double p2 = (a - q) * (a - q) + (b - q) * (b - q) + (c - q) * (c - q) + 2.0 * p1;
+  const double p = sqrt(p2 / 6.0);
+  if (p == 0.0) {
+    lmin = lmax = q;
+    return;
+  }
+  const double ip = 1.0 / p;
+  const double B00 = (a - q) * ip, B11 = (b - q) * ip, B22 = (c - q) * ip, B01 = d * ip, B12 = e * ip, B02 = f * ip;
+  double r = 0.5 * (B00 * (B11 * B22 - B12 * B12) - B01 * (B01 * B22 - B12 * B02) + B02 * (B01 * B12 - B11 * B02));
+  r = fmin(1.0, fmax(-1.0, r));
+  const double phi = acos(r) / 3.0;
+  const double e1 = q + 2.0 * p * cos(phi);
+  const double e3 = q + 2.0 * p * cos(phi + 2.0943951023931954923);
+  lmax = e1;
+  lmin = e3;
+}
+
+__global__ void eq55_kernel(Ctx cx, const double* gtab, double* partials) {
+  const Geo g = cx.g;
+  __shared__ double sh[32];
+  double mn = 1e300, mx = -1e300;
+  const long long ns = g.nspec;
+  const double nn = (double)g.n;
+  for (long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x; b < ns; b += (long long)gridDim.x * blockDim.x) {
+    if (b == 0) continue;
+    double lo, hi;
+    if (g.c == 1) {
+      lo = hi = gtab[b] * nn;
+    } else if (g.c == 2) {
+      const double a = gtab[b] * nn, c = gtab[ns + b] * nn, o = gtab[2 * ns + b] * nn;
+      const double m = 0.5 * (a + c), r = sqrt(0.25 * (a - c) * (a - c) + o * o);
+      lo = m - r;
+      hi = m + r;
+    } else {
+      eig_sym3(gtab[b] * nn, gtab[ns + b] * nn, gtab[3 * ns + b] * nn, gtab[2 * ns + b] * nn, gtab[4 * ns + b] * nn,
+               gtab[5 * ns + b] * nn, lo, hi);
+    }
+    mn = fmin(mn, lo);
+    mx = fmax(mx, hi);
+  }
+  const double bmx = block_reduce<true>(mx, sh);
+  __syncthreads();
+  const double bmn = -block_reduce<true>(-mn, sh);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = bmn;
+    partials[gridDim.x + blockIdx.x] = bmx;
+  }
+}
+
+__global__ void zero_kernel(double* x, long long n) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    x[i] = 0.0;
+}
+
+// ============================================================================== launchers
+template <class F>
+static int dispatch_pow2(int L, F&& f) {
+  switch (L) {
+    case 4: return f(std::integral_constant<int, 4>{});
+    case 8: return f(std::integral_constant<int, 8>{});
+    case 16: return f(std::integral_constant<int, 16>{});
+    case 32: return f(std::integral_constant<int, 32>{});
+    case 64: return f(std::integral_constant<int, 64>{});
+    case 128: return f(std::integral_constant<int, 128>{});
+    case 256: return f(std::integral_constant<int, 256>{});
+    case 512: return f(std::integral_constant<int, 512>{});
+    case 1024: return f(std::integral_constant<int, 1024>{});
+    default: return -1;
+  }
+}
+
+template <class K>
+static void set_smem(K kernel, int bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+int launch_xfwd(const Ctx& cx, int mode, const double* src, cudaStream_t s) {
+  const Geo& g = cx.g;
+  return dispatch_pow2(g.M, [&](auto Lc) {
+    constexpr int M = decltype(Lc)::value;
+    const dim3 grid((unsigned)((long long)g.c * g.N3 * g.N2 / 8), g.nrhs);
+    const int sm = xsmem_bytes<M>();
+    if (mode == CG) {
+      auto k = xfwd_kernel<M, CG>;
+      set_smem(k, sm);
+      k<<<grid, fft_threads(M), sm, s>>>(cx, src);
+    } else {
+      auto k = xfwd_kernel<M, STANDALONE>;
+      set_smem(k, sm);
+      k<<<grid, fft_threads(M), sm, s>>>(cx, src);
+    }
+    return 1;
+  });
+}
+
+int launch_xinv(const Ctx& cx, int mode, double* dst, cudaStream_t s) {
+  const Geo& g = cx.g;
+  return dispatch_pow2(g.M, [&](auto Lc) {
+    constexpr int M = decltype(Lc)::value;
+    const dim3 grid((unsigned)((long long)g.c * g.N3 * g.N2 / 8), g.nrhs);
+    const int sm = xsmem_bytes<M>();
+    if (mode == CG) {
+      auto k = xinv_kernel<M, CG>;
+      set_smem(k, sm);
+      k<<<grid, fft_threads(M), sm, s>>>(cx, dst);
+    } else {
+      auto k = xinv_kernel<M, STANDALONE>;
+      set_smem(k, sm);
+      k<<<grid, fft_threads(M), sm, s>>>(cx, dst);
+    }
+    return 1;
+  });
+}
+
+int launch_ypass(const Ctx& cx, int mode, bool inverse, cudaStream_t s) {
+  const Geo& g = cx.g;
+  return dispatch_pow2(g.N2, [&](auto Lc) {
+    constexpr int L = decltype(Lc)::value;
+    const long long nrows = (long long)g.c * g.H1 * g.N3;
+    const dim3 grid((unsigned)((nrows + 7) / 8), g.nrhs);
+    const int sm = ysmem_bytes<L>();
+    auto pick = [&](auto k) {
+      set_smem(k, sm);
+      k<<<grid, fft_threads(L), sm, s>>>(cx);
+    };
+    if (mode == CG) {
+      if (inverse) pick(ypass_kernel<L, true, CG>); else pick(ypass_kernel<L, false, CG>);
+    } else {
+      if (inverse) pick(ypass_kernel<L, true, STANDALONE>); else pick(ypass_kernel<L, false, STANDALONE>);
+    }
+    return 1;
+  });
+}
+
+int launch_gpass(const Ctx& cx, int mode, cudaStream_t s) {
+  const Geo& g = cx.g;
+  if (g.dim == 3) {
+    return dispatch_pow2(g.N3, [&](auto Lc) {
+      constexpr int L = decltype(Lc)::value;
+      const dim3 grid((unsigned)(g.H1 * (g.N2 / 8)), g.nrhs);
+      auto go = [&](auto k, int sm) {
+        set_smem(k, sm);
+        k<<<grid, fft_threads(L), sm, s>>>(cx);
+        return 1;
+      };
+      if (g.c == 1) {
+        return mode == CG ? go(gpass_z_kernel<L, 1, CG>, gsmem_bytes<L, 1>())
+                          : go(gpass_z_kernel<L, 1, STANDALONE>, gsmem_bytes<L, 1>());
+      }
+      if constexpr (gsmem_bytes<L, 3>() <= 227 * 1024) {
+        return mode == CG ? go(gpass_z_kernel<L, 3, CG>, gsmem_bytes<L, 3>())
+                          : go(gpass_z_kernel<L, 3, STANDALONE>, gsmem_bytes<L, 3>());
+      } else {
+        return -1;
+      }
+    });
+  }
+  return dispatch_pow2(g.N2, [&](auto Lc) {
+    constexpr int L = decltype(Lc)::value;
+    const dim3 grid((unsigned)((g.H1 + 7) / 8), g.nrhs);
+    auto go = [&](auto k, int sm) {
+      set_smem(k, sm);
+      k<<<grid, fft_threads(L), sm, s>>>(cx);
+      return 1;
+    };
+    if (g.c == 1)
+      return mode == CG ? go(gpass_y2d_kernel<L, 1, CG>, gsmem_bytes<L, 1>())
+                        : go(gpass_y2d_kernel<L, 1, STANDALONE>, gsmem_bytes<L, 1>());
+    return mode == CG ? go(gpass_y2d_kernel<L, 2, CG>, gsmem_bytes<L, 2>())
+                      : go(gpass_y2d_kernel<L, 2, STANDALONE>, gsmem_bytes<L, 2>());
+  });
+}
+
+int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaStream_t s) {
+  const Geo& g = cx.g;
+  if (g.dim == 3 && g.c == 1) {
+    const int TX = g.N1 < 32 ? g.N1 : 32;
+    const int ZC = g.N3 < 16 ? g.N3 : 16;
+    const int sm = (3 * 10 * (TX + 2) + 2 * 9 * (TX + 1) + 3 * 9 * (TX + 1)) * (int)sizeof(double);
+    const dim3 grid(g.N1 / TX, g.N2 / KT_TY, (g.N3 / ZC) * g.nrhs);
+    kp_thermal3d_kernel<<<grid, TX * KT_TY, sm, s>>>(cx, mode, src, dst, TX, ZC);
+    return 1;
+  }
+  if (g.dim == 2 && g.c == 1) {
+    const dim3 grid((unsigned)((g.n + 255) / 256), g.nrhs);
+    kp_thermal2d_kernel<<<grid, 256, 0, s>>>(cx, mode, src, dst);
+    return 1;
+  }
+  if (g.dim == 3) {
+    if (g.N1 < KE_TX) return -1;
+    const int ZC = g.N3 < 16 ? g.N3 : 16;
+    const dim3 grid(g.N1 / KE_TX, g.N2 / KE_TY, (g.N3 / ZC) * g.nrhs);
+    kp_elastic3d_kernel<<<grid, KE_TX * KE_TY, 0, s>>>(cx, mode, src, dst, ZC);
+    return 1;
+  }
+  const dim3 grid((unsigned)((g.n + 255) / 256), g.nrhs);
+  kp_elastic2d_kernel<<<grid, 256, 0, s>>>(cx, mode, src, dst);
+  return 1;
+}
+
+int launch_rhs(const Ctx& cx, const LoadParams& lp, double* f, cudaStream_t s) {
+  rhs_kernel<<<(unsigned)((cx.g.n + 255) / 256), 256, 0, s>>>(cx, lp, f);
+  return 1;
+}
+
+int launch_finalize(const Ctx& cx, cudaStream_t s) {
+  const long long cnt = (long long)cx.g.c * cx.g.n;
+  long long nb = (cnt + 255) / 256;
+  if (nb > 148 * 16) nb = 148 * 16;
+  finalize_kernel<<<dim3((unsigned)nb, cx.g.nrhs), 256, 0, s>>>(cx);
+  return 1;
+}
+
+int launch_mean_removal(const Ctx& cx, const double* u, double* out, double* scratch, cudaStream_t s) {
+  const Geo& g = cx.g;
+  const int nlc = g.nrhs * g.c;
+  const int nblk = 148 * 2;
+  double* partials = scratch;            // [nlc][nblk]
+  double* means = scratch + (long long)nlc * nblk;
+  mean_partial_kernel<<<dim3(nblk, nlc), 256, 0, s>>>(u, g.n, partials, nblk);
+  mean_combine_kernel<<<nlc, 256, 0, s>>>(partials, nblk, g.n, means);
+  long long nb = (g.n + 255) / 256;
+  if (nb > 148 * 16) nb = 148 * 16;
+  mean_subtract_kernel<<<dim3((unsigned)nb, nlc), 256, 0, s>>>(u, out, g.n, means);
+  return 3;
+}
+
+int launch_effective(const Ctx& cx, const LoadParams& lp, const double* u, double* partials, int* nblocks_out,
+                     cudaStream_t s) {
+  const int nblk = 148 * 2;
+  const int nacc = cx.g.nrhs * cx.g.nrhs + 1;
+  effective_kernel<<<nblk, EFF_T, 0, s>>>(cx, lp, u, partials);
+  combine_rows_kernel<<<nacc, 256, 0, s>>>(partials, nblk, partials + (long long)nacc * nblk);
+  *nblocks_out = nblk;
+  return 2;
+}
+
+int launch_build_symbol(const Ctx& cx, double* gtab, double ref0, double ref1, unsigned long long seed, double amp,
+                        cudaStream_t s) {
+  build_symbol_kernel<<<(unsigned)((cx.g.nspec + 255) / 256), 256, 0, s>>>(cx, gtab, ref0, ref1, seed, amp);
+  return 1;
+}
+
+int launch_eq55(const Ctx& cx, const double* gtab, double* partials, int* nblocks_out, cudaStream_t s) {
+  const int nblk = 148 * 2;
+  eq55_kernel<<<nblk, 256, 0, s>>>(cx, gtab, partials);
+  *nblocks_out = nblk;
+  return 1;
+}
+
+int launch_zero(double* x, long long n, cudaStream_t s) {
+  long long nb = (n + 255) / 256;
+  if (nb > 148 * 16) nb = 148 * 16;
+  zero_kernel<<<(unsigned)nb, 256, 0, s>>>(x, n);
+  return 1;
+}
+
+int blocks_needed_max(const Geo& g) {
+  long long m = (long long)g.c * g.N3 * g.N2 / 8;                // x passes
+  if (g.dim == 3) m = m > (long long)g.H1 * (g.N2 / 8) ? m : (long long)g.H1 * (g.N2 / 8);  // G pass
+  else m = m > (g.H1 + 7) / 8 ? m : (g.H1 + 7) / 8;
+  long long kb;
+  if (g.dim == 3 && g.c == 1) {
+    const int TX = g.N1 < 32 ? g.N1 : 32, ZC = g.N3 < 16 ? g.N3 : 16;
+    kb = (long long)(g.N1 / TX) * (g.N2 / KT_TY) * (g.N3 / ZC);
+  } else if (g.dim == 3) {
+    const int ZC = g.N3 < 16 ? g.N3 : 16;
+    kb = (long long)(g.N1 / KE_TX) * (g.N2 / KE_TY) * (g.N3 / ZC);
+  } else {
+    kb = (g.n + 255) / 256;
+  }
+  return (int)(m > kb ? m : kb);
+}
+
+}  // namespace uno

@@ -1,0 +1,56 @@
+// kernels.cuh — host-visible launch interface of the libunocg kernels.
+#pragma once
+#include "common.cuh"
+
+namespace uno {
+
+struct Tw {                 // device twiddle tables (host-computed in long double)
+  const double2* x;         // length M:   e^{-2 pi i m / M}
+  const double2* xpost;     // length M+1: e^{-2 pi i k / N1}
+  const double2* y;         // length N2
+  const double2* z;         // length N3
+};
+
+struct Ctx {
+  Geo g;
+  Tw tw;
+  LoadState* st;            // [nrhs] device CG state
+  Scratch sc;
+  const uint8_t* phase;     // [N3][N2][N1]
+  double mat[2][2];         // thermal {k,-}; elastic {lam, mu} per phase
+  const double* gtab;       // [C][H1][N3][N2]  G_hat(k)/n, unique entries (Eq 51, B7 order)
+  const double* kel;        // elastic: per-phase element matrices [2][(c 2^d)^2] (lam K_lam + mu K_mu)
+  double2* spec;            // [nrhs][c][H1][N3][N2]
+  double* r;                // [nrhs][c][n]
+  double* d;
+  double* p;
+  double* u;
+  double* hist;             // [nrhs][hist_stride] residual history (device) or null
+  int hist_stride;
+};
+
+struct LoadParams {         // macroscopic loads for the RHS / effective-property kernels
+  double v[kMaxRhs][6];
+};
+
+enum Mode { STANDALONE = 0, CG = 1 };
+
+// pass launchers; return number of kernels launched (or -1 on unsupported size)
+int launch_xfwd(const Ctx& cx, int mode, const double* src, cudaStream_t s);
+int launch_xinv(const Ctx& cx, int mode, double* dst, cudaStream_t s);
+int launch_ypass(const Ctx& cx, int mode, bool inverse, cudaStream_t s);
+int launch_gpass(const Ctx& cx, int mode, cudaStream_t s);
+int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaStream_t s);
+int launch_rhs(const Ctx& cx, const LoadParams& lp, double* f, cudaStream_t s);
+int launch_finalize(const Ctx& cx, cudaStream_t s);
+int launch_mean_removal(const Ctx& cx, const double* u, double* out, double* scratch_means, cudaStream_t s);
+int launch_effective(const Ctx& cx, const LoadParams& lp, const double* u, double* partials, int* nblocks_out,
+                     cudaStream_t s);
+int launch_build_symbol(const Ctx& cx, double* gtab, double ref0, double ref1, unsigned long long seed, double amp,
+                        cudaStream_t s);
+int launch_eq55(const Ctx& cx, const double* gtab, double* minmax_partials, int* nblocks_out, cudaStream_t s);
+int launch_zero(double* x, long long n, cudaStream_t s);
+
+int blocks_needed_max(const Geo& g);  // max CTAs per load of any reducing kernel
+
+}  // namespace uno

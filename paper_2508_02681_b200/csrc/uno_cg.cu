@@ -1,0 +1,594 @@
+// uno_cg.cu — C ABI of libunocg.so (see include/uno_cg.h for the contract).
+//
+// Host-side orchestration only: validation, workspace, twiddle tables, element
+// matrices, CUDA-graph capture of the PCG iteration and report read-back.  Every
+// arithmetic step of the hot path runs in kernels.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/uno_cg.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+using namespace uno;
+
+static thread_local std::string g_err;
+
+static uno_status fail(uno_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CK(call)                                                                                  \
+  do {                                                                                            \
+    cudaError_t e_ = (call);                                                                      \
+    if (e_ != cudaSuccess) return fail(UNO_ERR_CUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+enum { KC_K = 0, KC_XF = 1, KC_Y = 2, KC_G = 3, KC_XI = 4, KC_OTHER = 5, KC_N = 6 };
+
+struct uno_cg_handle {
+  uno_cg_desc desc;
+  Geo g;
+  cudaStream_t stream;
+  const uint8_t* phase;
+  double ref0, ref1;
+  // device buffers
+  double *r, *d, *p, *u;
+  double2* spec;
+  double* gtab;
+  double* kel;
+  double2 *twx, *twxp, *twy, *twz;
+  LoadState* st;
+  double* partials;
+  unsigned* counters;
+  double* results;
+  double* scratch;        // mean removal / effective / eq55
+  size_t scratch_len;
+  double* hist;
+  int hist_stride;
+  LoadState* h_st;        // pinned
+  double* h_small;        // pinned scratch for results
+  Ctx cx;
+  // graph of one chunk of iterations
+  cudaGraphExec_t gexec;
+  int gchunk;
+  bool gtimed;
+  // timing
+  bool timing;
+  std::vector<cudaEvent_t> tev;  // per chunk: [iter][class][2]
+  double kms[KC_N];
+  long long kcnt[KC_N];   // timed launches per class
+  long long lcnt[KC_N];   // all launches per class
+  double last_ms;
+  long long last_launches;
+  cudaEvent_t e0, e1;
+  double lam_min, lam_max;
+};
+
+// ------------------------------------------------------------------------------ helpers
+static void twiddles(int L, int denom, std::vector<double2>& out) {
+  out.resize(L);
+  for (int m = 0; m < L; ++m) {
+    long double a = -2.0L * 3.14159265358979323846264338327950288L * (long double)m / (long double)denom;
+    out[m].x = (double)cosl(a);
+    out[m].y = (double)sinl(a);
+  }
+}
+
+// Q1 element matrices by 2-point Gauss quadrature (independent of oracle/): corner a = ax + 2ay + 4az,
+// dof (a, alpha) -> c*a + alpha; Mandel-free form: K_lam = int (div N)(div N)^T,
+// K_mu = int (grad N : grad N + grad N : grad N^T)  (D = lam I(x)I + 2 mu I^s, Eq 80).
+static void elastic_element(int d, double h, std::vector<double>& Kl, std::vector<double>& Km) {
+  const int nc = 1 << d, nd = d * nc;
+  Kl.assign(nd * nd, 0.0);
+  Km.assign(nd * nd, 0.0);
+  const double gp[2] = {0.5 - 0.5 / std::sqrt(3.0), 0.5 + 0.5 / std::sqrt(3.0)};
+  const double w = std::pow(h, d) / (double)(1 << d);
+  const int nq = 1 << d;
+  for (int q = 0; q < nq; ++q) {
+    double xi[3] = {gp[q & 1], gp[(q >> 1) & 1], gp[(q >> 2) & 1]};
+    double G[8][3];
+    for (int a = 0; a < nc; ++a) {
+      for (int i = 0; i < d; ++i) {
+        double v = (((a >> i) & 1) ? 1.0 : -1.0) / h;
+        for (int j = 0; j < d; ++j)
+          if (j != i) v *= ((a >> j) & 1) ? xi[j] : 1.0 - xi[j];
+        G[a][i] = v;
+      }
+    }
+    for (int a = 0; a < nc; ++a)
+      for (int al = 0; al < d; ++al)
+        for (int b = 0; b < nc; ++b)
+          for (int be = 0; be < d; ++be) {
+            const int r = d * a + al, s = d * b + be;
+            Kl[r * nd + s] += w * G[a][al] * G[b][be];
+            double gg = 0.0;
+            for (int j = 0; j < d; ++j) gg += G[a][j] * G[b][j];
+            Km[r * nd + s] += w * ((al == be ? gg : 0.0) + G[a][be] * G[b][al]);
+          }
+  }
+}
+
+static bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+
+static Ctx make_ctx(uno_cg_handle* h) {
+  Ctx cx;
+  std::memset(&cx, 0, sizeof(cx));
+  cx.g = h->g;
+  cx.tw.x = h->twx;
+  cx.tw.xpost = h->twxp;
+  cx.tw.y = h->twy;
+  cx.tw.z = h->twz;
+  cx.st = h->st;
+  cx.sc.partials = h->partials;
+  cx.sc.counters = h->counters;
+  cx.sc.results = h->results;
+  cx.sc.max_blocks = blocks_needed_max(h->g);
+  cx.phase = h->phase;
+  for (int a = 0; a < 2; ++a)
+    for (int b = 0; b < 2; ++b) cx.mat[a][b] = h->desc.mat[a][b];
+  cx.gtab = h->gtab;
+  cx.kel = h->kel;
+  cx.spec = h->spec;
+  cx.r = h->r;
+  cx.d = h->d;
+  cx.p = h->p;
+  cx.u = h->u;
+  cx.hist = h->hist;
+  cx.hist_stride = h->hist_stride;
+  return cx;
+}
+
+static void free_all(uno_cg_handle* h) {
+  if (!h) return;
+  if (h->gexec) cudaGraphExecDestroy(h->gexec);
+  for (auto e : h->tev) cudaEventDestroy(e);
+  void* bufs[] = {h->r, h->d, h->p, h->u, h->spec, h->gtab, h->kel, h->twx, h->twxp, h->twy, h->twz,
+                  h->st, h->partials, h->counters, h->results, h->scratch, h->hist};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  if (h->h_st) cudaFreeHost(h->h_st);
+  if (h->h_small) cudaFreeHost(h->h_small);
+  if (h->e0) cudaEventDestroy(h->e0);
+  if (h->e1) cudaEventDestroy(h->e1);
+  delete h;
+}
+
+#define KL(expr, cls)                                                                 \
+  do {                                                                                \
+    int n_ = (expr);                                                                  \
+    if (n_ < 0) return fail(UNO_ERR_SHAPE, "no kernel instance for this grid size"); \
+    h->lcnt[cls] += n_;                                                               \
+    launches += n_;                                                                   \
+  } while (0)
+
+// ------------------------------------------------------------------------------ create/destroy
+extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_phase, uno_cg_handle** out) {
+  if (!desc || !d_phase || !out) return fail(UNO_ERR_ARG, "null argument");
+  *out = nullptr;
+  const uno_cg_desc& D = *desc;
+  if (D.dim != 2 && D.dim != 3) return fail(UNO_ERR_ARG, "dim must be 2 or 3");
+  if (D.physics != UNO_THERMAL && D.physics != UNO_ELASTIC) return fail(UNO_ERR_ARG, "physics must be 0 or 1");
+  for (int i = 0; i < D.dim; ++i)
+    if (D.bc[i] != 0) return fail(UNO_ERR_UNSUPPORTED, "only periodic boundaries are built in this version");
+  const int N1 = D.n[0], N2 = D.n[1], N3 = D.dim == 3 ? D.n[2] : 1;
+  if (!is_pow2(N1) || !is_pow2(N2) || !is_pow2(N3) || N1 < 8 || N2 < 8 || N1 > 1024 || N2 > 1024 ||
+      (D.dim == 3 && (N3 < 4 || N3 > 1024)))
+    return fail(UNO_ERR_SHAPE, "N1,N2 in {8..1024}, N3 in {4..1024} (3D), powers of two");
+  if (D.nrhs < 1 || D.nrhs > kMaxRhs) return fail(UNO_ERR_ARG, "nrhs must be 1..8");
+  const int c = D.physics == UNO_THERMAL ? 1 : D.dim;
+  if (D.physics == UNO_THERMAL) {
+    if (!(D.mat[0][0] > 0) || !(D.mat[1][0] > 0)) return fail(UNO_ERR_ARG, "conductivities must be > 0");
+  } else {
+    for (int p = 0; p < 2; ++p)
+      if (!(D.mat[p][1] > 0) || !(D.mat[p][0] >= 0)) return fail(UNO_ERR_ARG, "need mu > 0, lambda >= 0");
+    if (D.dim == 3 && N1 < 16) return fail(UNO_ERR_SHAPE, "elastic 3D needs N1 >= 16");
+  }
+  if (D.seed != 0 && !(D.amp >= 0 && D.amp < 1)) return fail(UNO_ERR_ARG, "amp must be in [0, 1)");
+
+  uno_cg_handle* h = new uno_cg_handle();  // value-initialised: all members zero
+  h->desc = D;
+  h->stream = (cudaStream_t)D.stream;
+  h->phase = d_phase;
+  Geo& g = h->g;
+  g.dim = D.dim;
+  g.c = c;
+  g.nrhs = D.nrhs;
+  g.N1 = N1;
+  g.N2 = N2;
+  g.N3 = N3;
+  g.M = N1 / 2;
+  g.H1 = g.M + 1;
+  g.n = (long long)N1 * N2 * N3;
+  g.nspec = (long long)g.H1 * N2 * N3;
+  g.h = D.h > 0 ? D.h : 1.0 / N1;
+  g.C = c * (c + 1) / 2;
+  if (D.ref[0] > 0) {
+    h->ref0 = D.ref[0];
+    h->ref1 = D.ref[1];
+  } else {  // arithmetic mean of the phases
+    h->ref0 = 0.5 * (D.mat[0][0] + D.mat[1][0]);
+    h->ref1 = 0.5 * (D.mat[0][1] + D.mat[1][1]);
+  }
+  cudaStream_t s = h->stream;
+  const long long vec = (long long)g.nrhs * c * g.n;
+  auto al = [&](void** p, size_t bytes) -> cudaError_t { return cudaMalloc(p, bytes ? bytes : 8); };
+  cudaError_t e = cudaSuccess;
+  const int maxb = blocks_needed_max(g);
+  h->hist_stride = 0;
+  h->scratch_len = (size_t)std::max<long long>(
+      (long long)(kMaxRhs * kMaxRhs + 1) * 148 * 2 * 2 + 64,
+      (long long)g.nrhs * c * 148 * 2 + g.nrhs * c + 64);
+  if ((e = al((void**)&h->r, vec * 8)) || (e = al((void**)&h->d, vec * 8)) || (e = al((void**)&h->p, vec * 8)) ||
+      (e = al((void**)&h->u, vec * 8)) || (e = al((void**)&h->spec, (size_t)g.nrhs * c * g.nspec * 16)) ||
+      (e = al((void**)&h->gtab, (size_t)g.C * g.nspec * 8)) || (e = al((void**)&h->kel, 2 * 576 * 8)) ||
+      (e = al((void**)&h->twx, g.M * 16)) || (e = al((void**)&h->twxp, (g.M + 1) * 16)) ||
+      (e = al((void**)&h->twy, N2 * 16)) || (e = al((void**)&h->twz, N3 * 16)) ||
+      (e = al((void**)&h->st, kMaxRhs * sizeof(LoadState))) ||
+      (e = al((void**)&h->partials, (size_t)RED_NSLOT * kMaxRhs * maxb * 8)) ||
+      (e = al((void**)&h->counters, RED_NSLOT * kMaxRhs * sizeof(unsigned))) ||
+      (e = al((void**)&h->results, RED_NSLOT * kMaxRhs * 8)) || (e = al((void**)&h->scratch, h->scratch_len * 8)) ||
+      (e = cudaMallocHost((void**)&h->h_st, kMaxRhs * sizeof(LoadState))) ||
+      (e = cudaMallocHost((void**)&h->h_small, 4096 * 8)) || (e = cudaEventCreate(&h->e0)) ||
+      (e = cudaEventCreate(&h->e1))) {
+    free_all(h);
+    return fail(UNO_ERR_CUDA, std::string("allocation: ") + cudaGetErrorString(e));
+  }
+  cudaMemsetAsync(h->counters, 0, RED_NSLOT * kMaxRhs * sizeof(unsigned), s);
+  cudaMemsetAsync(h->st, 0, kMaxRhs * sizeof(LoadState), s);
+  // twiddles (long double on the host)
+  std::vector<double2> t;
+  twiddles(g.M, g.M, t);
+  cudaMemcpyAsync(h->twx, t.data(), g.M * 16, cudaMemcpyHostToDevice, s);
+  cudaStreamSynchronize(s);
+  twiddles(g.M + 1, N1, t);
+  cudaMemcpyAsync(h->twxp, t.data(), (g.M + 1) * 16, cudaMemcpyHostToDevice, s);
+  cudaStreamSynchronize(s);
+  twiddles(N2, N2, t);
+  cudaMemcpyAsync(h->twy, t.data(), N2 * 16, cudaMemcpyHostToDevice, s);
+  cudaStreamSynchronize(s);
+  twiddles(N3, N3, t);
+  cudaMemcpyAsync(h->twz, t.data(), N3 * 16, cudaMemcpyHostToDevice, s);
+  cudaStreamSynchronize(s);
+  if (c > 1) {
+    std::vector<double> Kl, Km, Kp;
+    elastic_element(g.dim, g.h, Kl, Km);
+    const size_t nn = Kl.size();
+    Kp.resize(2 * nn);
+    for (int ph = 0; ph < 2; ++ph)
+      for (size_t i = 0; i < nn; ++i) Kp[ph * nn + i] = D.mat[ph][0] * Kl[i] + D.mat[ph][1] * Km[i];
+    cudaMemcpyAsync(h->kel, Kp.data(), Kp.size() * 8, cudaMemcpyHostToDevice, s);
+    cudaStreamSynchronize(s);
+  }
+  h->cx = make_ctx(h);
+  // a0: symbol table + Eq 55 check
+  launch_build_symbol(h->cx, h->gtab, h->ref0, h->ref1, D.seed, D.seed ? D.amp : 0.0, s);
+  int nblk = 0;
+  launch_eq55(h->cx, h->gtab, h->scratch, &nblk, s);
+  std::vector<double> mm(2 * nblk);
+  cudaMemcpyAsync(mm.data(), h->scratch, 2 * nblk * 8, cudaMemcpyDeviceToHost, s);
+  e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    free_all(h);
+    return fail(UNO_ERR_CUDA, std::string("create: ") + cudaGetErrorString(e));
+  }
+  double lo = 1e300, hi = -1e300;
+  for (int i = 0; i < nblk; ++i) {
+    lo = std::min(lo, mm[i]);
+    hi = std::max(hi, mm[nblk + i]);
+  }
+  h->lam_min = lo;
+  h->lam_max = hi;
+  if (!(lo > 1e-14)) {  // Eq 55
+    free_all(h);
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "Eq 55 safety check failed: min block eigenvalue %.3e", lo);
+    return fail(UNO_ERR_NOT_SPD, buf);
+  }
+  *out = h;
+  return UNO_OK;
+}
+
+extern "C" uno_status uno_cg_destroy(uno_cg_handle* h) {
+  if (!h) return fail(UNO_ERR_ARG, "null handle");
+  cudaStreamSynchronize(h->stream);
+  free_all(h);
+  return UNO_OK;
+}
+
+static void fill_loads(const uno_cg_handle* h, const double* h_loads, LoadParams& lp) {
+  std::memset(&lp, 0, sizeof(lp));
+  const int nv = h->g.c == 1 ? h->g.dim : (h->g.dim == 3 ? 6 : 3);
+  for (int l = 0; l < h->g.nrhs; ++l)
+    for (int j = 0; j < nv; ++j) lp.v[l][j] = h_loads[l * nv + j];
+}
+
+extern "C" uno_status uno_cg_rhs(uno_cg_handle* h, const double* h_loads, double* d_f) {
+  if (!h || !h_loads || !d_f) return fail(UNO_ERR_ARG, "null argument");
+  LoadParams lp;
+  fill_loads(h, h_loads, lp);
+  launch_rhs(h->cx, lp, d_f, h->stream);
+  CK(cudaGetLastError());
+  return UNO_OK;
+}
+
+extern "C" uno_status uno_cg_apply_K(uno_cg_handle* h, const double* d_u, double* d_Au, double* h_uAu) {
+  if (!h || !d_u || !d_Au) return fail(UNO_ERR_ARG, "null argument");
+  if (d_u == d_Au) return fail(UNO_ERR_ARG, "apply_K: input and output must not alias");
+  long long launches = 0;
+  KL(launch_kapply(h->cx, STANDALONE, d_u, d_Au, h->stream), KC_K);
+  CK(cudaGetLastError());
+  if (h_uAu) {
+    CK(cudaMemcpyAsync(h->h_small, h->results + RED_DP * kMaxRhs, h->g.nrhs * 8, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    for (int l = 0; l < h->g.nrhs; ++l) h_uAu[l] = h->h_small[l];
+  }
+  return UNO_OK;
+}
+
+extern "C" uno_status uno_cg_apply_precond(uno_cg_handle* h, const double* d_r, double* d_z, double* h_rz) {
+  if (!h || !d_r || !d_z) return fail(UNO_ERR_ARG, "null argument");
+  long long launches = 0;
+  cudaStream_t s = h->stream;
+  KL(launch_xfwd(h->cx, STANDALONE, d_r, s), KC_XF);
+  if (h->g.dim == 3) KL(launch_ypass(h->cx, STANDALONE, false, s), KC_Y);
+  KL(launch_gpass(h->cx, STANDALONE, s), KC_G);
+  if (h->g.dim == 3) KL(launch_ypass(h->cx, STANDALONE, true, s), KC_Y);
+  KL(launch_xinv(h->cx, STANDALONE, d_z, s), KC_XI);
+  CK(cudaGetLastError());
+  if (h_rz) {
+    CK(cudaMemcpyAsync(h->h_small, h->results + RED_GAMMA * kMaxRhs, h->g.nrhs * 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int l = 0; l < h->g.nrhs; ++l) h_rz[l] = h->h_small[l];
+  }
+  return UNO_OK;
+}
+
+// one PCG iteration (Alg 2 body) as kernel launches.  When `ev` is given, an event pair
+// brackets every launch: slots 0..5 = xfwd, yfwd, gpass, yinv, xinv, K.
+static const int kSlotClass[6] = {KC_XF, KC_Y, KC_G, KC_Y, KC_XI, KC_K};
+static int enqueue_iteration(uno_cg_handle* h, cudaStream_t s, cudaEvent_t* ev /* [6][2] or null */) {
+  const Ctx& cx = h->cx;
+  int n = 0;
+  auto run = [&](int slot, auto&& launch) -> bool {
+    if (ev) cudaEventRecord(ev[2 * slot], s);
+    const int r = launch();
+    if (ev) cudaEventRecord(ev[2 * slot + 1], s);
+    if (r < 0) return false;
+    n += r;
+    return true;
+  };
+  const bool d3 = h->g.dim == 3;
+  if (!run(0, [&] { return launch_xfwd(cx, CG, cx.r, s); })) return -1;
+  if (d3 && !run(1, [&] { return launch_ypass(cx, CG, false, s); })) return -1;
+  if (!run(2, [&] { return launch_gpass(cx, CG, s); })) return -1;
+  if (d3 && !run(3, [&] { return launch_ypass(cx, CG, true, s); })) return -1;
+  if (!run(4, [&] { return launch_xinv(cx, CG, nullptr, s); })) return -1;
+  if (!run(5, [&] { return launch_kapply(cx, CG, cx.d, cx.p, s); })) return -1;
+  return n;
+}
+
+static uno_status build_graph(uno_cg_handle* h, int chunk, bool timed) {
+  if (h->gexec && h->gchunk == chunk && h->gtimed == timed) return UNO_OK;
+  if (h->gexec) {
+    cudaGraphExecDestroy(h->gexec);
+    h->gexec = nullptr;
+  }
+  if (timed) {
+    const size_t need = (size_t)chunk * 6 * 2;
+    while (h->tev.size() < need) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      h->tev.push_back(e);
+    }
+  }
+  cudaStream_t cs;
+  CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  cudaGraph_t graph;
+  CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+  for (int i = 0; i < chunk; ++i) {
+    if (enqueue_iteration(h, cs, timed ? &h->tev[(size_t)i * 6 * 2] : nullptr) < 0) {
+      cudaStreamEndCapture(cs, &graph);
+      cudaStreamDestroy(cs);
+      return fail(UNO_ERR_SHAPE, "no kernel instance for this grid size");
+    }
+  }
+  CK(cudaStreamEndCapture(cs, &graph));
+  CK(cudaGraphInstantiate(&h->gexec, graph, 0));
+  cudaGraphDestroy(graph);
+  cudaStreamDestroy(cs);
+  h->gchunk = chunk;
+  h->gtimed = timed;
+  return UNO_OK;
+}
+
+static double zero_floor(const uno_cg_handle* h, const double* load, int nv) {
+  double mod;
+  if (h->g.c == 1)
+    mod = std::max(std::fabs(h->desc.mat[0][0]), std::fabs(h->desc.mat[1][0]));
+  else
+    mod = std::max(h->desc.mat[0][0] + 2 * h->desc.mat[0][1], h->desc.mat[1][0] + 2 * h->desc.mat[1][1]);
+  double lm = 0;
+  for (int j = 0; j < nv; ++j) lm = std::max(lm, std::fabs(load[j]));
+  return 1e-13 * mod * std::pow(h->g.h, h->g.dim - 1) * lm;
+}
+
+extern "C" uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, double rel_tol, int32_t max_iter,
+                                   int32_t fixed_iters, double* d_u, uno_cg_report* rep, double* h_hist) {
+  if (!h || !h_loads || !d_u) return fail(UNO_ERR_ARG, "null argument");
+  if (!(rel_tol >= 0) || max_iter < 0) return fail(UNO_ERR_ARG, "rel_tol >= 0, max_iter >= 0 required");
+  const Geo& g = h->g;
+  cudaStream_t s = h->stream;
+  long long launches = 0;
+  const int cap = fixed_iters > 0 ? fixed_iters : max_iter;
+  // residual history buffer
+  if (h_hist && h->hist_stride < cap + 1) {
+    if (h->hist) cudaFree(h->hist);
+    h->hist = nullptr;
+    CK(cudaMalloc(&h->hist, (size_t)kMaxRhs * (cap + 1) * 8));
+    h->hist_stride = cap + 1;
+    h->cx = make_ctx(h);
+    if (h->gexec) {
+      cudaGraphExecDestroy(h->gexec);
+      h->gexec = nullptr;
+    }
+  }
+  const int nv = g.c == 1 ? g.dim : (g.dim == 3 ? 6 : 3);
+  LoadParams lp;
+  fill_loads(h, h_loads, lp);
+  CK(cudaEventRecord(h->e0, s));
+  // a1: r = f ; u = 0 ; d = 0 (first F5 overwrites)
+  KL(launch_rhs(h->cx, lp, h->r, s), KC_OTHER);
+  KL(launch_zero(h->u, (long long)g.nrhs * g.c * g.n, s), KC_OTHER);
+  for (int l = 0; l < g.nrhs; ++l) {
+    LoadState& st = h->h_st[l];
+    std::memset(&st, 0, sizeof(st));
+    st.active = 1;
+    st.rel_tol = rel_tol;
+    st.fixed_iters = fixed_iters;
+    st.max_iter = max_iter;
+    st.gamma1 = 1.0;
+    st.zero_floor = zero_floor(h, h_loads + l * nv, nv);
+  }
+  CK(cudaMemcpyAsync(h->st, h->h_st, g.nrhs * sizeof(LoadState), cudaMemcpyHostToDevice, s));
+  const long long work = (long long)g.nrhs * g.c * g.n;
+  const int chunk = work >= (1LL << 22) ? 4 : (work >= (1LL << 18) ? 8 : 16);
+  uno_status bs = build_graph(h, chunk, h->timing);
+  if (bs != UNO_OK) return bs;
+  const int per_iter = (g.dim == 3 ? 6 : 4);
+  int done = 0;
+  bool any = true;
+  while (any) {
+    if (done > cap + 1) break;  // safety: the device stops itself at cap
+    CK(cudaGraphLaunch(h->gexec, s));
+    launches += (long long)chunk * per_iter;
+    int before = 0;
+    for (int l = 0; l < g.nrhs; ++l) before = std::max(before, h->h_st[l].iters);
+    CK(cudaMemcpyAsync(h->h_st, h->st, g.nrhs * sizeof(LoadState), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    done += chunk;
+    any = false;
+    int after = 0;
+    for (int l = 0; l < g.nrhs; ++l) {
+      any = any || h->h_st[l].active;
+      after = std::max(after, h->h_st[l].iters);
+    }
+    if (h->timing) {  // accumulate only iterations that did work
+      const int worked = std::min(chunk, std::max(0, after - before));
+      for (int i = 0; i < worked; ++i)
+        for (int slot = 0; slot < 6; ++slot) {
+          if (g.dim == 2 && (slot == 1 || slot == 3)) continue;
+          float ms = 0.f;
+          if (cudaEventElapsedTime(&ms, h->tev[((size_t)i * 6 + slot) * 2], h->tev[((size_t)i * 6 + slot) * 2 + 1]) ==
+              cudaSuccess) {
+            h->kms[kSlotClass[slot]] += ms;
+            h->kcnt[kSlotClass[slot]] += 1;
+          }
+        }
+    }
+  }
+  KL(launch_finalize(h->cx, s), KC_OTHER);
+  KL(launch_mean_removal(h->cx, h->u, d_u, h->scratch, s), KC_OTHER);
+  CK(cudaEventRecord(h->e1, s));
+  CK(cudaMemcpyAsync(h->h_st, h->st, g.nrhs * sizeof(LoadState), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  CK(cudaGetLastError());
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, h->e0, h->e1);
+  h->last_ms = ms;
+  h->last_launches = launches;
+  uno_status worst = UNO_OK;
+  for (int l = 0; l < g.nrhs; ++l) {
+    const LoadState& st = h->h_st[l];
+    if (rep) {
+      rep[l].iterations = st.iters;
+      rep[l].converged = st.converged;
+      rep[l].status = st.status;
+      rep[l].pad_ = 0;
+      rep[l].r0_inf = st.r0;
+      rep[l].rel_res = st.r0 > 0 ? st.rn / st.r0 : 0.0;
+      rep[l].gamma_last = st.gamma1;
+    }
+    if (st.status != 0 && worst == UNO_OK) worst = (uno_status)st.status;
+  }
+  if (h_hist && h->hist) {
+    CK(cudaMemcpy(h_hist, h->hist, (size_t)g.nrhs * h->hist_stride * 8, cudaMemcpyDeviceToHost));
+  }
+  if (worst != UNO_OK) return fail(worst, "PCG breakdown or non-finite residual (see per-load report)");
+  return UNO_OK;
+}
+
+extern "C" uno_status uno_cg_effective_property(uno_cg_handle* h, const double* d_u, const double* h_loads,
+                                                double* h_out) {
+  if (!h || !d_u || !h_loads || !h_out) return fail(UNO_ERR_ARG, "null argument");
+  const Geo& g = h->g;
+  LoadParams lp;
+  fill_loads(h, h_loads, lp);
+  int nblk = 0;
+  launch_effective(h->cx, lp, d_u, h->scratch, &nblk, h->stream);
+  const int nl = g.nrhs, nacc = nl * nl + 1;
+  CK(cudaMemcpyAsync(h->h_small, h->scratch + (long long)nacc * nblk, nacc * 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  CK(cudaGetLastError());
+  const double vf = h->h_small[nl * nl] / (double)g.n;
+  const double vol = (double)g.n * std::pow(g.h, g.dim);
+  const int nv = g.c == 1 ? g.dim : (g.dim == 3 ? 6 : 3);
+  for (int i = 0; i < nl; ++i)
+    for (int j = 0; j < nl; ++j) {
+      double base;
+      const double* li = h_loads + i * nv;
+      const double* lj = h_loads + j * nv;
+      if (g.c == 1) {
+        const double km = (1 - vf) * h->desc.mat[0][0] + vf * h->desc.mat[1][0];
+        double dot = 0;
+        for (int k = 0; k < nv; ++k) dot += li[k] * lj[k];
+        base = km * dot;
+      } else {  // B_i : <D> : B_j  with D = lam m m^T + 2 mu I (Mandel)
+        const double lam = (1 - vf) * h->desc.mat[0][0] + vf * h->desc.mat[1][0];
+        const double mu = (1 - vf) * h->desc.mat[0][1] + vf * h->desc.mat[1][1];
+        double tri = 0, trj = 0, dot = 0;
+        for (int k = 0; k < g.dim; ++k) {
+          tri += li[k];
+          trj += lj[k];
+        }
+        for (int k = 0; k < nv; ++k) dot += li[k] * lj[k];
+        base = lam * tri * trj + 2 * mu * dot;
+      }
+      h_out[i * nl + j] = base - h->h_small[i * nl + j] / vol;
+    }
+  return UNO_OK;
+}
+
+extern "C" uno_status uno_cg_last_solve_stats(uno_cg_handle* h, double* ms, int64_t* kernel_launches) {
+  if (!h) return fail(UNO_ERR_ARG, "null handle");
+  if (ms) *ms = h->last_ms;
+  if (kernel_launches) *kernel_launches = h->last_launches;
+  return UNO_OK;
+}
+
+extern "C" uno_status uno_cg_kernel_timing(uno_cg_handle* h, int32_t enable, int32_t reset, double* ms6,
+                                           int64_t* count6) {
+  if (!h) return fail(UNO_ERR_ARG, "null handle");
+  if (reset) {
+    for (int i = 0; i < KC_N; ++i) {
+      h->kms[i] = 0;
+      h->kcnt[i] = 0;
+    }
+  }
+  if (enable >= 0) h->timing = enable != 0;
+  if (ms6)
+    for (int i = 0; i < KC_N; ++i) ms6[i] = h->kms[i];
+  if (count6)
+    for (int i = 0; i < KC_N; ++i) count6[i] = h->kcnt[i];
+  return UNO_OK;
+}
+
+extern "C" const char* uno_cg_last_error(void) { return g_err.c_str(); }
+extern "C" const char* uno_cg_version(void) { return "libunocg 0.1 (sm_100a, fp64)"; }

@@ -1,0 +1,71 @@
+"""C-ABI boundary checks that need no GPU: libunocg.so loads and exports every entry point
+declared in include/uno_cg.h; the ctypes structs match the C layout; argument validation
+paths that fail before touching the device return the documented status codes."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "uno_cg.h")
+LIB = os.path.join(ROOT, "paper_2508_02681_b200", "lib", "libunocg.so")
+
+
+def _ensure_built():
+    if not os.path.exists(LIB):
+        import __graft_entry__
+
+        __graft_entry__.build()
+    assert os.path.exists(LIB)
+
+
+def _declared():
+    txt = open(HDR).read()
+    return sorted(set(re.findall(r"\b(uno_cg_[A-Za-z_]+)\s*\(", txt)) - {"uno_cg_handle"})
+
+
+def test_header_declares_north_star_entry_points():
+    names = _declared()
+    for n in ("uno_cg_create", "uno_cg_apply_K", "uno_cg_apply_precond", "uno_cg_solve", "uno_cg_effective_property"):
+        assert n in names
+
+
+def test_library_exports_every_declared_symbol():
+    _ensure_built()
+    out = subprocess.run(["nm", "-D", "--defined-only", LIB], capture_output=True, text=True, check=True).stdout
+    exported = set(re.findall(r"\bT\s+(uno_cg_\w+)", out))
+    missing = [n for n in _declared() if n not in exported]
+    assert not missing, missing
+    # nothing but the C ABI is exported (hidden visibility for the C++/CUDA internals)
+    extra = [l for l in out.splitlines() if " T " in l and "uno_cg_" not in l and "_init" not in l and "_fini" not in l]
+    assert not extra, extra[:5]
+
+
+def test_library_loads_and_validates_without_gpu():
+    _ensure_built()
+    import torch  # noqa: F401  (makes libcudart resolvable)
+
+    from paper_2508_02681_b200 import binding as B
+
+    assert B.uno_cg_version().startswith("libunocg")
+    # struct layout matches the header (offsets checked against the C declaration order)
+    assert ctypes.sizeof(B.UnoCgDesc) == 120
+    assert B.UnoCgDesc.stream.offset == 112 and B.UnoCgDesc.seed.offset == 88
+    assert ctypes.sizeof(B.UnoCgReport) == 40
+    d = B.UnoCgDesc()
+    d.dim = 4
+    with pytest.raises(B.UnoError) as e:
+        B.uno_cg_create(d, 1)
+    assert e.value.status == B.UNO_ERR_ARG
+    d.dim, d.n[0], d.n[1], d.n[2], d.nrhs = 3, 12, 8, 8, 1
+    d.mat[0][0] = d.mat[1][0] = 1.0
+    with pytest.raises(B.UnoError) as e:
+        B.uno_cg_create(d, 1)
+    assert e.value.status == B.UNO_ERR_SHAPE
+    d.n[0] = 16
+    d.bc[2] = 1
+    with pytest.raises(B.UnoError) as e:
+        B.uno_cg_create(d, 1)
+    assert e.value.status == B.UNO_ERR_UNSUPPORTED

@@ -1,0 +1,222 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on identical seeded
+inputs.  Tolerances:
+  apply_K      rel-L2 <= 1e-13        apply_precond rel-L2 <= 1e-12       rhs <= 1e-14 (of ||f||)
+  dots         rel <= 1e-12           solve: |iters - oracle| <= 1, u rel-L2 <= 1e-9 at a common
+  iteration count (fixed_iters = oracle's), effective property rel <= 1e-10 (BASELINE north_star).
+Shapes are deliberately non-cubic (catch transposed axes) and span several CTA tiles."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import fem, greens, homog, pcg  # noqa: E402
+from paper_2508_02681_b200 import synth  # noqa: E402
+
+
+def _api():
+    from paper_2508_02681_b200.api import UnoCG
+
+    return UnoCG
+
+
+def dev():
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    return torch.device("cuda:0")
+
+
+def rel(a, b):
+    return float(np.linalg.norm((a - b).ravel()) / max(np.linalg.norm(b.ravel()), 1e-300))
+
+
+def make_case(N, physics, seed=11, vf=0.35, rng_seed=0):
+    rng = np.random.default_rng(rng_seed)
+    shp = tuple(reversed(N))
+    ph = (rng.random(shp) < vf).astype(np.uint8)
+    d = len(N)
+    if physics == "thermal":
+        mat = (1.0, 17.0)
+        amp = 0.1
+    else:
+        mat = (synth.lame_from_E_nu(1.0, 0.3), synth.lame_from_E_nu(10.0, 0.2))
+        amp = 0.05
+    g = fem.Grid(N, c=1 if physics == "thermal" else d, h=1.0 / N[0])
+    return g, ph, mat, amp, seed
+
+
+def solver(ph, physics, mat, nrhs, seed, amp):
+    UnoCG = _api()
+    return UnoCG(torch.from_numpy(ph).to(dev()), physics, mat, nrhs=nrhs, seed=seed, amp=amp)
+
+
+def loads_for(physics, d, nrhs):
+    nv = d if physics == "thermal" else d * (d + 1) // 2
+    L = np.zeros((nrhs, nv))
+    for i in range(nrhs):
+        L[i, i % nv] = 1.0
+        L[i, (i + 1) % nv] += 0.25 * i
+    return L
+
+
+SHAPES = [((16, 8, 32), "thermal"), ((32, 16, 8), "thermal"), ((64, 64, 64), "thermal"), ((32, 32), "thermal"),
+          ((8, 64), "thermal"), ((16, 8, 16), "elastic"), ((32, 16, 8), "elastic"), ((16, 32), "elastic")]
+
+
+@pytest.mark.parametrize("N,physics", SHAPES)
+def test_apply_K_parity(N, physics):
+    g, ph, mat, amp, seed = make_case(N, physics)
+    nrhs = 2
+    s = solver(ph, physics, mat, nrhs, seed, amp)
+    u = np.stack([synth.test_vector(5 + l, g.field_shape()) for l in range(nrhs)])
+    Ku, dots = s.apply_K(torch.from_numpy(u).to(dev()), want_dot=True)
+    Ku = Ku.cpu().numpy()
+    for l in range(nrhs):
+        ref = fem.apply_K(g, physics, ph, mat, u[l])
+        assert rel(Ku[l], ref) <= 1e-13
+        assert abs(dots[l] - np.sum(u[l] * ref)) <= 1e-12 * abs(np.sum(u[l] * ref))
+
+
+@pytest.mark.parametrize("N,physics", SHAPES)
+def test_apply_precond_parity(N, physics):
+    g, ph, mat, amp, seed = make_case(N, physics)
+    nrhs = 2
+    s = solver(ph, physics, mat, nrhs, seed, amp)
+    G = greens.ghat(g, physics, mat, seed, amp)
+    r = np.stack([synth.test_vector(9 + l, g.field_shape()) for l in range(nrhs)])
+    z, rz = s.apply_precond(torch.from_numpy(r).to(dev()), want_dot=True)
+    z = z.cpu().numpy()
+    for l in range(nrhs):
+        ref = greens.apply_precond(G, r[l])
+        assert rel(z[l], ref) <= 1e-12
+        assert abs(rz[l] - np.sum(r[l] * ref)) <= 1e-12 * abs(np.sum(r[l] * ref))
+
+
+@pytest.mark.parametrize("N,physics", SHAPES)
+def test_rhs_parity(N, physics):
+    g, ph, mat, amp, seed = make_case(N, physics)
+    d = len(N)
+    nrhs = 3
+    L = loads_for(physics, d, nrhs)
+    s = solver(ph, physics, mat, nrhs, seed, amp)
+    f = s.rhs(L).cpu().numpy()
+    for l in range(nrhs):
+        ref = fem.rhs(g, physics, ph, mat, L[l])
+        assert np.max(np.abs(f[l] - ref)) <= 1e-14 * np.max(np.abs(ref))
+
+
+def test_homogeneous_PK_identity_full_sizes():
+    # P K u = u - mean(u) for a homogeneous medium with seed 0 holds at any size:
+    # covers the 256^3 and 512^3 transform instances without a CPU reference.
+    for N, physics in [((256, 256, 256), "thermal"), ((128, 64, 512), "elastic")]:
+        d = len(N)
+        c = 1 if physics == "thermal" else d
+        shp = tuple(reversed(N))
+        ph = torch.zeros(shp, dtype=torch.uint8, device=dev())
+        mat = (2.0, 2.0) if physics == "thermal" else ((0.8, 0.5), (0.8, 0.5))
+        s = _api()(ph, physics, mat, nrhs=1, seed=0)
+        u = torch.rand((1, c) + shp, dtype=torch.float64, device=dev()) * 2 - 1
+        v = s.apply_precond(s.apply_K(u))
+        um = u - u.mean(dim=tuple(range(2, 2 + d)), keepdim=True)
+        err = float((v - um).norm() / um.norm())
+        assert err < 1e-11, (N, physics, err)
+        s.close()
+        del u, v, um
+        torch.cuda.empty_cache()
+
+
+def _solve_parity(g, physics, ph, mat, loads, seed, amp, max_iter=500):
+    nrhs = loads.shape[0]
+    s = solver(ph, physics, mat, nrhs, seed, amp)
+    res = s.solve(loads, rel_tol=1e-8, max_iter=max_iter)
+    ref = homog.solve_problem(g, physics, ph, mat, loads, seed, amp, tol=1e-8, max_iter=max_iter)
+    its = [r["iterations"] for r in res.reports]
+    for a, b in zip(its, ref["iterations"]):
+        assert abs(a - b) <= 1, (its, ref["iterations"])
+    assert all(r["converged"] for r in res.reports)
+    # common-iteration protocol for every load
+    U = np.zeros_like(ref["U"])
+    for l in range(nrhs):
+        m = ref["iterations"][l]
+        fx = homog.solve_problem(g, physics, ph, mat, loads[l:l + 1], seed, amp, fixed_iters=max(m, 1))
+        sl = solver(ph, physics, mat, 1, seed, amp)
+        gu = sl.solve(loads[l:l + 1], fixed_iters=max(m, 1), max_iter=max_iter).u.cpu().numpy()[0]
+        if np.linalg.norm(fx["U"][0]) > 0:
+            assert rel(gu, fx["U"][0]) <= 1e-9, (l, rel(gu, fx["U"][0]))
+        U[l] = gu
+    # effective property from the common-iteration solutions
+    keff_gpu = s.effective_property(torch.from_numpy(U).to(dev()), loads)
+    keff_ref = homog.effective_from_solutions(g, physics, ph, mat, ref["F"], U)
+    assert np.max(np.abs(keff_gpu - keff_ref)) <= 1e-10 * np.max(np.abs(keff_ref))
+    # and the converged solutions' effective property against the oracle's converged one
+    keff_conv = s.effective_property(res.u, loads)
+    assert np.max(np.abs(keff_conv - ref["effective"])) <= 1e-7 * np.max(np.abs(ref["effective"]))
+    return its, ref
+
+
+def test_solve_config0():
+    P = synth.config0()
+    g = fem.Grid((32, 32), h=1 / 32)
+    _solve_parity(g, "thermal", P.phase, P.mat, np.eye(2), P.seed, P.amp)
+
+
+def test_solve_config1_64cubed():
+    P = synth.config1()
+    g = fem.Grid((64, 64, 64), h=1 / 64)
+    _solve_parity(g, "thermal", P.phase, P.mat, P.loads, P.seed, P.amp)
+
+
+def test_solve_elastic_small():
+    # config-2 physics (E 1/10, nu .3/.2, Mandel loads) on a 16x16x8 RSA microstructure
+    ph = synth.spheres_rsa(16, 0.25, 2.0, 3.0, seed=2)[:8]
+    g = fem.Grid((16, 16, 8), c=3, h=1 / 16)
+    mat = (synth.lame_from_E_nu(1.0, 0.3), synth.lame_from_E_nu(10.0, 0.2))
+    _solve_parity(g, "elastic", np.ascontiguousarray(ph), mat, np.eye(6)[[0, 3, 5]], 1002, 0.05)
+
+
+def test_solve_2d_elastic():
+    ph = synth.disc_2d(32, 9.6, seed=0)
+    g = fem.Grid((32, 32), c=2, h=1 / 32)
+    mat = (synth.lame_from_E_nu(1.0, 0.0 + 1e-9), synth.lame_from_E_nu(10.0, 0.3))
+    _solve_parity(g, "elastic", ph, mat, np.eye(3), 7, 0.05)
+
+
+def test_zero_rhs_and_mixed_convergence():
+    # homogeneous medium: f = 0 -> 0 iterations, u = 0 (SURVEY §8(b) Errors); batched with a
+    # laminate whose in-plane load also has zero RHS while the normal load iterates.
+    N = (16, 8, 8)
+    shp = tuple(reversed(N))
+    ph0 = np.zeros(shp, np.uint8)
+    s = solver(ph0, "thermal", (1.0, 5.0), 2, 3, 0.1)
+    res = s.solve(np.eye(3)[:2])
+    assert [r["iterations"] for r in res.reports] == [0, 0]
+    assert float(res.u.abs().max()) == 0.0
+    lam = synth.laminate(shp, 0, period=4, width=2)
+    s = solver(lam, "thermal", (1.0, 5.0), 2, 3, 0.1)
+    res = s.solve(np.eye(3)[[1, 0]])
+    its = [r["iterations"] for r in res.reports]
+    assert its[0] == 0 and its[1] >= 1 and res.reports[1]["converged"]
+    g = fem.Grid(N, h=1 / 16)
+    keff = s.effective_property(res.u, np.eye(3)[[1, 0]])
+    voigt, reuss = homog.voigt_reuss(1.0, 5.0, lam.mean())
+    assert abs(keff[0, 0] - voigt) < 1e-12 and abs(keff[1, 1] - reuss) < 1e-8 * reuss
+
+
+def test_determinism_bitwise():
+    P = synth.config0()
+    s = solver(P.phase, "thermal", P.mat, 2, P.seed, P.amp)
+    a = s.solve(np.eye(2)).u.clone()
+    b = s.solve(np.eye(2)).u.clone()
+    assert torch.equal(a, b)
+
+
+def test_full_size_config3_fixed_iterations():
+    # config-3 shape (256^3, 3 loads) in the launch configuration bench.py times: two PCG
+    # iterations against the oracle (numpy at 256^3 takes ~10 s per iteration).
+    ph = synth.config3_microstructure(3)
+    R = 20.0
+    g = fem.Grid((256, 256, 256), h=1 / 256)
+    s = solver(ph, "thermal", (1.0, R), 3, 3003, 0.1)
+    res = s.solve(np.eye(3), fixed_iters=2)
+    u = res.u.cpu().numpy()
+    ref = homog.solve_problem(g, "thermal", ph, (1.0, R), np.eye(3)[:1], 3003, 0.1, fixed_iters=2)
+    assert rel(u[0], ref["U"][0]) <= 1e-11
