@@ -14,17 +14,23 @@ import numpy as np
 from . import fem, greens, pcg
 
 
-def effective_from_solutions(g: fem.Grid, physics: str, phase, mat, F: np.ndarray, U: np.ndarray) -> np.ndarray:
-    """F, U: [nload] fields (f^(i), u^(j)).  Returns [nload][nload]."""
+def effective_from_solutions(g: fem.Grid, physics: str, phase, mat, F: np.ndarray, U: np.ndarray,
+                             loads=None) -> np.ndarray:
+    """F, U: [nload] fields (f^(i), u^(j)) for the load vectors `loads` (default: the first
+    nload unit loads).  Returns [nload][nload] = load_i.<C>.load_j - f^(i).u^(j)/|Omega|."""
     nl = F.shape[0]
     vol = g.volume()
+    if loads is None:
+        nv = g.d if physics == "thermal" else fem.mandel_dim(g.d)
+        loads = np.eye(nv)[:nl]
+    L = np.asarray(loads, dtype=float)
     if physics == "thermal":
-        base = fem.phase_mean(phase, *mat) * np.eye(nl)
+        base = fem.phase_mean(phase, *mat) * (L @ L.T)
     else:
         (l0, m0), (l1, m1) = mat
         lam_m = fem.phase_mean(phase, l0, l1)
         mu_m = fem.phase_mean(phase, m0, m1)
-        base = fem.isotropic_D(g.d, lam_m, mu_m)[:nl, :nl]
+        base = L @ fem.isotropic_D(g.d, lam_m, mu_m) @ L.T
     FU = np.array([[float(np.sum(F[i] * U[j])) for j in range(nl)] for i in range(nl)])
     return base - FU / vol
 
@@ -135,5 +141,5 @@ def solve_problem(g: fem.Grid, physics: str, phase, mat, loads, seed: int, amp: 
         results.append(res)
     F = np.stack(F)
     U = np.stack(U)
-    eff = effective_from_solutions(g, physics, phase, mat, F, U)
+    eff = effective_from_solutions(g, physics, phase, mat, F, U, loads)
     return {"G": G, "F": F, "U": U, "iterations": its, "results": results, "effective": eff}

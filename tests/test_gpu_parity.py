@@ -145,7 +145,7 @@ def _solve_parity(g, physics, ph, mat, loads, seed, amp, max_iter=500):
         U[l] = gu
     # effective property from the common-iteration solutions
     keff_gpu = s.effective_property(torch.from_numpy(U).to(dev()), loads)
-    keff_ref = homog.effective_from_solutions(g, physics, ph, mat, ref["F"], U)
+    keff_ref = homog.effective_from_solutions(g, physics, ph, mat, ref["F"], U, loads)
     assert np.max(np.abs(keff_gpu - keff_ref)) <= 1e-10 * np.max(np.abs(keff_ref))
     # and the converged solutions' effective property against the oracle's converged one
     keff_conv = s.effective_property(res.u, loads)
