@@ -452,81 +452,128 @@ __device__ void dp_finish(const Ctx& cx, int load, int nblk, int my, double part
 // element row (App. A1: h{1/3, 0, -1/12, -1/12}) gives
 //   p_i = h/12 [ 5 d_i sum_o k_o + sum_{6 axis nbrs j} d_j (sum of k over the 4 octants
 //         sharing edge ij) - sum_o k_o S_o ],   S_o = sum of the 8 corner values of o.
-// CTA = TX x 8 nodes marching over ZC z-planes with a 3-plane smem ring (2.5D blocking).
+// CTA = TX x 8 nodes marching over ZC z-planes (2.5D blocking).  Node planes of d stream
+// through a 7-deep shared-memory ring with cp.async (LDGSTS) issued 3 planes ahead, so HBM
+// latency overlaps the stencil arithmetic; S_o is built from per-plane 2x2 box sums Q.
 constexpr int KT_TY = 8;
-__global__ void __launch_bounds__(256) kp_thermal3d_kernel(Ctx cx, int mode, const double* __restrict__ src,
-                                                           double* __restrict__ dst, int TX, int ZC) {
+constexpr int KT_RING = 7;
+
+__device__ __forceinline__ void cp_async8(void* smem_ptr, const void* gptr) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_ptr);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gptr) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <int TX>
+__global__ void __launch_bounds__(TX * KT_TY) kp_thermal3d_kernel(Ctx cx, int mode, const double* __restrict__ src,
+                                                                  double* __restrict__ dst, int ZC) {
+  constexpr int T = TX * KT_TY;
+  constexpr int DW = TX + 2, DP = 10 * DW;       // d plane tile with halo
+  constexpr int EW = TX + 1, EP = 9 * EW;        // element-layer tile
+  constexpr int ND = (DP + T - 1) / T, NE = (EP + T - 1) / T;
   const Geo g = cx.g;
   const int nzc = g.N3 / ZC;
   const int load = blockIdx.z / nzc;
   const int zcI = blockIdx.z - load * nzc;
   if (mode == CG && !cx.st[load].active) return;
   extern __shared__ double ksm[];
-  const int DW = TX + 2, EW = TX + 1;
-  double* D = ksm;                       // [3][10][DW]
-  double* Kp = D + 3 * 10 * DW;          // [2][9][EW]
-  double* Q = Kp + 2 * 9 * EW;           // [3][9][EW]
+  double* D = ksm;                      // [KT_RING][DP]
+  double* Q = D + KT_RING * DP;         // [3][EP]
+  double* KA = Q + 3 * EP;              // [3][EP]
   __shared__ double red_sh[32];
-  const int t = threadIdx.x, T = blockDim.x;
+  const int t = threadIdx.x;
   const int tx = t % TX, ty = t / TX;
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * KT_TY, zs = zcI * ZC;
+  const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
+  const long long plane = (long long)N1 * N2;
   const double* dv = src + (long long)load * g.n;
   const double k0 = cx.mat[0][0], k1 = cx.mat[1][0];
-  const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
 
-  auto load_plane = [&](int zz, int slot) {
-    const int zw = (zz + N3) % N3;
-    double* Ds = D + slot * 10 * DW;
-    for (int i = t; i < 10 * DW; i += T) {
-      const int ly = i / DW, lx = i - ly * DW;
-      const int gx = (x0 - 1 + lx + N1) & (N1 - 1), gy = (y0 - 1 + ly + N2) & (N2 - 1);
-      Ds[i] = __ldg(dv + ((long long)zw * N2 + gy) * N1 + gx);
-    }
+  int goffD[ND], goffE[NE], qbase[NE];
+#pragma unroll
+  for (int m = 0; m < ND; ++m) {
+    const int j = t + m * T;
+    const int ly = j / DW, lx = j - ly * DW;
+    goffD[m] = ((y0 - 1 + ly + N2) & (N2 - 1)) * N1 + ((x0 - 1 + lx + N1) & (N1 - 1));
+  }
+#pragma unroll
+  for (int m = 0; m < NE; ++m) {
+    const int j = t + m * T;
+    const int ly = j / EW, lx = j - ly * EW;
+    goffE[m] = ((y0 - 1 + ly + N2) & (N2 - 1)) * N1 + ((x0 - 1 + lx + N1) & (N1 - 1));
+    qbase[m] = ly * DW + lx;
+  }
+  auto issue_plane = [&](int p) {  // node plane p -> ring slot
+    const int zw = (p + N3) & (N3 - 1);
+    double* Ds = D + ((p - zs + 1) % KT_RING) * DP;
+    const double* base = dv + (long long)zw * plane;
+#pragma unroll
+    for (int m = 0; m < ND; ++m)
+      if (t + m * T < DP) cp_async8(Ds + t + m * T, base + goffD[m]);
   };
-  auto load_kappa = [&](int layer, int slot) {
-    const int zw = (layer + N3) % N3;
-    double* Ks = Kp + slot * 9 * EW;
-    for (int i = t; i < 9 * EW; i += T) {
-      const int ly = i / EW, lx = i - ly * EW;
-      const int gx = (x0 - 1 + lx + N1) & (N1 - 1), gy = (y0 - 1 + ly + N2) & (N2 - 1);
-      Ks[i] = __ldg(cx.phase + ((long long)zw * N2 + gy) * N1 + gx) ? k1 : k0;
-    }
+  unsigned char phv[NE];
+  auto fetch_phase = [&](int layer) {
+    const int zw = (layer + N3) & (N3 - 1);
+    const uint8_t* base = cx.phase + (long long)zw * plane;
+#pragma unroll
+    for (int m = 0; m < NE; ++m) phv[m] = (t + m * T < EP) ? __ldg(base + goffE[m]) : 0;
   };
-  auto compute_Q = [&](int slot) {
-    const double* Ds = D + slot * 10 * DW;
-    double* Qs = Q + slot * 9 * EW;
-    for (int i = t; i < 9 * EW; i += T) {
-      const int ly = i / EW, lx = i - ly * EW;
-      const double* r0 = Ds + ly * DW + lx;
-      Qs[i] = (r0[0] + r0[1]) + (r0[DW] + r0[DW + 1]);
-    }
+  auto store_kappa = [&](int layer) {
+    double* Ks = KA + ((layer - zs + 1) % 3) * EP;
+#pragma unroll
+    for (int m = 0; m < NE; ++m)
+      if (t + m * T < EP) Ks[t + m * T] = phv[m] ? k1 : k0;
   };
-  // prologue: node planes zs-1, zs ; element layer zs-1
-  load_plane(zs - 1, 0);
-  load_plane(zs, 1);
-  load_kappa(zs - 1, 0);
+  auto compute_Q = [&](int p) {
+    const double* Ds = D + ((p - zs + 1) % KT_RING) * DP;
+    double* Qs = Q + ((p - zs + 1) % 3) * EP;
+#pragma unroll
+    for (int m = 0; m < NE; ++m)
+      if (t + m * T < EP) {
+        const double* r0 = Ds + qbase[m];
+        Qs[t + m * T] = (r0[0] + r0[1]) + (r0[DW] + r0[DW + 1]);
+      }
+  };
+
+  // prologue: planes zs-1 .. zs+3 in flight (one commit group each); layer zs-1 stored.
+#pragma unroll 1
+  for (int p = zs - 1; p <= zs + 3; ++p) {
+    if (p <= zs + ZC) issue_plane(p);
+    cp_commit();
+  }
+  fetch_phase(zs - 1);
+  store_kappa(zs - 1);
+  fetch_phase(zs);
+  cp_wait<3>();  // planes zs-1, zs landed (this thread's copies)
   __syncthreads();
-  compute_Q(0);
-  compute_Q(1);
+  compute_Q(zs - 1);
+  compute_Q(zs);
   double part = 0.0;
   const double hc = g.h / 12.0;
+#pragma unroll 1
   for (int k = zs; k < zs + ZC; ++k) {
-    const int q = k - zs;                       // plane k-1 -> slot q%3, k -> (q+1)%3, k+1 -> (q+2)%3
-    const int sm1 = q % 3, s0 = (q + 1) % 3, sp1 = (q + 2) % 3;
-    const int klo = q & 1, khi = (q + 1) & 1;   // layers k-1, k
-    load_plane(k + 1, sp1);
-    load_kappa(k, khi);
+    if (k + 4 <= zs + ZC) issue_plane(k + 4);
+    cp_commit();
+    cp_wait<3>();      // plane k+1 landed
+    store_kappa(k);    // layer k (fetched one iteration ago)
+    if (k + 1 < zs + ZC) fetch_phase(k + 1);
     __syncthreads();
-    compute_Q(sp1);
+    compute_Q(k + 1);
     __syncthreads();
     {
-      const double* Klo = Kp + klo * 9 * EW + ty * EW + tx;
-      const double* Khi = Kp + khi * 9 * EW + ty * EW + tx;
+      const int sm1 = (k - zs) % KT_RING, s0 = (k - zs + 1) % KT_RING, sp1 = (k - zs + 2) % KT_RING;
+      const int qm1 = (k - zs) % 3, q0 = (k - zs + 1) % 3, qp1 = (k - zs + 2) % 3;
+      const double* Klo = KA + qm1 * EP + ty * EW + tx;   // layer k-1 (slot of layer index k-1)
+      const double* Khi = KA + q0 * EP + ty * EW + tx;    // layer k
       const double a000 = Klo[0], a001 = Klo[1], a010 = Klo[EW], a011 = Klo[EW + 1];  // [oz][oy][ox]
       const double a100 = Khi[0], a101 = Khi[1], a110 = Khi[EW], a111 = Khi[EW + 1];
-      const double* Qm = Q + sm1 * 9 * EW + ty * EW + tx;
-      const double* Q0 = Q + s0 * 9 * EW + ty * EW + tx;
-      const double* Qp = Q + sp1 * 9 * EW + ty * EW + tx;
+      const double* Qm = Q + qm1 * EP + ty * EW + tx;
+      const double* Q0 = Q + q0 * EP + ty * EW + tx;
+      const double* Qp = Q + qp1 * EP + ty * EW + tx;
       const double S000 = Qm[0] + Q0[0], S001 = Qm[1] + Q0[1], S010 = Qm[EW] + Q0[EW], S011 = Qm[EW + 1] + Q0[EW + 1];
       const double S100 = Q0[0] + Qp[0], S101 = Q0[1] + Qp[1], S110 = Q0[EW] + Qp[EW], S111 = Q0[EW + 1] + Qp[EW + 1];
       const double Kxp = (a001 + a011) + (a101 + a111);
@@ -541,10 +588,11 @@ __global__ void __launch_bounds__(256) kp_thermal3d_kernel(Ctx cx, int mode, con
       KS = fma(a101, S101, KS);
       KS = fma(a110, S110, KS);
       KS = fma(a111, S111, KS);
-      const double* Dc = D + s0 * 10 * DW + (ty + 1) * DW + (tx + 1);
+      const int cidx = (ty + 1) * DW + (tx + 1);
+      const double* Dc = D + s0 * DP + cidx;
       const double di = Dc[0];
-      const double dzm = D[sm1 * 10 * DW + (ty + 1) * DW + (tx + 1)];
-      const double dzp = D[sp1 * 10 * DW + (ty + 1) * DW + (tx + 1)];
+      const double dzm = D[sm1 * DP + cidx];
+      const double dzp = D[sp1 * DP + cidx];
       double EE = Kxp * Dc[1];
       EE = fma(Ksum - Kxp, Dc[-1], EE);
       EE = fma(Kyp, Dc[DW], EE);
@@ -552,14 +600,11 @@ __global__ void __launch_bounds__(256) kp_thermal3d_kernel(Ctx cx, int mode, con
       EE = fma(Kzp, dzp, EE);
       EE = fma(Ksum - Kzp, dzm, EE);
       const double pv = hc * (fma(5.0 * di, Ksum, EE) - KS);
-      const int gx = x0 + tx, gy = y0 + ty;
-      if (gx < N1) {
-        dst[(long long)load * g.n + ((long long)k * N2 + gy) * N1 + gx] = pv;
-        part = fma(di, pv, part);
-      }
+      dst[(long long)load * g.n + (long long)k * plane + (long long)(y0 + ty) * N1 + (x0 + tx)] = pv;
+      part = fma(di, pv, part);
     }
-    __syncthreads();
   }
+  cp_wait<0>();
   const int nblk = gridDim.x * gridDim.y * nzc;
   const int my = (zcI * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
   dp_finish(cx, load, nblk, my, part, red_sh, mode);
@@ -1225,10 +1270,16 @@ int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaS
   const Geo& g = cx.g;
   if (g.dim == 3 && g.c == 1) {
     const int TX = g.N1 < 32 ? g.N1 : 32;
-    const int ZC = g.N3 < 16 ? g.N3 : 16;
-    const int sm = (3 * 10 * (TX + 2) + 2 * 9 * (TX + 1) + 3 * 9 * (TX + 1)) * (int)sizeof(double);
+    const int ZC = g.N3 < 32 ? g.N3 : 32;
+    const int sm = (KT_RING * 10 * (TX + 2) + 6 * 9 * (TX + 1)) * (int)sizeof(double);
     const dim3 grid(g.N1 / TX, g.N2 / KT_TY, (g.N3 / ZC) * g.nrhs);
-    kp_thermal3d_kernel<<<grid, TX * KT_TY, sm, s>>>(cx, mode, src, dst, TX, ZC);
+    auto go = [&](auto kern, int tpb) {
+      set_smem(kern, sm);
+      kern<<<grid, tpb, sm, s>>>(cx, mode, src, dst, ZC);
+    };
+    if (TX == 32) go(kp_thermal3d_kernel<32>, 256);
+    else if (TX == 16) go(kp_thermal3d_kernel<16>, 128);
+    else go(kp_thermal3d_kernel<8>, 64);
     return 1;
   }
   if (g.dim == 2 && g.c == 1) {
@@ -1311,7 +1362,7 @@ int blocks_needed_max(const Geo& g) {
   else m = m > (g.H1 + 7) / 8 ? m : (g.H1 + 7) / 8;
   long long kb;
   if (g.dim == 3 && g.c == 1) {
-    const int TX = g.N1 < 32 ? g.N1 : 32, ZC = g.N3 < 16 ? g.N3 : 16;
+    const int TX = g.N1 < 32 ? g.N1 : 32, ZC = g.N3 < 32 ? g.N3 : 32;
     kb = (long long)(g.N1 / TX) * (g.N2 / KT_TY) * (g.N3 / ZC);
   } else if (g.dim == 3) {
     const int ZC = g.N3 < 16 ? g.N3 : 16;

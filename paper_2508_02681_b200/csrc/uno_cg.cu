@@ -358,9 +358,10 @@ static int enqueue_iteration(uno_cg_handle* h, cudaStream_t s, cudaEvent_t* ev /
   const Ctx& cx = h->cx;
   int n = 0;
   auto run = [&](int slot, auto&& launch) -> bool {
-    if (ev) cudaEventRecord(ev[2 * slot], s);
+    // external event-record nodes (plain cudaEventRecord under capture is graph-internal)
+    if (ev) cudaEventRecordWithFlags(ev[2 * slot], s, cudaEventRecordExternal);
     const int r = launch();
-    if (ev) cudaEventRecord(ev[2 * slot + 1], s);
+    if (ev) cudaEventRecordWithFlags(ev[2 * slot + 1], s, cudaEventRecordExternal);
     if (r < 0) return false;
     n += r;
     return true;
@@ -490,6 +491,8 @@ extern "C" uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, doub
               cudaSuccess) {
             h->kms[kSlotClass[slot]] += ms;
             h->kcnt[kSlotClass[slot]] += 1;
+          } else {
+            (void)cudaGetLastError();  // clear the non-sticky error of a failed query
           }
         }
     }
