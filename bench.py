@@ -167,14 +167,18 @@ def run_ours(args):
     u = torch.empty((3, 1, n, n, n), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream()
     gen_s = time.time() - t0
+    # one solver per rank: its workspace is allocated once (like model memory); every problem
+    # of a step re-runs the a0 setup (reference medium, G_hat table, Eq 55) via uno_cg_update.
+    solver = UnoCG(phases[0], "thermal", (1.0, CONTRASTS[0]), nrhs=3, seed=3000, amp=0.1, stream=stream)
 
     def one_step(timing: bool):
         dofit = 0
         launches = 0
         kt = {}
         effs = []
+        s = solver
         for (m, R) in probs:
-            s = UnoCG(phases[m], "thermal", (1.0, R), nrhs=3, seed=3000 + m, amp=0.1, stream=stream)
+            s.update(phases[m], (1.0, R), seed=3000 + m, amp=0.1)
             launches += 2  # symbol build + Eq 55
             if timing:
                 s.kernel_timing(enable=1, reset=1)
@@ -188,7 +192,7 @@ def run_ours(args):
                     a = kt.setdefault(k, [0.0, 0])
                     a[0] += ms
                     a[1] += c
-            s.close()
+                s.kernel_timing(enable=0)
         return dofit, launches, kt, effs
 
     def barrier():
@@ -264,14 +268,14 @@ def run_ours(args):
             for i, p in enumerate(host_ph):
                 dph[i].copy_(p, non_blocking=True)
             out = []
+            s = solver
             for (m, R) in probs:
-                s = UnoCG(dph[m], "thermal", (1.0, R), nrhs=3, seed=3000 + m, amp=0.1, stream=stream)
+                s.update(dph[m], (1.0, R), seed=3000 + m, amp=0.1)
                 res = s.solve(loads, rel_tol=TOL, max_iter=MAX_IT, out=u)
                 keff = s.effective_property(res.u, loads)  # device -> host (9 doubles)
                 out.append((keff, [r["iterations"] for r in res.reports]))
-                d2h += keff.nbytes + 3 * 4 + 3 * 40  # kappa_bar + iteration counts + reports
+                d2h += keff.nbytes + 3 * 40  # kappa_bar + per-load reports
                 dofit += sum(r["iterations"] for r in res.reports) * n ** 3
-                s.close()
             return dofit
 
         e2e_step()

@@ -106,6 +106,13 @@ UNO_API uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_phase
 
 UNO_API uno_status uno_cg_destroy(uno_cg_handle* h);
 
+/* Re-target a handle to another problem of the SAME grid, physics, h and nrhs: new phase
+ * field, materials, reference medium, seed/amp.  Re-runs the a0 setup of uno_cg_create
+ * (reference medium, G_hat table, Eq 55) on the handle's workspace without reallocating.
+ * desc.stream is ignored (the handle keeps its stream).  On UNO_ERR_NOT_SPD the handle
+ * keeps the new (rejected) problem and must be updated again before solving.            */
+UNO_API uno_status uno_cg_update(uno_cg_handle* h, const uno_cg_desc* desc, const uint8_t* d_phase);
+
 /* Galerkin right-hand side f = l(phi_i) of the decomposition Eq 76 / Eq 81:
  *   thermal f_i = -sum_{e ni i} kappa_e (s(a).g_bar) h^(d-1)/2^(d-1)
  *   elastic f_(i,alpha) = -sum_e sum_j s(a)_j sigma_bar^e_(alpha j) h^(d-1)/2^(d-1),

@@ -59,6 +59,27 @@ class UnoCG:
         self.handle = B.uno_cg_create(d, phase)
         self.field_shape = (nrhs, self.c) + shp
 
+    def update(self, phase: torch.Tensor, mat, seed: int | None = None, amp: float | None = None, ref=None):
+        """Re-target this solver to another microstructure/material set of the same grid (a0 only)."""
+        assert phase.is_cuda and phase.dtype == torch.uint8 and phase.is_contiguous() and tuple(phase.shape) == tuple(self.phase.shape)
+        d = self.desc
+        if self.physics == "thermal":
+            d.mat[0][0], d.mat[1][0] = float(mat[0]), float(mat[1])
+        else:
+            (l0, m0), (l1, m1) = mat
+            d.mat[0][0], d.mat[0][1], d.mat[1][0], d.mat[1][1] = l0, m0, l1, m1
+        if ref is not None:
+            r = (ref, 0.0) if self.physics == "thermal" else tuple(ref)
+            d.ref[0], d.ref[1] = float(r[0]), float(r[1])
+        else:
+            d.ref[0] = d.ref[1] = 0.0
+        if seed is not None:
+            d.seed = int(seed)
+        if amp is not None:
+            d.amp = float(amp)
+        B.uno_cg_update(self.handle, d, phase)
+        self.phase = phase
+
     def close(self):
         if getattr(self, "handle", None):
             B.uno_cg_destroy(self.handle)

@@ -20,7 +20,7 @@ UNO_OK, UNO_ERR_ARG, UNO_ERR_SHAPE, UNO_ERR_CUDA, UNO_ERR_UNSUPPORTED, UNO_ERR_N
     UNO_ERR_NONFINITE = range(8)
 UNO_THERMAL, UNO_ELASTIC = 0, 1
 
-EXPORTS = ("uno_cg_create", "uno_cg_destroy", "uno_cg_rhs", "uno_cg_apply_K", "uno_cg_apply_precond",
+EXPORTS = ("uno_cg_create", "uno_cg_destroy", "uno_cg_update", "uno_cg_rhs", "uno_cg_apply_K", "uno_cg_apply_precond",
            "uno_cg_solve", "uno_cg_effective_property", "uno_cg_last_solve_stats", "uno_cg_kernel_timing",
            "uno_cg_last_error", "uno_cg_version")
 
@@ -49,6 +49,7 @@ def _load():
     P, D, I32, I64 = C.c_void_p, C.c_double, C.c_int32, C.c_int64
     lib.uno_cg_create.argtypes = [C.POINTER(UnoCgDesc), P, C.POINTER(P)]
     lib.uno_cg_destroy.argtypes = [P]
+    lib.uno_cg_update.argtypes = [P, C.POINTER(UnoCgDesc), P]
     lib.uno_cg_rhs.argtypes = [P, P, P]
     lib.uno_cg_apply_K.argtypes = [P, P, P, P]
     lib.uno_cg_apply_precond.argtypes = [P, P, P, P]
@@ -98,6 +99,10 @@ def uno_cg_create(desc: UnoCgDesc, d_phase) -> int:
 
 def uno_cg_destroy(h: int):
     _check(_lib.uno_cg_destroy(h), "uno_cg_destroy")
+
+
+def uno_cg_update(h: int, desc: UnoCgDesc, d_phase):
+    _check(_lib.uno_cg_update(h, C.byref(desc), _ptr(d_phase)), "uno_cg_update")
 
 
 def uno_cg_rhs(h: int, loads, d_f):

@@ -153,7 +153,7 @@ static void free_all(uno_cg_handle* h) {
   void* bufs[] = {h->r, h->d, h->p, h->u, h->spec, h->gtab, h->kel, h->twx, h->twxp, h->twy, h->twz,
                   h->st, h->partials, h->counters, h->results, h->scratch, h->hist};
   for (void* b : bufs)
-    if (b) cudaFree(b);
+    if (b) cudaFreeAsync(b, h->stream);
   if (h->h_st) cudaFreeHost(h->h_st);
   if (h->h_small) cudaFreeHost(h->h_small);
   if (h->e0) cudaEventDestroy(h->e0);
@@ -168,6 +168,58 @@ static void free_all(uno_cg_handle* h) {
     h->lcnt[cls] += n_;                                                               \
     launches += n_;                                                                   \
   } while (0)
+
+// a0: element matrices (elastic), tabulated G_hat(k)/n and the Eq 55 check.
+static uno_status setup_problem(uno_cg_handle* h) {
+  const uno_cg_desc& D = h->desc;
+  const Geo& g = h->g;
+  const int c = g.c;
+  cudaStream_t s = h->stream;
+  cudaError_t e;
+  if (D.ref[0] > 0) {
+    h->ref0 = D.ref[0];
+    h->ref1 = D.ref[1];
+  } else {  // arithmetic mean of the phases (SURVEY A7)
+    h->ref0 = 0.5 * (D.mat[0][0] + D.mat[1][0]);
+    h->ref1 = 0.5 * (D.mat[0][1] + D.mat[1][1]);
+  }
+  if (h->gexec) {  // materials are kernel parameters: re-capture on the next solve
+    cudaGraphExecDestroy(h->gexec);
+    h->gexec = nullptr;
+  }
+  if (c > 1) {
+    std::vector<double> Kl, Km, Kp;
+    elastic_element(g.dim, g.h, Kl, Km);
+    const size_t nn = Kl.size();
+    Kp.resize(2 * nn);
+    for (int ph = 0; ph < 2; ++ph)
+      for (size_t i = 0; i < nn; ++i) Kp[ph * nn + i] = D.mat[ph][0] * Kl[i] + D.mat[ph][1] * Km[i];
+    cudaMemcpyAsync(h->kel, Kp.data(), Kp.size() * 8, cudaMemcpyHostToDevice, s);
+    cudaStreamSynchronize(s);
+  }
+  h->cx = make_ctx(h);
+  // a0: symbol table + Eq 55 check
+  launch_build_symbol(h->cx, h->gtab, h->ref0, h->ref1, D.seed, D.seed ? D.amp : 0.0, s);
+  int nblk = 0;
+  launch_eq55(h->cx, h->gtab, h->scratch, &nblk, s);
+  std::vector<double> mm(2 * nblk);
+  cudaMemcpyAsync(mm.data(), h->scratch, 2 * nblk * 8, cudaMemcpyDeviceToHost, s);
+  e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(UNO_ERR_CUDA, std::string("create: ") + cudaGetErrorString(e));
+  double lo = 1e300, hi = -1e300;
+  for (int i = 0; i < nblk; ++i) {
+    lo = std::min(lo, mm[i]);
+    hi = std::max(hi, mm[nblk + i]);
+  }
+  h->lam_min = lo;
+  h->lam_max = hi;
+  if (!(lo > 1e-14)) {  // Eq 55, P:535-539
+    char buf[160];
+    std::snprintf(buf, sizeof buf, "Eq 55 safety check failed: min block eigenvalue %.3e", lo);
+    return fail(UNO_ERR_NOT_SPD, buf);
+  }
+  return UNO_OK;
+}
 
 // ------------------------------------------------------------------------------ create/destroy
 extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_phase, uno_cg_handle** out) {
@@ -210,16 +262,20 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
   g.nspec = (long long)g.H1 * N2 * N3;
   g.h = D.h > 0 ? D.h : 1.0 / N1;
   g.C = c * (c + 1) / 2;
-  if (D.ref[0] > 0) {
-    h->ref0 = D.ref[0];
-    h->ref1 = D.ref[1];
-  } else {  // arithmetic mean of the phases (SURVEY A7)
-    h->ref0 = 0.5 * (D.mat[0][0] + D.mat[1][0]);
-    h->ref1 = 0.5 * (D.mat[0][1] + D.mat[1][1]);
-  }
   cudaStream_t s = h->stream;
   const long long vec = (long long)g.nrhs * c * g.n;
-  auto al = [&](void** p, size_t bytes) -> cudaError_t { return cudaMalloc(p, bytes ? bytes : 8); };
+  static bool pool_cfg = false;
+  if (!pool_cfg) {  // keep freed workspace in the stream-ordered pool (cheap create/destroy)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ULL;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_cfg = true;
+  }
+  auto al = [&](void** p, size_t bytes) -> cudaError_t { return cudaMallocAsync(p, bytes ? bytes : 8, s); };
   cudaError_t e = cudaSuccess;
   const int maxb = blocks_needed_max(g);
   h->hist_stride = 0;
@@ -257,40 +313,10 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
   twiddles(N3, N3, t);
   cudaMemcpyAsync(h->twz, t.data(), N3 * 16, cudaMemcpyHostToDevice, s);
   cudaStreamSynchronize(s);
-  if (c > 1) {
-    std::vector<double> Kl, Km, Kp;
-    elastic_element(g.dim, g.h, Kl, Km);
-    const size_t nn = Kl.size();
-    Kp.resize(2 * nn);
-    for (int ph = 0; ph < 2; ++ph)
-      for (size_t i = 0; i < nn; ++i) Kp[ph * nn + i] = D.mat[ph][0] * Kl[i] + D.mat[ph][1] * Km[i];
-    cudaMemcpyAsync(h->kel, Kp.data(), Kp.size() * 8, cudaMemcpyHostToDevice, s);
-    cudaStreamSynchronize(s);
-  }
-  h->cx = make_ctx(h);
-  // a0: symbol table + Eq 55 check
-  launch_build_symbol(h->cx, h->gtab, h->ref0, h->ref1, D.seed, D.seed ? D.amp : 0.0, s);
-  int nblk = 0;
-  launch_eq55(h->cx, h->gtab, h->scratch, &nblk, s);
-  std::vector<double> mm(2 * nblk);
-  cudaMemcpyAsync(mm.data(), h->scratch, 2 * nblk * 8, cudaMemcpyDeviceToHost, s);
-  e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) {
+  const uno_status st0 = setup_problem(h);
+  if (st0 != UNO_OK) {
     free_all(h);
-    return fail(UNO_ERR_CUDA, std::string("create: ") + cudaGetErrorString(e));
-  }
-  double lo = 1e300, hi = -1e300;
-  for (int i = 0; i < nblk; ++i) {
-    lo = std::min(lo, mm[i]);
-    hi = std::max(hi, mm[nblk + i]);
-  }
-  h->lam_min = lo;
-  h->lam_max = hi;
-  if (!(lo > 1e-14)) {  // Eq 55, P:535-539
-    free_all(h);
-    char buf[160];
-    std::snprintf(buf, sizeof buf, "Eq 55 safety check failed: min block eigenvalue %.3e", lo);
-    return fail(UNO_ERR_NOT_SPD, buf);
+    return st0;
   }
   *out = h;
   return UNO_OK;
@@ -301,6 +327,29 @@ extern "C" uno_status uno_cg_destroy(uno_cg_handle* h) {
   cudaStreamSynchronize(h->stream);
   free_all(h);
   return UNO_OK;
+}
+
+extern "C" uno_status uno_cg_update(uno_cg_handle* h, const uno_cg_desc* desc, const uint8_t* d_phase) {
+  if (!h || !desc || !d_phase) return fail(UNO_ERR_ARG, "null argument");
+  const uno_cg_desc& D = *desc;
+  const uno_cg_desc& O = h->desc;
+  if (D.dim != O.dim || D.physics != O.physics || D.nrhs != O.nrhs || D.n[0] != O.n[0] || D.n[1] != O.n[1] ||
+      (D.dim == 3 && D.n[2] != O.n[2]) || D.h != O.h)
+    return fail(UNO_ERR_ARG, "update: grid, physics, h and nrhs must match the handle");
+  for (int i = 0; i < D.dim; ++i)
+    if (D.bc[i] != 0) return fail(UNO_ERR_UNSUPPORTED, "only periodic boundaries are built in this version");
+  if (D.physics == UNO_THERMAL) {
+    if (!(D.mat[0][0] > 0) || !(D.mat[1][0] > 0)) return fail(UNO_ERR_ARG, "conductivities must be > 0");
+  } else {
+    for (int p = 0; p < 2; ++p)
+      if (!(D.mat[p][1] > 0) || !(D.mat[p][0] >= 0)) return fail(UNO_ERR_ARG, "need mu > 0, lambda >= 0");
+  }
+  if (D.seed != 0 && !(D.amp >= 0 && D.amp < 1)) return fail(UNO_ERR_ARG, "amp must be in [0, 1)");
+  void* keep_stream = O.stream;
+  h->desc = D;
+  h->desc.stream = keep_stream;  // the handle stays on its creation stream
+  h->phase = d_phase;
+  return setup_problem(h);
 }
 
 static void fill_loads(const uno_cg_handle* h, const double* h_loads, LoadParams& lp) {
@@ -431,9 +480,9 @@ extern "C" uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, doub
   const int cap = fixed_iters > 0 ? fixed_iters : max_iter;
   // residual history buffer
   if (h_hist && h->hist_stride < cap + 1) {
-    if (h->hist) cudaFree(h->hist);
+    if (h->hist) cudaFreeAsync(h->hist, s);
     h->hist = nullptr;
-    CK(cudaMalloc(&h->hist, (size_t)kMaxRhs * (cap + 1) * 8));
+    CK(cudaMallocAsync(&h->hist, (size_t)kMaxRhs * (cap + 1) * 8, s));
     h->hist_stride = cap + 1;
     h->cx = make_ctx(h);
     if (h->gexec) {

@@ -220,3 +220,15 @@ def test_full_size_config3_fixed_iterations():
     u = res.u.cpu().numpy()
     ref = homog.solve_problem(g, "thermal", ph, (1.0, R), np.eye(3)[:1], 3003, 0.1, fixed_iters=2)
     assert rel(u[0], ref["U"][0]) <= 1e-11
+
+
+def test_update_equals_fresh_create():
+    # uno_cg_update re-runs a0 on the same workspace: results must be bitwise those of a fresh handle
+    P = synth.config0()
+    other = np.ascontiguousarray(np.roll(P.phase, 5, axis=1))
+    s = solver(P.phase, "thermal", P.mat, 2, P.seed, P.amp)
+    s.solve(np.eye(2))
+    s.update(torch.from_numpy(other).to(dev()), (1.0, 4.0), seed=77, amp=0.1)
+    a = s.solve(np.eye(2)).u.clone()
+    b = solver(other, "thermal", (1.0, 4.0), 2, 77, 0.1).solve(np.eye(2)).u
+    assert torch.equal(a, b)
