@@ -106,28 +106,43 @@ __device__ void scalar_after_dp(LoadState* st, double dp) {
   st->pending_u = 1;
 }
 
+// ============================================================================== async copy helpers
+__device__ __forceinline__ void cp_async16(void* smem_ptr, const void* gptr) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_ptr);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gptr) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem_ptr, const void* gptr) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_ptr);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gptr) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
 // ============================================================================== x passes
-template <int M>
+// smem: tile 8M | stage (xfwd: p rows 8M; xinv: spectrum rows, then d and u rows 16M) | tw M | twp M+1
+template <int M, bool INV>
 __host__ __device__ constexpr int xsmem_bytes() {
-  return (8 * M + M + (M + 1)) * (int)sizeof(double2);
+  return (8 * M + (INV ? 16 : 8) * M + M + (M + 1)) * (int)sizeof(double2);
 }
 
 // F1 / standalone forward: real rows of length N1 = 2M -> half spectrum [kx][z][y].
 template <int M, int MODE>
 __global__ void __launch_bounds__(fft_threads(M)) xfwd_kernel(Ctx cx, const double* __restrict__ src) {
+  constexpr int T = fft_threads(M);
   const Geo g = cx.g;
   const int load = blockIdx.y;
   LoadState* st = cx.st + load;
   if (MODE == CG && !st->active) return;
   extern __shared__ double2 smem[];
   double2* tile = smem;
-  double2* tw = smem + 8 * M;
+  double2* pbuf = smem + 8 * M;
+  double2* tw = pbuf + 8 * M;
   double2* twp = tw + M;
   __shared__ double red_sh[32];
-  const int T = blockDim.x, t = threadIdx.x;
-  for (int i = t; i < M; i += T) tw[i] = cx.tw.x[i];
-  for (int i = t; i <= M; i += T) twp[i] = cx.tw.xpost[i];
-
+  const int t = threadIdx.x;
   const long long row0 = (long long)blockIdx.x * 8;  // row = (comp, z, y) within the load
   const long long voff = (long long)load * g.c * g.n + row0 * g.N1;
   const double2* src2 = reinterpret_cast<const double2*>(src + voff);
@@ -139,18 +154,36 @@ __global__ void __launch_bounds__(fft_threads(M)) xfwd_kernel(Ctx cx, const doub
     upd = st->iters > 0;
     alpha = st->alpha;
   }
-  double mx = 0.0;
-  for (int e = t; e < 8 * M; e += T) {
-    const int row = e / M, j = e & (M - 1);
-    double2 v = src2[e];
-    if (MODE == CG && upd) {  // r <- r - alpha p   (Alg 2 l.11)
-      const double2 pv = p2[e];
-      v.x = fma(-alpha, pv.x, v.x);
-      v.y = fma(-alpha, pv.y, v.y);
-      r2[e] = v;
+  // all global reads in flight at once (cp.async), rows land transposed+swizzled in the tile
+#pragma unroll
+  for (int i = 0; i < (8 * M + T - 1) / T; ++i) {
+    const int e = t + i * T;
+    if (e < 8 * M) {
+      cp_async16(&tile[tidx(e & (M - 1), e / M)], src2 + e);
+      if (MODE == CG && upd) cp_async16(&pbuf[e], p2 + e);
     }
-    mx = fmax(mx, fmax(fabs(v.x), fabs(v.y)));
-    tile[tidx(j, row)] = v;
+  }
+  cp_commit();
+  for (int i = t; i < M; i += T) tw[i] = cx.tw.x[i];
+  for (int i = t; i <= M; i += T) twp[i] = cx.tw.xpost[i];
+  cp_wait<0>();
+  __syncthreads();
+  double mx = 0.0;
+#pragma unroll
+  for (int i = 0; i < (8 * M + T - 1) / T; ++i) {
+    const int e = t + i * T;
+    if (e < 8 * M) {
+      const int ti = tidx(e & (M - 1), e / M);
+      double2 v = tile[ti];
+      if (MODE == CG && upd) {  // r <- r - alpha p   (Alg 2 l.11)
+        const double2 pv = pbuf[e];
+        v.x = fma(-alpha, pv.x, v.x);
+        v.y = fma(-alpha, pv.y, v.y);
+        r2[e] = v;
+        tile[ti] = v;
+      }
+      mx = fmax(mx, fmax(fabs(v.x), fabs(v.y)));
+    }
   }
   __syncthreads();
   fft_tile<M, false>(tile, tw);
@@ -161,14 +194,18 @@ __global__ void __launch_bounds__(fft_threads(M)) xfwd_kernel(Ctx cx, const doub
   const int comp = (int)(zc / g.N3);
   double2* out = cx.spec + ((long long)load * g.c + comp) * g.nspec + (long long)z * g.N2 + y0;
   const long long plane = (long long)g.N3 * g.N2;
-  for (int it = t; it < (M / 2 + 1) * 8; it += T) {
-    const int row = it & 7, k = it >> 3;
-    const double2 a = tile[tidx(k, row)];
-    const double2 b = cconj(tile[tidx((M - k) & (M - 1), row)]);
-    const double2 E = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
-    const double2 O = mul_mi(make_double2(0.5 * (a.x - b.x), 0.5 * (a.y - b.y)));
-    out[(long long)k * plane + row] = cadd(E, cmul(twp[k], O));
-    if (k != M - k) out[(long long)(M - k) * plane + row] = cadd(cconj(E), cmul(twp[M - k], cconj(O)));
+#pragma unroll
+  for (int i = 0; i < ((M / 2 + 1) * 8 + T - 1) / T; ++i) {
+    const int it = t + i * T;
+    if (it < (M / 2 + 1) * 8) {
+      const int row = it & 7, k = it >> 3;
+      const double2 a = tile[tidx(k, row)];
+      const double2 b = cconj(tile[tidx((M - k) & (M - 1), row)]);
+      const double2 E = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
+      const double2 O = mul_mi(make_double2(0.5 * (a.x - b.x), 0.5 * (a.y - b.y)));
+      out[(long long)k * plane + row] = cadd(E, cmul(twp[k], O));
+      if (k != M - k) out[(long long)(M - k) * plane + row] = cadd(cconj(E), cmul(twp[M - k], cconj(O)));
+    }
   }
   if (MODE == CG) {
     double tot;
@@ -182,19 +219,17 @@ __global__ void __launch_bounds__(fft_threads(M)) xfwd_kernel(Ctx cx, const doub
 // F5 / standalone inverse: half spectrum -> real rows; CG epilogue d = s + beta d, u += alpha d_old.
 template <int M, int MODE>
 __global__ void __launch_bounds__(fft_threads(M)) xinv_kernel(Ctx cx, double* __restrict__ dst) {
+  constexpr int T = fft_threads(M);
   const Geo g = cx.g;
   const int load = blockIdx.y;
   LoadState* st = cx.st + load;
   if (MODE == CG && !st->active) return;
   extern __shared__ double2 smem[];
   double2* tile = smem;
-  double2* tw = smem + 8 * M;
+  double2* stage = smem + 8 * M;   // [M+1][8] spectrum rows, later d rows [8M] | u rows [8M]
+  double2* tw = stage + 16 * M;
   double2* twp = tw + M;
-  const int T = blockDim.x, t = threadIdx.x;
-  for (int i = t; i < M; i += T) tw[i] = cx.tw.x[i];
-  for (int i = t; i <= M; i += T) twp[i] = cx.tw.xpost[i];
-  __syncthreads();
-
+  const int t = threadIdx.x;
   const long long row0 = (long long)blockIdx.x * 8;
   const int y0 = (int)(row0 % g.N2);
   const long long zc = row0 / g.N2;
@@ -202,49 +237,87 @@ __global__ void __launch_bounds__(fft_threads(M)) xinv_kernel(Ctx cx, double* __
   const int comp = (int)(zc / g.N3);
   const double2* in = cx.spec + ((long long)load * g.c + comp) * g.nspec + (long long)z * g.N2 + y0;
   const long long plane = (long long)g.N3 * g.N2;
-  for (int it = t; it < (M / 2 + 1) * 8; it += T) {
-    const int row = it & 7, k = it >> 3;
-    if (k == 0) {
-      const double X0 = in[row].x, XM = in[(long long)M * plane + row].x;
-      tile[tidx(0, row)] = make_double2(X0 + XM, X0 - XM);
-    } else {
-      const double2 a = in[(long long)k * plane + row];
-      const double2 bm = in[(long long)(M - k) * plane + row];
-      const double2 b = cconj(bm);
-      const double2 E = cadd(a, b);
-      const double2 O = cmul(csub(a, b), cconj(twp[k]));
-      tile[tidx(k, row)] = cadd(E, mul_pi(O));
-      if (k != M - k) {
-        const double2 a2 = bm, b2 = cconj(a);
-        const double2 E2 = cadd(a2, b2);
-        const double2 O2 = cmul(csub(a2, b2), cconj(twp[M - k]));
-        tile[tidx(M - k, row)] = cadd(E2, mul_pi(O2));
+#pragma unroll
+  for (int i = 0; i < ((M + 1) * 8 + T - 1) / T; ++i) {
+    const int e = t + i * T;
+    if (e < (M + 1) * 8) cp_async16(&stage[e], in + (long long)(e >> 3) * plane + (e & 7));
+  }
+  cp_commit();
+  for (int i = t; i < M; i += T) tw[i] = cx.tw.x[i];
+  for (int i = t; i <= M; i += T) twp[i] = cx.tw.xpost[i];
+  cp_wait<0>();
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < ((M / 2 + 1) * 8 + T - 1) / T; ++i) {
+    const int it = t + i * T;
+    if (it < (M / 2 + 1) * 8) {
+      const int row = it & 7, k = it >> 3;
+      if (k == 0) {
+        const double X0 = stage[row].x, XM = stage[M * 8 + row].x;
+        tile[tidx(0, row)] = make_double2(X0 + XM, X0 - XM);
+      } else {
+        const double2 a = stage[k * 8 + row];
+        const double2 bm = stage[(M - k) * 8 + row];
+        const double2 b = cconj(bm);
+        const double2 E = cadd(a, b);
+        const double2 O = cmul(csub(a, b), cconj(twp[k]));
+        tile[tidx(k, row)] = cadd(E, mul_pi(O));
+        if (k != M - k) {
+          const double2 a2 = bm, b2 = cconj(a);
+          const double2 E2 = cadd(a2, b2);
+          const double2 O2 = cmul(csub(a2, b2), cconj(twp[M - k]));
+          tile[tidx(M - k, row)] = cadd(E2, mul_pi(O2));
+        }
       }
     }
   }
   __syncthreads();
-  fft_tile<M, true>(tile, tw);
-
   const long long voff = (long long)load * g.c * g.n + row0 * g.N1;
+  const int it0 = MODE == CG ? st->iters : 0;
+  if (MODE == CG) {  // d_old and u rows land while the inverse FFT runs
+    const double2* d2g = reinterpret_cast<const double2*>(cx.d + voff);
+    const double2* u2g = reinterpret_cast<const double2*>(cx.u + voff);
+    if (it0 > 0) {
+#pragma unroll
+      for (int i = 0; i < (8 * M + T - 1) / T; ++i) {
+        const int e = t + i * T;
+        if (e < 8 * M) {
+          cp_async16(&stage[e], d2g + e);
+          cp_async16(&stage[8 * M + e], u2g + e);
+        }
+      }
+    }
+    cp_commit();
+  }
+  fft_tile<M, true>(tile, tw);
   if (MODE == STANDALONE) {
     double2* o2 = reinterpret_cast<double2*>(dst + voff);
-    for (int e = t; e < 8 * M; e += T) o2[e] = tile[tidx(e & (M - 1), e / M)];
+#pragma unroll
+    for (int i = 0; i < (8 * M + T - 1) / T; ++i) {
+      const int e = t + i * T;
+      if (e < 8 * M) o2[e] = tile[tidx(e & (M - 1), e / M)];
+    }
   } else {
+    cp_wait<0>();
+    __syncthreads();
     double2* d2 = reinterpret_cast<double2*>(cx.d + voff);
     double2* u2 = reinterpret_cast<double2*>(cx.u + voff);
-    const int it0 = st->iters;
     const double beta = st->beta, alpha = st->alpha;
-    for (int e = t; e < 8 * M; e += T) {
-      const double2 s = tile[tidx(e & (M - 1), e / M)];
-      if (it0 == 0) {
-        d2[e] = s;  // d = s + (gamma1/gamma0) * 0   (Alg 2 l.2, l.8)
-      } else {
-        const double2 dold = d2[e];
-        double2 uu = u2[e];  // deferred u += alpha_{m-1} d_{m-1}  (Alg 2 l.12)
-        uu.x = fma(alpha, dold.x, uu.x);
-        uu.y = fma(alpha, dold.y, uu.y);
-        u2[e] = uu;
-        d2[e] = make_double2(fma(beta, dold.x, s.x), fma(beta, dold.y, s.y));
+#pragma unroll
+    for (int i = 0; i < (8 * M + T - 1) / T; ++i) {
+      const int e = t + i * T;
+      if (e < 8 * M) {
+        const double2 s = tile[tidx(e & (M - 1), e / M)];
+        if (it0 == 0) {
+          d2[e] = s;  // d = s + (gamma1/gamma0) * 0   (Alg 2 l.2, l.8)
+        } else {
+          const double2 dold = stage[e];
+          double2 uu = stage[8 * M + e];  // deferred u += alpha_{m-1} d_{m-1}  (Alg 2 l.12)
+          uu.x = fma(alpha, dold.x, uu.x);
+          uu.y = fma(alpha, dold.y, uu.y);
+          u2[e] = uu;
+          d2[e] = make_double2(fma(beta, dold.x, s.x), fma(beta, dold.y, s.y));
+        }
       }
     }
   }
@@ -258,26 +331,41 @@ __host__ __device__ constexpr int ysmem_bytes() {
 
 template <int L, bool INV, int MODE>
 __global__ void __launch_bounds__(fft_threads(L)) ypass_kernel(Ctx cx) {
+  constexpr int T = fft_threads(L);
   const Geo g = cx.g;
   const int load = blockIdx.y;
   if (MODE == CG && !cx.st[load].active) return;
   extern __shared__ double2 smem[];
   double2* tile = smem;
   double2* tw = smem + 8 * L;
-  const int T = blockDim.x, t = threadIdx.x;
-  for (int i = t; i < L; i += T) tw[i] = cx.tw.y[i];
+  const int t = threadIdx.x;
   const long long nrows = (long long)g.c * g.H1 * g.N3;
   const long long row0 = (long long)blockIdx.x * 8;
   double2* base = cx.spec + (long long)load * g.c * g.nspec + row0 * L;
-  for (int e = t; e < 8 * L; e += T) {
-    const int row = e / L, j = e & (L - 1);
-    tile[tidx(j, row)] = (row0 + row < nrows) ? base[e] : make_double2(0.0, 0.0);
+  const bool full = row0 + 8 <= nrows;
+#pragma unroll
+  for (int i = 0; i < (8 * L + T - 1) / T; ++i) {
+    const int e = t + i * T;
+    if (e < 8 * L) {
+      const int row = e / L, j = e & (L - 1);
+      if (full || row0 + row < nrows)
+        cp_async16(&tile[tidx(j, row)], base + e);
+      else
+        tile[tidx(j, row)] = make_double2(0.0, 0.0);
+    }
   }
+  cp_commit();
+  for (int i = t; i < L; i += T) tw[i] = cx.tw.y[i];
+  cp_wait<0>();
   __syncthreads();
   fft_tile<L, INV>(tile, tw);
-  for (int e = t; e < 8 * L; e += T) {
-    const int row = e / L, j = e & (L - 1);
-    if (row0 + row < nrows) base[e] = tile[tidx(j, row)];
+#pragma unroll
+  for (int i = 0; i < (8 * L + T - 1) / T; ++i) {
+    const int e = t + i * T;
+    if (e < 8 * L) {
+      const int row = e / L, j = e & (L - 1);
+      if (full || row0 + row < nrows) base[e] = tile[tidx(j, row)];
+    }
   }
 }
 
@@ -285,16 +373,16 @@ __global__ void __launch_bounds__(fft_threads(L)) ypass_kernel(Ctx cx) {
 // s_hat(k) = G_hat(k) r_hat(k) on one bin; returns w_k Re(r_hat^H G_hat r_hat) (Parseval term).
 // gtab holds the unique entries in Eq B7 order: v1=G11 v2=G22 v3=G12 v4=G33 v5=G23 v6=G13.
 template <int NC>
-__device__ __forceinline__ double gmul_bin(double2* const* tiles, int ti, const double* __restrict__ gtab,
-                                           long long nspec, long long b, double w) {
+__device__ __forceinline__ double gmul_bin(double2* const* tiles, int ti, const double* gtab, long long nspec,
+                                           long long b, double w) {
   if (NC == 1) {
-    const double gv = __ldg(gtab + b);
+    const double gv = gtab[b];
     double2 X = tiles[0][ti];
     const double q = w * gv * fma(X.x, X.x, X.y * X.y);
     tiles[0][ti] = make_double2(gv * X.x, gv * X.y);
     return q;
   } else if (NC == 2) {
-    const double v1 = __ldg(gtab + b), v2 = __ldg(gtab + nspec + b), v3 = __ldg(gtab + 2 * nspec + b);
+    const double v1 = gtab[b], v2 = gtab[nspec + b], v3 = gtab[2 * nspec + b];
     const double2 X1 = tiles[0][ti], X2 = tiles[1][ti];
     const double2 Y1 = make_double2(fma(v1, X1.x, v3 * X2.x), fma(v1, X1.y, v3 * X2.y));
     const double2 Y2 = make_double2(fma(v3, X1.x, v2 * X2.x), fma(v3, X1.y, v2 * X2.y));
@@ -302,8 +390,8 @@ __device__ __forceinline__ double gmul_bin(double2* const* tiles, int ti, const 
     tiles[1][ti] = Y2;
     return w * (X1.x * Y1.x + X1.y * Y1.y + X2.x * Y2.x + X2.y * Y2.y);
   } else {
-    const double v1 = __ldg(gtab + b), v2 = __ldg(gtab + nspec + b), v3 = __ldg(gtab + 2 * nspec + b);
-    const double v4 = __ldg(gtab + 3 * nspec + b), v5 = __ldg(gtab + 4 * nspec + b), v6 = __ldg(gtab + 5 * nspec + b);
+    const double v1 = gtab[b], v2 = gtab[nspec + b], v3 = gtab[2 * nspec + b];
+    const double v4 = gtab[3 * nspec + b], v5 = gtab[4 * nspec + b], v6 = gtab[5 * nspec + b];
     const double2 X1 = tiles[0][ti], X2 = tiles[1][ti], X3 = tiles[2][ti];
     double2 Y1, Y2, Y3;
     Y1.x = fma(v1, X1.x, fma(v3, X2.x, v6 * X3.x));
@@ -335,13 +423,24 @@ __device__ void gamma_finish(const Ctx& cx, int load, double part, double* red_s
 }
 
 template <int L, int NC>
-__host__ __device__ constexpr int gsmem_bytes() {
+__host__ __device__ constexpr int gsmem_tile_bytes() {
   return (NC * 8 * L + L) * (int)sizeof(double2);
+}
+// symbol entries of the tile's bins are staged in smem too when they fit
+template <int L, int NC>
+__host__ __device__ constexpr bool gstaged() {
+  return gsmem_tile_bytes<L, NC>() + 8 * L * (NC == 1 ? 1 : (NC == 2 ? 3 : 6)) * (int)sizeof(double) <= 200 * 1024;
+}
+template <int L, int NC>
+__host__ __device__ constexpr int gsmem_bytes() {
+  return gsmem_tile_bytes<L, NC>() + (gstaged<L, NC>() ? 8 * L * (NC == 1 ? 1 : (NC == 2 ? 3 : 6)) * (int)sizeof(double) : 0);
 }
 
 // 3D G pass: sequences along z (stride N2), tile = 8 consecutive y of one kx plane.
 template <int L, int NC, int MODE>
 __global__ void __launch_bounds__(fft_threads(L)) gpass_z_kernel(Ctx cx) {
+  constexpr int T = fft_threads(L);
+  constexpr int NCC = NC == 1 ? 1 : (NC == 2 ? 3 : 6);  // unique symbol entries per bin
   const Geo g = cx.g;
   const int load = blockIdx.y;
   if (MODE == CG && !cx.st[load].active) return;
@@ -350,9 +449,9 @@ __global__ void __launch_bounds__(fft_threads(L)) gpass_z_kernel(Ctx cx) {
 #pragma unroll
   for (int q = 0; q < NC; ++q) tiles[q] = smem + q * 8 * L;
   double2* tw = smem + NC * 8 * L;
+  double* gs = reinterpret_cast<double*>(tw + L);  // [NCC][8L] symbol entries of the tile's bins
   __shared__ double red_sh[32];
-  const int T = blockDim.x, t = threadIdx.x;
-  for (int i = t; i < L; i += T) tw[i] = cx.tw.z[i];
+  const int t = threadIdx.x;
   const int ntile_y = g.N2 >> 3;
   const int kx = blockIdx.x / ntile_y;
   const int y0 = (blockIdx.x - kx * ntile_y) * 8;
@@ -360,19 +459,40 @@ __global__ void __launch_bounds__(fft_threads(L)) gpass_z_kernel(Ctx cx) {
 #pragma unroll
   for (int q = 0; q < NC; ++q) {
     const double2* base = cx.spec + ((long long)load * g.c + q) * g.nspec + boff;
-    for (int e = t; e < 8 * L; e += T) {
-      const int j = e >> 3, c = e & 7;
-      tiles[q][tidx(j, c)] = base[(long long)j * g.N2 + c];
+#pragma unroll
+    for (int i = 0; i < (8 * L + T - 1) / T; ++i) {
+      const int e = t + i * T;
+      if (e < 8 * L) cp_async16(&tiles[q][tidx(e >> 3, e & 7)], base + (long long)(e >> 3) * g.N2 + (e & 7));
     }
   }
+  constexpr bool STG = gstaged<L, NC>();
+  if (STG) {
+#pragma unroll
+    for (int q = 0; q < NCC; ++q) {
+#pragma unroll
+      for (int i = 0; i < (8 * L + T - 1) / T; ++i) {
+        const int e = t + i * T;
+        if (e < 8 * L) cp_async8(&gs[q * 8 * L + e], cx.gtab + q * g.nspec + boff + (long long)(e >> 3) * g.N2 + (e & 7));
+      }
+    }
+  }
+  cp_commit();
+  for (int i = t; i < L; i += T) tw[i] = cx.tw.z[i];
+  cp_wait<0>();
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < NC; ++q) fft_tile<L, false>(tiles[q], tw);
   const double w = parseval_w(kx, g.M);
   double part = 0.0;
-  for (int e = t; e < 8 * L; e += T) {
-    const int j = e >> 3, c = e & 7;
-    part += gmul_bin<NC>(tiles, tidx(j, c), cx.gtab, g.nspec, boff + (long long)j * g.N2 + c, w);
+#pragma unroll
+  for (int i = 0; i < (8 * L + T - 1) / T; ++i) {
+    const int e = t + i * T;
+    if (e < 8 * L) {
+      if (STG)
+        part += gmul_bin<NC>(tiles, tidx(e >> 3, e & 7), gs, 8 * L, e, w);
+      else
+        part += gmul_bin<NC>(tiles, tidx(e >> 3, e & 7), cx.gtab, g.nspec, boff + (long long)(e >> 3) * g.N2 + (e & 7), w);
+    }
   }
   __syncthreads();
 #pragma unroll
@@ -380,9 +500,10 @@ __global__ void __launch_bounds__(fft_threads(L)) gpass_z_kernel(Ctx cx) {
 #pragma unroll
   for (int q = 0; q < NC; ++q) {
     double2* base = cx.spec + ((long long)load * g.c + q) * g.nspec + boff;
-    for (int e = t; e < 8 * L; e += T) {
-      const int j = e >> 3, c = e & 7;
-      base[(long long)j * g.N2 + c] = tiles[q][tidx(j, c)];
+#pragma unroll
+    for (int i = 0; i < (8 * L + T - 1) / T; ++i) {
+      const int e = t + i * T;
+      if (e < 8 * L) base[(long long)(e >> 3) * g.N2 + (e & 7)] = tiles[q][tidx(e >> 3, e & 7)];
     }
   }
   gamma_finish(cx, load, part, red_sh, MODE);
@@ -391,6 +512,8 @@ __global__ void __launch_bounds__(fft_threads(L)) gpass_z_kernel(Ctx cx) {
 // 2D G pass: sequences along y (contiguous), tile = 8 consecutive kx rows.
 template <int L, int NC, int MODE>
 __global__ void __launch_bounds__(fft_threads(L)) gpass_y2d_kernel(Ctx cx) {
+  constexpr int T = fft_threads(L);
+  constexpr int NCC = NC == 1 ? 1 : 3;
   const Geo g = cx.g;
   const int load = blockIdx.y;
   if (MODE == CG && !cx.st[load].active) return;
@@ -399,26 +522,48 @@ __global__ void __launch_bounds__(fft_threads(L)) gpass_y2d_kernel(Ctx cx) {
 #pragma unroll
   for (int q = 0; q < NC; ++q) tiles[q] = smem + q * 8 * L;
   double2* tw = smem + NC * 8 * L;
+  double* gs = reinterpret_cast<double*>(tw + L);  // [NCC][8 rows][L]
   __shared__ double red_sh[32];
-  const int T = blockDim.x, t = threadIdx.x;
-  for (int i = t; i < L; i += T) tw[i] = cx.tw.y[i];
+  const int t = threadIdx.x;
   const int kx0 = blockIdx.x * 8;
 #pragma unroll
   for (int q = 0; q < NC; ++q) {
     const double2* base = cx.spec + ((long long)load * g.c + q) * g.nspec + (long long)kx0 * L;
-    for (int e = t; e < 8 * L; e += T) {
-      const int row = e / L, j = e & (L - 1);
-      tiles[q][tidx(j, row)] = (kx0 + row < g.H1) ? base[e] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int i = 0; i < (8 * L + T - 1) / T; ++i) {
+      const int e = t + i * T;
+      if (e < 8 * L) {
+        const int row = e / L, j = e & (L - 1);
+        if (kx0 + row < g.H1)
+          cp_async16(&tiles[q][tidx(j, row)], base + e);
+        else
+          tiles[q][tidx(j, row)] = make_double2(0.0, 0.0);
+      }
     }
   }
+#pragma unroll
+  for (int q = 0; q < NCC; ++q) {
+#pragma unroll
+    for (int i = 0; i < (8 * L + T - 1) / T; ++i) {
+      const int e = t + i * T;
+      if (e < 8 * L && kx0 + e / L < g.H1) cp_async8(&gs[q * 8 * L + e], cx.gtab + q * g.nspec + (long long)kx0 * L + e);
+    }
+  }
+  cp_commit();
+  for (int i = t; i < L; i += T) tw[i] = cx.tw.y[i];
+  cp_wait<0>();
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < NC; ++q) fft_tile<L, false>(tiles[q], tw);
   double part = 0.0;
-  for (int e = t; e < 8 * L; e += T) {
-    const int row = e & 7, j = e >> 3;
-    const int kx = kx0 + row;
-    if (kx < g.H1) part += gmul_bin<NC>(tiles, tidx(j, row), cx.gtab, g.nspec, (long long)kx * L + j, parseval_w(kx, g.M));
+#pragma unroll
+  for (int i = 0; i < (8 * L + T - 1) / T; ++i) {
+    const int e = t + i * T;
+    if (e < 8 * L) {
+      const int row = e & 7, j = e >> 3;
+      const int kx = kx0 + row;
+      if (kx < g.H1) part += gmul_bin<NC>(tiles, tidx(j, row), gs, 8 * L, row * L + j, parseval_w(kx, g.M));
+    }
   }
   __syncthreads();
 #pragma unroll
@@ -426,9 +571,13 @@ __global__ void __launch_bounds__(fft_threads(L)) gpass_y2d_kernel(Ctx cx) {
 #pragma unroll
   for (int q = 0; q < NC; ++q) {
     double2* base = cx.spec + ((long long)load * g.c + q) * g.nspec + (long long)kx0 * L;
-    for (int e = t; e < 8 * L; e += T) {
-      const int row = e / L, j = e & (L - 1);
-      if (kx0 + row < g.H1) base[e] = tiles[q][tidx(j, row)];
+#pragma unroll
+    for (int i = 0; i < (8 * L + T - 1) / T; ++i) {
+      const int e = t + i * T;
+      if (e < 8 * L) {
+        const int row = e / L, j = e & (L - 1);
+        if (kx0 + row < g.H1) base[e] = tiles[q][tidx(j, row)];
+      }
     }
   }
   gamma_finish(cx, load, part, red_sh, MODE);
@@ -457,16 +606,6 @@ __device__ void dp_finish(const Ctx& cx, int load, int nblk, int my, double part
 // latency overlaps the stencil arithmetic; S_o is built from per-plane 2x2 box sums Q.
 constexpr int KT_TY = 8;
 constexpr int KT_RING = 7;
-
-__device__ __forceinline__ void cp_async8(void* smem_ptr, const void* gptr) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem_ptr);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gptr) : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
 
 template <int TX>
 __global__ void __launch_bounds__(TX * KT_TY) kp_thermal3d_kernel(Ctx cx, int mode, const double* __restrict__ src,
@@ -1174,7 +1313,7 @@ int launch_xfwd(const Ctx& cx, int mode, const double* src, cudaStream_t s) {
   return dispatch_pow2(g.M, [&](auto Lc) {
     constexpr int M = decltype(Lc)::value;
     const dim3 grid((unsigned)((long long)g.c * g.N3 * g.N2 / 8), g.nrhs);
-    const int sm = xsmem_bytes<M>();
+    const int sm = xsmem_bytes<M, false>();
     if (mode == CG) {
       auto k = xfwd_kernel<M, CG>;
       set_smem(k, sm);
@@ -1193,7 +1332,7 @@ int launch_xinv(const Ctx& cx, int mode, double* dst, cudaStream_t s) {
   return dispatch_pow2(g.M, [&](auto Lc) {
     constexpr int M = decltype(Lc)::value;
     const dim3 grid((unsigned)((long long)g.c * g.N3 * g.N2 / 8), g.nrhs);
-    const int sm = xsmem_bytes<M>();
+    const int sm = xsmem_bytes<M, true>();
     if (mode == CG) {
       auto k = xinv_kernel<M, CG>;
       set_smem(k, sm);
@@ -1242,7 +1381,7 @@ int launch_gpass(const Ctx& cx, int mode, cudaStream_t s) {
         return mode == CG ? go(gpass_z_kernel<L, 1, CG>, gsmem_bytes<L, 1>())
                           : go(gpass_z_kernel<L, 1, STANDALONE>, gsmem_bytes<L, 1>());
       }
-      if constexpr (gsmem_bytes<L, 3>() <= 227 * 1024) {
+      if constexpr (gsmem_bytes<L, 3>() <= 220 * 1024) {
         return mode == CG ? go(gpass_z_kernel<L, 3, CG>, gsmem_bytes<L, 3>())
                           : go(gpass_z_kernel<L, 3, STANDALONE>, gsmem_bytes<L, 3>());
       } else {
