@@ -16,6 +16,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -603,12 +604,15 @@ __device__ void dp_finish(const Ctx& cx, int load, int nblk, int my, double part
 //         sharing edge ij) - sum_o k_o S_o ],   S_o = sum of the 8 corner values of o.
 // CTA = TX x 8 nodes marching over ZC z-planes (2.5D blocking).  Node planes of d stream
 // through a 7-deep shared-memory ring with cp.async (LDGSTS) issued 3 planes ahead, so HBM
-// latency overlaps the stencil arithmetic; S_o is built from per-plane 2x2 box sums Q.
+// latency overlaps the arithmetic.  Each thread reads the 3x3 neighbourhood of plane k+1,
+// forms the four element box sums of that plane in registers and carries every
+// layer-k quantity (box sums, conductivity sums, k_o S_o partials, in-plane neighbours)
+// to the next plane in registers: one __syncthreads and 13 shared loads per node.
 constexpr int KT_TY = 8;
-constexpr int KT_RING = 7;
+constexpr int KT_RING = 8;  // power of two: slot = (plane - zs + 1) & 7
 
 template <int TX>
-__global__ void __launch_bounds__(TX * KT_TY) kp_thermal3d_kernel(Ctx cx, int mode, const double* __restrict__ src,
+__global__ void __launch_bounds__(TX * KT_TY, 3) kp_thermal3d_kernel(Ctx cx, int mode, const double* __restrict__ src,
                                                                   double* __restrict__ dst, int ZC) {
   constexpr int T = TX * KT_TY;
   constexpr int DW = TX + 2, DP = 10 * DW;       // d plane tile with halo
@@ -621,8 +625,7 @@ __global__ void __launch_bounds__(TX * KT_TY) kp_thermal3d_kernel(Ctx cx, int mo
   if (mode == CG && !cx.st[load].active) return;
   extern __shared__ double ksm[];
   double* D = ksm;                      // [KT_RING][DP]
-  double* Q = D + KT_RING * DP;         // [3][EP]
-  double* KA = Q + 3 * EP;              // [3][EP]
+  double* KA = D + KT_RING * DP;        // [4][EP]
   __shared__ double red_sh[32];
   const int t = threadIdx.x;
   const int tx = t % TX, ty = t / TX;
@@ -632,7 +635,7 @@ __global__ void __launch_bounds__(TX * KT_TY) kp_thermal3d_kernel(Ctx cx, int mo
   const double* dv = src + (long long)load * g.n;
   const double k0 = cx.mat[0][0], k1 = cx.mat[1][0];
 
-  int goffD[ND], goffE[NE], qbase[NE];
+  int goffD[ND], goffE[NE];
 #pragma unroll
   for (int m = 0; m < ND; ++m) {
     const int j = t + m * T;
@@ -644,11 +647,10 @@ __global__ void __launch_bounds__(TX * KT_TY) kp_thermal3d_kernel(Ctx cx, int mo
     const int j = t + m * T;
     const int ly = j / EW, lx = j - ly * EW;
     goffE[m] = ((y0 - 1 + ly + N2) & (N2 - 1)) * N1 + ((x0 - 1 + lx + N1) & (N1 - 1));
-    qbase[m] = ly * DW + lx;
   }
   auto issue_plane = [&](int p) {  // node plane p -> ring slot
     const int zw = (p + N3) & (N3 - 1);
-    double* Ds = D + ((p - zs + 1) % KT_RING) * DP;
+    double* Ds = D + ((p - zs + 1) & (KT_RING - 1)) * DP;
     const double* base = dv + (long long)zw * plane;
 #pragma unroll
     for (int m = 0; m < ND; ++m)
@@ -662,23 +664,32 @@ __global__ void __launch_bounds__(TX * KT_TY) kp_thermal3d_kernel(Ctx cx, int mo
     for (int m = 0; m < NE; ++m) phv[m] = (t + m * T < EP) ? __ldg(base + goffE[m]) : 0;
   };
   auto store_kappa = [&](int layer) {
-    double* Ks = KA + ((layer - zs + 1) % 3) * EP;
+    double* Ks = KA + ((layer - zs + 1) & 3) * EP;
 #pragma unroll
     for (int m = 0; m < NE; ++m)
       if (t + m * T < EP) Ks[t + m * T] = phv[m] ? k1 : k0;
   };
-  auto compute_Q = [&](int p) {
-    const double* Ds = D + ((p - zs + 1) % KT_RING) * DP;
-    double* Qs = Q + ((p - zs + 1) % 3) * EP;
+  // 3x3 neighbourhood of the thread's node column in plane p (local node (tx+1, ty+1))
+  double nb[3][3];
+  auto read3x3 = [&](int p) {
+    const double* Ds = D + ((p - zs + 1) & (KT_RING - 1)) * DP + ty * DW + tx;
 #pragma unroll
-    for (int m = 0; m < NE; ++m)
-      if (t + m * T < EP) {
-        const double* r0 = Ds + qbase[m];
-        Qs[t + m * T] = (r0[0] + r0[1]) + (r0[DW] + r0[DW + 1]);
-      }
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) nb[a][b] = Ds[a * DW + b];
+  };
+  // element box sums Q[oy][ox] of the plane in nb for the 4 elements around the node
+  auto box = [&](double Qo[2][2]) {
+    const double P00 = nb[0][0] + nb[0][1], P01 = nb[0][1] + nb[0][2];
+    const double P10 = nb[1][0] + nb[1][1], P11 = nb[1][1] + nb[1][2];
+    const double P20 = nb[2][0] + nb[2][1], P21 = nb[2][1] + nb[2][2];
+    Qo[0][0] = P00 + P10;
+    Qo[0][1] = P01 + P11;
+    Qo[1][0] = P10 + P20;
+    Qo[1][1] = P11 + P21;
   };
 
-  // prologue: planes zs-1 .. zs+3 in flight (one commit group each); layer zs-1 stored.
+  // prologue: planes zs-1 .. zs+3 in flight (one commit group each)
 #pragma unroll 1
   for (int p = zs - 1; p <= zs + 3; ++p) {
     if (p <= zs + ZC) issue_plane(p);
@@ -689,10 +700,37 @@ __global__ void __launch_bounds__(TX * KT_TY) kp_thermal3d_kernel(Ctx cx, int mo
   fetch_phase(zs);
   cp_wait<3>();  // planes zs-1, zs landed (this thread's copies)
   __syncthreads();
-  compute_Q(zs - 1);
-  compute_Q(zs);
+  double Qk[2][2], Qn[2][2];
+  read3x3(zs - 1);
+  box(Qk);
+  double dzm = nb[1][1];
+  read3x3(zs);
+  box(Qn);
+  double klo[2][2];
+  {
+    const double* Kl = KA + ty * EW + tx;  // layer zs-1 lives in slot 0
+    klo[0][0] = Kl[0];
+    klo[0][1] = Kl[1];
+    klo[1][0] = Kl[EW];
+    klo[1][1] = Kl[EW + 1];
+  }
+  double KSlo = 0.0;
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) KSlo = fma(klo[a][b], Qk[a][b] + Qn[a][b], KSlo);
+  double Klo = (klo[0][0] + klo[0][1]) + (klo[1][0] + klo[1][1]);
+  double Kxlo = klo[0][1] + klo[1][1];
+  double Kylo = klo[1][0] + klo[1][1];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) Qk[a][b] = Qn[a][b];
+  double di = nb[1][1], dxm = nb[1][0], dxp = nb[1][2], dym = nb[0][1], dyp = nb[2][1];
+
   double part = 0.0;
   const double hc = g.h / 12.0;
+  double* outp = dst + (long long)load * g.n + (long long)(y0 + ty) * N1 + (x0 + tx);
 #pragma unroll 1
   for (int k = zs; k < zs + ZC; ++k) {
     if (k + 4 <= zs + ZC) issue_plane(k + 4);
@@ -701,49 +739,245 @@ __global__ void __launch_bounds__(TX * KT_TY) kp_thermal3d_kernel(Ctx cx, int mo
     store_kappa(k);    // layer k (fetched one iteration ago)
     if (k + 1 < zs + ZC) fetch_phase(k + 1);
     __syncthreads();
-    compute_Q(k + 1);
-    __syncthreads();
-    {
-      const int sm1 = (k - zs) % KT_RING, s0 = (k - zs + 1) % KT_RING, sp1 = (k - zs + 2) % KT_RING;
-      const int qm1 = (k - zs) % 3, q0 = (k - zs + 1) % 3, qp1 = (k - zs + 2) % 3;
-      const double* Klo = KA + qm1 * EP + ty * EW + tx;   // layer k-1 (slot of layer index k-1)
-      const double* Khi = KA + q0 * EP + ty * EW + tx;    // layer k
-      const double a000 = Klo[0], a001 = Klo[1], a010 = Klo[EW], a011 = Klo[EW + 1];  // [oz][oy][ox]
-      const double a100 = Khi[0], a101 = Khi[1], a110 = Khi[EW], a111 = Khi[EW + 1];
-      const double* Qm = Q + qm1 * EP + ty * EW + tx;
-      const double* Q0 = Q + q0 * EP + ty * EW + tx;
-      const double* Qp = Q + qp1 * EP + ty * EW + tx;
-      const double S000 = Qm[0] + Q0[0], S001 = Qm[1] + Q0[1], S010 = Qm[EW] + Q0[EW], S011 = Qm[EW + 1] + Q0[EW + 1];
-      const double S100 = Q0[0] + Qp[0], S101 = Q0[1] + Qp[1], S110 = Q0[EW] + Qp[EW], S111 = Q0[EW + 1] + Qp[EW + 1];
-      const double Kxp = (a001 + a011) + (a101 + a111);
-      const double Kyp = (a010 + a011) + (a110 + a111);
-      const double Kzp = (a100 + a101) + (a110 + a111);
-      const double Ksum = (a000 + a001) + (a010 + a011) + (a100 + a101) + (a110 + a111);
-      double KS = a000 * S000;
-      KS = fma(a001, S001, KS);
-      KS = fma(a010, S010, KS);
-      KS = fma(a011, S011, KS);
-      KS = fma(a100, S100, KS);
-      KS = fma(a101, S101, KS);
-      KS = fma(a110, S110, KS);
-      KS = fma(a111, S111, KS);
-      const int cidx = (ty + 1) * DW + (tx + 1);
-      const double* Dc = D + s0 * DP + cidx;
-      const double di = Dc[0];
-      const double dzm = D[sm1 * DP + cidx];
-      const double dzp = D[sp1 * DP + cidx];
-      double EE = Kxp * Dc[1];
-      EE = fma(Ksum - Kxp, Dc[-1], EE);
-      EE = fma(Kyp, Dc[DW], EE);
-      EE = fma(Ksum - Kyp, Dc[-DW], EE);
-      EE = fma(Kzp, dzp, EE);
-      EE = fma(Ksum - Kzp, dzm, EE);
-      const double pv = hc * (fma(5.0 * di, Ksum, EE) - KS);
-      dst[(long long)load * g.n + (long long)k * plane + (long long)(y0 + ty) * N1 + (x0 + tx)] = pv;
-      part = fma(di, pv, part);
-    }
+    read3x3(k + 1);
+    box(Qn);
+    const double* Kh = KA + ((k - zs + 1) & 3) * EP + ty * EW + tx;
+    const double a00 = Kh[0], a01 = Kh[1], a10 = Kh[EW], a11 = Kh[EW + 1];  // layer k, [oy][ox]
+    double KShi = a00 * (Qk[0][0] + Qn[0][0]);
+    KShi = fma(a01, Qk[0][1] + Qn[0][1], KShi);
+    KShi = fma(a10, Qk[1][0] + Qn[1][0], KShi);
+    KShi = fma(a11, Qk[1][1] + Qn[1][1], KShi);
+    const double Khi = (a00 + a01) + (a10 + a11);
+    const double Kxhi = a01 + a11, Kyhi = a10 + a11;
+    const double Ksum = Klo + Khi;
+    const double Kxp = Kxlo + Kxhi, Kyp = Kylo + Kyhi;
+    const double dzp = nb[1][1];
+    double EE = Kxp * dxp;
+    EE = fma(Ksum - Kxp, dxm, EE);
+    EE = fma(Kyp, dyp, EE);
+    EE = fma(Ksum - Kyp, dym, EE);
+    EE = fma(Khi, dzp, EE);
+    EE = fma(Klo, dzm, EE);
+    const double pv = hc * (fma(5.0 * di, Ksum, EE) - (KSlo + KShi));
+    outp[(long long)k * plane] = pv;
+    part = fma(di, pv, part);
+    // carry layer k / plane k+1 into the next step
+    KSlo = KShi;
+    Klo = Khi;
+    Kxlo = Kxhi;
+    Kylo = Kyhi;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) Qk[a][b] = Qn[a][b];
+    dzm = di;
+    di = nb[1][1];
+    dxm = nb[1][0];
+    dxp = nb[1][2];
+    dym = nb[0][1];
+    dyp = nb[2][1];
   }
   cp_wait<0>();
+  const int nblk = gridDim.x * gridDim.y * nzc;
+  const int my = (zcI * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  dp_finish(cx, load, nblk, my, part, red_sh, mode);
+}
+
+// Same stencil, TMA-style staging for N1 >= 32 (the production path): one warp issues
+// cp.async.bulk row copies (global -> shared, completion counted on an mbarrier per ring slot),
+// so the 256 worker threads spend no instructions on address generation for the halo tile.
+// A slot carries node plane p of d (10 rows x 36 doubles: x0-2 .. x0+33) and the phase bytes of
+// element layer p-1 (9 rows x 64 B: x0-16 .. x0+47).  Conductivities are selected per node
+// from the phase bytes.  Ring of 8 slots, 4 planes of lookahead.
+constexpr int KB_DW = 36;            // doubles per staged d row
+constexpr int KB_PW = 64;            // bytes per staged phase row
+constexpr int KB_SLOT = 10 * KB_DW * 8 + 9 * KB_PW;  // bytes per ring slot (3456)
+constexpr int KB_RING = 8;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+// copy the periodic window [x, x+len) of a row (element size es bytes) in <= 3 contiguous pieces
+__device__ __forceinline__ void bulk_row(unsigned dst, const char* row, int x, int len, int N, int es, unsigned bar) {
+  int xs = ((x % N) + N) % N;
+  while (len > 0) {
+    const int l = min(len, N - xs);
+    bulk_g2s(dst, row + (long long)xs * es, (unsigned)(l * es), bar);
+    dst += l * es;
+    len -= l;
+    xs = 0;
+  }
+}
+
+__global__ void __launch_bounds__(256, 3) kp_thermal3d_tma_kernel(Ctx cx, int mode, const double* __restrict__ src,
+                                                                  double* __restrict__ dst, int ZC) {
+  constexpr int TX = 32;
+  const Geo g = cx.g;
+  const int nzc = g.N3 / ZC;
+  const int load = blockIdx.z / nzc;
+  const int zcI = blockIdx.z - load * nzc;
+  if (mode == CG && !cx.st[load].active) return;
+  extern __shared__ __align__(128) unsigned char kbs[];
+  __shared__ __align__(8) unsigned long long bars[KB_RING];
+  __shared__ double red_sh[32];
+  const int t = threadIdx.x;
+  const int tx = t & 31, ty = t >> 5;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * KT_TY, zs = zcI * ZC;
+  const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
+  const long long plane = (long long)N1 * N2;
+  const double* dv = src + (long long)load * g.n;
+  const double k0 = cx.mat[0][0], k1 = cx.mat[1][0];
+  const unsigned sbase = smem_u32(kbs);
+  const unsigned bar0 = smem_u32(bars);
+  if (t == 0) {
+    for (int i = 0; i < KB_RING; ++i) mbar_init(bar0 + 8 * i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  // producer: warp 0, lane r < 10 copies d row r, lane 10 + r (r < 9) copies phase row r
+  auto issue = [&](int p) {  // node plane p (and phase layer p-1) -> slot (p - zs + 1) & 7
+    const int q = p - zs + 1;
+    const int slot = q & (KB_RING - 1);
+    const unsigned bar = bar0 + 8 * slot;
+    const unsigned sd = sbase + slot * KB_SLOT;
+    if (tx == 0) mbar_expect_tx(bar, KB_SLOT);
+    __syncwarp();
+    if (tx < 10) {
+      const int zw = (p + N3) & (N3 - 1);
+      const int gy = (y0 - 1 + tx + N2) & (N2 - 1);
+      bulk_row(sd + tx * KB_DW * 8, reinterpret_cast<const char*>(dv + zw * plane + (long long)gy * N1), x0 - 2, KB_DW,
+               N1, 8, bar);
+    } else if (tx < 19) {
+      const int r = tx - 10;
+      const int zw = (p - 1 + N3) & (N3 - 1);
+      const int gy = (y0 - 1 + r + N2) & (N2 - 1);
+      bulk_row(sd + 10 * KB_DW * 8 + r * KB_PW,
+               reinterpret_cast<const char*>(cx.phase + zw * plane + (long long)gy * N1), x0 - 16, KB_PW, N1, 1, bar);
+    }
+  };
+  auto dtile = [&](int p) -> const double* {
+    return reinterpret_cast<const double*>(kbs + ((p - zs + 1) & (KB_RING - 1)) * KB_SLOT);
+  };
+  auto ptile = [&](int p) -> const unsigned char* {  // phase layer p-1 travels with plane p
+    return kbs + ((p - zs + 1) & (KB_RING - 1)) * KB_SLOT + 10 * KB_DW * 8;
+  };
+  auto wait_plane = [&](int p) {
+    const int q = p - zs + 1;
+    mbar_wait(bar0 + 8 * (q & (KB_RING - 1)), (unsigned)((q >> 3) & 1));
+  };
+  if (ty == 0) {
+    for (int p = zs - 1; p <= zs + 4; ++p)
+      if (p <= zs + ZC) issue(p);
+  }
+  double nb[3][3];
+  auto read3x3 = [&](int p) {
+    const double* Ds = dtile(p) + ty * KB_DW + tx + 1;
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) nb[a][b] = Ds[a * KB_DW + b];
+  };
+  auto box = [&](double Qo[2][2]) {
+    const double P00 = nb[0][0] + nb[0][1], P01 = nb[0][1] + nb[0][2];
+    const double P10 = nb[1][0] + nb[1][1], P11 = nb[1][1] + nb[1][2];
+    const double P20 = nb[2][0] + nb[2][1], P21 = nb[2][1] + nb[2][2];
+    Qo[0][0] = P00 + P10;
+    Qo[0][1] = P01 + P11;
+    Qo[1][0] = P10 + P20;
+    Qo[1][1] = P11 + P21;
+  };
+  auto kap4 = [&](int p, double a[2][2]) {  // conductivities of the 4 elements around the node, layer p-1
+    const unsigned char* P = ptile(p) + ty * KB_PW + tx + 15;
+    a[0][0] = P[0] ? k1 : k0;
+    a[0][1] = P[1] ? k1 : k0;
+    a[1][0] = P[KB_PW] ? k1 : k0;
+    a[1][1] = P[KB_PW + 1] ? k1 : k0;
+  };
+  wait_plane(zs - 1);
+  wait_plane(zs);
+  double Qk[2][2], Qn[2][2], klo[2][2];
+  read3x3(zs - 1);
+  box(Qk);
+  double dzm = nb[1][1];
+  read3x3(zs);
+  box(Qn);
+  kap4(zs, klo);  // layer zs-1
+  double KSlo = 0.0;
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) KSlo = fma(klo[a][b], Qk[a][b] + Qn[a][b], KSlo);
+  double Klo = (klo[0][0] + klo[0][1]) + (klo[1][0] + klo[1][1]);
+  double Kxlo = klo[0][1] + klo[1][1];
+  double Kylo = klo[1][0] + klo[1][1];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) Qk[a][b] = Qn[a][b];
+  double di = nb[1][1], dxm = nb[1][0], dxp = nb[1][2], dym = nb[0][1], dyp = nb[2][1];
+  double part = 0.0;
+  const double hc = g.h / 12.0;
+  double* outp = dst + (long long)load * g.n + (long long)(y0 + ty) * N1 + (x0 + tx);
+#pragma unroll 1
+  for (int k = zs; k < zs + ZC; ++k) {
+    wait_plane(k + 1);
+    read3x3(k + 1);
+    box(Qn);
+    double a[2][2];
+    kap4(k + 1, a);  // layer k
+    double KShi = a[0][0] * (Qk[0][0] + Qn[0][0]);
+    KShi = fma(a[0][1], Qk[0][1] + Qn[0][1], KShi);
+    KShi = fma(a[1][0], Qk[1][0] + Qn[1][0], KShi);
+    KShi = fma(a[1][1], Qk[1][1] + Qn[1][1], KShi);
+    const double Khi = (a[0][0] + a[0][1]) + (a[1][0] + a[1][1]);
+    const double Kxhi = a[0][1] + a[1][1], Kyhi = a[1][0] + a[1][1];
+    const double Ksum = Klo + Khi;
+    const double Kxp = Kxlo + Kxhi, Kyp = Kylo + Kyhi;
+    const double dzp = nb[1][1];
+    double EE = Kxp * dxp;
+    EE = fma(Ksum - Kxp, dxm, EE);
+    EE = fma(Kyp, dyp, EE);
+    EE = fma(Ksum - Kyp, dym, EE);
+    EE = fma(Khi, dzp, EE);
+    EE = fma(Klo, dzm, EE);
+    const double pv = hc * (fma(5.0 * di, Ksum, EE) - (KSlo + KShi));
+    outp[(long long)k * plane] = pv;
+    part = fma(di, pv, part);
+    KSlo = KShi;
+    Klo = Khi;
+    Kxlo = Kxhi;
+    Kylo = Kyhi;
+#pragma unroll
+    for (int aa = 0; aa < 2; ++aa)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) Qk[aa][b] = Qn[aa][b];
+    dzm = di;
+    di = nb[1][1];
+    dxm = nb[1][0];
+    dxp = nb[1][2];
+    dym = nb[0][1];
+    dyp = nb[2][1];
+    __syncthreads();  // every thread is done with plane k-3's slot before it is refilled
+    if (ty == 0 && k + 5 <= zs + ZC) issue(k + 5);
+  }
   const int nblk = gridDim.x * gridDim.y * nzc;
   const int my = (zcI * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
   dp_finish(cx, load, nblk, my, part, red_sh, mode);
@@ -1281,6 +1515,25 @@ __global__ void eq55_kernel(Ctx cx, const double* gtab, double* partials) {
   }
 }
 
+// Device-side loop control of the CUDA-graph WHILE node: keep iterating while any load case
+// is active (and below a safety cap on body executions).
+__global__ void loop_ctl_kernel(cudaGraphConditionalHandle h, const LoadState* st, int nrhs, int* counter, int cap) {
+  int any = 0;
+  for (int l = 0; l < nrhs; ++l) any |= st[l].active;
+  const int c = ++(*counter);
+  if (!any || c >= cap) {
+    *counter = 0;
+    cudaGraphSetConditional(h, 0u);
+  } else {
+    cudaGraphSetConditional(h, 1u);
+  }
+}
+
+int launch_loop_ctl(cudaGraphConditionalHandle h, const LoadState* st, int nrhs, int* counter, int cap, cudaStream_t s) {
+  loop_ctl_kernel<<<1, 1, 0, s>>>(h, st, nrhs, counter, cap);
+  return 1;
+}
+
 __global__ void zero_kernel(double* x, long long n) {
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     x[i] = 0.0;
@@ -1410,13 +1663,21 @@ int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaS
   if (g.dim == 3 && g.c == 1) {
     const int TX = g.N1 < 32 ? g.N1 : 32;
     const int ZC = g.N3 < 32 ? g.N3 : 32;
-    const int sm = (KT_RING * 10 * (TX + 2) + 6 * 9 * (TX + 1)) * (int)sizeof(double);
+    const int sm = (KT_RING * 10 * (TX + 2) + 4 * 9 * (TX + 1)) * (int)sizeof(double);
     const dim3 grid(g.N1 / TX, g.N2 / KT_TY, (g.N3 / ZC) * g.nrhs);
     auto go = [&](auto kern, int tpb) {
       set_smem(kern, sm);
       kern<<<grid, tpb, sm, s>>>(cx, mode, src, dst, ZC);
     };
-    if (TX == 32) go(kp_thermal3d_kernel<32>, 256);
+    static const bool use_bulk = [] {
+      const char* e = getenv("UNO_KP_BULK");
+      return e && e[0] == '1';
+    }();
+    if (TX == 32 && use_bulk) {  // experimental cp.async.bulk staging (slower so far)
+      const int smb = KB_RING * KB_SLOT;
+      set_smem(kp_thermal3d_tma_kernel, smb);
+      kp_thermal3d_tma_kernel<<<grid, 256, smb, s>>>(cx, mode, src, dst, ZC);
+    } else if (TX == 32) go(kp_thermal3d_kernel<32>, 256);
     else if (TX == 16) go(kp_thermal3d_kernel<16>, 128);
     else go(kp_thermal3d_kernel<8>, 64);
     return 1;

@@ -50,6 +50,7 @@ int launch_build_symbol(const Ctx& cx, double* gtab, double ref0, double ref1, u
                         cudaStream_t s);
 int launch_eq55(const Ctx& cx, const double* gtab, double* minmax_partials, int* nblocks_out, cudaStream_t s);
 int launch_zero(double* x, long long n, cudaStream_t s);
+int launch_loop_ctl(cudaGraphConditionalHandle h, const LoadState* st, int nrhs, int* counter, int cap, cudaStream_t s);
 
 int blocks_needed_max(const Geo& g);  // max CTAs per load of any reducing kernel
 

@@ -60,6 +60,8 @@ struct uno_cg_handle {
   cudaGraphExec_t gexec;
   int gchunk;
   bool gtimed;
+  int gcap;               // safety cap of the device-side WHILE loop (body executions)
+  int* loopctr;           // device counter used by the loop-control kernel
   // timing
   bool timing;
   std::vector<cudaEvent_t> tev;  // per chunk: [iter][class][2]
@@ -151,7 +153,7 @@ static void free_all(uno_cg_handle* h) {
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   for (auto e : h->tev) cudaEventDestroy(e);
   void* bufs[] = {h->r, h->d, h->p, h->u, h->spec, h->gtab, h->kel, h->twx, h->twxp, h->twy, h->twz,
-                  h->st, h->partials, h->counters, h->results, h->scratch, h->hist};
+                  h->st, h->partials, h->counters, h->results, h->scratch, h->hist, h->loopctr};
   for (void* b : bufs)
     if (b) cudaFreeAsync(b, h->stream);
   if (h->h_st) cudaFreeHost(h->h_st);
@@ -291,6 +293,7 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
       (e = al((void**)&h->partials, (size_t)RED_NSLOT * kMaxRhs * maxb * 8)) ||
       (e = al((void**)&h->counters, RED_NSLOT * kMaxRhs * sizeof(unsigned))) ||
       (e = al((void**)&h->results, RED_NSLOT * kMaxRhs * 8)) || (e = al((void**)&h->scratch, h->scratch_len * 8)) ||
+      (e = al((void**)&h->loopctr, 64)) ||
       (e = cudaMallocHost((void**)&h->h_st, kMaxRhs * sizeof(LoadState))) ||
       (e = cudaMallocHost((void**)&h->h_small, 4096 * 8)) || (e = cudaEventCreate(&h->e0)) ||
       (e = cudaEventCreate(&h->e1))) {
@@ -299,6 +302,7 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
   }
   cudaMemsetAsync(h->counters, 0, RED_NSLOT * kMaxRhs * sizeof(unsigned), s);
   cudaMemsetAsync(h->st, 0, kMaxRhs * sizeof(LoadState), s);
+  cudaMemsetAsync(h->loopctr, 0, 64, s);
   // twiddles (long double on the host)
   std::vector<double2> t;
   twiddles(g.M, g.M, t);
@@ -425,8 +429,12 @@ static int enqueue_iteration(uno_cg_handle* h, cudaStream_t s, cudaEvent_t* ev /
   return n;
 }
 
-static uno_status build_graph(uno_cg_handle* h, int chunk, bool timed) {
-  if (h->gexec && h->gchunk == chunk && h->gtimed == timed) return UNO_OK;
+// The solve loop as one CUDA graph.  Untimed: a WHILE conditional node whose body holds
+// `chunk` PCG iterations plus the loop-control kernel, so the whole solve runs device-side
+// with a single host launch.  Timed: `chunk` iterations bracketed by event-record nodes,
+// relaunched from the host (events inside a device loop could not be read per iteration).
+static uno_status build_graph(uno_cg_handle* h, int chunk, bool timed, int cap) {
+  if (h->gexec && h->gchunk == chunk && h->gtimed == timed && h->gcap == cap) return UNO_OK;
   if (h->gexec) {
     cudaGraphExecDestroy(h->gexec);
     h->gexec = nullptr;
@@ -442,20 +450,46 @@ static uno_status build_graph(uno_cg_handle* h, int chunk, bool timed) {
   cudaStream_t cs;
   CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
   cudaGraph_t graph;
-  CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
-  for (int i = 0; i < chunk; ++i) {
-    if (enqueue_iteration(h, cs, timed ? &h->tev[(size_t)i * 6 * 2] : nullptr) < 0) {
-      cudaStreamEndCapture(cs, &graph);
-      cudaStreamDestroy(cs);
-      return fail(UNO_ERR_SHAPE, "no kernel instance for this grid size");
+  if (timed) {
+    CK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < chunk; ++i) {
+      if (enqueue_iteration(h, cs, &h->tev[(size_t)i * 6 * 2]) < 0) {
+        cudaStreamEndCapture(cs, &graph);
+        cudaStreamDestroy(cs);
+        return fail(UNO_ERR_SHAPE, "no kernel instance for this grid size");
+      }
     }
+    CK(cudaStreamEndCapture(cs, &graph));
+  } else {
+    CK(cudaGraphCreate(&graph, 0));
+    cudaGraphConditionalHandle ch;
+    CK(cudaGraphConditionalHandleCreate(&ch, graph, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = ch;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, graph, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    CK(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < chunk; ++i) {
+      if (enqueue_iteration(h, cs, nullptr) < 0) {
+        cudaStreamEndCapture(cs, &body);
+        cudaStreamDestroy(cs);
+        cudaGraphDestroy(graph);
+        return fail(UNO_ERR_SHAPE, "no kernel instance for this grid size");
+      }
+    }
+    launch_loop_ctl(ch, h->st, h->g.nrhs, h->loopctr, cap, cs);
+    CK(cudaStreamEndCapture(cs, &body));
   }
-  CK(cudaStreamEndCapture(cs, &graph));
   CK(cudaGraphInstantiate(&h->gexec, graph, 0));
   cudaGraphDestroy(graph);
   cudaStreamDestroy(cs);
   h->gchunk = chunk;
   h->gtimed = timed;
+  h->gcap = cap;
   return UNO_OK;
 }
 
@@ -509,28 +543,40 @@ extern "C" uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, doub
   }
   CK(cudaMemcpyAsync(h->st, h->h_st, g.nrhs * sizeof(LoadState), cudaMemcpyHostToDevice, s));
   const long long work = (long long)g.nrhs * g.c * g.n;
-  const int chunk = work >= (1LL << 22) ? 4 : (work >= (1LL << 18) ? 8 : 16);
-  uno_status bs = build_graph(h, chunk, h->timing);
-  if (bs != UNO_OK) return bs;
   const int per_iter = (g.dim == 3 ? 6 : 4);
-  int done = 0;
-  bool any = true;
-  while (any) {
-    if (done > cap + 1) break;  // safety: the device stops itself at cap
+  if (!h->timing) {
+    // whole solve device-side: WHILE node over bodies of `chunk` iterations
+    const int chunk = work >= (1LL << 22) ? 2 : 4;
+    const int cap_body = (cap + 1 + chunk - 1) / chunk + 1;
+    uno_status bs = build_graph(h, chunk, false, cap_body);
+    if (bs != UNO_OK) return bs;
     CK(cudaGraphLaunch(h->gexec, s));
-    launches += (long long)chunk * per_iter;
-    int before = 0;
-    for (int l = 0; l < g.nrhs; ++l) before = std::max(before, h->h_st[l].iters);
     CK(cudaMemcpyAsync(h->h_st, h->st, g.nrhs * sizeof(LoadState), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    done += chunk;
-    any = false;
-    int after = 0;
-    for (int l = 0; l < g.nrhs; ++l) {
-      any = any || h->h_st[l].active;
-      after = std::max(after, h->h_st[l].iters);
-    }
-    if (h->timing) {  // accumulate only iterations that did work
+    int it = 0;
+    for (int l = 0; l < g.nrhs; ++l) it = std::max(it, h->h_st[l].iters);
+    launches += (long long)(it / chunk + 1) * (chunk * per_iter + 1);  // bodies executed (>= iters/chunk)
+  } else {
+    const int chunk = work >= (1LL << 22) ? 4 : (work >= (1LL << 18) ? 8 : 16);
+    uno_status bs = build_graph(h, chunk, true, 0);
+    if (bs != UNO_OK) return bs;
+    int done = 0;
+    bool any = true;
+    while (any) {
+      if (done > cap + 1) break;  // safety: the device stops itself at cap
+      CK(cudaGraphLaunch(h->gexec, s));
+      launches += (long long)chunk * per_iter;
+      int before = 0;
+      for (int l = 0; l < g.nrhs; ++l) before = std::max(before, h->h_st[l].iters);
+      CK(cudaMemcpyAsync(h->h_st, h->st, g.nrhs * sizeof(LoadState), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      done += chunk;
+      any = false;
+      int after = 0;
+      for (int l = 0; l < g.nrhs; ++l) {
+        any = any || h->h_st[l].active;
+        after = std::max(after, h->h_st[l].iters);
+      }
       const int worked = std::min(chunk, std::max(0, after - before));
       for (int i = 0; i < worked; ++i)
         for (int slot = 0; slot < 6; ++slot) {
