@@ -156,6 +156,7 @@ def run_ours(args):
         dist.init_process_group("nccl", init_method="env://")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    from paper_2508_02681_b200 import dist as D
     from paper_2508_02681_b200.api import UnoCG
 
     n = args.grid
@@ -218,16 +219,8 @@ def run_ours(args):
                 a[1] += c
         ev1.record(stream)
         barrier()
-    ms = ev0.elapsed_time(ev1)
-    if ws > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        c = torch.tensor([float(tot_dofit)], device=dev, dtype=torch.float64)
-        dist.all_reduce(c, op=dist.ReduceOp.SUM)
-        all_dofit = float(c.item())
-    else:
-        all_dofit = float(tot_dofit)
+    ms = D.reduce_max(ev0.elapsed_time(ev1))      # max over ranks of the device time
+    all_dofit = D.reduce_sum(float(tot_dofit))    # units processed by all ranks
     value = all_dofit / (ms / 1e3)
 
     # ---- roofline of the dominant kernel (live per-launch CUDA-event durations) ----
@@ -287,13 +280,8 @@ def run_ours(args):
             dsum += e2e_step()
         e1.record(stream)
         barrier()
-        ems = e0.elapsed_time(e1)
-        if ws > 1:
-            t = torch.tensor([ems, float(dsum)], device=dev, dtype=torch.float64)
-            t2 = t.clone()
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dist.all_reduce(t2, op=dist.ReduceOp.SUM)
-            ems, dsum = float(t[0]), float(t2[1])
+        ems = D.reduce_max(e0.elapsed_time(e1))
+        dsum = D.reduce_sum(float(dsum))
         e2e = {"value": dsum / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
     cpu = None
