@@ -18,6 +18,7 @@ struct Geo {
   long long nspec;      // H1*N2*N3 complex bins per component
   double h;             // voxel edge
   int C;                // unique symbol entries per bin: c(c+1)/2 (Eq 51)
+  int NA, NB;           // 3-pass (four-step) schedule: N2 = NA*NB, y = y_a + NA*y_b; NB = 0 -> 5-pass
 };
 
 // Per-load CG state (device resident; Alg 2 scalars).

@@ -165,4 +165,82 @@ __device__ __forceinline__ void fft_tile(double2* s, const double2* tw) {
   FftStages<L, 1, INV>::run(s, tw);
 }
 
+// ---- NT tiles at once (tile q at s + q*8L): more butterflies per stage for bigger CTAs ----
+template <int L, int NT, int R, int NS, bool INV>
+__device__ __forceinline__ void fft_stage_nt(double2* s, const double2* __restrict__ tw) {
+  constexpr int NJ = L / R;
+  constexpr int ITEMS = NJ * kTile * NT;
+  const int t = threadIdx.x;
+  const bool act = t < ITEMS;
+  const int q = t / (NJ * kTile), rem = t - q * (NJ * kTile);
+  const int c = rem & 7, j = rem >> 3;
+  const int k = j % NS;
+  double2* sq = s + q * 8 * L;
+  double2 v[R];
+  if (act) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = sq[tidx(j + r * NJ, c)];
+    if (NS > 1) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        double2 w = tw[r * k * (L / (NS * R))];
+        if (INV) w.y = -w.y;
+        v[r] = cmul(v[r], w);
+      }
+    }
+    if (INV) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r].y = -v[r].y;
+    }
+    Dft<R>::run(v);
+    if (INV) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r].y = -v[r].y;
+    }
+  }
+  __syncthreads();
+  if (act) {
+    const int base = (j / NS) * NS * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) sq[tidx(base + r * NS, c)] = v[r];
+  }
+  __syncthreads();
+}
+
+template <int L, int NT, int NS, bool INV>
+struct FftStagesNT {
+  static __device__ __forceinline__ void run(double2* s, const double2* tw) {
+    constexpr int R = pick_radix(L / NS);
+    fft_stage_nt<L, NT, R, NS, INV>(s, tw);
+    FftStagesNT<L, NT, NS * R, INV>::run(s, tw);
+  }
+};
+template <int L, int NT, bool INV>
+struct FftStagesNT<L, NT, L, INV> {
+  static __device__ __forceinline__ void run(double2*, const double2*) {}
+};
+
+template <int L, int NT, bool INV>
+__device__ __forceinline__ void fft_tiles(double2* s, const double2* tw) {
+  FftStagesNT<L, NT, 1, INV>::run(s, tw);
+}
+// threads for one butterfly per thread in every stage of NT tiles
+__host__ __device__ constexpr int fft_threads_nt(int L, int NT) {
+  return (NT * 8 * L / min_radix(L)) < 64 ? 64 : NT * 8 * L / min_radix(L);
+}
+
+// In-register forward/inverse DFT of length R (R = 2, 4, 8, 16).
+template <int R, bool INV>
+__device__ __forceinline__ void dft_reg(double2* v) {
+  if (INV) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r].y = -v[r].y;
+  }
+  Dft<R>::run(v);
+  if (INV) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r].y = -v[r].y;
+  }
+}
+
 }  // namespace uno

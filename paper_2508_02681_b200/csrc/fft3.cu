@@ -1,0 +1,494 @@
+// fft3.cu — the 3-pass ("four-step") schedule of the UNO apply for 3D grids.
+//
+// The y transform (length N2 = NA*NB, y = y_a + NA*y_b, k_y = k_b + NB*k_a) is split
+// between the x pass and the z pass (decimation in time):
+//   A[y_a, k_b]   = w_N2^{y_a k_b} * sum_{y_b} x[y_a + NA y_b] w_NB^{y_b k_b}        (F1)
+//   X[k_b + NB k_a] = sum_{y_a} A[y_a, k_b] w_NA^{y_a k_a}                           (F2)
+// so one pass over the spectrum disappears on each side:
+//   F1 f1_kernel:  r -= alpha p ; ||r||_inf ; x R2C of NB rows ; NB-point DFT across them
+//   F2 f2_kernel:  NA-point DFT along y_a ; z FFT ; s_hat = G_hat r_hat ; gamma_1 ; inverses
+//   F3 f3_kernel:  inverse of F1 ; x C2R ; d = s + beta d ; u += alpha d_old
+// (Alg 2 l.3-12; the operator is exactly T^H Q T of Eq 48 — only the order of the
+// butterflies differs from the 5-pass schedule in kernels.cu.)
+// Spectrum layout for this schedule: [nrhs][c][kx][k_b][kz][k_a]  (F2 reads one contiguous
+// NA x N3 block per (kx, k_b)); the tabulated symbol uses the same layout.
+#include <cuda_runtime.h>
+
+#include <type_traits>
+
+#include "common.cuh"
+#include "dev_common.cuh"
+#include "fft.cuh"
+#include "kernels.cuh"
+
+namespace uno {
+
+template <int M, int NB>
+__host__ __device__ constexpr int f1_stage() {
+  return (NB * M > (M + 1) * (NB + 1)) ? NB * M : (M + 1) * (NB + 1);
+}
+template <int M, int NB>
+__host__ __device__ constexpr int f3_stage() {
+  return (2 * NB * M > (M + 1) * (NB + 1)) ? 2 * NB * M : (M + 1) * (NB + 1);
+}
+template <int M, int NB, bool INV>
+__host__ __device__ constexpr int f13_smem_elems() {
+  return NB * M + (INV ? f3_stage<M, NB>() : f1_stage<M, NB>()) + M + (M + 1);
+}
+
+// ------------------------------------------------------------------------------------- F1
+template <int M, int NB, int MODE>
+__global__ void __launch_bounds__(fft_threads_nt(M, NB / 8)) f1_kernel(Ctx cx, const double* __restrict__ src) {
+  constexpr int NT = NB / 8;
+  constexpr int T = fft_threads_nt(M, NT);
+  constexpr int H1 = M + 1;
+  constexpr int XS = NB + 1;  // padded row stride of the X[kx][y_b] buffer (bank-conflict free)
+  const Geo g = cx.g;
+  const int load = blockIdx.y;
+  LoadState* st = cx.st + load;
+  if (MODE == CG && !st->active) return;
+  extern __shared__ double2 smem[];
+  double2* tiles = smem;                        // NT tiles of 8 rows x M
+  double2* stage = tiles + NB * M;              // p rows, later X[kx][y_b]
+  double2* tw = stage + f1_stage<M, NB>();      // M
+  double2* twp = tw + M;                        // M + 1
+  double2* twy = twp + H1;                      // N2 (runtime)
+  __shared__ double red_sh[32];
+  const int t = threadIdx.x;
+  const int NA = g.NA, N2 = g.N2, N1 = g.N1;
+  const int ya = blockIdx.x % NA;
+  const int zc = blockIdx.x / NA;
+  const int z = zc % g.N3, comp = zc / g.N3;
+  const long long vbase = (long long)load * g.c * g.n + (long long)comp * g.n + (long long)z * N2 * N1;
+  bool upd = false;
+  double alpha = 0.0;
+  if (MODE == CG) {
+    upd = st->iters > 0;
+    alpha = st->alpha;
+  }
+#pragma unroll
+  for (int i = 0; i < (NB * M + T - 1) / T; ++i) {
+    const int e = t + i * T;
+    if (e < NB * M) {
+      const int r = e / M, j = e & (M - 1);
+      const long long off = vbase + (long long)(ya + NA * r) * N1 + 2 * j;
+      cp_async16(&tiles[(r >> 3) * 8 * M + tidx(j, r & 7)], src + off);
+      if (MODE == CG && upd) cp_async16(&stage[e], cx.p + off);
+    }
+  }
+  cp_commit();
+  for (int i = t; i < M; i += T) tw[i] = cx.tw.x[i];
+  for (int i = t; i <= M; i += T) twp[i] = cx.tw.xpost[i];
+  for (int i = t; i < N2; i += T) twy[i] = cx.tw.y[i];
+  cp_wait<0>();
+  __syncthreads();
+  double mx = 0.0;
+#pragma unroll
+  for (int i = 0; i < (NB * M + T - 1) / T; ++i) {
+    const int e = t + i * T;
+    if (e < NB * M) {
+      const int r = e / M, j = e & (M - 1);
+      const int ti = (r >> 3) * 8 * M + tidx(j, r & 7);
+      double2 v = tiles[ti];
+      if (MODE == CG && upd) {  // r <- r - alpha p   (Alg 2 l.11)
+        const double2 pv = stage[e];
+        v.x = fma(-alpha, pv.x, v.x);
+        v.y = fma(-alpha, pv.y, v.y);
+        *reinterpret_cast<double2*>(cx.r + vbase + (long long)(ya + NA * r) * N1 + 2 * j) = v;
+        tiles[ti] = v;
+      }
+      mx = fmax(mx, fmax(fabs(v.x), fabs(v.y)));
+    }
+  }
+  __syncthreads();
+  fft_tiles<M, NT, false>(tiles, tw);
+  // R2C post-processing of every row into X[kx][y_b]
+#pragma unroll
+  for (int i = 0; i < ((M / 2 + 1) * NB + T - 1) / T; ++i) {
+    const int it = t + i * T;
+    if (it < (M / 2 + 1) * NB) {
+      const int r = it % NB, k = it / NB;
+      const double2* tq = tiles + (r >> 3) * 8 * M;
+      const double2 a = tq[tidx(k, r & 7)];
+      const double2 b = cconj(tq[tidx((M - k) & (M - 1), r & 7)]);
+      const double2 E = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
+      const double2 O = mul_mi(make_double2(0.5 * (a.x - b.x), 0.5 * (a.y - b.y)));
+      stage[k * XS + r] = cadd(E, cmul(twp[k], O));
+      if (k != M - k) stage[(M - k) * XS + r] = cadd(cconj(E), cmul(twp[M - k], cconj(O)));
+    }
+  }
+  __syncthreads();
+  // NB-point DFT across the rows (y_b -> k_b), twiddle w_N2^{y_a k_b}, scatter to [kx][k_b][z][y_a]
+  double2* out = cx.spec + ((long long)load * g.c + comp) * g.nspec + (long long)z * NA + ya;
+  const long long kbstride = (long long)g.N3 * NA;
+  for (int kx = t; kx < H1; kx += T) {
+    double2 v[NB];
+#pragma unroll
+    for (int r = 0; r < NB; ++r) v[r] = stage[kx * XS + r];
+    Dft<NB>::run(v);
+#pragma unroll
+    for (int kb = 0; kb < NB; ++kb) {
+      const double2 w = twy[ya * kb];
+      out[((long long)kx * NB + kb) * kbstride] = kb ? cmul(v[kb], w) : v[kb];
+    }
+  }
+  if (MODE == CG) {
+    double tot;
+    if (grid_reduce<true>(mx, red_partials(cx.sc, RED_RNORM, load), red_counter(cx.sc, RED_RNORM, load), gridDim.x,
+                          blockIdx.x, &tot, red_sh)) {
+      if (threadIdx.x == 0) scalar_after_rnorm(st, tot, cx.hist, cx.hist_stride, load);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------- F3
+template <int M, int NB, int MODE>
+__global__ void __launch_bounds__(fft_threads_nt(M, NB / 8)) f3_kernel(Ctx cx, double* __restrict__ dst) {
+  constexpr int NT = NB / 8;
+  constexpr int T = fft_threads_nt(M, NT);
+  constexpr int H1 = M + 1;
+  constexpr int XS = NB + 1;
+  const Geo g = cx.g;
+  const int load = blockIdx.y;
+  LoadState* st = cx.st + load;
+  if (MODE == CG && !st->active) return;
+  extern __shared__ double2 smem[];
+  double2* tiles = smem;
+  double2* stage = tiles + NB * M;              // X[kx][k_b], later d rows | u rows
+  double2* tw = stage + f3_stage<M, NB>();
+  double2* twp = tw + M;
+  double2* twy = twp + H1;
+  const int t = threadIdx.x;
+  const int NA = g.NA, N2 = g.N2, N1 = g.N1;
+  const int ya = blockIdx.x % NA;
+  const int zc = blockIdx.x / NA;
+  const int z = zc % g.N3, comp = zc / g.N3;
+  const double2* in = cx.spec + ((long long)load * g.c + comp) * g.nspec + (long long)z * NA + ya;
+  const long long kbstride = (long long)g.N3 * NA;
+#pragma unroll
+  for (int i = 0; i < (H1 * NB + T - 1) / T; ++i) {
+    const int e = t + i * T;
+    if (e < H1 * NB) cp_async16(&stage[(e / NB) * XS + (e % NB)], in + (long long)e * kbstride);
+  }
+  cp_commit();
+  for (int i = t; i < M; i += T) tw[i] = cx.tw.x[i];
+  for (int i = t; i <= M; i += T) twp[i] = cx.tw.xpost[i];
+  for (int i = t; i < N2; i += T) twy[i] = cx.tw.y[i];
+  cp_wait<0>();
+  __syncthreads();
+  // conj twiddle + inverse NB-point DFT (k_b -> y_b), in place
+  for (int kx = t; kx < H1; kx += T) {
+    double2 v[NB];
+#pragma unroll
+    for (int kb = 0; kb < NB; ++kb) {
+      const double2 a = stage[kx * XS + kb];
+      v[kb] = kb ? cmul(a, cconj(twy[ya * kb])) : a;
+    }
+    dft_reg<NB, true>(v);
+#pragma unroll
+    for (int r = 0; r < NB; ++r) stage[kx * XS + r] = v[r];
+  }
+  __syncthreads();
+  // C2R pre-processing of each row r into the x tiles
+#pragma unroll
+  for (int i = 0; i < ((M / 2 + 1) * NB + T - 1) / T; ++i) {
+    const int it = t + i * T;
+    if (it < (M / 2 + 1) * NB) {
+      const int r = it % NB, k = it / NB;
+      double2* tq = tiles + (r >> 3) * 8 * M;
+      const int c = r & 7;
+      if (k == 0) {
+        const double X0 = stage[r].x, XM = stage[M * XS + r].x;
+        tq[tidx(0, c)] = make_double2(X0 + XM, X0 - XM);
+      } else {
+        const double2 a = stage[k * XS + r];
+        const double2 bm = stage[(M - k) * XS + r];
+        const double2 b = cconj(bm);
+        const double2 E = cadd(a, b);
+        const double2 O = cmul(csub(a, b), cconj(twp[k]));
+        tq[tidx(k, c)] = cadd(E, mul_pi(O));
+        if (k != M - k) {
+          const double2 a2 = bm, b2 = cconj(a);
+          const double2 E2 = cadd(a2, b2);
+          const double2 O2 = cmul(csub(a2, b2), cconj(twp[M - k]));
+          tq[tidx(M - k, c)] = cadd(E2, mul_pi(O2));
+        }
+      }
+    }
+  }
+  __syncthreads();
+  const long long vbase = (long long)load * g.c * g.n + (long long)comp * g.n + (long long)z * N2 * N1;
+  const int it0 = MODE == CG ? st->iters : 0;
+  if (MODE == CG) {  // d_old and u rows land while the inverse x FFT runs
+    if (it0 > 0) {
+#pragma unroll
+      for (int i = 0; i < (NB * M + T - 1) / T; ++i) {
+        const int e = t + i * T;
+        if (e < NB * M) {
+          const int r = e / M, j = e & (M - 1);
+          const long long off = vbase + (long long)(ya + NA * r) * N1 + 2 * j;
+          cp_async16(&stage[e], cx.d + off);
+          cp_async16(&stage[NB * M + e], cx.u + off);
+        }
+      }
+    }
+    cp_commit();
+  }
+  fft_tiles<M, NT, true>(tiles, tw);
+  if (MODE == CG) {
+    cp_wait<0>();
+    __syncthreads();
+  }
+  const double beta = MODE == CG ? st->beta : 0.0, alpha = MODE == CG ? st->alpha : 0.0;
+#pragma unroll
+  for (int i = 0; i < (NB * M + T - 1) / T; ++i) {
+    const int e = t + i * T;
+    if (e < NB * M) {
+      const int r = e / M, j = e & (M - 1);
+      const double2 s = tiles[(r >> 3) * 8 * M + tidx(j, r & 7)];
+      const long long off = vbase + (long long)(ya + NA * r) * N1 + 2 * j;
+      if (MODE == STANDALONE) {
+        *reinterpret_cast<double2*>(dst + off) = s;
+      } else if (it0 == 0) {
+        *reinterpret_cast<double2*>(cx.d + off) = s;  // d = s  (Alg 2 l.2, l.8)
+      } else {
+        const double2 dold = stage[e];
+        double2 uu = stage[NB * M + e];  // deferred u += alpha_{m-1} d_{m-1}  (Alg 2 l.12)
+        uu.x = fma(alpha, dold.x, uu.x);
+        uu.y = fma(alpha, dold.y, uu.y);
+        *reinterpret_cast<double2*>(cx.u + off) = uu;
+        *reinterpret_cast<double2*>(cx.d + off) = make_double2(fma(beta, dold.x, s.x), fma(beta, dold.y, s.y));
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------- F2
+template <int NA, int L3, int NC>
+__host__ __device__ constexpr int f2_tile_elems() {
+  return NC * NA * L3 + L3;  // tiles + z twiddles (double2)
+}
+template <int NA, int L3, int NC>
+__host__ __device__ constexpr bool f2_staged() {
+  return f2_tile_elems<NA, L3, NC>() * 16 + NA * L3 * (NC == 1 ? 1 : (NC == 2 ? 3 : 6)) * 8 <= 200 * 1024;
+}
+template <int NA, int L3, int NC>
+__host__ __device__ constexpr int f2_smem_bytes() {
+  return f2_tile_elems<NA, L3, NC>() * 16 + (f2_staged<NA, L3, NC>() ? NA * L3 * (NC == 1 ? 1 : (NC == 2 ? 3 : 6)) * 8 : 0);
+}
+
+template <int NA, int L3, int NC, bool INV>
+__device__ __forceinline__ void row_dft(double2* const* tiles) {
+  // NA-point DFT along the tile columns of each row z (columns a = 0..NA-1 over NA/8 tiles)
+  for (int z = threadIdx.x; z < L3; z += blockDim.x) {
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      double2 v[NA];
+#pragma unroll
+      for (int a = 0; a < NA; ++a) v[a] = tiles[q][(a >> 3) * 8 * L3 + tidx(z, a & 7)];
+      dft_reg<NA, INV>(v);
+#pragma unroll
+      for (int a = 0; a < NA; ++a) tiles[q][(a >> 3) * 8 * L3 + tidx(z, a & 7)] = v[a];
+    }
+  }
+}
+
+template <int NA, int L3, int NC, int MODE>
+__global__ void __launch_bounds__(fft_threads_nt(L3, NA / 8)) f2_kernel(Ctx cx) {
+  constexpr int NT = NA / 8;
+  constexpr int T = fft_threads_nt(L3, NT);
+  constexpr int NCC = NC == 1 ? 1 : (NC == 2 ? 3 : 6);
+  constexpr bool STG = f2_staged<NA, L3, NC>();
+  const Geo g = cx.g;
+  const int load = blockIdx.y;
+  if (MODE == CG && !cx.st[load].active) return;
+  extern __shared__ double2 smem[];
+  double2* tiles[NC];
+#pragma unroll
+  for (int q = 0; q < NC; ++q) tiles[q] = smem + q * NA * L3;
+  double2* tw = smem + NC * NA * L3;
+  double* gs = reinterpret_cast<double*>(tw + L3);
+  __shared__ double red_sh[32];
+  const int t = threadIdx.x;
+  const int kxkb = blockIdx.x;
+  const int kx = kxkb / g.NB;
+  const long long boff = (long long)kxkb * L3 * NA;
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    const double2* base = cx.spec + ((long long)load * g.c + q) * g.nspec + boff;
+#pragma unroll
+    for (int i = 0; i < (NA * L3 + T - 1) / T; ++i) {
+      const int e = t + i * T;
+      if (e < NA * L3) {
+        const int z = e / NA, a = e % NA;
+        cp_async16(&tiles[q][(a >> 3) * 8 * L3 + tidx(z, a & 7)], base + e);
+      }
+    }
+  }
+  if (STG) {
+#pragma unroll
+    for (int q = 0; q < NCC; ++q) {
+#pragma unroll
+      for (int i = 0; i < (NA * L3 + T - 1) / T; ++i) {
+        const int e = t + i * T;
+        if (e < NA * L3) cp_async8(&gs[q * NA * L3 + e], cx.gtab + q * g.nspec + boff + e);
+      }
+    }
+  }
+  cp_commit();
+  for (int i = t; i < L3; i += T) tw[i] = cx.tw.z[i];
+  cp_wait<0>();
+  __syncthreads();
+  row_dft<NA, L3, NC, false>(tiles);
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NC; ++q) fft_tiles<L3, NT, false>(tiles[q], tw);
+  const double w = parseval_w(kx, g.M);
+  double part = 0.0;
+#pragma unroll
+  for (int i = 0; i < (NA * L3 + T - 1) / T; ++i) {
+    const int e = t + i * T;
+    if (e < NA * L3) {
+      const int z = e / NA, a = e % NA;
+      const int ti = (a >> 3) * 8 * L3 + tidx(z, a & 7);
+      if (STG)
+        part += gmul_bin<NC>(tiles, ti, gs, NA * L3, e, w);
+      else
+        part += gmul_bin<NC>(tiles, ti, cx.gtab, g.nspec, boff + e, w);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NC; ++q) fft_tiles<L3, NT, true>(tiles[q], tw);
+  row_dft<NA, L3, NC, true>(tiles);
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NC; ++q) {
+    double2* base = cx.spec + ((long long)load * g.c + q) * g.nspec + boff;
+#pragma unroll
+    for (int i = 0; i < (NA * L3 + T - 1) / T; ++i) {
+      const int e = t + i * T;
+      if (e < NA * L3) {
+        const int z = e / NA, a = e % NA;
+        base[e] = tiles[q][(a >> 3) * 8 * L3 + tidx(z, a & 7)];
+      }
+    }
+  }
+  gamma_finish(cx, load, part, red_sh, MODE);
+}
+
+// ------------------------------------------------------------------------------------- launchers
+template <class K>
+static void set_smem3(K kernel, int bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+template <class F>
+static int dispatch_m(int M, F&& f) {
+  switch (M) {
+    case 16: return f(std::integral_constant<int, 16>{});
+    case 32: return f(std::integral_constant<int, 32>{});
+    case 64: return f(std::integral_constant<int, 64>{});
+    case 128: return f(std::integral_constant<int, 128>{});
+    case 256: return f(std::integral_constant<int, 256>{});
+    default: return -1;
+  }
+}
+template <class F>
+static int dispatch_nb(int NB, F&& f) {
+  switch (NB) {
+    case 8: return f(std::integral_constant<int, 8>{});
+    case 16: return f(std::integral_constant<int, 16>{});
+    default: return -1;
+  }
+}
+
+bool schedule3_supported(const Geo& g) {
+  if (g.dim != 3 || g.N2 < 64 || g.N2 > 256 || g.M < 16 || g.M > 256) return false;
+  if (g.N3 < 16 || g.N3 > 512) return false;
+  const int NB = g.N2 >= 128 ? 16 : 8;
+  const int NA = g.N2 / NB;
+  if (NA != 8 && NA != 16) return false;
+  // F2 tile must fit the shared memory of one CTA
+  const long long bytes = ((long long)g.c * NA * g.N3 + g.N3) * 16;
+  return bytes <= 200 * 1024 && (g.c == 1 || g.c == 3);
+}
+
+int launch_f1(const Ctx& cx, int mode, const double* src, cudaStream_t s) {
+  const Geo& g = cx.g;
+  return dispatch_m(g.M, [&](auto Mc) {
+    constexpr int M = decltype(Mc)::value;
+    return dispatch_nb(g.NB, [&](auto Bc) {
+      constexpr int NB = decltype(Bc)::value;
+      const int sm = (f13_smem_elems<M, NB, false>() + g.N2) * 16;
+      const dim3 grid((unsigned)(g.NA * g.N3 * g.c), g.nrhs);
+      auto go = [&](auto k) {
+        set_smem3(k, sm);
+        k<<<grid, fft_threads_nt(M, NB / 8), sm, s>>>(cx, src);
+        return 1;
+      };
+      return mode == CG ? go(f1_kernel<M, NB, CG>) : go(f1_kernel<M, NB, STANDALONE>);
+    });
+  });
+}
+
+int launch_f3(const Ctx& cx, int mode, double* dst, cudaStream_t s) {
+  const Geo& g = cx.g;
+  return dispatch_m(g.M, [&](auto Mc) {
+    constexpr int M = decltype(Mc)::value;
+    return dispatch_nb(g.NB, [&](auto Bc) {
+      constexpr int NB = decltype(Bc)::value;
+      const int sm = (f13_smem_elems<M, NB, true>() + g.N2) * 16;
+      const dim3 grid((unsigned)(g.NA * g.N3 * g.c), g.nrhs);
+      auto go = [&](auto k) {
+        set_smem3(k, sm);
+        k<<<grid, fft_threads_nt(M, NB / 8), sm, s>>>(cx, dst);
+        return 1;
+      };
+      return mode == CG ? go(f3_kernel<M, NB, CG>) : go(f3_kernel<M, NB, STANDALONE>);
+    });
+  });
+}
+
+template <class F>
+static int dispatch_l3(int L, F&& f) {
+  switch (L) {
+    case 16: return f(std::integral_constant<int, 16>{});
+    case 32: return f(std::integral_constant<int, 32>{});
+    case 64: return f(std::integral_constant<int, 64>{});
+    case 128: return f(std::integral_constant<int, 128>{});
+    case 256: return f(std::integral_constant<int, 256>{});
+    case 512: return f(std::integral_constant<int, 512>{});
+    default: return -1;
+  }
+}
+
+int launch_f2(const Ctx& cx, int mode, cudaStream_t s) {
+  const Geo& g = cx.g;
+  return dispatch_l3(g.N3, [&](auto Lc) {
+    constexpr int L3 = decltype(Lc)::value;
+    const dim3 grid((unsigned)(g.H1 * g.NB), g.nrhs);
+    auto run = [&](auto Ac) {
+      constexpr int NA = decltype(Ac)::value;
+      auto go = [&](auto k, int sm) {
+        set_smem3(k, sm);
+        k<<<grid, fft_threads_nt(L3, NA / 8), sm, s>>>(cx);
+        return 1;
+      };
+      if (g.c == 1)
+        return mode == CG ? go(f2_kernel<NA, L3, 1, CG>, f2_smem_bytes<NA, L3, 1>())
+                          : go(f2_kernel<NA, L3, 1, STANDALONE>, f2_smem_bytes<NA, L3, 1>());
+      if constexpr (f2_smem_bytes<NA, L3, 3>() <= 220 * 1024) {
+        return mode == CG ? go(f2_kernel<NA, L3, 3, CG>, f2_smem_bytes<NA, L3, 3>())
+                          : go(f2_kernel<NA, L3, 3, STANDALONE>, f2_smem_bytes<NA, L3, 3>());
+      } else {
+        return -1;
+      }
+    };
+    if (g.NA == 8) return run(std::integral_constant<int, 8>{});
+    if (g.NA == 16) return run(std::integral_constant<int, 16>{});
+    return -1;
+  });
+}
+
+}  // namespace uno

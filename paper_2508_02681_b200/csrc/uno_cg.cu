@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -264,6 +265,18 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
   g.nspec = (long long)g.H1 * N2 * N3;
   g.h = D.h > 0 ? D.h : 1.0 / N1;
   g.C = c * (c + 1) / 2;
+  g.NA = g.NB = 0;
+  {  // 3-pass four-step schedule where it applies (UNO_SCHEDULE=5 forces the 5-pass one)
+    const char* ev = getenv("UNO_SCHEDULE");
+    const bool force5 = ev && ev[0] == '5';
+    Geo t3 = g;
+    t3.NB = N2 >= 128 ? 16 : 8;
+    t3.NA = N2 / t3.NB;
+    if (!force5 && schedule3_supported(t3)) {
+      g.NB = t3.NB;
+      g.NA = t3.NA;
+    }
+  }
   cudaStream_t s = h->stream;
   const long long vec = (long long)g.nrhs * c * g.n;
   static bool pool_cfg = false;
@@ -390,11 +403,17 @@ extern "C" uno_status uno_cg_apply_precond(uno_cg_handle* h, const double* d_r, 
   if (!h || !d_r || !d_z) return fail(UNO_ERR_ARG, "null argument");
   long long launches = 0;
   cudaStream_t s = h->stream;
-  KL(launch_xfwd(h->cx, STANDALONE, d_r, s), KC_XF);
-  if (h->g.dim == 3) KL(launch_ypass(h->cx, STANDALONE, false, s), KC_Y);
-  KL(launch_gpass(h->cx, STANDALONE, s), KC_G);
-  if (h->g.dim == 3) KL(launch_ypass(h->cx, STANDALONE, true, s), KC_Y);
-  KL(launch_xinv(h->cx, STANDALONE, d_z, s), KC_XI);
+  if (h->g.NB > 0) {  // 3-pass four-step schedule
+    KL(launch_f1(h->cx, STANDALONE, d_r, s), KC_XF);
+    KL(launch_f2(h->cx, STANDALONE, s), KC_G);
+    KL(launch_f3(h->cx, STANDALONE, d_z, s), KC_XI);
+  } else {
+    KL(launch_xfwd(h->cx, STANDALONE, d_r, s), KC_XF);
+    if (h->g.dim == 3) KL(launch_ypass(h->cx, STANDALONE, false, s), KC_Y);
+    KL(launch_gpass(h->cx, STANDALONE, s), KC_G);
+    if (h->g.dim == 3) KL(launch_ypass(h->cx, STANDALONE, true, s), KC_Y);
+    KL(launch_xinv(h->cx, STANDALONE, d_z, s), KC_XI);
+  }
   CK(cudaGetLastError());
   if (h_rz) {
     CK(cudaMemcpyAsync(h->h_small, h->results + RED_GAMMA * kMaxRhs, h->g.nrhs * 8, cudaMemcpyDeviceToHost, s));
@@ -419,12 +438,18 @@ static int enqueue_iteration(uno_cg_handle* h, cudaStream_t s, cudaEvent_t* ev /
     n += r;
     return true;
   };
-  const bool d3 = h->g.dim == 3;
-  if (!run(0, [&] { return launch_xfwd(cx, CG, cx.r, s); })) return -1;
-  if (d3 && !run(1, [&] { return launch_ypass(cx, CG, false, s); })) return -1;
-  if (!run(2, [&] { return launch_gpass(cx, CG, s); })) return -1;
-  if (d3 && !run(3, [&] { return launch_ypass(cx, CG, true, s); })) return -1;
-  if (!run(4, [&] { return launch_xinv(cx, CG, nullptr, s); })) return -1;
+  if (h->g.NB > 0) {  // 3-pass four-step schedule (fft3.cu)
+    if (!run(0, [&] { return launch_f1(cx, CG, cx.r, s); })) return -1;
+    if (!run(2, [&] { return launch_f2(cx, CG, s); })) return -1;
+    if (!run(4, [&] { return launch_f3(cx, CG, nullptr, s); })) return -1;
+  } else {
+    const bool d3 = h->g.dim == 3;
+    if (!run(0, [&] { return launch_xfwd(cx, CG, cx.r, s); })) return -1;
+    if (d3 && !run(1, [&] { return launch_ypass(cx, CG, false, s); })) return -1;
+    if (!run(2, [&] { return launch_gpass(cx, CG, s); })) return -1;
+    if (d3 && !run(3, [&] { return launch_ypass(cx, CG, true, s); })) return -1;
+    if (!run(4, [&] { return launch_xinv(cx, CG, nullptr, s); })) return -1;
+  }
   if (!run(5, [&] { return launch_kapply(cx, CG, cx.d, cx.p, s); })) return -1;
   return n;
 }
@@ -543,7 +568,7 @@ extern "C" uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, doub
   }
   CK(cudaMemcpyAsync(h->st, h->h_st, g.nrhs * sizeof(LoadState), cudaMemcpyHostToDevice, s));
   const long long work = (long long)g.nrhs * g.c * g.n;
-  const int per_iter = (g.dim == 3 ? 6 : 4);
+  const int per_iter = (g.dim == 3 && g.NB == 0) ? 6 : 4;
   if (!h->timing) {
     // whole solve device-side: WHILE node over bodies of `chunk` iterations
     const int chunk = work >= (1LL << 22) ? 2 : 4;
@@ -580,7 +605,7 @@ extern "C" uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, doub
       const int worked = std::min(chunk, std::max(0, after - before));
       for (int i = 0; i < worked; ++i)
         for (int slot = 0; slot < 6; ++slot) {
-          if (g.dim == 2 && (slot == 1 || slot == 3)) continue;
+          if ((g.dim == 2 || g.NB > 0) && (slot == 1 || slot == 3)) continue;
           float ms = 0.f;
           if (cudaEventElapsedTime(&ms, h->tev[((size_t)i * 6 + slot) * 2], h->tev[((size_t)i * 6 + slot) * 2 + 1]) ==
               cudaSuccess) {

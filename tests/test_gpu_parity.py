@@ -59,7 +59,16 @@ def loads_for(physics, d, nrhs):
 
 
 SHAPES = [((16, 8, 32), "thermal"), ((32, 16, 8), "thermal"), ((64, 64, 64), "thermal"), ((32, 32), "thermal"),
-          ((8, 64), "thermal"), ((16, 8, 16), "elastic"), ((32, 16, 8), "elastic"), ((16, 32), "elastic")]
+          ((8, 64), "thermal"), ((16, 8, 16), "elastic"), ((32, 16, 8), "elastic"), ((16, 32), "elastic"),
+          # 3-pass (four-step) schedule shapes: N2 in {64, 128, 256}, N3 >= 16
+          ((32, 64, 16), "thermal"), ((16, 128, 32), "thermal"), ((32, 256, 16), "thermal"), ((16, 64, 16), "elastic")]
+
+
+@pytest.fixture(params=["3", "5"])
+def schedule(request, monkeypatch):
+    """Both transform schedules (UNO_SCHEDULE is read at handle creation)."""
+    monkeypatch.setenv("UNO_SCHEDULE", request.param)
+    return request.param
 
 
 @pytest.mark.parametrize("N,physics", SHAPES)
@@ -77,7 +86,7 @@ def test_apply_K_parity(N, physics):
 
 
 @pytest.mark.parametrize("N,physics", SHAPES)
-def test_apply_precond_parity(N, physics):
+def test_apply_precond_parity(N, physics, schedule):
     g, ph, mat, amp, seed = make_case(N, physics)
     nrhs = 2
     s = solver(ph, physics, mat, nrhs, seed, amp)
@@ -159,7 +168,7 @@ def test_solve_config0():
     _solve_parity(g, "thermal", P.phase, P.mat, np.eye(2), P.seed, P.amp)
 
 
-def test_solve_config1_64cubed():
+def test_solve_config1_64cubed(schedule):
     P = synth.config1()
     g = fem.Grid((64, 64, 64), h=1 / 64)
     _solve_parity(g, "thermal", P.phase, P.mat, P.loads, P.seed, P.amp)
