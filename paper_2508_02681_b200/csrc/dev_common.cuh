@@ -142,32 +142,60 @@ __device__ __forceinline__ double gmul_bin(double2* const* tiles, int ti, const 
   }
 }
 
-__device__ __forceinline__ double parseval_w(int kx, int M) { return (kx == 0 || kx == M) ? 1.0 : 2.0; }
-
-static __device__ void gamma_finish(const Ctx& cx, int load, double part, double* red_sh, int mode) {
-  double tot;
-  if (grid_reduce<false>(part, red_partials(cx.sc, RED_GAMMA, load), red_counter(cx.sc, RED_GAMMA, load),
-                         gridDim.x, blockIdx.x, &tot, red_sh)) {
-    if (threadIdx.x == 0) {
-      if (mode == CG)
-        scalar_after_gamma(cx.st + load, tot);
-      else
-        cx.sc.results[RED_GAMMA * kMaxRhs + load] = tot;
-    }
+// Same multiply on NC register values of one bin (fused-butterfly variant).
+template <int NC>
+__device__ __forceinline__ double gmul_vals(double2* x, const double* gtab, long long nspec, long long b, double w) {
+  if (NC == 1) {
+    const double gv = gtab[b];
+    const double q = w * gv * fma(x[0].x, x[0].x, x[0].y * x[0].y);
+    x[0] = make_double2(gv * x[0].x, gv * x[0].y);
+    return q;
+  } else if (NC == 2) {
+    const double v1 = gtab[b], v2 = gtab[nspec + b], v3 = gtab[2 * nspec + b];
+    const double2 X1 = x[0], X2 = x[1];
+    const double2 Y1 = make_double2(fma(v1, X1.x, v3 * X2.x), fma(v1, X1.y, v3 * X2.y));
+    const double2 Y2 = make_double2(fma(v3, X1.x, v2 * X2.x), fma(v3, X1.y, v2 * X2.y));
+    x[0] = Y1;
+    x[1] = Y2;
+    return w * (X1.x * Y1.x + X1.y * Y1.y + X2.x * Y2.x + X2.y * Y2.y);
+  } else {
+    const double v1 = gtab[b], v2 = gtab[nspec + b], v3 = gtab[2 * nspec + b];
+    const double v4 = gtab[3 * nspec + b], v5 = gtab[4 * nspec + b], v6 = gtab[5 * nspec + b];
+    const double2 X1 = x[0], X2 = x[1], X3 = x[2];
+    double2 Y1, Y2, Y3;
+    Y1.x = fma(v1, X1.x, fma(v3, X2.x, v6 * X3.x));
+    Y1.y = fma(v1, X1.y, fma(v3, X2.y, v6 * X3.y));
+    Y2.x = fma(v3, X1.x, fma(v2, X2.x, v5 * X3.x));
+    Y2.y = fma(v3, X1.y, fma(v2, X2.y, v5 * X3.y));
+    Y3.x = fma(v6, X1.x, fma(v5, X2.x, v4 * X3.x));
+    Y3.y = fma(v6, X1.y, fma(v5, X2.y, v4 * X3.y));
+    x[0] = Y1;
+    x[1] = Y2;
+    x[2] = Y3;
+    return w * (X1.x * Y1.x + X1.y * Y1.y + X2.x * Y2.x + X2.y * Y2.y + X3.x * Y3.x + X3.y * Y3.y);
   }
 }
 
+__device__ __forceinline__ double parseval_w(int kx, int M) { return (kx == 0 || kx == M) ? 1.0 : 2.0; }
+
+// Per-CTA partial of a reduction: deterministic block reduce, thread 0 stores the partial.
+// The fixed-order combine over CTAs and the CG scalar logic run in scalar_kernel (a 1-CTA-per-
+// load launch right after the producing pass) so no CTA waits on a global atomic at its end.
+template <bool MAX>
+__device__ __forceinline__ void partial_write(const Ctx& cx, int slot, int load, int my, double v, double* red_sh) {
+  const double b = block_reduce<MAX>(v, red_sh);
+  if (threadIdx.x == 0) red_partials(cx.sc, slot, load)[my] = b;
+}
+
+static __device__ void gamma_finish(const Ctx& cx, int load, double part, double* red_sh, int mode) {
+  (void)mode;
+  partial_write<false>(cx, RED_GAMMA, load, blockIdx.x, part, red_sh);
+}
+
 static __device__ void dp_finish(const Ctx& cx, int load, int nblk, int my, double part, double* red_sh, int mode) {
-  double tot;
-  if (grid_reduce<false>(part, red_partials(cx.sc, RED_DP, load), red_counter(cx.sc, RED_DP, load), nblk, my, &tot,
-                         red_sh)) {
-    if (threadIdx.x == 0) {
-      if (mode == CG)
-        scalar_after_dp(cx.st + load, tot);
-      else
-        cx.sc.results[RED_DP * kMaxRhs + load] = tot;
-    }
-  }
+  (void)nblk;
+  (void)mode;
+  partial_write<false>(cx, RED_DP, load, my, part, red_sh);
 }
 
 }  // namespace uno

@@ -220,6 +220,15 @@ struct FftStagesNT<L, NT, L, INV> {
   static __device__ __forceinline__ void run(double2*, const double2*) {}
 };
 
+template <int R>
+__device__ __forceinline__ void dft_reg_inv_inline(double2* v) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) v[r].y = -v[r].y;
+  Dft<R>::run(v);
+#pragma unroll
+  for (int r = 0; r < R; ++r) v[r].y = -v[r].y;
+}
+
 template <int L, int NT, bool INV>
 __device__ __forceinline__ void fft_tiles(double2* s, const double2* tw) {
   FftStagesNT<L, NT, 1, INV>::run(s, tw);
@@ -227,6 +236,87 @@ __device__ __forceinline__ void fft_tiles(double2* s, const double2* tw) {
 // threads for one butterfly per thread in every stage of NT tiles
 __host__ __device__ constexpr int fft_threads_nt(int L, int NT) {
   return (NT * 8 * L / min_radix(L)) < 64 ? 64 : NT * 8 * L / min_radix(L);
+}
+
+// ---- forward FFT -> per-bin operator -> inverse FFT, with the operator fused into the middle
+// butterfly: the last forward stage (radix R, span L/R) produces, per thread, the R bins
+// j + r L/R in registers; they are exactly the inputs of the first inverse stage (radix R,
+// span 1) when the plan's first and last radices agree, so the symbol multiply needs no extra
+// shared-memory round trip or barrier.
+__host__ __device__ constexpr int plan_ns(int L, int s) {  // span of stage s
+  return s == 0 ? 1 : plan_ns(L, s - 1) * pick_radix(L / plan_ns(L, s - 1));
+}
+__host__ __device__ constexpr int plan_stages(int L, int ns = 1) {
+  return ns >= L ? 0 : 1 + plan_stages(L, ns * pick_radix(L / ns));
+}
+__host__ __device__ constexpr int plan_radix(int L, int s) { return pick_radix(L / plan_ns(L, s)); }
+__host__ __device__ constexpr bool gconv_fusable(int L) {
+  return plan_stages(L) >= 2 && plan_radix(L, 0) == plan_radix(L, plan_stages(L) - 1);
+}
+
+template <int L, int NT, int NS, int STOP, bool INV>
+struct FftStagesNTUntil {
+  static __device__ __forceinline__ void run(double2* s, const double2* tw) {
+    if constexpr (NS < STOP) {
+      constexpr int R = pick_radix(L / NS);
+      fft_stage_nt<L, NT, R, NS, INV>(s, tw);
+      FftStagesNTUntil<L, NT, NS * R, STOP, INV>::run(s, tw);
+    }
+  }
+};
+
+// op(int tile, int col, int kbin, double2* x /*NC values of that bin*/) -> Parseval term;
+// modifies x in place.  Returns the thread's sum of op results.  Caller syncs before.
+template <int L, int NT, int NC, class Op>
+__device__ __forceinline__ double fft_gconv(double2* const* tiles, const double2* __restrict__ tw, Op op) {
+  constexpr int S = plan_stages(L);
+  constexpr int RL = plan_radix(L, S - 1);
+  constexpr int NJ = L / RL;
+  static_assert(gconv_fusable(L), "first and last radix must agree");
+#pragma unroll
+  for (int q = 0; q < NC; ++q) FftStagesNTUntil<L, NT, 1, NJ, false>::run(tiles[q], tw);
+  constexpr int ITEMS = NJ * kTile * NT;
+  const int t = threadIdx.x;
+  const bool act = t < ITEMS;
+  const int tq = t / (NJ * kTile), rem = t - tq * (NJ * kTile);
+  const int c = rem & 7, j = rem >> 3;
+  double part = 0.0;
+  double2 v[NC][RL];
+  if (act) {
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      const double2* sq = tiles[q] + tq * 8 * L;
+#pragma unroll
+      for (int r = 0; r < RL; ++r) v[q][r] = sq[tidx(j + r * NJ, c)];
+#pragma unroll
+      for (int r = 1; r < RL; ++r) v[q][r] = cmul(v[q][r], tw[r * j]);  // last-stage twiddles (span NJ)
+      Dft<RL>::run(v[q]);
+    }
+#pragma unroll
+    for (int r = 0; r < RL; ++r) {
+      double2 x[NC];
+#pragma unroll
+      for (int q = 0; q < NC; ++q) x[q] = v[q][r];
+      part += op(tq, c, j + r * NJ, x);
+#pragma unroll
+      for (int q = 0; q < NC; ++q) v[q][r] = x[q];
+    }
+#pragma unroll
+    for (int q = 0; q < NC; ++q) dft_reg_inv_inline<RL>(v[q]);  // first inverse stage (span 1)
+  }
+  __syncthreads();
+  if (act) {
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      double2* sq = tiles[q] + tq * 8 * L;
+#pragma unroll
+      for (int r = 0; r < RL; ++r) sq[tidx(j * RL + r, c)] = v[q][r];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NC; ++q) FftStagesNT<L, NT, plan_radix(L, 0), true>::run(tiles[q], tw);
+  return part;
 }
 
 // In-register forward/inverse DFT of length R (R = 2, 4, 8, 16).

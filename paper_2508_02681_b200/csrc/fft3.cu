@@ -341,25 +341,34 @@ __global__ void __launch_bounds__(fft_threads_nt(L3, NA / 8)) f2_kernel(Ctx cx) 
   __syncthreads();
   row_dft<NA, L3, NC, false>(tiles);
   __syncthreads();
-#pragma unroll
-  for (int q = 0; q < NC; ++q) fft_tiles<L3, NT, false>(tiles[q], tw);
   const double w = parseval_w(kx, g.M);
   double part = 0.0;
+  if constexpr (gconv_fusable(L3) && NC * plan_radix(L3, plan_stages(L3) - 1) <= 32) {
+    // symbol multiply fused into the middle butterfly of the z FFT (fft.cuh fft_gconv)
+    part = fft_gconv<L3, NT, NC>(tiles, tw, [&](int tq, int c, int kz, double2* x) {
+      const int a = tq * 8 + c;
+      return STG ? gmul_vals<NC>(x, gs, NA * L3, (long long)kz * NA + a, w)
+                 : gmul_vals<NC>(x, cx.gtab, g.nspec, boff + (long long)kz * NA + a, w);
+    });
+  } else {
 #pragma unroll
-  for (int i = 0; i < (NA * L3 + T - 1) / T; ++i) {
-    const int e = t + i * T;
-    if (e < NA * L3) {
-      const int z = e / NA, a = e % NA;
-      const int ti = (a >> 3) * 8 * L3 + tidx(z, a & 7);
-      if (STG)
-        part += gmul_bin<NC>(tiles, ti, gs, NA * L3, e, w);
-      else
-        part += gmul_bin<NC>(tiles, ti, cx.gtab, g.nspec, boff + e, w);
+    for (int q = 0; q < NC; ++q) fft_tiles<L3, NT, false>(tiles[q], tw);
+#pragma unroll
+    for (int i = 0; i < (NA * L3 + T - 1) / T; ++i) {
+      const int e = t + i * T;
+      if (e < NA * L3) {
+        const int z = e / NA, a = e % NA;
+        const int ti = (a >> 3) * 8 * L3 + tidx(z, a & 7);
+        if (STG)
+          part += gmul_bin<NC>(tiles, ti, gs, NA * L3, e, w);
+        else
+          part += gmul_bin<NC>(tiles, ti, cx.gtab, g.nspec, boff + e, w);
+      }
     }
-  }
-  __syncthreads();
+    __syncthreads();
 #pragma unroll
-  for (int q = 0; q < NC; ++q) fft_tiles<L3, NT, true>(tiles[q], tw);
+    for (int q = 0; q < NC; ++q) fft_tiles<L3, NT, true>(tiles[q], tw);
+  }
   row_dft<NA, L3, NC, true>(tiles);
   __syncthreads();
 #pragma unroll

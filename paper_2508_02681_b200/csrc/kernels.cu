@@ -112,13 +112,7 @@ __global__ void __launch_bounds__(fft_threads(M)) xfwd_kernel(Ctx cx, const doub
       if (k != M - k) out[(long long)(M - k) * plane + row] = cadd(cconj(E), cmul(twp[M - k], cconj(O)));
     }
   }
-  if (MODE == CG) {
-    double tot;
-    if (grid_reduce<true>(mx, red_partials(cx.sc, RED_RNORM, load), red_counter(cx.sc, RED_RNORM, load), gridDim.x,
-                          blockIdx.x, &tot, red_sh)) {
-      if (threadIdx.x == 0) scalar_after_rnorm(st, tot, cx.hist, cx.hist_stride, load);
-    }
-  }
+  if (MODE == CG) partial_write<true>(cx, RED_RNORM, load, blockIdx.x, mx, red_sh);
 }
 
 // F5 / standalone inverse: half spectrum -> real rows; CG epilogue d = s + beta d, u += alpha d_old.
@@ -332,23 +326,31 @@ __global__ void __launch_bounds__(fft_threads(L)) gpass_z_kernel(Ctx cx) {
   for (int i = t; i < L; i += T) tw[i] = cx.tw.z[i];
   cp_wait<0>();
   __syncthreads();
-#pragma unroll
-  for (int q = 0; q < NC; ++q) fft_tile<L, false>(tiles[q], tw);
   const double w = parseval_w(kx, g.M);
   double part = 0.0;
+  if constexpr (gconv_fusable(L) && NC * plan_radix(L, plan_stages(L) - 1) <= 32) {
+    // symbol multiply fused into the middle butterfly (fft.cuh fft_gconv)
+    part = fft_gconv<L, 1, NC>(tiles, tw, [&](int, int c, int kz, double2* x) {
+      return STG ? gmul_vals<NC>(x, gs, 8 * L, (long long)kz * 8 + c, w)
+                 : gmul_vals<NC>(x, cx.gtab, g.nspec, boff + (long long)kz * g.N2 + c, w);
+    });
+  } else {
 #pragma unroll
-  for (int i = 0; i < (8 * L + T - 1) / T; ++i) {
-    const int e = t + i * T;
-    if (e < 8 * L) {
-      if (STG)
-        part += gmul_bin<NC>(tiles, tidx(e >> 3, e & 7), gs, 8 * L, e, w);
-      else
-        part += gmul_bin<NC>(tiles, tidx(e >> 3, e & 7), cx.gtab, g.nspec, boff + (long long)(e >> 3) * g.N2 + (e & 7), w);
+    for (int q = 0; q < NC; ++q) fft_tile<L, false>(tiles[q], tw);
+#pragma unroll
+    for (int i = 0; i < (8 * L + T - 1) / T; ++i) {
+      const int e = t + i * T;
+      if (e < 8 * L) {
+        if (STG)
+          part += gmul_bin<NC>(tiles, tidx(e >> 3, e & 7), gs, 8 * L, e, w);
+        else
+          part += gmul_bin<NC>(tiles, tidx(e >> 3, e & 7), cx.gtab, g.nspec, boff + (long long)(e >> 3) * g.N2 + (e & 7), w);
+      }
     }
-  }
-  __syncthreads();
+    __syncthreads();
 #pragma unroll
-  for (int q = 0; q < NC; ++q) fft_tile<L, true>(tiles[q], tw);
+    for (int q = 0; q < NC; ++q) fft_tile<L, true>(tiles[q], tw);
+  }
 #pragma unroll
   for (int q = 0; q < NC; ++q) {
     double2* base = cx.spec + ((long long)load * g.c + q) * g.nspec + boff;
@@ -1360,6 +1362,54 @@ __global__ void eq55_kernel(Ctx cx, const double* gtab, double* partials) {
     partials[blockIdx.x] = bmn;
     partials[gridDim.x + blockIdx.x] = bmx;
   }
+}
+
+// Fixed-order combine of the per-CTA partials of one reduction slot and the CG scalar step
+// that consumes it (Alg 2 l.3 / l.7-8 / l.10); one CTA per load case.
+__global__ void __launch_bounds__(256) scalar_kernel(Ctx cx, int slot, int nblk, int mode) {
+  __shared__ double sh[32];
+  const int load = blockIdx.x;
+  LoadState* st = cx.st + load;
+  if (mode == CG && !st->active) return;
+  const double* part = red_partials(cx.sc, slot, load);
+  const bool mx = slot == RED_RNORM;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
+    const double v = part[i];
+    acc = (i == (int)threadIdx.x) ? v : (mx ? fmax(acc, v) : acc + v);
+  }
+  const double tot = mx ? block_reduce<true>(acc, sh) : block_reduce<false>(acc, sh);
+  if (threadIdx.x == 0) {
+    if (mode == CG) {
+      if (slot == RED_RNORM) scalar_after_rnorm(st, tot, cx.hist, cx.hist_stride, load);
+      else if (slot == RED_GAMMA) scalar_after_gamma(st, tot);
+      else scalar_after_dp(st, tot);
+    } else {
+      cx.sc.results[slot * kMaxRhs + load] = tot;
+    }
+  }
+}
+
+int launch_scalar(const Ctx& cx, int slot, int mode, cudaStream_t s) {
+  const Geo& g = cx.g;
+  int nblk;
+  if (slot == RED_RNORM) {
+    nblk = g.NB > 0 ? g.NA * g.N3 * g.c : g.c * g.N3 * g.N2 / 8;
+  } else if (slot == RED_GAMMA) {
+    nblk = g.NB > 0 ? g.H1 * g.NB : (g.dim == 3 ? g.H1 * (g.N2 / 8) : (g.H1 + 7) / 8);
+  } else {
+    if (g.dim == 3 && g.c == 1) {
+      const int TX = g.N1 < 32 ? g.N1 : 32, ZC = g.N3 < 32 ? g.N3 : 32;
+      nblk = (g.N1 / TX) * (g.N2 / KT_TY) * (g.N3 / ZC);
+    } else if (g.dim == 3) {
+      const int ZC = g.N3 < 16 ? g.N3 : 16;
+      nblk = (g.N1 / KE_TX) * (g.N2 / KE_TY) * (g.N3 / ZC);
+    } else {
+      nblk = (int)((g.n + 255) / 256);
+    }
+  }
+  scalar_kernel<<<g.nrhs, 256, 0, s>>>(cx, slot, nblk, mode);
+  return 1;
 }
 
 // Device-side loop control of the CUDA-graph WHILE node: keep iterating while any load case

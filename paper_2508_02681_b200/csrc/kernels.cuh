@@ -52,7 +52,8 @@ int launch_eq55(const Ctx& cx, const double* gtab, double* minmax_partials, int*
 int launch_zero(double* x, long long n, cudaStream_t s);
 int launch_loop_ctl(cudaGraphConditionalHandle h, const LoadState* st, int nrhs, int* counter, int cap, cudaStream_t s);
 
-int blocks_needed_max(const Geo& g);  // max CTAs per load of any reducing kernel
+int blocks_needed_max(const Geo& g);
+int launch_scalar(const Ctx& cx, int slot, int mode, cudaStream_t s);  // combine partials + CG scalars  // max CTAs per load of any reducing kernel
 
 // 3-pass (four-step) schedule, fft3.cu
 bool schedule3_supported(const Geo& g);

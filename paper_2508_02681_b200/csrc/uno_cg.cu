@@ -390,6 +390,7 @@ extern "C" uno_status uno_cg_apply_K(uno_cg_handle* h, const double* d_u, double
   if (d_u == d_Au) return fail(UNO_ERR_ARG, "apply_K: input and output must not alias");
   long long launches = 0;
   KL(launch_kapply(h->cx, STANDALONE, d_u, d_Au, h->stream), KC_K);
+  KL(launch_scalar(h->cx, RED_DP, STANDALONE, h->stream), KC_OTHER);
   CK(cudaGetLastError());
   if (h_uAu) {
     CK(cudaMemcpyAsync(h->h_small, h->results + RED_DP * kMaxRhs, h->g.nrhs * 8, cudaMemcpyDeviceToHost, h->stream));
@@ -407,12 +408,14 @@ extern "C" uno_status uno_cg_apply_precond(uno_cg_handle* h, const double* d_r, 
     KL(launch_f1(h->cx, STANDALONE, d_r, s), KC_XF);
     KL(launch_f2(h->cx, STANDALONE, s), KC_G);
     KL(launch_f3(h->cx, STANDALONE, d_z, s), KC_XI);
+    KL(launch_scalar(h->cx, RED_GAMMA, STANDALONE, s), KC_OTHER);
   } else {
     KL(launch_xfwd(h->cx, STANDALONE, d_r, s), KC_XF);
     if (h->g.dim == 3) KL(launch_ypass(h->cx, STANDALONE, false, s), KC_Y);
     KL(launch_gpass(h->cx, STANDALONE, s), KC_G);
     if (h->g.dim == 3) KL(launch_ypass(h->cx, STANDALONE, true, s), KC_Y);
     KL(launch_xinv(h->cx, STANDALONE, d_z, s), KC_XI);
+    KL(launch_scalar(h->cx, RED_GAMMA, STANDALONE, s), KC_OTHER);
   }
   CK(cudaGetLastError());
   if (h_rz) {
@@ -440,17 +443,22 @@ static int enqueue_iteration(uno_cg_handle* h, cudaStream_t s, cudaEvent_t* ev /
   };
   if (h->g.NB > 0) {  // 3-pass four-step schedule (fft3.cu)
     if (!run(0, [&] { return launch_f1(cx, CG, cx.r, s); })) return -1;
+    n += launch_scalar(cx, RED_RNORM, CG, s);
     if (!run(2, [&] { return launch_f2(cx, CG, s); })) return -1;
+    n += launch_scalar(cx, RED_GAMMA, CG, s);
     if (!run(4, [&] { return launch_f3(cx, CG, nullptr, s); })) return -1;
   } else {
     const bool d3 = h->g.dim == 3;
     if (!run(0, [&] { return launch_xfwd(cx, CG, cx.r, s); })) return -1;
+    n += launch_scalar(cx, RED_RNORM, CG, s);
     if (d3 && !run(1, [&] { return launch_ypass(cx, CG, false, s); })) return -1;
     if (!run(2, [&] { return launch_gpass(cx, CG, s); })) return -1;
+    n += launch_scalar(cx, RED_GAMMA, CG, s);
     if (d3 && !run(3, [&] { return launch_ypass(cx, CG, true, s); })) return -1;
     if (!run(4, [&] { return launch_xinv(cx, CG, nullptr, s); })) return -1;
   }
   if (!run(5, [&] { return launch_kapply(cx, CG, cx.d, cx.p, s); })) return -1;
+  n += launch_scalar(cx, RED_DP, CG, s);
   return n;
 }
 
@@ -568,7 +576,7 @@ extern "C" uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, doub
   }
   CK(cudaMemcpyAsync(h->st, h->h_st, g.nrhs * sizeof(LoadState), cudaMemcpyHostToDevice, s));
   const long long work = (long long)g.nrhs * g.c * g.n;
-  const int per_iter = (g.dim == 3 && g.NB == 0) ? 6 : 4;
+  const int per_iter = ((g.dim == 3 && g.NB == 0) ? 6 : 4) + 3;  // passes + 3 scalar kernels
   if (!h->timing) {
     // whole solve device-side: WHILE node over bodies of `chunk` iterations
     const int chunk = work >= (1LL << 22) ? 2 : 4;

@@ -27,6 +27,7 @@ else:
     mat = (synth.lame_from_E_nu(1.0, 0.3), synth.lame_from_E_nu(10.0, 0.2))
     s = UnoCG(ph, "elastic", mat, nrhs=1, seed=1002, amp=0.05)
     loads = np.eye(6)[:1]
+s.kernel_timing(enable=1)  # chunked (non-conditional) graphs: profilable by ncu
 r = s.solve(loads, fixed_iters=a.iters)
 torch.cuda.synchronize()
 print("iters", [x["iterations"] for x in r.reports], "ms", r.ms)
