@@ -623,6 +623,203 @@ __global__ void __launch_bounds__(TX * KT_TY, 3) kp_thermal3d_kernel(Ctx cx, int
   dp_finish(cx, load, nblk, my, part, red_sh, mode);
 }
 
+// Production variant for N1 >= 32: 128 threads own a 32 x 8 node tile, each thread TWO
+// vertically adjacent node columns (rows 2ty, 2ty+1).  The two nodes share 6 of their 8 box
+// sums and conductivities, so a thread reads a 4x3 block of the next plane (12 loads) and
+// 6 conductivities per plane for 2 nodes, and the per-plane bookkeeping (cp.async issue,
+// phase fetch, barrier) is amortised over twice the work.
+template <int TX>
+__global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx cx, int mode,
+                                                                          const double* __restrict__ src,
+                                                                          double* __restrict__ dst, int ZC) {
+  constexpr int T = TX * KT_TY / 2;
+  constexpr int DW = TX + 2, DP = 10 * DW;
+  constexpr int EW = TX + 1, EP = 9 * EW;
+  constexpr int ND = (DP + T - 1) / T, NE = (EP + T - 1) / T;
+  const Geo g = cx.g;
+  const int nzc = g.N3 / ZC;
+  const int load = blockIdx.z / nzc;
+  const int zcI = blockIdx.z - load * nzc;
+  if (mode == CG && !cx.st[load].active) return;
+  extern __shared__ double ksm[];
+  double* D = ksm;                      // [KT_RING][DP]
+  double* KA = D + KT_RING * DP;        // [4][EP]
+  __shared__ double red_sh[32];
+  const int t = threadIdx.x;
+  const int tx = t % TX, ty = t / TX;   // node rows 2ty, 2ty+1 of the tile
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * KT_TY, zs = zcI * ZC;
+  const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
+  const long long plane = (long long)N1 * N2;
+  const double* dv = src + (long long)load * g.n;
+  const double k0 = cx.mat[0][0], k1 = cx.mat[1][0];
+  int goffD[ND], goffE[NE];
+#pragma unroll
+  for (int m = 0; m < ND; ++m) {
+    const int j = t + m * T;
+    const int ly = j / DW, lx = j - ly * DW;
+    goffD[m] = ((y0 - 1 + ly + N2) & (N2 - 1)) * N1 + ((x0 - 1 + lx + N1) & (N1 - 1));
+  }
+#pragma unroll
+  for (int m = 0; m < NE; ++m) {
+    const int j = t + m * T;
+    const int ly = j / EW, lx = j - ly * EW;
+    goffE[m] = ((y0 - 1 + ly + N2) & (N2 - 1)) * N1 + ((x0 - 1 + lx + N1) & (N1 - 1));
+  }
+  auto issue_plane = [&](int p) {
+    const int zw = (p + N3) & (N3 - 1);
+    double* Ds = D + ((p - zs + 1) & (KT_RING - 1)) * DP;
+    const double* base = dv + (long long)zw * plane;
+#pragma unroll
+    for (int m = 0; m < ND; ++m)
+      if (t + m * T < DP) cp_async8(Ds + t + m * T, base + goffD[m]);
+  };
+  unsigned char phv[NE];
+  auto fetch_phase = [&](int layer) {
+    const int zw = (layer + N3) & (N3 - 1);
+    const uint8_t* base = cx.phase + (long long)zw * plane;
+#pragma unroll
+    for (int m = 0; m < NE; ++m) phv[m] = (t + m * T < EP) ? __ldg(base + goffE[m]) : 0;
+  };
+  auto store_kappa = [&](int layer) {
+    double* Ks = KA + ((layer - zs + 1) & 3) * EP;
+#pragma unroll
+    for (int m = 0; m < NE; ++m)
+      if (t + m * T < EP) Ks[t + m * T] = phv[m] ? k1 : k0;
+  };
+  // 4x3 block: tile rows 2ty..2ty+3, cols tx..tx+2 (node columns at tile (tx+1, 2ty+1), (tx+1, 2ty+2))
+  double nb[4][3];
+  auto read4x3 = [&](int p) {
+    const double* Ds = D + ((p - zs + 1) & (KT_RING - 1)) * DP + 2 * ty * DW + tx;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) nb[a][b] = Ds[a * DW + b];
+  };
+  // box sums of the 3 x 2 elements (rows 2ty..2ty+2, cols tx..tx+1 of the element tile)
+  auto box = [&](double Qo[3][2]) {
+    double P[4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      P[a][0] = nb[a][0] + nb[a][1];
+      P[a][1] = nb[a][1] + nb[a][2];
+    }
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+      Qo[e][0] = P[e][0] + P[e + 1][0];
+      Qo[e][1] = P[e][1] + P[e + 1][1];
+    }
+  };
+  auto kap6 = [&](int layer, double a[3][2]) {
+    const double* Kl = KA + ((layer - zs + 1) & 3) * EP + 2 * ty * EW + tx;
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+      a[e][0] = Kl[e * EW];
+      a[e][1] = Kl[e * EW + 1];
+    }
+  };
+#pragma unroll 1
+  for (int p = zs - 1; p <= zs + 3; ++p) {
+    if (p <= zs + ZC) issue_plane(p);
+    cp_commit();
+  }
+  fetch_phase(zs - 1);
+  store_kappa(zs - 1);
+  fetch_phase(zs);
+  cp_wait<3>();
+  __syncthreads();
+  double Qk[3][2], Qn[3][2], kl[3][2];
+  read4x3(zs - 1);
+  box(Qk);
+  double dzm0 = nb[1][1], dzm1 = nb[2][1];
+  read4x3(zs);
+  box(Qn);
+  kap6(zs - 1, kl);
+  // per-node "lo" (layer zs-1) quantities; node 0 uses element rows 0,1 and node 1 rows 1,2
+  double KS[3], KSlo[2], Klo[2], Kxlo[2], Kylo[2];
+#pragma unroll
+  for (int e = 0; e < 3; ++e) KS[e] = fma(kl[e][0], Qk[e][0] + Qn[e][0], kl[e][1] * (Qk[e][1] + Qn[e][1]));
+#pragma unroll
+  for (int m = 0; m < 2; ++m) {
+    KSlo[m] = KS[m] + KS[m + 1];
+    Klo[m] = (kl[m][0] + kl[m][1]) + (kl[m + 1][0] + kl[m + 1][1]);
+    Kxlo[m] = kl[m][1] + kl[m + 1][1];
+    Kylo[m] = kl[m + 1][0] + kl[m + 1][1];
+  }
+#pragma unroll
+  for (int e = 0; e < 3; ++e) {
+    Qk[e][0] = Qn[e][0];
+    Qk[e][1] = Qn[e][1];
+  }
+  // in-plane values of plane zs: rows 0..3, centre column 1 and x neighbours of rows 1,2
+  double c0 = nb[1][1], c1 = nb[2][1], ym = nb[0][1], yp = nb[3][1];
+  double xm0 = nb[1][0], xp0 = nb[1][2], xm1 = nb[2][0], xp1 = nb[2][2];
+  double part = 0.0;
+  const double hc = g.h / 12.0;
+  double* outp = dst + (long long)load * g.n + (long long)(y0 + 2 * ty) * N1 + (x0 + tx);
+#pragma unroll 1
+  for (int k = zs; k < zs + ZC; ++k) {
+    if (k + 4 <= zs + ZC) issue_plane(k + 4);
+    cp_commit();
+    cp_wait<3>();
+    store_kappa(k);
+    if (k + 1 < zs + ZC) fetch_phase(k + 1);
+    __syncthreads();
+    read4x3(k + 1);
+    box(Qn);
+    double a[3][2];
+    kap6(k, a);
+#pragma unroll
+    for (int e = 0; e < 3; ++e) KS[e] = fma(a[e][0], Qk[e][0] + Qn[e][0], a[e][1] * (Qk[e][1] + Qn[e][1]));
+    const double cz0 = nb[1][1], cz1 = nb[2][1];  // plane k+1 centres
+    double pv[2];
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+      const double KShi = KS[m] + KS[m + 1];
+      const double Khi = (a[m][0] + a[m][1]) + (a[m + 1][0] + a[m + 1][1]);
+      const double Kxhi = a[m][1] + a[m + 1][1], Kyhi = a[m + 1][0] + a[m + 1][1];
+      const double Ksum = Klo[m] + Khi;
+      const double Kxp = Kxlo[m] + Kxhi, Kyp = Kylo[m] + Kyhi;
+      const double di = m ? c1 : c0;
+      const double dxp = m ? xp1 : xp0, dxm = m ? xm1 : xm0;
+      const double dyp = m ? yp : c1, dym = m ? c0 : ym;
+      const double dzp = m ? cz1 : cz0, dzm = m ? dzm1 : dzm0;
+      double EE = Kxp * dxp;
+      EE = fma(Ksum - Kxp, dxm, EE);
+      EE = fma(Kyp, dyp, EE);
+      EE = fma(Ksum - Kyp, dym, EE);
+      EE = fma(Khi, dzp, EE);
+      EE = fma(Klo[m], dzm, EE);
+      pv[m] = hc * (fma(5.0 * di, Ksum, EE) - (KSlo[m] + KShi));
+      part = fma(di, pv[m], part);
+      KSlo[m] = KShi;
+      Klo[m] = Khi;
+      Kxlo[m] = Kxhi;
+      Kylo[m] = Kyhi;
+    }
+    outp[(long long)k * plane] = pv[0];
+    outp[(long long)k * plane + N1] = pv[1];
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+      Qk[e][0] = Qn[e][0];
+      Qk[e][1] = Qn[e][1];
+    }
+    dzm0 = c0;
+    dzm1 = c1;
+    c0 = cz0;
+    c1 = cz1;
+    ym = nb[0][1];
+    yp = nb[3][1];
+    xm0 = nb[1][0];
+    xp0 = nb[1][2];
+    xm1 = nb[2][0];
+    xp1 = nb[2][2];
+  }
+  cp_wait<0>();
+  const int nblk = gridDim.x * gridDim.y * nzc;
+  const int my = (zcI * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  dp_finish(cx, load, nblk, my, part, red_sh, mode);
+}
+
 // Same stencil, TMA-style staging for N1 >= 32 (the production path): one warp issues
 // cp.async.bulk row copies (global -> shared, completion counted on an mbarrier per ring slot),
 // so the 256 worker threads spend no instructions on address generation for the halo tile.
@@ -1574,7 +1771,11 @@ int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaS
       const int smb = KB_RING * KB_SLOT;
       set_smem(kp_thermal3d_tma_kernel, smb);
       kp_thermal3d_tma_kernel<<<grid, 256, smb, s>>>(cx, mode, src, dst, ZC);
-    } else if (TX == 32) go(kp_thermal3d_kernel<32>, 256);
+    } else if (TX == 32) {
+      const int sm2 = (KT_RING * 10 * (TX + 2) + 4 * 9 * (TX + 1)) * (int)sizeof(double);
+      set_smem(kp_thermal3d_r2_kernel<32>, sm2);
+      kp_thermal3d_r2_kernel<32><<<grid, 128, sm2, s>>>(cx, mode, src, dst, ZC);
+    }
     else if (TX == 16) go(kp_thermal3d_kernel<16>, 128);
     else go(kp_thermal3d_kernel<8>, 64);
     return 1;

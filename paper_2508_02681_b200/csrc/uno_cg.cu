@@ -266,13 +266,14 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
   g.h = D.h > 0 ? D.h : 1.0 / N1;
   g.C = c * (c + 1) / 2;
   g.NA = g.NB = 0;
-  {  // 3-pass four-step schedule where it applies (UNO_SCHEDULE=5 forces the 5-pass one)
+  {  // transform schedule: 5-pass by default (faster on B200 so far);
+     // UNO_SCHEDULE=3 selects the 3-pass four-step schedule where it applies
     const char* ev = getenv("UNO_SCHEDULE");
-    const bool force5 = ev && ev[0] == '5';
+    const bool want3 = ev && ev[0] == '3';
     Geo t3 = g;
     t3.NB = N2 >= 128 ? 16 : 8;
     t3.NA = N2 / t3.NB;
-    if (!force5 && schedule3_supported(t3)) {
+    if (want3 && schedule3_supported(t3)) {
       g.NB = t3.NB;
       g.NA = t3.NA;
     }
