@@ -628,6 +628,12 @@ __global__ void __launch_bounds__(TX * KT_TY, 3) kp_thermal3d_kernel(Ctx cx, int
 // sums and conductivities, so a thread reads a 4x3 block of the next plane (12 loads) and
 // 6 conductivities per plane for 2 nodes, and the per-plane bookkeeping (cp.async issue,
 // phase fetch, barrier) is amortised over twice the work.
+struct KR2State {   // everything a thread carries from node plane k to k+1 (two node rows)
+  double Qk[3][2];                       // box sums of element rows 0..2 (cols 0,1), plane k
+  double KSlo[2], Klo[2], Kxlo[2], Kylo[2];  // layer k-1 sums for node 0 / node 1
+  double c0, c1, ym, yp, xm0, xp0, xm1, xp1, dzm0, dzm1;  // in-plane values of plane k, centres of k-1
+};
+
 template <int TX>
 __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx cx, int mode,
                                                                           const double* __restrict__ src,
@@ -642,8 +648,8 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
   const int zcI = blockIdx.z - load * nzc;
   if (mode == CG && !cx.st[load].active) return;
   extern __shared__ double ksm[];
-  double* D = ksm;                      // [KT_RING][DP]
-  double* KA = D + KT_RING * DP;        // [4][EP]
+  double* D = ksm;                      // [KT_RING][ND*T] (padded: every thread copies ND elements)
+  double* KA = D + KT_RING * ND * T;    // [4][NE*T]
   __shared__ double red_sh[32];
   const int t = threadIdx.x;
   const int tx = t % TX, ty = t / TX;   // node rows 2ty, 2ty+1 of the tile
@@ -652,50 +658,50 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
   const long long plane = (long long)N1 * N2;
   const double* dv = src + (long long)load * g.n;
   const double k0 = cx.mat[0][0], k1 = cx.mat[1][0];
+  // per-thread copy assignment (indices past the tile are clamped: harmless duplicate copies)
   int goffD[ND], goffE[NE];
+  unsigned sD[ND];
 #pragma unroll
   for (int m = 0; m < ND; ++m) {
-    const int j = t + m * T;
+    const int j = min(t + m * T, DP - 1);
     const int ly = j / DW, lx = j - ly * DW;
     goffD[m] = ((y0 - 1 + ly + N2) & (N2 - 1)) * N1 + ((x0 - 1 + lx + N1) & (N1 - 1));
+    sD[m] = (unsigned)__cvta_generic_to_shared(D + t + m * T);
   }
 #pragma unroll
   for (int m = 0; m < NE; ++m) {
-    const int j = t + m * T;
+    const int j = min(t + m * T, EP - 1);
     const int ly = j / EW, lx = j - ly * EW;
     goffE[m] = ((y0 - 1 + ly + N2) & (N2 - 1)) * N1 + ((x0 - 1 + lx + N1) & (N1 - 1));
   }
+  constexpr unsigned SLOTB = ND * T * 8;  // bytes per D ring slot
   auto issue_plane = [&](int p) {
     const int zw = (p + N3) & (N3 - 1);
-    double* Ds = D + ((p - zs + 1) & (KT_RING - 1)) * DP;
+    const unsigned so = ((p - zs + 1) & (KT_RING - 1)) * SLOTB;
     const double* base = dv + (long long)zw * plane;
 #pragma unroll
     for (int m = 0; m < ND; ++m)
-      if (t + m * T < DP) cp_async8(Ds + t + m * T, base + goffD[m]);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sD[m] + so), "l"(base + goffD[m]) : "memory");
   };
   unsigned char phv[NE];
   auto fetch_phase = [&](int layer) {
-    const int zw = (layer + N3) & (N3 - 1);
-    const uint8_t* base = cx.phase + (long long)zw * plane;
+    const uint8_t* base = cx.phase + (long long)((layer + N3) & (N3 - 1)) * plane;
 #pragma unroll
-    for (int m = 0; m < NE; ++m) phv[m] = (t + m * T < EP) ? __ldg(base + goffE[m]) : 0;
+    for (int m = 0; m < NE; ++m) phv[m] = __ldg(base + goffE[m]);
   };
   auto store_kappa = [&](int layer) {
-    double* Ks = KA + ((layer - zs + 1) & 3) * EP;
+    double* Ks = KA + ((layer - zs + 1) & 3) * (NE * T);
 #pragma unroll
-    for (int m = 0; m < NE; ++m)
-      if (t + m * T < EP) Ks[t + m * T] = phv[m] ? k1 : k0;
+    for (int m = 0; m < NE; ++m) Ks[t + m * T] = phv[m] ? k1 : k0;
   };
-  // 4x3 block: tile rows 2ty..2ty+3, cols tx..tx+2 (node columns at tile (tx+1, 2ty+1), (tx+1, 2ty+2))
   double nb[4][3];
   auto read4x3 = [&](int p) {
-    const double* Ds = D + ((p - zs + 1) & (KT_RING - 1)) * DP + 2 * ty * DW + tx;
+    const double* Ds = D + ((p - zs + 1) & (KT_RING - 1)) * (ND * T) + 2 * ty * DW + tx;
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < 3; ++b) nb[a][b] = Ds[a * DW + b];
   };
-  // box sums of the 3 x 2 elements (rows 2ty..2ty+2, cols tx..tx+1 of the element tile)
   auto box = [&](double Qo[3][2]) {
     double P[4][2];
 #pragma unroll
@@ -710,7 +716,7 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
     }
   };
   auto kap6 = [&](int layer, double a[3][2]) {
-    const double* Kl = KA + ((layer - zs + 1) & 3) * EP + 2 * ty * EW + tx;
+    const double* Kl = KA + ((layer - zs + 1) & 3) * (NE * T) + 2 * ty * EW + tx;
 #pragma unroll
     for (int e = 0; e < 3; ++e) {
       a[e][0] = Kl[e * EW];
@@ -727,37 +733,45 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
   fetch_phase(zs);
   cp_wait<3>();
   __syncthreads();
-  double Qk[3][2], Qn[3][2], kl[3][2];
-  read4x3(zs - 1);
-  box(Qk);
-  double dzm0 = nb[1][1], dzm1 = nb[2][1];
-  read4x3(zs);
-  box(Qn);
-  kap6(zs - 1, kl);
-  // per-node "lo" (layer zs-1) quantities; node 0 uses element rows 0,1 and node 1 rows 1,2
-  double KS[3], KSlo[2], Klo[2], Kxlo[2], Kylo[2];
+  KR2State A, B;
+  {
+    double Qn[3][2], kl[3][2];
+    read4x3(zs - 1);
+    box(A.Qk);
+    A.dzm0 = nb[1][1];
+    A.dzm1 = nb[2][1];
+    read4x3(zs);
+    box(Qn);
+    kap6(zs - 1, kl);
+    double KS[3];
 #pragma unroll
-  for (int e = 0; e < 3; ++e) KS[e] = fma(kl[e][0], Qk[e][0] + Qn[e][0], kl[e][1] * (Qk[e][1] + Qn[e][1]));
+    for (int e = 0; e < 3; ++e) KS[e] = fma(kl[e][0], A.Qk[e][0] + Qn[e][0], kl[e][1] * (A.Qk[e][1] + Qn[e][1]));
 #pragma unroll
-  for (int m = 0; m < 2; ++m) {
-    KSlo[m] = KS[m] + KS[m + 1];
-    Klo[m] = (kl[m][0] + kl[m][1]) + (kl[m + 1][0] + kl[m + 1][1]);
-    Kxlo[m] = kl[m][1] + kl[m + 1][1];
-    Kylo[m] = kl[m + 1][0] + kl[m + 1][1];
+    for (int m = 0; m < 2; ++m) {
+      A.KSlo[m] = KS[m] + KS[m + 1];
+      A.Klo[m] = (kl[m][0] + kl[m][1]) + (kl[m + 1][0] + kl[m + 1][1]);
+      A.Kxlo[m] = kl[m][1] + kl[m + 1][1];
+      A.Kylo[m] = kl[m + 1][0] + kl[m + 1][1];
+    }
+#pragma unroll
+    for (int e = 0; e < 3; ++e) {
+      A.Qk[e][0] = Qn[e][0];
+      A.Qk[e][1] = Qn[e][1];
+    }
+    A.c0 = nb[1][1];
+    A.c1 = nb[2][1];
+    A.ym = nb[0][1];
+    A.yp = nb[3][1];
+    A.xm0 = nb[1][0];
+    A.xp0 = nb[1][2];
+    A.xm1 = nb[2][0];
+    A.xp1 = nb[2][2];
   }
-#pragma unroll
-  for (int e = 0; e < 3; ++e) {
-    Qk[e][0] = Qn[e][0];
-    Qk[e][1] = Qn[e][1];
-  }
-  // in-plane values of plane zs: rows 0..3, centre column 1 and x neighbours of rows 1,2
-  double c0 = nb[1][1], c1 = nb[2][1], ym = nb[0][1], yp = nb[3][1];
-  double xm0 = nb[1][0], xp0 = nb[1][2], xm1 = nb[2][0], xp1 = nb[2][2];
   double part = 0.0;
-  const double hc = g.h / 12.0;
+  const double hc = g.h * (1.0 / 12.0);
   double* outp = dst + (long long)load * g.n + (long long)(y0 + 2 * ty) * N1 + (x0 + tx);
-#pragma unroll 1
-  for (int k = zs; k < zs + ZC; ++k) {
+  // one node plane: reads state `I`, writes the carried state for plane k+1 into `O`
+  auto step = [&](int k, const KR2State& I, KR2State& O) {
     if (k + 4 <= zs + ZC) issue_plane(k + 4);
     cp_commit();
     cp_wait<3>();
@@ -765,55 +779,56 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
     if (k + 1 < zs + ZC) fetch_phase(k + 1);
     __syncthreads();
     read4x3(k + 1);
-    box(Qn);
+    box(O.Qk);
     double a[3][2];
     kap6(k, a);
+    double KS[3];
 #pragma unroll
-    for (int e = 0; e < 3; ++e) KS[e] = fma(a[e][0], Qk[e][0] + Qn[e][0], a[e][1] * (Qk[e][1] + Qn[e][1]));
+    for (int e = 0; e < 3; ++e) KS[e] = fma(a[e][0], I.Qk[e][0] + O.Qk[e][0], a[e][1] * (I.Qk[e][1] + O.Qk[e][1]));
     const double cz0 = nb[1][1], cz1 = nb[2][1];  // plane k+1 centres
-    double pv[2];
 #pragma unroll
     for (int m = 0; m < 2; ++m) {
       const double KShi = KS[m] + KS[m + 1];
       const double Khi = (a[m][0] + a[m][1]) + (a[m + 1][0] + a[m + 1][1]);
       const double Kxhi = a[m][1] + a[m + 1][1], Kyhi = a[m + 1][0] + a[m + 1][1];
-      const double Ksum = Klo[m] + Khi;
-      const double Kxp = Kxlo[m] + Kxhi, Kyp = Kylo[m] + Kyhi;
-      const double di = m ? c1 : c0;
-      const double dxp = m ? xp1 : xp0, dxm = m ? xm1 : xm0;
-      const double dyp = m ? yp : c1, dym = m ? c0 : ym;
-      const double dzp = m ? cz1 : cz0, dzm = m ? dzm1 : dzm0;
+      const double Ksum = I.Klo[m] + Khi;
+      const double Kxp = I.Kxlo[m] + Kxhi, Kyp = I.Kylo[m] + Kyhi;
+      const double di = m ? I.c1 : I.c0;
+      const double dxp = m ? I.xp1 : I.xp0, dxm = m ? I.xm1 : I.xm0;
+      const double dyp = m ? I.yp : I.c1, dym = m ? I.c0 : I.ym;
+      const double dzp = m ? cz1 : cz0, dzm = m ? I.dzm1 : I.dzm0;
       double EE = Kxp * dxp;
       EE = fma(Ksum - Kxp, dxm, EE);
       EE = fma(Kyp, dyp, EE);
       EE = fma(Ksum - Kyp, dym, EE);
       EE = fma(Khi, dzp, EE);
-      EE = fma(Klo[m], dzm, EE);
-      pv[m] = hc * (fma(5.0 * di, Ksum, EE) - (KSlo[m] + KShi));
-      part = fma(di, pv[m], part);
-      KSlo[m] = KShi;
-      Klo[m] = Khi;
-      Kxlo[m] = Kxhi;
-      Kylo[m] = Kyhi;
+      EE = fma(I.Klo[m], dzm, EE);
+      const double pv = hc * (fma(5.0 * di, Ksum, EE) - (I.KSlo[m] + KShi));
+      outp[(long long)k * plane + m * N1] = pv;
+      part = fma(di, pv, part);
+      O.KSlo[m] = KShi;
+      O.Klo[m] = Khi;
+      O.Kxlo[m] = Kxhi;
+      O.Kylo[m] = Kyhi;
     }
-    outp[(long long)k * plane] = pv[0];
-    outp[(long long)k * plane + N1] = pv[1];
-#pragma unroll
-    for (int e = 0; e < 3; ++e) {
-      Qk[e][0] = Qn[e][0];
-      Qk[e][1] = Qn[e][1];
-    }
-    dzm0 = c0;
-    dzm1 = c1;
-    c0 = cz0;
-    c1 = cz1;
-    ym = nb[0][1];
-    yp = nb[3][1];
-    xm0 = nb[1][0];
-    xp0 = nb[1][2];
-    xm1 = nb[2][0];
-    xp1 = nb[2][2];
+    O.dzm0 = I.c0;
+    O.dzm1 = I.c1;
+    O.c0 = cz0;
+    O.c1 = cz1;
+    O.ym = nb[0][1];
+    O.yp = nb[3][1];
+    O.xm0 = nb[1][0];
+    O.xp0 = nb[1][2];
+    O.xm1 = nb[2][0];
+    O.xp1 = nb[2][2];
+  };
+  int k = zs;
+#pragma unroll 1
+  for (; k + 1 < zs + ZC; k += 2) {  // unrolled by two: the carried state ping-pongs A <-> B
+    step(k, A, B);
+    step(k + 1, B, A);
   }
+  if (k < zs + ZC) step(k, A, B);
   cp_wait<0>();
   const int nblk = gridDim.x * gridDim.y * nzc;
   const int my = (zcI * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
@@ -1772,7 +1787,8 @@ int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaS
       set_smem(kp_thermal3d_tma_kernel, smb);
       kp_thermal3d_tma_kernel<<<grid, 256, smb, s>>>(cx, mode, src, dst, ZC);
     } else if (TX == 32) {
-      const int sm2 = (KT_RING * 10 * (TX + 2) + 4 * 9 * (TX + 1)) * (int)sizeof(double);
+      constexpr int T2 = 128, ND2 = (10 * 34 + T2 - 1) / T2, NE2 = (9 * 33 + T2 - 1) / T2;
+      const int sm2 = (KT_RING * ND2 * T2 + 4 * NE2 * T2) * (int)sizeof(double);
       set_smem(kp_thermal3d_r2_kernel<32>, sm2);
       kp_thermal3d_r2_kernel<32><<<grid, 128, sm2, s>>>(cx, mode, src, dst, ZC);
     }
