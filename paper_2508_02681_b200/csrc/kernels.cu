@@ -649,7 +649,9 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
   if (mode == CG && !cx.st[load].active) return;
   extern __shared__ double ksm[];
   double* D = ksm;                      // [KT_RING][ND*T] (padded: every thread copies ND elements)
-  double* KA = D + KT_RING * ND * T;    // [4][NE*T]
+  // phase bytes of element layer p-1 travel with node plane p: 9 rows x 36 bytes (x0-4 .. x0+31)
+  unsigned char* PH = reinterpret_cast<unsigned char*>(D + KT_RING * ND * T);  // [KT_RING][9*36]
+  constexpr int PHS = 9 * 36;
   __shared__ double red_sh[32];
   const int t = threadIdx.x;
   const int tx = t % TX, ty = t / TX;   // node rows 2ty, 2ty+1 of the tile
@@ -659,7 +661,7 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
   const double* dv = src + (long long)load * g.n;
   const double k0 = cx.mat[0][0], k1 = cx.mat[1][0];
   // per-thread copy assignment (indices past the tile are clamped: harmless duplicate copies)
-  int goffD[ND], goffE[NE];
+  int goffD[ND];
   unsigned sD[ND];
 #pragma unroll
   for (int m = 0; m < ND; ++m) {
@@ -668,31 +670,24 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
     goffD[m] = ((y0 - 1 + ly + N2) & (N2 - 1)) * N1 + ((x0 - 1 + lx + N1) & (N1 - 1));
     sD[m] = (unsigned)__cvta_generic_to_shared(D + t + m * T);
   }
-#pragma unroll
-  for (int m = 0; m < NE; ++m) {
-    const int j = min(t + m * T, EP - 1);
-    const int ly = j / EW, lx = j - ly * EW;
-    goffE[m] = ((y0 - 1 + ly + N2) & (N2 - 1)) * N1 + ((x0 - 1 + lx + N1) & (N1 - 1));
-  }
+  // phase words: thread t < 81 copies 4 bytes of row t/9, word t%9
+  const bool phw = t < 81;
+  const int pj = phw ? t : 0;
+  const int poff = ((y0 - 1 + pj / 9 + N2) & (N2 - 1)) * N1 + ((x0 - 4 + 4 * (pj % 9) + N1) & (N1 - 1));
+  const unsigned psm = (unsigned)__cvta_generic_to_shared(PH + 4 * pj);
   constexpr unsigned SLOTB = ND * T * 8;  // bytes per D ring slot
-  auto issue_plane = [&](int p) {
+  auto issue_plane = [&](int p) {  // node plane p of d and phase layer p-1 -> ring slot
     const int zw = (p + N3) & (N3 - 1);
-    const unsigned so = ((p - zs + 1) & (KT_RING - 1)) * SLOTB;
+    const unsigned slot = (p - zs + 1) & (KT_RING - 1);
+    const unsigned so = slot * SLOTB;
     const double* base = dv + (long long)zw * plane;
 #pragma unroll
     for (int m = 0; m < ND; ++m)
       asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sD[m] + so), "l"(base + goffD[m]) : "memory");
-  };
-  unsigned char phv[NE];
-  auto fetch_phase = [&](int layer) {
-    const uint8_t* base = cx.phase + (long long)((layer + N3) & (N3 - 1)) * plane;
-#pragma unroll
-    for (int m = 0; m < NE; ++m) phv[m] = __ldg(base + goffE[m]);
-  };
-  auto store_kappa = [&](int layer) {
-    double* Ks = KA + ((layer - zs + 1) & 3) * (NE * T);
-#pragma unroll
-    for (int m = 0; m < NE; ++m) Ks[t + m * T] = phv[m] ? k1 : k0;
+    if (phw) {
+      const uint8_t* pb = cx.phase + (long long)((p - 1 + N3) & (N3 - 1)) * plane + poff;
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(psm + slot * PHS), "l"(pb) : "memory");
+    }
   };
   double nb[4][3];
   auto read4x3 = [&](int p) {
@@ -715,12 +710,12 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
       Qo[e][1] = P[e][1] + P[e + 1][1];
     }
   };
-  auto kap6 = [&](int layer, double a[3][2]) {
-    const double* Kl = KA + ((layer - zs + 1) & 3) * (NE * T) + 2 * ty * EW + tx;
+  auto kap6 = [&](int layer, double a[3][2]) {  // layer travels with plane layer+1
+    const unsigned char* Pl = PH + ((layer + 1 - zs + 1) & (KT_RING - 1)) * PHS + 2 * ty * 36 + tx + 3;
 #pragma unroll
     for (int e = 0; e < 3; ++e) {
-      a[e][0] = Kl[e * EW];
-      a[e][1] = Kl[e * EW + 1];
+      a[e][0] = Pl[e * 36] ? k1 : k0;
+      a[e][1] = Pl[e * 36 + 1] ? k1 : k0;
     }
   };
 #pragma unroll 1
@@ -728,9 +723,6 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
     if (p <= zs + ZC) issue_plane(p);
     cp_commit();
   }
-  fetch_phase(zs - 1);
-  store_kappa(zs - 1);
-  fetch_phase(zs);
   cp_wait<3>();
   __syncthreads();
   KR2State A, B;
@@ -775,8 +767,6 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
     if (k + 4 <= zs + ZC) issue_plane(k + 4);
     cp_commit();
     cp_wait<3>();
-    store_kappa(k);
-    if (k + 1 < zs + ZC) fetch_phase(k + 1);
     __syncthreads();
     read4x3(k + 1);
     box(O.Qk);
@@ -1787,8 +1777,8 @@ int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaS
       set_smem(kp_thermal3d_tma_kernel, smb);
       kp_thermal3d_tma_kernel<<<grid, 256, smb, s>>>(cx, mode, src, dst, ZC);
     } else if (TX == 32) {
-      constexpr int T2 = 128, ND2 = (10 * 34 + T2 - 1) / T2, NE2 = (9 * 33 + T2 - 1) / T2;
-      const int sm2 = (KT_RING * ND2 * T2 + 4 * NE2 * T2) * (int)sizeof(double);
+      constexpr int T2 = 128, ND2 = (10 * 34 + T2 - 1) / T2;
+      const int sm2 = KT_RING * ND2 * T2 * (int)sizeof(double) + KT_RING * 9 * 36;
       set_smem(kp_thermal3d_r2_kernel<32>, sm2);
       kp_thermal3d_r2_kernel<32><<<grid, 128, sm2, s>>>(cx, mode, src, dst, ZC);
     }
