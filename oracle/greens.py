@@ -194,3 +194,94 @@ def eq55_check(G: np.ndarray, eps: float = 1e-14):
     ev = np.linalg.eigvalsh(B)
     lo, hi = float(ev.min()), float(ev.max())
     return lo > eps, lo, hi
+
+
+# --------------------------------------------------------------------------------------------
+# Mixed BC: Dirichlet on z.  A_r is circulant in x, y and tridiagonal Toeplitz
+# (3-point) in z.  Probing an interior impulse gives the z-coupling coefficients a_{-1}, a_0, a_1
+# (c x c, after the DFT in x, y); the DST-I basis diagonalises the symmetric part, so the
+# diagonal block of U K_r U^H is  a_0 + (a_1 + a_{-1}) cos(pi m / N3),  m = 1..N3-1.
+# Thermal: that block is the exact symbol (K_r fully diagonalised); elastic: the odd x-z / y-z
+# couplings leave the diagonal block (reading A13).
+# --------------------------------------------------------------------------------------------
+
+def symbol_probe_mixed(g: fem.Grid, physics: str, ref) -> np.ndarray:
+    assert g.d == 3 and g.bc == (0, 0, 1), "mixed reading: periodic x, y; Dirichlet z"
+    c = g.c
+    nz, ny, nx = g.node_shape  # nz = N3 - 1
+    assert nz >= 3
+    z0 = nz // 2
+    phase0 = np.zeros(g.elem_shape, dtype=np.uint8)
+    mat = (ref, ref)
+    coef = np.zeros((3, c, c, ny, nx), dtype=complex)  # dz = -1, 0, +1
+    for b in range(c):
+        delta = np.zeros((c,) + g.node_shape)
+        delta[b, z0, 0, 0] = 1.0
+        col = fem.apply_K(g, physics, phase0, mat, delta)
+        for a in range(c):
+            for i, dz in enumerate((-1, 0, 1)):
+                coef[i, a, b] = np.fft.fft2(col[a, z0 + dz])
+    am, a0, ap = coef.real  # imaginary parts are round-off (symmetric stencils)
+    m = np.arange(1, nz + 1)
+    cz = np.cos(np.pi * m / (nz + 1))
+    A = a0[:, :, None] + (ap + am)[:, :, None] * cz[None, None, :, None, None]
+    # symmetrise exactly: A(-kx,-ky) = A(kx,ky) and A^T = A
+    Am = np.roll(np.flip(np.roll(np.flip(A, axis=-1), 1, axis=-1), axis=-2), 1, axis=-2)
+    A = 0.5 * (A + Am)
+    A = 0.5 * (A + np.swapaxes(A, 0, 1))
+    return A  # (c, c, nz, ny, nx)
+
+
+def canon_index_mixed(shape) -> np.ndarray:
+    """Pairs {k, -k} over the Fourier axes only (sine modes are self-conjugate): flat index
+    (p N2 + ky) N1 + kx with p = m - 1 the sine-mode plane, minimised over (kx, ky) -> (-kx, -ky)."""
+    nz, ny, nx = shape
+    P, Y, X = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    flat = (P * ny + Y) * nx + X
+    flatn = (P * ny + (-Y) % ny) * nx + (-X) % nx
+    return np.minimum(flat, flatn)
+
+
+def ghat_mixed(g: fem.Grid, physics: str, mat, seed: int, amp: float, ref=None) -> np.ndarray:
+    if ref is None:
+        ref = reference_medium(physics, mat)
+    A = symbol_probe_mixed(g, physics, ref)
+    c = g.c
+    shp = g.node_shape
+    can = canon_index_mixed(shp)
+    if c == 1:
+        rho = (1.0 - amp + 2.0 * amp * u01(seed, 2, can.astype(np.uint64))) if seed else np.ones(shp)
+        return (rho / A[0, 0])[None, None]
+    Am = np.moveaxis(A.reshape(c, c, -1), -1, 0)
+    Phi = np.linalg.inv(Am)
+    Phi = 0.5 * (Phi + np.transpose(Phi, (0, 2, 1)))
+    if seed:
+        base = (8 * can.reshape(-1)).astype(np.uint64)
+        th = np.stack([u01(seed, 2, base + np.uint64(t)) for t in range(6)])
+        for t in (0, 1, 3):
+            th[t] = 0.5 + 0.5 * th[t]
+        for t in (2, 4, 5):
+            th[t] = th[t] - 0.5
+        P = np.moveaxis(psi3(th), -1, 0)
+        tr = np.trace(Phi, axis1=1, axis2=2) / 3.0
+        Phi = Phi + amp * tr[:, None, None] * P
+    return np.moveaxis(Phi, 0, -1).reshape((c, c) + shp)
+
+
+def apply_precond_mixed(G: np.ndarray, r: np.ndarray) -> np.ndarray:
+    """s = U^H Q U r with U = F_x (x) F_y (x) DST-I_z (Eq 48 with the mixed transform)."""
+    rh = transform.forward_mixed(r)
+    Gh = half(G)
+    sh = np.einsum("ab...,b...->a...", Gh, rh)
+    return transform.inverse_mixed(sh, r.shape[1:])
+
+
+def dense_P_mixed(G: np.ndarray, spatial_shape) -> np.ndarray:
+    c = G.shape[0]
+    n = int(np.prod(spatial_shape))
+    T = transform.dense_T_mixed(spatial_shape)
+    P = np.zeros((c * n, c * n), dtype=complex)
+    for a in range(c):
+        for b in range(c):
+            P[a * n:(a + 1) * n, b * n:(b + 1) * n] = T.conj().T @ (G[a, b].reshape(-1)[:, None] * T)
+    return P.real

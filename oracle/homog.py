@@ -127,12 +127,13 @@ def solve_problem(g: fem.Grid, physics: str, phase, mat, loads, seed: int, amp: 
                   tol: float = 1e-8, max_iter: int = 10000, fixed_iters: int = 0):
     """Full oracle pipeline for one problem: RHS (a1), G_hat (a0), Alg 2 (a2-a8), mean
     removal and effective property (a9).  Returns dict with per-load results."""
-    G = greens.ghat(g, physics, mat, seed, amp)
+    mixed = g.bc == (0, 0, 1)
+    G = greens.ghat_mixed(g, physics, mat, seed, amp) if mixed else greens.ghat(g, physics, mat, seed, amp)
+    applyP = (lambda v: greens.apply_precond_mixed(G, v)) if mixed else (lambda v: greens.apply_precond(G, v))
     F, U, its, results = [], [], [], []
     for ld in loads:
         f = fem.rhs(g, physics, phase, mat, ld)
-        res = pcg.pcg(lambda v: fem.apply_K(g, physics, phase, mat, v),
-                      lambda v: greens.apply_precond(G, v), f, tol=tol, max_iter=max_iter,
+        res = pcg.pcg(lambda v: fem.apply_K(g, physics, phase, mat, v), applyP, f, tol=tol, max_iter=max_iter,
                       fixed_iters=fixed_iters, zero_floor=zero_rhs_floor(g, physics, mat, ld))
         u = pcg.remove_mean(res.u) if all(b == 0 for b in g.bc) else res.u
         F.append(f)

@@ -49,3 +49,37 @@ def parseval_weights(spatial_shape) -> np.ndarray:
     if n1 % 2 == 0:
         w[-1] = 1.0
     return np.broadcast_to(w, tuple(spatial_shape[:-1]) + (h,))
+
+
+# --------------------------------------------------------------------------------------------
+# Mixed BC (Table 1 row "Mixed"; 3D generalisation SPEC S:250): DFT on periodic axes,
+# orthonormal DST-I on Dirichlet axes (DST variant fixed by SPEC S:249).
+# --------------------------------------------------------------------------------------------
+
+def dst1_matrix(nm1: int) -> np.ndarray:
+    """Orthonormal DST-I of length N-1 (N = nm1 + 1): S[m, j] = sqrt(2/N) sin(pi m j / N),
+    m, j = 1..N-1 (written out; symmetric and self-inverse)."""
+    N = nm1 + 1
+    m = np.arange(1, N)[:, None]
+    j = np.arange(1, N)[None, :]
+    return np.sqrt(2.0 / N) * np.sin(np.pi * m * j / N)
+
+
+def forward_mixed(r: np.ndarray) -> np.ndarray:
+    """r_hat = (F_x (x) F_y (x) S_z) r for fields (c, N3-1, N2, N1): DST-I along z (numpy axis 1),
+    then the orthonormal R2C DFT over (y, x)."""
+    from scipy.fft import dst
+    rz = dst(r, type=1, axis=1, norm="ortho")
+    return np.fft.rfftn(rz, axes=(2, 3), norm="ortho")
+
+
+def inverse_mixed(rh: np.ndarray, spatial_shape) -> np.ndarray:
+    from scipy.fft import idst
+    r = np.fft.irfftn(rh, s=spatial_shape[1:], axes=(2, 3), norm="ortho")
+    return idst(r, type=1, axis=1, norm="ortho")
+
+
+def dense_T_mixed(spatial_shape) -> np.ndarray:
+    """Unitary F_x (x) F_y (x) S_z for C-order (z, y, x) flattened fields with z Dirichlet."""
+    nz, ny, nx = spatial_shape
+    return np.kron(np.kron(dst1_matrix(nz).astype(complex), dft_matrix(ny)), dft_matrix(nx))
