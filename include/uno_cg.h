@@ -17,10 +17,13 @@
  * -----------------------
  *  - fp64 everywhere; phase fields are uint8 (0 = matrix, 1 = inclusion, §5).
  *  - Grid: N1 (x, fastest) x N2 (y) x N3 (z) voxels, N3 = 1 in 2D; cubic voxels of
- *    edge h.  Periodic boundaries on every axis (bc[] must be 0 in this version;
- *    Dirichlet/mixed axes return UNO_ERR_UNSUPPORTED).  N1, N2 in {8..1024},
- *    N3 in {1} U {4..1024}, all powers of two.
- *  - Field layout (device): component-planar C order [nrhs][c][N3][N2][N1]; node
+ *    edge h.  Boundary conditions: periodic on every axis, or (3D) the mixed case of
+ *    Eq 82 / §6.4 with periodic x, y and Dirichlet faces on z (bc = {0,0,1}; U = DFT_x (x)
+ *    DFT_y (x) DST-I_z, Table 1 "Mixed" P:452; node planes z = 1..N3-1 are the unknowns,
+ *    N1 >= 32, N3 <= 512).  Other combinations return UNO_ERR_UNSUPPORTED.
+ *    N1, N2 in {8..1024}, N3 in {1} U {4..1024}, all powers of two.
+ *  - Field layout (device): component-planar C order [nrhs][c][P3][N2][N1] with P3 = N3
+ *    (periodic) or N3 - 1 (Dirichlet z: stored planes are nodes z = 1..N3-1); node
  *    (i,j,k) at h*(i,j,k); voxel (i,j,k) has corners (i+a1, j+a2, k+a3) mod N.
  *    The paper's interleaved vec() (§1.6 Eq 1) is a fixed permutation of this.
  *  - c = 1 (thermal) or c = dim (elastic).  nrhs load cases are iterated together,
@@ -75,7 +78,7 @@ typedef struct {
   int32_t n[3];       /* voxel counts N1, N2, N3 (N3 = 1 when dim == 2)                  */
   double h;           /* voxel edge; <= 0 means 1/N1 (unit cell)              */
   int32_t physics;    /* UNO_THERMAL (c = 1) or UNO_ELASTIC (c = dim)                    */
-  int32_t bc[3];      /* per axis: 0 periodic (only value accepted in this version)      */
+  int32_t bc[3];      /* per axis: 0 periodic, 1 Dirichlet ({0,0,0} or {0,0,1} accepted)   */
   double mat[2][2];   /* phase 0 / phase 1: thermal {kappa, unused}; elastic {lambda, mu} */
   double ref[2];      /* reference medium (kappa_r | lambda_r, mu_r); ref[0] <= 0 means the
                          arithmetic mean of the phases          */

@@ -27,7 +27,7 @@ class SolveResult:
 
 class UnoCG:
     def __init__(self, phase: torch.Tensor, physics: str, mat, nrhs: int, seed: int = 0, amp: float | None = None,
-                 h: float = 0.0, ref=None, stream: torch.cuda.Stream | None = None):
+                 h: float = 0.0, ref=None, stream: torch.cuda.Stream | None = None, bc=(0, 0, 0)):
         assert phase.is_cuda and phase.dtype == torch.uint8 and phase.is_contiguous()
         self.phase = phase
         self.dim = phase.dim()
@@ -43,6 +43,9 @@ class UnoCG:
         d.n[2] = self.N[2] if self.dim == 3 else 1
         d.h = float(h)
         d.physics = B.UNO_THERMAL if physics == "thermal" else B.UNO_ELASTIC
+        for i, b in enumerate(tuple(bc)[: self.dim]):
+            d.bc[i] = int(b)
+        self.bc = tuple(bc)
         if physics == "thermal":
             d.mat[0][0], d.mat[1][0] = float(mat[0]), float(mat[1])
         else:
@@ -57,7 +60,8 @@ class UnoCG:
         d.stream = self.stream.cuda_stream
         self.desc = d
         self.handle = B.uno_cg_create(d, phase)
-        self.field_shape = (nrhs, self.c) + shp
+        nshp = (shp[0] - 1,) + shp[1:] if (self.dim == 3 and self.bc[2] == 1) else shp  # Dirichlet z: interior planes
+        self.field_shape = (nrhs, self.c) + nshp
 
     def update(self, phase: torch.Tensor, mat, seed: int | None = None, amp: float | None = None, ref=None):
         """Re-target this solver to another microstructure/material set of the same grid (a0 only)."""

@@ -19,6 +19,8 @@ struct Geo {
   double h;             // voxel edge
   int C;                // unique symbol entries per bin: c(c+1)/2 (Eq 51)
   int NA, NB;           // 3-pass (four-step) schedule: N2 = NA*NB, y = y_a + NA*y_b; NB = 0 -> 5-pass
+  int dirz;             // 1: Dirichlet on z (mixed BC; DST-I along z), node planes 1..N3-1 stored
+  int P3;               // stored node planes along z: N3 (periodic) or N3 - 1 (dirz); 1 in 2D
 };
 
 // Per-load CG state (device resident; Alg 2 scalars).

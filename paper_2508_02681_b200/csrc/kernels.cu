@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(fft_threads(M)) xfwd_kernel(Ctx cx, const doub
   const Geo g = cx.g;
   const int load = blockIdx.y;
   LoadState* st = cx.st + load;
-  if (MODE == CG && !st->active) return;
+  if (MODE != STANDALONE && !st->active) return;
   extern __shared__ double2 smem[];
   double2* tile = smem;
   double2* pbuf = smem + 8 * M;
@@ -95,10 +95,10 @@ __global__ void __launch_bounds__(fft_threads(M)) xfwd_kernel(Ctx cx, const doub
 
   const int y0 = (int)(row0 % g.N2);
   const long long zc = row0 / g.N2;
-  const int z = (int)(zc % g.N3);
-  const int comp = (int)(zc / g.N3);
+  const int z = (int)(zc % g.P3);
+  const int comp = (int)(zc / g.P3);
   double2* out = cx.spec + ((long long)load * g.c + comp) * g.nspec + (long long)z * g.N2 + y0;
-  const long long plane = (long long)g.N3 * g.N2;
+  const long long plane = (long long)g.P3 * g.N2;
 #pragma unroll
   for (int i = 0; i < ((M / 2 + 1) * 8 + T - 1) / T; ++i) {
     const int it = t + i * T;
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(fft_threads(M)) xinv_kernel(Ctx cx, double* __
   const Geo g = cx.g;
   const int load = blockIdx.y;
   LoadState* st = cx.st + load;
-  if (MODE == CG && !st->active) return;
+  if (MODE != STANDALONE && !st->active) return;
   extern __shared__ double2 smem[];
   double2* tile = smem;
   double2* stage = smem + 8 * M;   // [M+1][8] spectrum rows, later d rows [8M] | u rows [8M]
@@ -132,10 +132,10 @@ __global__ void __launch_bounds__(fft_threads(M)) xinv_kernel(Ctx cx, double* __
   const long long row0 = (long long)blockIdx.x * 8;
   const int y0 = (int)(row0 % g.N2);
   const long long zc = row0 / g.N2;
-  const int z = (int)(zc % g.N3);
-  const int comp = (int)(zc / g.N3);
+  const int z = (int)(zc % g.P3);
+  const int comp = (int)(zc / g.P3);
   const double2* in = cx.spec + ((long long)load * g.c + comp) * g.nspec + (long long)z * g.N2 + y0;
-  const long long plane = (long long)g.N3 * g.N2;
+  const long long plane = (long long)g.P3 * g.N2;
 #pragma unroll
   for (int i = 0; i < ((M + 1) * 8 + T - 1) / T; ++i) {
     const int e = t + i * T;
@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(fft_threads(M)) xinv_kernel(Ctx cx, double* __
     cp_commit();
   }
   fft_tile<M, true>(tile, tw);
-  if (MODE == STANDALONE) {
+  if (MODE != CG) {
     double2* o2 = reinterpret_cast<double2*>(dst + voff);
 #pragma unroll
     for (int i = 0; i < (8 * M + T - 1) / T; ++i) {
@@ -363,11 +363,12 @@ __global__ void __launch_bounds__(fft_threads(L)) gpass_z_kernel(Ctx cx) {
   gamma_finish(cx, load, part, red_sh, MODE);
 }
 
-// 2D G pass: sequences along y (contiguous), tile = 8 consecutive kx rows.
+// G pass along y (contiguous rows): 2D grids (rows = kx) and the mixed-BC schedule (rows = (kx, m),
+// m the DST-I mode along z, P3 planes); tile = 8 consecutive rows.
 template <int L, int NC, int MODE>
 __global__ void __launch_bounds__(fft_threads(L)) gpass_y2d_kernel(Ctx cx) {
   constexpr int T = fft_threads(L);
-  constexpr int NCC = NC == 1 ? 1 : 3;
+  constexpr int NCC = NC == 1 ? 1 : (NC == 2 ? 3 : 6);
   const Geo g = cx.g;
   const int load = blockIdx.y;
   if (MODE == CG && !cx.st[load].active) return;
@@ -379,28 +380,33 @@ __global__ void __launch_bounds__(fft_threads(L)) gpass_y2d_kernel(Ctx cx) {
   double* gs = reinterpret_cast<double*>(tw + L);  // [NCC][8 rows][L]
   __shared__ double red_sh[32];
   const int t = threadIdx.x;
-  const int kx0 = blockIdx.x * 8;
+  const int row0 = blockIdx.x * 8;
+  const int nrows = g.H1 * g.P3;
 #pragma unroll
   for (int q = 0; q < NC; ++q) {
-    const double2* base = cx.spec + ((long long)load * g.c + q) * g.nspec + (long long)kx0 * L;
+    const double2* base = cx.spec + ((long long)load * g.c + q) * g.nspec + (long long)row0 * L;
 #pragma unroll
     for (int i = 0; i < (8 * L + T - 1) / T; ++i) {
       const int e = t + i * T;
       if (e < 8 * L) {
         const int row = e / L, j = e & (L - 1);
-        if (kx0 + row < g.H1)
+        if (row0 + row < nrows)
           cp_async16(&tiles[q][tidx(j, row)], base + e);
         else
           tiles[q][tidx(j, row)] = make_double2(0.0, 0.0);
       }
     }
   }
+  constexpr bool STG = gstaged<L, NC>();
+  if (STG) {
 #pragma unroll
-  for (int q = 0; q < NCC; ++q) {
+    for (int q = 0; q < NCC; ++q) {
 #pragma unroll
-    for (int i = 0; i < (8 * L + T - 1) / T; ++i) {
-      const int e = t + i * T;
-      if (e < 8 * L && kx0 + e / L < g.H1) cp_async8(&gs[q * 8 * L + e], cx.gtab + q * g.nspec + (long long)kx0 * L + e);
+      for (int i = 0; i < (8 * L + T - 1) / T; ++i) {
+        const int e = t + i * T;
+        if (e < 8 * L && row0 + e / L < nrows)
+          cp_async8(&gs[q * 8 * L + e], cx.gtab + q * g.nspec + (long long)row0 * L + e);
+      }
     }
   }
   cp_commit();
@@ -415,8 +421,13 @@ __global__ void __launch_bounds__(fft_threads(L)) gpass_y2d_kernel(Ctx cx) {
     const int e = t + i * T;
     if (e < 8 * L) {
       const int row = e & 7, j = e >> 3;
-      const int kx = kx0 + row;
-      if (kx < g.H1) part += gmul_bin<NC>(tiles, tidx(j, row), gs, 8 * L, row * L + j, parseval_w(kx, g.M));
+      const int rg = row0 + row;
+      if (rg < nrows) {
+        if (STG)
+          part += gmul_bin<NC>(tiles, tidx(j, row), gs, 8 * L, row * L + j, parseval_w(rg / g.P3, g.M));
+        else
+          part += gmul_bin<NC>(tiles, tidx(j, row), cx.gtab, g.nspec, (long long)rg * L + j, parseval_w(rg / g.P3, g.M));
+      }
     }
   }
   __syncthreads();
@@ -424,13 +435,13 @@ __global__ void __launch_bounds__(fft_threads(L)) gpass_y2d_kernel(Ctx cx) {
   for (int q = 0; q < NC; ++q) fft_tile<L, true>(tiles[q], tw);
 #pragma unroll
   for (int q = 0; q < NC; ++q) {
-    double2* base = cx.spec + ((long long)load * g.c + q) * g.nspec + (long long)kx0 * L;
+    double2* base = cx.spec + ((long long)load * g.c + q) * g.nspec + (long long)row0 * L;
 #pragma unroll
     for (int i = 0; i < (8 * L + T - 1) / T; ++i) {
       const int e = t + i * T;
       if (e < 8 * L) {
         const int row = e / L, j = e & (L - 1);
-        if (kx0 + row < g.H1) base[e] = tiles[q][tidx(j, row)];
+        if (row0 + row < nrows) base[e] = tiles[q][tidx(j, row)];
       }
     }
   }
@@ -643,9 +654,10 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
   constexpr int EW = TX + 1, EP = 9 * EW;
   constexpr int ND = (DP + T - 1) / T, NE = (EP + T - 1) / T;
   const Geo g = cx.g;
-  const int nzc = g.N3 / ZC;
+  const int nzc = (g.P3 + ZC - 1) / ZC;
   const int load = blockIdx.z / nzc;
   const int zcI = blockIdx.z - load * nzc;
+  const int dz = g.dirz;  // Dirichlet z: node planes 1..N3-1 stored at index p-1; planes 0, N3 are zero
   if (mode == CG && !cx.st[load].active) return;
   extern __shared__ double ksm[];
   double* D = ksm;                      // [KT_RING][ND*T] (padded: every thread copies ND elements)
@@ -655,7 +667,8 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
   __shared__ double red_sh[32];
   const int t = threadIdx.x;
   const int tx = t % TX, ty = t / TX;   // node rows 2ty, 2ty+1 of the tile
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * KT_TY, zs = zcI * ZC;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * KT_TY, zs = zcI * ZC + dz;
+  const int ze = min(zs + ZC, g.P3 + dz);  // node planes [zs, ze)
   const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
   const long long plane = (long long)N1 * N2;
   const double* dv = src + (long long)load * g.n;
@@ -677,13 +690,18 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
   const unsigned psm = (unsigned)__cvta_generic_to_shared(PH + 4 * pj);
   constexpr unsigned SLOTB = ND * T * 8;  // bytes per D ring slot
   auto issue_plane = [&](int p) {  // node plane p of d and phase layer p-1 -> ring slot
-    const int zw = (p + N3) & (N3 - 1);
     const unsigned slot = (p - zs + 1) & (KT_RING - 1);
     const unsigned so = slot * SLOTB;
-    const double* base = dv + (long long)zw * plane;
+    if (dz && (p <= 0 || p >= N3)) {  // fixed (zero) Dirichlet node plane (Fig 4)
 #pragma unroll
-    for (int m = 0; m < ND; ++m)
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sD[m] + so), "l"(base + goffD[m]) : "memory");
+      for (int m = 0; m < ND; ++m) asm volatile("st.shared.f64 [%0], 0d0000000000000000;\n" ::"r"(sD[m] + so) : "memory");
+    } else {
+      const int zw = dz ? p - 1 : ((p + N3) & (N3 - 1));
+      const double* base = dv + (long long)zw * plane;
+#pragma unroll
+      for (int m = 0; m < ND; ++m)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sD[m] + so), "l"(base + goffD[m]) : "memory");
+    }
     if (phw) {
       const uint8_t* pb = cx.phase + (long long)((p - 1 + N3) & (N3 - 1)) * plane + poff;
       asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(psm + slot * PHS), "l"(pb) : "memory");
@@ -720,7 +738,7 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
   };
 #pragma unroll 1
   for (int p = zs - 1; p <= zs + 3; ++p) {
-    if (p <= zs + ZC) issue_plane(p);
+    if (p <= ze) issue_plane(p);
     cp_commit();
   }
   cp_wait<3>();
@@ -764,7 +782,7 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
   double* outp = dst + (long long)load * g.n + (long long)(y0 + 2 * ty) * N1 + (x0 + tx);
   // one node plane: reads state `I`, writes the carried state for plane k+1 into `O`
   auto step = [&](int k, const KR2State& I, KR2State& O) {
-    if (k + 4 <= zs + ZC) issue_plane(k + 4);
+    if (k + 4 <= ze) issue_plane(k + 4);
     cp_commit();
     cp_wait<3>();
     __syncthreads();
@@ -794,7 +812,7 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
       EE = fma(Khi, dzp, EE);
       EE = fma(I.Klo[m], dzm, EE);
       const double pv = hc * (fma(5.0 * di, Ksum, EE) - (I.KSlo[m] + KShi));
-      outp[(long long)k * plane + m * N1] = pv;
+      outp[(long long)(k - dz) * plane + m * N1] = pv;
       part = fma(di, pv, part);
       O.KSlo[m] = KShi;
       O.Klo[m] = Khi;
@@ -814,11 +832,11 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
   };
   int k = zs;
 #pragma unroll 1
-  for (; k + 1 < zs + ZC; k += 2) {  // unrolled by two: the carried state ping-pongs A <-> B
+  for (; k + 1 < ze; k += 2) {  // unrolled by two: the carried state ping-pongs A <-> B
     step(k, A, B);
     step(k + 1, B, A);
   }
-  if (k < zs + ZC) step(k, A, B);
+  if (k < ze) step(k, A, B);
   cp_wait<0>();
   const int nblk = gridDim.x * gridDim.y * nzc;
   const int my = (zcI * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
@@ -1070,9 +1088,10 @@ constexpr int KE_TX = 16, KE_TY = 8;
 __global__ void __launch_bounds__(128) kp_elastic3d_kernel(Ctx cx, int mode, const double* __restrict__ src,
                                                            double* __restrict__ dst, int ZC) {
   const Geo g = cx.g;
-  const int nzc = g.N3 / ZC;
+  const int nzc = (g.P3 + ZC - 1) / ZC;
   const int load = blockIdx.z / nzc;
   const int zcI = blockIdx.z - load * nzc;
+  const int dz = g.dirz;
   if (mode == CG && !cx.st[load].active) return;
   constexpr int DW = KE_TX + 2, DH = KE_TY + 2, EW = KE_TX + 1, EH = KE_TY + 1;
   __shared__ double D[3][3][DH * DW];        // [slot][comp][...]
@@ -1082,17 +1101,19 @@ __global__ void __launch_bounds__(128) kp_elastic3d_kernel(Ctx cx, int mode, con
   const int t = threadIdx.x, T = blockDim.x;
   for (int i = t; i < 2 * 576; i += T) Ks[i / 576][i % 576] = __ldg(cx.kel + i);
   const int tx = t % KE_TX, ty = t / KE_TX;
-  const int x0 = blockIdx.x * KE_TX, y0 = blockIdx.y * KE_TY, zs = zcI * ZC;
+  const int x0 = blockIdx.x * KE_TX, y0 = blockIdx.y * KE_TY, zs = zcI * ZC + dz;
+  const int ze = min(zs + ZC, g.P3 + dz);
   const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
   const long long n = g.n;
   const double* dv = src + (long long)load * 3 * n;
   auto load_plane = [&](int zz, int slot) {
-    const int zw = (zz + N3) % N3;
+    const bool zero = dz && (zz <= 0 || zz >= N3);  // fixed Dirichlet node plane
+    const int zw = dz ? zz - 1 : (zz + N3) % N3;
     for (int i = t; i < 3 * DH * DW; i += T) {
       const int comp = i / (DH * DW), r = i - comp * DH * DW;
       const int ly = r / DW, lx = r - ly * DW;
       const int gx = (x0 - 1 + lx + N1) & (N1 - 1), gy = (y0 - 1 + ly + N2) & (N2 - 1);
-      D[slot][comp][r] = __ldg(dv + comp * n + ((long long)zw * N2 + gy) * N1 + gx);
+      D[slot][comp][r] = zero ? 0.0 : __ldg(dv + comp * n + ((long long)zw * N2 + gy) * N1 + gx);
     }
   };
   auto load_phase = [&](int layer, int slot) {
@@ -1107,7 +1128,7 @@ __global__ void __launch_bounds__(128) kp_elastic3d_kernel(Ctx cx, int mode, con
   load_plane(zs, 1);
   load_phase(zs - 1, 0);
   double part = 0.0;
-  for (int k = zs; k < zs + ZC; ++k) {
+  for (int k = zs; k < ze; ++k) {
     const int q = k - zs;
     const int sl[3] = {q % 3, (q + 1) % 3, (q + 2) % 3};  // planes k-1, k, k+1
     const int pl[2] = {q & 1, (q + 1) & 1};                // layers k-1, k
@@ -1136,7 +1157,7 @@ __global__ void __launch_bounds__(128) kp_elastic3d_kernel(Ctx cx, int mode, con
     }
     const int gx = x0 + tx, gy = y0 + ty;
     const int offc = (ty + 1) * DW + tx + 1;
-    const long long gi = ((long long)k * N2 + gy) * N1 + gx;
+    const long long gi = ((long long)(k - dz) * N2 + gy) * N1 + gx;
 #pragma unroll
     for (int al = 0; al < 3; ++al) {
       dst[(long long)load * 3 * n + al * n + gi] = acc[al];
@@ -1196,7 +1217,7 @@ __global__ void rhs_kernel(Ctx cx, LoadParams lp, double* __restrict__ f) {
   const int N1 = g.N1, N2 = g.N2, N3 = g.N3, d = g.dim;
   const int x = (int)(i % N1);
   const int y = (int)((i / N1) % N2);
-  const int z = (int)(i / ((long long)N1 * N2));
+  const int z = (int)(i / ((long long)N1 * N2)) + g.dirz;  // Dirichlet z: stored planes are nodes 1..N3-1
   const double scale = (d == 3 ? g.h * g.h / 4.0 : g.h / 2.0);
   int ph[8];
   const int no = 1 << d;
@@ -1301,7 +1322,7 @@ __global__ void __launch_bounds__(EFF_T) effective_kernel(Ctx cx, LoadParams lp,
   const double scale = (d == 3 ? g.h * g.h / 4.0 : g.h / 2.0);
   const double rt2 = 0.70710678118654752440;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += (long long)gridDim.x * blockDim.x) {
-    const int x = (int)(i % N1), y = (int)((i / N1) % N2), z = (int)(i / ((long long)N1 * N2));
+    const int x = (int)(i % N1), y = (int)((i / N1) % N2), z = (int)(i / ((long long)N1 * N2)) + g.dirz;
     int ph[8];
     const int no = 1 << d;
     for (int o = 0; o < no; ++o) {
@@ -1311,6 +1332,7 @@ __global__ void __launch_bounds__(EFF_T) effective_kernel(Ctx cx, LoadParams lp,
       ph[o] = __ldg(cx.phase + ((long long)ez * N2 + ey) * N1 + ex) ? 1 : 0;
     }
     acc[nl * nl] += ph[no - 1];  // voxel i itself is octant (1,1,1) of node i: count each voxel once
+    if (g.dirz && z == 1) acc[nl * nl] += ph[3];  // Dirichlet z: voxel layer 0 has no stored node below
     for (int li = 0; li < nl; ++li) {
       double fi[3] = {0.0, 0.0, 0.0};
       if (g.c == 1) {
@@ -1397,23 +1419,39 @@ __global__ void build_symbol_kernel(Ctx cx, double* gtab, double ref0, double re
     const int kb = (int)((b / ((long long)g.NA * N3)) % g.NB);
     kx = (int)(b / ((long long)g.NA * N3 * g.NB));
     ky = kb + g.NB * ka;
-  } else {         // 5-pass layout [kx][kz][ky]
+  } else {         // 5-pass / mixed layout [kx][kz or sine plane][ky]
     ky = (int)(b % N2);
-    kz = (int)((b / N2) % N3);
-    kx = (int)(b / ((long long)N2 * N3));
+    kz = (int)((b / N2) % g.P3);
+    kx = (int)(b / ((long long)N2 * g.P3));
   }
   double cs[3], sn[3];
   axis_trig(kx, N1, cs[0], sn[0]);
   axis_trig(ky, N2, cs[1], sn[1]);
-  axis_trig(kz, N3, cs[2], sn[2]);
+  double inv_n;
+  unsigned long long flat, flatm;
+  bool zero;
+  if (g.dirz) {
+    // mixed BC: sine mode m = kz+1 along z, theta_z = pi m / N3; the odd x-z / y-z
+    // couplings leave the diagonal block (S_xz = S_yz = 0); sine modes are self-conjugate.
+    double sz, cz;
+    sincospi((double)(kz + 1) / (double)N3, &sz, &cz);
+    cs[2] = cz;
+    sn[2] = 0.0;
+    inv_n = 2.0 / ((double)N1 * N2 * N3);  // F_x F_y unnormalised (N1 N2) x sine sums (N3/2)
+    flat = ((unsigned long long)kz * N2 + ky) * N1 + kx;
+    flatm = ((unsigned long long)kz * N2 + (unsigned long long)((N2 - ky) % N2)) * N1 + (unsigned long long)((N1 - kx) % N1);
+    zero = false;
+  } else {
+    axis_trig(kz, N3, cs[2], sn[2]);
+    inv_n = 1.0 / (double)g.n;
+    flat = ((unsigned long long)kz * N2 + ky) * N1 + kx;
+    flatm = ((unsigned long long)((N3 - kz) % N3) * N2 + (unsigned long long)((N2 - ky) % N2)) * N1 +
+            (unsigned long long)((N1 - kx) % N1);
+    zero = (kx == 0 && ky == 0 && kz == 0);
+  }
   const double h = g.h;
-  const double inv_n = 1.0 / (double)g.n;
   const long long ns = g.nspec;
-  const unsigned long long flat = ((unsigned long long)kz * N2 + ky) * N1 + kx;
-  const unsigned long long flatm =
-      ((unsigned long long)((N3 - kz) % N3) * N2 + (unsigned long long)((N2 - ky) % N2)) * N1 + (unsigned long long)((N1 - kx) % N1);
   const unsigned long long canon = flat < flatm ? flat : flatm;
-  const bool zero = (kx == 0 && ky == 0 && kz == 0);
   double mass[3], S[3][3];
   for (int i = 0; i < d; ++i) mass[i] = (h / 3.0) * (2.0 + cs[i]);
   for (int i = 0; i < d; ++i) {
@@ -1541,7 +1579,7 @@ __global__ void eq55_kernel(Ctx cx, const double* gtab, double* partials) {
   const long long ns = g.nspec;
   const double nn = (double)g.n;
   for (long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x; b < ns; b += (long long)gridDim.x * blockDim.x) {
-    if (b == 0) continue;
+    if (b == 0 && !g.dirz) continue;  // periodic: G_hat(0) = 0 shares the null space
     double lo, hi;
     if (g.c == 1) {
       lo = hi = gtab[b] * nn;
@@ -1596,16 +1634,17 @@ int launch_scalar(const Ctx& cx, int slot, int mode, cudaStream_t s) {
   const Geo& g = cx.g;
   int nblk;
   if (slot == RED_RNORM) {
-    nblk = g.NB > 0 ? g.NA * g.N3 * g.c : g.c * g.N3 * g.N2 / 8;
+    nblk = g.NB > 0 ? g.NA * g.N3 * g.c : (g.dirz ? g.c * g.N2 * (g.N1 / 16) : g.c * g.P3 * g.N2 / 8);
   } else if (slot == RED_GAMMA) {
-    nblk = g.NB > 0 ? g.H1 * g.NB : (g.dim == 3 ? g.H1 * (g.N2 / 8) : (g.H1 + 7) / 8);
+    nblk = g.NB > 0 ? g.H1 * g.NB
+                    : ((g.dim == 3 && !g.dirz) ? g.H1 * (g.N2 / 8) : (int)(((long long)g.H1 * g.P3 + 7) / 8));
   } else {
     if (g.dim == 3 && g.c == 1) {
       const int TX = g.N1 < 32 ? g.N1 : 32, ZC = g.N3 < 32 ? g.N3 : 32;
-      nblk = (g.N1 / TX) * (g.N2 / KT_TY) * (g.N3 / ZC);
+      nblk = (g.N1 / TX) * (g.N2 / KT_TY) * ((g.P3 + ZC - 1) / ZC);
     } else if (g.dim == 3) {
       const int ZC = g.N3 < 16 ? g.N3 : 16;
-      nblk = (g.N1 / KE_TX) * (g.N2 / KE_TY) * (g.N3 / ZC);
+      nblk = (g.N1 / KE_TX) * (g.N2 / KE_TY) * ((g.P3 + ZC - 1) / ZC);
     } else {
       nblk = (int)((g.n + 255) / 256);
     }
@@ -1664,10 +1703,14 @@ int launch_xfwd(const Ctx& cx, int mode, const double* src, cudaStream_t s) {
   const Geo& g = cx.g;
   return dispatch_pow2(g.M, [&](auto Lc) {
     constexpr int M = decltype(Lc)::value;
-    const dim3 grid((unsigned)((long long)g.c * g.N3 * g.N2 / 8), g.nrhs);
+    const dim3 grid((unsigned)((long long)g.c * g.P3 * g.N2 / 8), g.nrhs);
     const int sm = xsmem_bytes<M, false>();
     if (mode == CG) {
       auto k = xfwd_kernel<M, CG>;
+      set_smem(k, sm);
+      k<<<grid, fft_threads(M), sm, s>>>(cx, src);
+    } else if (mode == PLAIN) {
+      auto k = xfwd_kernel<M, PLAIN>;
       set_smem(k, sm);
       k<<<grid, fft_threads(M), sm, s>>>(cx, src);
     } else {
@@ -1683,10 +1726,14 @@ int launch_xinv(const Ctx& cx, int mode, double* dst, cudaStream_t s) {
   const Geo& g = cx.g;
   return dispatch_pow2(g.M, [&](auto Lc) {
     constexpr int M = decltype(Lc)::value;
-    const dim3 grid((unsigned)((long long)g.c * g.N3 * g.N2 / 8), g.nrhs);
+    const dim3 grid((unsigned)((long long)g.c * g.P3 * g.N2 / 8), g.nrhs);
     const int sm = xsmem_bytes<M, true>();
     if (mode == CG) {
       auto k = xinv_kernel<M, CG>;
+      set_smem(k, sm);
+      k<<<grid, fft_threads(M), sm, s>>>(cx, dst);
+    } else if (mode == PLAIN) {
+      auto k = xinv_kernel<M, PLAIN>;
       set_smem(k, sm);
       k<<<grid, fft_threads(M), sm, s>>>(cx, dst);
     } else {
@@ -1720,7 +1767,7 @@ int launch_ypass(const Ctx& cx, int mode, bool inverse, cudaStream_t s) {
 
 int launch_gpass(const Ctx& cx, int mode, cudaStream_t s) {
   const Geo& g = cx.g;
-  if (g.dim == 3) {
+  if (g.dim == 3 && !g.dirz) {
     return dispatch_pow2(g.N3, [&](auto Lc) {
       constexpr int L = decltype(Lc)::value;
       const dim3 grid((unsigned)(g.H1 * (g.N2 / 8)), g.nrhs);
@@ -1743,7 +1790,7 @@ int launch_gpass(const Ctx& cx, int mode, cudaStream_t s) {
   }
   return dispatch_pow2(g.N2, [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
-    const dim3 grid((unsigned)((g.H1 + 7) / 8), g.nrhs);
+    const dim3 grid((unsigned)(((long long)g.H1 * g.P3 + 7) / 8), g.nrhs);
     auto go = [&](auto k, int sm) {
       set_smem(k, sm);
       k<<<grid, fft_threads(L), sm, s>>>(cx);
@@ -1752,8 +1799,15 @@ int launch_gpass(const Ctx& cx, int mode, cudaStream_t s) {
     if (g.c == 1)
       return mode == CG ? go(gpass_y2d_kernel<L, 1, CG>, gsmem_bytes<L, 1>())
                         : go(gpass_y2d_kernel<L, 1, STANDALONE>, gsmem_bytes<L, 1>());
-    return mode == CG ? go(gpass_y2d_kernel<L, 2, CG>, gsmem_bytes<L, 2>())
-                      : go(gpass_y2d_kernel<L, 2, STANDALONE>, gsmem_bytes<L, 2>());
+    if (g.c == 2)
+      return mode == CG ? go(gpass_y2d_kernel<L, 2, CG>, gsmem_bytes<L, 2>())
+                        : go(gpass_y2d_kernel<L, 2, STANDALONE>, gsmem_bytes<L, 2>());
+    if constexpr (gsmem_bytes<L, 3>() <= 220 * 1024) {
+      return mode == CG ? go(gpass_y2d_kernel<L, 3, CG>, gsmem_bytes<L, 3>())
+                        : go(gpass_y2d_kernel<L, 3, STANDALONE>, gsmem_bytes<L, 3>());
+    } else {
+      return -1;
+    }
   });
 }
 
@@ -1763,7 +1817,8 @@ int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaS
     const int TX = g.N1 < 32 ? g.N1 : 32;
     const int ZC = g.N3 < 32 ? g.N3 : 32;
     const int sm = (KT_RING * 10 * (TX + 2) + 4 * 9 * (TX + 1)) * (int)sizeof(double);
-    const dim3 grid(g.N1 / TX, g.N2 / KT_TY, (g.N3 / ZC) * g.nrhs);
+    const dim3 grid(g.N1 / TX, g.N2 / KT_TY, ((g.P3 + ZC - 1) / ZC) * g.nrhs);
+    if (g.dirz && TX != 32) return -1;  // mixed BC: production kernel only (N1 >= 32)
     auto go = [&](auto kern, int tpb) {
       set_smem(kern, sm);
       kern<<<grid, tpb, sm, s>>>(cx, mode, src, dst, ZC);
@@ -1794,7 +1849,7 @@ int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaS
   if (g.dim == 3) {
     if (g.N1 < KE_TX) return -1;
     const int ZC = g.N3 < 16 ? g.N3 : 16;
-    const dim3 grid(g.N1 / KE_TX, g.N2 / KE_TY, (g.N3 / ZC) * g.nrhs);
+    const dim3 grid(g.N1 / KE_TX, g.N2 / KE_TY, ((g.P3 + ZC - 1) / ZC) * g.nrhs);
     kp_elastic3d_kernel<<<grid, KE_TX * KE_TY, 0, s>>>(cx, mode, src, dst, ZC);
     return 1;
   }
@@ -1864,6 +1919,12 @@ int blocks_needed_max(const Geo& g) {
   long long m = (long long)g.c * g.N3 * g.N2 / 8;                // x passes
   if (g.dim == 3) m = m > (long long)g.H1 * (g.N2 / 8) ? m : (long long)g.H1 * (g.N2 / 8);  // G pass
   else m = m > (g.H1 + 7) / 8 ? m : (g.H1 + 7) / 8;
+  if (g.dirz) {  // DST pass grid
+    const long long a = (long long)g.c * g.N2 * (g.N1 / 16);
+    m = m > a ? m : a;
+    const long long b2 = ((long long)g.H1 * g.P3 + 7) / 8;
+    m = m > b2 ? m : b2;
+  }
   if (g.NB > 0) {  // 3-pass schedule: F1/F3 grids NA*N3*c, F2 grid H1*NB
     const long long a = (long long)g.NA * g.N3 * g.c, b = (long long)g.H1 * g.NB;
     m = m > a ? m : a;
@@ -1872,10 +1933,10 @@ int blocks_needed_max(const Geo& g) {
   long long kb;
   if (g.dim == 3 && g.c == 1) {
     const int TX = g.N1 < 32 ? g.N1 : 32, ZC = g.N3 < 32 ? g.N3 : 32;
-    kb = (long long)(g.N1 / TX) * (g.N2 / KT_TY) * (g.N3 / ZC);
+    kb = (long long)(g.N1 / TX) * (g.N2 / KT_TY) * ((g.P3 + ZC - 1) / ZC);
   } else if (g.dim == 3) {
     const int ZC = g.N3 < 16 ? g.N3 : 16;
-    kb = (long long)(g.N1 / KE_TX) * (g.N2 / KE_TY) * (g.N3 / ZC);
+    kb = (long long)(g.N1 / KE_TX) * (g.N2 / KE_TY) * ((g.P3 + ZC - 1) / ZC);
   } else {
     kb = (g.n + 255) / 256;
   }

@@ -9,6 +9,7 @@ struct Tw {                 // device twiddle tables (host-computed in long doub
   const double2* xpost;     // length M+1: e^{-2 pi i k / N1}
   const double2* y;         // length N2
   const double2* z;         // length N3
+  const double2* z2;        // length 2 N3 (DST-I via odd extension, mixed BC)
 };
 
 struct Ctx {
@@ -33,7 +34,7 @@ struct LoadParams {         // macroscopic loads for the RHS / effective-propert
   double v[kMaxRhs][6];
 };
 
-enum Mode { STANDALONE = 0, CG = 1 };
+enum Mode { STANDALONE = 0, CG = 1, PLAIN = 2 };  // PLAIN: skips inactive loads, no CG fusions
 
 // pass launchers; return number of kernels launched (or -1 on unsupported size)
 int launch_xfwd(const Ctx& cx, int mode, const double* src, cudaStream_t s);
@@ -60,5 +61,8 @@ bool schedule3_supported(const Geo& g);
 int launch_f1(const Ctx& cx, int mode, const double* src, cudaStream_t s);
 int launch_f2(const Ctx& cx, int mode, cudaStream_t s);
 int launch_f3(const Ctx& cx, int mode, double* dst, cudaStream_t s);
+
+// mixed BC (Dirichlet on z), dst.cu
+int launch_dstz(const Ctx& cx, int mode, bool inverse, const double* src, double* dst, cudaStream_t s);
 
 }  // namespace uno

@@ -45,7 +45,8 @@ struct uno_cg_handle {
   double2* spec;
   double* gtab;
   double* kel;
-  double2 *twx, *twxp, *twy, *twz;
+  double2 *twx, *twxp, *twy, *twz, *twz2;
+  double* rt;             // mixed BC: z-sine-space intermediate vector [nrhs][c][n]
   LoadState* st;
   double* partials;
   unsigned* counters;
@@ -129,6 +130,7 @@ static Ctx make_ctx(uno_cg_handle* h) {
   cx.tw.xpost = h->twxp;
   cx.tw.y = h->twy;
   cx.tw.z = h->twz;
+  cx.tw.z2 = h->twz2;
   cx.st = h->st;
   cx.sc.partials = h->partials;
   cx.sc.counters = h->counters;
@@ -153,7 +155,7 @@ static void free_all(uno_cg_handle* h) {
   if (!h) return;
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   for (auto e : h->tev) cudaEventDestroy(e);
-  void* bufs[] = {h->r, h->d, h->p, h->u, h->spec, h->gtab, h->kel, h->twx, h->twxp, h->twy, h->twz,
+  void* bufs[] = {h->r, h->d, h->p, h->u, h->spec, h->gtab, h->kel, h->twx, h->twxp, h->twy, h->twz, h->twz2, h->rt,
                   h->st, h->partials, h->counters, h->results, h->scratch, h->hist, h->loopctr};
   for (void* b : bufs)
     if (b) cudaFreeAsync(b, h->stream);
@@ -231,8 +233,11 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
   const uno_cg_desc& D = *desc;
   if (D.dim != 2 && D.dim != 3) return fail(UNO_ERR_ARG, "dim must be 2 or 3");
   if (D.physics != UNO_THERMAL && D.physics != UNO_ELASTIC) return fail(UNO_ERR_ARG, "physics must be 0 or 1");
+  // boundary conditions: all periodic, or (3D) periodic x, y with Dirichlet z (mixed)
+  const bool dirz = D.dim == 3 && D.bc[0] == 0 && D.bc[1] == 0 && D.bc[2] == 1;
   for (int i = 0; i < D.dim; ++i)
-    if (D.bc[i] != 0) return fail(UNO_ERR_UNSUPPORTED, "only periodic boundaries are built in this version");
+    if (D.bc[i] != 0 && !dirz)
+      return fail(UNO_ERR_UNSUPPORTED, "boundary conditions: all periodic, or periodic x,y + Dirichlet z");
   const int N1 = D.n[0], N2 = D.n[1], N3 = D.dim == 3 ? D.n[2] : 1;
   if (!is_pow2(N1) || !is_pow2(N2) || !is_pow2(N3) || N1 < 8 || N2 < 8 || N1 > 1024 || N2 > 1024 ||
       (D.dim == 3 && (N3 < 4 || N3 > 1024)))
@@ -246,6 +251,8 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
       if (!(D.mat[p][1] > 0) || !(D.mat[p][0] >= 0)) return fail(UNO_ERR_ARG, "need mu > 0, lambda >= 0");
     if (D.dim == 3 && N1 < 16) return fail(UNO_ERR_SHAPE, "elastic 3D needs N1 >= 16");
   }
+  if (dirz && ((c == 1 && N1 < 32) || N1 < 16 || N3 < 8 || N3 > 512))
+    return fail(UNO_ERR_SHAPE, "mixed BC needs N1 >= 32 (thermal) / 16 (elastic), 8 <= N3 <= 512");
   if (D.seed != 0 && !(D.amp >= 0 && D.amp < 1)) return fail(UNO_ERR_ARG, "amp must be in [0, 1)");
 
   uno_cg_handle* h = new uno_cg_handle();  // value-initialised: all members zero
@@ -261,8 +268,10 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
   g.N3 = N3;
   g.M = N1 / 2;
   g.H1 = g.M + 1;
-  g.n = (long long)N1 * N2 * N3;
-  g.nspec = (long long)g.H1 * N2 * N3;
+  g.dirz = dirz ? 1 : 0;
+  g.P3 = dirz ? N3 - 1 : N3;
+  g.n = (long long)N1 * N2 * g.P3;
+  g.nspec = (long long)g.H1 * N2 * g.P3;
   g.h = D.h > 0 ? D.h : 1.0 / N1;
   g.C = c * (c + 1) / 2;
   g.NA = g.NB = 0;
@@ -273,7 +282,7 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
     Geo t3 = g;
     t3.NB = N2 >= 128 ? 16 : 8;
     t3.NA = N2 / t3.NB;
-    if (want3 && schedule3_supported(t3)) {
+    if (want3 && !dirz && schedule3_supported(t3)) {
       g.NB = t3.NB;
       g.NA = t3.NA;
     }
@@ -303,6 +312,7 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
       (e = al((void**)&h->gtab, (size_t)g.C * g.nspec * 8)) || (e = al((void**)&h->kel, 2 * 576 * 8)) ||
       (e = al((void**)&h->twx, g.M * 16)) || (e = al((void**)&h->twxp, (g.M + 1) * 16)) ||
       (e = al((void**)&h->twy, N2 * 16)) || (e = al((void**)&h->twz, N3 * 16)) ||
+      (e = al((void**)&h->twz2, 2 * N3 * 16)) || (e = al((void**)&h->rt, dirz ? vec * 8 : 8)) ||
       (e = al((void**)&h->st, kMaxRhs * sizeof(LoadState))) ||
       (e = al((void**)&h->partials, (size_t)RED_NSLOT * kMaxRhs * maxb * 8)) ||
       (e = al((void**)&h->counters, RED_NSLOT * kMaxRhs * sizeof(unsigned))) ||
@@ -330,6 +340,9 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
   cudaStreamSynchronize(s);
   twiddles(N3, N3, t);
   cudaMemcpyAsync(h->twz, t.data(), N3 * 16, cudaMemcpyHostToDevice, s);
+  cudaStreamSynchronize(s);
+  twiddles(2 * N3, 2 * N3, t);
+  cudaMemcpyAsync(h->twz2, t.data(), 2 * N3 * 16, cudaMemcpyHostToDevice, s);
   cudaStreamSynchronize(s);
   const uno_status st0 = setup_problem(h);
   if (st0 != UNO_OK) {
@@ -405,7 +418,14 @@ extern "C" uno_status uno_cg_apply_precond(uno_cg_handle* h, const double* d_r, 
   if (!h || !d_r || !d_z) return fail(UNO_ERR_ARG, "null argument");
   long long launches = 0;
   cudaStream_t s = h->stream;
-  if (h->g.NB > 0) {  // 3-pass four-step schedule
+  if (h->g.dirz) {  // mixed BC: DST-I along z first, then the periodic x/y machinery
+    KL(launch_dstz(h->cx, STANDALONE, false, d_r, h->rt, s), KC_XF);
+    KL(launch_xfwd(h->cx, STANDALONE, h->rt, s), KC_XF);
+    KL(launch_gpass(h->cx, STANDALONE, s), KC_G);
+    KL(launch_xinv(h->cx, STANDALONE, h->rt, s), KC_XI);
+    KL(launch_dstz(h->cx, STANDALONE, true, h->rt, d_z, s), KC_XI);
+    KL(launch_scalar(h->cx, RED_GAMMA, STANDALONE, s), KC_OTHER);
+  } else if (h->g.NB > 0) {  // 3-pass four-step schedule
     KL(launch_f1(h->cx, STANDALONE, d_r, s), KC_XF);
     KL(launch_f2(h->cx, STANDALONE, s), KC_G);
     KL(launch_f3(h->cx, STANDALONE, d_z, s), KC_XI);
@@ -442,7 +462,15 @@ static int enqueue_iteration(uno_cg_handle* h, cudaStream_t s, cudaEvent_t* ev /
     n += r;
     return true;
   };
-  if (h->g.NB > 0) {  // 3-pass four-step schedule (fft3.cu)
+  if (h->g.dirz) {  // mixed BC (dst.cu): DST_z (+CG r update) | x | y.G.y^-1 | x^-1 | DST_z^-1 (+d, u)
+    if (!run(0, [&] { return launch_dstz(cx, CG, false, cx.r, h->rt, s); })) return -1;
+    n += launch_scalar(cx, RED_RNORM, CG, s);
+    if (!run(1, [&] { return launch_xfwd(cx, PLAIN, h->rt, s); })) return -1;
+    if (!run(2, [&] { return launch_gpass(cx, CG, s); })) return -1;
+    n += launch_scalar(cx, RED_GAMMA, CG, s);
+    if (!run(3, [&] { return launch_xinv(cx, PLAIN, h->rt, s); })) return -1;
+    if (!run(4, [&] { return launch_dstz(cx, CG, true, h->rt, nullptr, s); })) return -1;
+  } else if (h->g.NB > 0) {  // 3-pass four-step schedule (fft3.cu)
     if (!run(0, [&] { return launch_f1(cx, CG, cx.r, s); })) return -1;
     n += launch_scalar(cx, RED_RNORM, CG, s);
     if (!run(2, [&] { return launch_f2(cx, CG, s); })) return -1;
@@ -577,7 +605,7 @@ extern "C" uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, doub
   }
   CK(cudaMemcpyAsync(h->st, h->h_st, g.nrhs * sizeof(LoadState), cudaMemcpyHostToDevice, s));
   const long long work = (long long)g.nrhs * g.c * g.n;
-  const int per_iter = ((g.dim == 3 && g.NB == 0) ? 6 : 4) + 3;  // passes + 3 scalar kernels
+  const int per_iter = ((g.dim == 3 && g.NB == 0) ? 6 : 4) + 3;  // passes + 3 scalar kernels (mixed: 6 too)
   if (!h->timing) {
     // whole solve device-side: WHILE node over bodies of `chunk` iterations
     const int chunk = work >= (1LL << 22) ? 2 : 4;
@@ -627,7 +655,10 @@ extern "C" uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, doub
     }
   }
   KL(launch_finalize(h->cx, s), KC_OTHER);
-  KL(launch_mean_removal(h->cx, h->u, d_u, h->scratch, s), KC_OTHER);
+  if (g.dirz)  // Dirichlet z: no null space, the fluctuation is not mean-free
+    CK(cudaMemcpyAsync(d_u, h->u, (size_t)g.nrhs * g.c * g.n * 8, cudaMemcpyDeviceToDevice, s));
+  else
+    KL(launch_mean_removal(h->cx, h->u, d_u, h->scratch, s), KC_OTHER);
   CK(cudaEventRecord(h->e1, s));
   CK(cudaMemcpyAsync(h->h_st, h->st, g.nrhs * sizeof(LoadState), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
@@ -669,8 +700,9 @@ extern "C" uno_status uno_cg_effective_property(uno_cg_handle* h, const double* 
   CK(cudaMemcpyAsync(h->h_small, h->scratch + (long long)nacc * nblk, nacc * 8, cudaMemcpyDeviceToHost, h->stream));
   CK(cudaStreamSynchronize(h->stream));
   CK(cudaGetLastError());
-  const double vf = h->h_small[nl * nl] / (double)g.n;
-  const double vol = (double)g.n * std::pow(g.h, g.dim);
+  const double nvox = (double)g.N1 * g.N2 * g.N3;
+  const double vf = h->h_small[nl * nl] / nvox;
+  const double vol = nvox * std::pow(g.h, g.dim);
   const int nv = g.c == 1 ? g.dim : (g.dim == 3 ? 6 : 3);
   for (int i = 0; i < nl; ++i)
     for (int j = 0; j < nl; ++j) {

@@ -65,7 +65,7 @@ def test_library_loads_and_validates_without_gpu():
         B.uno_cg_create(d, 1)
     assert e.value.status == B.UNO_ERR_SHAPE
     d.n[0] = 16
-    d.bc[2] = 1
+    d.bc[0] = 1  # Dirichlet on x: only all-periodic or periodic x,y + Dirichlet z are built
     with pytest.raises(B.UnoError) as e:
         B.uno_cg_create(d, 1)
     assert e.value.status == B.UNO_ERR_UNSUPPORTED

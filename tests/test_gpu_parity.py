@@ -241,3 +241,75 @@ def test_update_equals_fresh_create():
     a = s.solve(np.eye(2)).u.clone()
     b = solver(other, "thermal", (1.0, 4.0), 2, 77, 0.1).solve(np.eye(2)).u
     assert torch.equal(a, b)
+
+
+# ----------------------------------------------------------------------------- mixed BC (Dirichlet z)
+MIXED = [((32, 16, 16), "thermal"), ((32, 8, 32), "thermal"), ((16, 16, 8), "elastic"), ((32, 16, 16), "elastic")]
+
+
+def mixed_case(N, physics, seed=21):
+    rng = np.random.default_rng(5)
+    shp = tuple(reversed(N))
+    ph = (rng.random(shp) < 0.35).astype(np.uint8)
+    if physics == "thermal":
+        mat, amp = (1.0, 17.0), 0.1
+    else:
+        mat, amp = (synth.lame_from_E_nu(1.0, 0.3), synth.lame_from_E_nu(20.0, 0.2)), 0.05
+    g = fem.Grid(N, bc=(0, 0, 1), c=1 if physics == "thermal" else 3, h=1.0 / N[0])
+    return g, ph, mat, amp, seed
+
+
+def msolver(ph, physics, mat, nrhs, seed, amp):
+    return _api()(torch.from_numpy(ph).to(dev()), physics, mat, nrhs=nrhs, seed=seed, amp=amp, bc=(0, 0, 1))
+
+
+@pytest.mark.parametrize("N,physics", MIXED)
+def test_mixed_apply_K_rhs_precond(N, physics):
+    g, ph, mat, amp, seed = mixed_case(N, physics)
+    s = msolver(ph, physics, mat, 2, seed, amp)
+    u = np.stack([synth.test_vector(40 + l, g.field_shape()) for l in range(2)])
+    Ku = s.apply_K(torch.from_numpy(u).to(dev())).cpu().numpy()
+    for l in range(2):
+        assert rel(Ku[l], fem.apply_K(g, physics, ph, mat, u[l])) <= 1e-13
+    L = loads_for(physics, 3, 2)
+    f = s.rhs(L).cpu().numpy()
+    for l in range(2):
+        ref = fem.rhs(g, physics, ph, mat, L[l])
+        assert np.max(np.abs(f[l] - ref)) <= 1e-14 * np.max(np.abs(ref))
+    G = greens.ghat_mixed(g, physics, mat, seed, amp)
+    z, rz = s.apply_precond(torch.from_numpy(u).to(dev()), want_dot=True)
+    z = z.cpu().numpy()
+    for l in range(2):
+        ref = greens.apply_precond_mixed(G, u[l])
+        assert rel(z[l], ref) <= 1e-12
+        assert abs(rz[l] - np.sum(u[l] * ref)) <= 1e-12 * abs(np.sum(u[l] * ref))
+
+
+@pytest.mark.parametrize("N,physics", [((32, 16, 16), "thermal"), ((16, 16, 8), "elastic")])
+def test_mixed_solve(N, physics):
+    g, ph, mat, amp, seed = mixed_case(N, physics)
+    loads = np.eye(3 if physics == "thermal" else 6)[[0, 2]]
+    s = msolver(ph, physics, mat, 2, seed, amp)
+    res = s.solve(loads, rel_tol=1e-8, max_iter=500)
+    ref = homog.solve_problem(g, physics, ph, mat, loads, seed, amp, tol=1e-8, max_iter=500)
+    its = [r["iterations"] for r in res.reports]
+    assert all(abs(a - b) <= 1 for a, b in zip(its, ref["iterations"])), (its, ref["iterations"])
+    for l in range(2):
+        m = ref["iterations"][l]
+        fx = homog.solve_problem(g, physics, ph, mat, loads[l:l + 1], seed, amp, fixed_iters=m)
+        gu = msolver(ph, physics, mat, 1, seed, amp).solve(loads[l:l + 1], fixed_iters=m).u.cpu().numpy()[0]
+        assert rel(gu, fx["U"][0]) <= 1e-9
+    keff = s.effective_property(res.u, loads)
+    assert np.max(np.abs(keff - ref["effective"])) <= 1e-7 * np.max(np.abs(ref["effective"]))
+
+
+def test_mixed_thermal_exact_inverse_large():
+    # homogeneous thermal, seed 0: P K u = u exactly (F x F x DST-I diagonalises K_r); N3 = 512
+    # exercises the length-1024 odd-extension DST of config 4's mixed variant.
+    N = (64, 32, 512)
+    shp = tuple(reversed(N))
+    ph = torch.zeros(shp, dtype=torch.uint8, device=dev())
+    s = _api()(ph, "thermal", (3.0, 3.0), nrhs=1, seed=0, bc=(0, 0, 1))
+    u = torch.rand(s.field_shape, dtype=torch.float64, device=dev()) * 2 - 1
+    v = s.apply_precond(s.apply_K(u))
+    assert float((v - u).norm() / u.norm()) < 1e-11
