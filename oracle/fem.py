@@ -353,3 +353,21 @@ def assemble_dense(g: Grid, physics: str, phase: np.ndarray, mat) -> np.ndarray:
 
 def phase_mean(phase: np.ndarray, v0: float, v1: float) -> float:
     return float(np.mean(coeff_field(phase, v0, v1)))
+
+
+def apply_K_at(g: Grid, physics: str, phase: np.ndarray, mat, u: np.ndarray, nodes) -> np.ndarray:
+    """(K u) at selected nodes of a periodic grid, one node at a time: K u at node i depends only
+    on u in the 3^d node neighbourhood and on the 2^d elements around i (Eq 22 assembly), so the
+    value equals the matrix-free apply on a periodic 4^d sub-block whose local node 1 is i.
+    nodes: iterable of numpy-order index tuples.  Returns (len(nodes), c)."""
+    assert all(b == 0 for b in g.bc)
+    d = g.d
+    out = []
+    sub = Grid((4,) * d, c=g.c, h=g.h[0])
+    for nd in nodes:
+        idx = [np.arange(k - 1, k + 3) % n for k, n in zip(nd, g.node_shape)]
+        ub = u[(slice(None),) + np.ix_(*idx)]
+        pb = phase[np.ix_(*idx)]
+        kb = apply_K(sub, physics, pb, mat, np.ascontiguousarray(ub))
+        out.append(kb[(slice(None),) + (1,) * d])
+    return np.array(out)

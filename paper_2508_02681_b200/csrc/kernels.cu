@@ -1210,57 +1210,77 @@ __global__ void __launch_bounds__(256) kp_elastic2d_kernel(Ctx cx, int mode, con
 // ============================================================================== RHS (Eq 76 / 81)
 // f_(i,alpha) = -(h^(d-1)/2^(d-1)) sum_o sum_j s_j(o) sigma^o_(alpha j),  s_j(o) = +1 if o_j = 0 else -1,
 // sigma^o = kappa_o g_bar (thermal, alpha = 0) or lambda_o tr(eps) I + 2 mu_o eps (elastic).
-__global__ void rhs_kernel(Ctx cx, LoadParams lp, double* __restrict__ f) {
-  const Geo g = cx.g;
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= g.n) return;
-  const int N1 = g.N1, N2 = g.N2, N3 = g.N3, d = g.dim;
-  const int x = (int)(i % N1);
-  const int y = (int)((i / N1) % N2);
-  const int z = (int)(i / ((long long)N1 * N2)) + g.dirz;  // Dirichlet z: stored planes are nodes 1..N3-1
+// The factor of each (phase, load, component, octant) is tabulated once per CTA in shared memory
+// (W[ph][l][alpha][o]); a node then sums 2^d table entries selected by its octant phases.
+__device__ void rhs_weights(const Ctx& cx, const LoadParams& lp, double* W /* [2][nrhs][c][8] */) {
+  const Geo& g = cx.g;
+  const int d = g.dim, c = g.c, nl = g.nrhs;
   const double scale = (d == 3 ? g.h * g.h / 4.0 : g.h / 2.0);
-  int ph[8];
-  const int no = 1 << d;
-  for (int o = 0; o < no; ++o) {
-    const int ox = o & 1, oy = (o >> 1) & 1, oz = (o >> 2) & 1;
-    const int ex = (x - 1 + ox + N1) & (N1 - 1), ey = (y - 1 + oy + N2) & (N2 - 1);
-    const int ez = d == 3 ? (z - 1 + oz + N3) % N3 : 0;
-    ph[o] = __ldg(cx.phase + ((long long)ez * N2 + ey) * N1 + ex) ? 1 : 0;
-  }
   const double rt2 = 0.70710678118654752440;
-  for (int l = 0; l < g.nrhs; ++l) {
-    if (g.c == 1) {
-      double acc = 0.0;
-      for (int o = 0; o < no; ++o) {
-        double sg = 0.0;
-        for (int j = 0; j < d; ++j) sg += ((o >> j) & 1) ? -lp.v[l][j] : lp.v[l][j];
-        acc += cx.mat[ph[o]][0] * sg;
-      }
-      f[(long long)l * g.n + i] = -scale * acc;
-    } else {
-      double e[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-      if (d == 3) {
-        e[0][0] = lp.v[l][0]; e[1][1] = lp.v[l][1]; e[2][2] = lp.v[l][2];
-        e[0][1] = e[1][0] = lp.v[l][3] * rt2;
-        e[0][2] = e[2][0] = lp.v[l][4] * rt2;
-        e[1][2] = e[2][1] = lp.v[l][5] * rt2;
+  for (int idx = threadIdx.x; idx < 2 * nl * c * 8; idx += blockDim.x) {
+    const int o = idx & 7, al = (idx >> 3) % c, l = (idx >> 3) / c % nl, ph = (idx >> 3) / (c * nl);
+    double acc = 0.0;
+    if (o < (1 << d)) {
+      if (c == 1) {
+        for (int j = 0; j < d; ++j) acc += ((o >> j) & 1) ? -lp.v[l][j] : lp.v[l][j];
+        acc *= cx.mat[ph][0];
       } else {
-        e[0][0] = lp.v[l][0]; e[1][1] = lp.v[l][1];
-        e[0][1] = e[1][0] = lp.v[l][2] * rt2;
-      }
-      const double tr = e[0][0] + e[1][1] + e[2][2];
-      for (int al = 0; al < d; ++al) {
-        double acc = 0.0;
-        for (int o = 0; o < no; ++o) {
-          const double lam = cx.mat[ph[o]][0], mu = cx.mat[ph[o]][1];
-          for (int j = 0; j < d; ++j) {
-            const double sig = (al == j ? lam * tr : 0.0) + 2.0 * mu * e[al][j];
-            acc += ((o >> j) & 1) ? -sig : sig;
-          }
+        double e[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+        if (d == 3) {
+          e[0][0] = lp.v[l][0]; e[1][1] = lp.v[l][1]; e[2][2] = lp.v[l][2];
+          e[0][1] = e[1][0] = lp.v[l][3] * rt2;
+          e[0][2] = e[2][0] = lp.v[l][4] * rt2;
+          e[1][2] = e[2][1] = lp.v[l][5] * rt2;
+        } else {
+          e[0][0] = lp.v[l][0]; e[1][1] = lp.v[l][1];
+          e[0][1] = e[1][0] = lp.v[l][2] * rt2;
         }
-        f[((long long)l * g.c + al) * g.n + i] = -scale * acc;
+        const double tr = e[0][0] + e[1][1] + e[2][2];
+        const double lam = cx.mat[ph][0], mu = cx.mat[ph][1];
+        for (int j = 0; j < d; ++j) {
+          const double sig = (al == j ? lam * tr : 0.0) + 2.0 * mu * e[al][j];
+          acc += ((o >> j) & 1) ? -sig : sig;
+        }
       }
     }
+    W[idx] = -scale * acc;
+  }
+  __syncthreads();
+}
+
+// octant phases of node i (stored index), shift-based decode (N1, N2 powers of two)
+__device__ __forceinline__ unsigned node_octants(const Ctx& cx, long long i, int& z) {
+  const Geo& g = cx.g;
+  const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
+  const int s1 = __ffs(N1) - 1, s2 = __ffs(N2) - 1;
+  const int x = (int)(i & (N1 - 1));
+  const int y = (int)((i >> s1) & (N2 - 1));
+  z = (int)(i >> (s1 + s2)) + g.dirz;  // Dirichlet z: stored planes are nodes 1..N3-1
+  unsigned bits = 0;
+  const int no = 1 << g.dim;
+  for (int o = 0; o < no; ++o) {
+    const int ox = o & 1, oy = (o >> 1) & 1, oz = (o >> 2) & 1;
+    const int ex = (x - 1 + ox) & (N1 - 1), ey = (y - 1 + oy) & (N2 - 1);
+    const int ez = g.dim == 3 ? (z - 1 + oz + N3) % N3 : 0;
+    bits |= (__ldg(cx.phase + ((long long)ez * N2 + ey) * N1 + ex) ? 1u : 0u) << o;
+  }
+  return bits;
+}
+
+__global__ void __launch_bounds__(256) rhs_kernel(Ctx cx, LoadParams lp, double* __restrict__ f) {
+  __shared__ double W[2 * kMaxRhs * 3 * 8];
+  const Geo g = cx.g;
+  rhs_weights(cx, lp, W);
+  const int nl = g.nrhs, c = g.c, no = 1 << g.dim;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += (long long)gridDim.x * blockDim.x) {
+    int z;
+    const unsigned bits = node_octants(cx, i, z);
+    for (int l = 0; l < nl; ++l)
+      for (int al = 0; al < c; ++al) {
+        double acc = 0.0;
+        for (int o = 0; o < no; ++o) acc += W[(((bits >> o) & 1) * nl * c + l * c + al) * 8 + o];
+        f[((long long)l * c + al) * g.n + i] = acc;
+      }
   }
 }
 
@@ -1308,73 +1328,40 @@ __global__ void mean_subtract_kernel(const double* __restrict__ src, double* __r
 }
 
 // ============================================================================== effective property
-// acc[i][j] = f^(i) . u^(j); plus the count of phase-1 voxels for <C>.
+// acc[i][j] = f^(i) . u^(j) (f recomputed per node from the weight table); plus the count of
+// phase-1 voxels for <C>.
 constexpr int EFF_T = 256;
+template <int NL>
 __global__ void __launch_bounds__(EFF_T) effective_kernel(Ctx cx, LoadParams lp, const double* __restrict__ u,
                                                           double* partials) {
-  const Geo g = cx.g;
-  const int nl = g.nrhs;
-  const int nacc = nl * nl + 1;
+  __shared__ double W[2 * kMaxRhs * 3 * 8];
   __shared__ double sh[32];
-  double acc[kMaxRhs * kMaxRhs + 1];
-  for (int a = 0; a < nacc; ++a) acc[a] = 0.0;
-  const int N1 = g.N1, N2 = g.N2, N3 = g.N3, d = g.dim;
-  const double scale = (d == 3 ? g.h * g.h / 4.0 : g.h / 2.0);
-  const double rt2 = 0.70710678118654752440;
+  const Geo g = cx.g;
+  rhs_weights(cx, lp, W);
+  const int c = g.c, no = 1 << g.dim;
+  double acc[NL * NL + 1];
+#pragma unroll
+  for (int a = 0; a < NL * NL + 1; ++a) acc[a] = 0.0;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += (long long)gridDim.x * blockDim.x) {
-    const int x = (int)(i % N1), y = (int)((i / N1) % N2), z = (int)(i / ((long long)N1 * N2)) + g.dirz;
-    int ph[8];
-    const int no = 1 << d;
-    for (int o = 0; o < no; ++o) {
-      const int ox = o & 1, oy = (o >> 1) & 1, oz = (o >> 2) & 1;
-      const int ex = (x - 1 + ox + N1) & (N1 - 1), ey = (y - 1 + oy + N2) & (N2 - 1);
-      const int ez = d == 3 ? (z - 1 + oz + N3) % N3 : 0;
-      ph[o] = __ldg(cx.phase + ((long long)ez * N2 + ey) * N1 + ex) ? 1 : 0;
-    }
-    acc[nl * nl] += ph[no - 1];  // voxel i itself is octant (1,1,1) of node i: count each voxel once
-    if (g.dirz && z == 1) acc[nl * nl] += ph[3];  // Dirichlet z: voxel layer 0 has no stored node below
-    for (int li = 0; li < nl; ++li) {
-      double fi[3] = {0.0, 0.0, 0.0};
-      if (g.c == 1) {
-        double s = 0.0;
-        for (int o = 0; o < no; ++o) {
-          double sg = 0.0;
-          for (int j = 0; j < d; ++j) sg += ((o >> j) & 1) ? -lp.v[li][j] : lp.v[li][j];
-          s += cx.mat[ph[o]][0] * sg;
-        }
-        fi[0] = -scale * s;
-      } else {
-        double e[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-        if (d == 3) {
-          e[0][0] = lp.v[li][0]; e[1][1] = lp.v[li][1]; e[2][2] = lp.v[li][2];
-          e[0][1] = e[1][0] = lp.v[li][3] * rt2;
-          e[0][2] = e[2][0] = lp.v[li][4] * rt2;
-          e[1][2] = e[2][1] = lp.v[li][5] * rt2;
-        } else {
-          e[0][0] = lp.v[li][0]; e[1][1] = lp.v[li][1];
-          e[0][1] = e[1][0] = lp.v[li][2] * rt2;
-        }
-        const double tr = e[0][0] + e[1][1] + e[2][2];
-        for (int al = 0; al < d; ++al) {
-          double s = 0.0;
-          for (int o = 0; o < no; ++o) {
-            const double lam = cx.mat[ph[o]][0], mu = cx.mat[ph[o]][1];
-            for (int j = 0; j < d; ++j) {
-              const double sig = (al == j ? lam * tr : 0.0) + 2.0 * mu * e[al][j];
-              s += ((o >> j) & 1) ? -sig : sig;
-            }
-          }
-          fi[al] = -scale * s;
-        }
-      }
-      for (int lj = 0; lj < nl; ++lj) {
-        double s = 0.0;
-        for (int al = 0; al < g.c; ++al) s = fma(fi[al], u[((long long)lj * g.c + al) * g.n + i], s);
-        acc[li * nl + lj] += s;
+    int z;
+    const unsigned bits = node_octants(cx, i, z);
+    acc[NL * NL] += (bits >> (no - 1)) & 1;  // voxel i is octant (1,1,1) of node i: each voxel once
+    if (g.dirz && z == 1) acc[NL * NL] += (bits >> 3) & 1;  // Dirichlet z: voxel layer 0
+    for (int al = 0; al < c; ++al) {
+      double uv[NL];
+#pragma unroll
+      for (int lj = 0; lj < NL; ++lj) uv[lj] = u[((long long)lj * c + al) * g.n + i];
+#pragma unroll
+      for (int li = 0; li < NL; ++li) {
+        double fi = 0.0;
+        for (int o = 0; o < no; ++o) fi += W[(((bits >> o) & 1) * NL * c + li * c + al) * 8 + o];
+#pragma unroll
+        for (int lj = 0; lj < NL; ++lj) acc[li * NL + lj] = fma(fi, uv[lj], acc[li * NL + lj]);
       }
     }
   }
-  for (int a = 0; a < nacc; ++a) {
+#pragma unroll
+  for (int a = 0; a < NL * NL + 1; ++a) {
     const double b = block_reduce<false>(acc[a], sh);
     if (threadIdx.x == 0) partials[(long long)a * gridDim.x + blockIdx.x] = b;
     __syncthreads();
@@ -1859,7 +1846,9 @@ int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaS
 }
 
 int launch_rhs(const Ctx& cx, const LoadParams& lp, double* f, cudaStream_t s) {
-  rhs_kernel<<<(unsigned)((cx.g.n + 255) / 256), 256, 0, s>>>(cx, lp, f);
+  long long nb = (cx.g.n + 255) / 256;
+  if (nb > 148 * 8) nb = 148 * 8;
+  rhs_kernel<<<(unsigned)nb, 256, 0, s>>>(cx, lp, f);
   return 1;
 }
 
@@ -1889,7 +1878,16 @@ int launch_effective(const Ctx& cx, const LoadParams& lp, const double* u, doubl
                      cudaStream_t s) {
   const int nblk = 148 * 2;
   const int nacc = cx.g.nrhs * cx.g.nrhs + 1;
-  effective_kernel<<<nblk, EFF_T, 0, s>>>(cx, lp, u, partials);
+  switch (cx.g.nrhs) {
+    case 1: effective_kernel<1><<<nblk, EFF_T, 0, s>>>(cx, lp, u, partials); break;
+    case 2: effective_kernel<2><<<nblk, EFF_T, 0, s>>>(cx, lp, u, partials); break;
+    case 3: effective_kernel<3><<<nblk, EFF_T, 0, s>>>(cx, lp, u, partials); break;
+    case 4: effective_kernel<4><<<nblk, EFF_T, 0, s>>>(cx, lp, u, partials); break;
+    case 5: effective_kernel<5><<<nblk, EFF_T, 0, s>>>(cx, lp, u, partials); break;
+    case 6: effective_kernel<6><<<nblk, EFF_T, 0, s>>>(cx, lp, u, partials); break;
+    case 7: effective_kernel<7><<<nblk, EFF_T, 0, s>>>(cx, lp, u, partials); break;
+    default: effective_kernel<8><<<nblk, EFF_T, 0, s>>>(cx, lp, u, partials); break;
+  }
   combine_rows_kernel<<<nacc, 256, 0, s>>>(partials, nblk, partials + (long long)nacc * nblk);
   *nblocks_out = nblk;
   return 2;

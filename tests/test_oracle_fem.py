@@ -183,3 +183,17 @@ def test_rhs(physics, bc):
     fa = fem.rhs(g, physics, ph, mat, a)
     fs = sum(a[j] * fem.rhs(g, physics, ph, mat, np.eye(nl)[j]) for j in range(nl))
     assert np.max(np.abs(fa - fs)) < 1e-13
+
+
+@pytest.mark.parametrize("physics", ["thermal", "elastic"])
+def test_apply_K_at_equals_full_apply(physics):
+    # sampled-output evaluator used by the full-size GPU tests == full matrix-free apply
+    c = 1 if physics == "thermal" else 3
+    g = fem.Grid((8, 6, 10), c=c, h=1 / 8)
+    ph = (RNG.random(g.elem_shape) < 0.4).astype(np.uint8)
+    mat = (1.0, 9.0) if physics == "thermal" else ((0.5, 0.3), (2.0, 4.0))
+    u = RNG.standard_normal(g.field_shape())
+    K = fem.apply_K(g, physics, ph, mat, u)
+    nodes = [(0, 0, 0), (9, 5, 7), (4, 2, 3), (9, 0, 7)]
+    got = fem.apply_K_at(g, physics, ph, mat, u, nodes)
+    assert np.max(np.abs(got - np.array([K[(slice(None),) + n] for n in nodes]))) < 1e-14
