@@ -1630,8 +1630,13 @@ int launch_scalar(const Ctx& cx, int slot, int mode, cudaStream_t s) {
       const int TX = g.N1 < 32 ? g.N1 : 32, ZC = g.N3 < 32 ? g.N3 : 32;
       nblk = (g.N1 / TX) * (g.N2 / KT_TY) * ((g.P3 + ZC - 1) / ZC);
     } else if (g.dim == 3) {
-      const int ZC = g.N3 < 16 ? g.N3 : 16;
-      nblk = (g.N1 / KE_TX) * (g.N2 / KE_TY) * ((g.P3 + ZC - 1) / ZC);
+      const char* e = getenv("UNO_ELASTIC_DENSE");
+      if (!(e && e[0] == '1')) {
+        nblk = kp_elastic_modal_nblk(g);
+      } else {
+        const int ZC = g.N3 < 16 ? g.N3 : 16;
+        nblk = (g.N1 / KE_TX) * (g.N2 / KE_TY) * ((g.P3 + ZC - 1) / ZC);
+      }
     } else {
       nblk = (int)((g.n + 255) / 256);
     }
@@ -1834,6 +1839,11 @@ int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaS
     return 1;
   }
   if (g.dim == 3) {
+    static const bool dense = [] {
+      const char* e = getenv("UNO_ELASTIC_DENSE");
+      return e && e[0] == '1';
+    }();
+    if (!dense) return launch_kp_elastic_modal(cx, mode, src, dst, s);
     if (g.N1 < KE_TX) return -1;
     const int ZC = g.N3 < 16 ? g.N3 : 16;
     const dim3 grid(g.N1 / KE_TX, g.N2 / KE_TY, ((g.P3 + ZC - 1) / ZC) * g.nrhs);
@@ -1935,6 +1945,8 @@ int blocks_needed_max(const Geo& g) {
   } else if (g.dim == 3) {
     const int ZC = g.N3 < 16 ? g.N3 : 16;
     kb = (long long)(g.N1 / KE_TX) * (g.N2 / KE_TY) * ((g.P3 + ZC - 1) / ZC);
+    const long long km = kp_elastic_modal_nblk(g);
+    kb = kb > km ? kb : km;
   } else {
     kb = (g.n + 255) / 256;
   }

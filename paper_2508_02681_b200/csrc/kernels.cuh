@@ -62,6 +62,10 @@ int launch_f1(const Ctx& cx, int mode, const double* src, cudaStream_t s);
 int launch_f2(const Ctx& cx, int mode, cudaStream_t s);
 int launch_f3(const Ctx& cx, int mode, double* dst, cudaStream_t s);
 
+// elastic K.u in the Walsh-Hadamard modal basis, kp_elastic.cu
+int launch_kp_elastic_modal(const Ctx& cx, int mode, const double* src, double* dst, cudaStream_t s);
+int kp_elastic_modal_nblk(const Geo& g);
+
 // mixed BC (Dirichlet on z), dst.cu
 int launch_dstz(const Ctx& cx, int mode, bool inverse, const double* src, double* dst, cudaStream_t s);
 

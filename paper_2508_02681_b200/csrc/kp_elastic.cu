@@ -1,0 +1,179 @@
+// kp_elastic.cu — matrix-free Q1 elasticity K.u (Eq 22 with D of Eq 80) in the
+// Walsh-Hadamard modal basis of the element (elastic_modal.cuh).
+//
+// Per element: forward 8-point WHT of the corner displacements (3 components), the 45-entry
+// sparse modal operator (lam, mu of the element's phase), inverse WHT: ~240 flops instead of the
+// 576 FMAs of the dense 24x24 element matrix.  Node-centric gather without atomics: a CTA owns a
+// 16 x 8 node tile marching over z; each z step computes the 17 x 9 element layer above the
+// current node plane once (160 threads, one element each) into shared memory, split into the
+// lower-face outputs (consumed by this node plane) and the upper-face outputs (kept for the
+// next plane), and every node sums its 8 octant contributions.  d planes stream through a
+// 4-slot cp.async ring (planes k+2, k+3 in flight while layer k is computed).
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "dev_common.cuh"
+#include "elastic_modal.cuh"
+#include "kernels.cuh"
+
+namespace uno {
+
+constexpr int KM_TX = 16, KM_TY = 8, KM_T = 160;
+constexpr int KM_DW = KM_TX + 2, KM_DH = KM_TY + 2, KM_DP = KM_DW * KM_DH;  // 18 x 10 node tile
+constexpr int KM_EW = KM_TX + 1, KM_EH = KM_TY + 1, KM_NE = KM_EW * KM_EH;  // 17 x 9 elements
+constexpr int KM_RING = 4;
+constexpr int KM_PLANE = 3 * KM_DP;                 // doubles per ring slot (3 components)
+constexpr int KM_NCP = (KM_PLANE + KM_T - 1) / KM_T;  // cp.async per thread per plane
+
+__host__ __device__ constexpr int km_smem_bytes() {
+  return (KM_RING * KM_PLANE + 12 * KM_NE + 2 * 12 * KM_NE) * (int)sizeof(double);
+}
+
+__global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int mode, const double* __restrict__ src,
+                                                                     double* __restrict__ dst, int ZC) {
+  const Geo g = cx.g;
+  const int nzc = (g.P3 + ZC - 1) / ZC;
+  const int load = blockIdx.z / nzc;
+  const int zcI = blockIdx.z - load * nzc;
+  if (mode == CG && !cx.st[load].active) return;
+  const int dz = g.dirz;
+  extern __shared__ double kms[];
+  double* D = kms;                           // [RING][3][10][18]
+  double* Lb = D + KM_RING * KM_PLANE;       // [12][NE] lower-face outputs of the current layer
+  double* Ub = Lb + 12 * KM_NE;              // [2][12][NE] upper-face outputs (ping-pong)
+  __shared__ double red_sh[32];
+  const int t = threadIdx.x;
+  const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
+  const long long n = g.n;
+  const long long plane = (long long)N1 * N2;
+  const int x0 = blockIdx.x * KM_TX, y0 = blockIdx.y * KM_TY;
+  const int zs = zcI * ZC + dz, ze = min(zs + ZC, g.P3 + dz);
+  const double* dv = src + (long long)load * 3 * n;
+  const double hs = g.h / (72.0 * 64.0);
+  const double l0 = cx.mat[0][0] * hs, m0 = cx.mat[0][1] * hs, l1 = cx.mat[1][0] * hs, m1 = cx.mat[1][1] * hs;
+  // copy assignment of the 3 x 10 x 18 plane tile (clamped: harmless duplicate copies)
+  long long goff[KM_NCP];
+  unsigned sdst[KM_NCP];
+#pragma unroll
+  for (int m = 0; m < KM_NCP; ++m) {
+    const int j = min(t + m * KM_T, KM_PLANE - 1);
+    const int comp = j / KM_DP, r = j - comp * KM_DP;
+    const int ly = r / KM_DW, lx = r - ly * KM_DW;
+    goff[m] = comp * n + (long long)((y0 - 1 + ly + N2) & (N2 - 1)) * N1 + ((x0 - 1 + lx + N1) & (N1 - 1));
+    sdst[m] = (unsigned)__cvta_generic_to_shared(D + j);  // clamped copies rewrite entry PLANE-1
+  }
+  auto slot_of = [&](int p) { return (p - zs + 1) & (KM_RING - 1); };
+  auto issue_plane = [&](int p) {
+    const unsigned so = slot_of(p) * KM_PLANE * 8;
+    if (dz && (p <= 0 || p >= N3)) {
+#pragma unroll
+      for (int m = 0; m < KM_NCP; ++m)
+        asm volatile("st.shared.f64 [%0], 0d0000000000000000;\n" ::"r"(sdst[m] + so) : "memory");
+    } else {
+      const int zw = dz ? p - 1 : ((p + N3) & (N3 - 1));
+      const double* base = dv + (long long)zw * plane;
+#pragma unroll
+      for (int m = 0; m < KM_NCP; ++m)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sdst[m] + so), "l"(base + goff[m]) : "memory");
+    }
+  };
+  // element owned by this thread in every layer
+  const bool eth = t < KM_NE;
+  const int exl = eth ? t % KM_EW : 0, eyl = eth ? t / KM_EW : 0;
+  const long long pbase = (long long)((y0 - 1 + eyl + N2) & (N2 - 1)) * N1 + ((x0 - 1 + exl + N1) & (N1 - 1));
+  auto element_layer = [&](int k, double* Uout, bool want_lower) {  // element layer between node planes k, k+1
+    if (!eth) return;
+    const int layer = dz ? k : ((k + N3) & (N3 - 1));
+    const bool ph = __ldg(cx.phase + (long long)layer * plane + pbase) != 0;
+    const double ls = ph ? l1 : l0, ms = ph ? m1 : m0;
+    double u[24];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+      const double* Dp = D + slot_of(k + ((a >> 2) & 1)) * KM_PLANE + (eyl + ((a >> 1) & 1)) * KM_DW + exl + (a & 1);
+#pragma unroll
+      for (int al = 0; al < 3; ++al) u[3 * a + al] = Dp[al * KM_DP];
+    }
+#pragma unroll
+    for (int al = 0; al < 3; ++al) modal::wht8(u + al);
+    double v[24];
+#pragma unroll
+    for (int i = 0; i < 24; ++i) v[i] = 0.0;
+    modal::modal_apply<3>(v, u, ls, ms);  // rows of mode 0 are zero
+#pragma unroll
+    for (int al = 0; al < 3; ++al) modal::wht8(v + al);
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int al = 0; al < 3; ++al) {
+        if (want_lower) Lb[(3 * a + al) * KM_NE + t] = v[3 * a + al];
+        Uout[(3 * a + al) * KM_NE + t] = v[3 * (a + 4) + al];
+      }
+  };
+  // prologue: planes zs-1 .. zs+2 in flight; element layer zs-1 (its upper faces feed plane zs)
+#pragma unroll 1
+  for (int p = zs - 1; p <= zs + 2; ++p) {
+    if (p <= ze) issue_plane(p);
+    cp_commit();
+  }
+  cp_wait<2>();  // planes zs-1, zs
+  __syncthreads();
+  element_layer(zs - 1, Ub + ((zs - 1) & 1) * 12 * KM_NE, false);
+  const bool nth = t < KM_TX * KM_TY;
+  const int tx = t % KM_TX, ty = t / KM_TX;
+  double part = 0.0;
+#pragma unroll 1
+  for (int k = zs; k < ze; ++k) {
+    cp_wait<1>();  // planes k, k+1 landed (plane k+2 may still be in flight)
+    __syncthreads();
+    // refill the slot of plane k-1 only now: every thread has left step k-1 (its node phase read it)
+    if (k + 3 <= ze) issue_plane(k + 3);
+    cp_commit();
+    element_layer(k, Ub + (k & 1) * 12 * KM_NE, true);
+    __syncthreads();
+    if (nth) {
+      const double* Up = Ub + ((k - 1) & 1) * 12 * KM_NE;
+      double p[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        const int ox = o & 1, oy = o >> 1;
+        const int e = (ty + oy) * KM_EW + tx + ox;
+        const int a = (1 - ox) + 2 * (1 - oy);  // the node's corner in both element layers
+#pragma unroll
+        for (int al = 0; al < 3; ++al) p[al] += Lb[(3 * a + al) * KM_NE + e] + Up[(3 * a + al) * KM_NE + e];
+      }
+      const double* Dc = D + slot_of(k) * KM_PLANE + (ty + 1) * KM_DW + tx + 1;
+      const long long gi = (long long)(k - dz) * plane + (long long)(y0 + ty) * N1 + x0 + tx;
+#pragma unroll
+      for (int al = 0; al < 3; ++al) {
+        dst[(long long)load * 3 * n + al * n + gi] = p[al];
+        part = fma(Dc[al * KM_DP], p[al], part);
+      }
+    }
+  }
+  cp_wait<0>();
+  const int nblk = gridDim.x * gridDim.y * nzc;
+  const int my = (zcI * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  dp_finish(cx, load, nblk, my, part, red_sh, mode);
+}
+
+int launch_kp_elastic_modal(const Ctx& cx, int mode, const double* src, double* dst, cudaStream_t s) {
+  const Geo& g = cx.g;
+  if (g.dim != 3 || g.c != 3 || g.N1 < KM_TX || g.N2 < KM_TY) return -1;
+  const int ZC = g.N3 < 32 ? g.N3 : 32;
+  const dim3 grid(g.N1 / KM_TX, g.N2 / KM_TY, ((g.P3 + ZC - 1) / ZC) * g.nrhs);
+  const int sm = km_smem_bytes();
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kp_elastic3d_modal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    attr = true;
+  }
+  kp_elastic3d_modal_kernel<<<grid, KM_T, sm, s>>>(cx, mode, src, dst, ZC);
+  return 1;
+}
+
+int kp_elastic_modal_nblk(const Geo& g) {
+  const int ZC = g.N3 < 32 ? g.N3 : 32;
+  return (g.N1 / KM_TX) * (g.N2 / KM_TY) * ((g.P3 + ZC - 1) / ZC);
+}
+
+}  // namespace uno
