@@ -207,21 +207,36 @@ def run_ours(args):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     tot_dofit, tot_launch, ktimes = 0, 0, {}
     with ClockSampler(local) as clk:
+        # timed region: the production path (each solve one CUDA graph with a device-side WHILE loop)
         barrier()
         ev0.record(stream)
         for _ in range(args.steps):
-            d_, l_, kt, effs = one_step(True)
+            d_, l_, _, effs = one_step(False)
             tot_dofit += d_
             tot_launch += l_
-            for k, (ms, c) in kt.items():
-                a = ktimes.setdefault(k, [0.0, 0])
-                a[0] += ms
-                a[1] += c
         ev1.record(stream)
+        barrier()
+        # kernel-timing region: the same steps again with a CUDA-event pair around every kernel
+        # launch (chunked graphs; the event nodes cost ~10 % of the step, so it is kept out of
+        # `value`).  Per-kernel durations for the roofline come from here.
+        kt0, kt1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        kt0.record(stream)
+        kt_dofit = 0
+        for _ in range(args.steps):
+            d_, _, kt, _ = one_step(True)
+            kt_dofit += d_
+            for k, (ms_, c) in kt.items():
+                a = ktimes.setdefault(k, [0.0, 0])
+                a[0] += ms_
+                a[1] += c
+        kt1.record(stream)
         barrier()
     ms = D.reduce_max(ev0.elapsed_time(ev1))      # max over ranks of the device time
     all_dofit = D.reduce_sum(float(tot_dofit))    # units processed by all ranks
     value = all_dofit / (ms / 1e3)
+    kt_ms = D.reduce_max(kt0.elapsed_time(kt1))
+    kt_value = D.reduce_sum(float(kt_dofit)) / (kt_ms / 1e3)
 
     # ---- roofline of the dominant kernel (live per-launch CUDA-event durations) ----
     peak, peak_src = peaks()
@@ -244,6 +259,8 @@ def run_ours(args):
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(per[dom]["GBps"], 1), "peak": peak, "unit": "GB/s",
                 "frac": round(per[dom]["GBps"] / peak, 4), "traffic": traffic,
                 "algorithmic_bytes_per_launch": kb[dom], "peak_source": peak_src,
+                "timing": "CUDA-event pairs around every launch on the launch stream, in a second timed pass of "
+                          f"the same {args.steps} steps (that pass ran at {kt_value / 1e9:.2f} G{UNIT})",
                 "kernels": {k: {kk: round(vv, 4) for kk, vv in v.items()} for k, v in per.items()}}
 
     # ---- e2e: host buffers in, host results out, through the public API ----

@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libunocg.so")
+LIB_PATH = os.environ.get("UNO_LIB_PATH") or os.path.join(_HERE, "lib", "libunocg.so")  # override: A/B builds
 
 UNO_OK, UNO_ERR_ARG, UNO_ERR_SHAPE, UNO_ERR_CUDA, UNO_ERR_UNSUPPORTED, UNO_ERR_NOT_SPD, UNO_ERR_BREAKDOWN, \
     UNO_ERR_NONFINITE = range(8)

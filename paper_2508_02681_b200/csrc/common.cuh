@@ -21,6 +21,8 @@ struct Geo {
   int NA, NB;           // 3-pass (four-step) schedule: N2 = NA*NB, y = y_a + NA*y_b; NB = 0 -> 5-pass
   int dirz;             // 1: Dirichlet on z (mixed BC; DST-I along z), node planes 1..N3-1 stored
   int P3;               // stored node planes along z: N3 (periodic) or N3 - 1 (dirz); 1 in 2D
+  int KZC;              // z planes per CTA of the 3D thermal K kernel
+  int ZP;               // z-chunk of the L2-pipelined 5-pass schedule (0: off), DESIGN.md §5
 };
 
 // Per-load CG state (device resident; Alg 2 scalars).

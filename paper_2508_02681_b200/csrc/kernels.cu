@@ -24,6 +24,17 @@
 #include "kernels.cuh"
 #include "dev_common.cuh"
 
+// minimum resident CTAs per SM requested from ptxas for the 256-point passes (occupancy experiments)
+#ifndef UNO_YMINB
+#define UNO_YMINB 1
+#endif
+#ifndef UNO_GMINB
+#define UNO_GMINB 1
+#endif
+#ifndef UNO_XMINB
+#define UNO_XMINB 1
+#endif
+
 namespace uno {
 
 // ============================================================================== x passes
@@ -35,7 +46,7 @@ __host__ __device__ constexpr int xsmem_bytes() {
 
 // F1 / standalone forward: real rows of length N1 = 2M -> half spectrum [kx][z][y].
 template <int M, int MODE>
-__global__ void __launch_bounds__(fft_threads(M)) xfwd_kernel(Ctx cx, const double* __restrict__ src) {
+__global__ void __launch_bounds__(fft_threads(M), M == 128 ? UNO_XMINB : 1) xfwd_kernel(Ctx cx, const double* __restrict__ src, int bofs) {
   constexpr int T = fft_threads(M);
   const Geo g = cx.g;
   const int load = blockIdx.y;
@@ -48,7 +59,8 @@ __global__ void __launch_bounds__(fft_threads(M)) xfwd_kernel(Ctx cx, const doub
   double2* twp = tw + M;
   __shared__ double red_sh[32];
   const int t = threadIdx.x;
-  const long long row0 = (long long)blockIdx.x * 8;  // row = (comp, z, y) within the load
+  const int bx = bofs + blockIdx.x;  // block of 8 rows (a z-chunk launch covers a contiguous range)
+  const long long row0 = (long long)bx * 8;  // row = (comp, z, y) within the load
   const long long voff = (long long)load * g.c * g.n + row0 * g.N1;
   const double2* src2 = reinterpret_cast<const double2*>(src + voff);
   double2* r2 = reinterpret_cast<double2*>(cx.r + voff);
@@ -112,12 +124,12 @@ __global__ void __launch_bounds__(fft_threads(M)) xfwd_kernel(Ctx cx, const doub
       if (k != M - k) out[(long long)(M - k) * plane + row] = cadd(cconj(E), cmul(twp[M - k], cconj(O)));
     }
   }
-  if (MODE == CG) partial_write<true>(cx, RED_RNORM, load, blockIdx.x, mx, red_sh);
+  if (MODE == CG) partial_write<true>(cx, RED_RNORM, load, bx, mx, red_sh);
 }
 
 // F5 / standalone inverse: half spectrum -> real rows; CG epilogue d = s + beta d, u += alpha d_old.
 template <int M, int MODE>
-__global__ void __launch_bounds__(fft_threads(M)) xinv_kernel(Ctx cx, double* __restrict__ dst) {
+__global__ void __launch_bounds__(fft_threads(M)) xinv_kernel(Ctx cx, double* __restrict__ dst, int bofs) {
   constexpr int T = fft_threads(M);
   const Geo g = cx.g;
   const int load = blockIdx.y;
@@ -129,7 +141,7 @@ __global__ void __launch_bounds__(fft_threads(M)) xinv_kernel(Ctx cx, double* __
   double2* tw = stage + 16 * M;
   double2* twp = tw + M;
   const int t = threadIdx.x;
-  const long long row0 = (long long)blockIdx.x * 8;
+  const long long row0 = (long long)(bofs + blockIdx.x) * 8;
   const int y0 = (int)(row0 % g.N2);
   const long long zc = row0 / g.N2;
   const int z = (int)(zc % g.P3);
@@ -229,7 +241,7 @@ __host__ __device__ constexpr int ysmem_bytes() {
 }
 
 template <int L, bool INV, int MODE>
-__global__ void __launch_bounds__(fft_threads(L)) ypass_kernel(Ctx cx) {
+__global__ void __launch_bounds__(fft_threads(L), L == 256 ? UNO_YMINB : 1) ypass_kernel(Ctx cx, int z0, int zc) {
   constexpr int T = fft_threads(L);
   const Geo g = cx.g;
   const int load = blockIdx.y;
@@ -239,7 +251,12 @@ __global__ void __launch_bounds__(fft_threads(L)) ypass_kernel(Ctx cx) {
   double2* tw = smem + 8 * L;
   const int t = threadIdx.x;
   const long long nrows = (long long)g.c * g.H1 * g.N3;
-  const long long row0 = (long long)blockIdx.x * 8;
+  long long row0 = (long long)blockIdx.x * 8;  // row = (comp, kx, z)
+  if (zc > 0) {  // z-chunk [z0, z0+zc) of every (comp, kx) plane (zc, z0 multiples of 8)
+    const int nb = zc >> 3;
+    const int q = blockIdx.x / nb;
+    row0 = (long long)q * g.N3 + z0 + (blockIdx.x - q * nb) * 8;
+  }
   double2* base = cx.spec + (long long)load * g.c * g.nspec + row0 * L;
   const bool full = row0 + 8 <= nrows;
 #pragma unroll
@@ -284,7 +301,7 @@ __host__ __device__ constexpr int gsmem_bytes() {
 
 // 3D G pass: sequences along z (stride N2), tile = 8 consecutive y of one kx plane.
 template <int L, int NC, int MODE>
-__global__ void __launch_bounds__(fft_threads(L)) gpass_z_kernel(Ctx cx) {
+__global__ void __launch_bounds__(fft_threads(L), L == 256 ? UNO_GMINB : 1) gpass_z_kernel(Ctx cx) {
   constexpr int T = fft_threads(L);
   constexpr int NCC = NC == 1 ? 1 : (NC == 2 ? 3 : 6);  // unique symbol entries per bin
   const Geo g = cx.g;
@@ -645,18 +662,19 @@ struct KR2State {   // everything a thread carries from node plane k to k+1 (two
   double c0, c1, ym, yp, xm0, xp0, xm1, xp1, dzm0, dzm1;  // in-plane values of plane k, centres of k-1
 };
 
-template <int TX>
+template <int TX, int LA>  // LA: planes of cp.async lookahead (< KT_RING)
 __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx cx, int mode,
                                                                           const double* __restrict__ src,
-                                                                          double* __restrict__ dst, int ZC) {
+                                                                          double* __restrict__ dst, int ZC,
+                                                                          int zc0, int nzl) {
   constexpr int T = TX * KT_TY / 2;
   constexpr int DW = TX + 2, DP = 10 * DW;
   constexpr int EW = TX + 1, EP = 9 * EW;
-  constexpr int ND = (DP + T - 1) / T, NE = (EP + T - 1) / T;
+  constexpr int ND = (DP + T - 1) / T;
   const Geo g = cx.g;
   const int nzc = (g.P3 + ZC - 1) / ZC;
-  const int load = blockIdx.z / nzc;
-  const int zcI = blockIdx.z - load * nzc;
+  const int load = blockIdx.z / nzl;                // launch covers z-chunks [zc0, zc0 + nzl)
+  const int zcI = zc0 + (blockIdx.z - load * nzl);
   const int dz = g.dirz;  // Dirichlet z: node planes 1..N3-1 stored at index p-1; planes 0, N3 are zero
   if (mode == CG && !cx.st[load].active) return;
   extern __shared__ double ksm[];
@@ -736,12 +754,13 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
       a[e][1] = Pl[e * 36 + 1] ? k1 : k0;
     }
   };
+  static_assert(LA >= 2 && LA < KT_RING, "ring slot of plane k+LA must not be read at step k-1");
 #pragma unroll 1
-  for (int p = zs - 1; p <= zs + 3; ++p) {
+  for (int p = zs - 1; p <= zs + LA - 1; ++p) {
     if (p <= ze) issue_plane(p);
     cp_commit();
   }
-  cp_wait<3>();
+  cp_wait<LA - 1>();
   __syncthreads();
   KR2State A, B;
   {
@@ -782,9 +801,9 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
   double* outp = dst + (long long)load * g.n + (long long)(y0 + 2 * ty) * N1 + (x0 + tx);
   // one node plane: reads state `I`, writes the carried state for plane k+1 into `O`
   auto step = [&](int k, const KR2State& I, KR2State& O) {
-    if (k + 4 <= ze) issue_plane(k + 4);
+    if (k + LA <= ze) issue_plane(k + LA);
     cp_commit();
-    cp_wait<3>();
+    cp_wait<LA - 1>();
     __syncthreads();
     read4x3(k + 1);
     box(O.Qk);
@@ -1593,17 +1612,26 @@ __global__ void eq55_kernel(Ctx cx, const double* gtab, double* partials) {
 
 // Fixed-order combine of the per-CTA partials of one reduction slot and the CG scalar step
 // that consumes it (Alg 2 l.3 / l.7-8 / l.10); one CTA per load case.
-__global__ void __launch_bounds__(256) scalar_kernel(Ctx cx, int slot, int nblk, int mode) {
+constexpr int SC_T = 1024;
+__global__ void __launch_bounds__(SC_T) scalar_kernel(Ctx cx, int slot, int nblk, int mode) {
   __shared__ double sh[32];
   const int load = blockIdx.x;
   LoadState* st = cx.st + load;
   if (mode == CG && !st->active) return;
   const double* part = red_partials(cx.sc, slot, load);
   const bool mx = slot == RED_RNORM;
-  double acc = 0.0;
-  for (int i = threadIdx.x; i < nblk; i += blockDim.x) {
-    const double v = part[i];
-    acc = (i == (int)threadIdx.x) ? v : (mx ? fmax(acc, v) : acc + v);
+  // fixed-order combine (deterministic); 8 independent loads in flight per thread, since the
+  // partials come from L2 and a dependent chain of them is pure latency
+  double acc = 0.0;  // identity of both: ||r||_inf >= 0, sums
+  for (int i0 = threadIdx.x; i0 < nblk; i0 += 8 * SC_T) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * SC_T;
+      v[u] = i < nblk ? __ldcg(part + i) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc = mx ? fmax(acc, v[u]) : acc + v[u];
   }
   const double tot = mx ? block_reduce<true>(acc, sh) : block_reduce<false>(acc, sh);
   if (threadIdx.x == 0) {
@@ -1627,7 +1655,7 @@ int launch_scalar(const Ctx& cx, int slot, int mode, cudaStream_t s) {
                     : ((g.dim == 3 && !g.dirz) ? g.H1 * (g.N2 / 8) : (int)(((long long)g.H1 * g.P3 + 7) / 8));
   } else {
     if (g.dim == 3 && g.c == 1) {
-      const int TX = g.N1 < 32 ? g.N1 : 32, ZC = g.N3 < 32 ? g.N3 : 32;
+      const int TX = g.N1 < 32 ? g.N1 : 32, ZC = g.KZC;
       nblk = (g.N1 / TX) * (g.N2 / KT_TY) * ((g.P3 + ZC - 1) / ZC);
     } else if (g.dim == 3) {
       const char* e = getenv("UNO_ELASTIC_DENSE");
@@ -1641,7 +1669,7 @@ int launch_scalar(const Ctx& cx, int slot, int mode, cudaStream_t s) {
       nblk = (int)((g.n + 255) / 256);
     }
   }
-  scalar_kernel<<<g.nrhs, 256, 0, s>>>(cx, slot, nblk, mode);
+  scalar_kernel<<<g.nrhs, SC_T, 0, s>>>(cx, slot, nblk, mode);
   return 1;
 }
 
@@ -1691,62 +1719,63 @@ static void set_smem(K kernel, int bytes) {
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
-int launch_xfwd(const Ctx& cx, int mode, const double* src, cudaStream_t s) {
+int launch_xfwd(const Ctx& cx, int mode, const double* src, cudaStream_t s, int b0, int nb) {
   const Geo& g = cx.g;
   return dispatch_pow2(g.M, [&](auto Lc) {
     constexpr int M = decltype(Lc)::value;
-    const dim3 grid((unsigned)((long long)g.c * g.P3 * g.N2 / 8), g.nrhs);
+    const dim3 grid(nb > 0 ? (unsigned)nb : (unsigned)((long long)g.c * g.P3 * g.N2 / 8), g.nrhs);
     const int sm = xsmem_bytes<M, false>();
     if (mode == CG) {
       auto k = xfwd_kernel<M, CG>;
       set_smem(k, sm);
-      k<<<grid, fft_threads(M), sm, s>>>(cx, src);
+      k<<<grid, fft_threads(M), sm, s>>>(cx, src, b0);
     } else if (mode == PLAIN) {
       auto k = xfwd_kernel<M, PLAIN>;
       set_smem(k, sm);
-      k<<<grid, fft_threads(M), sm, s>>>(cx, src);
+      k<<<grid, fft_threads(M), sm, s>>>(cx, src, b0);
     } else {
       auto k = xfwd_kernel<M, STANDALONE>;
       set_smem(k, sm);
-      k<<<grid, fft_threads(M), sm, s>>>(cx, src);
+      k<<<grid, fft_threads(M), sm, s>>>(cx, src, b0);
     }
     return 1;
   });
 }
 
-int launch_xinv(const Ctx& cx, int mode, double* dst, cudaStream_t s) {
+int launch_xinv(const Ctx& cx, int mode, double* dst, cudaStream_t s, int b0, int nb) {
   const Geo& g = cx.g;
   return dispatch_pow2(g.M, [&](auto Lc) {
     constexpr int M = decltype(Lc)::value;
-    const dim3 grid((unsigned)((long long)g.c * g.P3 * g.N2 / 8), g.nrhs);
+    const dim3 grid(nb > 0 ? (unsigned)nb : (unsigned)((long long)g.c * g.P3 * g.N2 / 8), g.nrhs);
     const int sm = xsmem_bytes<M, true>();
     if (mode == CG) {
       auto k = xinv_kernel<M, CG>;
       set_smem(k, sm);
-      k<<<grid, fft_threads(M), sm, s>>>(cx, dst);
+      k<<<grid, fft_threads(M), sm, s>>>(cx, dst, b0);
     } else if (mode == PLAIN) {
       auto k = xinv_kernel<M, PLAIN>;
       set_smem(k, sm);
-      k<<<grid, fft_threads(M), sm, s>>>(cx, dst);
+      k<<<grid, fft_threads(M), sm, s>>>(cx, dst, b0);
     } else {
       auto k = xinv_kernel<M, STANDALONE>;
       set_smem(k, sm);
-      k<<<grid, fft_threads(M), sm, s>>>(cx, dst);
+      k<<<grid, fft_threads(M), sm, s>>>(cx, dst, b0);
     }
     return 1;
   });
 }
 
-int launch_ypass(const Ctx& cx, int mode, bool inverse, cudaStream_t s) {
+int launch_ypass(const Ctx& cx, int mode, bool inverse, cudaStream_t s, int z0, int zc) {
   const Geo& g = cx.g;
+  if (zc > 0 && ((zc | z0) & 7)) return -1;
   return dispatch_pow2(g.N2, [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
-    const long long nrows = (long long)g.c * g.H1 * g.N3;
+    const long long nrows = zc > 0 ? (long long)g.c * g.H1 * zc : (long long)g.c * g.H1 * g.N3;
     const dim3 grid((unsigned)((nrows + 7) / 8), g.nrhs);
     const int sm = ysmem_bytes<L>();
     auto pick = [&](auto k) {
       set_smem(k, sm);
-      k<<<grid, fft_threads(L), sm, s>>>(cx);
+      k<<<grid, fft_threads(L), sm, s>>>(cx, z0, zc);
     };
     if (mode == CG) {
       if (inverse) pick(ypass_kernel<L, true, CG>); else pick(ypass_kernel<L, false, CG>);
@@ -1803,13 +1832,20 @@ int launch_gpass(const Ctx& cx, int mode, cudaStream_t s) {
   });
 }
 
-int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaStream_t s) {
+int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaStream_t s, int zc0, int nzl) {
   const Geo& g = cx.g;
   if (g.dim == 3 && g.c == 1) {
     const int TX = g.N1 < 32 ? g.N1 : 32;
-    const int ZC = g.N3 < 32 ? g.N3 : 32;
+    const int ZC = g.KZC;
+    const int nzc = (g.P3 + ZC - 1) / ZC;
+    if (nzl <= 0) {
+      zc0 = 0;
+      nzl = nzc;
+    } else if (TX != 32) {
+      return -1;  // z-chunk ranges: production kernel only
+    }
     const int sm = (KT_RING * 10 * (TX + 2) + 4 * 9 * (TX + 1)) * (int)sizeof(double);
-    const dim3 grid(g.N1 / TX, g.N2 / KT_TY, ((g.P3 + ZC - 1) / ZC) * g.nrhs);
+    const dim3 grid(g.N1 / TX, g.N2 / KT_TY, nzl * g.nrhs);
     if (g.dirz && TX != 32) return -1;  // mixed BC: production kernel only (N1 >= 32)
     auto go = [&](auto kern, int tpb) {
       set_smem(kern, sm);
@@ -1826,8 +1862,14 @@ int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaS
     } else if (TX == 32) {
       constexpr int T2 = 128, ND2 = (10 * 34 + T2 - 1) / T2;
       const int sm2 = KT_RING * ND2 * T2 * (int)sizeof(double) + KT_RING * 9 * 36;
-      set_smem(kp_thermal3d_r2_kernel<32>, sm2);
-      kp_thermal3d_r2_kernel<32><<<grid, 128, sm2, s>>>(cx, mode, src, dst, ZC);
+      static const int la = [] {
+        const char* e = getenv("UNO_KLA");
+        return e ? atoi(e) : 4;
+      }();
+      auto k2 = la >= 7 ? kp_thermal3d_r2_kernel<32, 7> : la == 6 ? kp_thermal3d_r2_kernel<32, 6>
+                                                                   : kp_thermal3d_r2_kernel<32, 4>;
+      set_smem(k2, sm2);
+      k2<<<grid, 128, sm2, s>>>(cx, mode, src, dst, ZC, zc0, nzl);
     }
     else if (TX == 16) go(kp_thermal3d_kernel<16>, 128);
     else go(kp_thermal3d_kernel<8>, 64);
@@ -1940,7 +1982,7 @@ int blocks_needed_max(const Geo& g) {
   }
   long long kb;
   if (g.dim == 3 && g.c == 1) {
-    const int TX = g.N1 < 32 ? g.N1 : 32, ZC = g.N3 < 32 ? g.N3 : 32;
+    const int TX = g.N1 < 32 ? g.N1 : 32, ZC = g.KZC;
     kb = (long long)(g.N1 / TX) * (g.N2 / KT_TY) * ((g.P3 + ZC - 1) / ZC);
   } else if (g.dim == 3) {
     const int ZC = g.N3 < 16 ? g.N3 : 16;

@@ -37,11 +37,14 @@ struct LoadParams {         // macroscopic loads for the RHS / effective-propert
 enum Mode { STANDALONE = 0, CG = 1, PLAIN = 2 };  // PLAIN: skips inactive loads, no CG fusions
 
 // pass launchers; return number of kernels launched (or -1 on unsupported size)
-int launch_xfwd(const Ctx& cx, int mode, const double* src, cudaStream_t s);
-int launch_xinv(const Ctx& cx, int mode, double* dst, cudaStream_t s);
-int launch_ypass(const Ctx& cx, int mode, bool inverse, cudaStream_t s);
+// b0/nb: launch only blocks [b0, b0+nb) of 8 x-rows (nb = 0: all) — z-chunks of the pipelined schedule
+int launch_xfwd(const Ctx& cx, int mode, const double* src, cudaStream_t s, int b0 = 0, int nb = 0);
+int launch_xinv(const Ctx& cx, int mode, double* dst, cudaStream_t s, int b0 = 0, int nb = 0);
+// z0/zc: only z in [z0, z0+zc) of every (comp, kx) plane (zc = 0: all; multiples of 8)
+int launch_ypass(const Ctx& cx, int mode, bool inverse, cudaStream_t s, int z0 = 0, int zc = 0);
 int launch_gpass(const Ctx& cx, int mode, cudaStream_t s);
-int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaStream_t s);
+// zc0/nzl: 3D thermal only, z-chunks [zc0, zc0+nzl) of g.KZC planes (nzl = 0: all)
+int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaStream_t s, int zc0 = 0, int nzl = 0);
 int launch_rhs(const Ctx& cx, const LoadParams& lp, double* f, cudaStream_t s);
 int launch_finalize(const Ctx& cx, cudaStream_t s);
 int launch_mean_removal(const Ctx& cx, const double* u, double* out, double* scratch_means, cudaStream_t s);

@@ -74,6 +74,9 @@ struct uno_cg_handle {
   long long last_launches;
   cudaEvent_t e0, e1;
   double lam_min, lam_max;
+  // pipelined schedule: fork/join streams and dependency events used during graph capture
+  cudaStream_t aux[2];
+  cudaEvent_t pev[4];
 };
 
 // ------------------------------------------------------------------------------ helpers
@@ -163,6 +166,10 @@ static void free_all(uno_cg_handle* h) {
   if (h->h_small) cudaFreeHost(h->h_small);
   if (h->e0) cudaEventDestroy(h->e0);
   if (h->e1) cudaEventDestroy(h->e1);
+  for (auto st : h->aux)
+    if (st) cudaStreamDestroy(st);
+  for (auto e : h->pev)
+    if (e) cudaEventDestroy(e);
   delete h;
 }
 
@@ -287,6 +294,16 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
       g.NA = t3.NA;
     }
   }
+  g.KZC = g.N3 < 32 ? g.N3 : 32;
+  g.ZP = 0;
+  {  // L2-pipelined 5-pass schedule (z-chunks), UNO_ZPIPE=<planes per chunk>
+    const char* ev = getenv("UNO_ZPIPE");
+    const int Z = ev ? atoi(ev) : 0;
+    if (Z > 0 && g.dim == 3 && c == 1 && !dirz && g.NB == 0 && N1 >= 32 && Z % 8 == 0 && N3 % Z == 0 && N3 / Z >= 2) {
+      g.ZP = Z;
+      g.KZC = Z;
+    }
+  }
   cudaStream_t s = h->stream;
   const long long vec = (long long)g.nrhs * c * g.n;
   static bool pool_cfg = false;
@@ -323,6 +340,16 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
       (e = cudaEventCreate(&h->e1))) {
     free_all(h);
     return fail(UNO_ERR_CUDA, std::string("allocation: ") + cudaGetErrorString(e));
+  }
+  if (g.ZP > 0) {
+    for (auto& st : h->aux)
+      if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking))) break;
+    for (auto& ev : h->pev)
+      if (!e) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e) {
+      free_all(h);
+      return fail(UNO_ERR_CUDA, std::string("stream/event creation: ") + cudaGetErrorString(e));
+    }
   }
   cudaMemsetAsync(h->counters, 0, RED_NSLOT * kMaxRhs * sizeof(unsigned), s);
   cudaMemsetAsync(h->st, 0, kMaxRhs * sizeof(LoadState), s);
@@ -476,6 +503,52 @@ static int enqueue_iteration(uno_cg_handle* h, cudaStream_t s, cudaEvent_t* ev /
     if (!run(2, [&] { return launch_f2(cx, CG, s); })) return -1;
     n += launch_scalar(cx, RED_GAMMA, CG, s);
     if (!run(4, [&] { return launch_f3(cx, CG, nullptr, s); })) return -1;
+  } else if (h->g.ZP > 0) {
+    // L2-pipelined 5-pass schedule over C = N3/Z z-chunks: the y pass of chunk c
+    // reads the x-pass output of chunk c while it is still L2 resident, likewise x^-1 after y^-1
+    // and K after x^-1 (K of chunk c waits for x^-1 of chunk c+1: its z+1 halo plane).
+    const Geo& g = h->g;
+    const int Z = g.ZP, C = g.N3 / Z, nbx = Z * g.N2 / 8;
+    cudaStream_t s1 = h->aux[0], s2 = h->aux[1];
+    cudaEvent_t ea = h->pev[0], eb = h->pev[1], ec = h->pev[2], ej = h->pev[3];
+    auto fork = [&](cudaStream_t from, cudaStream_t to, cudaEvent_t e) {
+      cudaEventRecord(e, from);
+      cudaStreamWaitEvent(to, e, 0);
+    };
+    if (ev) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
+    for (int c = 0; c < C; ++c) {  // phase A: x pass (s) -> y pass (s1)
+      if (launch_xfwd(cx, CG, cx.r, s, c * nbx, nbx) < 0) return -1;
+      fork(s, s1, ea);
+      if (launch_ypass(cx, CG, false, s1, c * Z, Z) < 0) return -1;
+      n += 2;
+    }
+    n += launch_scalar(cx, RED_RNORM, CG, s);
+    fork(s1, s, ej);
+    if (ev) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
+    if (!run(2, [&] { return launch_gpass(cx, CG, s); })) return -1;
+    n += launch_scalar(cx, RED_GAMMA, CG, s);
+    if (ev) cudaEventRecordWithFlags(ev[8], s, cudaEventRecordExternal);
+    fork(s, s1, ea);  // s1: x^-1 chain; s2: K chain
+    fork(s, s2, eb);
+    for (int c = 0; c < C; ++c) {  // phase C: y^-1 (s) -> x^-1 (s1) -> K (s2, one chunk behind)
+      if (launch_ypass(cx, CG, true, s, c * Z, Z) < 0) return -1;
+      fork(s, s1, ea);
+      if (launch_xinv(cx, CG, nullptr, s1, c * nbx, nbx) < 0) return -1;
+      n += 2;
+      if (c >= 2) {
+        fork(s1, s2, ec);
+        if (launch_kapply(cx, CG, cx.d, cx.p, s2, c - 1, 1) < 0) return -1;
+        ++n;
+      }
+    }
+    fork(s1, s2, ec);
+    if (C >= 2 && launch_kapply(cx, CG, cx.d, cx.p, s2, C - 1, 1) < 0) return -1;
+    if (launch_kapply(cx, CG, cx.d, cx.p, s2, 0, 1) < 0) return -1;
+    n += 2;
+    fork(s2, s, ej);
+    if (ev) cudaEventRecordWithFlags(ev[9], s, cudaEventRecordExternal);
+    n += launch_scalar(cx, RED_DP, CG, s);
+    return n;
   } else {
     const bool d3 = h->g.dim == 3;
     if (!run(0, [&] { return launch_xfwd(cx, CG, cx.r, s); })) return -1;
@@ -605,7 +678,8 @@ extern "C" uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, doub
   }
   CK(cudaMemcpyAsync(h->st, h->h_st, g.nrhs * sizeof(LoadState), cudaMemcpyHostToDevice, s));
   const long long work = (long long)g.nrhs * g.c * g.n;
-  const int per_iter = ((g.dim == 3 && g.NB == 0) ? 6 : 4) + 3;  // passes + 3 scalar kernels (mixed: 6 too)
+  // passes + 3 scalar kernels (mixed: 6 too); pipelined: 2C + 1 + 3C over C z-chunks
+  const int per_iter = g.ZP > 0 ? 5 * (g.N3 / g.ZP) + 4 : ((g.dim == 3 && g.NB == 0) ? 6 : 4) + 3;
   if (!h->timing) {
     // whole solve device-side: WHILE node over bodies of `chunk` iterations
     const int chunk = work >= (1LL << 22) ? 2 : 4;

@@ -64,10 +64,13 @@ SHAPES = [((16, 8, 32), "thermal"), ((32, 16, 8), "thermal"), ((64, 64, 64), "th
           ((32, 64, 16), "thermal"), ((16, 128, 32), "thermal"), ((32, 256, 16), "thermal"), ((16, 64, 16), "elastic")]
 
 
-@pytest.fixture(params=["3", "5"])
+@pytest.fixture(params=["3", "5", "5p"])
 def schedule(request, monkeypatch):
-    """Both transform schedules (UNO_SCHEDULE is read at handle creation)."""
-    monkeypatch.setenv("UNO_SCHEDULE", request.param)
+    """Every transform schedule (UNO_SCHEDULE / UNO_ZPIPE are read at handle creation);
+    "5p" = 5-pass with the z-chunk pipelined CG iteration (16-plane chunks)."""
+    monkeypatch.setenv("UNO_SCHEDULE", request.param[0])
+    if request.param == "5p":
+        monkeypatch.setenv("UNO_ZPIPE", "16")
     return request.param
 
 
