@@ -32,13 +32,37 @@ __host__ __device__ constexpr int f3_stage() {
   return (2 * NB * M > (M + 1) * (NB + 1)) ? 2 * NB * M : (M + 1) * (NB + 1);
 }
 template <int M, int NB, bool INV>
-__host__ __device__ constexpr int f13_smem_elems() {
-  return NB * M + (INV ? f3_stage<M, NB>() : f1_stage<M, NB>()) + M + (M + 1);
+__host__ __device__ constexpr int f13_smem_elems() {  // + NB twiddles w_N2^{y_a k_b} + NB/2 w_NB^r
+  return NB * M + (INV ? f3_stage<M, NB>() : f1_stage<M, NB>()) + M + (M + 1) + NB + NB / 2;
+}
+
+// resident CTAs per SM the shared-memory footprint allows (1 KB driver reserve per CTA), asked of
+// ptxas through __launch_bounds__ so registers do not become the tighter limit
+template <int M, int NB, bool INV>
+__host__ __device__ constexpr int f13_minb() {
+  return (f13_smem_elems<M, NB, INV>() * 16 + 1024) * 3 <= 228 * 1024   ? 3
+         : (f13_smem_elems<M, NB, INV>() * 16 + 1024) * 2 <= 228 * 1024 ? 2
+                                                                       : 1;
+}
+
+// Half of an NB-point DFT: the outputs k = 2m + h (m < NB/2) of X[k] = sum_r v_r w^{rk}
+// (w = w_NB, conjugated for INV) as an NB/2-point DFT of v_r + v_{r+NB/2} (h = 0) or of
+// (v_r - v_{r+NB/2}) w^r (h = 1).  Two threads per sequence keep every thread of the CTA busy
+// in the across-row DFT of F1/F3 (H1 = M + 1 sequences only).  twb[r] = w_NB^r, r < NB/2.
+template <int NB, bool INV>
+__device__ __forceinline__ void dft_half(const double2* v, int h, const double2* twb, double2* o) {
+  constexpr int NH = NB / 2;
+#pragma unroll
+  for (int r = 0; r < NH; ++r) {
+    const double2 a = v[r], b = v[r + NH];
+    o[r] = h == 0 ? cadd(a, b) : cmul(csub(a, b), INV ? cconj(twb[r]) : twb[r]);
+  }
+  dft_reg<NH, INV>(o);
 }
 
 // ------------------------------------------------------------------------------------- F1
 template <int M, int NB, int MODE>
-__global__ void __launch_bounds__(fft_threads_nt(M, NB / 8)) f1_kernel(Ctx cx, const double* __restrict__ src) {
+__global__ void __launch_bounds__(fft_threads_nt(M, NB / 8), f13_minb<M, NB, false>()) f1_kernel(Ctx cx, const double* __restrict__ src) {
   constexpr int NT = NB / 8;
   constexpr int T = fft_threads_nt(M, NT);
   constexpr int H1 = M + 1;
@@ -52,7 +76,8 @@ __global__ void __launch_bounds__(fft_threads_nt(M, NB / 8)) f1_kernel(Ctx cx, c
   double2* stage = tiles + NB * M;              // p rows, later X[kx][y_b]
   double2* tw = stage + f1_stage<M, NB>();      // M
   double2* twp = tw + M;                        // M + 1
-  double2* twy = twp + H1;                      // N2 (runtime)
+  double2* twa = twp + H1;                      // NB: w_N2^{y_a k_b}
+  double2* twb = twa + NB;                      // NB/2: w_NB^r
   __shared__ double red_sh[32];
   const int t = threadIdx.x;
   const int NA = g.NA, N2 = g.N2, N1 = g.N1;
@@ -79,7 +104,8 @@ __global__ void __launch_bounds__(fft_threads_nt(M, NB / 8)) f1_kernel(Ctx cx, c
   cp_commit();
   for (int i = t; i < M; i += T) tw[i] = cx.tw.x[i];
   for (int i = t; i <= M; i += T) twp[i] = cx.tw.xpost[i];
-  for (int i = t; i < N2; i += T) twy[i] = cx.tw.y[i];
+  if (t < NB) twa[t] = cx.tw.y[ya * t];
+  if (t < NB / 2) twb[t] = cx.tw.y[t * NA];
   cp_wait<0>();
   __syncthreads();
   double mx = 0.0;
@@ -121,15 +147,16 @@ __global__ void __launch_bounds__(fft_threads_nt(M, NB / 8)) f1_kernel(Ctx cx, c
   // NB-point DFT across the rows (y_b -> k_b), twiddle w_N2^{y_a k_b}, scatter to [kx][k_b][z][y_a]
   double2* out = cx.spec + ((long long)load * g.c + comp) * g.nspec + (long long)z * NA + ya;
   const long long kbstride = (long long)g.N3 * NA;
-  for (int kx = t; kx < H1; kx += T) {
-    double2 v[NB];
+  for (int it = t; it < 2 * H1; it += T) {
+    const int kx = it >> 1, h = it & 1;
+    double2 v[NB], o[NB / 2];
 #pragma unroll
     for (int r = 0; r < NB; ++r) v[r] = stage[kx * XS + r];
-    Dft<NB>::run(v);
+    dft_half<NB, false>(v, h, twb, o);
 #pragma unroll
-    for (int kb = 0; kb < NB; ++kb) {
-      const double2 w = twy[ya * kb];
-      out[((long long)kx * NB + kb) * kbstride] = kb ? cmul(v[kb], w) : v[kb];
+    for (int m = 0; m < NB / 2; ++m) {
+      const int kb = 2 * m + h;
+      out[((long long)kx * NB + kb) * kbstride] = kb ? cmul(o[m], twa[kb]) : o[m];
     }
   }
   if (MODE == CG) {
@@ -143,7 +170,7 @@ __global__ void __launch_bounds__(fft_threads_nt(M, NB / 8)) f1_kernel(Ctx cx, c
 
 // ------------------------------------------------------------------------------------- F3
 template <int M, int NB, int MODE>
-__global__ void __launch_bounds__(fft_threads_nt(M, NB / 8)) f3_kernel(Ctx cx, double* __restrict__ dst) {
+__global__ void __launch_bounds__(fft_threads_nt(M, NB / 8), f13_minb<M, NB, true>()) f3_kernel(Ctx cx, double* __restrict__ dst) {
   constexpr int NT = NB / 8;
   constexpr int T = fft_threads_nt(M, NT);
   constexpr int H1 = M + 1;
@@ -157,7 +184,8 @@ __global__ void __launch_bounds__(fft_threads_nt(M, NB / 8)) f3_kernel(Ctx cx, d
   double2* stage = tiles + NB * M;              // X[kx][k_b], later d rows | u rows
   double2* tw = stage + f3_stage<M, NB>();
   double2* twp = tw + M;
-  double2* twy = twp + H1;
+  double2* twa = twp + H1;  // NB: w_N2^{y_a k_b}
+  double2* twb = twa + NB;  // NB/2: w_NB^r
   const int t = threadIdx.x;
   const int NA = g.NA, N2 = g.N2, N1 = g.N1;
   const int ya = blockIdx.x % NA;
@@ -173,20 +201,32 @@ __global__ void __launch_bounds__(fft_threads_nt(M, NB / 8)) f3_kernel(Ctx cx, d
   cp_commit();
   for (int i = t; i < M; i += T) tw[i] = cx.tw.x[i];
   for (int i = t; i <= M; i += T) twp[i] = cx.tw.xpost[i];
-  for (int i = t; i < N2; i += T) twy[i] = cx.tw.y[i];
+  if (t < NB) twa[t] = cx.tw.y[ya * t];
+  if (t < NB / 2) twb[t] = cx.tw.y[t * NA];
   cp_wait<0>();
   __syncthreads();
-  // conj twiddle + inverse NB-point DFT (k_b -> y_b), in place
-  for (int kx = t; kx < H1; kx += T) {
-    double2 v[NB];
+  // conj twiddle + inverse NB-point DFT (k_b -> y_b), in place; two threads per kx (outputs
+  // y_b = 2m + h), so every round reads all inputs before anyone writes
+#pragma unroll 1
+  for (int i = 0; i < (2 * H1 + T - 1) / T; ++i) {
+    const int it = t + i * T;
+    const int kx = it >> 1, h = it & 1;
+    const bool act = it < 2 * H1;
+    double2 o[NB / 2];
+    if (act) {
+      double2 v[NB];
 #pragma unroll
-    for (int kb = 0; kb < NB; ++kb) {
-      const double2 a = stage[kx * XS + kb];
-      v[kb] = kb ? cmul(a, cconj(twy[ya * kb])) : a;
+      for (int kb = 0; kb < NB; ++kb) {
+        const double2 a = stage[kx * XS + kb];
+        v[kb] = kb ? cmul(a, cconj(twa[kb])) : a;
+      }
+      dft_half<NB, true>(v, h, twb, o);
     }
-    dft_reg<NB, true>(v);
+    __syncthreads();
+    if (act) {
 #pragma unroll
-    for (int r = 0; r < NB; ++r) stage[kx * XS + r] = v[r];
+      for (int m = 0; m < NB / 2; ++m) stage[kx * XS + 2 * m + h] = o[m];
+    }
   }
   __syncthreads();
   // C2R pre-processing of each row r into the x tiles
@@ -429,7 +469,7 @@ int launch_f1(const Ctx& cx, int mode, const double* src, cudaStream_t s) {
     constexpr int M = decltype(Mc)::value;
     return dispatch_nb(g.NB, [&](auto Bc) {
       constexpr int NB = decltype(Bc)::value;
-      const int sm = (f13_smem_elems<M, NB, false>() + g.N2) * 16;
+      const int sm = f13_smem_elems<M, NB, false>() * 16;
       const dim3 grid((unsigned)(g.NA * g.N3 * g.c), g.nrhs);
       auto go = [&](auto k) {
         set_smem3(k, sm);
@@ -447,7 +487,7 @@ int launch_f3(const Ctx& cx, int mode, double* dst, cudaStream_t s) {
     constexpr int M = decltype(Mc)::value;
     return dispatch_nb(g.NB, [&](auto Bc) {
       constexpr int NB = decltype(Bc)::value;
-      const int sm = (f13_smem_elems<M, NB, true>() + g.N2) * 16;
+      const int sm = f13_smem_elems<M, NB, true>() * 16;
       const dim3 grid((unsigned)(g.NA * g.N3 * g.c), g.nrhs);
       auto go = [&](auto k) {
         set_smem3(k, sm);

@@ -285,6 +285,64 @@ __global__ void __launch_bounds__(fft_threads(L), L == 256 ? UNO_YMINB : 1) ypas
   }
 }
 
+// y pass for N2 = 256, register-direct four-step (256 = 16 x 16, y = n1 + 16 n2,
+// k = k1 + 16 k2): each of 16 threads per row loads its 16 elements n1 + 16 n2 straight into
+// registers (coalesced across n1), does DFT16 over n2 and the twiddle w_256^{n1 k1}, one padded
+// shared-memory transpose, then DFT16 over n1 and stores X[k1 + 16 k2] straight from
+// registers.  One shared-memory round trip per element instead of four.
+constexpr int YR_R = 16, YR_ROWS = 8, YR_RS = YR_R * (YR_R + 1);
+template <bool INV, int MODE>
+__global__ void __launch_bounds__(YR_ROWS * YR_R) ypass256_kernel(Ctx cx, int z0, int zc) {
+  constexpr int L = 256;
+  const Geo g = cx.g;
+  const int load = blockIdx.y;
+  if (MODE == CG && !cx.st[load].active) return;
+  __shared__ double2 buf[YR_ROWS * YR_RS];
+  __shared__ double2 tw[L];
+  const int t = threadIdx.x;
+  const int r = t >> 4, lane16 = t & 15;
+  const long long nrows = (long long)g.c * g.H1 * g.N3;
+  long long row0 = (long long)blockIdx.x * YR_ROWS;  // row = (comp, kx, z)
+  if (zc > 0) {
+    const int nb = zc >> 3;
+    const int q = blockIdx.x / nb;
+    row0 = (long long)q * g.N3 + z0 + (blockIdx.x - q * nb) * 8;
+  }
+  const bool ok = row0 + r < nrows;
+  double2* rowp = cx.spec + (long long)load * g.c * g.nspec + (row0 + r) * L;
+  double2 v[YR_R];
+  if (ok) {
+#pragma unroll
+    for (int n2 = 0; n2 < YR_R; ++n2) v[n2] = __ldcg(rowp + lane16 + YR_R * n2);
+  }
+  for (int i = t; i < L; i += YR_ROWS * YR_R) tw[i] = cx.tw.y[i];
+  __syncthreads();
+  // stage 1 (thread = n1): DFT16 over n2 -> k1, twiddle w_256^{n1 k1}
+  dft_reg<YR_R, INV>(v);
+  {
+    const int n1 = lane16;
+#pragma unroll
+    for (int k1 = 1; k1 < YR_R; ++k1) {
+      const double2 w = tw[(n1 * k1) & (L - 1)];
+      v[k1] = cmul(v[k1], INV ? cconj(w) : w);
+    }
+#pragma unroll
+    for (int k1 = 0; k1 < YR_R; ++k1) buf[r * YR_RS + k1 * (YR_R + 1) + n1] = v[k1];
+  }
+  __syncthreads();
+  // stage 2 (thread = k1): DFT16 over n1 -> k2 ; X[k1 + 16 k2]
+  {
+    const int k1 = lane16;
+#pragma unroll
+    for (int n1 = 0; n1 < YR_R; ++n1) v[n1] = buf[r * YR_RS + k1 * (YR_R + 1) + n1];
+    dft_reg<YR_R, INV>(v);
+    if (ok) {
+#pragma unroll
+      for (int k2 = 0; k2 < YR_R; ++k2) __stcg(rowp + k1 + YR_R * k2, v[k2]);
+    }
+  }
+}
+
 template <int L, int NC>
 __host__ __device__ constexpr int gsmem_tile_bytes() {
   return (NC * 8 * L + L) * (int)sizeof(double2);
@@ -1768,6 +1826,22 @@ int launch_xinv(const Ctx& cx, int mode, double* dst, cudaStream_t s, int b0, in
 int launch_ypass(const Ctx& cx, int mode, bool inverse, cudaStream_t s, int z0, int zc) {
   const Geo& g = cx.g;
   if (zc > 0 && ((zc | z0) & 7)) return -1;
+  static const bool rd = [] {
+    const char* e = getenv("UNO_YRD");
+    return !(e && e[0] == '0');
+  }();
+  if (rd && g.N2 == 256) {
+    const long long nrows = zc > 0 ? (long long)g.c * g.H1 * zc : (long long)g.c * g.H1 * g.N3;
+    const dim3 grid((unsigned)((nrows + YR_ROWS - 1) / YR_ROWS), g.nrhs);
+    if (mode == CG) {
+      if (inverse) ypass256_kernel<true, CG><<<grid, YR_ROWS * YR_R, 0, s>>>(cx, z0, zc);
+      else ypass256_kernel<false, CG><<<grid, YR_ROWS * YR_R, 0, s>>>(cx, z0, zc);
+    } else {
+      if (inverse) ypass256_kernel<true, STANDALONE><<<grid, YR_ROWS * YR_R, 0, s>>>(cx, z0, zc);
+      else ypass256_kernel<false, STANDALONE><<<grid, YR_ROWS * YR_R, 0, s>>>(cx, z0, zc);
+    }
+    return 1;
+  }
   return dispatch_pow2(g.N2, [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
     const long long nrows = zc > 0 ? (long long)g.c * g.H1 * zc : (long long)g.c * g.H1 * g.N3;
