@@ -438,6 +438,74 @@ __global__ void __launch_bounds__(fft_threads(L), L == 256 ? UNO_GMINB : 1) gpas
   gamma_finish(cx, load, part, red_sh, MODE);
 }
 
+// Thermal G pass for N3 = 256, register-direct (same four-step as ypass256_kernel, along z):
+// tile = 8 consecutive y columns of one kx plane, thread (c, l) with c the column, l = n1 in the
+// loads / k1 after the first transpose.  Forward DFT16 (n2) -> twiddle -> transpose -> DFT16
+// (n1) leaves the bins k1 + 16 k2 in registers, where s_hat = G_hat r_hat and the Parseval
+// partial of gamma (Eq 46/49) are formed; the inverse mirrors the forward.  Column stride 273
+// (odd in 16-byte units) keeps every quarter-warp access bank-conflict free.
+constexpr int GR_CS = YR_R * (YR_R + 1) + 1;
+template <int MODE>
+__global__ void __launch_bounds__(8 * YR_R, 3) gpass256_kernel(Ctx cx) {  // smem: gpass256_smem
+  constexpr int L = 256, R = YR_R, RP = R + 1;
+  const Geo g = cx.g;
+  const int load = blockIdx.y;
+  if (MODE == CG && !cx.st[load].active) return;
+  extern __shared__ double2 gsm[];
+  double2* buf = gsm;                                          // [8][GR_CS]
+  double2* tw = buf + 8 * GR_CS;                               // [L]
+  double* gs = reinterpret_cast<double*>(tw + L);              // [L][8] symbol of the tile's bins
+  __shared__ double red_sh[32];
+  const int t = threadIdx.x, c = t & 7, ln = t >> 3;
+  const int ntile_y = g.N2 >> 3;
+  const int kx = blockIdx.x / ntile_y;
+  const int y0 = (blockIdx.x - kx * ntile_y) * 8;
+  const long long boff = (long long)kx * g.N3 * g.N2 + y0;
+  double2* col = cx.spec + (long long)load * g.nspec + boff + c;
+  const long long zs = g.N2;
+  // symbol of the tile lands in shared memory while the forward transform runs
+#pragma unroll
+  for (int i = 0; i < L * 8 / (2 * 8 * R); ++i) {  // 16-byte copies: 2 bins each
+    const int e = 2 * (t + i * 8 * R);
+    cp_async16(&gs[e], cx.gtab + boff + (long long)(e >> 3) * zs + (e & 7));
+  }
+  cp_commit();
+  double2 v[R];
+#pragma unroll
+  for (int n2 = 0; n2 < R; ++n2) v[n2] = __ldcg(col + (ln + R * n2) * zs);
+  for (int i = t; i < L; i += 8 * R) tw[i] = cx.tw.z[i];
+  __syncthreads();
+  double2* bc = buf + c * GR_CS;
+  dft_reg<R, false>(v);  // thread = n1: DFT over n2 -> k1
+#pragma unroll
+  for (int k1 = 1; k1 < R; ++k1) v[k1] = cmul(v[k1], tw[(ln * k1) & (L - 1)]);
+#pragma unroll
+  for (int k1 = 0; k1 < R; ++k1) bc[k1 * RP + ln] = v[k1];
+  __syncthreads();
+#pragma unroll
+  for (int n1 = 0; n1 < R; ++n1) v[n1] = bc[ln * RP + n1];
+  dft_reg<R, false>(v);  // thread = k1: v[k2] = r_hat(kz = k1 + 16 k2)
+  const double w = parseval_w(kx, g.M);
+  cp_wait<0>();
+  __syncthreads();
+  double part = 0.0;
+#pragma unroll
+  for (int k2 = 0; k2 < R; ++k2) part += gmul_vals<1>(&v[k2], gs + c, 0, (long long)(ln + R * k2) * 8, w);
+  dft_reg<R, true>(v);  // inverse over k2 -> n1 (thread = k1)
+#pragma unroll
+  for (int n1 = 1; n1 < R; ++n1) v[n1] = cmul(v[n1], cconj(tw[(ln * n1) & (L - 1)]));
+  __syncthreads();  // every stage-2 read of buf done
+#pragma unroll
+  for (int n1 = 0; n1 < R; ++n1) bc[n1 * RP + ln] = v[n1];
+  __syncthreads();
+#pragma unroll
+  for (int k1 = 0; k1 < R; ++k1) v[k1] = bc[ln * RP + k1];
+  dft_reg<R, true>(v);  // thread = n1: inverse over k1 -> n2
+#pragma unroll
+  for (int n2 = 0; n2 < R; ++n2) __stcg(col + (ln + R * n2) * zs, v[n2]);
+  gamma_finish(cx, load, part, red_sh, MODE);
+}
+
 // G pass along y (contiguous rows): 2D grids (rows = kx) and the mixed-BC schedule (rows = (kx, m),
 // m the DST-I mode along z, P3 planes); tile = 8 consecutive rows.
 template <int L, int NC, int MODE>
@@ -1862,6 +1930,22 @@ int launch_ypass(const Ctx& cx, int mode, bool inverse, cudaStream_t s, int z0, 
 
 int launch_gpass(const Ctx& cx, int mode, cudaStream_t s) {
   const Geo& g = cx.g;
+  static const bool rd = [] {
+    const char* e = getenv("UNO_GRD");
+    return !(e && e[0] == '0');
+  }();
+  if (rd && g.dim == 3 && !g.dirz && g.c == 1 && g.N3 == 256) {
+    const dim3 grid((unsigned)(g.H1 * (g.N2 / 8)), g.nrhs);
+    constexpr int sm = (8 * GR_CS + 256) * 16 + 256 * 8 * 8;
+    if (mode == CG) {
+      set_smem(gpass256_kernel<CG>, sm);
+      gpass256_kernel<CG><<<grid, 8 * YR_R, sm, s>>>(cx);
+    } else {
+      set_smem(gpass256_kernel<STANDALONE>, sm);
+      gpass256_kernel<STANDALONE><<<grid, 8 * YR_R, sm, s>>>(cx);
+    }
+    return 1;
+  }
   if (g.dim == 3 && !g.dirz) {
     return dispatch_pow2(g.N3, [&](auto Lc) {
       constexpr int L = decltype(Lc)::value;
