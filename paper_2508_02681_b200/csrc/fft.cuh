@@ -333,4 +333,20 @@ __device__ __forceinline__ void dft_reg(double2* v) {
   }
 }
 
+// Half of an NB-point DFT: the outputs k = 2m + h (m < NB/2) of X[k] = sum_r v_r w^{rk}
+// (w = w_NB, conjugated for INV) as an NB/2-point DFT of v_r + v_{r+NB/2} (h = 0) or of
+// (v_r - v_{r+NB/2}) w^r (h = 1).  Two threads per sequence keep every thread of the CTA busy
+// in the across-row DFT of F1/F3 (H1 = M + 1 sequences only) and in
+// the x pass (8 rows x 8 sequences of 16).  twb[r] = w_NB^r, r < NB/2.
+template <int NB, bool INV>
+__device__ __forceinline__ void dft_half(const double2* v, int h, const double2* twb, double2* o) {
+  constexpr int NH = NB / 2;
+#pragma unroll
+  for (int r = 0; r < NH; ++r) {
+    const double2 a = v[r], b = v[r + NH];
+    o[r] = h == 0 ? cadd(a, b) : cmul(csub(a, b), INV ? cconj(twb[r]) : twb[r]);
+  }
+  dft_reg<NH, INV>(o);
+}
+
 }  // namespace uno

@@ -127,6 +127,96 @@ __global__ void __launch_bounds__(fft_threads(M), M == 128 ? UNO_XMINB : 1) xfwd
   if (MODE == CG) partial_write<true>(cx, RED_RNORM, load, bx, mx, red_sh);
 }
 
+// F1 for N1 = 256, register-direct: the complex FFT of length M = 128 (z_j = r_2j + i r_2j+1)
+// as 8-point DFTs over n2 (j = n1 + 16 n2, thread = n1, 16 threads per row) -> twiddle
+// w_128^{n1 k1} -> padded transpose -> 16-point DFT over n1 split between two threads
+// (dft_half) -> X[k1 + 8 k2] to a swizzled row buffer -> R2C post-processing straight to the
+// half spectrum.  r -= alpha p, ||r||_inf and the r write-back happen on the registers loaded.
+constexpr int XR_RS = 8 * 17;             // transpose buffer per row (8 x 16, padded)
+constexpr int XR_XS = 129;                // X row stride (odd in 16-byte units)
+__device__ __forceinline__ int xr_swz(int k) { return k ^ (((k >> 3) & 1) << 2); }
+template <int MODE>
+__global__ void __launch_bounds__(128) xfwd256_kernel(Ctx cx, const double* __restrict__ src, int bofs) {
+  constexpr int M = 128;
+  const Geo g = cx.g;
+  const int load = blockIdx.y;
+  LoadState* st = cx.st + load;
+  if (MODE != STANDALONE && !st->active) return;
+  __shared__ double2 tb[8 * XR_RS];
+  __shared__ double2 xs[8 * XR_XS];
+  __shared__ double2 tw[M];
+  __shared__ double2 twp[M + 1];
+  __shared__ double2 tw16[8];  // w_16^r = w_128^{8r}
+  __shared__ double red_sh[32];
+  const int t = threadIdx.x;
+  const int r = t >> 4, l16 = t & 15;
+  const int bx = bofs + blockIdx.x;
+  const long long row0 = (long long)bx * 8;  // row = (comp, z, y)
+  const long long voff = (long long)load * g.c * g.n + (row0 + r) * g.N1;
+  const double2* s2 = reinterpret_cast<const double2*>(src + voff);
+  double2 v[8];
+#pragma unroll
+  for (int n2 = 0; n2 < 8; ++n2) v[n2] = __ldcg(s2 + l16 + 16 * n2);
+  double mx = 0.0;
+  if (MODE == CG) {
+    if (st->iters > 0) {  // r <- r - alpha p   (Alg 2 l.11)
+      const double alpha = st->alpha;
+      const double2* p2 = reinterpret_cast<const double2*>(cx.p + voff);
+      double2* r2 = reinterpret_cast<double2*>(cx.r + voff);
+      double2 pv[8];
+#pragma unroll
+      for (int n2 = 0; n2 < 8; ++n2) pv[n2] = __ldcs(p2 + l16 + 16 * n2);
+#pragma unroll
+      for (int n2 = 0; n2 < 8; ++n2) {
+        v[n2].x = fma(-alpha, pv[n2].x, v[n2].x);
+        v[n2].y = fma(-alpha, pv[n2].y, v[n2].y);
+        __stcg(r2 + l16 + 16 * n2, v[n2]);
+      }
+    }
+#pragma unroll
+    for (int n2 = 0; n2 < 8; ++n2) mx = fmax(mx, fmax(fabs(v[n2].x), fabs(v[n2].y)));
+  }
+  for (int i = t; i < M; i += 128) tw[i] = cx.tw.x[i];
+  for (int i = t; i <= M; i += 128) twp[i] = cx.tw.xpost[i];
+  if (t < 8) tw16[t] = cx.tw.x[8 * t];
+  __syncthreads();
+  // stage 1 (thread = n1): DFT8 over n2 -> k1, twiddle w_128^{n1 k1}
+  dft_reg<8, false>(v);
+#pragma unroll
+  for (int k1 = 1; k1 < 8; ++k1) v[k1] = cmul(v[k1], tw[(l16 * k1) & (M - 1)]);
+#pragma unroll
+  for (int k1 = 0; k1 < 8; ++k1) tb[r * XR_RS + k1 * 17 + l16] = v[k1];
+  __syncthreads();
+  // stage 2 (thread = (k1, h)): half of DFT16 over n1 -> k2 = 2m + h ; X[k1 + 8 k2]
+  {
+    const int k1 = l16 >> 1, h = l16 & 1;
+    double2 a[16], o[8];
+#pragma unroll
+    for (int n1 = 0; n1 < 16; ++n1) a[n1] = tb[r * XR_RS + k1 * 17 + n1];
+    dft_half<16, false>(a, h, tw16, o);
+#pragma unroll
+    for (int m = 0; m < 8; ++m) xs[r * XR_XS + xr_swz(k1 + 8 * (2 * m + h))] = o[m];
+  }
+  __syncthreads();
+  // R2C post-processing: bins k and M - k of row c
+  const int y0 = (int)(row0 % g.N2);
+  const long long zc = row0 / g.N2;
+  const int z = (int)(zc % g.P3);
+  const int comp = (int)(zc / g.P3);
+  double2* out = cx.spec + ((long long)load * g.c + comp) * g.nspec + (long long)z * g.N2 + y0;
+  const long long plane = (long long)g.P3 * g.N2;
+  for (int it = t; it < (M / 2 + 1) * 8; it += 128) {
+    const int c = it & 7, k = it >> 3;
+    const double2 a = xs[c * XR_XS + xr_swz(k)];
+    const double2 b = cconj(xs[c * XR_XS + xr_swz((M - k) & (M - 1))]);
+    const double2 E = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
+    const double2 O = mul_mi(make_double2(0.5 * (a.x - b.x), 0.5 * (a.y - b.y)));
+    __stcg(out + (long long)k * plane + c, cadd(E, cmul(twp[k], O)));
+    if (k != M - k) __stcg(out + (long long)(M - k) * plane + c, cadd(cconj(E), cmul(twp[M - k], cconj(O))));
+  }
+  if (MODE == CG) partial_write<true>(cx, RED_RNORM, load, bx, mx, red_sh);
+}
+
 // F5 / standalone inverse: half spectrum -> real rows; CG epilogue d = s + beta d, u += alpha d_old.
 template <int M, int MODE>
 __global__ void __launch_bounds__(fft_threads(M)) xinv_kernel(Ctx cx, double* __restrict__ dst, int bofs) {
@@ -1847,6 +1937,16 @@ static void set_smem(K kernel, int bytes) {
 
 int launch_xfwd(const Ctx& cx, int mode, const double* src, cudaStream_t s, int b0, int nb) {
   const Geo& g = cx.g;
+  static const bool rd = [] {
+    const char* e = getenv("UNO_XRD");
+    return !(e && e[0] == '0');
+  }();
+  if (rd && g.N1 == 256 && mode != PLAIN) {
+    const dim3 grid(nb > 0 ? (unsigned)nb : (unsigned)((long long)g.c * g.P3 * g.N2 / 8), g.nrhs);
+    if (mode == CG) xfwd256_kernel<CG><<<grid, 128, 0, s>>>(cx, src, b0);
+    else xfwd256_kernel<STANDALONE><<<grid, 128, 0, s>>>(cx, src, b0);
+    return 1;
+  }
   return dispatch_pow2(g.M, [&](auto Lc) {
     constexpr int M = decltype(Lc)::value;
     const dim3 grid(nb > 0 ? (unsigned)nb : (unsigned)((long long)g.c * g.P3 * g.N2 / 8), g.nrhs);
