@@ -1445,20 +1445,43 @@ __global__ void __launch_bounds__(256) kp_elastic2d_kernel(Ctx cx, int mode, con
 // ============================================================================== RHS (Eq 76 / 81)
 // f_(i,alpha) = -(h^(d-1)/2^(d-1)) sum_o sum_j s_j(o) sigma^o_(alpha j),  s_j(o) = +1 if o_j = 0 else -1,
 // sigma^o = kappa_o g_bar (thermal, alpha = 0) or lambda_o tr(eps) I + 2 mu_o eps (elastic).
-// The factor of each (phase, load, component, octant) is tabulated once per CTA in shared memory
-// (W[ph][l][alpha][o]); a node then sums 2^d table entries selected by its octant phases.
-__device__ void rhs_weights(const Ctx& cx, const LoadParams& lp, double* W /* [2][nrhs][c][8] */) {
+
+// octant phases of node i (stored index), shift-based decode (N1, N2 powers of two)
+__device__ __forceinline__ unsigned node_octants(const Ctx& cx, long long i, int& z) {
+  const Geo& g = cx.g;
+  const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
+  const int s1 = __ffs(N1) - 1, s2 = __ffs(N2) - 1;
+  const int x = (int)(i & (N1 - 1));
+  const int y = (int)((i >> s1) & (N2 - 1));
+  z = (int)(i >> (s1 + s2)) + g.dirz;  // Dirichlet z: stored planes are nodes 1..N3-1
+  unsigned bits = 0;
+  const int no = 1 << g.dim;
+#pragma unroll
+  for (int o = 0; o < 8; ++o) {
+    if (o >= no) break;
+    const int ox = o & 1, oy = (o >> 1) & 1, oz = (o >> 2) & 1;
+    const int ex = (x - 1 + ox) & (N1 - 1), ey = (y - 1 + oy) & (N2 - 1);
+    const int ez = g.dim == 3 ? (z - 1 + oz + N3) % N3 : 0;
+    bits |= (__ldg(cx.phase + ((long long)ez * N2 + ey) * N1 + ex) ? 1u : 0u) << o;
+  }
+  return bits;
+}
+
+// Since sum_o s_j(o) = 0, only the phase contrast survives: with the per-node integers
+//   n_j = sum_o s_j(o) [phase_o = 1]   (in [-2^(d-1), 2^(d-1)]),
+// f_(i,alpha) = sum_j C[l][alpha][j] n_j with C = -(h^(d-1)/2^(d-1)) * { (k1 - k0) g_bar_j  (thermal);
+// (lam1 - lam0) tr(eps) delta_(alpha j) + 2 (mu1 - mu0) eps_(alpha j)  (elastic) }.
+__device__ void rhs_coef(const Ctx& cx, const LoadParams& lp, double* C /* [nrhs][c][3] */) {
   const Geo& g = cx.g;
   const int d = g.dim, c = g.c, nl = g.nrhs;
   const double scale = (d == 3 ? g.h * g.h / 4.0 : g.h / 2.0);
   const double rt2 = 0.70710678118654752440;
-  for (int idx = threadIdx.x; idx < 2 * nl * c * 8; idx += blockDim.x) {
-    const int o = idx & 7, al = (idx >> 3) % c, l = (idx >> 3) / c % nl, ph = (idx >> 3) / (c * nl);
-    double acc = 0.0;
-    if (o < (1 << d)) {
+  for (int idx = threadIdx.x; idx < nl * c * 3; idx += blockDim.x) {
+    const int j = idx % 3, al = (idx / 3) % c, l = idx / (3 * c);
+    double v = 0.0;
+    if (j < d) {
       if (c == 1) {
-        for (int j = 0; j < d; ++j) acc += ((o >> j) & 1) ? -lp.v[l][j] : lp.v[l][j];
-        acc *= cx.mat[ph][0];
+        v = (cx.mat[1][0] - cx.mat[0][0]) * lp.v[l][j];
       } else {
         double e[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
         if (d == 3) {
@@ -1471,50 +1494,71 @@ __device__ void rhs_weights(const Ctx& cx, const LoadParams& lp, double* W /* [2
           e[0][1] = e[1][0] = lp.v[l][2] * rt2;
         }
         const double tr = e[0][0] + e[1][1] + e[2][2];
-        const double lam = cx.mat[ph][0], mu = cx.mat[ph][1];
-        for (int j = 0; j < d; ++j) {
-          const double sig = (al == j ? lam * tr : 0.0) + 2.0 * mu * e[al][j];
-          acc += ((o >> j) & 1) ? -sig : sig;
-        }
+        v = (al == j ? (cx.mat[1][0] - cx.mat[0][0]) * tr : 0.0) + 2.0 * (cx.mat[1][1] - cx.mat[0][1]) * e[al][j];
       }
     }
-    W[idx] = -scale * acc;
+    C[idx] = -scale * v;
   }
   __syncthreads();
 }
 
-// octant phases of node i (stored index), shift-based decode (N1, N2 powers of two)
-__device__ __forceinline__ unsigned node_octants(const Ctx& cx, long long i, int& z) {
+// Warp variant for 3D grids with N1 % 32 == 0: the 32 lanes hold 32 consecutive x of one row,
+// so every lane loads only the 4 voxels (x, y-1..y, z-1..z) and takes the x-1 voxels from its
+// left neighbour (lane 0 loads them itself).  All 32 lanes must be active.
+__device__ __forceinline__ unsigned node_octants_warp(const Ctx& cx, long long i, int& z) {
   const Geo& g = cx.g;
   const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
   const int s1 = __ffs(N1) - 1, s2 = __ffs(N2) - 1;
+  const int lane = threadIdx.x & 31;
   const int x = (int)(i & (N1 - 1));
   const int y = (int)((i >> s1) & (N2 - 1));
-  z = (int)(i >> (s1 + s2)) + g.dirz;  // Dirichlet z: stored planes are nodes 1..N3-1
-  unsigned bits = 0;
-  const int no = 1 << g.dim;
-  for (int o = 0; o < no; ++o) {
-    const int ox = o & 1, oy = (o >> 1) & 1, oz = (o >> 2) & 1;
-    const int ex = (x - 1 + ox) & (N1 - 1), ey = (y - 1 + oy) & (N2 - 1);
-    const int ez = g.dim == 3 ? (z - 1 + oz + N3) % N3 : 0;
-    bits |= (__ldg(cx.phase + ((long long)ez * N2 + ey) * N1 + ex) ? 1u : 0u) << o;
+  z = (int)(i >> (s1 + s2)) + g.dirz;
+  const int ym = (y - 1) & (N2 - 1);
+  const int zm = g.dirz ? z - 1 : ((z - 1) & (N3 - 1));
+  const int zp = z;  // voxel layer z (node planes 0..N3-1 periodic, 1..N3-1 Dirichlet: no wrap)
+  const uint8_t* p00 = cx.phase + ((long long)zm * N2 + ym) * N1;  // [oz=0][oy=0]
+  const uint8_t* p01 = cx.phase + ((long long)zm * N2 + y) * N1;   // [oz=0][oy=1]
+  const uint8_t* p10 = cx.phase + ((long long)zp * N2 + ym) * N1;  // [oz=1][oy=0]
+  const uint8_t* p11 = cx.phase + ((long long)zp * N2 + y) * N1;   // [oz=1][oy=1]
+  const unsigned b00 = __ldg(p00 + x) != 0, b01 = __ldg(p01 + x) != 0, b10 = __ldg(p10 + x) != 0,
+                 b11 = __ldg(p11 + x) != 0;
+  // octant o = ox + 2 oy + 4 oz; ox = 1 is voxel x, ox = 0 voxel x - 1
+  unsigned hi = (b00 << 1) | (b01 << 3) | (b10 << 5) | (b11 << 7);
+  unsigned lo = __shfl_up_sync(0xffffffffu, hi, 1) >> 1;
+  if (lane == 0) {
+    const int xm = (x - 1) & (N1 - 1);
+    lo = (__ldg(p00 + xm) != 0) | ((__ldg(p01 + xm) != 0) << 2) | ((__ldg(p10 + xm) != 0) << 4) |
+         ((__ldg(p11 + xm) != 0) << 6);
   }
-  return bits;
+  return hi | lo;
+}
+
+__device__ __forceinline__ void octant_counts(unsigned bits, int d, int n[3]) {
+  n[0] = n[1] = n[2] = 0;
+#pragma unroll
+  for (int o = 0; o < 8; ++o) {  // bits of absent octants (2D: o >= 4) are zero
+    const int b = (bits >> o) & 1;
+    n[0] += (o & 1) ? -b : b;
+    n[1] += (o & 2) ? -b : b;
+    n[2] += (o & 4) ? -b : b;
+  }
+  if (d == 2) n[2] = 0;
 }
 
 __global__ void __launch_bounds__(256) rhs_kernel(Ctx cx, LoadParams lp, double* __restrict__ f) {
-  __shared__ double W[2 * kMaxRhs * 3 * 8];
+  __shared__ double C[kMaxRhs * 3 * 3];
   const Geo g = cx.g;
-  rhs_weights(cx, lp, W);
-  const int nl = g.nrhs, c = g.c, no = 1 << g.dim;
+  rhs_coef(cx, lp, C);
+  const int nl = g.nrhs, c = g.c;
+  const bool warp_ok = g.dim == 3 && (g.N1 & 31) == 0;  // block-uniform
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += (long long)gridDim.x * blockDim.x) {
-    int z;
-    const unsigned bits = node_octants(cx, i, z);
+    int z, n[3];
+    octant_counts(warp_ok ? node_octants_warp(cx, i, z) : node_octants(cx, i, z), g.dim, n);
+    const double n0 = n[0], n1 = n[1], n2 = n[2];
     for (int l = 0; l < nl; ++l)
       for (int al = 0; al < c; ++al) {
-        double acc = 0.0;
-        for (int o = 0; o < no; ++o) acc += W[(((bits >> o) & 1) * nl * c + l * c + al) * 8 + o];
-        f[((long long)l * c + al) * g.n + i] = acc;
+        const double* Cr = C + (l * c + al) * 3;
+        f[((long long)l * c + al) * g.n + i] = fma(Cr[0], n0, fma(Cr[1], n1, Cr[2] * n2));
       }
   }
 }
@@ -1563,44 +1607,58 @@ __global__ void mean_subtract_kernel(const double* __restrict__ src, double* __r
 }
 
 // ============================================================================== effective property
-// acc[i][j] = f^(i) . u^(j) (f recomputed per node from the weight table); plus the count of
-// phase-1 voxels for <C>.
+// acc[i][j] = f^(i) . u^(j) (f recomputed per node, never stored); plus the count of phase-1
+// voxels for <C>.
 constexpr int EFF_T = 256;
-template <int NL>
-__global__ void __launch_bounds__(EFF_T) effective_kernel(Ctx cx, LoadParams lp, const double* __restrict__ u,
-                                                          double* partials) {
-  __shared__ double W[2 * kMaxRhs * 3 * 8];
+// Same quantity through the octant counts: f^(li) . u^(lj) = sum_(alpha, j) C[li][alpha][j] T[lj][alpha][j],
+// T[lj][alpha][j] = sum_nodes n_j u^(lj)_alpha accumulated per thread and contracted at the end.
+template <int NL, int CC>
+__global__ void __launch_bounds__(EFF_T) effective_n_kernel(Ctx cx, LoadParams lp, const double* __restrict__ u,
+                                                            double* partials) {
+  __shared__ double C[kMaxRhs * 3 * 3];
   __shared__ double sh[32];
   const Geo g = cx.g;
-  rhs_weights(cx, lp, W);
-  const int c = g.c, no = 1 << g.dim;
-  double acc[NL * NL + 1];
+  rhs_coef(cx, lp, C);
+  double T[NL][CC][3];
 #pragma unroll
-  for (int a = 0; a < NL * NL + 1; ++a) acc[a] = 0.0;
+  for (int l = 0; l < NL; ++l)
+#pragma unroll
+    for (int a = 0; a < CC; ++a) T[l][a][0] = T[l][a][1] = T[l][a][2] = 0.0;
+  double cnt = 0.0;
+  const int no = 1 << g.dim;
+  const bool warp_ok = g.dim == 3 && (g.N1 & 31) == 0;  // block-uniform
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < g.n; i += (long long)gridDim.x * blockDim.x) {
-    int z;
-    const unsigned bits = node_octants(cx, i, z);
-    acc[NL * NL] += (bits >> (no - 1)) & 1;  // voxel i is octant (1,1,1) of node i: each voxel once
-    if (g.dirz && z == 1) acc[NL * NL] += (bits >> 3) & 1;  // Dirichlet z: voxel layer 0
-    for (int al = 0; al < c; ++al) {
-      double uv[NL];
+    int z, n[3];
+    const unsigned bits = warp_ok ? node_octants_warp(cx, i, z) : node_octants(cx, i, z);
+    cnt += (bits >> (no - 1)) & 1;  // voxel i is octant (1,1,1) of node i: each voxel once
+    if (g.dirz && z == 1) cnt += (bits >> 3) & 1;  // Dirichlet z: voxel layer 0
+    octant_counts(bits, g.dim, n);
+    const double n0 = n[0], n1 = n[1], n2 = n[2];
 #pragma unroll
-      for (int lj = 0; lj < NL; ++lj) uv[lj] = u[((long long)lj * c + al) * g.n + i];
+    for (int l = 0; l < NL; ++l)
 #pragma unroll
-      for (int li = 0; li < NL; ++li) {
-        double fi = 0.0;
-        for (int o = 0; o < no; ++o) fi += W[(((bits >> o) & 1) * NL * c + li * c + al) * 8 + o];
-#pragma unroll
-        for (int lj = 0; lj < NL; ++lj) acc[li * NL + lj] = fma(fi, uv[lj], acc[li * NL + lj]);
+      for (int a = 0; a < CC; ++a) {
+        const double uv = u[((long long)l * CC + a) * g.n + i];
+        T[l][a][0] = fma(n0, uv, T[l][a][0]);
+        T[l][a][1] = fma(n1, uv, T[l][a][1]);
+        T[l][a][2] = fma(n2, uv, T[l][a][2]);
       }
-    }
   }
 #pragma unroll
-  for (int a = 0; a < NL * NL + 1; ++a) {
-    const double b = block_reduce<false>(acc[a], sh);
-    if (threadIdx.x == 0) partials[(long long)a * gridDim.x + blockIdx.x] = b;
-    __syncthreads();
-  }
+  for (int li = 0; li < NL; ++li)
+#pragma unroll
+    for (int lj = 0; lj < NL; ++lj) {
+      double acc = 0.0;
+#pragma unroll
+      for (int a = 0; a < CC; ++a)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) acc = fma(C[(li * CC + a) * 3 + j], T[lj][a][j], acc);
+      const double b = block_reduce<false>(acc, sh);
+      if (threadIdx.x == 0) partials[(long long)(li * NL + lj) * gridDim.x + blockIdx.x] = b;
+      __syncthreads();
+    }
+  const double b = block_reduce<false>(cnt, sh);
+  if (threadIdx.x == 0) partials[(long long)(NL * NL) * gridDim.x + blockIdx.x] = b;
 }
 
 __global__ void combine_rows_kernel(const double* partials, int nblk, double* out) {
@@ -1641,7 +1699,12 @@ __global__ void build_symbol_kernel(Ctx cx, double* gtab, double ref0, double re
     const int kb = (int)((b / ((long long)g.NA * N3)) % g.NB);
     kx = (int)(b / ((long long)g.NA * N3 * g.NB));
     ky = kb + g.NB * ka;
-  } else {         // 5-pass / mixed layout [kx][kz or sine plane][ky]
+  } else if (!g.dirz) {  // 5-pass layout [kx][kz][ky]: powers of two, shifts only
+    const int s2 = __ffs(N2) - 1, s3 = __ffs(N3) - 1;
+    ky = (int)(b & (N2 - 1));
+    kz = (int)((b >> s2) & (N3 - 1));
+    kx = (int)(b >> (s2 + s3));
+  } else {         // mixed layout [kx][sine plane][ky]
     ky = (int)(b % N2);
     kz = (int)((b / N2) % g.P3);
     kx = (int)(b / ((long long)N2 * g.P3));
@@ -1667,13 +1730,27 @@ __global__ void build_symbol_kernel(Ctx cx, double* gtab, double ref0, double re
     axis_trig(kz, N3, cs[2], sn[2]);
     inv_n = 1.0 / (double)g.n;
     flat = ((unsigned long long)kz * N2 + ky) * N1 + kx;
-    flatm = ((unsigned long long)((N3 - kz) % N3) * N2 + (unsigned long long)((N2 - ky) % N2)) * N1 +
-            (unsigned long long)((N1 - kx) % N1);
+    flatm = ((unsigned long long)((N3 - kz) & (N3 - 1)) * N2 + (unsigned long long)((N2 - ky) & (N2 - 1))) * N1 +
+            (unsigned long long)((N1 - kx) & (N1 - 1));
     zero = (kx == 0 && ky == 0 && kz == 0);
   }
   const double h = g.h;
   const long long ns = g.nspec;
   const unsigned long long canon = flat < flatm ? flat : flatm;
+  if (g.c == 1 && d == 3) {  // thermal 3D in scalars (same operation order as the general path)
+    const double m0 = (h / 3.0) * (2.0 + cs[0]), m1 = (h / 3.0) * (2.0 + cs[1]), m2 = (h / 3.0) * (2.0 + cs[2]);
+    const double S00 = (2.0 / h) * (1.0 - cs[0]) * m1 * m2;
+    const double S11 = (2.0 / h) * (1.0 - cs[1]) * m0 * m2;
+    const double S22 = (2.0 / h) * (1.0 - cs[2]) * m0 * m1;
+    const double a = (((0.0 + S00) + S11) + S22) * ref0;
+    double gv = 0.0;
+    if (!zero) {
+      const double rho = seed ? (1.0 - amp + 2.0 * amp * u01(seed, 2, canon)) : 1.0;
+      gv = rho / a * inv_n;
+    }
+    gtab[b] = gv;
+    return;
+  }
   double mass[3], S[3][3];
   for (int i = 0; i < d; ++i) mass[i] = (h / 3.0) * (2.0 + cs[i]);
   for (int i = 0; i < d; ++i) {
@@ -2186,17 +2263,23 @@ int launch_mean_removal(const Ctx& cx, const double* u, double* out, double* scr
 
 int launch_effective(const Ctx& cx, const LoadParams& lp, const double* u, double* partials, int* nblocks_out,
                      cudaStream_t s) {
-  const int nblk = 148 * 2;
+  const int nblk = 148 * 4;
   const int nacc = cx.g.nrhs * cx.g.nrhs + 1;
+  auto pick = [&](auto nlc) {
+    constexpr int NL = decltype(nlc)::value;
+    if (cx.g.c == 1) effective_n_kernel<NL, 1><<<nblk, EFF_T, 0, s>>>(cx, lp, u, partials);
+    else if (cx.g.c == 2) effective_n_kernel<NL, 2><<<nblk, EFF_T, 0, s>>>(cx, lp, u, partials);
+    else effective_n_kernel<NL, 3><<<nblk, EFF_T, 0, s>>>(cx, lp, u, partials);
+  };
   switch (cx.g.nrhs) {
-    case 1: effective_kernel<1><<<nblk, EFF_T, 0, s>>>(cx, lp, u, partials); break;
-    case 2: effective_kernel<2><<<nblk, EFF_T, 0, s>>>(cx, lp, u, partials); break;
-    case 3: effective_kernel<3><<<nblk, EFF_T, 0, s>>>(cx, lp, u, partials); break;
-    case 4: effective_kernel<4><<<nblk, EFF_T, 0, s>>>(cx, lp, u, partials); break;
-    case 5: effective_kernel<5><<<nblk, EFF_T, 0, s>>>(cx, lp, u, partials); break;
-    case 6: effective_kernel<6><<<nblk, EFF_T, 0, s>>>(cx, lp, u, partials); break;
-    case 7: effective_kernel<7><<<nblk, EFF_T, 0, s>>>(cx, lp, u, partials); break;
-    default: effective_kernel<8><<<nblk, EFF_T, 0, s>>>(cx, lp, u, partials); break;
+    case 1: pick(std::integral_constant<int, 1>{}); break;
+    case 2: pick(std::integral_constant<int, 2>{}); break;
+    case 3: pick(std::integral_constant<int, 3>{}); break;
+    case 4: pick(std::integral_constant<int, 4>{}); break;
+    case 5: pick(std::integral_constant<int, 5>{}); break;
+    case 6: pick(std::integral_constant<int, 6>{}); break;
+    case 7: pick(std::integral_constant<int, 7>{}); break;
+    default: pick(std::integral_constant<int, 8>{}); break;
   }
   combine_rows_kernel<<<nacc, 256, 0, s>>>(partials, nblk, partials + (long long)nacc * nblk);
   *nblocks_out = nblk;

@@ -322,7 +322,7 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
   const int maxb = blocks_needed_max(g);
   h->hist_stride = 0;
   h->scratch_len = (size_t)std::max<long long>(
-      (long long)(kMaxRhs * kMaxRhs + 1) * 148 * 2 * 2 + 64,
+      (long long)(kMaxRhs * kMaxRhs + 1) * (148 * 4 + 1) * 2 + 64,
       (long long)g.nrhs * c * 148 * 2 + g.nrhs * c + 64);
   if ((e = al((void**)&h->r, vec * 8)) || (e = al((void**)&h->d, vec * 8)) || (e = al((void**)&h->p, vec * 8)) ||
       (e = al((void**)&h->u, vec * 8)) || (e = al((void**)&h->spec, (size_t)g.nrhs * c * g.nspec * 16)) ||
