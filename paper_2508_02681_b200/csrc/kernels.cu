@@ -872,6 +872,7 @@ __global__ void __launch_bounds__(TX * KT_TY, 3) kp_thermal3d_kernel(Ctx cx, int
 // sums and conductivities, so a thread reads a 4x3 block of the next plane (12 loads) and
 // 6 conductivities per plane for 2 nodes, and the per-plane bookkeeping (cp.async issue,
 // phase fetch, barrier) is amortised over twice the work.
+constexpr int KR2_DW = 36, KR2_DPL = 10 * KR2_DW, KR2_PW = 64, KR2_PHS = 9 * KR2_PW;
 struct KR2State {   // everything a thread carries from node plane k to k+1 (two node rows)
   double Qk[3][2];                       // box sums of element rows 0..2 (cols 0,1), plane k
   double KSlo[2], Klo[2], Kxlo[2], Kylo[2];  // layer k-1 sums for node 0 / node 1
@@ -883,10 +884,15 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
                                                                           const double* __restrict__ src,
                                                                           double* __restrict__ dst, int ZC,
                                                                           int zc0, int nzl) {
+  static_assert(TX == 32, "16-byte staging assumes a 32-wide tile");
   constexpr int T = TX * KT_TY / 2;
-  constexpr int DW = TX + 2, DP = 10 * DW;
-  constexpr int EW = TX + 1, EP = 9 * EW;
-  constexpr int ND = (DP + T - 1) / T;
+  constexpr int DW = KR2_DW;              // staged d row: x0-2 .. x0+33 (16-byte aligned copies)
+  constexpr int DPL = KR2_DPL;            // doubles per ring slot (10 rows)
+  constexpr int NCH = 10 * (DW / 2);      // 16-byte chunks of d per plane
+  constexpr int NDC = (NCH + T - 1) / T;  // per thread
+  constexpr int PW = KR2_PW;              // staged phase row: x0-16 .. x0+47 (bytes)
+  constexpr int PHS = KR2_PHS;            // phase bytes per ring slot (9 rows)
+  constexpr int NPC = PHS / 16;           // 16-byte chunks of phase per plane
   const Geo g = cx.g;
   const int nzc = (g.P3 + ZC - 1) / ZC;
   const int load = blockIdx.z / nzl;                // launch covers z-chunks [zc0, zc0 + nzl)
@@ -894,10 +900,9 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
   const int dz = g.dirz;  // Dirichlet z: node planes 1..N3-1 stored at index p-1; planes 0, N3 are zero
   if (mode == CG && !cx.st[load].active) return;
   extern __shared__ double ksm[];
-  double* D = ksm;                      // [KT_RING][ND*T] (padded: every thread copies ND elements)
-  // phase bytes of element layer p-1 travel with node plane p: 9 rows x 36 bytes (x0-4 .. x0+31)
-  unsigned char* PH = reinterpret_cast<unsigned char*>(D + KT_RING * ND * T);  // [KT_RING][9*36]
-  constexpr int PHS = 9 * 36;
+  double* D = ksm;  // [KT_RING][10][DW]
+  // phase bytes of element layer p-1 travel with node plane p
+  unsigned char* PH = reinterpret_cast<unsigned char*>(D + KT_RING * DPL);  // [KT_RING][9][PW]
   __shared__ double red_sh[32];
   const int t = threadIdx.x;
   const int tx = t % TX, ty = t / TX;   // node rows 2ty, 2ty+1 of the tile
@@ -907,43 +912,45 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
   const long long plane = (long long)N1 * N2;
   const double* dv = src + (long long)load * g.n;
   const double k0 = cx.mat[0][0], k1 = cx.mat[1][0];
-  // per-thread copy assignment (indices past the tile are clamped: harmless duplicate copies)
-  int goffD[ND];
-  unsigned sD[ND];
+  // per-thread 16-byte copy assignment (indices past the tile are clamped: harmless duplicates);
+  // x pairs start at even x so every chunk stays contiguous across the periodic wrap
+  int goffD[NDC];
+  unsigned sD[NDC];
 #pragma unroll
-  for (int m = 0; m < ND; ++m) {
-    const int j = min(t + m * T, DP - 1);
-    const int ly = j / DW, lx = j - ly * DW;
-    goffD[m] = ((y0 - 1 + ly + N2) & (N2 - 1)) * N1 + ((x0 - 1 + lx + N1) & (N1 - 1));
-    sD[m] = (unsigned)__cvta_generic_to_shared(D + t + m * T);
+  for (int m = 0; m < NDC; ++m) {
+    const int j = min(t + m * T, NCH - 1);
+    const int ly = j / (DW / 2), q = j - ly * (DW / 2);
+    goffD[m] = ((y0 - 1 + ly + N2) & (N2 - 1)) * N1 + ((x0 - 2 + 2 * q + N1) & (N1 - 1));
+    sD[m] = (unsigned)__cvta_generic_to_shared(D + ly * DW + 2 * q);
   }
-  // phase words: thread t < 81 copies 4 bytes of row t/9, word t%9
-  const bool phw = t < 81;
+  const bool phw = t < NPC;
   const int pj = phw ? t : 0;
-  const int poff = ((y0 - 1 + pj / 9 + N2) & (N2 - 1)) * N1 + ((x0 - 4 + 4 * (pj % 9) + N1) & (N1 - 1));
-  const unsigned psm = (unsigned)__cvta_generic_to_shared(PH + 4 * pj);
-  constexpr unsigned SLOTB = ND * T * 8;  // bytes per D ring slot
+  const int prow = pj / (PW / 16), pq = pj - prow * (PW / 16);
+  const int poff = ((y0 - 1 + prow + N2) & (N2 - 1)) * N1 + ((x0 - 16 + 16 * pq + N1) & (N1 - 1));
+  const unsigned psm = (unsigned)__cvta_generic_to_shared(PH + prow * PW + 16 * pq);
+  constexpr unsigned SLOTB = DPL * 8;  // bytes per D ring slot
   auto issue_plane = [&](int p) {  // node plane p of d and phase layer p-1 -> ring slot
     const unsigned slot = (p - zs + 1) & (KT_RING - 1);
     const unsigned so = slot * SLOTB;
     if (dz && (p <= 0 || p >= N3)) {  // fixed (zero) Dirichlet node plane (Fig 4)
 #pragma unroll
-      for (int m = 0; m < ND; ++m) asm volatile("st.shared.f64 [%0], 0d0000000000000000;\n" ::"r"(sD[m] + so) : "memory");
+      for (int m = 0; m < NDC; ++m)
+        asm volatile("st.shared.v2.f64 [%0], {0d0000000000000000, 0d0000000000000000};\n" ::"r"(sD[m] + so) : "memory");
     } else {
       const int zw = dz ? p - 1 : ((p + N3) & (N3 - 1));
       const double* base = dv + (long long)zw * plane;
 #pragma unroll
-      for (int m = 0; m < ND; ++m)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sD[m] + so), "l"(base + goffD[m]) : "memory");
+      for (int m = 0; m < NDC; ++m)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sD[m] + so), "l"(base + goffD[m]) : "memory");
     }
     if (phw) {
       const uint8_t* pb = cx.phase + (long long)((p - 1 + N3) & (N3 - 1)) * plane + poff;
-      asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(psm + slot * PHS), "l"(pb) : "memory");
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(psm + slot * PHS), "l"(pb) : "memory");
     }
   };
   double nb[4][3];
   auto read4x3 = [&](int p) {
-    const double* Ds = D + ((p - zs + 1) & (KT_RING - 1)) * (ND * T) + 2 * ty * DW + tx;
+    const double* Ds = D + ((p - zs + 1) & (KT_RING - 1)) * DPL + 2 * ty * DW + tx + 1;
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -963,11 +970,11 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
     }
   };
   auto kap6 = [&](int layer, double a[3][2]) {  // layer travels with plane layer+1
-    const unsigned char* Pl = PH + ((layer + 1 - zs + 1) & (KT_RING - 1)) * PHS + 2 * ty * 36 + tx + 3;
+    const unsigned char* Pl = PH + ((layer + 1 - zs + 1) & (KT_RING - 1)) * PHS + 2 * ty * PW + tx + 15;
 #pragma unroll
     for (int e = 0; e < 3; ++e) {
-      a[e][0] = Pl[e * 36] ? k1 : k0;
-      a[e][1] = Pl[e * 36 + 1] ? k1 : k0;
+      a[e][0] = Pl[e * PW] ? k1 : k0;
+      a[e][1] = Pl[e * PW + 1] ? k1 : k0;
     }
   };
   static_assert(LA >= 2 && LA < KT_RING, "ring slot of plane k+LA must not be read at step k-1");
@@ -2195,8 +2202,7 @@ int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaS
       set_smem(kp_thermal3d_tma_kernel, smb);
       kp_thermal3d_tma_kernel<<<grid, 256, smb, s>>>(cx, mode, src, dst, ZC);
     } else if (TX == 32) {
-      constexpr int T2 = 128, ND2 = (10 * 34 + T2 - 1) / T2;
-      const int sm2 = KT_RING * ND2 * T2 * (int)sizeof(double) + KT_RING * 9 * 36;
+      const int sm2 = KT_RING * (KR2_DPL * (int)sizeof(double) + KR2_PHS);
       static const int la = [] {
         const char* e = getenv("UNO_KLA");
         return e ? atoi(e) : 4;
