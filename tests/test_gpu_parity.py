@@ -234,6 +234,34 @@ def test_full_size_config3_fixed_iterations():
     assert rel(u[0], ref["U"][0]) <= 1e-11
 
 
+_FULL_REF = {}
+
+
+def _full_size_reference():
+    """Oracle precond apply and 2 fixed PCG iterations on a config-3 problem (cached per run)."""
+    if not _FULL_REF:
+        ph = synth.config3_microstructure(5)
+        g = fem.Grid((256, 256, 256), h=1 / 256)
+        G = greens.ghat(g, "thermal", (1.0, 50.0), 3005, 0.1)
+        r = synth.test_vector(21, g.field_shape())
+        _FULL_REF["ph"], _FULL_REF["r"] = ph, r
+        _FULL_REF["z"] = greens.apply_precond(G, r)
+        _FULL_REF["u"] = homog.solve_problem(g, "thermal", ph, (1.0, 50.0), np.eye(3)[1:2], 3005, 0.1,
+                                             fixed_iters=2)["U"][0]
+    return _FULL_REF
+
+
+def test_full_size_every_schedule(schedule):
+    # 256^3 in every schedule: the size-specialised register-direct kernels (x/y/z passes and the
+    # 3-pass F1/F2/F3 at N = 256) only run at this size.
+    ref = _full_size_reference()
+    s = solver(ref["ph"], "thermal", (1.0, 50.0), 1, 3005, 0.1)
+    z = s.apply_precond(torch.from_numpy(ref["r"][None]).to(dev())).cpu().numpy()[0]
+    assert rel(z, ref["z"]) <= 1e-12
+    u = s.solve(np.eye(3)[1:2], fixed_iters=2).u.cpu().numpy()[0]
+    assert rel(u, ref["u"]) <= 1e-11
+
+
 def test_update_equals_fresh_create():
     # uno_cg_update re-runs a0 on the same workspace: results must be bitwise those of a fresh handle
     P = synth.config0()
