@@ -479,7 +479,7 @@ __global__ void __launch_bounds__(256, UNO_F1R_MINB) f1r_kernel(Ctx cx, const do
 #pragma unroll
     for (int n2 = 0; n2 < 8; ++n2) mx = fmax(mx, fmax(fabs(v[n2].x), fabs(v[n2].y)));
   }
-  for (int i = t; i < M; i += 256) tw[i] = cx.tw.x[i];
+  for (int i = t; i < M; i += 256) tw[i] = cx.tw.x[((i & 15) * (i >> 4)) & (M - 1)];  // [k1][n1]
   for (int i = t; i <= M; i += 256) twp[i] = cx.tw.xpost[i];
   if (t < NB) twa[t] = cx.tw.y[ya * t];
   if (t < 8) {
@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(256, UNO_F1R_MINB) f1r_kernel(Ctx cx, const do
   // row FFT stage 1 (thread (y_b, n1 = l16)): DFT8 over n2 -> k1, twiddle w_128^{n1 k1}
   dft_reg<8, false>(v);
 #pragma unroll
-  for (int k1 = 1; k1 < 8; ++k1) v[k1] = cmul(v[k1], tw[(l16 * k1) & (M - 1)]);
+  for (int k1 = 1; k1 < 8; ++k1) v[k1] = cmul(v[k1], tw[k1 * 16 + l16]);
   double2* Tr = TY + yb * (8 * 17);
 #pragma unroll
   for (int k1 = 0; k1 < 8; ++k1) Tr[k1 * 17 + l16] = v[k1];

@@ -176,14 +176,14 @@ __global__ void __launch_bounds__(128) xfwd256_kernel(Ctx cx, const double* __re
 #pragma unroll
     for (int n2 = 0; n2 < 8; ++n2) mx = fmax(mx, fmax(fabs(v[n2].x), fabs(v[n2].y)));
   }
-  for (int i = t; i < M; i += 128) tw[i] = cx.tw.x[i];
+  for (int i = t; i < M; i += 128) tw[i] = cx.tw.x[((i & 15) * (i >> 4)) & (M - 1)];  // [k1][n1]
   for (int i = t; i <= M; i += 128) twp[i] = cx.tw.xpost[i];
   if (t < 8) tw16[t] = cx.tw.x[8 * t];
   __syncthreads();
-  // stage 1 (thread = n1): DFT8 over n2 -> k1, twiddle w_128^{n1 k1}
+  // stage 1 (thread = n1): DFT8 over n2 -> k1, twiddle w_128^{n1 k1} (table [k1][n1])
   dft_reg<8, false>(v);
 #pragma unroll
-  for (int k1 = 1; k1 < 8; ++k1) v[k1] = cmul(v[k1], tw[(l16 * k1) & (M - 1)]);
+  for (int k1 = 1; k1 < 8; ++k1) v[k1] = cmul(v[k1], tw[k1 * 16 + l16]);
 #pragma unroll
   for (int k1 = 0; k1 < 8; ++k1) tb[r * XR_RS + k1 * 17 + l16] = v[k1];
   __syncthreads();
@@ -405,7 +405,9 @@ __global__ void __launch_bounds__(YR_ROWS * YR_R) ypass256_kernel(Ctx cx, int z0
 #pragma unroll
     for (int n2 = 0; n2 < YR_R; ++n2) v[n2] = __ldcg(rowp + lane16 + YR_R * n2);
   }
-  for (int i = t; i < L; i += YR_ROWS * YR_R) tw[i] = cx.tw.y[i];
+  // twiddle table tw[k1][n1] = w_256^{n1 k1}: a quarter-warp (8 consecutive n1) reads 8
+  // consecutive entries (conflict-free)
+  for (int i = t; i < L; i += YR_ROWS * YR_R) tw[i] = cx.tw.y[((i & 15) * (i >> 4)) & (L - 1)];
   __syncthreads();
   // stage 1 (thread = n1): DFT16 over n2 -> k1, twiddle w_256^{n1 k1}
   dft_reg<YR_R, INV>(v);
@@ -413,7 +415,7 @@ __global__ void __launch_bounds__(YR_ROWS * YR_R) ypass256_kernel(Ctx cx, int z0
     const int n1 = lane16;
 #pragma unroll
     for (int k1 = 1; k1 < YR_R; ++k1) {
-      const double2 w = tw[(n1 * k1) & (L - 1)];
+      const double2 w = tw[k1 * YR_R + n1];
       v[k1] = cmul(v[k1], INV ? cconj(w) : w);
     }
 #pragma unroll
@@ -1083,6 +1085,224 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
   const int nblk = gridDim.x * gridDim.y * nzc;
   const int my = (zcI * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
   dp_finish(cx, load, nblk, my, part, red_sh, mode);
+}
+
+// Generalisation of the r2 kernel to NR node rows per thread (128 threads, 32 x 4NR node tile):
+// the per-plane bookkeeping (ring slot, cp.async issue, barrier, loop) and the box/kappa sums
+// shared between vertically adjacent nodes are amortised over NR nodes, so the kernel issues
+// fewer instructions per node (it is issue-bound: ncu 65 % issue, 56 % LSU at NR = 2).
+template <int NR>
+struct KRNState {
+  double Qk[NR + 1][2];
+  double KSlo[NR], Klo[NR], Kxlo[NR], Kylo[NR];
+  double c[NR], xm[NR], xp[NR], dzm[NR];
+  double ym, yp;
+};
+
+template <int NR>
+__global__ void __launch_bounds__(128, 2) kp_thermal3d_rn_kernel(Ctx cx, int mode, const double* __restrict__ src,
+                                                                double* __restrict__ dst, int ZC, int zc0, int nzl) {
+  constexpr int LA = 4;
+  constexpr int T = 128, TX = 32, TH = 4 * NR;  // tile: 32 x TH nodes
+  constexpr int DW = KR2_DW, DR = TH + 2, DPL = DR * DW;  // d rows y0-1 .. y0+TH
+  constexpr int NCH = DR * (DW / 2);
+  constexpr int NDC = (NCH + T - 1) / T;
+  constexpr int PW = KR2_PW, PR = TH + 1, PHS = PR * PW;  // phase rows y0-1 .. y0+TH-1
+  constexpr int NPC = PHS / 16;
+  constexpr int NPCT = (NPC + T - 1) / T;
+  const Geo g = cx.g;
+  const int nzc = (g.P3 + ZC - 1) / ZC;
+  const int load = blockIdx.z / nzl;
+  const int zcI = zc0 + (blockIdx.z - load * nzl);
+  const int dz = g.dirz;
+  if (mode == CG && !cx.st[load].active) return;
+  extern __shared__ double ksm[];
+  double* D = ksm;                                                          // [KT_RING][DR][DW]
+  unsigned char* PH = reinterpret_cast<unsigned char*>(D + KT_RING * DPL);  // [KT_RING][PR][PW]
+  __shared__ double red_sh[32];
+  const int t = threadIdx.x;
+  const int tx = t % TX, ty = t / TX;  // node rows NR ty .. NR ty + NR - 1
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TH, zs = zcI * ZC + dz;
+  const int ze = min(zs + ZC, g.P3 + dz);
+  const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
+  const long long plane = (long long)N1 * N2;
+  const double* dv = src + (long long)load * g.n;
+  const double k0 = cx.mat[0][0], k1 = cx.mat[1][0];
+  int goffD[NDC];
+  unsigned sD[NDC];
+#pragma unroll
+  for (int m = 0; m < NDC; ++m) {
+    const int j = min(t + m * T, NCH - 1);
+    const int ly = j / (DW / 2), q = j - ly * (DW / 2);
+    goffD[m] = ((y0 - 1 + ly + N2) & (N2 - 1)) * N1 + ((x0 - 2 + 2 * q + N1) & (N1 - 1));
+    sD[m] = (unsigned)__cvta_generic_to_shared(D + ly * DW + 2 * q);
+  }
+  int poff[NPCT];
+  unsigned psm[NPCT];
+#pragma unroll
+  for (int m = 0; m < NPCT; ++m) {
+    const int j = min(t + m * T, NPC - 1);
+    const int prow = j / (PW / 16), pq = j - prow * (PW / 16);
+    poff[m] = ((y0 - 1 + prow + N2) & (N2 - 1)) * N1 + ((x0 - 16 + 16 * pq + N1) & (N1 - 1));
+    psm[m] = (unsigned)__cvta_generic_to_shared(PH + prow * PW + 16 * pq);
+  }
+  constexpr unsigned SLOTB = DPL * 8;
+  auto issue_plane = [&](int p) {
+    const unsigned slot = (p - zs + 1) & (KT_RING - 1);
+    const unsigned so = slot * SLOTB;
+    if (dz && (p <= 0 || p >= N3)) {
+#pragma unroll
+      for (int m = 0; m < NDC; ++m)
+        asm volatile("st.shared.v2.f64 [%0], {0d0000000000000000, 0d0000000000000000};\n" ::"r"(sD[m] + so) : "memory");
+    } else {
+      const int zw = dz ? p - 1 : ((p + N3) & (N3 - 1));
+      const double* base = dv + (long long)zw * plane;
+#pragma unroll
+      for (int m = 0; m < NDC; ++m)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sD[m] + so), "l"(base + goffD[m]) : "memory");
+    }
+    const uint8_t* pbase = cx.phase + (long long)((p - 1 + N3) & (N3 - 1)) * plane;
+#pragma unroll
+    for (int m = 0; m < NPCT; ++m)
+      if (m * T + t < NPC)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(psm[m] + slot * PHS), "l"(pbase + poff[m]) : "memory");
+  };
+  double nb[NR + 2][3];
+  auto readn = [&](int p) {
+    const double* Ds = D + ((p - zs + 1) & (KT_RING - 1)) * DPL + NR * ty * DW + tx + 1;
+#pragma unroll
+    for (int a = 0; a < NR + 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) nb[a][b] = Ds[a * DW + b];
+  };
+  auto box = [&](double Qo[NR + 1][2]) {
+    double P[NR + 2][2];
+#pragma unroll
+    for (int a = 0; a < NR + 2; ++a) {
+      P[a][0] = nb[a][0] + nb[a][1];
+      P[a][1] = nb[a][1] + nb[a][2];
+    }
+#pragma unroll
+    for (int e = 0; e < NR + 1; ++e) {
+      Qo[e][0] = P[e][0] + P[e + 1][0];
+      Qo[e][1] = P[e][1] + P[e + 1][1];
+    }
+  };
+  auto kap = [&](int layer, double a[NR + 1][2]) {
+    const unsigned char* Pl = PH + ((layer + 1 - zs + 1) & (KT_RING - 1)) * PHS + NR * ty * PW + tx + 15;
+#pragma unroll
+    for (int e = 0; e < NR + 1; ++e) {
+      a[e][0] = Pl[e * PW] ? k1 : k0;
+      a[e][1] = Pl[e * PW + 1] ? k1 : k0;
+    }
+  };
+#pragma unroll 1
+  for (int p = zs - 1; p <= zs + LA - 1; ++p) {
+    if (p <= ze) issue_plane(p);
+    cp_commit();
+  }
+  cp_wait<LA - 1>();
+  __syncthreads();
+  KRNState<NR> A, B;
+  {
+    double Qn[NR + 1][2], kl[NR + 1][2];
+    readn(zs - 1);
+    box(A.Qk);
+#pragma unroll
+    for (int m = 0; m < NR; ++m) A.dzm[m] = nb[m + 1][1];
+    readn(zs);
+    box(Qn);
+    kap(zs - 1, kl);
+    double KS[NR + 1];
+#pragma unroll
+    for (int e = 0; e < NR + 1; ++e) KS[e] = fma(kl[e][0], A.Qk[e][0] + Qn[e][0], kl[e][1] * (A.Qk[e][1] + Qn[e][1]));
+#pragma unroll
+    for (int m = 0; m < NR; ++m) {
+      A.KSlo[m] = KS[m] + KS[m + 1];
+      A.Klo[m] = (kl[m][0] + kl[m][1]) + (kl[m + 1][0] + kl[m + 1][1]);
+      A.Kxlo[m] = kl[m][1] + kl[m + 1][1];
+      A.Kylo[m] = kl[m + 1][0] + kl[m + 1][1];
+      A.c[m] = nb[m + 1][1];
+      A.xm[m] = nb[m + 1][0];
+      A.xp[m] = nb[m + 1][2];
+    }
+#pragma unroll
+    for (int e = 0; e < NR + 1; ++e) {
+      A.Qk[e][0] = Qn[e][0];
+      A.Qk[e][1] = Qn[e][1];
+    }
+    A.ym = nb[0][1];
+    A.yp = nb[NR + 1][1];
+  }
+  double part = 0.0;
+  const double hc = g.h * (1.0 / 12.0);
+  double* outp = dst + (long long)load * g.n + (long long)(y0 + NR * ty) * N1 + (x0 + tx);
+  auto step = [&](int k, const KRNState<NR>& I, KRNState<NR>& O) {
+    if (k + LA <= ze) issue_plane(k + LA);
+    cp_commit();
+    cp_wait<LA - 1>();
+    __syncthreads();
+    readn(k + 1);
+    box(O.Qk);
+    double a[NR + 1][2];
+    kap(k, a);
+    double KS[NR + 1];
+#pragma unroll
+    for (int e = 0; e < NR + 1; ++e) KS[e] = fma(a[e][0], I.Qk[e][0] + O.Qk[e][0], a[e][1] * (I.Qk[e][1] + O.Qk[e][1]));
+#pragma unroll
+    for (int m = 0; m < NR; ++m) {
+      const double KShi = KS[m] + KS[m + 1];
+      const double Khi = (a[m][0] + a[m][1]) + (a[m + 1][0] + a[m + 1][1]);
+      const double Kxhi = a[m][1] + a[m + 1][1], Kyhi = a[m + 1][0] + a[m + 1][1];
+      const double Ksum = I.Klo[m] + Khi;
+      const double Kxp = I.Kxlo[m] + Kxhi, Kyp = I.Kylo[m] + Kyhi;
+      const double di = I.c[m];
+      const double dyp = m + 1 < NR ? I.c[m + 1] : I.yp, dym = m > 0 ? I.c[m - 1] : I.ym;
+      const double dzp = nb[m + 1][1];  // plane k+1 centre
+      double EE = Kxp * I.xp[m];
+      EE = fma(Ksum - Kxp, I.xm[m], EE);
+      EE = fma(Kyp, dyp, EE);
+      EE = fma(Ksum - Kyp, dym, EE);
+      EE = fma(Khi, dzp, EE);
+      EE = fma(I.Klo[m], I.dzm[m], EE);
+      const double pv = hc * (fma(5.0 * di, Ksum, EE) - (I.KSlo[m] + KShi));
+      outp[(long long)(k - dz) * plane + m * N1] = pv;
+      part = fma(di, pv, part);
+      O.KSlo[m] = KShi;
+      O.Klo[m] = Khi;
+      O.Kxlo[m] = Kxhi;
+      O.Kylo[m] = Kyhi;
+    }
+#pragma unroll
+    for (int m = 0; m < NR; ++m) {
+      O.dzm[m] = I.c[m];
+      O.c[m] = nb[m + 1][1];
+      O.xm[m] = nb[m + 1][0];
+      O.xp[m] = nb[m + 1][2];
+    }
+    O.ym = nb[0][1];
+    O.yp = nb[NR + 1][1];
+  };
+  int k = zs;
+#pragma unroll 1
+  for (; k + 1 < ze; k += 2) {
+    step(k, A, B);
+    step(k + 1, B, A);
+  }
+  if (k < ze) step(k, A, B);
+  cp_wait<0>();
+  const int nblk = gridDim.x * gridDim.y * nzc;
+  const int my = (zcI * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  dp_finish(cx, load, nblk, my, part, red_sh, mode);
+}
+
+// rows per thread of the production thermal 3D K kernel (UNO_KNR = 2 or 4)
+static int k_nr(const Geo& g) {
+  static const int nr = [] {
+    const char* e = getenv("UNO_KNR");
+    return e && e[0] == '2' ? 2 : 4;
+  }();
+  return (nr == 4 && g.N2 >= 16) ? 4 : 2;
 }
 
 // Same stencil, TMA-style staging for N1 >= 32 (the production path): one warp issues
@@ -1956,7 +2176,8 @@ int launch_scalar(const Ctx& cx, int slot, int mode, cudaStream_t s) {
   } else {
     if (g.dim == 3 && g.c == 1) {
       const int TX = g.N1 < 32 ? g.N1 : 32, ZC = g.KZC;
-      nblk = (g.N1 / TX) * (g.N2 / KT_TY) * ((g.P3 + ZC - 1) / ZC);
+      const int TY = (TX == 32 && k_nr(g) == 4) ? 16 : KT_TY;
+      nblk = (g.N1 / TX) * (g.N2 / TY) * ((g.P3 + ZC - 1) / ZC);
     } else if (g.dim == 3) {
       const char* e = getenv("UNO_ELASTIC_DENSE");
       if (!(e && e[0] == '1')) {
@@ -2201,6 +2422,11 @@ int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaS
       const int smb = KB_RING * KB_SLOT;
       set_smem(kp_thermal3d_tma_kernel, smb);
       kp_thermal3d_tma_kernel<<<grid, 256, smb, s>>>(cx, mode, src, dst, ZC);
+    } else if (TX == 32 && k_nr(g) == 4) {
+      const dim3 grid4(g.N1 / 32, g.N2 / 16, nzl * g.nrhs);
+      const int sm4 = KT_RING * (18 * KR2_DW * (int)sizeof(double) + 17 * KR2_PW);
+      set_smem(kp_thermal3d_rn_kernel<4>, sm4);
+      kp_thermal3d_rn_kernel<4><<<grid4, 128, sm4, s>>>(cx, mode, src, dst, ZC, zc0, nzl);
     } else if (TX == 32) {
       const int sm2 = KT_RING * (KR2_DPL * (int)sizeof(double) + KR2_PHS);
       static const int la = [] {
