@@ -23,6 +23,10 @@ UNO_THERMAL, UNO_ELASTIC = 0, 1
 EXPORTS = ("uno_cg_create", "uno_cg_destroy", "uno_cg_update", "uno_cg_rhs", "uno_cg_apply_K", "uno_cg_apply_precond",
            "uno_cg_solve", "uno_cg_effective_property", "uno_cg_last_solve_stats", "uno_cg_kernel_timing",
            "uno_cg_last_error", "uno_cg_version")
+# include/uno_cg_slab.h (z-slab decomposition)
+SLAB_EXPORTS = ("uno_slab_create", "uno_slab_destroy", "uno_slab_sizes", "uno_slab_begin", "uno_slab_forward",
+                "uno_slab_green", "uno_slab_inverse", "uno_slab_kapply", "uno_slab_reduce", "uno_slab_apply",
+                "uno_slab_state", "uno_slab_finish", "uno_slab_local_means", "uno_slab_subtract_means")
 
 
 class UnoCgDesc(C.Structure):
@@ -57,7 +61,21 @@ def _load():
     lib.uno_cg_effective_property.argtypes = [P, P, P, P]
     lib.uno_cg_last_solve_stats.argtypes = [P, C.POINTER(D), C.POINTER(I64)]
     lib.uno_cg_kernel_timing.argtypes = [P, I32, I32, P, P]
-    for f in EXPORTS[:-2]:
+    lib.uno_slab_create.argtypes = [C.POINTER(UnoCgDesc), I32, I32, P, C.POINTER(P)]
+    lib.uno_slab_destroy.argtypes = [P]
+    lib.uno_slab_sizes.argtypes = [P, P]
+    lib.uno_slab_begin.argtypes = [P, P, D, I32, I32]
+    lib.uno_slab_forward.argtypes = [P, P]
+    lib.uno_slab_green.argtypes = [P, P, P]
+    lib.uno_slab_inverse.argtypes = [P, P, P]
+    lib.uno_slab_kapply.argtypes = [P, P]
+    lib.uno_slab_reduce.argtypes = [P, I32, P]
+    lib.uno_slab_apply.argtypes = [P, I32, P]
+    lib.uno_slab_state.argtypes = [P, P, P]
+    lib.uno_slab_finish.argtypes = [P, P]
+    lib.uno_slab_local_means.argtypes = [P, P, P]
+    lib.uno_slab_subtract_means.argtypes = [P, P, P]
+    for f in EXPORTS[:-2] + SLAB_EXPORTS:
         getattr(lib, f).restype = C.c_int
     lib.uno_cg_last_error.restype = C.c_char_p
     lib.uno_cg_version.restype = C.c_char_p
@@ -159,3 +177,70 @@ def uno_cg_kernel_timing(h: int, enable: int = -1, reset: int = 0):
 
 def uno_cg_version() -> str:
     return _lib.uno_cg_version().decode()
+
+
+# ---------------------------------------------------------------------------------- slab mode
+def uno_slab_create(desc: UnoCgDesc, rank: int, nranks: int, d_phase) -> int:
+    h = C.c_void_p()
+    _check(_lib.uno_slab_create(C.byref(desc), int(rank), int(nranks), _ptr(d_phase), C.byref(h)), "uno_slab_create")
+    return h.value
+
+
+def uno_slab_destroy(h: int):
+    _check(_lib.uno_slab_destroy(h), "uno_slab_destroy")
+
+
+def uno_slab_sizes(h: int):
+    out = np.zeros(4, dtype=np.int64)
+    _check(_lib.uno_slab_sizes(h, _ptr(out)), "uno_slab_sizes")
+    return [int(v) for v in out]
+
+
+def uno_slab_begin(h: int, loads, rel_tol: float, max_iter: int, fixed_iters: int):
+    L = _host_f64(loads)
+    _check(_lib.uno_slab_begin(h, _ptr(L), float(rel_tol), int(max_iter), int(fixed_iters)), "uno_slab_begin")
+
+
+def uno_slab_forward(h: int, d_send):
+    _check(_lib.uno_slab_forward(h, _ptr(d_send)), "uno_slab_forward")
+
+
+def uno_slab_green(h: int, d_recv, d_send):
+    _check(_lib.uno_slab_green(h, _ptr(d_recv), _ptr(d_send)), "uno_slab_green")
+
+
+def uno_slab_inverse(h: int, d_recv, d_halo_send):
+    _check(_lib.uno_slab_inverse(h, _ptr(d_recv), _ptr(d_halo_send)), "uno_slab_inverse")
+
+
+def uno_slab_kapply(h: int, d_halo_recv):
+    _check(_lib.uno_slab_kapply(h, _ptr(d_halo_recv)), "uno_slab_kapply")
+
+
+def uno_slab_reduce(h: int, slot: int, d_out):
+    _check(_lib.uno_slab_reduce(h, int(slot), _ptr(d_out)), "uno_slab_reduce")
+
+
+def uno_slab_apply(h: int, slot: int, d_in):
+    _check(_lib.uno_slab_apply(h, int(slot), _ptr(d_in)), "uno_slab_apply")
+
+
+def uno_slab_state(h: int, nrhs: int):
+    any_active = np.zeros(1, dtype=np.int32)
+    reps = (UnoCgReport * nrhs)()
+    _check(_lib.uno_slab_state(h, _ptr(any_active), reps), "uno_slab_state")
+    out = [dict(iterations=r.iterations, converged=bool(r.converged), status=r.status, r0_inf=r.r0_inf,
+                rel_res=r.rel_res, gamma_last=r.gamma_last) for r in reps]
+    return bool(any_active[0]), out
+
+
+def uno_slab_finish(h: int, d_u):
+    _check(_lib.uno_slab_finish(h, _ptr(d_u)), "uno_slab_finish")
+
+
+def uno_slab_local_means(h: int, d_u, d_means):
+    _check(_lib.uno_slab_local_means(h, _ptr(d_u), _ptr(d_means)), "uno_slab_local_means")
+
+
+def uno_slab_subtract_means(h: int, d_u, d_means):
+    _check(_lib.uno_slab_subtract_means(h, _ptr(d_u), _ptr(d_means)), "uno_slab_subtract_means")

@@ -23,6 +23,10 @@ struct Geo {
   int P3;               // stored node planes along z: N3 (periodic) or N3 - 1 (dirz); 1 in 2D
   int KZC;              // z planes per CTA of the 3D thermal K kernel
   int ZP;               // z-chunk of the L2-pipelined 5-pass schedule (0: off), DESIGN.md §5
+  // z-slab decomposition (slab.cu; all 0 for a whole-grid handle):
+  int zlo;              // global z of the first stored node plane of this slab
+  int halo;             // 1: K reads node planes zlo-1 / zlo+P3 from Ctx::hlo / Ctx::hhi
+  int Ny, ky0;          // symbol of a y-chunk pencil: global N2 and the chunk's first k_y (Ny = 0: N2)
 };
 
 // Per-load CG state (device resident; Alg 2 scalars).

@@ -1122,8 +1122,8 @@ __global__ void __launch_bounds__(128, 2) kp_thermal3d_rn_kernel(Ctx cx, int mod
   __shared__ double red_sh[32];
   const int t = threadIdx.x;
   const int tx = t % TX, ty = t / TX;  // node rows NR ty .. NR ty + NR - 1
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TH, zs = zcI * ZC + dz;
-  const int ze = min(zs + ZC, g.P3 + dz);
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TH, zs = zcI * ZC + dz + g.zlo;
+  const int ze = min(zs + ZC, g.P3 + dz + g.zlo);  // slab mode: global node planes [zlo, zlo + P3)
   const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
   const long long plane = (long long)N1 * N2;
   const double* dv = src + (long long)load * g.n;
@@ -1155,8 +1155,12 @@ __global__ void __launch_bounds__(128, 2) kp_thermal3d_rn_kernel(Ctx cx, int mod
       for (int m = 0; m < NDC; ++m)
         asm volatile("st.shared.v2.f64 [%0], {0d0000000000000000, 0d0000000000000000};\n" ::"r"(sD[m] + so) : "memory");
     } else {
-      const int zw = dz ? p - 1 : ((p + N3) & (N3 - 1));
-      const double* base = dv + (long long)zw * plane;
+      const double* base;
+      if (g.halo)  // slab: neighbours' boundary planes arrive in separate halo buffers
+        base = p < g.zlo ? cx.hlo + (long long)load * plane
+                         : (p >= g.zlo + g.P3 ? cx.hhi + (long long)load * plane : dv + (long long)(p - g.zlo) * plane);
+      else
+        base = dv + (long long)(dz ? p - 1 : ((p + N3) & (N3 - 1))) * plane;
 #pragma unroll
       for (int m = 0; m < NDC; ++m)
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sD[m] + so), "l"(base + goffD[m]) : "memory");
@@ -1266,7 +1270,7 @@ __global__ void __launch_bounds__(128, 2) kp_thermal3d_rn_kernel(Ctx cx, int mod
       EE = fma(Khi, dzp, EE);
       EE = fma(I.Klo[m], I.dzm[m], EE);
       const double pv = hc * (fma(5.0 * di, Ksum, EE) - (I.KSlo[m] + KShi));
-      outp[(long long)(k - dz) * plane + m * N1] = pv;
+      outp[(long long)(k - dz - g.zlo) * plane + m * N1] = pv;
       part = fma(di, pv, part);
       O.KSlo[m] = KShi;
       O.Klo[m] = Khi;
@@ -1680,7 +1684,7 @@ __device__ __forceinline__ unsigned node_octants(const Ctx& cx, long long i, int
   const int s1 = __ffs(N1) - 1, s2 = __ffs(N2) - 1;
   const int x = (int)(i & (N1 - 1));
   const int y = (int)((i >> s1) & (N2 - 1));
-  z = (int)(i >> (s1 + s2)) + g.dirz;  // Dirichlet z: stored planes are nodes 1..N3-1
+  z = (int)(i >> (s1 + s2)) + g.dirz + g.zlo;  // Dirichlet z: stored planes are nodes 1..N3-1; slab offset
   unsigned bits = 0;
   const int no = 1 << g.dim;
 #pragma unroll
@@ -1739,7 +1743,7 @@ __device__ __forceinline__ unsigned node_octants_warp(const Ctx& cx, long long i
   const int lane = threadIdx.x & 31;
   const int x = (int)(i & (N1 - 1));
   const int y = (int)((i >> s1) & (N2 - 1));
-  z = (int)(i >> (s1 + s2)) + g.dirz;
+  z = (int)(i >> (s1 + s2)) + g.dirz + g.zlo;
   const int ym = (y - 1) & (N2 - 1);
   const int zm = g.dirz ? z - 1 : ((z - 1) & (N3 - 1));
   const int zp = z;  // voxel layer z (node planes 0..N3-1 periodic, 1..N3-1 Dirichlet: no wrap)
@@ -1918,7 +1922,8 @@ __global__ void build_symbol_kernel(Ctx cx, double* gtab, double ref0, double re
   const Geo g = cx.g;
   const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= g.nspec) return;
-  const int N1 = g.N1, N2 = g.N2, N3 = g.N3, d = g.dim;
+  // N2l: stored k_y extent of this table (a y-chunk in slab mode); N2: the grid's N2 (frequencies)
+  const int N1 = g.N1, N2l = g.N2, N2 = g.Ny ? g.Ny : g.N2, N3 = g.N3, d = g.dim;
   int kx, ky, kz;
   if (g.NB > 0) {  // 3-pass layout [kx][k_b][kz][k_a], k_y = k_b + NB k_a (fft3.cu)
     const int ka = (int)(b % g.NA);
@@ -1927,14 +1932,14 @@ __global__ void build_symbol_kernel(Ctx cx, double* gtab, double ref0, double re
     kx = (int)(b / ((long long)g.NA * N3 * g.NB));
     ky = kb + g.NB * ka;
   } else if (!g.dirz) {  // 5-pass layout [kx][kz][ky]: powers of two, shifts only
-    const int s2 = __ffs(N2) - 1, s3 = __ffs(N3) - 1;
-    ky = (int)(b & (N2 - 1));
+    const int s2 = __ffs(N2l) - 1, s3 = __ffs(N3) - 1;
+    ky = (int)(b & (N2l - 1)) + g.ky0;  // y-chunk pencil (slab mode): global k_y
     kz = (int)((b >> s2) & (N3 - 1));
     kx = (int)(b >> (s2 + s3));
   } else {         // mixed layout [kx][sine plane][ky]
-    ky = (int)(b % N2);
-    kz = (int)((b / N2) % g.P3);
-    kx = (int)(b / ((long long)N2 * g.P3));
+    ky = (int)(b % N2l);
+    kz = (int)((b / N2l) % g.P3);
+    kx = (int)(b / ((long long)N2l * g.P3));
   }
   double cs[3], sn[3];
   axis_trig(kx, N1, cs[0], sn[0]);
@@ -1955,7 +1960,7 @@ __global__ void build_symbol_kernel(Ctx cx, double* gtab, double ref0, double re
     zero = false;
   } else {
     axis_trig(kz, N3, cs[2], sn[2]);
-    inv_n = 1.0 / (double)g.n;
+    inv_n = 1.0 / ((double)N1 * N2 * N3);  // = 1/n (N2: the whole grid, also for a y-chunk pencil)
     flat = ((unsigned long long)kz * N2 + ky) * N1 + kx;
     flatm = ((unsigned long long)((N3 - kz) & (N3 - 1)) * N2 + (unsigned long long)((N2 - ky) & (N2 - 1))) * N1 +
             (unsigned long long)((N1 - kx) & (N1 - 1));
@@ -2103,9 +2108,9 @@ __global__ void eq55_kernel(Ctx cx, const double* gtab, double* partials) {
   __shared__ double sh[32];
   double mn = 1e300, mx = -1e300;
   const long long ns = g.nspec;
-  const double nn = (double)g.n;
+  const double nn = g.dirz ? (double)g.n : (double)g.N1 * (g.Ny ? g.Ny : g.N2) * g.N3;
   for (long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x; b < ns; b += (long long)gridDim.x * blockDim.x) {
-    if (b == 0 && !g.dirz) continue;  // periodic: G_hat(0) = 0 shares the null space
+    if (b == 0 && !g.dirz && g.ky0 == 0) continue;  // periodic: G_hat(0) = 0 shares the null space
     double lo, hi;
     if (g.c == 1) {
       lo = hi = gtab[b] * nn;
@@ -2422,6 +2427,8 @@ int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaS
       const int smb = KB_RING * KB_SLOT;
       set_smem(kp_thermal3d_tma_kernel, smb);
       kp_thermal3d_tma_kernel<<<grid, 256, smb, s>>>(cx, mode, src, dst, ZC);
+    } else if (g.halo && !(TX == 32 && k_nr(g) == 4)) {
+      return -1;  // slab halos: the NR = 4 kernel only
     } else if (TX == 32 && k_nr(g) == 4) {
       const dim3 grid4(g.N1 / 32, g.N2 / 16, nzl * g.nrhs);
       const int sm4 = KT_RING * (18 * KR2_DW * (int)sizeof(double) + 17 * KR2_PW);

@@ -28,6 +28,8 @@ struct Ctx {
   double* u;
   double* hist;             // [nrhs][hist_stride] residual history (device) or null
   int hist_stride;
+  const double* hlo;        // slab mode (g.halo): node plane zlo-1 of d, [nrhs][c][N2][N1]
+  const double* hhi;        // slab mode: node plane zlo+P3 of d
 };
 
 struct LoadParams {         // macroscopic loads for the RHS / effective-property kernels

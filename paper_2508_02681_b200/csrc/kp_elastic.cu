@@ -47,19 +47,21 @@ __global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int
   const long long n = g.n;
   const long long plane = (long long)N1 * N2;
   const int x0 = blockIdx.x * KM_TX, y0 = blockIdx.y * KM_TY;
-  const int zs = zcI * ZC + dz, ze = min(zs + ZC, g.P3 + dz);
+  const int zs = zcI * ZC + dz + g.zlo, ze = min(zs + ZC, g.P3 + dz + g.zlo);  // slab: global planes
   const double* dv = src + (long long)load * 3 * n;
   const double hs = g.h / (72.0 * 64.0);
   const double l0 = cx.mat[0][0] * hs, m0 = cx.mat[0][1] * hs, l1 = cx.mat[1][0] * hs, m1 = cx.mat[1][1] * hs;
   // copy assignment of the 3 x 10 x 18 plane tile (clamped: harmless duplicate copies)
-  long long goff[KM_NCP];
+  long long goff[KM_NCP];  // in-plane offset
+  int gcomp[KM_NCP];
   unsigned sdst[KM_NCP];
 #pragma unroll
   for (int m = 0; m < KM_NCP; ++m) {
     const int j = min(t + m * KM_T, KM_PLANE - 1);
     const int comp = j / KM_DP, r = j - comp * KM_DP;
     const int ly = r / KM_DW, lx = r - ly * KM_DW;
-    goff[m] = comp * n + (long long)((y0 - 1 + ly + N2) & (N2 - 1)) * N1 + ((x0 - 1 + lx + N1) & (N1 - 1));
+    gcomp[m] = comp;
+    goff[m] = (long long)((y0 - 1 + ly + N2) & (N2 - 1)) * N1 + ((x0 - 1 + lx + N1) & (N1 - 1));
     sdst[m] = (unsigned)__cvta_generic_to_shared(D + j);  // clamped copies rewrite entry PLANE-1
   }
   auto slot_of = [&](int p) { return (p - zs + 1) & (KM_RING - 1); };
@@ -70,11 +72,19 @@ __global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int
       for (int m = 0; m < KM_NCP; ++m)
         asm volatile("st.shared.f64 [%0], 0d0000000000000000;\n" ::"r"(sdst[m] + so) : "memory");
     } else {
-      const int zw = dz ? p - 1 : ((p + N3) & (N3 - 1));
-      const double* base = dv + (long long)zw * plane;
+      // component c of plane p starts at base + c * cst (slab halo buffers: [nrhs][3][N2][N1])
+      const double* base;
+      long long cst = n;
+      if (g.halo && (p < g.zlo || p >= g.zlo + g.P3)) {
+        base = (p < g.zlo ? cx.hlo : cx.hhi) + (long long)load * 3 * plane;
+        cst = plane;
+      } else {
+        base = dv + (long long)(g.halo ? p - g.zlo : (dz ? p - 1 : ((p + N3) & (N3 - 1)))) * plane;
+      }
 #pragma unroll
       for (int m = 0; m < KM_NCP; ++m)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sdst[m] + so), "l"(base + goff[m]) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sdst[m] + so), "l"(base + gcomp[m] * cst + goff[m])
+                     : "memory");
     }
   };
   // element owned by this thread in every layer
@@ -142,7 +152,7 @@ __global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int
         for (int al = 0; al < 3; ++al) p[al] += Lb[(3 * a + al) * KM_NE + e] + Up[(3 * a + al) * KM_NE + e];
       }
       const double* Dc = D + slot_of(k) * KM_PLANE + (ty + 1) * KM_DW + tx + 1;
-      const long long gi = (long long)(k - dz) * plane + (long long)(y0 + ty) * N1 + x0 + tx;
+      const long long gi = (long long)(k - dz - g.zlo) * plane + (long long)(y0 + ty) * N1 + x0 + tx;
 #pragma unroll
       for (int al = 0; al < 3; ++al) {
         dst[(long long)load * 3 * n + al * n + gi] = p[al];

@@ -26,6 +26,13 @@ static uno_status fail(uno_status s, const std::string& msg) {
   return s;
 }
 
+namespace uno {
+uno_status set_last_error(uno_status s, const char* msg) {  // shared with slab.cu
+  g_err = msg;
+  return s;
+}
+}  // namespace uno
+
 #define CK(call)                                                                                  \
   do {                                                                                            \
     cudaError_t e_ = (call);                                                                      \

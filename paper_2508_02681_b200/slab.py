@@ -1,0 +1,201 @@
+"""z-slab decomposition of one UNO-CG problem over several ranks (include/uno_cg_slab.h;
+SURVEY.md §8(e) "Config 4 (one 512^3 grid)").
+
+Orchestration only: every arithmetic step of PAPER.md Alg 2 runs in libunocg kernels
+(binding.uno_slab_*); this module allocates the exchange buffers, moves them between ranks
+and sequences the stages of one iteration:
+
+    forward -> [||r|| all-reduce] -> all-to-all -> green -> [gamma all-reduce] -> all-to-all
+    -> inverse -> halo exchange -> kapply -> [d.p all-reduce]
+
+Two transports implement the exchanges with identical buffer semantics:
+  * DistComm  — one rank per process/GPU, torch.distributed (NCCL on GPUs; gloo in the CPU
+                tests), point-to-point batches for the all-to-all and the halo planes;
+  * LocalComm — all ranks emulated in this process (one device), plain copies.  Used by the
+                single-GPU parity tests: the per-rank kernels and the data movement pattern
+                are exactly those of the multi-GPU run.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import binding as B
+
+SUM, MAX = "sum", "max"
+
+
+class LocalComm:
+    """All `nranks` ranks live in this process; buffers are lists indexed by rank."""
+
+    def __init__(self, nranks: int):
+        self.nranks = nranks
+        self.ranks = list(range(nranks))
+
+    def all_to_all(self, sends, recvs):
+        # recvs[q][r] <- sends[r][q]  (block r of rank q's receive buffer came from rank r)
+        for r in self.ranks:
+            for q in self.ranks:
+                recvs[q][r].copy_(sends[r][q])
+
+    def halo(self, sends, recvs):
+        # sends[r][0] = first node plane of rank r -> rank r-1 (its plane zlo+Z)
+        # sends[r][1] = last node plane of rank r  -> rank r+1 (its plane zlo-1)
+        n = self.nranks
+        for r in self.ranks:
+            recvs[(r - 1) % n][1].copy_(sends[r][0])
+            recvs[(r + 1) % n][0].copy_(sends[r][1])
+
+    def allreduce(self, vals, op: str):
+        tot = vals[0].clone()
+        for v in vals[1:]:
+            tot = tot + v if op == SUM else torch.maximum(tot, v)
+        for v in vals:
+            v.copy_(tot)
+
+
+class DistComm:
+    """One rank per process (torch.distributed already initialised)."""
+
+    def __init__(self):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.rank = dist.get_rank()
+        self.nranks = dist.get_world_size()
+        self.ranks = [self.rank]
+
+    def all_to_all(self, sends, recvs):
+        send, recv = sends[0], recvs[0]
+        r, n = self.rank, self.nranks
+        recv[r].copy_(send[r])
+        ops = []
+        for k in range(1, n):  # pairwise order: every rank sends to r+k while receiving from r-k
+            q_to, q_from = (r + k) % n, (r - k) % n
+            ops.append(self.dist.P2POp(self.dist.isend, send[q_to], q_to))
+            ops.append(self.dist.P2POp(self.dist.irecv, recv[q_from], q_from))
+        if ops:
+            for w in self.dist.batch_isend_irecv(ops):
+                w.wait()
+
+    def halo(self, sends, recvs):
+        send, recv = sends[0], recvs[0]
+        r, n = self.rank, self.nranks
+        if n == 1:
+            recv[1].copy_(send[0])
+            recv[0].copy_(send[1])
+            return
+        lo, hi = (r - 1) % n, (r + 1) % n
+        ops = [self.dist.P2POp(self.dist.isend, send[0], lo), self.dist.P2POp(self.dist.irecv, recv[1], hi),
+               self.dist.P2POp(self.dist.isend, send[1], hi), self.dist.P2POp(self.dist.irecv, recv[0], lo)]
+        for w in self.dist.batch_isend_irecv(ops):
+            w.wait()
+
+    def allreduce(self, vals, op: str):
+        self.dist.all_reduce(vals[0], op=self.dist.ReduceOp.SUM if op == SUM else self.dist.ReduceOp.MAX)
+
+
+@dataclass
+class SlabResult:
+    u: list          # per local rank: [nrhs][c][Z][N2][N1] (mean-free per component)
+    reports: list    # per load: iterations, converged, status, r0_inf, rel_res, gamma_last
+    iterations: int  # loop bodies executed
+
+
+class SlabSolver:
+    """UNO-CG on a z-slab decomposed grid.  `phase` is the whole [N3][N2][N1] uint8 field on
+    this process's device (every rank keeps all of it: 1 byte per voxel)."""
+
+    def __init__(self, phase: torch.Tensor, physics: str, mat, comm, nrhs: int = 1, seed: int = 0, amp: float = 0.0,
+                 h: float = 0.0, ref=None):
+        assert phase.dim() == 3 and phase.dtype == torch.uint8 and phase.is_cuda
+        self.phase = phase.contiguous()
+        self.comm = comm
+        self.nrhs = nrhs
+        N3, N2, N1 = self.phase.shape
+        self.c = 1 if physics == "thermal" else 3
+        d = B.UnoCgDesc()
+        d.dim = 3
+        d.n[0], d.n[1], d.n[2] = N1, N2, N3
+        d.h = h
+        d.physics = B.UNO_THERMAL if physics == "thermal" else B.UNO_ELASTIC
+        if physics == "thermal":
+            d.mat[0][0], d.mat[1][0] = float(mat[0]), float(mat[1])
+        else:
+            (d.mat[0][0], d.mat[0][1]), (d.mat[1][0], d.mat[1][1]) = mat
+        if ref is not None:
+            if physics == "thermal":
+                d.ref[0] = float(ref)
+            else:
+                d.ref[0], d.ref[1] = ref
+        d.seed, d.amp, d.nrhs = seed, amp, nrhs
+        d.stream = torch.cuda.current_stream().cuda_stream
+        self.desc = d
+        self.handles = [B.uno_slab_create(d, r, comm.nranks, self.phase) for r in comm.ranks]
+        nvec, blk, hs, Z = B.uno_slab_sizes(self.handles[0])
+        self.Z, self.shape = Z, (nrhs, self.c, Z, N2, N1)
+        dev = self.phase.device
+        f64 = dict(dtype=torch.float64, device=dev)
+        R = comm.nranks
+        self.send = [torch.empty((R, 2 * blk), **f64) for _ in comm.ranks]
+        self.recv = [torch.empty((R, 2 * blk), **f64) for _ in comm.ranks]
+        self.hsend = [torch.empty((2, hs), **f64) for _ in comm.ranks]
+        self.hrecv = [torch.empty((2, hs), **f64) for _ in comm.ranks]
+        self.red = [torch.empty(nrhs, **f64) for _ in comm.ranks]
+
+    def close(self):
+        for h in self.handles:
+            B.uno_slab_destroy(h)
+        self.handles = []
+
+    def _scalar(self, slot: int, op: str):
+        for h, v in zip(self.handles, self.red):
+            B.uno_slab_reduce(h, slot, v)
+        self.comm.allreduce(self.red, op)
+        for h, v in zip(self.handles, self.red):
+            B.uno_slab_apply(h, slot, v)
+
+    def iterate(self):
+        """One PCG iteration (Alg 2 l.3-12) on every local rank."""
+        c, H = self.comm, self.handles
+        for h, s in zip(H, self.send):
+            B.uno_slab_forward(h, s)
+        self._scalar(0, MAX)                      # ||r||_inf: stop test (l.3)
+        c.all_to_all(self.send, self.recv)
+        for h, r, s in zip(H, self.recv, self.send):
+            B.uno_slab_green(h, r, s)
+        self._scalar(1, SUM)                      # gamma_1 = r.s (l.7)
+        c.all_to_all(self.send, self.recv)
+        for h, r, hs in zip(H, self.recv, self.hsend):
+            B.uno_slab_inverse(h, r, hs)
+        c.halo(self.hsend, self.hrecv)
+        for h, hr in zip(H, self.hrecv):
+            B.uno_slab_kapply(h, hr)
+        self._scalar(2, SUM)                      # d.p -> alpha (l.10)
+
+    def solve(self, loads, rel_tol: float = 1e-8, max_iter: int = 1000, fixed_iters: int = 0,
+              check_every: int = 1) -> SlabResult:
+        for h in self.handles:
+            B.uno_slab_begin(h, loads, rel_tol, max_iter, fixed_iters)
+        cap = (fixed_iters if fixed_iters > 0 else max_iter) + 2
+        bodies = 0
+        while bodies < cap:
+            self.iterate()
+            bodies += 1
+            if bodies % check_every == 0:
+                active, _ = B.uno_slab_state(self.handles[0], self.nrhs)  # identical on every rank
+                if not active:
+                    break
+        _, reps = B.uno_slab_state(self.handles[0], self.nrhs)
+        us = [torch.empty(self.shape, dtype=torch.float64, device=self.phase.device) for _ in self.handles]
+        for h, u in zip(self.handles, us):
+            B.uno_slab_finish(h, u)
+        # per-component mean over the whole grid: equal slabs -> mean of the slab means
+        means = [torch.empty(self.nrhs * self.c, dtype=torch.float64, device=self.phase.device) for _ in self.handles]
+        for h, u, m in zip(self.handles, us, means):
+            B.uno_slab_local_means(h, u, m)
+        self.comm.allreduce(means, SUM)
+        for h, u, m in zip(self.handles, us, means):
+            B.uno_slab_subtract_means(h, u, m)
+        return SlabResult(us, reps, bodies)

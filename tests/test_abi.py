@@ -1,6 +1,7 @@
 """C-ABI boundary checks that need no GPU: libunocg.so loads and exports every entry point
-declared in include/uno_cg.h; the ctypes structs match the C layout; argument validation
-paths that fail before touching the device return the documented status codes."""
+declared in include/*.h (uno_cg.h, uno_cg_slab.h); the ctypes structs match the C layout;
+argument validation paths that fail before touching the device return the documented
+status codes."""
 import ctypes
 import os
 import re
@@ -9,7 +10,7 @@ import subprocess
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-HDR = os.path.join(ROOT, "include", "uno_cg.h")
+HDRS = [os.path.join(ROOT, "include", f) for f in sorted(os.listdir(os.path.join(ROOT, "include"))) if f.endswith(".h")]
 LIB = os.path.join(ROOT, "paper_2508_02681_b200", "lib", "libunocg.so")
 
 
@@ -22,8 +23,8 @@ def _ensure_built():
 
 
 def _declared():
-    txt = open(HDR).read()
-    return sorted(set(re.findall(r"\b(uno_cg_[A-Za-z_]+)\s*\(", txt)) - {"uno_cg_handle"})
+    txt = "".join(open(h).read() for h in HDRS)
+    return sorted(set(re.findall(r"\b(uno_(?:cg|slab)_[A-Za-z_]+)\s*\(", txt)) - {"uno_cg_handle", "uno_slab_handle"})
 
 
 def test_header_declares_north_star_entry_points():
@@ -35,11 +36,13 @@ def test_header_declares_north_star_entry_points():
 def test_library_exports_every_declared_symbol():
     _ensure_built()
     out = subprocess.run(["nm", "-D", "--defined-only", LIB], capture_output=True, text=True, check=True).stdout
-    exported = set(re.findall(r"\bT\s+(uno_cg_\w+)", out))
+    exported = set(re.findall(r"\bT\s+(uno_(?:cg|slab)_\w+)", out))
     missing = [n for n in _declared() if n not in exported]
     assert not missing, missing
+    assert "uno_slab_create" in exported and "uno_slab_kapply" in exported
     # nothing but the C ABI is exported (hidden visibility for the C++/CUDA internals)
-    extra = [l for l in out.splitlines() if " T " in l and "uno_cg_" not in l and "_init" not in l and "_fini" not in l]
+    extra = [l for l in out.splitlines()
+             if " T " in l and "uno_cg_" not in l and "uno_slab_" not in l and "_init" not in l and "_fini" not in l]
     assert not extra, extra[:5]
 
 
@@ -69,3 +72,25 @@ def test_library_loads_and_validates_without_gpu():
     with pytest.raises(B.UnoError) as e:
         B.uno_cg_create(d, 1)
     assert e.value.status == B.UNO_ERR_UNSUPPORTED
+
+
+def test_slab_create_validates_without_gpu():
+    _ensure_built()
+    import torch  # noqa: F401
+
+    from paper_2508_02681_b200 import binding as B
+
+    d = B.UnoCgDesc()
+    d.dim, d.n[0], d.n[1], d.n[2], d.nrhs = 2, 32, 32, 1, 1
+    d.mat[0][0] = d.mat[1][0] = 1.0
+    with pytest.raises(B.UnoError) as e:
+        B.uno_slab_create(d, 0, 2, 1)
+    assert e.value.status == B.UNO_ERR_UNSUPPORTED  # slab mode: 3D only
+    d.dim, d.n[2] = 3, 24
+    with pytest.raises(B.UnoError) as e:
+        B.uno_slab_create(d, 0, 2, 1)
+    assert e.value.status == B.UNO_ERR_SHAPE  # N3 not a power of two
+    d.n[2] = 32
+    with pytest.raises(B.UnoError) as e:
+        B.uno_slab_create(d, 2, 2, 1)
+    assert e.value.status == B.UNO_ERR_ARG  # rank out of range

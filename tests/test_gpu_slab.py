@@ -1,0 +1,77 @@
+"""z-slab decomposition (include/uno_cg_slab.h) on one GPU with the
+ranks emulated in-process (slab.LocalComm): the per-rank kernels, halo planes, all-to-all
+block layout and cross-rank scalar reductions are exactly those of a multi-GPU run; the
+result must equal the whole-grid solver (same Krylov iterates up to reduction order) and
+the CPU oracle at a common iteration count."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import fem, homog  # noqa: E402
+from paper_2508_02681_b200 import synth  # noqa: E402
+
+
+def dev():
+    assert torch.cuda.is_available(), "gpu tests need a CUDA device"
+    return torch.device("cuda:0")
+
+
+def rel(a, b):
+    return float(np.linalg.norm((a - b).ravel()) / max(np.linalg.norm(b.ravel()), 1e-300))
+
+
+def whole(ph, physics, mat, nrhs, seed, amp, loads, fixed):
+    from paper_2508_02681_b200.api import UnoCG
+
+    s = UnoCG(torch.from_numpy(ph).to(dev()), physics, mat, nrhs=nrhs, seed=seed, amp=amp)
+    r = s.solve(loads, fixed_iters=fixed) if fixed else s.solve(loads)
+    return r.u.cpu().numpy(), r.reports
+
+
+def slab(ph, physics, mat, nrhs, seed, amp, loads, fixed, nranks):
+    from paper_2508_02681_b200.slab import LocalComm, SlabSolver
+
+    sv = SlabSolver(torch.from_numpy(ph).to(dev()), physics, mat, LocalComm(nranks), nrhs=nrhs, seed=seed, amp=amp)
+    res = sv.solve(loads, fixed_iters=fixed) if fixed else sv.solve(loads)
+    sv.close()
+    return np.concatenate([u.cpu().numpy() for u in res.u], axis=2), res.reports
+
+
+@pytest.mark.parametrize("nranks", [1, 2, 4])
+def test_thermal_slab_equals_whole_grid(nranks):
+    P = synth.config1()
+    ph, mat = P.phase, P.mat
+    loads = np.eye(3)[:2]
+    uw, _ = whole(ph, "thermal", mat, 2, P.seed, P.amp, loads, 6)
+    us, reps = slab(ph, "thermal", mat, 2, P.seed, P.amp, loads, 6, nranks)
+    assert [r["iterations"] for r in reps] == [6, 6]
+    assert rel(us, uw) <= 1e-11
+    # converged solves: same iteration counts (+-1 for the reduction order) and solutions
+    uw, rw = whole(ph, "thermal", mat, 2, P.seed, P.amp, loads, 0)
+    us, rs = slab(ph, "thermal", mat, 2, P.seed, P.amp, loads, 0, nranks)
+    for a, b in zip(rw, rs):
+        assert abs(a["iterations"] - b["iterations"]) <= 1 and b["converged"]
+    assert rel(us, uw) <= 1e-7
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_elastic_slab_equals_whole_grid(nranks):
+    ph = np.ascontiguousarray(synth.spheres_rsa(32, 0.25, 3.0, 5.0, seed=2))
+    mat = (synth.lame_from_E_nu(1.0, 0.3), synth.lame_from_E_nu(10.0, 0.2))
+    loads = np.eye(6)[[0, 3]]
+    uw, _ = whole(ph, "elastic", mat, 2, 1002, 0.05, loads, 5)
+    us, reps = slab(ph, "elastic", mat, 2, 1002, 0.05, loads, 5, nranks)
+    assert [r["iterations"] for r in reps] == [5, 5]
+    assert rel(us, uw) <= 1e-11
+
+
+def test_slab_against_oracle():
+    ph = np.ascontiguousarray(synth.spheres_rsa(32, 0.3, 3.0, 5.0, seed=1))
+    mat = (1.0, 30.0)
+    g = fem.Grid((32, 32, 32), h=1 / 32)
+    load = np.eye(3)[2:3]
+    ref = homog.solve_problem(g, "thermal", ph, mat, load, 77, 0.1, fixed_iters=7)
+    us, _ = slab(ph, "thermal", mat, 1, 77, 0.1, load, 7, 2)
+    assert rel(us[0], ref["U"][0]) <= 1e-9
