@@ -11,6 +11,7 @@
 // -> caller all-reduce -> slab_apply_kernel (the same device CG logic as the whole-grid loop).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -56,41 +57,40 @@ struct uno_slab_handle {
 };
 
 // ---------------------------------------------------------------------------------------- kernels
-// forward pack: slab spectrum S[lc][kx][z][y] -> send[q][lc][kx][z][yc], y = q Yc + yc
-__global__ void slab_pack_kernel(const double2* __restrict__ S, double2* __restrict__ out, long long blk, int Yc,
-                                 int N2, int nranks) {
-  const long long tot = blk * nranks;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
-    const long long q = e / blk, rem = e - q * blk;          // rem = (row) * Yc + yc, row = (lc, kx, z)
-    const long long row = rem / Yc;
-    const int yc = (int)(rem - row * Yc);
-    out[e] = S[row * N2 + q * Yc + yc];
-  }
+// forward pack: slab spectrum S[row][y] (row = (lc, kx, z), N2 per row) -> send[q][row][yc],
+// y = q Yc + yc; unpack is the inverse.  grid.z = q, grid.y strides the rows, threads the yc
+// of a row (contiguous on both sides), 16-byte elements, no 64-bit divisions.
+__global__ void slab_pack_kernel(const double2* __restrict__ S, double2* __restrict__ out, long long rows, int Yc,
+                                 int N2) {
+  const int q = blockIdx.z;
+  const int ty = threadIdx.x / Yc, yc = threadIdx.x - ty * Yc, rpb = blockDim.x / Yc;
+  double2* o = out + (long long)q * rows * Yc;
+  for (long long row = (long long)blockIdx.y * rpb + ty; row < rows; row += (long long)gridDim.y * rpb)
+    o[row * Yc + yc] = S[row * N2 + (long long)q * Yc + yc];
 }
-// inverse of slab_pack_kernel: recv[q][lc][kx][z][yc] -> S[lc][kx][z][q Yc + yc]
-__global__ void slab_unpack_kernel(const double2* __restrict__ in, double2* __restrict__ S, long long blk, int Yc,
-                                   int N2, int nranks) {
-  const long long tot = blk * nranks;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
-    const long long q = e / blk, rem = e - q * blk;
-    const long long row = rem / Yc;
-    const int yc = (int)(rem - row * Yc);
-    S[row * N2 + q * Yc + yc] = in[e];
-  }
+__global__ void slab_unpack_kernel(const double2* __restrict__ in, double2* __restrict__ S, long long rows, int Yc,
+                                   int N2) {
+  const int q = blockIdx.z;
+  const int ty = threadIdx.x / Yc, yc = threadIdx.x - ty * Yc, rpb = blockDim.x / Yc;
+  const double2* src = in + (long long)q * rows * Yc;
+  for (long long row = (long long)blockIdx.y * rpb + ty; row < rows; row += (long long)gridDim.y * rpb)
+    S[row * N2 + (long long)q * Yc + yc] = src[row * Yc + yc];
 }
-// recv[q][lc][kx][zq][yc] <-> pencil P[lc][kx][q Z + zq][yc]  (dir 0: into the pencil)
-__global__ void slab_pencil_kernel(double2* __restrict__ buf, double2* __restrict__ P, long long blk, int Z, int Yc,
-                                   int N3, int nranks, int dir) {
-  const long long tot = blk * nranks;
-  const long long zy = (long long)Z * Yc;
-  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
-    const long long q = e / blk, rem = e - q * blk;  // rem = (lckx) * Z Yc + zq Yc + yc
-    const long long lckx = rem / zy, r2 = rem - lckx * zy;
-    const long long pi = lckx * (long long)N3 * Yc + q * zy + r2;
-    if (dir == 0)
-      P[pi] = buf[e];
-    else
-      buf[e] = P[pi];
+// recv[q][lckx][zq][yc] <-> pencil P[lckx][q Z + zq][yc]: both sides are contiguous runs of Z Yc
+// (dir 0: into the pencil)
+__global__ void slab_pencil_kernel(double2* __restrict__ buf, double2* __restrict__ P, long long nlckx, int Z, int Yc,
+                                   int N3, int dir) {
+  const int q = blockIdx.z;
+  const long long run = (long long)Z * Yc;
+  for (long long lk = blockIdx.y; lk < nlckx; lk += gridDim.y) {
+    double2* b = buf + ((long long)q * nlckx + lk) * run;
+    double2* p = P + lk * (long long)N3 * Yc + (long long)q * run;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < run; i += (long long)gridDim.x * blockDim.x) {
+      if (dir == 0)
+        p[i] = b[i];
+      else
+        b[i] = p[i];
+    }
   }
 }
 // halo send: plane 0 and plane Z-1 of every (load, comp) slab of d -> out[2][lc][plane]
@@ -128,6 +128,13 @@ __global__ void slab_subtract_kernel(double* __restrict__ u, long long n, const 
 static unsigned grid_for(long long n) {
   long long b = (n + 255) / 256;
   return (unsigned)(b > 148 * 16 ? 148 * 16 : (b < 1 ? 1 : b));
+}
+
+static int pack_threads(int Yc) { return Yc >= 256 ? Yc : 256; }  // whole rows per CTA (Yc | 256 or Yc >= 256)
+static dim3 pack_grid(long long rows, int Yc, int nranks) {
+  const long long rpb = pack_threads(Yc) / Yc;
+  const long long nb = (rows + rpb - 1) / rpb;
+  return dim3(1, (unsigned)std::min<long long>(nb, 8192), nranks);
 }
 
 static void twid(int L, int denom, std::vector<double2>& out) {
@@ -366,9 +373,9 @@ extern "C" uno_status uno_slab_forward(uno_slab_handle* h, double* d_send) {
   SKL(launch_xfwd(h->cxy, CG, h->r, h->s));
   SKL(launch_ypass(h->cxy, CG, false, h->s));
   const Geo& g = h->gxy;
-  const long long blk = (long long)g.nrhs * g.c * g.H1 * h->Z * h->Yc;
-  slab_pack_kernel<<<grid_for(blk * h->nranks), 256, 0, h->s>>>(h->spec, reinterpret_cast<double2*>(d_send), blk, h->Yc,
-                                                               g.N2, h->nranks);
+  const long long rows = (long long)g.nrhs * g.c * g.H1 * h->Z;
+  slab_pack_kernel<<<pack_grid(rows, h->Yc, h->nranks), pack_threads(h->Yc), 0, h->s>>>(
+      h->spec, reinterpret_cast<double2*>(d_send), rows, h->Yc, g.N2);
   SCK(cudaGetLastError());
   return UNO_OK;
 }
@@ -376,13 +383,13 @@ extern "C" uno_status uno_slab_forward(uno_slab_handle* h, double* d_send) {
 extern "C" uno_status uno_slab_green(uno_slab_handle* h, const double* d_recv, double* d_send) {
   if (!h || !d_recv || !d_send) return sfail(UNO_ERR_ARG, "null argument");
   const Geo& g = h->gxy;
-  const long long blk = (long long)g.nrhs * g.c * g.H1 * h->Z * h->Yc;
-  const unsigned gb = grid_for(blk * h->nranks);
+  const long long nlckx = (long long)g.nrhs * g.c * g.H1;
+  const dim3 gb(1, (unsigned)std::min<long long>(nlckx, 4096), h->nranks);
   slab_pencil_kernel<<<gb, 256, 0, h->s>>>(const_cast<double2*>(reinterpret_cast<const double2*>(d_recv)), h->pencil,
-                                          blk, h->Z, h->Yc, h->gz.N3, h->nranks, 0);
+                                          nlckx, h->Z, h->Yc, h->gz.N3, 0);
   SKL(launch_gpass(h->cz, CG, h->s));
-  slab_pencil_kernel<<<gb, 256, 0, h->s>>>(reinterpret_cast<double2*>(d_send), h->pencil, blk, h->Z, h->Yc, h->gz.N3,
-                                          h->nranks, 1);
+  slab_pencil_kernel<<<gb, 256, 0, h->s>>>(reinterpret_cast<double2*>(d_send), h->pencil, nlckx, h->Z, h->Yc, h->gz.N3,
+                                          1);
   SCK(cudaGetLastError());
   return UNO_OK;
 }
@@ -390,9 +397,9 @@ extern "C" uno_status uno_slab_green(uno_slab_handle* h, const double* d_recv, d
 extern "C" uno_status uno_slab_inverse(uno_slab_handle* h, const double* d_recv, double* d_halo_send) {
   if (!h || !d_recv || !d_halo_send) return sfail(UNO_ERR_ARG, "null argument");
   const Geo& g = h->gxy;
-  const long long blk = (long long)g.nrhs * g.c * g.H1 * h->Z * h->Yc;
-  slab_unpack_kernel<<<grid_for(blk * h->nranks), 256, 0, h->s>>>(reinterpret_cast<const double2*>(d_recv), h->spec, blk,
-                                                                 h->Yc, g.N2, h->nranks);
+  const long long rows = (long long)g.nrhs * g.c * g.H1 * h->Z;
+  slab_unpack_kernel<<<pack_grid(rows, h->Yc, h->nranks), pack_threads(h->Yc), 0, h->s>>>(
+      reinterpret_cast<const double2*>(d_recv), h->spec, rows, h->Yc, g.N2);
   SKL(launch_ypass(h->cxy, CG, true, h->s));
   SKL(launch_xinv(h->cxy, CG, nullptr, h->s));
   const long long plane = (long long)g.N1 * g.N2;

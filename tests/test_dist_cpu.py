@@ -72,3 +72,79 @@ def test_gloo_world2_sharding_and_reductions(world):
 def test_shard_single_rank_is_identity():
     probs = list(range(10))
     assert D.shard(probs, 1, 0) == probs
+
+
+# ----------------------------------------------------------------------------- slab exchanges
+def _slab_bufs(rank, world, blk=6, hs=5):
+    import torch
+
+    g = torch.Generator().manual_seed(100 + rank)
+    send = torch.randn((world, blk), generator=g, dtype=torch.float64)
+    hsend = torch.randn((2, hs), generator=g, dtype=torch.float64)
+    red = torch.randn(3, generator=g, dtype=torch.float64)
+    return send, hsend, red
+
+
+def _slab_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2508_02681_b200.slab import MAX, SUM, DistComm
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    comm = DistComm()
+    send, hsend, red = _slab_bufs(rank, world)
+    recv = torch.empty_like(send)
+    hrecv = torch.empty_like(hsend)
+    comm.all_to_all([send], [recv])
+    comm.halo([hsend], [hrecv])
+    rs, rm = red.clone(), red.clone()
+    comm.allreduce([rs], SUM)
+    comm.allreduce([rm], MAX)
+    q.put((rank, recv.numpy(), hrecv.numpy(), rs.numpy(), rm.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gloo_slab_exchanges_match_in_process_emulation(world):
+    # DistComm (one process per rank) moves exactly what LocalComm (the single-GPU emulation
+    # the GPU parity tests run) moves: all-to-all blocks, periodic halo planes, reductions.
+    import numpy as np
+
+    from paper_2508_02681_b200.slab import MAX, SUM, LocalComm
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_slab_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    outs = sorted([q.get(timeout=120) for _ in range(world)], key=lambda o: o[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    loc = LocalComm(world)
+    bufs = [_slab_bufs(r, world) for r in range(world)]
+    sends = [b[0] for b in bufs]
+    recvs = [s.clone() * 0 for s in sends]
+    loc.all_to_all(sends, recvs)
+    hs = [b[1] for b in bufs]
+    hr = [h.clone() * 0 for h in hs]
+    loc.halo(hs, hr)
+    rs = [b[2].clone() for b in bufs]
+    rm = [b[2].clone() for b in bufs]
+    loc.allreduce(rs, SUM)
+    loc.allreduce(rm, MAX)
+    for rank, recv, hrecv, s, m in outs:
+        np.testing.assert_array_equal(recv, recvs[rank].numpy())
+        np.testing.assert_array_equal(hrecv, hr[rank].numpy())
+        np.testing.assert_allclose(s, rs[rank].numpy(), rtol=1e-15)
+        np.testing.assert_array_equal(m, rm[rank].numpy())
+    # the all-to-all is a block transpose; the halo delivers each rank its z-neighbours' planes
+    for q_ in range(world):
+        for r in range(world):
+            np.testing.assert_array_equal(recvs[q_][r].numpy(), sends[r][q_].numpy())
+        np.testing.assert_array_equal(hr[q_][0].numpy(), hs[(q_ - 1) % world][1].numpy())
+        np.testing.assert_array_equal(hr[q_][1].numpy(), hs[(q_ + 1) % world][0].numpy())
