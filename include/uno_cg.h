@@ -153,6 +153,15 @@ UNO_API uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, double 
  *   d_u: device [nrhs][c][N3][N2][N1]; h_loads as uno_cg_rhs; h_out: host [nrhs][nrhs]. */
 UNO_API uno_status uno_cg_effective_property(uno_cg_handle* h, const double* d_u, const double* h_loads, double* h_out);
 
+/* Preconditioner of the PCG loop (uno_cg_solve) and of uno_cg_apply_precond:
+ *   UNO_PRECOND_UNO      P = T^H Q T, the UNO / FANS symbol (default; Eq 48)
+ *   UNO_PRECOND_IDENTITY P = I, unpreconditioned CG
+ *   UNO_PRECOND_JACOBI   P = diag(A)^-1 (Eq 25), diag(A) from the phase field
+ * — the paper's baselines of §6 / Table 4.  The choice stays with the handle
+ * (uno_cg_update recomputes the Jacobi diagonal for the new problem).                     */
+enum { UNO_PRECOND_UNO = 0, UNO_PRECOND_IDENTITY = 1, UNO_PRECOND_JACOBI = 2 };
+UNO_API uno_status uno_cg_set_preconditioner(uno_cg_handle* h, int32_t kind);
+
 /* Timing of the most recent uno_cg_solve (CUDA events on desc.stream, ms), and the number
  * of library kernels it launched.                                                       */
 UNO_API uno_status uno_cg_last_solve_stats(uno_cg_handle* h, double* ms, int64_t* kernel_launches);

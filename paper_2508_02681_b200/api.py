@@ -27,7 +27,8 @@ class SolveResult:
 
 class UnoCG:
     def __init__(self, phase: torch.Tensor, physics: str, mat, nrhs: int, seed: int = 0, amp: float | None = None,
-                 h: float = 0.0, ref=None, stream: torch.cuda.Stream | None = None, bc=(0, 0, 0)):
+                 h: float = 0.0, ref=None, stream: torch.cuda.Stream | None = None, bc=(0, 0, 0),
+                 precond: str = "uno"):
         assert phase.is_cuda and phase.dtype == torch.uint8 and phase.is_contiguous()
         self.phase = phase
         self.dim = phase.dim()
@@ -60,8 +61,16 @@ class UnoCG:
         d.stream = self.stream.cuda_stream
         self.desc = d
         self.handle = B.uno_cg_create(d, phase)
+        self.precond = "uno"
+        if precond != "uno":
+            self.set_preconditioner(precond)
         nshp = (shp[0] - 1,) + shp[1:] if (self.dim == 3 and self.bc[2] == 1) else shp  # Dirichlet z: interior planes
         self.field_shape = (nrhs, self.c) + nshp
+
+    def set_preconditioner(self, kind: str):
+        """"uno" (T^H Q T, default), "identity" (unpreconditioned CG) or "jacobi" (Eq 25)."""
+        B.uno_cg_set_preconditioner(self.handle, kind)
+        self.precond = kind
 
     def update(self, phase: torch.Tensor, mat, seed: int | None = None, amp: float | None = None, ref=None):
         """Re-target this solver to another microstructure/material set of the same grid (a0 only)."""

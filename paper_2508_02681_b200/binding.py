@@ -21,8 +21,9 @@ UNO_OK, UNO_ERR_ARG, UNO_ERR_SHAPE, UNO_ERR_CUDA, UNO_ERR_UNSUPPORTED, UNO_ERR_N
 UNO_THERMAL, UNO_ELASTIC = 0, 1
 
 EXPORTS = ("uno_cg_create", "uno_cg_destroy", "uno_cg_update", "uno_cg_rhs", "uno_cg_apply_K", "uno_cg_apply_precond",
-           "uno_cg_solve", "uno_cg_effective_property", "uno_cg_last_solve_stats", "uno_cg_kernel_timing",
-           "uno_cg_last_error", "uno_cg_version")
+           "uno_cg_solve", "uno_cg_effective_property", "uno_cg_set_preconditioner", "uno_cg_last_solve_stats",
+           "uno_cg_kernel_timing", "uno_cg_last_error", "uno_cg_version")
+UNO_PRECOND = {"uno": 0, "identity": 1, "jacobi": 2}
 # include/uno_cg_slab.h (z-slab decomposition)
 SLAB_EXPORTS = ("uno_slab_create", "uno_slab_destroy", "uno_slab_sizes", "uno_slab_begin", "uno_slab_forward",
                 "uno_slab_green", "uno_slab_inverse", "uno_slab_kapply", "uno_slab_reduce", "uno_slab_apply",
@@ -60,6 +61,7 @@ def _load():
     lib.uno_cg_solve.argtypes = [P, P, D, I32, I32, P, P, P]
     lib.uno_cg_effective_property.argtypes = [P, P, P, P]
     lib.uno_cg_last_solve_stats.argtypes = [P, C.POINTER(D), C.POINTER(I64)]
+    lib.uno_cg_set_preconditioner.argtypes = [P, I32]
     lib.uno_cg_kernel_timing.argtypes = [P, I32, I32, P, P]
     lib.uno_slab_create.argtypes = [C.POINTER(UnoCgDesc), I32, I32, P, C.POINTER(P)]
     lib.uno_slab_destroy.argtypes = [P]
@@ -152,6 +154,10 @@ def uno_cg_solve(h: int, loads, rel_tol: float, max_iter: int, fixed_iters: int,
     out = [dict(iterations=r.iterations, converged=bool(r.converged), status=r.status, r0_inf=r.r0_inf,
                 rel_res=r.rel_res, gamma_last=r.gamma_last) for r in reps]
     return out, hist
+
+
+def uno_cg_set_preconditioner(h: int, kind: str):
+    _check(_lib.uno_cg_set_preconditioner(h, UNO_PRECOND[kind]), "uno_cg_set_preconditioner")
 
 
 def uno_cg_effective_property(h: int, d_u, loads, nrhs: int) -> np.ndarray:

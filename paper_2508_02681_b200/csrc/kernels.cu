@@ -2199,6 +2199,11 @@ int launch_scalar(const Ctx& cx, int slot, int mode, cudaStream_t s) {
   return 1;
 }
 
+int launch_scalar_n(const Ctx& cx, int slot, int mode, int nblk, cudaStream_t s) {
+  scalar_kernel<<<cx.g.nrhs, SC_T, 0, s>>>(cx, slot, nblk, mode);
+  return 1;
+}
+
 // Device-side loop control of the CUDA-graph WHILE node: keep iterating while any load case
 // is active (and below a safety cap on body executions).
 __global__ void loop_ctl_kernel(cudaGraphConditionalHandle h, const LoadState* st, int nrhs, int* counter, int cap) {

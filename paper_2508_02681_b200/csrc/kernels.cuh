@@ -71,6 +71,13 @@ int launch_f3(const Ctx& cx, int mode, double* dst, cudaStream_t s);
 int launch_kp_elastic_modal(const Ctx& cx, int mode, const double* src, double* dst, cudaStream_t s);
 int kp_elastic_modal_nblk(const Geo& g);
 
+// baseline preconditioners P = I / Jacobi (Eq 25), precond.cu; kind 1 = identity, 2 = Jacobi
+int launch_jacobi_dinv(const Ctx& cx, double* dinv, cudaStream_t s);
+int launch_jac_r(const Ctx& cx, int kind, int mode, const double* dinv, const double* src, double* z, cudaStream_t s);
+int launch_jac_d(const Ctx& cx, int kind, const double* dinv, cudaStream_t s);
+int jacobi_nblk(const Geo& g);
+int launch_scalar_n(const Ctx& cx, int slot, int mode, int nblk, cudaStream_t s);  // explicit partial count
+
 // mixed BC (Dirichlet on z), dst.cu
 int launch_dstz(const Ctx& cx, int mode, bool inverse, const double* src, double* dst, cudaStream_t s);
 

@@ -84,6 +84,9 @@ struct uno_cg_handle {
   // pipelined schedule: fork/join streams and dependency events used during graph capture
   cudaStream_t aux[2];
   cudaEvent_t pev[4];
+  // preconditioner kind (0 UNO, 1 identity, 2 Jacobi) and the Jacobi inverse diagonal [n]
+  int precond;
+  double* dinv;
 };
 
 // ------------------------------------------------------------------------------ helpers
@@ -166,7 +169,7 @@ static void free_all(uno_cg_handle* h) {
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   for (auto e : h->tev) cudaEventDestroy(e);
   void* bufs[] = {h->r, h->d, h->p, h->u, h->spec, h->gtab, h->kel, h->twx, h->twxp, h->twy, h->twz, h->twz2, h->rt,
-                  h->st, h->partials, h->counters, h->results, h->scratch, h->hist, h->loopctr};
+                  h->st, h->partials, h->counters, h->results, h->scratch, h->hist, h->loopctr, h->dinv};
   for (void* b : bufs)
     if (b) cudaFreeAsync(b, h->stream);
   if (h->h_st) cudaFreeHost(h->h_st);
@@ -217,6 +220,7 @@ static uno_status setup_problem(uno_cg_handle* h) {
     cudaStreamSynchronize(s);
   }
   h->cx = make_ctx(h);
+  if (h->precond == 2 && h->dinv) launch_jacobi_dinv(h->cx, h->dinv, s);  // Eq 25 for the new problem
   // a0: symbol table + Eq 55 check
   launch_build_symbol(h->cx, h->gtab, h->ref0, h->ref1, D.seed, D.seed ? D.amp : 0.0, s);
   int nblk = 0;
@@ -417,6 +421,20 @@ extern "C" uno_status uno_cg_update(uno_cg_handle* h, const uno_cg_desc* desc, c
   return setup_problem(h);
 }
 
+extern "C" uno_status uno_cg_set_preconditioner(uno_cg_handle* h, int32_t kind) {
+  if (!h) return fail(UNO_ERR_ARG, "null handle");
+  if (kind < UNO_PRECOND_UNO || kind > UNO_PRECOND_JACOBI) return fail(UNO_ERR_ARG, "kind must be 0, 1 or 2");
+  if (kind == UNO_PRECOND_JACOBI && !h->dinv) CK(cudaMallocAsync((void**)&h->dinv, (size_t)h->g.n * 8, h->stream));
+  h->precond = kind;
+  if (kind == UNO_PRECOND_JACOBI) launch_jacobi_dinv(h->cx, h->dinv, h->stream);
+  if (h->gexec) {  // the iteration body changes: re-capture on the next solve
+    cudaGraphExecDestroy(h->gexec);
+    h->gexec = nullptr;
+  }
+  CK(cudaGetLastError());
+  return UNO_OK;
+}
+
 static void fill_loads(const uno_cg_handle* h, const double* h_loads, LoadParams& lp) {
   std::memset(&lp, 0, sizeof(lp));
   const int nv = h->g.c == 1 ? h->g.dim : (h->g.dim == 3 ? 6 : 3);
@@ -452,7 +470,10 @@ extern "C" uno_status uno_cg_apply_precond(uno_cg_handle* h, const double* d_r, 
   if (!h || !d_r || !d_z) return fail(UNO_ERR_ARG, "null argument");
   long long launches = 0;
   cudaStream_t s = h->stream;
-  if (h->g.dirz) {  // mixed BC: DST-I along z first, then the periodic x/y machinery
+  if (h->precond != 0) {  // z = P r (identity / Jacobi) and r.z
+    KL(launch_jac_r(h->cx, h->precond, STANDALONE, h->dinv, d_r, d_z, s), KC_XF);
+    KL(launch_scalar_n(h->cx, RED_GAMMA, STANDALONE, jacobi_nblk(h->g), s), KC_OTHER);
+  } else if (h->g.dirz) {  // mixed BC: DST-I along z first, then the periodic x/y machinery
     KL(launch_dstz(h->cx, STANDALONE, false, d_r, h->rt, s), KC_XF);
     KL(launch_xfwd(h->cx, STANDALONE, h->rt, s), KC_XF);
     KL(launch_gpass(h->cx, STANDALONE, s), KC_G);
@@ -496,7 +517,13 @@ static int enqueue_iteration(uno_cg_handle* h, cudaStream_t s, cudaEvent_t* ev /
     n += r;
     return true;
   };
-  if (h->g.dirz) {  // mixed BC (dst.cu): DST_z (+CG r update) | x | y.G.y^-1 | x^-1 | DST_z^-1 (+d, u)
+  if (h->precond != 0) {  // baselines (precond.cu): r pass | scalars | d pass, then K
+    const int nb = jacobi_nblk(h->g);
+    if (!run(0, [&] { return launch_jac_r(cx, h->precond, CG, h->dinv, nullptr, nullptr, s); })) return -1;
+    n += launch_scalar_n(cx, RED_RNORM, CG, nb, s);
+    n += launch_scalar_n(cx, RED_GAMMA, CG, nb, s);
+    if (!run(4, [&] { return launch_jac_d(cx, h->precond, h->dinv, s); })) return -1;
+  } else if (h->g.dirz) {  // mixed BC (dst.cu): DST_z (+CG r update) | x | y.G.y^-1 | x^-1 | DST_z^-1 (+d, u)
     if (!run(0, [&] { return launch_dstz(cx, CG, false, cx.r, h->rt, s); })) return -1;
     n += launch_scalar(cx, RED_RNORM, CG, s);
     if (!run(1, [&] { return launch_xfwd(cx, PLAIN, h->rt, s); })) return -1;
@@ -686,7 +713,7 @@ extern "C" uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, doub
   CK(cudaMemcpyAsync(h->st, h->h_st, g.nrhs * sizeof(LoadState), cudaMemcpyHostToDevice, s));
   const long long work = (long long)g.nrhs * g.c * g.n;
   // passes + 3 scalar kernels (mixed: 6 too); pipelined: 2C + 1 + 3C over C z-chunks
-  const int per_iter = g.ZP > 0 ? 5 * (g.N3 / g.ZP) + 4 : ((g.dim == 3 && g.NB == 0) ? 6 : 4) + 3;
+  const int per_iter = h->precond != 0 ? 6 : (g.ZP > 0 ? 5 * (g.N3 / g.ZP) + 4 : ((g.dim == 3 && g.NB == 0) ? 6 : 4) + 3);
   if (!h->timing) {
     // whole solve device-side: WHILE node over bodies of `chunk` iterations
     const int chunk = work >= (1LL << 22) ? 2 : 4;
