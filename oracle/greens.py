@@ -285,3 +285,85 @@ def dense_P_mixed(G: np.ndarray, spatial_shape) -> np.ndarray:
         for b in range(c):
             P[a * n:(a + 1) * n, b * n:(b + 1) * n] = T.conj().T @ (G[a, b].reshape(-1)[:, None] * T)
     return P.real
+
+
+# ---------------------------------------------------------------- all-Dirichlet
+def symbol_probe_dirichlet(g: fem.Grid, physics: str, ref) -> np.ndarray:
+    """Diagonal block of U K_r U^T for U = DST-I on every axis, by probing: the stencil of the
+    homogeneous reference operator is read off K_r applied to a delta at an interior node; a
+    stencil row maps sin(theta j) to sin(theta j) sum_d c_d cos(theta d) + cos(theta j) sum_d c_d
+    sin(theta d), so the diagonal block keeps the part even in every offset:
+        A_ab(m) = sum_off c_ab(off) prod_i cos(pi m_i off_i / N_i),  m_i = 1..N_i - 1
+    (thermal: exact — the sine basis diagonalises K_r; elastic: the couplings odd in two
+    offsets drop, the reading of SURVEY A13 on every axis).  Returns (c, c, N3-1, N2-1, N1-1)."""
+    assert all(b == 1 for b in g.bc)
+    c, d = g.c, g.d
+    shp = g.node_shape
+    assert all(v >= 3 for v in shp)
+    ctr = tuple(v // 2 for v in shp)
+    phase0 = np.zeros(g.elem_shape, dtype=np.uint8)
+    mat = (ref, ref)
+    A = np.zeros((c, c) + shp)
+    offs = list(np.ndindex(*([3] * d)))
+    grids = np.meshgrid(*[np.arange(1, v + 1) for v in shp], indexing="ij")
+    for b in range(c):
+        delta = np.zeros((c,) + shp)
+        delta[(b,) + ctr] = 1.0
+        col = fem.apply_K(g, physics, phase0, mat, delta)
+        for off in offs:
+            o = tuple(k - 1 for k in off)  # numpy-axis offsets (z, y, x)
+            idx = tuple(ct + oo for ct, oo in zip(ctr, o))
+            w = np.ones(shp)
+            for ax, oo in enumerate(o):
+                w = w * np.cos(np.pi * grids[ax] * oo / (shp[ax] + 1))
+            for a in range(c):
+                # K_r is symmetric: c_ab(off) = (K_r e_b)_a at ctr + off
+                A[a, b] += col[(a,) + idx] * w
+    return 0.5 * (A + np.swapaxes(A, 0, 1))
+
+
+def ghat_dirichlet(g: fem.Grid, physics: str, mat, seed: int, amp: float, ref=None) -> np.ndarray:
+    """G_hat(m) = rho(m) / A(m) (c = 1) or inv(A(m)) + amp tr/3 psi(theta(m)) (c = 3), the
+    perturbation of SURVEY A8 drawn at the flat mode index (sine modes are self-conjugate):
+    canon(m) = ((m3-1)(N2-1) + (m2-1))(N1-1) + (m1-1)."""
+    if ref is None:
+        ref = reference_medium(physics, mat)
+    A = symbol_probe_dirichlet(g, physics, ref)
+    c = g.c
+    shp = g.node_shape
+    can = np.arange(int(np.prod(shp))).reshape(shp)
+    if c == 1:
+        rho = (1.0 - amp + 2.0 * amp * u01(seed, 2, can.astype(np.uint64))) if seed else np.ones(shp)
+        return (rho / A[0, 0])[None, None]
+    Am = np.moveaxis(A.reshape(c, c, -1), -1, 0)
+    Phi = np.linalg.inv(Am)
+    Phi = 0.5 * (Phi + np.transpose(Phi, (0, 2, 1)))
+    if seed:
+        base = (8 * can.reshape(-1)).astype(np.uint64)
+        th = np.stack([u01(seed, 2, base + np.uint64(t)) for t in range(6)])
+        for t in (0, 1, 3):
+            th[t] = 0.5 + 0.5 * th[t]
+        for t in (2, 4, 5):
+            th[t] = th[t] - 0.5
+        P = np.moveaxis(psi3(th), -1, 0)
+        tr = np.trace(Phi, axis1=1, axis2=2) / 3.0
+        Phi = Phi + amp * tr[:, None, None] * P
+    return np.moveaxis(Phi, 0, -1).reshape((c, c) + shp)
+
+
+def apply_precond_dirichlet(G: np.ndarray, r: np.ndarray) -> np.ndarray:
+    """s = U^T Q U r with U = DST-I on every axis (Eq 48 with the Dirichlet transform)."""
+    rh = transform.forward_dirichlet(r)
+    sh = np.einsum("ab...,b...->a...", G, rh)
+    return transform.inverse_dirichlet(sh)
+
+
+def dense_P_dirichlet(G: np.ndarray, spatial_shape) -> np.ndarray:
+    c = G.shape[0]
+    n = int(np.prod(spatial_shape))
+    T = transform.dense_T_dirichlet(spatial_shape)
+    P = np.zeros((c * n, c * n))
+    for a in range(c):
+        for b in range(c):
+            P[a * n:(a + 1) * n, b * n:(b + 1) * n] = T.T @ (G[a, b].reshape(-1)[:, None] * T)
+    return P

@@ -128,8 +128,16 @@ def solve_problem(g: fem.Grid, physics: str, phase, mat, loads, seed: int, amp: 
     """Full oracle pipeline for one problem: RHS (a1), G_hat (a0), Alg 2 (a2-a8), mean
     removal and effective property (a9).  Returns dict with per-load results."""
     mixed = g.bc == (0, 0, 1)
-    G = greens.ghat_mixed(g, physics, mat, seed, amp) if mixed else greens.ghat(g, physics, mat, seed, amp)
-    applyP = (lambda v: greens.apply_precond_mixed(G, v)) if mixed else (lambda v: greens.apply_precond(G, v))
+    alld = g.d == 3 and all(b == 1 for b in g.bc)
+    if alld:
+        G = greens.ghat_dirichlet(g, physics, mat, seed, amp)
+        applyP = lambda v: greens.apply_precond_dirichlet(G, v)  # noqa: E731
+    elif mixed:
+        G = greens.ghat_mixed(g, physics, mat, seed, amp)
+        applyP = lambda v: greens.apply_precond_mixed(G, v)  # noqa: E731
+    else:
+        G = greens.ghat(g, physics, mat, seed, amp)
+        applyP = lambda v: greens.apply_precond(G, v)  # noqa: E731
     F, U, its, results = [], [], [], []
     for ld in loads:
         f = fem.rhs(g, physics, phase, mat, ld)

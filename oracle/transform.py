@@ -83,3 +83,24 @@ def dense_T_mixed(spatial_shape) -> np.ndarray:
     """Unitary F_x (x) F_y (x) S_z for C-order (z, y, x) flattened fields with z Dirichlet."""
     nz, ny, nx = spatial_shape
     return np.kron(np.kron(dst1_matrix(nz).astype(complex), dft_matrix(ny)), dft_matrix(nx))
+
+
+# ---------------------------------------------------------------- all-Dirichlet (SURVEY §8(f) rank 1)
+def forward_dirichlet(r: np.ndarray) -> np.ndarray:
+    """r_hat = (S_x (x) S_y (x) S_z) r for fields (c, N3-1, N2-1, N1-1): orthonormal DST-I along
+    every spatial axis (Table 1 row "Dirichlet").  Real, symmetric, self-inverse."""
+    from scipy.fft import dstn
+    return dstn(r, type=1, axes=tuple(range(1, r.ndim)), norm="ortho")
+
+
+def inverse_dirichlet(rh: np.ndarray) -> np.ndarray:
+    from scipy.fft import idstn
+    return idstn(rh, type=1, axes=tuple(range(1, rh.ndim)), norm="ortho")
+
+
+def dense_T_dirichlet(spatial_shape) -> np.ndarray:
+    """S_z (x) S_y (x) S_x for C-order flattened interior-node fields (brute force, tiny grids)."""
+    T = np.ones((1, 1))
+    for nm1 in spatial_shape:
+        T = np.kron(T, dst1_matrix(nm1))
+    return T
