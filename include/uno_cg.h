@@ -20,10 +20,14 @@
  *    edge h.  Boundary conditions: periodic on every axis, or (3D) the mixed case of
  *    Eq 82 / §6.4 with periodic x, y and Dirichlet faces on z (bc = {0,0,1}; U = DFT_x (x)
  *    DFT_y (x) DST-I_z, Table 1 "Mixed" P:452; node planes z = 1..N3-1 are the unknowns,
- *    N1 >= 32, N3 <= 512).  Other combinations return UNO_ERR_UNSUPPORTED.
+ *    N1 >= 32, N3 <= 512), or (3D) Dirichlet faces on every axis (bc = {1,1,1}; U = DST-I on
+ *    every axis, Table 1 row "Dirichlet" P:451; N1 >= 32 thermal / 16 elastic, N2 >= 16,
+ *    8 <= N3, all <= 512).  Other combinations return UNO_ERR_UNSUPPORTED.
  *    N1, N2 in {8..1024}, N3 in {1} U {4..1024}, all powers of two.
  *  - Field layout (device): component-planar C order [nrhs][c][P3][N2][N1] with P3 = N3
- *    (periodic) or N3 - 1 (Dirichlet z: stored planes are nodes z = 1..N3-1); node
+ *    (periodic, and all-Dirichlet: the nodes with index 0 on any axis are the fixed boundary
+ *    nodes, held at 0 on input and output) or N3 - 1 (Dirichlet z: stored planes are nodes
+ *    z = 1..N3-1); node
  *    (i,j,k) at h*(i,j,k); voxel (i,j,k) has corners (i+a1, j+a2, k+a3) mod N.
  *    The paper's interleaved vec() (§1.6 Eq 1) is a fixed permutation of this.
  *  - c = 1 (thermal) or c = dim (elastic).  nrhs load cases are iterated together,

@@ -64,7 +64,8 @@ class UnoCG:
         self.precond = "uno"
         if precond != "uno":
             self.set_preconditioner(precond)
-        nshp = (shp[0] - 1,) + shp[1:] if (self.dim == 3 and self.bc[2] == 1) else shp  # Dirichlet z: interior planes
+        mixed = self.dim == 3 and tuple(self.bc) == (0, 0, 1)
+        nshp = (shp[0] - 1,) + shp[1:] if mixed else shp  # Dirichlet z: interior planes; all-Dirichlet: padded
         self.field_shape = (nrhs, self.c) + nshp
 
     def set_preconditioner(self, kind: str):

@@ -1,0 +1,261 @@
+// dirichlet.cu — all-Dirichlet boundaries (bc = {1,1,1}; Table 1 row "Dirichlet", P:451;
+// SURVEY §8(f) rank 1): U = DST-I along every axis.
+//
+// Storage: the periodic layout [N3][N2][N1] with the boundary nodes (index 0 on any axis) held
+// at zero.  Node N_i on the far face is node 0 of the periodic wrap, so the periodic K gather
+// reads exactly the Dirichlet zeros, and K / RHS outputs are masked on the index-0 planes.
+// P r: DST-I of every axis (odd extension of length 2N as a complex FFT on two packed real
+// sequences, as dst.cu does along z), the per-mode c x c symbol multiply, and the DST-I again
+// (self-inverse up to N/2 per axis, folded into the table).  The CG loop runs it as an opaque
+// s = P r between the fused r and d passes of precond.cu, with gamma = r.s in its own pass.
+#include <cuda_runtime.h>
+
+#include <type_traits>
+
+#include "common.cuh"
+#include "dev_common.cuh"
+#include "fft.cuh"
+#include "kernels.cuh"
+
+namespace uno {
+
+template <int L2>
+__host__ __device__ constexpr int d3_smem_bytes() {
+  return (8 * L2 + L2) * (int)sizeof(double2);
+}
+
+// One DST-I pass along `axis` (0 x, 1 y, 2 z) of every (load, comp) field, src -> dst (may alias).
+// A CTA transforms 8 packed sequences (16 real ones): axes y, z pack adjacent x pairs (16-byte
+// loads); axis x packs the rows y, y+1.
+template <int L2>
+__global__ void __launch_bounds__(fft_threads(L2)) dst3_kernel(Ctx cx, const double* __restrict__ src,
+                                                              double* __restrict__ dst, int axis, const double2* twl) {
+  constexpr int T = fft_threads(L2);
+  constexpr int N = L2 / 2;
+  const Geo g = cx.g;
+  extern __shared__ double2 smem[];
+  double2* tile = smem;
+  double2* tw = smem + 8 * L2;
+  const int t = threadIdx.x;
+  const int N1 = g.N1, N2 = g.N2;
+  const long long plane = (long long)N1 * N2;
+  long long base;   // offset of element j = 0 of packed sequence 0
+  long long es;     // element stride (doubles)
+  long long qs;     // stride between packed sequences (doubles)
+  long long ps;     // stride between the two real halves of a packed sequence
+  {
+    int b = blockIdx.x;
+    if (axis == 0) {  // rows: 8 packed pairs = 16 rows y0..y0+15 of plane z
+      const int nyb = N2 / 16;
+      const int yb = b % nyb;
+      b /= nyb;
+      const int z = b % g.N3;
+      const int lc = b / g.N3;
+      base = (long long)lc * g.n + z * plane + (long long)yb * 16 * N1;
+      es = 1;
+      qs = 2LL * N1;
+      ps = N1;
+    } else {  // columns: 8 packed pairs = x0..x0+15 at fixed (y | z)
+      const int nxb = N1 / 16;
+      const int xb = b % nxb;
+      b /= nxb;
+      const int other = axis == 1 ? g.N3 : N2;
+      const int o = b % other;
+      const int lc = b / other;
+      base = (long long)lc * g.n + xb * 16 + (axis == 1 ? (long long)o * plane : (long long)o * N1);
+      es = axis == 1 ? N1 : plane;
+      qs = 2;
+      ps = 1;
+    }
+  }
+  for (int i = t; i < L2; i += T) tw[i] = twl[i];
+  for (int e = t; e < 8 * N; e += T) {
+    const int j = e >> 3, q = e & 7;
+    double2 v = make_double2(0.0, 0.0);
+    if (j > 0) {
+      const long long a = base + q * qs + j * es;
+      v = make_double2(src[a], src[a + ps]);
+    }
+    tile[tidx(j, q)] = v;
+    if (j > 0) tile[tidx(L2 - j, q)] = make_double2(-v.x, -v.y);
+  }
+  if (t < 8) tile[tidx(N, t)] = make_double2(0.0, 0.0);
+  __syncthreads();
+  fft_tile<L2, false>(tile, tw);
+  // sine coefficients m = 1..N-1 of the two halves: (-Im Y_m, Re Y_m) / 2; m = 0 stays 0
+  for (int e = t; e < 8 * N; e += T) {
+    const int m = e >> 3, q = e & 7;
+    const long long a = base + q * qs + m * es;
+    if (m == 0) {
+      dst[a] = 0.0;
+      dst[a + ps] = 0.0;
+    } else {
+      const double2 Y = tile[tidx(m, q)];
+      dst[a] = -0.5 * Y.y;
+      dst[a + ps] = 0.5 * Y.x;
+    }
+  }
+}
+
+// s_hat = G_hat s_hat per sine mode (c x c, unique entries in Eq B7 order), in place
+__global__ void d3_gmul_kernel(Ctx cx, double* __restrict__ v) {
+  const Geo g = cx.g;
+  const long long n = g.n;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    for (int l = 0; l < g.nrhs; ++l) {
+      double* w = v + (long long)l * g.c * n;
+      if (g.c == 1) {
+        w[i] *= cx.gtab[i];
+      } else {
+        const double* G = cx.gtab;
+        const double g1 = G[i], g2 = G[n + i], g3 = G[2 * n + i], g4 = G[3 * n + i], g5 = G[4 * n + i],
+                     g6 = G[5 * n + i];
+        const double a = w[i], b = w[n + i], c = w[2 * n + i];
+        w[i] = fma(g1, a, fma(g3, b, g6 * c));
+        w[n + i] = fma(g3, a, fma(g2, b, g5 * c));
+        w[2 * n + i] = fma(g6, a, fma(g5, b, g4 * c));
+      }
+    }
+  }
+}
+
+// gamma_1 = r.s partial per CTA (fixed grid: jacobi_nblk)
+__global__ void __launch_bounds__(256) d3_dot_kernel(Ctx cx, const double* __restrict__ a, const double* __restrict__ b,
+                                                     int mode) {
+  const Geo g = cx.g;
+  const int load = blockIdx.y;
+  if (mode == CG && !cx.st[load].active) return;
+  __shared__ double red_sh[32];
+  const long long cn = (long long)g.c * g.n;
+  const double* x = a + (long long)load * cn;
+  const double* y = b + (long long)load * cn;
+  double acc = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < cn; i += (long long)gridDim.x * blockDim.x)
+    acc = fma(x[i], y[i], acc);
+  partial_write<false>(cx, RED_GAMMA, load, blockIdx.x, acc, red_sh);
+}
+
+// all-Dirichlet symbol on [N3][N2][N1] (mode m_i at index m_i; index-0 entries 0), already
+// scaled by (2/N1)(2/N2)(2/N3) (unnormalised DST-I round trips).  Closed form of the diagonal
+// block (SURVEY A3 with theta_i = pi m_i / N_i and S_ij = 0 for i != j); perturbation of
+// SURVEY A8 at canon(m) = ((m3-1)(N2-1) + (m2-1))(N1-1) + (m1-1) (oracle/greens.ghat_dirichlet).
+__global__ void d3_symbol_kernel(Ctx cx, double* gtab, double ref0, double ref1, unsigned long long seed, double amp) {
+  const Geo g = cx.g;
+  const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= g.n) return;
+  const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
+  const int s1 = __ffs(N1) - 1, s2 = __ffs(N2) - 1;
+  const int m1 = (int)(b & (N1 - 1)), m2 = (int)((b >> s1) & (N2 - 1)), m3 = (int)(b >> (s1 + s2));
+  const long long n = g.n;
+  if (m1 == 0 || m2 == 0 || m3 == 0) {
+    for (int q = 0; q < g.C; ++q) gtab[q * n + b] = 0.0;
+    return;
+  }
+  double cs[3];
+  cs[0] = cospi((double)m1 / N1);
+  cs[1] = cospi((double)m2 / N2);
+  cs[2] = cospi((double)m3 / N3);
+  const double h = g.h;
+  double mass[3], S[3];
+  for (int i = 0; i < 3; ++i) mass[i] = (h / 3.0) * (2.0 + cs[i]);
+  for (int i = 0; i < 3; ++i) {
+    double v = (2.0 / h) * (1.0 - cs[i]);
+    for (int j = 0; j < 3; ++j)
+      if (j != i) v *= mass[j];
+    S[i] = v;
+  }
+  const double scale = 8.0 / ((double)N1 * N2 * N3);
+  const unsigned long long canon = ((unsigned long long)(m3 - 1) * (N2 - 1) + (m2 - 1)) * (N1 - 1) + (m1 - 1);
+  const double tr = (S[0] + S[1]) + S[2];
+  if (g.c == 1) {
+    const double rho = seed ? (1.0 - amp + 2.0 * amp * u01(seed, 2, canon)) : 1.0;
+    gtab[b] = rho / (tr * ref0) * scale;
+    return;
+  }
+  double P[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+  for (int i = 0; i < 3; ++i) P[i][i] = 1.0 / ((ref0 + ref1) * S[i] + ref1 * tr);
+  if (seed) {
+    double th[6];
+    for (int t = 0; t < 6; ++t) th[t] = u01(seed, 2, 8ULL * canon + t);
+    th[0] = 0.5 + 0.5 * th[0];
+    th[1] = 0.5 + 0.5 * th[1];
+    th[3] = 0.5 + 0.5 * th[3];
+    th[2] -= 0.5;
+    th[4] -= 0.5;
+    th[5] -= 0.5;
+    const double t1 = th[0], t2 = th[1], t3 = th[2], t4 = th[3], t5 = th[4], t6 = th[5];
+    const double psi[3][3] = {{t1 * t1, t1 * t3, t1 * t6},  // psi = L L^T, Eq B5
+                              {t1 * t3, t2 * t2 + t3 * t3, t2 * t5 + t3 * t6},
+                              {t1 * t6, t2 * t5 + t3 * t6, t4 * t4 + t5 * t5 + t6 * t6}};
+    const double a = amp * (P[0][0] + P[1][1] + P[2][2]) / 3.0;
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) P[i][j] += a * psi[i][j];
+  }
+  gtab[b] = P[0][0] * scale;
+  gtab[n + b] = P[1][1] * scale;
+  gtab[2 * n + b] = P[0][1] * scale;
+  gtab[3 * n + b] = P[2][2] * scale;
+  gtab[4 * n + b] = P[1][2] * scale;
+  gtab[5 * n + b] = P[0][2] * scale;
+}
+
+template <class F>
+static int d3_dispatch(int L2, F&& f) {
+  switch (L2) {
+    case 16: return f(std::integral_constant<int, 16>{});
+    case 32: return f(std::integral_constant<int, 32>{});
+    case 64: return f(std::integral_constant<int, 64>{});
+    case 128: return f(std::integral_constant<int, 128>{});
+    case 256: return f(std::integral_constant<int, 256>{});
+    case 512: return f(std::integral_constant<int, 512>{});
+    case 1024: return f(std::integral_constant<int, 1024>{});
+    default: return -1;
+  }
+}
+
+static int launch_dst3(const Ctx& cx, const double* src, double* dst, int axis, const double2* twl, cudaStream_t s) {
+  const Geo& g = cx.g;
+  const int N = axis == 0 ? g.N1 : (axis == 1 ? g.N2 : g.N3);
+  const long long nlc = (long long)g.nrhs * g.c;
+  const long long nb = axis == 0 ? nlc * g.N3 * (g.N2 / 16) : nlc * (axis == 1 ? g.N3 : g.N2) * (g.N1 / 16);
+  return d3_dispatch(2 * N, [&](auto Lc) {
+    constexpr int L2 = decltype(Lc)::value;
+    const int sm = d3_smem_bytes<L2>();
+    if (sm > 48 * 1024) cudaFuncSetAttribute(dst3_kernel<L2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    dst3_kernel<L2><<<(unsigned)nb, fft_threads(L2), sm, s>>>(cx, src, dst, axis, twl);
+    return 1;
+  });
+}
+
+// s = P r for all nrhs fields (7 passes)
+int launch_d3_precond(const Ctx& cx, const double* r, double* sbuf, const double2* const tw2[3], cudaStream_t s) {
+  int n = 0, k;
+  if ((k = launch_dst3(cx, r, sbuf, 0, tw2[0], s)) < 0) return -1;
+  n += k;
+  for (int axis = 1; axis < 3; ++axis) {
+    if ((k = launch_dst3(cx, sbuf, sbuf, axis, tw2[axis], s)) < 0) return -1;
+    n += k;
+  }
+  long long b = (cx.g.n + 255) / 256;
+  d3_gmul_kernel<<<(unsigned)(b > 148 * 16 ? 148 * 16 : b), 256, 0, s>>>(cx, sbuf);
+  ++n;
+  for (int axis = 2; axis >= 0; --axis) {
+    if ((k = launch_dst3(cx, sbuf, sbuf, axis, tw2[axis], s)) < 0) return -1;
+    n += k;
+  }
+  return n;
+}
+
+int launch_d3_dot(const Ctx& cx, const double* a, const double* b, int mode, cudaStream_t s) {
+  const dim3 grid(jacobi_nblk(cx.g), cx.g.nrhs);
+  d3_dot_kernel<<<grid, 256, 0, s>>>(cx, a, b, mode);
+  return 1;
+}
+
+int launch_d3_symbol(const Ctx& cx, double* gtab, double ref0, double ref1, unsigned long long seed, double amp,
+                     cudaStream_t s) {
+  d3_symbol_kernel<<<(unsigned)((cx.g.n + 255) / 256), 256, 0, s>>>(cx, gtab, ref0, ref1, seed, amp);
+  return 1;
+}
+
+}  // namespace uno

@@ -1055,7 +1055,8 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
       EE = fma(Ksum - Kyp, dym, EE);
       EE = fma(Khi, dzp, EE);
       EE = fma(I.Klo[m], dzm, EE);
-      const double pv = hc * (fma(5.0 * di, Ksum, EE) - (I.KSlo[m] + KShi));
+      double pv = hc * (fma(5.0 * di, Ksum, EE) - (I.KSlo[m] + KShi));
+      if (g.dir3 && (x0 + tx == 0 || y0 + 2 * ty + m == 0 || k == 0)) pv = 0.0;  // Dirichlet nodes
       outp[(long long)(k - dz) * plane + m * N1] = pv;
       part = fma(di, pv, part);
       O.KSlo[m] = KShi;
@@ -1269,7 +1270,8 @@ __global__ void __launch_bounds__(128, 2) kp_thermal3d_rn_kernel(Ctx cx, int mod
       EE = fma(Ksum - Kyp, dym, EE);
       EE = fma(Khi, dzp, EE);
       EE = fma(I.Klo[m], I.dzm[m], EE);
-      const double pv = hc * (fma(5.0 * di, Ksum, EE) - (I.KSlo[m] + KShi));
+      double pv = hc * (fma(5.0 * di, Ksum, EE) - (I.KSlo[m] + KShi));
+      if (g.dir3 && (x0 + tx == 0 || y0 + NR * ty + m == 0 || k == 0)) pv = 0.0;  // Dirichlet nodes
       outp[(long long)(k - dz - g.zlo) * plane + m * N1] = pv;
       part = fma(di, pv, part);
       O.KSlo[m] = KShi;
@@ -1786,10 +1788,11 @@ __global__ void __launch_bounds__(256) rhs_kernel(Ctx cx, LoadParams lp, double*
     int z, n[3];
     octant_counts(warp_ok ? node_octants_warp(cx, i, z) : node_octants(cx, i, z), g.dim, n);
     const double n0 = n[0], n1 = n[1], n2 = n[2];
+    const bool fixed = g.dir3 && ((i & (g.N1 - 1)) == 0 || ((i / g.N1) & (g.N2 - 1)) == 0 || z == 0);  // Dirichlet node
     for (int l = 0; l < nl; ++l)
       for (int al = 0; al < c; ++al) {
         const double* Cr = C + (l * c + al) * 3;
-        f[((long long)l * c + al) * g.n + i] = fma(Cr[0], n0, fma(Cr[1], n1, Cr[2] * n2));
+        f[((long long)l * c + al) * g.n + i] = fixed ? 0.0 : fma(Cr[0], n0, fma(Cr[1], n1, Cr[2] * n2));
       }
   }
 }
@@ -2111,6 +2114,8 @@ __global__ void eq55_kernel(Ctx cx, const double* gtab, double* partials) {
   const double nn = g.dirz ? (double)g.n : (double)g.N1 * (g.Ny ? g.Ny : g.N2) * g.N3;
   for (long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x; b < ns; b += (long long)gridDim.x * blockDim.x) {
     if (b == 0 && !g.dirz && g.ky0 == 0) continue;  // periodic: G_hat(0) = 0 shares the null space
+    if (g.dir3 && ((b & (g.N1 - 1)) == 0 || ((b / g.N1) & (g.N2 - 1)) == 0 || b / ((long long)g.N1 * g.N2) == 0))
+      continue;  // all-Dirichlet: index-0 entries are not modes
     double lo, hi;
     if (g.c == 1) {
       lo = hi = gtab[b] * nn;

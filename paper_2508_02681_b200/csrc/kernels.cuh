@@ -78,6 +78,13 @@ int launch_jac_d(const Ctx& cx, int kind, const double* dinv, cudaStream_t s);
 int jacobi_nblk(const Geo& g);
 int launch_scalar_n(const Ctx& cx, int slot, int mode, int nblk, cudaStream_t s);  // explicit partial count
 
+// all-Dirichlet (dirichlet.cu): s = P r (DST-I on every axis, 7 passes), r.s partials, symbol
+int launch_d3_precond(const Ctx& cx, const double* r, double* sbuf, const double2* const tw2[3], cudaStream_t s);
+int launch_d3_dot(const Ctx& cx, const double* a, const double* b, int mode, cudaStream_t s);
+int launch_d3_symbol(const Ctx& cx, double* gtab, double ref0, double ref1, unsigned long long seed, double amp,
+                     cudaStream_t s);
+int launch_jac_d_ext(const Ctx& cx, const double* sbuf, cudaStream_t s);  // d = s + beta d from a buffer
+
 // mixed BC (Dirichlet on z), dst.cu
 int launch_dstz(const Ctx& cx, int mode, bool inverse, const double* src, double* dst, cudaStream_t s);
 

@@ -94,8 +94,9 @@ __global__ void __launch_bounds__(JT) jac_r_kernel(Ctx cx, const double* __restr
   partial_write<false>(cx, RED_GAMMA, load, blockIdx.x, gm, red_sh);
 }
 
-template <bool JAC>
-__global__ void __launch_bounds__(JT) jac_d_kernel(Ctx cx, const double* __restrict__ dinv) {
+// KIND 0: s = r (identity), 1: s = r dinv (Jacobi), 2: s read from `aux` (an opaque P r, dirichlet.cu)
+template <int KIND>
+__global__ void __launch_bounds__(JT) jac_d_kernel(Ctx cx, const double* __restrict__ aux) {
   const Geo g = cx.g;
   const int load = blockIdx.y;
   const LoadState* st = cx.st + load;
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(JT) jac_d_kernel(Ctx cx, const double* __restr
   const int it0 = st->iters;
   const double beta = st->beta, alpha = st->alpha;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < cn; i += (long long)gridDim.x * blockDim.x) {
-    const double s = JAC ? rr[i] * dinv[g.c == 1 ? i : i % g.n] : rr[i];
+    const double s = KIND == 2 ? aux[(long long)load * cn + i] : (KIND == 1 ? rr[i] * aux[g.c == 1 ? i : i % g.n] : rr[i]);
     if (it0 == 0) {
       d[i] = s;  // d = s  (Alg 2 l.2, l.8)
     } else {
@@ -147,8 +148,14 @@ int launch_jac_r(const Ctx& cx, int kind, int mode, const double* dinv, const do
 
 int launch_jac_d(const Ctx& cx, int kind, const double* dinv, cudaStream_t s) {
   const dim3 grid(jac_grid(cx.g), cx.g.nrhs);
-  if (kind == 2) jac_d_kernel<true><<<grid, JT, 0, s>>>(cx, dinv);
-  else jac_d_kernel<false><<<grid, JT, 0, s>>>(cx, dinv);
+  if (kind == 2) jac_d_kernel<1><<<grid, JT, 0, s>>>(cx, dinv);
+  else jac_d_kernel<0><<<grid, JT, 0, s>>>(cx, dinv);
+  return 1;
+}
+
+int launch_jac_d_ext(const Ctx& cx, const double* sbuf, cudaStream_t s) {
+  const dim3 grid(jac_grid(cx.g), cx.g.nrhs);
+  jac_d_kernel<2><<<grid, JT, 0, s>>>(cx, sbuf);
   return 1;
 }
 

@@ -53,6 +53,7 @@ struct uno_cg_handle {
   double* gtab;
   double* kel;
   double2 *twx, *twxp, *twy, *twz, *twz2;
+  double2 *twx2, *twy2;    // all-Dirichlet: length-2N1 / 2N2 tables of the odd-extension FFTs
   double* rt;             // mixed BC: z-sine-space intermediate vector [nrhs][c][n]
   LoadState* st;
   double* partials;
@@ -169,6 +170,7 @@ static void free_all(uno_cg_handle* h) {
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   for (auto e : h->tev) cudaEventDestroy(e);
   void* bufs[] = {h->r, h->d, h->p, h->u, h->spec, h->gtab, h->kel, h->twx, h->twxp, h->twy, h->twz, h->twz2, h->rt,
+                  h->twx2, h->twy2,
                   h->st, h->partials, h->counters, h->results, h->scratch, h->hist, h->loopctr, h->dinv};
   for (void* b : bufs)
     if (b) cudaFreeAsync(b, h->stream);
@@ -222,7 +224,10 @@ static uno_status setup_problem(uno_cg_handle* h) {
   h->cx = make_ctx(h);
   if (h->precond == 2 && h->dinv) launch_jacobi_dinv(h->cx, h->dinv, s);  // Eq 25 for the new problem
   // a0: symbol table + Eq 55 check
-  launch_build_symbol(h->cx, h->gtab, h->ref0, h->ref1, D.seed, D.seed ? D.amp : 0.0, s);
+  if (g.dir3)
+    launch_d3_symbol(h->cx, h->gtab, h->ref0, h->ref1, D.seed, D.seed ? D.amp : 0.0, s);
+  else
+    launch_build_symbol(h->cx, h->gtab, h->ref0, h->ref1, D.seed, D.seed ? D.amp : 0.0, s);
   int nblk = 0;
   launch_eq55(h->cx, h->gtab, h->scratch, &nblk, s);
   std::vector<double> mm(2 * nblk);
@@ -253,9 +258,11 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
   if (D.physics != UNO_THERMAL && D.physics != UNO_ELASTIC) return fail(UNO_ERR_ARG, "physics must be 0 or 1");
   // boundary conditions: all periodic, or (3D) periodic x, y with Dirichlet z (mixed)
   const bool dirz = D.dim == 3 && D.bc[0] == 0 && D.bc[1] == 0 && D.bc[2] == 1;
+  const bool dir3 = D.dim == 3 && D.bc[0] == 1 && D.bc[1] == 1 && D.bc[2] == 1;
   for (int i = 0; i < D.dim; ++i)
-    if (D.bc[i] != 0 && !dirz)
-      return fail(UNO_ERR_UNSUPPORTED, "boundary conditions: all periodic, or periodic x,y + Dirichlet z");
+    if (D.bc[i] != 0 && !dirz && !dir3)
+      return fail(UNO_ERR_UNSUPPORTED,
+                  "boundary conditions: all periodic, periodic x,y + Dirichlet z, or (3D) all Dirichlet");
   const int N1 = D.n[0], N2 = D.n[1], N3 = D.dim == 3 ? D.n[2] : 1;
   if (!is_pow2(N1) || !is_pow2(N2) || !is_pow2(N3) || N1 < 8 || N2 < 8 || N1 > 1024 || N2 > 1024 ||
       (D.dim == 3 && (N3 < 4 || N3 > 1024)))
@@ -271,6 +278,8 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
   }
   if (dirz && ((c == 1 && N1 < 32) || N1 < 16 || N3 < 8 || N3 > 512))
     return fail(UNO_ERR_SHAPE, "mixed BC needs N1 >= 32 (thermal) / 16 (elastic), 8 <= N3 <= 512");
+  if (dir3 && ((c == 1 && (N1 < 32 || N2 < 16)) || N1 < 16 || N2 < 16 || N3 < 8 || N1 > 512 || N2 > 512 || N3 > 512))
+    return fail(UNO_ERR_SHAPE, "all-Dirichlet needs N1 >= 32 (thermal) / 16 (elastic), N2 >= 16, N3 >= 8, all <= 512");
   if (D.seed != 0 && !(D.amp >= 0 && D.amp < 1)) return fail(UNO_ERR_ARG, "amp must be in [0, 1)");
 
   uno_cg_handle* h = new uno_cg_handle();  // value-initialised: all members zero
@@ -287,9 +296,10 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
   g.M = N1 / 2;
   g.H1 = g.M + 1;
   g.dirz = dirz ? 1 : 0;
+  g.dir3 = dir3 ? 1 : 0;
   g.P3 = dirz ? N3 - 1 : N3;
   g.n = (long long)N1 * N2 * g.P3;
-  g.nspec = (long long)g.H1 * N2 * g.P3;
+  g.nspec = dir3 ? g.n : (long long)g.H1 * N2 * g.P3;  // all-Dirichlet: real sine coefficients on the node grid
   g.h = D.h > 0 ? D.h : 1.0 / N1;
   g.C = c * (c + 1) / 2;
   g.NA = g.NB = 0;
@@ -300,7 +310,7 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
     Geo t3 = g;
     t3.NB = N2 >= 128 ? 16 : 8;
     t3.NA = N2 / t3.NB;
-    if (want3 && !dirz && schedule3_supported(t3)) {
+    if (want3 && !dirz && !dir3 && schedule3_supported(t3)) {
       g.NB = t3.NB;
       g.NA = t3.NA;
     }
@@ -310,7 +320,7 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
   {  // L2-pipelined 5-pass schedule (z-chunks), UNO_ZPIPE=<planes per chunk>
     const char* ev = getenv("UNO_ZPIPE");
     const int Z = ev ? atoi(ev) : 0;
-    if (Z > 0 && g.dim == 3 && c == 1 && !dirz && g.NB == 0 && N1 >= 32 && Z % 8 == 0 && N3 % Z == 0 && N3 / Z >= 2) {
+    if (Z > 0 && g.dim == 3 && c == 1 && !dirz && !dir3 && g.NB == 0 && N1 >= 32 && Z % 8 == 0 && N3 % Z == 0 && N3 / Z >= 2) {
       g.ZP = Z;
       g.KZC = Z;
     }
@@ -340,7 +350,8 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
       (e = al((void**)&h->gtab, (size_t)g.C * g.nspec * 8)) || (e = al((void**)&h->kel, 2 * 576 * 8)) ||
       (e = al((void**)&h->twx, g.M * 16)) || (e = al((void**)&h->twxp, (g.M + 1) * 16)) ||
       (e = al((void**)&h->twy, N2 * 16)) || (e = al((void**)&h->twz, N3 * 16)) ||
-      (e = al((void**)&h->twz2, 2 * N3 * 16)) || (e = al((void**)&h->rt, dirz ? vec * 8 : 8)) ||
+      (e = al((void**)&h->twz2, 2 * N3 * 16)) || (e = al((void**)&h->rt, (dirz || dir3) ? vec * 8 : 8)) ||
+      (e = al((void**)&h->twx2, dir3 ? 2 * N1 * 16 : 16)) || (e = al((void**)&h->twy2, dir3 ? 2 * N2 * 16 : 16)) ||
       (e = al((void**)&h->st, kMaxRhs * sizeof(LoadState))) ||
       (e = al((void**)&h->partials, (size_t)RED_NSLOT * kMaxRhs * maxb * 8)) ||
       (e = al((void**)&h->counters, RED_NSLOT * kMaxRhs * sizeof(unsigned))) ||
@@ -382,6 +393,14 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
   twiddles(2 * N3, 2 * N3, t);
   cudaMemcpyAsync(h->twz2, t.data(), 2 * N3 * 16, cudaMemcpyHostToDevice, s);
   cudaStreamSynchronize(s);
+  if (dir3) {
+    twiddles(2 * N1, 2 * N1, t);
+    cudaMemcpyAsync(h->twx2, t.data(), 2 * N1 * 16, cudaMemcpyHostToDevice, s);
+    cudaStreamSynchronize(s);
+    twiddles(2 * N2, 2 * N2, t);
+    cudaMemcpyAsync(h->twy2, t.data(), 2 * N2 * 16, cudaMemcpyHostToDevice, s);
+    cudaStreamSynchronize(s);
+  }
   const uno_status st0 = setup_problem(h);
   if (st0 != UNO_OK) {
     free_all(h);
@@ -406,7 +425,7 @@ extern "C" uno_status uno_cg_update(uno_cg_handle* h, const uno_cg_desc* desc, c
       (D.dim == 3 && D.n[2] != O.n[2]) || D.h != O.h)
     return fail(UNO_ERR_ARG, "update: grid, physics, h and nrhs must match the handle");
   for (int i = 0; i < D.dim; ++i)
-    if (D.bc[i] != 0) return fail(UNO_ERR_UNSUPPORTED, "only periodic boundaries are built in this version");
+    if (D.bc[i] != O.bc[i]) return fail(UNO_ERR_ARG, "update: boundary conditions must match the handle");
   if (D.physics == UNO_THERMAL) {
     if (!(D.mat[0][0] > 0) || !(D.mat[1][0] > 0)) return fail(UNO_ERR_ARG, "conductivities must be > 0");
   } else {
@@ -473,6 +492,11 @@ extern "C" uno_status uno_cg_apply_precond(uno_cg_handle* h, const double* d_r, 
   if (h->precond != 0) {  // z = P r (identity / Jacobi) and r.z
     KL(launch_jac_r(h->cx, h->precond, STANDALONE, h->dinv, d_r, d_z, s), KC_XF);
     KL(launch_scalar_n(h->cx, RED_GAMMA, STANDALONE, jacobi_nblk(h->g), s), KC_OTHER);
+  } else if (h->g.dir3) {  // all-Dirichlet: DST-I on every axis (dirichlet.cu)
+    const double2* tw2[3] = {h->twx2, h->twy2, h->twz2};
+    KL(launch_d3_precond(h->cx, d_r, d_z, tw2, s), KC_G);
+    KL(launch_d3_dot(h->cx, d_r, d_z, STANDALONE, s), KC_OTHER);
+    KL(launch_scalar_n(h->cx, RED_GAMMA, STANDALONE, jacobi_nblk(h->g), s), KC_OTHER);
   } else if (h->g.dirz) {  // mixed BC: DST-I along z first, then the periodic x/y machinery
     KL(launch_dstz(h->cx, STANDALONE, false, d_r, h->rt, s), KC_XF);
     KL(launch_xfwd(h->cx, STANDALONE, h->rt, s), KC_XF);
@@ -523,6 +547,15 @@ static int enqueue_iteration(uno_cg_handle* h, cudaStream_t s, cudaEvent_t* ev /
     n += launch_scalar_n(cx, RED_RNORM, CG, nb, s);
     n += launch_scalar_n(cx, RED_GAMMA, CG, nb, s);
     if (!run(4, [&] { return launch_jac_d(cx, h->precond, h->dinv, s); })) return -1;
+  } else if (h->g.dir3) {  // all-Dirichlet: r pass | s = P r (7 passes) | r.s | d pass
+    const int nb = jacobi_nblk(h->g);
+    const double2* tw2[3] = {h->twx2, h->twy2, h->twz2};
+    if (!run(0, [&] { return launch_jac_r(cx, 1, CG, nullptr, nullptr, nullptr, s); })) return -1;
+    n += launch_scalar_n(cx, RED_RNORM, CG, nb, s);
+    if (!run(2, [&] { return launch_d3_precond(cx, cx.r, h->rt, tw2, s); })) return -1;
+    n += launch_d3_dot(cx, cx.r, h->rt, CG, s);
+    n += launch_scalar_n(cx, RED_GAMMA, CG, nb, s);
+    if (!run(4, [&] { return launch_jac_d_ext(cx, h->rt, s); })) return -1;
   } else if (h->g.dirz) {  // mixed BC (dst.cu): DST_z (+CG r update) | x | y.G.y^-1 | x^-1 | DST_z^-1 (+d, u)
     if (!run(0, [&] { return launch_dstz(cx, CG, false, cx.r, h->rt, s); })) return -1;
     n += launch_scalar(cx, RED_RNORM, CG, s);
@@ -713,7 +746,7 @@ extern "C" uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, doub
   CK(cudaMemcpyAsync(h->st, h->h_st, g.nrhs * sizeof(LoadState), cudaMemcpyHostToDevice, s));
   const long long work = (long long)g.nrhs * g.c * g.n;
   // passes + 3 scalar kernels (mixed: 6 too); pipelined: 2C + 1 + 3C over C z-chunks
-  const int per_iter = h->precond != 0 ? 6 : (g.ZP > 0 ? 5 * (g.N3 / g.ZP) + 4 : ((g.dim == 3 && g.NB == 0) ? 6 : 4) + 3);
+  const int per_iter = h->precond != 0 ? 6 : g.dir3 ? 15 : (g.ZP > 0 ? 5 * (g.N3 / g.ZP) + 4 : ((g.dim == 3 && g.NB == 0) ? 6 : 4) + 3);
   if (!h->timing) {
     // whole solve device-side: WHILE node over bodies of `chunk` iterations
     const int chunk = work >= (1LL << 22) ? 2 : 4;
@@ -763,7 +796,7 @@ extern "C" uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, doub
     }
   }
   KL(launch_finalize(h->cx, s), KC_OTHER);
-  if (g.dirz)  // Dirichlet z: no null space, the fluctuation is not mean-free
+  if (g.dirz || g.dir3)  // Dirichlet faces: no null space, the fluctuation is not mean-free
     CK(cudaMemcpyAsync(d_u, h->u, (size_t)g.nrhs * g.c * g.n * 8, cudaMemcpyDeviceToDevice, s));
   else
     KL(launch_mean_removal(h->cx, h->u, d_u, h->scratch, s), KC_OTHER);

@@ -396,3 +396,69 @@ def test_preconditioner_effectiveness_order():
         s = UnoCG(torch.from_numpy(P.phase).to(dev()), "thermal", P.mat, nrhs=1, seed=P.seed, amp=P.amp, precond=kind)
         its[kind] = s.solve(P.loads[:1], max_iter=20000).reports[0]["iterations"]
     assert its["uno"] * 5 < its["jacobi"] < its["identity"], its
+
+
+# ------------------------------------------------------------------ all-Dirichlet (bc = 1,1,1)
+D3_SHAPES = [((32, 16, 8), "thermal"), ((32, 32, 16), "thermal"), ((16, 16, 8), "elastic")]
+
+
+def _pad(u):  # oracle interior-node field (c, N3-1, N2-1, N1-1) -> library padded (c, N3, N2, N1)
+    c = u.shape[0]
+    out = np.zeros((c,) + tuple(s + 1 for s in u.shape[1:]))
+    out[:, 1:, 1:, 1:] = u
+    return out
+
+
+@pytest.mark.parametrize("N,physics", D3_SHAPES)
+def test_all_dirichlet_operators(N, physics):
+    from paper_2508_02681_b200.api import UnoCG
+
+    g0, ph, mat, amp, seed = make_case(N, physics)
+    g = fem.Grid(N, bc=(1, 1, 1), c=g0.c, h=1.0 / N[0])
+    s = UnoCG(torch.from_numpy(ph).to(dev()), physics, mat, nrhs=1, seed=seed, amp=amp, bc=(1, 1, 1))
+    u = synth.test_vector(41, g.field_shape())
+    Ku = s.apply_K(torch.from_numpy(_pad(u)[None]).to(dev())).cpu().numpy()[0]
+    ref = fem.apply_K(g, physics, ph, mat, u)
+    assert rel(Ku, _pad(ref)) <= 1e-13
+    load = loads_for(physics, 3, 1)
+    f = s.rhs(load).cpu().numpy()[0]
+    fr = fem.rhs(g, physics, ph, mat, load[0])
+    assert np.max(np.abs(f - _pad(fr))) <= 1e-14 * max(np.abs(fr).max(), 1e-300)
+    G = greens.ghat_dirichlet(g, physics, mat, seed, amp)
+    z, rz = s.apply_precond(torch.from_numpy(_pad(u)[None]).to(dev()), want_dot=True)
+    zr = greens.apply_precond_dirichlet(G, u)
+    assert rel(z.cpu().numpy()[0], _pad(zr)) <= 1e-12
+    assert abs(rz[0] - np.sum(u * zr)) <= 1e-12 * abs(np.sum(u * zr))
+
+
+@pytest.mark.parametrize("N,physics", D3_SHAPES)
+def test_all_dirichlet_solve(N, physics):
+    from paper_2508_02681_b200.api import UnoCG
+
+    g0, ph, mat, amp, seed = make_case(N, physics)
+    g = fem.Grid(N, bc=(1, 1, 1), c=g0.c, h=1.0 / N[0])
+    load = loads_for(physics, 3, 1)
+    ref = homog.solve_problem(g, physics, ph, mat, load, seed, amp, tol=1e-8)
+    s = UnoCG(torch.from_numpy(ph).to(dev()), physics, mat, nrhs=1, seed=seed, amp=amp, bc=(1, 1, 1))
+    res = s.solve(load)
+    assert abs(res.reports[0]["iterations"] - ref["iterations"][0]) <= 1 and res.reports[0]["converged"]
+    m = ref["iterations"][0]
+    fx = homog.solve_problem(g, physics, ph, mat, load, seed, amp, fixed_iters=m)
+    u = s.solve(load, fixed_iters=m).u.cpu().numpy()[0]
+    assert rel(u, _pad(fx["U"][0])) <= 1e-9
+
+
+def test_all_dirichlet_thermal_exact_inverse():
+    # homogeneous medium, seed 0: the sine basis diagonalises K exactly -> one PCG iteration
+    from paper_2508_02681_b200.api import UnoCG
+
+    N = (64, 32, 16)
+    ph = np.zeros(tuple(reversed(N)), np.uint8)
+    ph[3:9, 5:20, 10:40] = 1  # any RHS source; the operator of a homogeneous medium is what matters
+    s = UnoCG(torch.from_numpy(np.zeros_like(ph)).to(dev()), "thermal", (2.0, 2.0), nrhs=1, seed=0, amp=0.0,
+              bc=(1, 1, 1))
+    g = fem.Grid(N, bc=(1, 1, 1), h=1 / 64)
+    u = synth.test_vector(43, g.field_shape())
+    Ku = s.apply_K(torch.from_numpy(_pad(u)[None]).to(dev()))
+    z = s.apply_precond(Ku).cpu().numpy()[0]
+    assert rel(z, _pad(u)) <= 1e-12
