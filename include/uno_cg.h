@@ -166,6 +166,29 @@ UNO_API uno_status uno_cg_effective_property(uno_cg_handle* h, const double* d_u
 enum { UNO_PRECOND_UNO = 0, UNO_PRECOND_IDENTITY = 1, UNO_PRECOND_JACOBI = 2 };
 UNO_API uno_status uno_cg_set_preconditioner(uno_cg_handle* h, int32_t kind);
 
+/* Second-order UNO preconditioner training (§4.4 Alg 4, Eq 59-72, App. B; 3D
+ * periodic grids, c = 1 or 3).  Training pairs (Eq 58, 60): r = f, s = A^-1 f (e.g. from
+ * uno_cg_rhs / uno_cg_solve on the training microstructures).
+ *   uno_cg_train_features: transforms the nrhs pairs once with the library's forward passes and
+ *     accumulates d_feat += scale * (alpha_1..alpha_C, beta_1..beta_C) per half-spectrum bin
+ *     (Eq 67 / B.2 with the unitary T).  d_r, d_s: device [nrhs][c][N3][N2][N1];
+ *     d_feat: device [2C][H1][N3][N2] (C = c(c+1)/2), caller-zeroed, layout [kx][kz][ky].
+ *   uno_cg_train_pairs: the mode set K = {|k_i| <= M} as conjugate pairs {k, -k}, ordered by
+ *     min(flat(k), flat(-k)) with flat = (kz N2 + ky) N1 + kx; h_bins [npair][2] receives the
+ *     half-spectrum bins of each pair (-1: none).
+ *   uno_cg_train_newton: `epochs` Newton-Raphson steps (Alg 4 l.3-7; step halved while the
+ *     loss increases) on theta_0 (bypass, Eq 43; host [C] in/out) and theta_p (device [npair][C]
+ *     in/out), v(k) = psi(theta_0) + [k in K] psi(theta_p(k)) with psi of Eq 45 (c=1: t^2) / B5.
+ *     h_loss [epochs+1] (or NULL) receives the loss without the constant delta.
+ *   uno_cg_train_install: uses the trained symbol (G(0) = 0) as this handle's preconditioner
+ *     and runs the Eq 55 check (UNO_ERR_NOT_SPD if it fails).                               */
+UNO_API uno_status uno_cg_train_features(uno_cg_handle* h, const double* d_r, const double* d_s, double scale,
+                                         double* d_feat);
+UNO_API uno_status uno_cg_train_pairs(uno_cg_handle* h, int32_t M, int64_t* npair, int32_t* h_bins);
+UNO_API uno_status uno_cg_train_newton(uno_cg_handle* h, const double* d_feat, int32_t M, int32_t epochs,
+                                       double* h_theta0, double* d_thetas, double* h_loss);
+UNO_API uno_status uno_cg_train_install(uno_cg_handle* h, int32_t M, const double* h_theta0, const double* d_thetas);
+
 /* Timing of the most recent uno_cg_solve (CUDA events on desc.stream, ms), and the number
  * of library kernels it launched.                                                       */
 UNO_API uno_status uno_cg_last_solve_stats(uno_cg_handle* h, double* ms, int64_t* kernel_launches);

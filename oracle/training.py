@@ -164,8 +164,9 @@ def symbol(theta0: np.ndarray, thetas: np.ndarray, ids: np.ndarray, c: int) -> n
 def newton(A, B, delta, M: int, theta0, thetas, epochs: int = 10, ids=None, npair=None, max_halvings: int = 30):
     """Alg 4: Newton-Raphson on (theta_0, theta_p).  Returns theta0, thetas, loss history.
     Reading (R15): the loss is quartic in theta, so far from the optimum a full Newton
-    step can increase it; the step is then halved until the loss decreases (backtracking), which
-    leaves the quadratically convergent full steps near the optimum untouched."""
+    step can increase it; the step is then halved until the loss does not increase (backtracking;
+    after max_halvings without decrease theta is kept), which leaves the quadratically convergent
+    full steps near the optimum untouched."""
     c = A.shape[0]
     C = len(PAIRS[c])
     shape = A.shape[2:]
@@ -209,9 +210,9 @@ def newton(A, B, delta, M: int, theta0, thetas, epochs: int = 10, ids=None, npai
         for _ in range(max_halvings):
             cand0, cands = theta0 - t * d0, thetas - t * dp
             if loss_features(symbol(cand0, cands, ids, c), A, B, delta) <= hist[-1]:
+                theta0, thetas = cand0, cands
                 break
-            t *= 0.5
-        theta0, thetas = cand0, cands
+            t *= 0.5  # no decrease after max_halvings: stationary to round-off, keep theta
     v = symbol(theta0, thetas, ids, c)
     hist.append(loss_features(v, A, B, delta))
     return theta0, thetas, hist

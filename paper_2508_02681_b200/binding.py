@@ -21,7 +21,8 @@ UNO_OK, UNO_ERR_ARG, UNO_ERR_SHAPE, UNO_ERR_CUDA, UNO_ERR_UNSUPPORTED, UNO_ERR_N
 UNO_THERMAL, UNO_ELASTIC = 0, 1
 
 EXPORTS = ("uno_cg_create", "uno_cg_destroy", "uno_cg_update", "uno_cg_rhs", "uno_cg_apply_K", "uno_cg_apply_precond",
-           "uno_cg_solve", "uno_cg_effective_property", "uno_cg_set_preconditioner", "uno_cg_last_solve_stats",
+           "uno_cg_solve", "uno_cg_effective_property", "uno_cg_set_preconditioner", "uno_cg_train_features",
+           "uno_cg_train_pairs", "uno_cg_train_newton", "uno_cg_train_install", "uno_cg_last_solve_stats",
            "uno_cg_kernel_timing", "uno_cg_last_error", "uno_cg_version")
 UNO_PRECOND = {"uno": 0, "identity": 1, "jacobi": 2}
 # include/uno_cg_slab.h (z-slab decomposition)
@@ -62,6 +63,10 @@ def _load():
     lib.uno_cg_effective_property.argtypes = [P, P, P, P]
     lib.uno_cg_last_solve_stats.argtypes = [P, C.POINTER(D), C.POINTER(I64)]
     lib.uno_cg_set_preconditioner.argtypes = [P, I32]
+    lib.uno_cg_train_features.argtypes = [P, P, P, D, P]
+    lib.uno_cg_train_pairs.argtypes = [P, I32, P, P]
+    lib.uno_cg_train_newton.argtypes = [P, P, I32, I32, P, P, P]
+    lib.uno_cg_train_install.argtypes = [P, I32, P, P]
     lib.uno_cg_kernel_timing.argtypes = [P, I32, I32, P, P]
     lib.uno_slab_create.argtypes = [C.POINTER(UnoCgDesc), I32, I32, P, C.POINTER(P)]
     lib.uno_slab_destroy.argtypes = [P]
@@ -158,6 +163,31 @@ def uno_cg_solve(h: int, loads, rel_tol: float, max_iter: int, fixed_iters: int,
 
 def uno_cg_set_preconditioner(h: int, kind: str):
     _check(_lib.uno_cg_set_preconditioner(h, UNO_PRECOND[kind]), "uno_cg_set_preconditioner")
+
+
+def uno_cg_train_features(h: int, d_r, d_s, scale: float, d_feat):
+    _check(_lib.uno_cg_train_features(h, _ptr(d_r), _ptr(d_s), float(scale), _ptr(d_feat)), "uno_cg_train_features")
+
+
+def uno_cg_train_pairs(h: int, M: int):
+    n = np.zeros(1, dtype=np.int64)
+    _check(_lib.uno_cg_train_pairs(h, int(M), _ptr(n), None), "uno_cg_train_pairs")
+    bins = np.zeros((int(n[0]), 2), dtype=np.int32)
+    _check(_lib.uno_cg_train_pairs(h, int(M), _ptr(n), _ptr(bins)), "uno_cg_train_pairs")
+    return bins
+
+
+def uno_cg_train_newton(h: int, d_feat, M: int, epochs: int, theta0, d_thetas):
+    t0 = _host_f64(theta0).copy()
+    loss = np.zeros(epochs + 1)
+    _check(_lib.uno_cg_train_newton(h, _ptr(d_feat), int(M), int(epochs), _ptr(t0), _ptr(d_thetas), _ptr(loss)),
+           "uno_cg_train_newton")
+    return t0, loss
+
+
+def uno_cg_train_install(h: int, M: int, theta0, d_thetas):
+    t0 = _host_f64(theta0)
+    _check(_lib.uno_cg_train_install(h, int(M), _ptr(t0), _ptr(d_thetas)), "uno_cg_train_install")
 
 
 def uno_cg_effective_property(h: int, d_u, loads, nrhs: int) -> np.ndarray:

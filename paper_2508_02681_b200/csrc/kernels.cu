@@ -478,7 +478,7 @@ __global__ void __launch_bounds__(fft_threads(L), L == 256 ? UNO_GMINB : 1) gpas
       if (e < 8 * L) cp_async16(&tiles[q][tidx(e >> 3, e & 7)], base + (long long)(e >> 3) * g.N2 + (e & 7));
     }
   }
-  constexpr bool STG = gstaged<L, NC>();
+  constexpr bool STG = gstaged<L, NC>() && MODE != FWDZ;
   if (STG) {
 #pragma unroll
     for (int q = 0; q < NCC; ++q) {
@@ -493,6 +493,20 @@ __global__ void __launch_bounds__(fft_threads(L), L == 256 ? UNO_GMINB : 1) gpas
   for (int i = t; i < L; i += T) tw[i] = cx.tw.z[i];
   cp_wait<0>();
   __syncthreads();
+  if constexpr (MODE == FWDZ) {  // forward z transform only (training features, train.cu)
+#pragma unroll
+    for (int q = 0; q < NC; ++q) fft_tile<L, false>(tiles[q], tw);
+#pragma unroll
+    for (int q = 0; q < NC; ++q) {
+      double2* base = cx.spec + ((long long)load * g.c + q) * g.nspec + boff;
+#pragma unroll
+      for (int i = 0; i < (8 * L + T - 1) / T; ++i) {
+        const int e = t + i * T;
+        if (e < 8 * L) base[(long long)(e >> 3) * g.N2 + (e & 7)] = tiles[q][tidx(e >> 3, e & 7)];
+      }
+    }
+    return;
+  }
   const double w = parseval_w(kx, g.M);
   double part = 0.0;
   if constexpr (gconv_fusable(L) && NC * plan_radix(L, plan_stages(L) - 1) <= 32) {
@@ -2354,6 +2368,24 @@ int launch_gpass(const Ctx& cx, int mode, cudaStream_t s) {
     const char* e = getenv("UNO_GRD");
     return !(e && e[0] == '0');
   }();
+  if (mode == FWDZ) {  // forward z FFT of the half spectrum (3D periodic; training features)
+    if (g.dim != 3 || g.dirz || g.dir3) return -1;
+    return dispatch_pow2(g.N3, [&](auto Lc) {
+      constexpr int L = decltype(Lc)::value;
+      const dim3 grid((unsigned)(g.H1 * (g.N2 / 8)), g.nrhs);
+      auto go = [&](auto k, int sm) {
+        set_smem(k, sm);
+        k<<<grid, fft_threads(L), sm, s>>>(cx);
+        return 1;
+      };
+      if (g.c == 1) return go(gpass_z_kernel<L, 1, FWDZ>, gsmem_tile_bytes<L, 1>());
+      if constexpr (gsmem_tile_bytes<L, 3>() <= 220 * 1024) {
+        return go(gpass_z_kernel<L, 3, FWDZ>, gsmem_tile_bytes<L, 3>());
+      } else {
+        return -1;
+      }
+    });
+  }
   if (rd && g.dim == 3 && !g.dirz && g.c == 1 && g.N3 == 256) {
     const dim3 grid((unsigned)(g.H1 * (g.N2 / 8)), g.nrhs);
     constexpr int sm = (8 * GR_CS + 256) * 16 + 256 * 8 * 8;

@@ -1,5 +1,8 @@
 // kernels.cuh — host-visible launch interface of the libunocg kernels.
 #pragma once
+#include <string>
+#include <vector>
+
 #include "common.cuh"
 
 namespace uno {
@@ -36,7 +39,8 @@ struct LoadParams {         // macroscopic loads for the RHS / effective-propert
   double v[kMaxRhs][6];
 };
 
-enum Mode { STANDALONE = 0, CG = 1, PLAIN = 2 };  // PLAIN: skips inactive loads, no CG fusions
+enum Mode { STANDALONE = 0, CG = 1, PLAIN = 2, FWDZ = 3 };  // PLAIN: skips inactive loads, no CG fusions;
+                                                           // FWDZ: forward z FFT only (G pass, training)
 
 // pass launchers; return number of kernels launched (or -1 on unsupported size)
 // b0/nb: launch only blocks [b0, b0+nb) of 8 x-rows (nb = 0: all) — z-chunks of the pipelined schedule
@@ -84,6 +88,14 @@ int launch_d3_dot(const Ctx& cx, const double* a, const double* b, int mode, cud
 int launch_d3_symbol(const Ctx& cx, double* gtab, double ref0, double ref1, unsigned long long seed, double amp,
                      cudaStream_t s);
 int launch_jac_d_ext(const Ctx& cx, const double* sbuf, cudaStream_t s);  // d = s + beta d from a buffer
+
+// second-order UNO training (train.cu, Alg 4)
+int launch_train_feat(const Ctx& cx, const double2* sr, const double2* ss, double scale, double* feat, cudaStream_t s);
+void train_build_pairs(const Geo& g, int M, std::vector<int>& pbin, std::vector<int>& binpair);
+int train_newton_run(const Ctx& cx, const double* feat, const std::vector<int>& pbin, const std::vector<int>& binpair,
+                     int epochs, double* th0_host, double* d_ths, double* loss_hist, cudaStream_t s, std::string& err);
+int train_install_run(const Ctx& cx, const std::vector<int>& pbin, const std::vector<int>& binpair,
+                      const double* th0_host, const double* d_ths, double* gtab, cudaStream_t s);
 
 // mixed BC (Dirichlet on z), dst.cu
 int launch_dstz(const Ctx& cx, int mode, bool inverse, const double* src, double* dst, cudaStream_t s);

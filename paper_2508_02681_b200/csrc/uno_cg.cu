@@ -88,6 +88,7 @@ struct uno_cg_handle {
   // preconditioner kind (0 UNO, 1 identity, 2 Jacobi) and the Jacobi inverse diagonal [n]
   int precond;
   double* dinv;
+  double2* tspec;  // training: spectrum of r while s is transformed (train.cu)
 };
 
 // ------------------------------------------------------------------------------ helpers
@@ -170,7 +171,7 @@ static void free_all(uno_cg_handle* h) {
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   for (auto e : h->tev) cudaEventDestroy(e);
   void* bufs[] = {h->r, h->d, h->p, h->u, h->spec, h->gtab, h->kel, h->twx, h->twxp, h->twy, h->twz, h->twz2, h->rt,
-                  h->twx2, h->twy2,
+                  h->twx2, h->twy2, h->tspec,
                   h->st, h->partials, h->counters, h->results, h->scratch, h->hist, h->loopctr, h->dinv};
   for (void* b : bufs)
     if (b) cudaFreeAsync(b, h->stream);
@@ -451,6 +452,87 @@ extern "C" uno_status uno_cg_set_preconditioner(uno_cg_handle* h, int32_t kind) 
     h->gexec = nullptr;
   }
   CK(cudaGetLastError());
+  return UNO_OK;
+}
+
+// ------------------------------------------------------------------------------ training (Alg 4)
+static uno_status train_check(const uno_cg_handle* h) {
+  const Geo& g = h->g;
+  if (g.dim != 3 || g.dirz || g.dir3 || g.NB != 0 || g.ZP != 0)
+    return fail(UNO_ERR_UNSUPPORTED, "training: 3D periodic grids with the 5-pass transforms");
+  return UNO_OK;
+}
+
+extern "C" uno_status uno_cg_train_features(uno_cg_handle* h, const double* d_r, const double* d_s, double scale,
+                                            double* d_feat) {
+  if (!h || !d_r || !d_s || !d_feat) return fail(UNO_ERR_ARG, "null argument");
+  uno_status st = train_check(h);
+  if (st != UNO_OK) return st;
+  const Geo& g = h->g;
+  cudaStream_t s = h->stream;
+  long long launches = 0;
+  if (!h->tspec) CK(cudaMallocAsync((void**)&h->tspec, (size_t)g.nrhs * g.c * g.nspec * 16, s));
+  auto fwd = [&](const double* x) -> uno_status {  // r_hat = T x (unnormalised: x, y, z passes)
+    KL(launch_xfwd(h->cx, STANDALONE, x, s), KC_XF);
+    KL(launch_ypass(h->cx, STANDALONE, false, s), KC_Y);
+    KL(launch_gpass(h->cx, FWDZ, s), KC_G);
+    return UNO_OK;
+  };
+  if ((st = fwd(d_r)) != UNO_OK) return st;
+  CK(cudaMemcpyAsync(h->tspec, h->spec, (size_t)g.nrhs * g.c * g.nspec * 16, cudaMemcpyDeviceToDevice, s));
+  if ((st = fwd(d_s)) != UNO_OK) return st;
+  // unitary T = FFT / sqrt(n): products of two transforms carry 1/n
+  KL(launch_train_feat(h->cx, h->tspec, h->spec, scale / (double)g.n, d_feat, s), KC_OTHER);
+  CK(cudaGetLastError());
+  return UNO_OK;
+}
+
+extern "C" uno_status uno_cg_train_pairs(uno_cg_handle* h, int32_t M, int64_t* npair, int32_t* h_bins) {
+  if (!h || !npair) return fail(UNO_ERR_ARG, "null argument");
+  uno_status st = train_check(h);
+  if (st != UNO_OK) return st;
+  if (M < 0) return fail(UNO_ERR_ARG, "M >= 0");
+  std::vector<int> pbin, binpair;
+  train_build_pairs(h->g, M, pbin, binpair);
+  *npair = (int64_t)(pbin.size() / 2);
+  if (h_bins) std::memcpy(h_bins, pbin.data(), pbin.size() * 4);
+  return UNO_OK;
+}
+
+extern "C" uno_status uno_cg_train_newton(uno_cg_handle* h, const double* d_feat, int32_t M, int32_t epochs,
+                                          double* h_theta0, double* d_thetas, double* h_loss) {
+  if (!h || !d_feat || !h_theta0 || epochs < 0) return fail(UNO_ERR_ARG, "null argument / epochs");
+  uno_status st = train_check(h);
+  if (st != UNO_OK) return st;
+  std::vector<int> pbin, binpair;
+  train_build_pairs(h->g, M, pbin, binpair);
+  if (!d_thetas && !pbin.empty()) return fail(UNO_ERR_ARG, "d_thetas required when K is not empty");
+  std::string err;
+  if (train_newton_run(h->cx, d_feat, pbin, binpair, epochs, h_theta0, d_thetas, h_loss, h->stream, err) < 0)
+    return fail(UNO_ERR_CUDA, "training: " + err);
+  return UNO_OK;
+}
+
+extern "C" uno_status uno_cg_train_install(uno_cg_handle* h, int32_t M, const double* h_theta0, const double* d_thetas) {
+  if (!h || !h_theta0) return fail(UNO_ERR_ARG, "null argument");
+  uno_status st = train_check(h);
+  if (st != UNO_OK) return st;
+  std::vector<int> pbin, binpair;
+  train_build_pairs(h->g, M, pbin, binpair);
+  if (train_install_run(h->cx, pbin, binpair, h_theta0, d_thetas, h->gtab, h->stream) < 0)
+    return fail(UNO_ERR_CUDA, "training install");
+  if (h->gexec) {
+    cudaGraphExecDestroy(h->gexec);
+    h->gexec = nullptr;
+  }
+  int nblk = 0;  // Eq 55 on the learned symbol; psi makes it SPD by construction
+  launch_eq55(h->cx, h->gtab, h->scratch, &nblk, h->stream);
+  std::vector<double> mm(2 * nblk);
+  CK(cudaMemcpyAsync(mm.data(), h->scratch, 2 * nblk * 8, cudaMemcpyDeviceToHost, h->stream));
+  CK(cudaStreamSynchronize(h->stream));
+  double lo = 1e300;
+  for (int i = 0; i < nblk; ++i) lo = std::min(lo, mm[i]);
+  if (!(lo > 1e-14)) return fail(UNO_ERR_NOT_SPD, "Eq 55 safety check failed on the trained symbol");
   return UNO_OK;
 }
 
