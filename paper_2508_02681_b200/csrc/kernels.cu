@@ -1114,7 +1114,9 @@ struct KRNState {
   double ym, yp;
 };
 
-template <int NR>
+// HALO: slab mode (neighbour planes from Ctx::hlo/hhi); D3: all-Dirichlet output mask.  Both are
+// template flags so the common periodic instance carries none of their per-plane logic.
+template <int NR, bool HALO, bool D3>
 __global__ void __launch_bounds__(128, 2) kp_thermal3d_rn_kernel(Ctx cx, int mode, const double* __restrict__ src,
                                                                 double* __restrict__ dst, int ZC, int zc0, int nzl) {
   constexpr int LA = 4;
@@ -1171,7 +1173,7 @@ __global__ void __launch_bounds__(128, 2) kp_thermal3d_rn_kernel(Ctx cx, int mod
         asm volatile("st.shared.v2.f64 [%0], {0d0000000000000000, 0d0000000000000000};\n" ::"r"(sD[m] + so) : "memory");
     } else {
       const double* base;
-      if (g.halo)  // slab: neighbours' boundary planes arrive in separate halo buffers
+      if (HALO)  // slab: neighbours' boundary planes arrive in separate halo buffers
         base = p < g.zlo ? cx.hlo + (long long)load * plane
                          : (p >= g.zlo + g.P3 ? cx.hhi + (long long)load * plane : dv + (long long)(p - g.zlo) * plane);
       else
@@ -1256,6 +1258,12 @@ __global__ void __launch_bounds__(128, 2) kp_thermal3d_rn_kernel(Ctx cx, int mod
   double part = 0.0;
   const double hc = g.h * (1.0 / 12.0);
   double* outp = dst + (long long)load * g.n + (long long)(y0 + NR * ty) * N1 + (x0 + tx);
+  // Dirichlet-node mask bits of this thread's NR nodes (all-Dirichlet storage), loop invariant
+  unsigned fixed_xy = 0;
+  if (D3)
+#pragma unroll
+    for (int m = 0; m < NR; ++m)
+      if (x0 + tx == 0 || y0 + NR * ty + m == 0) fixed_xy |= 1u << m;
   auto step = [&](int k, const KRNState<NR>& I, KRNState<NR>& O) {
     if (k + LA <= ze) issue_plane(k + LA);
     cp_commit();
@@ -1268,6 +1276,7 @@ __global__ void __launch_bounds__(128, 2) kp_thermal3d_rn_kernel(Ctx cx, int mod
     double KS[NR + 1];
 #pragma unroll
     for (int e = 0; e < NR + 1; ++e) KS[e] = fma(a[e][0], I.Qk[e][0] + O.Qk[e][0], a[e][1] * (I.Qk[e][1] + O.Qk[e][1]));
+    double* orow = outp + (long long)(k - dz - g.zlo) * plane;
 #pragma unroll
     for (int m = 0; m < NR; ++m) {
       const double KShi = KS[m] + KS[m + 1];
@@ -1285,8 +1294,8 @@ __global__ void __launch_bounds__(128, 2) kp_thermal3d_rn_kernel(Ctx cx, int mod
       EE = fma(Khi, dzp, EE);
       EE = fma(I.Klo[m], I.dzm[m], EE);
       double pv = hc * (fma(5.0 * di, Ksum, EE) - (I.KSlo[m] + KShi));
-      if (g.dir3 && (x0 + tx == 0 || y0 + NR * ty + m == 0 || k == 0)) pv = 0.0;  // Dirichlet nodes
-      outp[(long long)(k - dz - g.zlo) * plane + m * N1] = pv;
+      if (D3 && (((fixed_xy >> m) & 1u) || k == 0)) pv = 0.0;  // Dirichlet nodes
+      orow[m * N1] = pv;
       part = fma(di, pv, part);
       O.KSlo[m] = KShi;
       O.Klo[m] = Khi;
@@ -2474,8 +2483,10 @@ int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaS
     } else if (TX == 32 && k_nr(g) == 4) {
       const dim3 grid4(g.N1 / 32, g.N2 / 16, nzl * g.nrhs);
       const int sm4 = KT_RING * (18 * KR2_DW * (int)sizeof(double) + 17 * KR2_PW);
-      set_smem(kp_thermal3d_rn_kernel<4>, sm4);
-      kp_thermal3d_rn_kernel<4><<<grid4, 128, sm4, s>>>(cx, mode, src, dst, ZC, zc0, nzl);
+      auto k4 = g.halo ? kp_thermal3d_rn_kernel<4, true, false>
+                       : (g.dir3 ? kp_thermal3d_rn_kernel<4, false, true> : kp_thermal3d_rn_kernel<4, false, false>);
+      set_smem(k4, sm4);
+      k4<<<grid4, 128, sm4, s>>>(cx, mode, src, dst, ZC, zc0, nzl);
     } else if (TX == 32) {
       const int sm2 = KT_RING * (KR2_DPL * (int)sizeof(double) + KR2_PHS);
       static const int la = [] {
