@@ -263,6 +263,16 @@ def run_ours(args):
                           f"the same {args.steps} steps (that pass ran at {kt_value / 1e9:.2f} G{UNIT})",
                 "kernels": {k: {kk: round(vv, 4) for kk, vv in v.items()} for k, v in per.items()}}
 
+    # ---- whole-iteration roofline (north star: bytes per iteration / HBM peak) ----
+    per_it = {"K": 1, "xfwd": 1, "ypass": 2, "gpass": 1, "xinv": 1}
+    b_dof_it = sum(kb[k] * c for k, c in per_it.items()) / (n ** 3 * 3)
+    iter_roof = {"bytes_per_dof_iteration": round(b_dof_it, 2),
+                 "achieved_GBps": round(value * b_dof_it / 1e9, 1),
+                 "frac_measured_peak": round(value * b_dof_it / 1e9 / peak, 4),
+                 "frac_nominal_8TBs": round(value * b_dof_it / 8e12, 4),
+                 "note": "5-pass schedule algorithmic bytes (DESIGN.md §5) x DOF-iterations/s of `value` "
+                         "(includes the per-problem setup inside the step)"}
+
     # ---- e2e: host buffers in, host results out, through the public API ----
     e2e = None
     if not args.no_e2e:
@@ -316,7 +326,8 @@ def run_ours(args):
                        "l2": "inputs larger than L2 (~1.7 GB working set per solve vs 126 MB L2)",
                        "parallelism": f"batch-shard x{ws} (no data-path collective)",
                        "input_generation_s": round(gen_s, 1)},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(tot_launch),
+            "roofline": roof, "iteration_roofline": iter_roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(tot_launch),
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
