@@ -16,12 +16,13 @@ ap.add_argument("--grid", type=int, default=256)
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--physics", default="thermal")
 ap.add_argument("--nrhs", type=int, default=3)
+ap.add_argument("--bc", default="0,0,0", help="per-axis boundary conditions, e.g. 0,0,1 (mixed)")
 a = ap.parse_args()
 n = a.grid
 dev = torch.device("cuda:0")
 if a.physics == "thermal":
     ph = torch.from_numpy(synth.config3_microstructure(3, n=n)).to(dev)
-    s = UnoCG(ph, "thermal", (1.0, 20.0), nrhs=a.nrhs, seed=3003, amp=0.1)
+    s = UnoCG(ph, "thermal", (1.0, 20.0), nrhs=a.nrhs, seed=3003, amp=0.1, bc=tuple(int(v) for v in a.bc.split(",")))
     loads = np.eye(3)[: a.nrhs]
     nb = {"K": 17, "xfwd": 24 + 8.06, "ypass": 16.1, "gpass": 20.1, "xinv": 40.06}
 else:
