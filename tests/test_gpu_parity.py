@@ -462,3 +462,39 @@ def test_all_dirichlet_thermal_exact_inverse():
     Ku = s.apply_K(torch.from_numpy(_pad(u)[None]).to(dev()))
     z = s.apply_precond(Ku).cpu().numpy()[0]
     assert rel(z, _pad(u)) <= 1e-12
+
+
+# ------------------------------------------------------------------ maximum sizes (N_i = 1024)
+MAX_SHAPES = [((1024, 1024, 8), "thermal"), ((16, 16, 1024), "thermal"), ((1024, 1024), "thermal"),
+              ((1024, 16, 8), "elastic"), ((16, 1024, 8), "elastic")]
+
+
+@pytest.mark.parametrize("N,physics", MAX_SHAPES)
+def test_maximum_axis_lengths(N, physics):
+    # the largest transform / tile instances (1024-point passes) against the oracle
+    g, ph, mat, amp, seed = make_case(N, physics, vf=0.3)
+    s = solver(ph, physics, mat, 1, seed, amp)
+    u = synth.test_vector(61, g.field_shape())
+    Ku = s.apply_K(torch.from_numpy(u[None]).to(dev())).cpu().numpy()[0]
+    assert rel(Ku, fem.apply_K(g, physics, ph, mat, u)) <= 1e-13
+    G = greens.ghat(g, physics, mat, seed, amp)
+    z = s.apply_precond(torch.from_numpy(u[None]).to(dev())).cpu().numpy()[0]
+    # at N = 1024 the lowest frequencies carry |A(k)| ~ (2 pi / N)^2 ~ 4e-5 of max|A|: the oracle's
+    # probed symbol (an FFT of the stencil response, then inverted) has relative error ~ eps (N / 2pi)^2
+    # ~ 3e-12 there (x the 3x3 block condition ~ 5 for elastic), and those modes dominate z; the
+    # tolerance of the moderate sizes (1e-12) therefore becomes 5e-11 (measured 1.4e-12 thermal,
+    # 1.7e-11 elastic)
+    assert rel(z, greens.apply_precond(G, u)) <= 5e-11
+
+
+def test_maximum_load_cases():
+    # nrhs = 8 (kMaxRhs): every load keeps its own CG scalars; each equals its single-load solve
+    P = synth.config1()
+    ph = P.phase[:16, :32, :32].copy()
+    loads = np.array([[np.cos(0.4 * i), np.sin(0.4 * i), 0.1 * i] for i in range(8)])
+    s = solver(ph, "thermal", P.mat, 8, P.seed, P.amp)
+    res = s.solve(loads)
+    for i in (0, 5, 7):
+        one = solver(ph, "thermal", P.mat, 1, P.seed, P.amp).solve(loads[i:i + 1])
+        assert res.reports[i]["iterations"] == one.reports[0]["iterations"]
+        assert rel(res.u[i].cpu().numpy(), one.u[0].cpu().numpy()) <= 1e-12
