@@ -498,3 +498,37 @@ def test_maximum_load_cases():
         one = solver(ph, "thermal", P.mat, 1, P.seed, P.amp).solve(loads[i:i + 1])
         assert res.reports[i]["iterations"] == one.reports[0]["iterations"]
         assert rel(res.u[i].cpu().numpy(), one.u[0].cpu().numpy()) <= 1e-12
+
+
+@pytest.mark.parametrize("N,physics", [((8, 8, 4), "thermal"), ((16, 8, 4), "elastic"), ((8, 8), "thermal"),
+                                       ((8, 8), "elastic")])
+def test_minimum_sizes(N, physics):
+    # the smallest grids the ABI accepts (single partial tiles everywhere): K, P and a solve
+    g, ph, mat, amp, seed = make_case(N, physics, vf=0.4)
+    s = solver(ph, physics, mat, 1, seed, amp)
+    u = synth.test_vector(71, g.field_shape())
+    Ku = s.apply_K(torch.from_numpy(u[None]).to(dev())).cpu().numpy()[0]
+    assert rel(Ku, fem.apply_K(g, physics, ph, mat, u)) <= 1e-13
+    G = greens.ghat(g, physics, mat, seed, amp)
+    z = s.apply_precond(torch.from_numpy(u[None]).to(dev())).cpu().numpy()[0]
+    assert rel(z, greens.apply_precond(G, u)) <= 1e-12
+    load = loads_for(physics, len(N), 1)
+    ref = homog.solve_problem(g, physics, ph, mat, load, seed, amp, tol=1e-8)
+    res = s.solve(load)
+    assert abs(res.reports[0]["iterations"] - ref["iterations"][0]) <= 1
+
+
+def test_invalid_arguments_rejected():
+    from paper_2508_02681_b200 import binding as Bn
+    from paper_2508_02681_b200.api import UnoCG
+
+    ph = torch.zeros((8, 8, 8), dtype=torch.uint8, device=dev())
+    with pytest.raises(Bn.UnoError) as e:
+        UnoCG(ph, "thermal", (1.0, 2.0), nrhs=0)
+    assert e.value.status == Bn.UNO_ERR_ARG
+    with pytest.raises(Bn.UnoError) as e:
+        UnoCG(ph, "thermal", (1.0, -2.0), nrhs=1)
+    assert e.value.status == Bn.UNO_ERR_ARG
+    with pytest.raises(Bn.UnoError) as e:
+        UnoCG(torch.zeros((8, 8, 12), dtype=torch.uint8, device=dev()), "thermal", (1.0, 2.0), nrhs=1)
+    assert e.value.status == Bn.UNO_ERR_SHAPE
