@@ -338,17 +338,30 @@ def ghat_dirichlet(g: fem.Grid, physics: str, mat, seed: int, amp: float, ref=No
     Am = np.moveaxis(A.reshape(c, c, -1), -1, 0)
     Phi = np.linalg.inv(Am)
     Phi = 0.5 * (Phi + np.transpose(Phi, (0, 2, 1)))
-    if seed:
-        base = (8 * can.reshape(-1)).astype(np.uint64)
+    Phi = _perturb_blocks(Phi, can.reshape(-1), seed, amp, c)
+    return np.moveaxis(Phi, 0, -1).reshape((c, c) + shp)
+
+
+def _perturb_blocks(Phi: np.ndarray, can: np.ndarray, seed: int, amp: float, c: int) -> np.ndarray:
+    """Phi + amp tr(Phi)/c psi(theta) per block: c = 2 with Eq 45 (theta_1,2 in [0.5, 1],
+    theta_3 in [-0.5, 0.5]), c = 3 with Eq B5; theta drawn at u01(seed, 2, 8 canon + t)."""
+    if not seed:
+        return Phi
+    base = (8 * can).astype(np.uint64)
+    if c == 2:
+        t1 = 0.5 + 0.5 * u01(seed, 2, base)
+        t2 = 0.5 + 0.5 * u01(seed, 2, base + np.uint64(1))
+        t3 = u01(seed, 2, base + np.uint64(2)) - 0.5
+        P = np.moveaxis(np.array([[t1 * t1, t1 * t3], [t1 * t3, t2 * t2 + t3 * t3]]), -1, 0)
+    else:
         th = np.stack([u01(seed, 2, base + np.uint64(t)) for t in range(6)])
         for t in (0, 1, 3):
             th[t] = 0.5 + 0.5 * th[t]
         for t in (2, 4, 5):
             th[t] = th[t] - 0.5
         P = np.moveaxis(psi3(th), -1, 0)
-        tr = np.trace(Phi, axis1=1, axis2=2) / 3.0
-        Phi = Phi + amp * tr[:, None, None] * P
-    return np.moveaxis(Phi, 0, -1).reshape((c, c) + shp)
+    tr = np.trace(Phi, axis1=1, axis2=2) / c
+    return Phi + amp * tr[:, None, None] * P
 
 
 def apply_precond_dirichlet(G: np.ndarray, r: np.ndarray) -> np.ndarray:
@@ -367,3 +380,72 @@ def dense_P_dirichlet(G: np.ndarray, spatial_shape) -> np.ndarray:
         for b in range(c):
             P[a * n:(a + 1) * n, b * n:(b + 1) * n] = T.T @ (G[a, b].reshape(-1)[:, None] * T)
     return P
+
+
+# ---------------------------------------------------------------- 2D mixed: periodic x, Dirichlet y
+def symbol_probe_mixed2d(g: fem.Grid, physics: str, ref) -> np.ndarray:
+    """Diagonal block of U K_r U^H for U = F_x (x) S_y (Table 1 row "Mixed"): the stencil
+    response to a delta, Fourier-transformed along x, with the part even in the y offset kept:
+    A(m, kx) = a_0(kx) + (a_+(kx) + a_-(kx)) cos(pi m / N2) (SURVEY A13 in 2D).  (c, c, N2-1, N1)."""
+    assert g.d == 2 and g.bc == (0, 1)
+    c = g.c
+    ny, nx = g.node_shape  # ny = N2 - 1
+    assert ny >= 3
+    y0 = ny // 2
+    phase0 = np.zeros(g.elem_shape, dtype=np.uint8)
+    coef = np.zeros((3, c, c, nx), dtype=complex)
+    for b in range(c):
+        delta = np.zeros((c,) + g.node_shape)
+        delta[b, y0, 0] = 1.0
+        col = fem.apply_K(g, physics, phase0, (ref, ref), delta)
+        for a in range(c):
+            for i, dy in enumerate((-1, 0, 1)):
+                coef[i, a, b] = np.fft.fft(col[a, y0 + dy])
+    am, a0, ap = coef.real  # the imaginary parts belong to the x-odd couplings of the y-odd terms
+    m = np.arange(1, ny + 1)
+    cy = np.cos(np.pi * m / (ny + 1))
+    A = a0[:, :, None] + (ap + am)[:, :, None] * cy[None, None, :, None]
+    Am = np.roll(np.flip(A, axis=-1), 1, axis=-1)  # A(-kx) = A(kx)
+    A = 0.5 * (A + Am)
+    return 0.5 * (A + np.swapaxes(A, 0, 1))
+
+
+def canon_index_mixed2d(shape) -> np.ndarray:
+    """Pairs {kx, -kx} at the same sine mode: flat p N1 + kx (p = m - 1), minimised over kx -> -kx."""
+    ny, nx = shape
+    P, X = np.meshgrid(np.arange(ny), np.arange(nx), indexing="ij")
+    return np.minimum(P * nx + X, P * nx + (-X) % nx)
+
+
+def ghat_mixed2d(g: fem.Grid, physics: str, mat, seed: int, amp: float, ref=None) -> np.ndarray:
+    if ref is None:
+        ref = reference_medium(physics, mat)
+    A = symbol_probe_mixed2d(g, physics, ref)
+    c = g.c
+    shp = g.node_shape
+    can = canon_index_mixed2d(shp)
+    if c == 1:
+        rho = (1.0 - amp + 2.0 * amp * u01(seed, 2, can.astype(np.uint64))) if seed else np.ones(shp)
+        return (rho / A[0, 0])[None, None]
+    Am = np.moveaxis(A.reshape(c, c, -1), -1, 0)
+    Phi = np.linalg.inv(Am)
+    Phi = 0.5 * (Phi + np.transpose(Phi, (0, 2, 1)))
+    Phi = _perturb_blocks(Phi, can.reshape(-1), seed, amp, c)
+    return np.moveaxis(Phi, 0, -1).reshape((c, c) + shp)
+
+
+def apply_precond_mixed2d(G: np.ndarray, r: np.ndarray) -> np.ndarray:
+    rh = transform.forward_mixed2d(r)
+    sh = np.einsum("ab...,b...->a...", half(G), rh)
+    return transform.inverse_mixed2d(sh, r.shape[1:])
+
+
+def dense_P_mixed2d(G: np.ndarray, spatial_shape) -> np.ndarray:
+    c = G.shape[0]
+    n = int(np.prod(spatial_shape))
+    T = transform.dense_T_mixed2d(spatial_shape)
+    P = np.zeros((c * n, c * n), dtype=complex)
+    for a in range(c):
+        for b in range(c):
+            P[a * n:(a + 1) * n, b * n:(b + 1) * n] = T.conj().T @ (G[a, b].reshape(-1)[:, None] * T)
+    return P.real

@@ -128,8 +128,11 @@ def solve_problem(g: fem.Grid, physics: str, phase, mat, loads, seed: int, amp: 
     """Full oracle pipeline for one problem: RHS (a1), G_hat (a0), Alg 2 (a2-a8), mean
     removal and effective property (a9).  Returns dict with per-load results."""
     mixed = g.bc == (0, 0, 1)
-    alld = g.d == 3 and all(b == 1 for b in g.bc)
-    if alld:
+    alld = all(b == 1 for b in g.bc)
+    if g.bc == (0, 1):  # 2D mixed: periodic x, Dirichlet y
+        G = greens.ghat_mixed2d(g, physics, mat, seed, amp)
+        applyP = lambda v: greens.apply_precond_mixed2d(G, v)  # noqa: E731
+    elif alld:
         G = greens.ghat_dirichlet(g, physics, mat, seed, amp)
         applyP = lambda v: greens.apply_precond_dirichlet(G, v)  # noqa: E731
     elif mixed:

@@ -104,3 +104,23 @@ def dense_T_dirichlet(spatial_shape) -> np.ndarray:
     for nm1 in spatial_shape:
         T = np.kron(T, dst1_matrix(nm1))
     return T
+
+
+# ---------------------------------------------------------------- 2D mixed: periodic x, Dirichlet y
+def forward_mixed2d(r: np.ndarray) -> np.ndarray:
+    """r_hat = (F_x (x) S_y) r for fields (c, N2-1, N1) (Table 1 row "Mixed"): DST-I along y
+    (numpy axis 1), then the orthonormal R2C DFT along x."""
+    from scipy.fft import dst
+    ry = dst(r, type=1, axis=1, norm="ortho")
+    return np.fft.rfft(ry, axis=2, norm="ortho")
+
+
+def inverse_mixed2d(rh: np.ndarray, spatial_shape) -> np.ndarray:
+    from scipy.fft import idst
+    r = np.fft.irfft(rh, n=spatial_shape[1], axis=2, norm="ortho")
+    return idst(r, type=1, axis=1, norm="ortho")
+
+
+def dense_T_mixed2d(spatial_shape) -> np.ndarray:
+    ny, nx = spatial_shape
+    return np.kron(dst1_matrix(ny).astype(complex), dft_matrix(nx))
