@@ -22,11 +22,14 @@
  *    DFT_y (x) DST-I_z, Table 1 "Mixed" P:452; node planes z = 1..N3-1 are the unknowns,
  *    N1 >= 32, N3 <= 512), or (3D) Dirichlet faces on every axis (bc = {1,1,1}; U = DST-I on
  *    every axis, Table 1 row "Dirichlet" P:451; N1 >= 32 thermal / 16 elastic, N2 >= 16,
- *    8 <= N3, all <= 512).  Other combinations return UNO_ERR_UNSUPPORTED.
+ *    8 <= N3, all <= 512); in 2D also Dirichlet on both axes (bc = {1,1,0}) and the mixed
+ *    case periodic x / Dirichlet y (bc = {0,1,0}; U = F_x (x) DST-I_y, Table 1 row "Mixed"),
+ *    16 <= N1, N2 <= 512.  Other combinations return UNO_ERR_UNSUPPORTED.
  *    N1, N2 in {8..1024}, N3 in {1} U {4..1024}, all powers of two.
  *  - Field layout (device): component-planar C order [nrhs][c][P3][N2][N1] with P3 = N3
- *    (periodic, and all-Dirichlet: the nodes with index 0 on any axis are the fixed boundary
- *    nodes, held at 0 on input and output) or N3 - 1 (Dirichlet z: stored planes are nodes
+ *    (periodic, and the all-Dirichlet / 2D cases: the nodes with index 0 on a Dirichlet axis
+ *    are the fixed boundary nodes, held at 0 on input and output) or N3 - 1 (3D mixed
+ *    Dirichlet z: stored planes are nodes
  *    z = 1..N3-1); node
  *    (i,j,k) at h*(i,j,k); voxel (i,j,k) has corners (i+a1, j+a2, k+a3) mod N.
  *    The paper's interleaved vec() (§1.6 Eq 1) is a fixed permutation of this.

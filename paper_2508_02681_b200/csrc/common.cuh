@@ -28,6 +28,8 @@ struct Geo {
   int halo;             // 1: K reads node planes zlo-1 / zlo+P3 from Ctx::hlo / Ctx::hhi
   int Ny, ky0;          // symbol of a y-chunk pencil: global N2 and the chunk's first k_y (Ny = 0: N2)
   int dir3;             // 1: Dirichlet on every axis (dirichlet.cu): periodic storage, index-0 nodes held at 0
+  int dmask;            // Dirichlet axes kept in that padded periodic storage (bit i = axis i): 7 (3D
+                        // all-Dirichlet), 3 (2D Dirichlet), 2 (2D mixed: periodic x, Dirichlet y)
 };
 
 // Per-load CG state (device resident; Alg 2 scalars).

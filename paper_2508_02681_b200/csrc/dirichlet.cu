@@ -10,6 +10,7 @@
 // s = P r between the fused r and d passes of precond.cu, with gamma = r.s in its own pass.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <type_traits>
 
 #include "common.cuh"
@@ -106,6 +107,11 @@ __global__ void d3_gmul_kernel(Ctx cx, double* __restrict__ v) {
       double* w = v + (long long)l * g.c * n;
       if (g.c == 1) {
         w[i] *= cx.gtab[i];
+      } else if (g.c == 2) {
+        const double g1 = cx.gtab[i], g2 = cx.gtab[n + i], g3 = cx.gtab[2 * n + i];
+        const double a = w[i], b = w[n + i];
+        w[i] = fma(g1, a, g3 * b);
+        w[n + i] = fma(g3, a, g2 * b);
       } else {
         const double* G = cx.gtab;
         const double g1 = G[i], g2 = G[n + i], g3 = G[2 * n + i], g4 = G[3 * n + i], g5 = G[4 * n + i],
@@ -199,6 +205,64 @@ __global__ void d3_symbol_kernel(Ctx cx, double* gtab, double ref0, double ref1,
   gtab[5 * n + b] = P[0][2] * scale;
 }
 
+// 2D symbols of the padded storage: dmask 3 (Dirichlet x, y: real per node [y][x], modes at index m)
+// and dmask 2 (periodic x, Dirichlet y: R2C half spectrum [kx][y-mode]); closed form of the diagonal
+// block (SURVEY A3 in 2D, S_xy dropped), perturbation of SURVEY A8 with Eq 45 for c = 2 at the canon
+// index of oracle/greens.ghat_dirichlet / ghat_mixed2d.
+__global__ void d2_symbol_kernel(Ctx cx, double* gtab, double ref0, double ref1, unsigned long long seed, double amp) {
+  const Geo g = cx.g;
+  const long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long ns = g.nspec;
+  if (b >= ns) return;
+  const int N1 = g.N1, N2 = g.N2;
+  int kx, m;
+  double cx_, cy, scale;
+  unsigned long long canon;
+  bool zero;
+  if (g.dmask == 3) {
+    kx = (int)(b % N1);  // sine mode m1
+    m = (int)(b / N1);
+    zero = kx == 0 || m == 0;
+    cx_ = cospi((double)kx / N1);
+    scale = 4.0 / ((double)N1 * N2);
+    canon = zero ? 0 : (unsigned long long)(m - 1) * (N1 - 1) + (kx - 1);
+  } else {
+    kx = (int)(b / N2);  // layout [kx][z = 0][y]
+    m = (int)(b % N2);
+    zero = m == 0;
+    const int ka = 2 * kx <= N1 ? kx : N1 - kx;
+    cx_ = cospi(2.0 * ka / N1);
+    scale = 2.0 / ((double)N1 * N2);
+    const unsigned long long p = zero ? 0 : (unsigned long long)(m - 1);
+    const unsigned long long f1 = p * N1 + kx, f2 = p * N1 + (unsigned long long)((N1 - kx) % N1);
+    canon = f1 < f2 ? f1 : f2;
+  }
+  if (zero) {
+    for (int q = 0; q < g.C; ++q) gtab[q * ns + b] = 0.0;
+    return;
+  }
+  cy = cospi((double)m / N2);
+  const double Sxx = (2.0 / 3.0) * (1.0 - cx_) * (2.0 + cy), Syy = (2.0 / 3.0) * (1.0 - cy) * (2.0 + cx_);
+  const double tr = Sxx + Syy;
+  if (g.c == 1) {
+    const double rho = seed ? (1.0 - amp + 2.0 * amp * u01(seed, 2, canon)) : 1.0;
+    gtab[b] = rho / (tr * ref0) * scale;
+    return;
+  }
+  double P11 = 1.0 / ((ref0 + ref1) * Sxx + ref1 * tr), P22 = 1.0 / ((ref0 + ref1) * Syy + ref1 * tr), P12 = 0.0;
+  if (seed) {  // Eq 45: theta_1,2 in [0.5, 1], theta_3 in [-0.5, 0.5]
+    const double t1 = 0.5 + 0.5 * u01(seed, 2, 8ULL * canon), t2 = 0.5 + 0.5 * u01(seed, 2, 8ULL * canon + 1);
+    const double t3 = u01(seed, 2, 8ULL * canon + 2) - 0.5;
+    const double a = amp * (P11 + P22) / 2.0;
+    P11 += a * t1 * t1;
+    P22 += a * (t2 * t2 + t3 * t3);
+    P12 += a * t1 * t3;
+  }
+  gtab[b] = P11 * scale;
+  gtab[ns + b] = P22 * scale;
+  gtab[2 * ns + b] = P12 * scale;
+}
+
 template <class F>
 static int d3_dispatch(int L2, F&& f) {
   switch (L2) {
@@ -227,19 +291,54 @@ static int launch_dst3(const Ctx& cx, const double* src, double* dst, int axis, 
   });
 }
 
-// s = P r for all nrhs fields (7 passes)
+// 2D mixed (periodic x, Dirichlet y): s_hat = G_hat s_hat on the R2C half spectrum [c][kx][y-mode]
+// (complex values, real symmetric c x c symbol), in place
+__global__ void d2m_gmul_kernel(Ctx cx, double2* __restrict__ spec) {
+  const Geo g = cx.g;
+  const long long ns = g.nspec;
+  for (long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x; b < ns; b += (long long)gridDim.x * blockDim.x) {
+    for (int l = 0; l < g.nrhs; ++l) {
+      double2* w = spec + (long long)l * g.c * ns;
+      if (g.c == 1) {
+        w[b] = cscale(w[b], cx.gtab[b]);
+      } else {
+        const double g1 = cx.gtab[b], g2 = cx.gtab[ns + b], g3 = cx.gtab[2 * ns + b];
+        const double2 a = w[b], c = w[ns + b];
+        w[b] = make_double2(fma(g1, a.x, g3 * c.x), fma(g1, a.y, g3 * c.y));
+        w[ns + b] = make_double2(fma(g3, a.x, g2 * c.x), fma(g3, a.y, g2 * c.y));
+      }
+    }
+  }
+}
+
+// s = P r for all nrhs fields: DST-I on every Dirichlet axis of the padded storage; for the 2D
+// mixed case the x axis in between is the periodic R2C machinery (xfwd / xinv, standalone).
 int launch_d3_precond(const Ctx& cx, const double* r, double* sbuf, const double2* const tw2[3], cudaStream_t s) {
+  const Geo& g = cx.g;
   int n = 0, k;
+  const long long gb = std::min<long long>((g.n + 255) / 256, 148 * 16);
+  if (g.dim == 2 && g.dmask == 2) {  // F_x (x) S_y
+    if ((k = launch_dst3(cx, r, sbuf, 1, tw2[1], s)) < 0) return -1;
+    n += k;
+    if ((k = launch_xfwd(cx, STANDALONE, sbuf, s)) < 0) return -1;
+    n += k;
+    const long long sb = std::min<long long>((g.nspec + 255) / 256, 148 * 16);
+    d2m_gmul_kernel<<<(unsigned)sb, 256, 0, s>>>(cx, cx.spec);
+    ++n;
+    if ((k = launch_xinv(cx, STANDALONE, sbuf, s)) < 0) return -1;
+    n += k;
+    if ((k = launch_dst3(cx, sbuf, sbuf, 1, tw2[1], s)) < 0) return -1;
+    return n + k;
+  }
   if ((k = launch_dst3(cx, r, sbuf, 0, tw2[0], s)) < 0) return -1;
   n += k;
-  for (int axis = 1; axis < 3; ++axis) {
+  for (int axis = 1; axis < g.dim; ++axis) {
     if ((k = launch_dst3(cx, sbuf, sbuf, axis, tw2[axis], s)) < 0) return -1;
     n += k;
   }
-  long long b = (cx.g.n + 255) / 256;
-  d3_gmul_kernel<<<(unsigned)(b > 148 * 16 ? 148 * 16 : b), 256, 0, s>>>(cx, sbuf);
+  d3_gmul_kernel<<<(unsigned)gb, 256, 0, s>>>(cx, sbuf);
   ++n;
-  for (int axis = 2; axis >= 0; --axis) {
+  for (int axis = g.dim - 1; axis >= 0; --axis) {
     if ((k = launch_dst3(cx, sbuf, sbuf, axis, tw2[axis], s)) < 0) return -1;
     n += k;
   }
@@ -254,7 +353,10 @@ int launch_d3_dot(const Ctx& cx, const double* a, const double* b, int mode, cud
 
 int launch_d3_symbol(const Ctx& cx, double* gtab, double ref0, double ref1, unsigned long long seed, double amp,
                      cudaStream_t s) {
-  d3_symbol_kernel<<<(unsigned)((cx.g.n + 255) / 256), 256, 0, s>>>(cx, gtab, ref0, ref1, seed, amp);
+  if (cx.g.dim == 2)
+    d2_symbol_kernel<<<(unsigned)((cx.g.nspec + 255) / 256), 256, 0, s>>>(cx, gtab, ref0, ref1, seed, amp);
+  else
+    d3_symbol_kernel<<<(unsigned)((cx.g.n + 255) / 256), 256, 0, s>>>(cx, gtab, ref0, ref1, seed, amp);
   return 1;
 }
 

@@ -1563,7 +1563,8 @@ __global__ void __launch_bounds__(256) kp_thermal2d_kernel(Ctx cx, int mode, con
     EE = fma(a00 + a10, dm0, EE);
     EE = fma(a10 + a11, d0p, EE);
     EE = fma(a00 + a01, d0m, EE);
-    const double pv = (fma(6.0 * d00, Ksum, EE) - 2.0 * KS) * (1.0 / 6.0);
+    double pv = (fma(6.0 * d00, Ksum, EE) - 2.0 * KS) * (1.0 / 6.0);
+    if (((g.dmask & 1) && x == 0) || ((g.dmask & 2) && y == 0)) pv = 0.0;  // Dirichlet nodes (padded storage)
     dst[(long long)load * g.n + i] = pv;
     part = d00 * pv;
   }
@@ -1690,6 +1691,7 @@ __global__ void __launch_bounds__(256) kp_elastic2d_kernel(Ctx cx, int mode, con
         }
       }
     }
+    if (((g.dmask & 1) && x == 0) || ((g.dmask & 2) && y == 0)) acc[0] = acc[1] = 0.0;  // Dirichlet nodes
     for (int al = 0; al < 2; ++al) {
       dst[(long long)load * 2 * n + al * n + i] = acc[al];
       part = fma(__ldg(dv + al * n + i), acc[al], part);
@@ -1811,7 +1813,8 @@ __global__ void __launch_bounds__(256) rhs_kernel(Ctx cx, LoadParams lp, double*
     int z, n[3];
     octant_counts(warp_ok ? node_octants_warp(cx, i, z) : node_octants(cx, i, z), g.dim, n);
     const double n0 = n[0], n1 = n[1], n2 = n[2];
-    const bool fixed = g.dir3 && ((i & (g.N1 - 1)) == 0 || ((i / g.N1) & (g.N2 - 1)) == 0 || z == 0);  // Dirichlet node
+    const bool fixed = ((g.dmask & 1) && (i & (g.N1 - 1)) == 0) || ((g.dmask & 2) && ((i / g.N1) & (g.N2 - 1)) == 0) ||
+                       ((g.dmask & 4) && z == 0);  // Dirichlet node of the padded storage
     for (int l = 0; l < nl; ++l)
       for (int al = 0; al < c; ++al) {
         const double* Cr = C + (l * c + al) * 3;
@@ -2136,9 +2139,11 @@ __global__ void eq55_kernel(Ctx cx, const double* gtab, double* partials) {
   const long long ns = g.nspec;
   const double nn = g.dirz ? (double)g.n : (double)g.N1 * (g.Ny ? g.Ny : g.N2) * g.N3;
   for (long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x; b < ns; b += (long long)gridDim.x * blockDim.x) {
-    if (b == 0 && !g.dirz && g.ky0 == 0) continue;  // periodic: G_hat(0) = 0 shares the null space
+    if (b == 0 && !g.dirz && g.ky0 == 0 && !g.dmask) continue;  // periodic: G_hat(0) = 0 shares the null space
     if (g.dir3 && ((b & (g.N1 - 1)) == 0 || ((b / g.N1) & (g.N2 - 1)) == 0 || b / ((long long)g.N1 * g.N2) == 0))
       continue;  // all-Dirichlet: index-0 entries are not modes
+    if (g.dim == 2 && g.dmask == 3 && ((b % g.N1) == 0 || (b / g.N1) == 0)) continue;
+    if (g.dim == 2 && g.dmask == 2 && (b % g.N2) == 0) continue;
     double lo, hi;
     if (g.c == 1) {
       lo = hi = gtab[b] * nn;

@@ -225,7 +225,7 @@ static uno_status setup_problem(uno_cg_handle* h) {
   h->cx = make_ctx(h);
   if (h->precond == 2 && h->dinv) launch_jacobi_dinv(h->cx, h->dinv, s);  // Eq 25 for the new problem
   // a0: symbol table + Eq 55 check
-  if (g.dir3)
+  if (g.dmask)
     launch_d3_symbol(h->cx, h->gtab, h->ref0, h->ref1, D.seed, D.seed ? D.amp : 0.0, s);
   else
     launch_build_symbol(h->cx, h->gtab, h->ref0, h->ref1, D.seed, D.seed ? D.amp : 0.0, s);
@@ -260,10 +260,12 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
   // boundary conditions: all periodic, or (3D) periodic x, y with Dirichlet z (mixed)
   const bool dirz = D.dim == 3 && D.bc[0] == 0 && D.bc[1] == 0 && D.bc[2] == 1;
   const bool dir3 = D.dim == 3 && D.bc[0] == 1 && D.bc[1] == 1 && D.bc[2] == 1;
+  const int dmask2 = D.dim == 2 ? (D.bc[0] ? 1 : 0) | (D.bc[1] ? 2 : 0) : 0;  // 2D: 3 Dirichlet, 2 mixed
   for (int i = 0; i < D.dim; ++i)
-    if (D.bc[i] != 0 && !dirz && !dir3)
+    if (D.bc[i] != 0 && !dirz && !dir3 && dmask2 != 3 && dmask2 != 2)
       return fail(UNO_ERR_UNSUPPORTED,
-                  "boundary conditions: all periodic, periodic x,y + Dirichlet z, or (3D) all Dirichlet");
+                  "boundary conditions: all periodic, periodic x,y + Dirichlet z, all Dirichlet, or (2D) "
+                  "periodic x + Dirichlet y");
   const int N1 = D.n[0], N2 = D.n[1], N3 = D.dim == 3 ? D.n[2] : 1;
   if (!is_pow2(N1) || !is_pow2(N2) || !is_pow2(N3) || N1 < 8 || N2 < 8 || N1 > 1024 || N2 > 1024 ||
       (D.dim == 3 && (N3 < 4 || N3 > 1024)))
@@ -281,6 +283,8 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
     return fail(UNO_ERR_SHAPE, "mixed BC needs N1 >= 32 (thermal) / 16 (elastic), 8 <= N3 <= 512");
   if (dir3 && ((c == 1 && (N1 < 32 || N2 < 16)) || N1 < 16 || N2 < 16 || N3 < 8 || N1 > 512 || N2 > 512 || N3 > 512))
     return fail(UNO_ERR_SHAPE, "all-Dirichlet needs N1 >= 32 (thermal) / 16 (elastic), N2 >= 16, N3 >= 8, all <= 512");
+  if (dmask2 && (N1 < 16 || N2 < 16 || N1 > 512 || N2 > 512))
+    return fail(UNO_ERR_SHAPE, "2D Dirichlet / mixed needs 16 <= N1, N2 <= 512");
   if (D.seed != 0 && !(D.amp >= 0 && D.amp < 1)) return fail(UNO_ERR_ARG, "amp must be in [0, 1)");
 
   uno_cg_handle* h = new uno_cg_handle();  // value-initialised: all members zero
@@ -298,9 +302,11 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
   g.H1 = g.M + 1;
   g.dirz = dirz ? 1 : 0;
   g.dir3 = dir3 ? 1 : 0;
+  g.dmask = dir3 ? 7 : dmask2;
   g.P3 = dirz ? N3 - 1 : N3;
   g.n = (long long)N1 * N2 * g.P3;
-  g.nspec = dir3 ? g.n : (long long)g.H1 * N2 * g.P3;  // all-Dirichlet: real sine coefficients on the node grid
+  // all-Dirichlet: real sine coefficients on the node grid; 2D mixed: R2C half spectrum along x
+  g.nspec = (dir3 || dmask2 == 3) ? g.n : (long long)g.H1 * N2 * g.P3;
   g.h = D.h > 0 ? D.h : 1.0 / N1;
   g.C = c * (c + 1) / 2;
   g.NA = g.NB = 0;
@@ -351,8 +357,8 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
       (e = al((void**)&h->gtab, (size_t)g.C * g.nspec * 8)) || (e = al((void**)&h->kel, 2 * 576 * 8)) ||
       (e = al((void**)&h->twx, g.M * 16)) || (e = al((void**)&h->twxp, (g.M + 1) * 16)) ||
       (e = al((void**)&h->twy, N2 * 16)) || (e = al((void**)&h->twz, N3 * 16)) ||
-      (e = al((void**)&h->twz2, 2 * N3 * 16)) || (e = al((void**)&h->rt, (dirz || dir3) ? vec * 8 : 8)) ||
-      (e = al((void**)&h->twx2, dir3 ? 2 * N1 * 16 : 16)) || (e = al((void**)&h->twy2, dir3 ? 2 * N2 * 16 : 16)) ||
+      (e = al((void**)&h->twz2, 2 * N3 * 16)) || (e = al((void**)&h->rt, (dirz || g.dmask) ? vec * 8 : 8)) ||
+      (e = al((void**)&h->twx2, g.dmask ? 2 * N1 * 16 : 16)) || (e = al((void**)&h->twy2, g.dmask ? 2 * N2 * 16 : 16)) ||
       (e = al((void**)&h->st, kMaxRhs * sizeof(LoadState))) ||
       (e = al((void**)&h->partials, (size_t)RED_NSLOT * kMaxRhs * maxb * 8)) ||
       (e = al((void**)&h->counters, RED_NSLOT * kMaxRhs * sizeof(unsigned))) ||
@@ -394,7 +400,7 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
   twiddles(2 * N3, 2 * N3, t);
   cudaMemcpyAsync(h->twz2, t.data(), 2 * N3 * 16, cudaMemcpyHostToDevice, s);
   cudaStreamSynchronize(s);
-  if (dir3) {
+  if (g.dmask) {
     twiddles(2 * N1, 2 * N1, t);
     cudaMemcpyAsync(h->twx2, t.data(), 2 * N1 * 16, cudaMemcpyHostToDevice, s);
     cudaStreamSynchronize(s);
@@ -458,7 +464,7 @@ extern "C" uno_status uno_cg_set_preconditioner(uno_cg_handle* h, int32_t kind) 
 // ------------------------------------------------------------------------------ training (Alg 4)
 static uno_status train_check(const uno_cg_handle* h) {
   const Geo& g = h->g;
-  if (g.dim != 3 || g.dirz || g.dir3 || g.NB != 0 || g.ZP != 0)
+  if (g.dim != 3 || g.dirz || g.dmask || g.NB != 0 || g.ZP != 0)
     return fail(UNO_ERR_UNSUPPORTED, "training: 3D periodic grids with the 5-pass transforms");
   return UNO_OK;
 }
@@ -574,7 +580,7 @@ extern "C" uno_status uno_cg_apply_precond(uno_cg_handle* h, const double* d_r, 
   if (h->precond != 0) {  // z = P r (identity / Jacobi) and r.z
     KL(launch_jac_r(h->cx, h->precond, STANDALONE, h->dinv, d_r, d_z, s), KC_XF);
     KL(launch_scalar_n(h->cx, RED_GAMMA, STANDALONE, jacobi_nblk(h->g), s), KC_OTHER);
-  } else if (h->g.dir3) {  // all-Dirichlet: DST-I on every axis (dirichlet.cu)
+  } else if (h->g.dmask) {  // all-Dirichlet / 2D mixed: DST-I axes (dirichlet.cu)
     const double2* tw2[3] = {h->twx2, h->twy2, h->twz2};
     KL(launch_d3_precond(h->cx, d_r, d_z, tw2, s), KC_G);
     KL(launch_d3_dot(h->cx, d_r, d_z, STANDALONE, s), KC_OTHER);
@@ -629,7 +635,7 @@ static int enqueue_iteration(uno_cg_handle* h, cudaStream_t s, cudaEvent_t* ev /
     n += launch_scalar_n(cx, RED_RNORM, CG, nb, s);
     n += launch_scalar_n(cx, RED_GAMMA, CG, nb, s);
     if (!run(4, [&] { return launch_jac_d(cx, h->precond, h->dinv, s); })) return -1;
-  } else if (h->g.dir3) {  // all-Dirichlet: r pass | s = P r (7 passes) | r.s | d pass
+  } else if (h->g.dmask) {  // all-Dirichlet / 2D mixed: r pass | s = P r | r.s | d pass
     const int nb = jacobi_nblk(h->g);
     const double2* tw2[3] = {h->twx2, h->twy2, h->twz2};
     if (!run(0, [&] { return launch_jac_r(cx, 1, CG, nullptr, nullptr, nullptr, s); })) return -1;
@@ -828,7 +834,7 @@ extern "C" uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, doub
   CK(cudaMemcpyAsync(h->st, h->h_st, g.nrhs * sizeof(LoadState), cudaMemcpyHostToDevice, s));
   const long long work = (long long)g.nrhs * g.c * g.n;
   // passes + 3 scalar kernels (mixed: 6 too); pipelined: 2C + 1 + 3C over C z-chunks
-  const int per_iter = h->precond != 0 ? 6 : g.dir3 ? 15 : (g.ZP > 0 ? 5 * (g.N3 / g.ZP) + 4 : ((g.dim == 3 && g.NB == 0) ? 6 : 4) + 3);
+  const int per_iter = h->precond != 0 ? 6 : g.dmask ? 15 : (g.ZP > 0 ? 5 * (g.N3 / g.ZP) + 4 : ((g.dim == 3 && g.NB == 0) ? 6 : 4) + 3);
   if (!h->timing) {
     // whole solve device-side: WHILE node over bodies of `chunk` iterations
     const int chunk = work >= (1LL << 22) ? 2 : 4;
@@ -878,7 +884,7 @@ extern "C" uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, doub
     }
   }
   KL(launch_finalize(h->cx, s), KC_OTHER);
-  if (g.dirz || g.dir3)  // Dirichlet faces: no null space, the fluctuation is not mean-free
+  if (g.dirz || g.dmask)  // Dirichlet faces: no null space, the fluctuation is not mean-free
     CK(cudaMemcpyAsync(d_u, h->u, (size_t)g.nrhs * g.c * g.n * 8, cudaMemcpyDeviceToDevice, s));
   else
     KL(launch_mean_removal(h->cx, h->u, d_u, h->scratch, s), KC_OTHER);

@@ -532,3 +532,52 @@ def test_invalid_arguments_rejected():
     with pytest.raises(Bn.UnoError) as e:
         UnoCG(torch.zeros((8, 8, 12), dtype=torch.uint8, device=dev()), "thermal", (1.0, 2.0), nrhs=1)
     assert e.value.status == Bn.UNO_ERR_SHAPE
+
+
+# ------------------------------------------------------------------ 2D Dirichlet / mixed (padded storage)
+BC2D = [((32, 16), "thermal", (1, 1)), ((16, 32), "elastic", (1, 1)), ((32, 16), "thermal", (0, 1)),
+        ((16, 16), "elastic", (0, 1))]
+
+
+def _pad2d(u, bc):  # oracle field (c, ny, nx) on the free nodes -> library padded (c, N2, N1)
+    c, ny, nx = u.shape
+    out = np.zeros((c, ny + bc[1], nx + bc[0]))
+    out[:, bc[1]:, bc[0]:] = u
+    return out
+
+
+def _ghat_bc2d(g, physics, mat, seed, amp, bc):
+    return greens.ghat_dirichlet(g, physics, mat, seed, amp) if bc == (1, 1) else \
+        greens.ghat_mixed2d(g, physics, mat, seed, amp)
+
+
+def _prec_bc2d(G, r, bc):
+    return greens.apply_precond_dirichlet(G, r) if bc == (1, 1) else greens.apply_precond_mixed2d(G, r)
+
+
+@pytest.mark.parametrize("N,physics,bc", BC2D)
+def test_2d_boundary_conditions(N, physics, bc):
+    from paper_2508_02681_b200.api import UnoCG
+
+    g0, ph, mat, amp, seed = make_case(N, physics)
+    g = fem.Grid(N, bc=bc, c=g0.c, h=1.0 / N[0])
+    s = UnoCG(torch.from_numpy(ph).to(dev()), physics, mat, nrhs=1, seed=seed, amp=amp, bc=bc + (0,))
+    u = synth.test_vector(81, g.field_shape())
+    Ku = s.apply_K(torch.from_numpy(_pad2d(u, bc)[None]).to(dev())).cpu().numpy()[0]
+    assert rel(Ku, _pad2d(fem.apply_K(g, physics, ph, mat, u), bc)) <= 1e-13
+    load = loads_for(physics, 2, 1)
+    f = s.rhs(load).cpu().numpy()[0]
+    fr = fem.rhs(g, physics, ph, mat, load[0])
+    assert np.max(np.abs(f - _pad2d(fr, bc))) <= 1e-14 * max(np.abs(fr).max(), 1e-300)
+    G = _ghat_bc2d(g, physics, mat, seed, amp, bc)
+    z, rz = s.apply_precond(torch.from_numpy(_pad2d(u, bc)[None]).to(dev()), want_dot=True)
+    zr = _prec_bc2d(G, u, bc)
+    assert rel(z.cpu().numpy()[0], _pad2d(zr, bc)) <= 1e-12
+    assert abs(rz[0] - np.sum(u * zr)) <= 1e-12 * abs(np.sum(u * zr))
+    ref = homog.solve_problem(g, physics, ph, mat, load, seed, amp, tol=1e-8)
+    res = s.solve(load)
+    assert abs(res.reports[0]["iterations"] - ref["iterations"][0]) <= 1 and res.reports[0]["converged"]
+    m = ref["iterations"][0]
+    fx = homog.solve_problem(g, physics, ph, mat, load, seed, amp, fixed_iters=m)
+    uu = s.solve(load, fixed_iters=m).u.cpu().numpy()[0]
+    assert rel(uu, _pad2d(fx["U"][0], bc)) <= 1e-9
