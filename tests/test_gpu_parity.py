@@ -581,3 +581,19 @@ def test_2d_boundary_conditions(N, physics, bc):
     fx = homog.solve_problem(g, physics, ph, mat, load, seed, amp, fixed_iters=m)
     uu = s.solve(load, fixed_iters=m).u.cpu().numpy()[0]
     assert rel(uu, _pad2d(fx["U"][0], bc)) <= 1e-9
+
+
+def test_fundamental_solution():
+    # Fig 19's P.delta (the preconditioner's discrete fundamental solution):
+    # equals the oracle's, and is point-symmetric about the source (G(-k) = G(k), Eq 16)
+    N = (64, 64)
+    g, ph, mat, amp, seed = make_case(N, "thermal")
+    s = solver(ph, "thermal", mat, 1, seed, amp)
+    delta = np.zeros(g.field_shape())
+    delta[0, 20, 30] = 1.0
+    z = s.apply_precond(torch.from_numpy(delta[None]).to(dev())).cpu().numpy()[0, 0]
+    zr = greens.apply_precond(greens.ghat(g, "thermal", mat, seed, amp), delta)[0]
+    assert rel(z, zr) <= 1e-12
+    zs = np.roll(np.roll(z, -20, 0), -30, 1)  # source at the origin
+    zm = np.roll(np.flip(np.roll(np.flip(zs, 0), 1, 0), 1), 1, 1)  # x -> -x
+    assert np.max(np.abs(zs - zm)) <= 1e-12 * np.abs(zs).max()
