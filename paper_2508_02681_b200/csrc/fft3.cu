@@ -14,8 +14,6 @@
 // NA x N3 block per (kx, k_b)); the tabulated symbol uses the same layout.
 #include <cuda_runtime.h>
 
-#include <cooperative_groups.h>
-
 #include <cstdlib>
 #include <type_traits>
 
@@ -430,10 +428,7 @@ constexpr int F1R_XS = 129;                // X row stride
 __device__ __forceinline__ int f1r_swz(int k) { return k ^ (((k >> 3) & 1) << 2); }
 __host__ __device__ constexpr int f1r_smem_bytes() { return (F1R_TY + 16 * F1R_XS + 128 + 129 + 16 + 8 + 8) * 16; }
 
-// CL > 1: a cluster of CL CTAs with consecutive y_a stages its outputs in shared memory and
-// each CTA stores a share of the (kx, k_b) pairs for all CL y_a values (16 CL contiguous bytes
-// instead of scattered 16-byte stores), reading the peers' shared memory over DSMEM.
-template <int MODE, int CL>
+template <int MODE>
 __global__ void __launch_bounds__(256, UNO_F1R_MINB) f1r_kernel(Ctx cx, const double* __restrict__ src) {
   constexpr int M = 128, NB = 16, NA = 16;
   const Geo g = cx.g;
@@ -519,7 +514,6 @@ __global__ void __launch_bounds__(256, UNO_F1R_MINB) f1r_kernel(Ctx cx, const do
   // NB-point DFT across the rows (y_b -> k_b), twiddle w_N2^{y_a k_b}, scatter to [kx][k_b][z][y_a]
   double2* out = cx.spec + ((long long)load * g.c + comp) * g.nspec + (long long)z * NA + ya;
   const long long kbstride = (long long)g.N3 * NA;
-  double2* OUT = X;  // CL > 1: [kx][k_b] staging (X is dead after the post-processing)
   for (int it = t; it < 2 * (M + 1); it += 256) {
     const int kx = it >> 1, h = it & 1;
     double2 a[16], o[8];
@@ -529,26 +523,8 @@ __global__ void __launch_bounds__(256, UNO_F1R_MINB) f1r_kernel(Ctx cx, const do
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
       const int kb = 2 * m + h;
-      const double2 val = kb ? cmul(o[m], twa[kb]) : o[m];
-      if constexpr (CL == 1)
-        __stcg(out + ((long long)kx * NB + kb) * kbstride, val);
-      else
-        OUT[kx * NB + kb] = val;
+      __stcg(out + ((long long)kx * NB + kb) * kbstride, kb ? cmul(o[m], twa[kb]) : o[m]);
     }
-  }
-  if constexpr (CL > 1) {
-    namespace cgr = cooperative_groups;
-    cgr::cluster_group cluster = cgr::this_cluster();
-    cluster.sync();
-    const int rank = (int)cluster.block_rank();  // = y_a mod CL (consecutive blockIdx.x)
-    double2* out0 = out - rank;                  // y_a0 = y_a - rank
-    constexpr int NP = (M + 1) * NB / CL;        // pairs per CTA
-    for (int it = t; it < NP * CL; it += 256) {
-      const int q = it % CL, p = rank + CL * (it / CL);
-      const double2* peer = cluster.map_shared_rank(OUT, q);
-      __stcg(out0 + (long long)p * kbstride + q, peer[p]);
-    }
-    cluster.sync();  // peers keep their staging alive until every read is done
   }
   if (MODE == CG) partial_write<true>(cx, RED_RNORM, load, blockIdx.x, mx, red_sh);
 }
@@ -564,7 +540,7 @@ constexpr int F3R_TS = 16 * 16 * 9;       // T: 16 rows x [16][9] (aliases Y)
 constexpr int F3R_TY = F3R_YS > F3R_TS ? F3R_YS : F3R_TS;
 __host__ __device__ constexpr int f3r_smem_bytes() { return (F3R_TY + 16 * F1R_XS + 128 + 129 + 16 + 8 + 8) * 16; }
 
-template <int MODE, int CL>
+template <int MODE>
 __global__ void __launch_bounds__(256, UNO_F1R_MINB) f3r_kernel(Ctx cx, double* __restrict__ dst) {
   constexpr int M = 128, NB = 16, NA = 16;
   const Geo g = cx.g;
@@ -586,22 +562,7 @@ __global__ void __launch_bounds__(256, UNO_F1R_MINB) f3r_kernel(Ctx cx, double* 
   const int z = zc % g.N3, comp = zc / g.N3;
   const double2* in = cx.spec + ((long long)load * g.c + comp) * g.nspec + (long long)z * NA + ya;
   const long long kbstride = (long long)g.N3 * NA;
-  if constexpr (CL == 1) {
-    for (int e = t; e < (M + 1) * NB; e += 256) cp_async16(&YT[(e >> 4) * 17 + (e & 15)], in + (long long)e * kbstride);
-  } else {  // cluster: 16 CL contiguous bytes per (kx, k_b) pair, distributed over DSMEM
-    namespace cgr = cooperative_groups;
-    cgr::cluster_group cluster = cgr::this_cluster();
-    const int rank = (int)cluster.block_rank();
-    const double2* in0 = in - rank;
-    constexpr int NP = (M + 1) * NB / CL;
-    cluster.sync();  // every peer is running before its shared memory is written
-    for (int it = t; it < NP * CL; it += 256) {
-      const int q = it % CL, p = rank + CL * (it / CL);
-      const double2 val = __ldcg(in0 + (long long)p * kbstride + q);
-      cluster.map_shared_rank(YT, q)[(p >> 4) * 17 + (p & 15)] = val;
-    }
-    cluster.sync();
-  }
+  for (int e = t; e < (M + 1) * NB; e += 256) cp_async16(&YT[(e >> 4) * 17 + (e & 15)], in + (long long)e * kbstride);
   cp_commit();
   for (int i = t; i < M; i += 256) tw[i] = cx.tw.x[i];
   for (int i = t; i <= M; i += 256) twp[i] = cx.tw.xpost[i];
@@ -808,34 +769,6 @@ static void set_smem3(K kernel, int bytes) {
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
-// cluster size of the register-direct F1/F3 (UNO_F13_CLUSTER = 1, 4 or 8; default 1: the
-// DSMEM-staged contiguous stores measured slower on B200)
-static int f13_cluster() {
-  static const int cl = [] {
-    const char* e = getenv("UNO_F13_CLUSTER");
-    const int v = e ? atoi(e) : 1;
-    return (v == 1 || v == 4 || v == 8) ? v : 1;
-  }();
-  return cl;
-}
-
-template <class K, class... A>
-static int launch_clustered(K kernel, dim3 grid, int smem, int cl, cudaStream_t s, A... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = dim3(256, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = cl;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kernel, args...) == cudaSuccess ? 1 : -1;
-}
-
 template <class F>
 static int dispatch_m(int M, F&& f) {
   switch (M) {
@@ -876,15 +809,12 @@ int launch_f1(const Ctx& cx, int mode, const double* src, cudaStream_t s) {
   if (rd && g.N1 == 256 && g.NA == 16 && g.NB == 16) {
     const dim3 grid((unsigned)(g.NA * g.N3 * g.c), g.nrhs);
     constexpr int sm = f1r_smem_bytes();
-    const int cl = f13_cluster();
-    auto go = [&](auto k, int c) {
+    auto go = [&](auto k) {
       set_smem3(k, sm);
-      return launch_clustered(k, grid, sm, c, s, cx, src);
+      k<<<grid, 256, sm, s>>>(cx, src);
+      return 1;
     };
-    if (mode == CG)
-      return cl == 8 ? go(f1r_kernel<CG, 8>, 8) : cl == 4 ? go(f1r_kernel<CG, 4>, 4) : go(f1r_kernel<CG, 1>, 1);
-    return cl == 8 ? go(f1r_kernel<STANDALONE, 8>, 8)
-                   : cl == 4 ? go(f1r_kernel<STANDALONE, 4>, 4) : go(f1r_kernel<STANDALONE, 1>, 1);
+    return mode == CG ? go(f1r_kernel<CG>) : go(f1r_kernel<STANDALONE>);
   }
   return dispatch_m(g.M, [&](auto Mc) {
     constexpr int M = decltype(Mc)::value;
@@ -911,15 +841,12 @@ int launch_f3(const Ctx& cx, int mode, double* dst, cudaStream_t s) {
   if (rd && g.N1 == 256 && g.NA == 16 && g.NB == 16) {
     const dim3 grid((unsigned)(g.NA * g.N3 * g.c), g.nrhs);
     constexpr int sm = f3r_smem_bytes();
-    const int cl = f13_cluster();
-    auto go = [&](auto k, int c) {
+    auto go = [&](auto k) {
       set_smem3(k, sm);
-      return launch_clustered(k, grid, sm, c, s, cx, dst);
+      k<<<grid, 256, sm, s>>>(cx, dst);
+      return 1;
     };
-    if (mode == CG)
-      return cl == 8 ? go(f3r_kernel<CG, 8>, 8) : cl == 4 ? go(f3r_kernel<CG, 4>, 4) : go(f3r_kernel<CG, 1>, 1);
-    return cl == 8 ? go(f3r_kernel<STANDALONE, 8>, 8)
-                   : cl == 4 ? go(f3r_kernel<STANDALONE, 4>, 4) : go(f3r_kernel<STANDALONE, 1>, 1);
+    return mode == CG ? go(f3r_kernel<CG>) : go(f3r_kernel<STANDALONE>);
   }
   return dispatch_m(g.M, [&](auto Mc) {
     constexpr int M = decltype(Mc)::value;

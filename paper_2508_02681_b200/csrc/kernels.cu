@@ -1334,205 +1334,6 @@ static int k_nr(const Geo& g) {
   return (nr == 4 && g.N2 >= 16) ? 4 : 2;
 }
 
-// Same stencil, TMA-style staging for N1 >= 32 (the production path): one warp issues
-// cp.async.bulk row copies (global -> shared, completion counted on an mbarrier per ring slot),
-// so the 256 worker threads spend no instructions on address generation for the halo tile.
-// A slot carries node plane p of d (10 rows x 36 doubles: x0-2 .. x0+33) and the phase bytes of
-// element layer p-1 (9 rows x 64 B: x0-16 .. x0+47).  Conductivities are selected per node
-// from the phase bytes.  Ring of 8 slots, 4 planes of lookahead.
-constexpr int KB_DW = 36;            // doubles per staged d row
-constexpr int KB_PW = 64;            // bytes per staged phase row
-constexpr int KB_SLOT = 10 * KB_DW * 8 + 9 * KB_PW;  // bytes per ring slot (3456)
-constexpr int KB_RING = 8;
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n}\n" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(bar)
-               : "memory");
-}
-// copy the periodic window [x, x+len) of a row (element size es bytes) in <= 3 contiguous pieces
-__device__ __forceinline__ void bulk_row(unsigned dst, const char* row, int x, int len, int N, int es, unsigned bar) {
-  int xs = ((x % N) + N) % N;
-  while (len > 0) {
-    const int l = min(len, N - xs);
-    bulk_g2s(dst, row + (long long)xs * es, (unsigned)(l * es), bar);
-    dst += l * es;
-    len -= l;
-    xs = 0;
-  }
-}
-
-__global__ void __launch_bounds__(256, 3) kp_thermal3d_tma_kernel(Ctx cx, int mode, const double* __restrict__ src,
-                                                                  double* __restrict__ dst, int ZC) {
-  constexpr int TX = 32;
-  const Geo g = cx.g;
-  const int nzc = g.N3 / ZC;
-  const int load = blockIdx.z / nzc;
-  const int zcI = blockIdx.z - load * nzc;
-  if (mode == CG && !cx.st[load].active) return;
-  extern __shared__ __align__(128) unsigned char kbs[];
-  __shared__ __align__(8) unsigned long long bars[KB_RING];
-  __shared__ double red_sh[32];
-  const int t = threadIdx.x;
-  const int tx = t & 31, ty = t >> 5;
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * KT_TY, zs = zcI * ZC;
-  const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
-  const long long plane = (long long)N1 * N2;
-  const double* dv = src + (long long)load * g.n;
-  const double k0 = cx.mat[0][0], k1 = cx.mat[1][0];
-  const unsigned sbase = smem_u32(kbs);
-  const unsigned bar0 = smem_u32(bars);
-  if (t == 0) {
-    for (int i = 0; i < KB_RING; ++i) mbar_init(bar0 + 8 * i, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-  // producer: warp 0, lane r < 10 copies d row r, lane 10 + r (r < 9) copies phase row r
-  auto issue = [&](int p) {  // node plane p (and phase layer p-1) -> slot (p - zs + 1) & 7
-    const int q = p - zs + 1;
-    const int slot = q & (KB_RING - 1);
-    const unsigned bar = bar0 + 8 * slot;
-    const unsigned sd = sbase + slot * KB_SLOT;
-    if (tx == 0) mbar_expect_tx(bar, KB_SLOT);
-    __syncwarp();
-    if (tx < 10) {
-      const int zw = (p + N3) & (N3 - 1);
-      const int gy = (y0 - 1 + tx + N2) & (N2 - 1);
-      bulk_row(sd + tx * KB_DW * 8, reinterpret_cast<const char*>(dv + zw * plane + (long long)gy * N1), x0 - 2, KB_DW,
-               N1, 8, bar);
-    } else if (tx < 19) {
-      const int r = tx - 10;
-      const int zw = (p - 1 + N3) & (N3 - 1);
-      const int gy = (y0 - 1 + r + N2) & (N2 - 1);
-      bulk_row(sd + 10 * KB_DW * 8 + r * KB_PW,
-               reinterpret_cast<const char*>(cx.phase + zw * plane + (long long)gy * N1), x0 - 16, KB_PW, N1, 1, bar);
-    }
-  };
-  auto dtile = [&](int p) -> const double* {
-    return reinterpret_cast<const double*>(kbs + ((p - zs + 1) & (KB_RING - 1)) * KB_SLOT);
-  };
-  auto ptile = [&](int p) -> const unsigned char* {  // phase layer p-1 travels with plane p
-    return kbs + ((p - zs + 1) & (KB_RING - 1)) * KB_SLOT + 10 * KB_DW * 8;
-  };
-  auto wait_plane = [&](int p) {
-    const int q = p - zs + 1;
-    mbar_wait(bar0 + 8 * (q & (KB_RING - 1)), (unsigned)((q >> 3) & 1));
-  };
-  if (ty == 0) {
-    for (int p = zs - 1; p <= zs + 4; ++p)
-      if (p <= zs + ZC) issue(p);
-  }
-  double nb[3][3];
-  auto read3x3 = [&](int p) {
-    const double* Ds = dtile(p) + ty * KB_DW + tx + 1;
-#pragma unroll
-    for (int a = 0; a < 3; ++a)
-#pragma unroll
-      for (int b = 0; b < 3; ++b) nb[a][b] = Ds[a * KB_DW + b];
-  };
-  auto box = [&](double Qo[2][2]) {
-    const double P00 = nb[0][0] + nb[0][1], P01 = nb[0][1] + nb[0][2];
-    const double P10 = nb[1][0] + nb[1][1], P11 = nb[1][1] + nb[1][2];
-    const double P20 = nb[2][0] + nb[2][1], P21 = nb[2][1] + nb[2][2];
-    Qo[0][0] = P00 + P10;
-    Qo[0][1] = P01 + P11;
-    Qo[1][0] = P10 + P20;
-    Qo[1][1] = P11 + P21;
-  };
-  auto kap4 = [&](int p, double a[2][2]) {  // conductivities of the 4 elements around the node, layer p-1
-    const unsigned char* P = ptile(p) + ty * KB_PW + tx + 15;
-    a[0][0] = P[0] ? k1 : k0;
-    a[0][1] = P[1] ? k1 : k0;
-    a[1][0] = P[KB_PW] ? k1 : k0;
-    a[1][1] = P[KB_PW + 1] ? k1 : k0;
-  };
-  wait_plane(zs - 1);
-  wait_plane(zs);
-  double Qk[2][2], Qn[2][2], klo[2][2];
-  read3x3(zs - 1);
-  box(Qk);
-  double dzm = nb[1][1];
-  read3x3(zs);
-  box(Qn);
-  kap4(zs, klo);  // layer zs-1
-  double KSlo = 0.0;
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int b = 0; b < 2; ++b) KSlo = fma(klo[a][b], Qk[a][b] + Qn[a][b], KSlo);
-  double Klo = (klo[0][0] + klo[0][1]) + (klo[1][0] + klo[1][1]);
-  double Kxlo = klo[0][1] + klo[1][1];
-  double Kylo = klo[1][0] + klo[1][1];
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int b = 0; b < 2; ++b) Qk[a][b] = Qn[a][b];
-  double di = nb[1][1], dxm = nb[1][0], dxp = nb[1][2], dym = nb[0][1], dyp = nb[2][1];
-  double part = 0.0;
-  const double hc = g.h / 12.0;
-  double* outp = dst + (long long)load * g.n + (long long)(y0 + ty) * N1 + (x0 + tx);
-#pragma unroll 1
-  for (int k = zs; k < zs + ZC; ++k) {
-    wait_plane(k + 1);
-    read3x3(k + 1);
-    box(Qn);
-    double a[2][2];
-    kap4(k + 1, a);  // layer k
-    double KShi = a[0][0] * (Qk[0][0] + Qn[0][0]);
-    KShi = fma(a[0][1], Qk[0][1] + Qn[0][1], KShi);
-    KShi = fma(a[1][0], Qk[1][0] + Qn[1][0], KShi);
-    KShi = fma(a[1][1], Qk[1][1] + Qn[1][1], KShi);
-    const double Khi = (a[0][0] + a[0][1]) + (a[1][0] + a[1][1]);
-    const double Kxhi = a[0][1] + a[1][1], Kyhi = a[1][0] + a[1][1];
-    const double Ksum = Klo + Khi;
-    const double Kxp = Kxlo + Kxhi, Kyp = Kylo + Kyhi;
-    const double dzp = nb[1][1];
-    double EE = Kxp * dxp;
-    EE = fma(Ksum - Kxp, dxm, EE);
-    EE = fma(Kyp, dyp, EE);
-    EE = fma(Ksum - Kyp, dym, EE);
-    EE = fma(Khi, dzp, EE);
-    EE = fma(Klo, dzm, EE);
-    const double pv = hc * (fma(5.0 * di, Ksum, EE) - (KSlo + KShi));
-    outp[(long long)k * plane] = pv;
-    part = fma(di, pv, part);
-    KSlo = KShi;
-    Klo = Khi;
-    Kxlo = Kxhi;
-    Kylo = Kyhi;
-#pragma unroll
-    for (int aa = 0; aa < 2; ++aa)
-#pragma unroll
-      for (int b = 0; b < 2; ++b) Qk[aa][b] = Qn[aa][b];
-    dzm = di;
-    di = nb[1][1];
-    dxm = nb[1][0];
-    dxp = nb[1][2];
-    dym = nb[0][1];
-    dyp = nb[2][1];
-    __syncthreads();  // every thread is done with plane k-3's slot before it is refilled
-    if (ty == 0 && k + 5 <= zs + ZC) issue(k + 5);
-  }
-  const int nblk = gridDim.x * gridDim.y * nzc;
-  const int my = (zcI * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-  dp_finish(cx, load, nblk, my, part, red_sh, mode);
-}
 
 // Thermal 2D: element row (App. A1: {2/3, -1/6, -1/3}) ->
 //   p_i = 1/6 [ 6 d_i sum_o k_o + sum_{4 axis nbrs} d_j (k of the 2 octants on edge ij) - 2 sum_o k_o S_o ].
@@ -2475,15 +2276,7 @@ int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaS
       set_smem(kern, sm);
       kern<<<grid, tpb, sm, s>>>(cx, mode, src, dst, ZC);
     };
-    static const bool use_bulk = [] {
-      const char* e = getenv("UNO_KP_BULK");
-      return e && e[0] == '1';
-    }();
-    if (TX == 32 && use_bulk) {  // experimental cp.async.bulk staging (slower so far)
-      const int smb = KB_RING * KB_SLOT;
-      set_smem(kp_thermal3d_tma_kernel, smb);
-      kp_thermal3d_tma_kernel<<<grid, 256, smb, s>>>(cx, mode, src, dst, ZC);
-    } else if (g.halo && !(TX == 32 && k_nr(g) == 4)) {
+    if (g.halo && !(TX == 32 && k_nr(g) == 4)) {
       return -1;  // slab halos: the NR = 4 kernel only
     } else if (TX == 32 && k_nr(g) == 4) {
       const dim3 grid4(g.N1 / 32, g.N2 / 16, nzl * g.nrhs);
