@@ -312,7 +312,7 @@ def run_ours(args):
         e2e = {"value": dsum / (ems / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
 
     cpu = None
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:  # the oracle baseline is an N = 1 figure
         cpu = cpu_baseline(micro[3], 20.0, n)
 
     if rank == 0:
