@@ -435,6 +435,62 @@ __global__ void __launch_bounds__(YR_ROWS * YR_R) ypass256_kernel(Ctx cx, int z0
   }
 }
 
+// y pass for N2 = 512: 512 = 32 x 16 (y = n1 + 32 n2, k = k1 + 16 k2).  32 threads per row: each
+// loads 16 elements, DFT16 over n2, twiddle w_512^{n1 k1}, padded transpose; then the 32-point
+// DFTs over n1 (one per k1) are split between thread pairs (dft_half, outputs k2 = 2m + h) and
+// stored straight from registers.  4 rows per 128-thread CTA.
+constexpr int Y5_ROWS = 4, Y5_RS = 16 * 33;
+template <bool INV, int MODE>
+__global__ void __launch_bounds__(128) ypass512_kernel(Ctx cx, int z0, int zc) {
+  constexpr int L = 512;
+  const Geo g = cx.g;
+  const int load = blockIdx.y;
+  if (MODE == CG && !cx.st[load].active) return;
+  __shared__ double2 buf[Y5_ROWS * Y5_RS];
+  __shared__ double2 tw[16 * 32];  // [k1][n1] = w_512^{n1 k1}
+  __shared__ double2 tw32[16];     // w_32^r
+  const int t = threadIdx.x;
+  const int r = t >> 5, l32 = t & 31;
+  const long long nrows = (long long)g.c * g.H1 * g.N3;
+  long long row0 = (long long)blockIdx.x * Y5_ROWS;
+  if (zc > 0) {
+    const int nb = zc / Y5_ROWS;
+    const int q = blockIdx.x / nb;
+    row0 = (long long)q * g.N3 + z0 + (blockIdx.x - q * nb) * Y5_ROWS;
+  }
+  const bool ok = row0 + r < nrows;
+  double2* rowp = cx.spec + (long long)load * g.c * g.nspec + (row0 + r) * L;
+  double2 v[16];
+  if (ok) {
+#pragma unroll
+    for (int n2 = 0; n2 < 16; ++n2) v[n2] = __ldcg(rowp + l32 + 32 * n2);
+  }
+  for (int i = t; i < 16 * 32; i += 128) tw[i] = cx.tw.y[((i & 31) * (i >> 5)) & (L - 1)];
+  if (t < 16) tw32[t] = cx.tw.y[16 * t];
+  __syncthreads();
+  dft_reg<16, INV>(v);  // thread = n1: over n2 -> k1
+#pragma unroll
+  for (int k1 = 1; k1 < 16; ++k1) {
+    const double2 w = tw[k1 * 32 + l32];
+    v[k1] = cmul(v[k1], INV ? cconj(w) : w);
+  }
+  double2* Tr = buf + r * Y5_RS;
+#pragma unroll
+  for (int k1 = 0; k1 < 16; ++k1) Tr[k1 * 33 + l32] = v[k1];
+  __syncthreads();
+  {
+    const int k1 = l32 >> 1, h = l32 & 1;
+    double2 a[32], o[16];
+#pragma unroll
+    for (int n1 = 0; n1 < 32; ++n1) a[n1] = Tr[k1 * 33 + n1];
+    dft_half<32, INV>(a, h, tw32, o);
+    if (ok) {
+#pragma unroll
+      for (int m = 0; m < 16; ++m) __stcg(rowp + k1 + 16 * (2 * m + h), o[m]);
+    }
+  }
+}
+
 template <int L, int NC>
 __host__ __device__ constexpr int gsmem_tile_bytes() {
   return (NC * 8 * L + L) * (int)sizeof(double2);
@@ -2147,6 +2203,18 @@ int launch_ypass(const Ctx& cx, int mode, bool inverse, cudaStream_t s, int z0, 
     const char* e = getenv("UNO_YRD");
     return !(e && e[0] == '0');
   }();
+  if (rd && g.N2 == 512 && !(zc > 0 && (zc % Y5_ROWS))) {
+    const long long nrows = zc > 0 ? (long long)g.c * g.H1 * zc : (long long)g.c * g.H1 * g.N3;
+    const dim3 grid((unsigned)((nrows + Y5_ROWS - 1) / Y5_ROWS), g.nrhs);
+    if (mode == CG) {
+      if (inverse) ypass512_kernel<true, CG><<<grid, 128, 0, s>>>(cx, z0, zc);
+      else ypass512_kernel<false, CG><<<grid, 128, 0, s>>>(cx, z0, zc);
+    } else {
+      if (inverse) ypass512_kernel<true, STANDALONE><<<grid, 128, 0, s>>>(cx, z0, zc);
+      else ypass512_kernel<false, STANDALONE><<<grid, 128, 0, s>>>(cx, z0, zc);
+    }
+    return 1;
+  }
   if (rd && g.N2 == 256) {
     const long long nrows = zc > 0 ? (long long)g.c * g.H1 * zc : (long long)g.c * g.H1 * g.N3;
     const dim3 grid((unsigned)((nrows + YR_ROWS - 1) / YR_ROWS), g.nrhs);

@@ -597,3 +597,20 @@ def test_fundamental_solution():
     zs = np.roll(np.roll(z, -20, 0), -30, 1)  # source at the origin
     zm = np.roll(np.flip(np.roll(np.flip(zs, 0), 1, 0), 1), 1, 1)  # x -> -x
     assert np.max(np.abs(zs - zm)) <= 1e-12 * np.abs(zs).max()
+
+
+@pytest.mark.parametrize("N,physics", [((16, 512, 8), "thermal"), ((16, 512, 8), "elastic"), ((32, 512, 16), "thermal")])
+def test_512_point_y_pass(N, physics):
+    # the register-direct 512-point y pass (config 4's N2) in the preconditioner and a short solve
+    g, ph, mat, amp, seed = make_case(N, physics)
+    s = solver(ph, physics, mat, 2, seed, amp)
+    G = greens.ghat(g, physics, mat, seed, amp)
+    r = np.stack([synth.test_vector(91 + l, g.field_shape()) for l in range(2)])
+    z = s.apply_precond(torch.from_numpy(r).to(dev())).cpu().numpy()
+    tol = 1e-11 if physics == "thermal" else 5e-11  # long axis: see test_maximum_axis_lengths
+    for l in range(2):
+        assert rel(z[l], greens.apply_precond(G, r[l])) <= tol
+    load = loads_for(physics, 3, 1)
+    fx = homog.solve_problem(g, physics, ph, mat, load, seed, amp, fixed_iters=4)
+    u = solver(ph, physics, mat, 1, seed, amp).solve(load, fixed_iters=4).u.cpu().numpy()[0]
+    assert rel(u, fx["U"][0]) <= 1e-10
