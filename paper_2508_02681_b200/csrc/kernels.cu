@@ -668,6 +668,99 @@ __global__ void __launch_bounds__(8 * YR_R, 3) gpass256_kernel(Ctx cx) {  // sme
   gamma_finish(cx, load, part, red_sh, MODE);
 }
 
+// Elastic G pass for N3 = 256 (c = 3), register-direct: tile = 4 consecutive y columns of one kx
+// plane, all three components; thread (q, c, l) = component q, column c, l as in gpass256_kernel.
+// After the forward four-step each thread holds r_hat_q at the bins k1 + 16 k2 of its column; the
+// bins go to shared memory once so that thread q forms row q of the 3x3 block multiply
+// s_hat_q = sum_p G_qp r_hat_p (Eq B7 entry order) and its share of the Parseval partial.  The
+// (component, column) buffers use stride 274 (= 2 mod 8 in 16-byte units): a quarter warp (4
+// columns x 2 l) hits 8 distinct bank groups.  2 CTAs/SM (106 KB of smem each).
+constexpr int GE_COLS = 4, GE_CS = YR_R * (YR_R + 1) + 2;
+constexpr int gpass256e_smem = (3 * GE_COLS * GE_CS + 256) * 16 + 6 * 256 * GE_COLS * 8;
+template <int MODE>
+__global__ void __launch_bounds__(3 * GE_COLS * YR_R, 2) gpass256e_kernel(Ctx cx) {
+  constexpr int L = 256, R = YR_R, RP = R + 1;
+  const Geo g = cx.g;
+  const int load = blockIdx.y;
+  if (MODE == CG && !cx.st[load].active) return;
+  extern __shared__ double2 gsm[];
+  double2* buf = gsm;                                  // [3][GE_COLS][GE_CS]
+  double2* tw = buf + 3 * GE_COLS * GE_CS;             // [L]
+  double* gs = reinterpret_cast<double*>(tw + L);      // [6][L][GE_COLS] symbol of the tile's bins
+  __shared__ double red_sh[32];
+  const int t = threadIdx.x, c = t & (GE_COLS - 1), ln = (t >> 2) & (R - 1), q = t >> 6;
+  const int ntile_y = g.N2 / GE_COLS;
+  const int kx = blockIdx.x / ntile_y;
+  const int y0 = (blockIdx.x - kx * ntile_y) * GE_COLS;
+  const long long boff = (long long)kx * g.N3 * g.N2 + y0;
+  double2* col = cx.spec + ((long long)load * 3 + q) * g.nspec + boff + c;
+  const long long zs = g.N2;
+#pragma unroll
+  for (int i = 0; i < 6 * L * GE_COLS / (2 * 3 * GE_COLS * R); ++i) {  // 16-byte copies: 2 bins each
+    const int e = 2 * (t + i * 3 * GE_COLS * R);                     // e = (ent * L + kz) * 4 + cc
+    const int ent = e / (L * GE_COLS), kz = (e / GE_COLS) & (L - 1), cc = e & (GE_COLS - 1);
+    cp_async16(&gs[e], cx.gtab + ent * g.nspec + boff + (long long)kz * zs + cc);
+  }
+  cp_commit();
+  double2 v[R];
+#pragma unroll
+  for (int n2 = 0; n2 < R; ++n2) v[n2] = __ldcg(col + (ln + R * n2) * zs);
+  for (int i = t; i < L; i += 3 * GE_COLS * R) tw[i] = cx.tw.z[i];
+  __syncthreads();
+  double2* bc = buf + (q * GE_COLS + c) * GE_CS;
+  dft_reg<R, false>(v);  // thread = n1: DFT over n2 -> k1
+#pragma unroll
+  for (int k1 = 1; k1 < R; ++k1) v[k1] = cmul(v[k1], tw[(ln * k1) & (L - 1)]);
+#pragma unroll
+  for (int k1 = 0; k1 < R; ++k1) bc[k1 * RP + ln] = v[k1];
+  __syncthreads();
+#pragma unroll
+  for (int n1 = 0; n1 < R; ++n1) v[n1] = bc[ln * RP + n1];
+  dft_reg<R, false>(v);  // thread = k1: v[k2] = r_hat_q(kz = k1 + 16 k2)
+  __syncthreads();       // every stage-2 read of buf done
+#pragma unroll
+  for (int k2 = 0; k2 < R; ++k2) bc[k2 * RP + ln] = v[k2];
+  cp_wait<0>();
+  __syncthreads();
+  const double w = parseval_w(kx, g.M);
+  // row q of the block in Eq B7 order (v1=G11 v2=G22 v3=G12 v4=G33 v5=G23 v6=G13): the own
+  // component stays in registers, the other two (p1 = q+1, p2 = q+2 mod 3) come from smem
+  const int p1 = q == 2 ? 0 : q + 1, p2 = q == 0 ? 2 : q - 1;
+  const int eq = q == 0 ? 0 : (q == 1 ? 1 : 3);   // G_qq
+  const int e1 = q == 0 ? 2 : (q == 1 ? 4 : 5);   // G_q,p1: G12, G23, G31
+  const int e2 = q == 0 ? 5 : (q == 1 ? 2 : 4);   // G_q,p2: G13, G21, G32
+  const double2* b1 = buf + (p1 * GE_COLS + c) * GE_CS;
+  const double2* b2 = buf + (p2 * GE_COLS + c) * GE_CS;
+  const double* gq = gs + eq * L * GE_COLS + c;
+  const double* g1 = gs + e1 * L * GE_COLS + c;
+  const double* g2 = gs + e2 * L * GE_COLS + c;
+  double part = 0.0;
+#pragma unroll
+  for (int k2 = 0; k2 < R; ++k2) {
+    const int kz = (ln + R * k2) * GE_COLS;
+    const double2 X1 = b1[k2 * RP + ln], X2 = b2[k2 * RP + ln];
+    const double a = gq[kz], b = g1[kz], cc = g2[kz];
+    double2 Y;
+    Y.x = fma(a, v[k2].x, fma(b, X1.x, cc * X2.x));
+    Y.y = fma(a, v[k2].y, fma(b, X1.y, cc * X2.y));
+    part = fma(w, fma(v[k2].x, Y.x, v[k2].y * Y.y), part);
+    v[k2] = Y;
+  }
+  dft_reg<R, true>(v);  // inverse over k2 -> n1 (thread = k1)
+#pragma unroll
+  for (int n1 = 1; n1 < R; ++n1) v[n1] = cmul(v[n1], cconj(tw[(ln * n1) & (L - 1)]));
+  __syncthreads();  // every multiply read of buf done
+#pragma unroll
+  for (int n1 = 0; n1 < R; ++n1) bc[n1 * RP + ln] = v[n1];
+  __syncthreads();
+#pragma unroll
+  for (int k1 = 0; k1 < R; ++k1) v[k1] = bc[ln * RP + k1];
+  dft_reg<R, true>(v);  // thread = n1: inverse over k1 -> n2
+#pragma unroll
+  for (int n2 = 0; n2 < R; ++n2) __stcg(col + (ln + R * n2) * zs, v[n2]);
+  gamma_finish(cx, load, part, red_sh, MODE);
+}
+
 // G pass along y (contiguous rows): 2D grids (rows = kx) and the mixed-BC schedule (rows = (kx, m),
 // m the DST-I mode along z, P3 planes); tile = 8 consecutive rows.
 template <int L, int NC, int MODE>
@@ -2066,8 +2159,7 @@ int launch_scalar(const Ctx& cx, int slot, int mode, cudaStream_t s) {
   if (slot == RED_RNORM) {
     nblk = g.NB > 0 ? g.NA * g.N3 * g.c : (g.dirz ? g.c * g.N2 * (g.N1 / 16) : g.c * g.P3 * g.N2 / 8);
   } else if (slot == RED_GAMMA) {
-    nblk = g.NB > 0 ? g.H1 * g.NB
-                    : ((g.dim == 3 && !g.dirz) ? g.H1 * (g.N2 / 8) : (int)(((long long)g.H1 * g.P3 + 7) / 8));
+    nblk = gpass_nblk(g);
   } else {
     if (g.dim == 3 && g.c == 1) {
       const int TX = g.N1 < 32 ? g.N1 : 32, ZC = g.KZC;
@@ -2245,12 +2337,26 @@ int launch_ypass(const Ctx& cx, int mode, bool inverse, cudaStream_t s, int z0, 
   });
 }
 
-int launch_gpass(const Ctx& cx, int mode, cudaStream_t s) {
-  const Geo& g = cx.g;
+static bool gpass_rd() {
   static const bool rd = [] {
     const char* e = getenv("UNO_GRD");
     return !(e && e[0] == '0');
   }();
+  return rd;
+}
+static bool gpass_e256(const Geo& g) {
+  return gpass_rd() && g.dim == 3 && !g.dirz && g.c == 3 && g.N3 == 256 && g.N2 % GE_COLS == 0;
+}
+// CTAs of the CG-mode G pass = gamma partials per load
+int gpass_nblk(const Geo& g) {
+  if (g.NB > 0) return g.H1 * g.NB;
+  if (g.dim == 3 && !g.dirz) return g.H1 * (g.N2 / (gpass_e256(g) ? GE_COLS : 8));
+  return (int)(((long long)g.H1 * g.P3 + 7) / 8);
+}
+
+int launch_gpass(const Ctx& cx, int mode, cudaStream_t s) {
+  const Geo& g = cx.g;
+  const bool rd = gpass_rd();
   if (mode == FWDZ) {  // forward z FFT of the half spectrum (3D periodic; training features)
     if (g.dim != 3 || g.dirz || g.dir3) return -1;
     return dispatch_pow2(g.N3, [&](auto Lc) {
@@ -2278,6 +2384,17 @@ int launch_gpass(const Ctx& cx, int mode, cudaStream_t s) {
     } else {
       set_smem(gpass256_kernel<STANDALONE>, sm);
       gpass256_kernel<STANDALONE><<<grid, 8 * YR_R, sm, s>>>(cx);
+    }
+    return 1;
+  }
+  if (mode != FWDZ && gpass_e256(g)) {
+    const dim3 grid((unsigned)(g.H1 * (g.N2 / GE_COLS)), g.nrhs);
+    if (mode == CG) {
+      set_smem(gpass256e_kernel<CG>, gpass256e_smem);
+      gpass256e_kernel<CG><<<grid, 3 * GE_COLS * YR_R, gpass256e_smem, s>>>(cx);
+    } else {
+      set_smem(gpass256e_kernel<STANDALONE>, gpass256e_smem);
+      gpass256e_kernel<STANDALONE><<<grid, 3 * GE_COLS * YR_R, gpass256e_smem, s>>>(cx);
     }
     return 1;
   }
@@ -2466,7 +2583,7 @@ int launch_zero(double* x, long long n, cudaStream_t s) {
 
 int blocks_needed_max(const Geo& g) {
   long long m = (long long)g.c * g.N3 * g.N2 / 8;                // x passes
-  if (g.dim == 3) m = m > (long long)g.H1 * (g.N2 / 8) ? m : (long long)g.H1 * (g.N2 / 8);  // G pass
+  if (g.dim == 3) m = m > (long long)g.H1 * (g.N2 / 4) ? m : (long long)g.H1 * (g.N2 / 4);  // G pass
   else m = m > (g.H1 + 7) / 8 ? m : (g.H1 + 7) / 8;
   if (g.dirz) {  // DST pass grid
     const long long a = (long long)g.c * g.N2 * (g.N1 / 16);

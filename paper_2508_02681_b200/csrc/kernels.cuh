@@ -49,6 +49,7 @@ int launch_xinv(const Ctx& cx, int mode, double* dst, cudaStream_t s, int b0 = 0
 // z0/zc: only z in [z0, z0+zc) of every (comp, kx) plane (zc = 0: all; multiples of 8)
 int launch_ypass(const Ctx& cx, int mode, bool inverse, cudaStream_t s, int z0 = 0, int zc = 0);
 int launch_gpass(const Ctx& cx, int mode, cudaStream_t s);
+int gpass_nblk(const Geo& g);  // CTAs (gamma partials per load) of the CG-mode G pass
 // zc0/nzl: 3D thermal only, z-chunks [zc0, zc0+nzl) of g.KZC planes (nzl = 0: all)
 int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaStream_t s, int zc0 = 0, int nzl = 0);
 int launch_rhs(const Ctx& cx, const LoadParams& lp, double* f, cudaStream_t s);

@@ -614,3 +614,21 @@ def test_512_point_y_pass(N, physics):
     fx = homog.solve_problem(g, physics, ph, mat, load, seed, amp, fixed_iters=4)
     u = solver(ph, physics, mat, 1, seed, amp).solve(load, fixed_iters=4).u.cpu().numpy()[0]
     assert rel(u, fx["U"][0]) <= 1e-10
+
+
+@pytest.mark.parametrize("N", [(16, 16, 256), (16, 8, 256), (32, 32, 256)])
+def test_elastic_256_point_g_pass(N):
+    # the register-direct elastic G pass (N3 = 256, 4-column tiles): 3x3 block multiply, the
+    # Parseval gamma partial (through the solve) and a single-tile y extent
+    g, ph, mat, amp, seed = make_case(N, "elastic")
+    s = solver(ph, "elastic", mat, 2, seed, amp)
+    G = greens.ghat(g, "elastic", mat, seed, amp)
+    r = np.stack([synth.test_vector(93 + l, g.field_shape()) for l in range(2)])
+    z = s.apply_precond(torch.from_numpy(r).to(dev())).cpu().numpy()
+    for l in range(2):
+        assert rel(z[l], greens.apply_precond(G, r[l])) <= 5e-11  # long axis: see test_maximum_axis_lengths
+    load = loads_for("elastic", 3, 2)
+    fx = homog.solve_problem(g, "elastic", ph, mat, load, seed, amp, fixed_iters=4)
+    u = solver(ph, "elastic", mat, 2, seed, amp).solve(load, fixed_iters=4).u.cpu().numpy()
+    for l in range(2):
+        assert rel(u[l], fx["U"][l]) <= 1e-10
