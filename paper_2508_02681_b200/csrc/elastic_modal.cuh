@@ -143,5 +143,18 @@ __device__ __forceinline__ void wht8(double* v /* stride 3 */) {
       }
 }
 
+// The x and y stages of wht8 on the 4 corners of one node plane (stride 3).
+__device__ __forceinline__ void wht4(double* v) {
+#pragma unroll
+  for (int b = 1; b < 4; b <<= 1)
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+      if (!(a & b)) {
+        const double x = v[3 * a], y = v[3 * (a | b)];
+        v[3 * a] = x + y;
+        v[3 * (a | b)] = x - y;
+      }
+}
+
 }  // namespace modal
 }  // namespace uno

@@ -5,10 +5,12 @@
 // sparse modal operator (lam, mu of the element's phase), inverse WHT: ~240 flops instead of the
 // 576 FMAs of the dense 24x24 element matrix.  Node-centric gather without atomics: a CTA owns a
 // 16 x 8 node tile marching over z; each z step computes the 17 x 9 element layer above the
-// current node plane once (160 threads, one element each) into shared memory, split into the
-// lower-face outputs (consumed by this node plane) and the upper-face outputs (kept for the
-// next plane), and every node sums its 8 octant contributions.  d planes stream through a
-// 4-slot cp.async ring (planes k+2, k+3 in flight while layer k is computed).
+// current node plane once (160 threads, one element column each).  A thread keeps its element
+// column's upper corner values and upper-face outputs in registers for the next layer, so a layer
+// reads one node plane of the tile from shared memory and stores only the plane's combined outputs
+// (lower faces of this layer + upper faces of the previous one); every node then sums its 4 (x, y)
+// element columns.  d planes stream through a 4-slot cp.async ring (planes k+2, k+3 in flight while
+// layer k is computed).
 #include <cuda_runtime.h>
 
 #include "common.cuh"
@@ -26,7 +28,7 @@ constexpr int KM_PLANE = 3 * KM_DP;                 // doubles per ring slot (3 
 constexpr int KM_NCP = (KM_PLANE + KM_T - 1) / KM_T;  // cp.async per thread per plane
 
 __host__ __device__ constexpr int km_smem_bytes() {
-  return (KM_RING * KM_PLANE + 12 * KM_NE + 2 * 12 * KM_NE) * (int)sizeof(double);
+  return (KM_RING * KM_PLANE + 12 * KM_NE) * (int)sizeof(double);
 }
 
 __global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int mode, const double* __restrict__ src,
@@ -39,8 +41,7 @@ __global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int
   const int dz = g.dirz;
   extern __shared__ double kms[];
   double* D = kms;                           // [RING][3][10][18]
-  double* Lb = D + KM_RING * KM_PLANE;       // [12][NE] lower-face outputs of the current layer
-  double* Ub = Lb + 12 * KM_NE;              // [2][12][NE] upper-face outputs (ping-pong)
+  double* Lb = D + KM_RING * KM_PLANE;       // [12][NE] node-plane outputs of the current layer
   __shared__ double red_sh[32];
   const int t = threadIdx.x;
   const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
@@ -87,37 +88,56 @@ __global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int
                      : "memory");
     }
   };
-  // element owned by this thread in every layer
+  // element column owned by this thread: the plane-(k+1) corner values (uc) and the upper-face
+  // outputs (vc) of layer k stay in registers for layer k+1, so a layer reads one node plane from
+  // smem and writes only the combined lower-face outputs Lb = v_lower(k) + v_upper(k-1).
   const bool eth = t < KM_NE;
   const int exl = eth ? t % KM_EW : 0, eyl = eth ? t / KM_EW : 0;
   const long long pbase = (long long)((y0 - 1 + eyl + N2) & (N2 - 1)) * N1 + ((x0 - 1 + exl + N1) & (N1 - 1));
-  auto element_layer = [&](int k, double* Uout, bool want_lower) {  // element layer between node planes k, k+1
+  // uc = 2D (x, y) Walsh-Hadamard modes of the plane-(k+1) corners, vc = the upper-face output
+  // modes of layer k: the 8-point WHT of a layer is the z butterfly of its two planes' 2D modes
+  // (the x and y butterflies of a shared node plane are done once), and the output plane k is one
+  // 2D inverse of (lower-face modes of layer k + upper-face modes of layer k-1).
+  double uc[12], vc[12];
+  auto read_corners = [&](int p, double* dstv) {  // the 4 (x, y) corners of node plane p
+    const double* Dp = D + slot_of(p) * KM_PLANE + eyl * KM_DW + exl;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int al = 0; al < 3; ++al) dstv[3 * a + al] = Dp[al * KM_DP + ((a >> 1) & 1) * KM_DW + (a & 1)];
+  };
+  auto element_layer = [&](int k, bool want_lower) {  // element layer between node planes k, k+1
     if (!eth) return;
     const int layer = dz ? k : ((k + N3) & (N3 - 1));
     const bool ph = __ldg(cx.phase + (long long)layer * plane + pbase) != 0;
     const double ls = ph ? l1 : l0, ms = ph ? m1 : m0;
-    double u[24];
+    double w[12];
+    read_corners(k + 1, w);
 #pragma unroll
-    for (int a = 0; a < 8; ++a) {
-      const double* Dp = D + slot_of(k + ((a >> 2) & 1)) * KM_PLANE + (eyl + ((a >> 1) & 1)) * KM_DW + exl + (a & 1);
+    for (int al = 0; al < 3; ++al) modal::wht4(w + al);
+    double u[24];  // modes m (z bit clear) = lower + upper, m | 4 = lower - upper
 #pragma unroll
-      for (int al = 0; al < 3; ++al) u[3 * a + al] = Dp[al * KM_DP];
+    for (int i = 0; i < 12; ++i) {
+      u[i] = uc[i] + w[i];
+      u[12 + i] = uc[i] - w[i];
+      uc[i] = w[i];
     }
-#pragma unroll
-    for (int al = 0; al < 3; ++al) modal::wht8(u + al);
     double v[24];
 #pragma unroll
     for (int i = 0; i < 24; ++i) v[i] = 0.0;
     modal::modal_apply<3>(v, u, ls, ms);  // rows of mode 0 are zero
+    double o[12];
 #pragma unroll
-    for (int al = 0; al < 3; ++al) modal::wht8(v + al);
+    for (int i = 0; i < 12; ++i) {
+      o[i] = (v[i] + v[12 + i]) + vc[i];
+      vc[i] = v[i] - v[12 + i];
+    }
+    if (want_lower) {
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+      for (int al = 0; al < 3; ++al) modal::wht4(o + al);
 #pragma unroll
-      for (int al = 0; al < 3; ++al) {
-        if (want_lower) Lb[(3 * a + al) * KM_NE + t] = v[3 * a + al];
-        Uout[(3 * a + al) * KM_NE + t] = v[3 * (a + 4) + al];
-      }
+      for (int i = 0; i < 12; ++i) Lb[i * KM_NE + t] = o[i];
+    }
   };
   // prologue: planes zs-1 .. zs+2 in flight; element layer zs-1 (its upper faces feed plane zs)
 #pragma unroll 1
@@ -127,7 +147,14 @@ __global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int
   }
   cp_wait<2>();  // planes zs-1, zs
   __syncthreads();
-  element_layer(zs - 1, Ub + ((zs - 1) & 1) * 12 * KM_NE, false);
+  if (eth) {
+    read_corners(zs - 1, uc);
+#pragma unroll
+    for (int al = 0; al < 3; ++al) modal::wht4(uc + al);
+  }
+#pragma unroll
+  for (int i = 0; i < 12; ++i) vc[i] = 0.0;
+  element_layer(zs - 1, false);
   const bool nth = t < KM_TX * KM_TY;
   const int tx = t % KM_TX, ty = t / KM_TX;
   double part = 0.0;
@@ -138,18 +165,17 @@ __global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int
     // refill the slot of plane k-1 only now: every thread has left step k-1 (its node phase read it)
     if (k + 3 <= ze) issue_plane(k + 3);
     cp_commit();
-    element_layer(k, Ub + (k & 1) * 12 * KM_NE, true);
+    element_layer(k, true);
     __syncthreads();
     if (nth) {
-      const double* Up = Ub + ((k - 1) & 1) * 12 * KM_NE;
       double p[3] = {0.0, 0.0, 0.0};
 #pragma unroll
       for (int o = 0; o < 4; ++o) {
         const int ox = o & 1, oy = o >> 1;
         const int e = (ty + oy) * KM_EW + tx + ox;
-        const int a = (1 - ox) + 2 * (1 - oy);  // the node's corner in both element layers
+        const int a = (1 - ox) + 2 * (1 - oy);  // the node's corner in the element
 #pragma unroll
-        for (int al = 0; al < 3; ++al) p[al] += Lb[(3 * a + al) * KM_NE + e] + Up[(3 * a + al) * KM_NE + e];
+        for (int al = 0; al < 3; ++al) p[al] += Lb[(3 * a + al) * KM_NE + e];
       }
       const double* Dc = D + slot_of(k) * KM_PLANE + (ty + 1) * KM_DW + tx + 1;
       const long long gi = (long long)(k - dz - g.zlo) * plane + (long long)(y0 + ty) * N1 + x0 + tx;
