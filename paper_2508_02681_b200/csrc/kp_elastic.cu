@@ -106,10 +106,16 @@ __global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int
 #pragma unroll
       for (int al = 0; al < 3; ++al) dstv[3 * a + al] = Dp[al * KM_DP + ((a >> 1) & 1) * KM_DW + (a & 1)];
   };
-  auto element_layer = [&](int k, bool want_lower) {  // element layer between node planes k, k+1
-    if (!eth) return;
+  // phase of element layer k (1 byte, read one layer ahead so its latency hides behind a layer)
+  auto phase_of = [&](int k) -> bool {
     const int layer = dz ? k : ((k + N3) & (N3 - 1));
-    const bool ph = __ldg(cx.phase + (long long)layer * plane + pbase) != 0;
+    return eth && __ldg(cx.phase + (long long)layer * plane + pbase) != 0;
+  };
+  bool phc = phase_of(zs - 1);
+  auto element_layer = [&](int k, bool want_lower) {  // element layer between node planes k, k+1
+    const bool ph = phc;
+    phc = phase_of(k + 1);
+    if (!eth) return;
     const double ls = ph ? l1 : l0, ms = ph ? m1 : m0;
     double w[12];
     read_corners(k + 1, w);
