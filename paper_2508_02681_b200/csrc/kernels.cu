@@ -761,6 +761,92 @@ __global__ void __launch_bounds__(3 * GE_COLS * YR_R, 2) gpass256e_kernel(Ctx cx
   gamma_finish(cx, load, part, red_sh, MODE);
 }
 
+// Thermal G pass for N3 = 512, register-direct four-step 512 = 32 x 16 along z (the z analogue of
+// ypass512_kernel): tile = 4 consecutive y columns of one kx plane, thread (n1, c) = ((t >> 2) & 31,
+// t & 3), so a warp loads 64-byte segments of 8 z rows.  Forward: DFT16 over n2 -> twiddle ->
+// transpose -> DFT32 over n1 split between thread pairs (dft_half: thread h gets the bins
+// k1 + 16 (2m + h)), where s_hat = G_hat r_hat and the Parseval partial are formed; the inverse
+// mirrors it.  Every shared-memory pattern is conflict-free for a quarter warp (4 columns x 2
+// threads): column buffers 546 apart (= 2 mod 8 in 16-byte units), k1-major rows of 34, and the
+// final n1-major transpose swizzled as k1 ^ (n1 & 1).  (An elastic variant — 3 components x 4
+// columns, 1 CTA/SM — measured 4.08 ms vs 3.67 ms for gpass_z_kernel at 512^3 and was dropped.)
+constexpr int G5_CS = 546, G5_C = 4, G5_T = 32 * G5_C;
+constexpr int gpass512_smem = (G5_C * G5_CS + 16 * 32 + 16) * 16 + 512 * G5_C * 8;
+template <int MODE>
+__global__ void __launch_bounds__(G5_T, 3) gpass512_kernel(Ctx cx) {
+  constexpr int L = 512;
+  const Geo g = cx.g;
+  const int load = blockIdx.y;
+  if (MODE == CG && !cx.st[load].active) return;
+  extern __shared__ double2 gsm[];
+  double2* buf = gsm;                                  // [G5_C][G5_CS]
+  double2* tw = buf + G5_C * G5_CS;                    // [k1][n1] = w_512^{k1 n1}
+  double2* tw32 = tw + 16 * 32;                        // w_32^r
+  double* gs = reinterpret_cast<double*>(tw32 + 16);   // [L][G5_C] symbol of the tile's bins
+  __shared__ double red_sh[32];
+  const int t = threadIdx.x, c = t & (G5_C - 1), l32 = t >> 2;
+  const int ntile_y = g.N2 / G5_C;
+  const int kx = blockIdx.x / ntile_y;
+  const int y0 = (blockIdx.x - kx * ntile_y) * G5_C;
+  const long long boff = (long long)kx * g.N3 * g.N2 + y0;
+  double2* col = cx.spec + (long long)load * g.nspec + boff + c;
+  const long long zs = g.N2;
+#pragma unroll
+  for (int i0 = 0; i0 < L * G5_C / 2; i0 += G5_T) {  // 16-byte copies: 2 columns of one kz
+    const int i = i0 + t;
+    cp_async16(&gs[2 * i], cx.gtab + boff + (long long)(i >> 1) * zs + 2 * (i & 1));
+  }
+  cp_commit();
+  double2 v[16];
+#pragma unroll
+  for (int n2 = 0; n2 < 16; ++n2) v[n2] = __ldcg(col + (l32 + 32 * n2) * zs);
+  for (int i = t; i < 16 * 32; i += G5_T) tw[i] = cx.tw.z[((i & 31) * (i >> 5)) & (L - 1)];
+  if (t < 16) tw32[t] = cx.tw.z[16 * t];
+  __syncthreads();
+  double2* B = buf + c * G5_CS;
+  dft_reg<16, false>(v);  // thread = n1: over n2 -> k1
+#pragma unroll
+  for (int k1 = 1; k1 < 16; ++k1) v[k1] = cmul(v[k1], tw[k1 * 32 + l32]);
+#pragma unroll
+  for (int k1 = 0; k1 < 16; ++k1) B[k1 * 34 + l32] = v[k1];
+  __syncthreads();
+  const int k1 = l32 >> 1, h = l32 & 1;
+  double2 o[16];
+  {
+    double2 a[32];
+#pragma unroll
+    for (int n1 = 0; n1 < 32; ++n1) a[n1] = B[k1 * 34 + n1];
+    dft_half<32, false>(a, h, tw32, o);  // o[m] = r_hat(kz = k1 + 16 (2m + h))
+  }
+  const double w = parseval_w(kx, g.M);
+  double part = 0.0;
+  cp_wait<0>();
+  __syncthreads();  // symbol landed; every stage-2 read of B done
+#pragma unroll
+  for (int m = 0; m < 16; ++m) part += gmul_vals<1>(&o[m], gs + c, 0, (long long)(k1 + 16 * (2 * m + h)) * G5_C, w);
+#pragma unroll
+  for (int m = 0; m < 16; ++m) B[k1 * 34 + 2 * m + h] = o[m];
+  __syncthreads();
+  {
+    double2 a[32];
+#pragma unroll
+    for (int k2 = 0; k2 < 32; ++k2) a[k2] = B[k1 * 34 + k2];
+    dft_half<32, true>(a, h, tw32, o);  // o[m] = x(n1 = 2m + h) of this k1
+  }
+  __syncthreads();  // every read of B done before the transposed writes
+#pragma unroll
+  for (int m = 0; m < 16; ++m) B[(2 * m + h) * 16 + (k1 ^ h)] = o[m];
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = B[l32 * 16 + (j ^ (l32 & 1))];
+#pragma unroll
+  for (int j = 1; j < 16; ++j) v[j] = cmul(v[j], cconj(tw[j * 32 + l32]));
+  dft_reg<16, true>(v);  // thread = n1: over k1 -> n2
+#pragma unroll
+  for (int n2 = 0; n2 < 16; ++n2) __stcg(col + (l32 + 32 * n2) * zs, v[n2]);
+  gamma_finish(cx, load, part, red_sh, MODE);
+}
+
 // G pass along y (contiguous rows): 2D grids (rows = kx) and the mixed-BC schedule (rows = (kx, m),
 // m the DST-I mode along z, P3 planes); tile = 8 consecutive rows.
 template <int L, int NC, int MODE>
@@ -2347,10 +2433,13 @@ static bool gpass_rd() {
 static bool gpass_e256(const Geo& g) {
   return gpass_rd() && g.dim == 3 && !g.dirz && g.c == 3 && g.N3 == 256 && g.N2 % GE_COLS == 0;
 }
+static bool gpass_512(const Geo& g) {
+  return gpass_rd() && g.dim == 3 && !g.dirz && g.c == 1 && g.N3 == 512 && g.N2 % G5_C == 0;
+}
 // CTAs of the CG-mode G pass = gamma partials per load
 int gpass_nblk(const Geo& g) {
   if (g.NB > 0) return g.H1 * g.NB;
-  if (g.dim == 3 && !g.dirz) return g.H1 * (g.N2 / (gpass_e256(g) ? GE_COLS : 8));
+  if (g.dim == 3 && !g.dirz) return g.H1 * (g.N2 / (gpass_512(g) ? G5_C : (gpass_e256(g) ? GE_COLS : 8)));
   return (int)(((long long)g.H1 * g.P3 + 7) / 8);
 }
 
@@ -2384,6 +2473,17 @@ int launch_gpass(const Ctx& cx, int mode, cudaStream_t s) {
     } else {
       set_smem(gpass256_kernel<STANDALONE>, sm);
       gpass256_kernel<STANDALONE><<<grid, 8 * YR_R, sm, s>>>(cx);
+    }
+    return 1;
+  }
+  if (mode != FWDZ && gpass_512(g)) {
+    const dim3 grid((unsigned)(g.H1 * (g.N2 / G5_C)), g.nrhs);
+    if (mode == CG) {
+      set_smem(gpass512_kernel<CG>, gpass512_smem);
+      gpass512_kernel<CG><<<grid, G5_T, gpass512_smem, s>>>(cx);
+    } else {
+      set_smem(gpass512_kernel<STANDALONE>, gpass512_smem);
+      gpass512_kernel<STANDALONE><<<grid, G5_T, gpass512_smem, s>>>(cx);
     }
     return 1;
   }

@@ -632,3 +632,26 @@ def test_elastic_256_point_g_pass(N):
     u = solver(ph, "elastic", mat, 2, seed, amp).solve(load, fixed_iters=4).u.cpu().numpy()
     for l in range(2):
         assert rel(u[l], fx["U"][l]) <= 1e-10
+
+
+@pytest.mark.parametrize("N,physics", [((16, 8, 512), "thermal"), ((16, 8, 512), "elastic"), ((16, 16, 512), "elastic"),
+                                       ((32, 16, 512), "thermal")])
+def test_512_point_g_pass(N, physics):
+    # N3 = 512 (config 4's length): the register-direct thermal z pass (4-column tiles, pair-split
+    # DFT32) and the tiled elastic z pass; symbol multiply, Parseval gamma
+    g, ph, mat, amp, seed = make_case(N, physics)
+    s = solver(ph, physics, mat, 2, seed, amp)
+    G = greens.ghat(g, physics, mat, seed, amp)
+    r = np.stack([synth.test_vector(95 + l, g.field_shape()) for l in range(2)])
+    z, rz = s.apply_precond(torch.from_numpy(r).to(dev()), want_dot=True)
+    z = z.cpu().numpy()
+    tol = 1e-11 if physics == "thermal" else 5e-11  # long axis: see test_maximum_axis_lengths
+    for l in range(2):
+        ref = greens.apply_precond(G, r[l])
+        assert rel(z[l], ref) <= tol
+        assert abs(rz[l] - np.sum(r[l] * ref)) <= tol * abs(np.sum(r[l] * ref))
+    load = loads_for(physics, 3, 2)
+    fx = homog.solve_problem(g, physics, ph, mat, load, seed, amp, fixed_iters=4)
+    u = solver(ph, physics, mat, 2, seed, amp).solve(load, fixed_iters=4).u.cpu().numpy()
+    for l in range(2):
+        assert rel(u[l], fx["U"][l]) <= 1e-10
