@@ -655,3 +655,21 @@ def test_512_point_g_pass(N, physics):
     u = solver(ph, physics, mat, 2, seed, amp).solve(load, fixed_iters=4).u.cpu().numpy()
     for l in range(2):
         assert rel(u[l], fx["U"][l]) <= 1e-10
+
+
+@pytest.mark.parametrize("N,physics", [((64, 64, 256), "elastic"), ((32, 32, 512), "thermal"), ((32, 512, 16), "thermal"),
+                                       ((128, 64, 64), "elastic"), ((256, 64, 64), "thermal")])
+def test_repeat_bitwise_deterministic(N, physics):
+    # compute-sanitizer is unavailable on the GPU pool: a shared-memory race in the tiled kernels
+    # (z-carried elastic K, gpass256e / gpass512 / ypass512, the thermal K ring) would show up as
+    # run-to-run differences, so K, the preconditioner and their dots must repeat bit for bit
+    g, ph, mat, amp, seed = make_case(N, physics)
+    s = solver(ph, physics, mat, 2, seed, amp)
+    x = torch.from_numpy(np.stack([synth.test_vector(97 + l, g.field_shape()) for l in range(2)])).to(dev())
+    K0, dk0 = s.apply_K(x, want_dot=True)
+    z0, rz0 = s.apply_precond(x, want_dot=True)
+    for _ in range(4):
+        K1, dk1 = s.apply_K(x, want_dot=True)
+        z1, rz1 = s.apply_precond(x, want_dot=True)
+        assert torch.equal(K0, K1) and torch.equal(z0, z1)
+        assert list(dk0) == list(dk1) and list(rz0) == list(rz1)
