@@ -196,6 +196,26 @@ UNO_API uno_status uno_cg_train_install(uno_cg_handle* h, int32_t M, const doubl
  * of library kernels it launched.                                                       */
 UNO_API uno_status uno_cg_last_solve_stats(uno_cg_handle* h, double* ms, int64_t* kernel_launches);
 
+/* PCG coefficients of the most recent uno_cg_solve for load case `load`: gamma_1 (= r.s,
+ * Alg 2 l.7) and alpha (= gamma_1 / d.p, l.10) of iterations 1..m, recorded on the device by
+ * the scalar kernels.  *m_out = m (iterations run); min(m, cap) entries are written to each
+ * host array [cap].  UNO_ERR_ARG: null handle / m_out, load outside [0, nrhs), cap < 0, or
+ * cap > 0 with a null array.                                                               */
+UNO_API uno_status uno_cg_last_coefficients(uno_cg_handle* h, int32_t load, int32_t cap, double* h_gamma,
+                                            double* h_alpha, int32_t* m_out);
+
+/* Spectral estimate of the preconditioned operator P A from the most recent solve (PAPER.md
+ * Tab 4 columns): the PCG coefficients define the Lanczos tridiagonal T_m of P A,
+ *   T[0][0] = 1/alpha_0,  T[j][j] = 1/alpha_j + beta_{j-1}/alpha_{j-1},
+ *   T[j][j+1] = T[j+1][j] = sqrt(beta_j)/alpha_j,  beta_j = gamma_{j+1}/gamma_j,
+ * whose extreme eigenvalues (host Sturm-sequence bisection) estimate lambda_min / lambda_max
+ * of P A from inside (Ritz values).  h_out[5] = {lambda_min, lambda_max, cond_2 = lambda_max /
+ * lambda_min, C_CG = (sqrt(cond) - 1)/(sqrt(cond) + 1) (Eq 27), N_iter_est =
+ * ln(tol/2)/ln(C_CG) (the Eq 27 bound 2 C^m <= tol, un-rounded; 1 if C_CG <= 0)}; *m_out = m.
+ * UNO_ERR_ARG: null pointers, load outside [0, nrhs), tol outside (0, 1), or no iteration
+ * recorded (m = 0).                                                                        */
+UNO_API uno_status uno_cg_spectrum(uno_cg_handle* h, int32_t load, double tol, double* h_out, int32_t* m_out);
+
 /* Kernel-level timing hook for bench.py: per-kernel-class accumulated device time (ms)
  * and launch counts since create or the last reset, measured with CUDA events on
  * desc.stream when enabled (adds an event pair per launch; off by default).

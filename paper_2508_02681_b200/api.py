@@ -131,6 +131,14 @@ class UnoCG:
         ms, n = B.uno_cg_last_solve_stats(self.handle)
         return SolveResult(u, reps, hh, ms, n)
 
+    def coefficients(self, load: int = 0):
+        """(gamma_1, alpha) per PCG iteration of the last solve (Alg 2 l.7, l.10)."""
+        return B.uno_cg_last_coefficients(self.handle, load)
+
+    def spectrum(self, load: int = 0, tol: float = 1e-8) -> dict:
+        """Tab 4 columns (lambda_min/max of P A, cond, C_CG, N_iter_est) of the last solve."""
+        return B.uno_cg_spectrum(self.handle, load, tol)
+
     def effective_property(self, u: torch.Tensor, loads) -> np.ndarray:
         return B.uno_cg_effective_property(self.handle, u.contiguous(), loads, self.nrhs)
 

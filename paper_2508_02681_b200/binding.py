@@ -23,6 +23,7 @@ UNO_THERMAL, UNO_ELASTIC = 0, 1
 EXPORTS = ("uno_cg_create", "uno_cg_destroy", "uno_cg_update", "uno_cg_rhs", "uno_cg_apply_K", "uno_cg_apply_precond",
            "uno_cg_solve", "uno_cg_effective_property", "uno_cg_set_preconditioner", "uno_cg_train_features",
            "uno_cg_train_pairs", "uno_cg_train_newton", "uno_cg_train_install", "uno_cg_last_solve_stats",
+           "uno_cg_last_coefficients", "uno_cg_spectrum",
            "uno_cg_kernel_timing", "uno_cg_last_error", "uno_cg_version")
 UNO_PRECOND = {"uno": 0, "identity": 1, "jacobi": 2}
 # include/uno_cg_slab.h (z-slab decomposition)
@@ -68,6 +69,8 @@ def _load():
     lib.uno_cg_train_newton.argtypes = [P, P, I32, I32, P, P, P]
     lib.uno_cg_train_install.argtypes = [P, I32, P, P]
     lib.uno_cg_kernel_timing.argtypes = [P, I32, I32, P, P]
+    lib.uno_cg_last_coefficients.argtypes = [P, I32, I32, P, P, C.POINTER(I32)]
+    lib.uno_cg_spectrum.argtypes = [P, I32, D, P, C.POINTER(I32)]
     lib.uno_slab_create.argtypes = [C.POINTER(UnoCgDesc), I32, I32, P, C.POINTER(P)]
     lib.uno_slab_destroy.argtypes = [P]
     lib.uno_slab_sizes.argtypes = [P, P]
@@ -202,6 +205,27 @@ def uno_cg_last_solve_stats(h: int):
     n = C.c_int64()
     _check(_lib.uno_cg_last_solve_stats(h, C.byref(ms), C.byref(n)), "uno_cg_last_solve_stats")
     return ms.value, n.value
+
+
+def uno_cg_last_coefficients(h: int, load: int, cap: int = 100000):
+    """(gamma_1, alpha) per iteration of the last solve for load case `load` (numpy arrays)."""
+    g = np.zeros(max(cap, 1))
+    a = np.zeros(max(cap, 1))
+    m = C.c_int32()
+    _check(_lib.uno_cg_last_coefficients(h, int(load), int(cap), _ptr(g), _ptr(a), C.byref(m)),
+           "uno_cg_last_coefficients")
+    n = min(m.value, cap)
+    return g[:n].copy(), a[:n].copy()
+
+
+def uno_cg_spectrum(h: int, load: int, tol: float = 1e-8):
+    """Tab 4 columns from the last solve's Lanczos tridiagonal: dict of lambda_min, lambda_max,
+    cond, C_CG, N_iter_est and m (iterations)."""
+    out = np.zeros(5)
+    m = C.c_int32()
+    _check(_lib.uno_cg_spectrum(h, int(load), float(tol), _ptr(out), C.byref(m)), "uno_cg_spectrum")
+    return {"lambda_min": out[0], "lambda_max": out[1], "cond": out[2], "C_CG": out[3], "N_iter_est": out[4],
+            "m": m.value}
 
 
 def uno_cg_kernel_timing(h: int, enable: int = -1, reset: int = 0):

@@ -51,8 +51,15 @@ static __device__ void scalar_after_rnorm(LoadState* st, double rn, double* hist
   if (hist && it < hist_stride) hist[(long long)load * hist_stride + it] = st->r0 > 0 ? rn / st->r0 : 0.0;
 }
 
+// Per-iteration coefficient record of the solve (hist planes: 0 ||r||_inf / ||r0||_inf, 1 gamma_1,
+// 2 alpha; [plane][kMaxRhs][hist_stride]) — the PCG-Lanczos tridiagonal of uno_cg_spectrum.
+__device__ __forceinline__ void record_coef(double* hist, int hist_stride, int plane, int load, int it, double v) {
+  if (hist && it < hist_stride) hist[((long long)plane * kMaxRhs + load) * hist_stride + it] = v;
+}
+
 // G-pass last CTA: gamma_0 <- gamma_1 ; gamma_1 <- r.s ; beta = gamma_1 / gamma_0 (Alg 2 l.7-8).
-static __device__ void scalar_after_gamma(LoadState* st, double g1) {
+static __device__ void scalar_after_gamma(LoadState* st, double g1, double* hist = nullptr, int hist_stride = 0,
+                                          int load = 0) {
   if (!isfinite(g1)) {
     st->status = ST_NONFINITE;
     st->active = 0;
@@ -67,10 +74,12 @@ static __device__ void scalar_after_gamma(LoadState* st, double g1) {
   st->gamma0 = g0;
   st->gamma1 = g1;
   st->beta = st->iters == 0 ? 0.0 : g1 / g0;
+  record_coef(hist, hist_stride, 1, load, st->iters, g1);
 }
 
 // K last CTA: alpha = gamma_1 / (d.p) (Alg 2 l.10).
-static __device__ void scalar_after_dp(LoadState* st, double dp) {
+static __device__ void scalar_after_dp(LoadState* st, double dp, double* hist = nullptr, int hist_stride = 0,
+                                       int load = 0) {
   st->dp = dp;
   if (!isfinite(dp)) {
     st->status = ST_NONFINITE;
@@ -85,6 +94,7 @@ static __device__ void scalar_after_dp(LoadState* st, double dp) {
     return;
   }
   st->alpha = st->gamma1 / dp;
+  record_coef(hist, hist_stride, 2, load, st->iters, st->alpha);
   st->iters += 1;
   st->pending_u = 1;
 }

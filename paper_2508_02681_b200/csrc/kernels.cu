@@ -2231,8 +2231,8 @@ __global__ void __launch_bounds__(SC_T) scalar_kernel(Ctx cx, int slot, int nblk
   if (threadIdx.x == 0) {
     if (mode == CG) {
       if (slot == RED_RNORM) scalar_after_rnorm(st, tot, cx.hist, cx.hist_stride, load);
-      else if (slot == RED_GAMMA) scalar_after_gamma(st, tot);
-      else scalar_after_dp(st, tot);
+      else if (slot == RED_GAMMA) scalar_after_gamma(st, tot, cx.hist, cx.hist_stride, load);
+      else scalar_after_dp(st, tot, cx.hist, cx.hist_stride, load);
     } else {
       cx.sc.results[slot * kMaxRhs + load] = tot;
     }

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <limits>
 #include <string>
 #include <vector>
 
@@ -802,11 +803,11 @@ extern "C" uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, doub
   cudaStream_t s = h->stream;
   long long launches = 0;
   const int cap = fixed_iters > 0 ? fixed_iters : max_iter;
-  // residual history buffer
-  if (h_hist && h->hist_stride < cap + 1) {
+  // per-iteration record: residual history, gamma_1, alpha (planes of kMaxRhs x (cap + 1))
+  if (h->hist_stride < cap + 1) {
     if (h->hist) cudaFreeAsync(h->hist, s);
     h->hist = nullptr;
-    CK(cudaMallocAsync(&h->hist, (size_t)kMaxRhs * (cap + 1) * 8, s));
+    CK(cudaMallocAsync(&h->hist, (size_t)3 * kMaxRhs * (cap + 1) * 8, s));
     h->hist_stride = cap + 1;
     h->cx = make_ctx(h);
     if (h->gexec) {
@@ -956,6 +957,97 @@ extern "C" uno_status uno_cg_effective_property(uno_cg_handle* h, const double* 
       }
       h_out[i * nl + j] = base - h->h_small[i * nl + j] / vol;
     }
+  return UNO_OK;
+}
+
+// ------------------------------------------------------------------ PCG coefficients / spectrum
+static uno_status read_coefficients(uno_cg_handle* h, int load, std::vector<double>& gam, std::vector<double>& alp) {
+  const int m = h->hist ? std::min(h->h_st[load].iters, h->hist_stride) : 0;
+  gam.assign(m, 0.0);
+  alp.assign(m, 0.0);
+  if (m > 0) {
+    CK(cudaMemcpy(gam.data(), h->hist + ((long long)1 * kMaxRhs + load) * h->hist_stride, (size_t)m * 8,
+                  cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(alp.data(), h->hist + ((long long)2 * kMaxRhs + load) * h->hist_stride, (size_t)m * 8,
+                  cudaMemcpyDeviceToHost));
+  }
+  return UNO_OK;
+}
+
+extern "C" uno_status uno_cg_last_coefficients(uno_cg_handle* h, int32_t load, int32_t cap, double* h_gamma,
+                                               double* h_alpha, int32_t* m_out) {
+  if (!h || !m_out || load < 0 || load >= h->g.nrhs || cap < 0 || (cap > 0 && (!h_gamma || !h_alpha)))
+    return fail(UNO_ERR_ARG, "null pointer, load out of range or cap < 0");
+  std::vector<double> gam, alp;
+  const uno_status e = read_coefficients(h, load, gam, alp);
+  if (e != UNO_OK) return e;
+  *m_out = (int32_t)gam.size();
+  for (int i = 0; i < (int)gam.size() && i < cap; ++i) {
+    h_gamma[i] = gam[i];
+    h_alpha[i] = alp[i];
+  }
+  return UNO_OK;
+}
+
+// number of eigenvalues of the symmetric tridiagonal (d, e) below x (Sturm sequence of the LDL^T
+// pivots; a zero pivot is replaced by -pivmin)
+static int sturm_count(const std::vector<double>& d, const std::vector<double>& e, double x, double pivmin) {
+  int c = 0;
+  double q = 1.0;
+  for (size_t i = 0; i < d.size(); ++i) {
+    q = (d[i] - x) - (i > 0 ? e[i - 1] * e[i - 1] / q : 0.0);
+    if (std::fabs(q) < pivmin) q = -pivmin;
+    if (q < 0) ++c;
+  }
+  return c;
+}
+
+// k-th smallest eigenvalue (k = 1 .. n) by bisection inside the Gershgorin interval
+static double tridiag_eig(const std::vector<double>& d, const std::vector<double>& e, int k) {
+  const int n = (int)d.size();
+  double lo = d[0], hi = d[0], scale = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double r = (i > 0 ? std::fabs(e[i - 1]) : 0.0) + (i + 1 < n ? std::fabs(e[i]) : 0.0);
+    lo = std::min(lo, d[i] - r);
+    hi = std::max(hi, d[i] + r);
+    scale = std::max(scale, std::fabs(d[i]) + r);
+  }
+  const double pivmin = std::numeric_limits<double>::min() * std::max(1.0, scale * scale);
+  lo -= 1e-15 * scale;
+  hi += 1e-15 * scale;
+  for (int it = 0; it < 200 && hi - lo > 2e-16 * std::max(std::fabs(lo), std::fabs(hi)); ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (sturm_count(d, e, mid, pivmin) >= k) hi = mid;
+    else lo = mid;
+  }
+  return 0.5 * (lo + hi);
+}
+
+extern "C" uno_status uno_cg_spectrum(uno_cg_handle* h, int32_t load, double tol, double* h_out, int32_t* m_out) {
+  if (!h || !h_out || !m_out || load < 0 || load >= h->g.nrhs || !(tol > 0 && tol < 1))
+    return fail(UNO_ERR_ARG, "null pointer, load out of range or tol outside (0, 1)");
+  std::vector<double> gam, alp;
+  const uno_status e = read_coefficients(h, load, gam, alp);
+  if (e != UNO_OK) return e;
+  const int m = (int)gam.size();
+  *m_out = m;
+  if (m == 0) return fail(UNO_ERR_ARG, "no PCG iteration recorded for this load");
+  // Lanczos tridiagonal of P A from the CG coefficients
+  std::vector<double> d(m), off(m > 1 ? m - 1 : 0);
+  for (int j = 0; j < m; ++j) {
+    d[j] = 1.0 / alp[j];
+    if (j > 0) d[j] += (gam[j] / gam[j - 1]) / alp[j - 1];
+    if (j + 1 < m) off[j] = std::sqrt(gam[j + 1] / gam[j]) / alp[j];
+  }
+  const double lmin = tridiag_eig(d, off, 1), lmax = tridiag_eig(d, off, m);
+  const double cond = lmax / lmin;
+  const double sq = std::sqrt(cond);
+  const double C = (sq - 1.0) / (sq + 1.0);
+  h_out[0] = lmin;
+  h_out[1] = lmax;
+  h_out[2] = cond;
+  h_out[3] = C;
+  h_out[4] = C > 0 ? std::log(tol / 2.0) / std::log(C) : 1.0;
   return UNO_OK;
 }
 

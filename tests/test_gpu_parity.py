@@ -673,3 +673,36 @@ def test_repeat_bitwise_deterministic(N, physics):
         z1, rz1 = s.apply_precond(x, want_dot=True)
         assert torch.equal(K0, K1) and torch.equal(z0, z1)
         assert list(dk0) == list(dk1) and list(rz0) == list(rz1)
+
+
+@pytest.mark.parametrize("N,physics", [((32, 32), "thermal"), ((16, 8, 32), "thermal"), ((16, 16, 8), "elastic"),
+                                       ((16, 32), "elastic")])
+def test_coefficients_and_spectrum(N, physics):
+    # the device-recorded PCG coefficients (gamma_1, alpha per iteration) and the Tab 4 columns
+    # from their Lanczos tridiagonal (uno_cg_spectrum, host bisection in the library) against the
+    # oracle's coefficients and numpy eigenvalues of the same tridiagonal (oracle/spectra.py), at
+    # the oracle's iteration count (common-iteration protocol)
+    from oracle import spectra
+    from paper_2508_02681_b200.binding import UnoError
+
+    g, ph, mat, amp, seed = make_case(N, physics)
+    L = loads_for(physics, len(N), 2)
+    for l in range(2):
+        ref = homog.solve_problem(g, physics, ph, mat, L[l:l + 1], seed, amp, tol=1e-8)
+        m = ref["iterations"][0]
+        rg, ra = np.array(ref["results"][0].gamma), np.array(ref["results"][0].alpha)
+        s = solver(ph, physics, mat, 1, seed, amp)
+        s.solve(L[l:l + 1], fixed_iters=m)
+        gam, alp = s.coefficients(0)
+        assert len(gam) == m and len(alp) == m
+        assert np.max(np.abs(gam - rg) / np.abs(rg)) <= 1e-8 and np.max(np.abs(alp - ra) / np.abs(ra)) <= 1e-8
+        sp = s.spectrum(0, tol=1e-6)
+        row = spectra.table4_row(*spectra.ritz_extremes(rg, ra), 1e-6)
+        assert sp["m"] == m
+        for k in ("lambda_min", "lambda_max", "cond", "C_CG", "N_iter_est"):
+            assert abs(sp[k] - row[k]) <= 1e-8 * abs(row[k]), (k, sp[k], row[k])
+        assert 0 < sp["lambda_min"] < sp["lambda_max"]
+        with pytest.raises(UnoError):
+            s.spectrum(1)  # load outside [0, nrhs)
+        with pytest.raises(UnoError):
+            s.spectrum(0, tol=1.5)
