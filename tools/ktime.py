@@ -28,7 +28,7 @@ if a.physics == "thermal":
 else:
     ph = torch.from_numpy(synth.spheres_rsa(n, 0.25, 6.0 * n / 64, 10.0 * n / 64, seed=2)).to(dev)
     mat = (synth.lame_from_E_nu(1.0, 0.3), synth.lame_from_E_nu(10.0, 0.2))
-    s = UnoCG(ph, "elastic", mat, nrhs=a.nrhs, seed=1002, amp=0.05)
+    s = UnoCG(ph, "elastic", mat, nrhs=a.nrhs, seed=1002, amp=0.05, bc=tuple(int(v) for v in a.bc.split(",")))
     loads = np.eye(6)[: a.nrhs]
     nb = {"K": 16.33, "xfwd": 24 + 8.06, "ypass": 16.1, "gpass": 24.1, "xinv": 40.06}
 s.solve(loads, fixed_iters=3)
