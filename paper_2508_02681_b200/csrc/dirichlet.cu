@@ -27,10 +27,13 @@ __host__ __device__ constexpr int d3_smem_bytes() {
 
 // One DST-I pass along `axis` (0 x, 1 y, 2 z) of every (load, comp) field, src -> dst (may alias).
 // A CTA transforms 8 packed sequences (16 real ones): axes y, z pack adjacent x pairs (16-byte
-// loads); axis x packs the rows y, y+1.
+// accesses, consecutive threads = consecutive pairs); axis x packs the rows y, y+1 (consecutive
+// threads = consecutive x of one row).  gmul (c = 1, last forward axis): the scalar symbol
+// multiply s_hat = G_hat r_hat of every sine mode is applied to the output (no separate pass).
 template <int L2>
 __global__ void __launch_bounds__(fft_threads(L2)) dst3_kernel(Ctx cx, const double* __restrict__ src,
-                                                              double* __restrict__ dst, int axis, const double2* twl) {
+                                                              double* __restrict__ dst, int axis, const double2* twl,
+                                                              int gmul) {
   constexpr int T = fft_threads(L2);
   constexpr int N = L2 / 2;
   const Geo g = cx.g;
@@ -44,6 +47,7 @@ __global__ void __launch_bounds__(fft_threads(L2)) dst3_kernel(Ctx cx, const dou
   long long es;     // element stride (doubles)
   long long qs;     // stride between packed sequences (doubles)
   long long ps;     // stride between the two real halves of a packed sequence
+  long long fbase;  // offset of the (load, comp) field
   {
     int b = blockIdx.x;
     if (axis == 0) {  // rows: 8 packed pairs = 16 rows y0..y0+15 of plane z
@@ -52,7 +56,8 @@ __global__ void __launch_bounds__(fft_threads(L2)) dst3_kernel(Ctx cx, const dou
       b /= nyb;
       const int z = b % g.N3;
       const int lc = b / g.N3;
-      base = (long long)lc * g.n + z * plane + (long long)yb * 16 * N1;
+      fbase = (long long)lc * g.n;
+      base = fbase + z * plane + (long long)yb * 16 * N1;
       es = 1;
       qs = 2LL * N1;
       ps = N1;
@@ -63,37 +68,71 @@ __global__ void __launch_bounds__(fft_threads(L2)) dst3_kernel(Ctx cx, const dou
       const int other = axis == 1 ? g.N3 : N2;
       const int o = b % other;
       const int lc = b / other;
-      base = (long long)lc * g.n + xb * 16 + (axis == 1 ? (long long)o * plane : (long long)o * N1);
+      fbase = (long long)lc * g.n;
+      base = fbase + xb * 16 + (axis == 1 ? (long long)o * plane : (long long)o * N1);
       es = axis == 1 ? N1 : plane;
       qs = 2;
       ps = 1;
     }
   }
-  for (int i = t; i < L2; i += T) tw[i] = twl[i];
-  for (int e = t; e < 8 * N; e += T) {
-    const int j = e >> 3, q = e & 7;
-    double2 v = make_double2(0.0, 0.0);
-    if (j > 0) {
+  // every load of the tile is issued before the first smem store (unrolled: memory-level
+  // parallelism); axes y, z read the packed pair (x, x+1) as one 16-byte access
+  constexpr int NE = (8 * N + T - 1) / T;
+  constexpr int LN = N >= 2 ? 31 - __builtin_clz(N) : 0;  // log2 N
+  const bool vec = ps == 1, rowmap = axis == 0;
+  auto jq = [&](int e, int& j, int& q) {
+    j = rowmap ? (e & (N - 1)) : (e >> 3);
+    q = rowmap ? (e >> LN) : (e & 7);
+  };
+  double2 vals[NE];
+#pragma unroll
+  for (int i = 0; i < NE; ++i) {
+    const int e = t + i * T;
+    int j, q;
+    jq(e, j, q);
+    vals[i] = make_double2(0.0, 0.0);
+    if (e < 8 * N && j > 0) {
       const long long a = base + q * qs + j * es;
-      v = make_double2(src[a], src[a + ps]);
+      vals[i] = vec ? __ldcg(reinterpret_cast<const double2*>(src + a)) : make_double2(__ldcg(src + a), __ldcg(src + a + ps));
     }
-    tile[tidx(j, q)] = v;
-    if (j > 0) tile[tidx(L2 - j, q)] = make_double2(-v.x, -v.y);
+  }
+  for (int i = t; i < L2; i += T) tw[i] = twl[i];
+#pragma unroll
+  for (int i = 0; i < NE; ++i) {
+    const int e = t + i * T;
+    int j, q;
+    jq(e, j, q);
+    if (e < 8 * N) {
+      tile[tidx(j, q)] = vals[i];
+      if (j > 0) tile[tidx(L2 - j, q)] = make_double2(-vals[i].x, -vals[i].y);
+    }
   }
   if (t < 8) tile[tidx(N, t)] = make_double2(0.0, 0.0);
   __syncthreads();
   fft_tile<L2, false>(tile, tw);
   // sine coefficients m = 1..N-1 of the two halves: (-Im Y_m, Re Y_m) / 2; m = 0 stays 0
-  for (int e = t; e < 8 * N; e += T) {
-    const int m = e >> 3, q = e & 7;
-    const long long a = base + q * qs + m * es;
-    if (m == 0) {
-      dst[a] = 0.0;
-      dst[a + ps] = 0.0;
-    } else {
-      const double2 Y = tile[tidx(m, q)];
-      dst[a] = -0.5 * Y.y;
-      dst[a + ps] = 0.5 * Y.x;
+#pragma unroll
+  for (int i = 0; i < NE; ++i) {
+    const int e = t + i * T;
+    int m, q;
+    jq(e, m, q);
+    if (e < 8 * N) {
+      const long long a = base + q * qs + m * es;
+      double2 o = make_double2(0.0, 0.0);
+      if (m > 0) {
+        const double2 Y = tile[tidx(m, q)];
+        o = make_double2(-0.5 * Y.y, 0.5 * Y.x);
+        if (gmul) {
+          o.x *= __ldg(cx.gtab + (a - fbase));
+          o.y *= __ldg(cx.gtab + (a + ps - fbase));
+        }
+      }
+      if (vec) {
+        __stcg(reinterpret_cast<double2*>(dst + a), o);
+      } else {
+        __stcg(dst + a, o.x);
+        __stcg(dst + a + ps, o.y);
+      }
     }
   }
 }
@@ -277,7 +316,8 @@ static int d3_dispatch(int L2, F&& f) {
   }
 }
 
-static int launch_dst3(const Ctx& cx, const double* src, double* dst, int axis, const double2* twl, cudaStream_t s) {
+static int launch_dst3(const Ctx& cx, const double* src, double* dst, int axis, const double2* twl, cudaStream_t s,
+                       int gmul = 0) {
   const Geo& g = cx.g;
   const int N = axis == 0 ? g.N1 : (axis == 1 ? g.N2 : g.N3);
   const long long nlc = (long long)g.nrhs * g.c;
@@ -286,7 +326,7 @@ static int launch_dst3(const Ctx& cx, const double* src, double* dst, int axis, 
     constexpr int L2 = decltype(Lc)::value;
     const int sm = d3_smem_bytes<L2>();
     if (sm > 48 * 1024) cudaFuncSetAttribute(dst3_kernel<L2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    dst3_kernel<L2><<<(unsigned)nb, fft_threads(L2), sm, s>>>(cx, src, dst, axis, twl);
+    dst3_kernel<L2><<<(unsigned)nb, fft_threads(L2), sm, s>>>(cx, src, dst, axis, twl, gmul);
     return 1;
   });
 }
@@ -330,14 +370,17 @@ int launch_d3_precond(const Ctx& cx, const double* r, double* sbuf, const double
     if ((k = launch_dst3(cx, sbuf, sbuf, 1, tw2[1], s)) < 0) return -1;
     return n + k;
   }
-  if ((k = launch_dst3(cx, r, sbuf, 0, tw2[0], s)) < 0) return -1;
+  const int fuse = g.c == 1;  // scalar symbol: multiplied in the last forward DST pass
+  if ((k = launch_dst3(cx, r, sbuf, 0, tw2[0], s, fuse && g.dim == 1)) < 0) return -1;
   n += k;
   for (int axis = 1; axis < g.dim; ++axis) {
-    if ((k = launch_dst3(cx, sbuf, sbuf, axis, tw2[axis], s)) < 0) return -1;
+    if ((k = launch_dst3(cx, sbuf, sbuf, axis, tw2[axis], s, fuse && axis == g.dim - 1)) < 0) return -1;
     n += k;
   }
-  d3_gmul_kernel<<<(unsigned)gb, 256, 0, s>>>(cx, sbuf);
-  ++n;
+  if (!fuse) {
+    d3_gmul_kernel<<<(unsigned)gb, 256, 0, s>>>(cx, sbuf);
+    ++n;
+  }
   for (int axis = g.dim - 1; axis >= 0; --axis) {
     if ((k = launch_dst3(cx, sbuf, sbuf, axis, tw2[axis], s)) < 0) return -1;
     n += k;
