@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -133,6 +134,111 @@ __global__ void __launch_bounds__(fft_threads(L2)) dst3_kernel(Ctx cx, const dou
         __stcg(dst + a, o.x);
         __stcg(dst + a + ps, o.y);
       }
+    }
+  }
+}
+
+// Register-direct DST-I pass for N = 256 (odd extension of length 512): 4 packed sequences per
+// CTA, thread (q, l) = (t & 3, t >> 2).  Each thread loads its 16 odd-extension entries
+// y_{l + 32 n2} straight into registers (y_j = x_j for j < 256, y_j = -x_{512-j} above; x_0 =
+// x_256 = 0 are the Dirichlet nodes — the mirrored half re-reads the tile through L1), then the
+// four-step FFT of gpass512_kernel (DFT16 -> twiddle -> transpose -> DFT32 split between thread
+// pairs) leaves bins k1 + 16 (2m + h) in registers, of which the 255 sine modes k < 256 are stored
+// (-Im Y_k, Re Y_k) / 2 (times the scalar symbol when gmul).  Buffers 546 apart, rows of 34: the
+// quarter-warp patterns of gpass512_kernel, conflict-free.
+constexpr int D5_C = 4, D5_CS = 546, D5_T = 32 * D5_C;
+constexpr int dst512r_smem = (D5_C * D5_CS + 16 * 32 + 16) * 16;
+__global__ void __launch_bounds__(D5_T, 4) dst512r_kernel(Ctx cx, const double* __restrict__ src,
+                                                          double* __restrict__ dst, int axis, const double2* twl,
+                                                          int gmul) {
+  constexpr int L = 512, N = 256;
+  const Geo g = cx.g;
+  extern __shared__ double2 dsm[];
+  double2* buf = dsm;                 // [D5_C][D5_CS]
+  double2* tw = buf + D5_C * D5_CS;   // [k1][n1] = w_512^{k1 n1}
+  double2* tw32 = tw + 16 * 32;       // w_32^r
+  const int t = threadIdx.x, c = t & (D5_C - 1), l32 = t >> 2;
+  const int N1 = g.N1, N2 = g.N2;
+  const long long plane = (long long)N1 * N2;
+  long long base, es, qs, ps, fbase;
+  {
+    int b = blockIdx.x;
+    if (axis == 0) {  // rows: 4 packed pairs = rows y0..y0+7 of plane z
+      const int nyb = N2 / 8;
+      const int yb = b % nyb;
+      b /= nyb;
+      const int z = b % g.N3;
+      fbase = (long long)(b / g.N3) * g.n;
+      base = fbase + z * plane + (long long)yb * 8 * N1;
+      es = 1;
+      qs = 2LL * N1;
+      ps = N1;
+    } else {  // columns: 4 packed pairs = x0..x0+7 at fixed (y | z)
+      const int nxb = N1 / 8;
+      const int xb = b % nxb;
+      b /= nxb;
+      const int other = axis == 1 ? g.N3 : N2;
+      const int o = b % other;
+      fbase = (long long)(b / other) * g.n;
+      base = fbase + xb * 8 + (axis == 1 ? (long long)o * plane : (long long)o * N1);
+      es = axis == 1 ? N1 : plane;
+      qs = 2;
+      ps = 1;
+    }
+  }
+  const bool vec = ps == 1;
+  const long long sq = base + c * qs;
+  auto ld = [&](int j) -> double2 {  // x_j of this packed sequence, 0 < j < N
+    const double* p = src + sq + j * es;
+    return vec ? __ldg(reinterpret_cast<const double2*>(p)) : make_double2(__ldg(p), __ldg(p + ps));
+  };
+  double2 v[16];
+#pragma unroll
+  for (int n2 = 0; n2 < 16; ++n2) {
+    const int j = l32 + 32 * n2;
+    if (n2 < 8) {
+      v[n2] = j == 0 ? make_double2(0.0, 0.0) : ld(j);
+    } else {
+      const int jj = L - j;  // 1 .. 256
+      const double2 x = jj == N ? make_double2(0.0, 0.0) : ld(jj);
+      v[n2] = make_double2(-x.x, -x.y);
+    }
+  }
+  for (int i = t; i < 16 * 32; i += D5_T) tw[i] = twl[((i & 31) * (i >> 5)) & (L - 1)];
+  if (t < 16) tw32[t] = twl[16 * t];
+  __syncthreads();
+  double2* B = buf + c * D5_CS;
+  dft_reg<16, false>(v);  // thread = n1: over n2 -> k1
+#pragma unroll
+  for (int k1 = 1; k1 < 16; ++k1) v[k1] = cmul(v[k1], tw[k1 * 32 + l32]);
+#pragma unroll
+  for (int k1 = 0; k1 < 16; ++k1) B[k1 * 34 + l32] = v[k1];
+  __syncthreads();
+  const int k1 = l32 >> 1, h = l32 & 1;
+  double2 o[16];
+  {
+    double2 a[32];
+#pragma unroll
+    for (int n1 = 0; n1 < 32; ++n1) a[n1] = B[k1 * 34 + n1];
+    dft_half<32, false>(a, h, tw32, o);  // o[m] = Y(k1 + 16 (2m + h))
+  }
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {  // sine modes k = k1 + 16 (2m + h) < 256
+    const int k = k1 + 16 * (2 * m + h);
+    const long long a = sq + k * es;
+    double2 r = make_double2(0.0, 0.0);
+    if (k > 0) {
+      r = make_double2(-0.5 * o[m].y, 0.5 * o[m].x);
+      if (gmul) {
+        r.x *= __ldg(cx.gtab + (a - fbase));
+        r.y *= __ldg(cx.gtab + (a + ps - fbase));
+      }
+    }
+    if (vec) {
+      __stcg(reinterpret_cast<double2*>(dst + a), r);
+    } else {
+      __stcg(dst + a, r.x);
+      __stcg(dst + a + ps, r.y);
     }
   }
 }
@@ -322,6 +428,15 @@ static int launch_dst3(const Ctx& cx, const double* src, double* dst, int axis, 
   const int N = axis == 0 ? g.N1 : (axis == 1 ? g.N2 : g.N3);
   const long long nlc = (long long)g.nrhs * g.c;
   const long long nb = axis == 0 ? nlc * g.N3 * (g.N2 / 16) : nlc * (axis == 1 ? g.N3 : g.N2) * (g.N1 / 16);
+  static const bool rd = [] {
+    const char* e = getenv("UNO_DRD");
+    return !(e && e[0] == '0');
+  }();
+  if (rd && N == 256 && (axis == 0 ? g.N2 % 8 == 0 : g.N1 % 8 == 0)) {
+    const long long nb8 = axis == 0 ? nlc * g.N3 * (g.N2 / 8) : nlc * (axis == 1 ? g.N3 : g.N2) * (g.N1 / 8);
+    dst512r_kernel<<<(unsigned)nb8, D5_T, dst512r_smem, s>>>(cx, src, dst, axis, twl, gmul);
+    return 1;
+  }
   return d3_dispatch(2 * N, [&](auto Lc) {
     constexpr int L2 = decltype(Lc)::value;
     const int sm = d3_smem_bytes<L2>();

@@ -706,3 +706,11 @@ def test_coefficients_and_spectrum(N, physics):
             s.spectrum(1)  # load outside [0, nrhs)
         with pytest.raises(UnoError):
             s.spectrum(0, tol=1.5)
+
+
+@pytest.mark.parametrize("N,physics", [((256, 16, 8), "thermal"), ((32, 256, 8), "thermal"), ((32, 16, 256), "thermal"),
+                                       ((16, 16, 256), "elastic")])
+def test_all_dirichlet_256_point_dst(N, physics):
+    # the register-direct DST-I pass (N = 256 on the x, y or z axis; odd extension of length 512,
+    # the scalar symbol fused into the last forward pass for c = 1) against the oracle
+    test_all_dirichlet_operators(N, physics)
