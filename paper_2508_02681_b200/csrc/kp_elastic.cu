@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int
 int launch_kp_elastic_modal(const Ctx& cx, int mode, const double* src, double* dst, cudaStream_t s) {
   const Geo& g = cx.g;
   if (g.dim != 3 || g.c != 3 || g.N1 < KM_TX || g.N2 < KM_TY) return -1;
-  const int ZC = g.N3 < 32 ? g.N3 : 32;
+  const int ZC = g.KZC;
   const dim3 grid(g.N1 / KM_TX, g.N2 / KM_TY, ((g.P3 + ZC - 1) / ZC) * g.nrhs);
   const int sm = km_smem_bytes();
   static bool attr = false;
@@ -215,7 +215,7 @@ int launch_kp_elastic_modal(const Ctx& cx, int mode, const double* src, double* 
 }
 
 int kp_elastic_modal_nblk(const Geo& g) {
-  const int ZC = g.N3 < 32 ? g.N3 : 32;
+  const int ZC = g.KZC;
   return (g.N1 / KM_TX) * (g.N2 / KM_TY) * ((g.P3 + ZC - 1) / ZC);
 }
 

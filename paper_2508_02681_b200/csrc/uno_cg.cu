@@ -323,7 +323,15 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
       g.NA = t3.NA;
     }
   }
+  // z planes per K CTA: 32, halved (down to 4) while the K grid is under two waves of 2 CTAs per
+  // SM (small grids such as configs 1 and 2 would otherwise leave most SMs idle)
   g.KZC = g.N3 < 32 ? g.N3 : 32;
+  if (g.dim == 3) {
+    const long long per = c == 1 ? (long long)std::max(1, N1 / 32) * std::max(1, N2 / 16)
+                                 : (long long)std::max(1, N1 / 16) * std::max(1, N2 / 8);
+    auto kblocks = [&](int zc) { return per * ((g.P3 + zc - 1) / zc) * g.nrhs; };
+    while (g.KZC > 4 && kblocks(g.KZC) < 2LL * 148 * 2) g.KZC /= 2;
+  }
   g.ZP = 0;
   {  // L2-pipelined 5-pass schedule (z-chunks), UNO_ZPIPE=<planes per chunk>
     const char* ev = getenv("UNO_ZPIPE");
