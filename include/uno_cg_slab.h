@@ -68,6 +68,20 @@ UNO_API uno_status uno_slab_green(uno_slab_handle* h, const double* d_recv, doub
 UNO_API uno_status uno_slab_inverse(uno_slab_handle* h, const double* d_recv, double* d_halo_send);
 UNO_API uno_status uno_slab_kapply(uno_slab_handle* h, const double* d_halo_recv);
 
+/* Peer-memory variants of forward / green (BASELINE north star (e), SURVEY §8(e) "v2"): the
+ * pack kernel stores each destination's block straight into that rank's receive buffer over
+ * NVLink (P2P / CUDA IPC / symmetric-memory mappings), so the exchange is done by this kernel
+ * and no send buffer or separate all-to-all exists.  h_peer_recv: HOST array [nranks] of
+ * DEVICE pointers, entry q = rank q's receive buffer as addressable from this device (entry
+ * `rank` = the local one); this rank writes block `rank` of each.  Use two receive buffer sets,
+ * A for forward and B for green: green_peer reads the local A (d_recv) and writes the peers' B,
+ * uno_slab_inverse then reads the local B.  Ordering (caller): every rank's forward_peer /
+ * green_peer must complete before any rank reads the written buffers — the ||r||_inf and gamma
+ * all-reduces that follow these stages (stream-ordered) provide exactly that; each pack kernel
+ * ends with a system-scope fence.  UNO_ERR_ARG: null arrays / entries.                    */
+UNO_API uno_status uno_slab_forward_peer(uno_slab_handle* h, double* const* h_peer_recv);
+UNO_API uno_status uno_slab_green_peer(uno_slab_handle* h, const double* d_recv, double* const* h_peer_recv);
+
 /* Per-rank partial of a CG scalar (slot UNO_SLAB_*), written to d_out[nrhs] (device);
  * uno_slab_apply takes the cross-rank totals d_in[nrhs] and updates the CG state.       */
 UNO_API uno_status uno_slab_reduce(uno_slab_handle* h, int32_t slot, double* d_out);

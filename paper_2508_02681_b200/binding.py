@@ -29,7 +29,8 @@ UNO_PRECOND = {"uno": 0, "identity": 1, "jacobi": 2}
 # include/uno_cg_slab.h (z-slab decomposition)
 SLAB_EXPORTS = ("uno_slab_create", "uno_slab_destroy", "uno_slab_sizes", "uno_slab_begin", "uno_slab_forward",
                 "uno_slab_green", "uno_slab_inverse", "uno_slab_kapply", "uno_slab_reduce", "uno_slab_apply",
-                "uno_slab_state", "uno_slab_finish", "uno_slab_local_means", "uno_slab_subtract_means")
+                "uno_slab_state", "uno_slab_finish", "uno_slab_local_means", "uno_slab_subtract_means",
+                "uno_slab_forward_peer", "uno_slab_green_peer")
 
 
 class UnoCgDesc(C.Structure):
@@ -85,6 +86,8 @@ def _load():
     lib.uno_slab_finish.argtypes = [P, P]
     lib.uno_slab_local_means.argtypes = [P, P, P]
     lib.uno_slab_subtract_means.argtypes = [P, P, P]
+    lib.uno_slab_forward_peer.argtypes = [P, P]
+    lib.uno_slab_green_peer.argtypes = [P, P, P]
     for f in EXPORTS[:-2] + SLAB_EXPORTS:
         getattr(lib, f).restype = C.c_int
     lib.uno_cg_last_error.restype = C.c_char_p
@@ -267,6 +270,20 @@ def uno_slab_forward(h: int, d_send):
 
 def uno_slab_green(h: int, d_recv, d_send):
     _check(_lib.uno_slab_green(h, _ptr(d_recv), _ptr(d_send)), "uno_slab_green")
+
+
+def _ptr_array(ptrs):
+    arr = (C.c_void_p * len(ptrs))(*[int(p) for p in ptrs])
+    return arr
+
+
+def uno_slab_forward_peer(h: int, peer_recv_ptrs):
+    """peer_recv_ptrs: device addresses (ints) of every rank's receive buffer A, in rank order."""
+    _check(_lib.uno_slab_forward_peer(h, _ptr_array(peer_recv_ptrs)), "uno_slab_forward_peer")
+
+
+def uno_slab_green_peer(h: int, d_recv, peer_recv_ptrs):
+    _check(_lib.uno_slab_green_peer(h, _ptr(d_recv), _ptr_array(peer_recv_ptrs)), "uno_slab_green_peer")
 
 
 def uno_slab_inverse(h: int, d_recv, d_halo_send):

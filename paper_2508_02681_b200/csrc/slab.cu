@@ -68,6 +68,20 @@ __global__ void slab_pack_kernel(const double2* __restrict__ S, double2* __restr
   for (long long row = (long long)blockIdx.y * rpb + ty; row < rows; row += (long long)gridDim.y * rpb)
     o[row * Yc + yc] = S[row * N2 + (long long)q * Yc + yc];
 }
+// peer variant: block q goes straight to rank q's receive buffer (block `rank` of it)
+constexpr int kMaxRanks = 8;
+struct SlabPeers {
+  double2* p[kMaxRanks];
+};
+__global__ void slab_pack_peer_kernel(const double2* __restrict__ S, SlabPeers peers, int rank, long long rows, int Yc,
+                                      int N2) {
+  const int q = blockIdx.z;
+  const int ty = threadIdx.x / Yc, yc = threadIdx.x - ty * Yc, rpb = blockDim.x / Yc;
+  double2* o = peers.p[q] + (long long)rank * rows * Yc;
+  for (long long row = (long long)blockIdx.y * rpb + ty; row < rows; row += (long long)gridDim.y * rpb)
+    o[row * Yc + yc] = S[row * N2 + (long long)q * Yc + yc];
+  __threadfence_system();
+}
 __global__ void slab_unpack_kernel(const double2* __restrict__ in, double2* __restrict__ S, long long rows, int Yc,
                                    int N2) {
   const int q = blockIdx.z;
@@ -92,6 +106,19 @@ __global__ void slab_pencil_kernel(double2* __restrict__ buf, double2* __restric
         b[i] = p[i];
     }
   }
+}
+// pencil -> block `rank` of every rank q's receive buffer (peer variant of dir 1)
+__global__ void slab_pencil_peer_kernel(SlabPeers peers, int rank, const double2* __restrict__ P, long long nlckx,
+                                        int Z, int Yc, int N3) {
+  const int q = blockIdx.z;
+  const long long run = (long long)Z * Yc;
+  for (long long lk = blockIdx.y; lk < nlckx; lk += gridDim.y) {
+    double2* b = peers.p[q] + ((long long)rank * nlckx + lk) * run;
+    const double2* p = P + lk * (long long)N3 * Yc + (long long)q * run;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < run; i += (long long)gridDim.x * blockDim.x)
+      b[i] = p[i];
+  }
+  __threadfence_system();
 }
 // halo send: plane 0 and plane Z-1 of every (load, comp) slab of d -> out[2][lc][plane]
 __global__ void slab_halo_kernel(const double* __restrict__ d, double* __restrict__ out, int nlc, int Z, long long plane) {
@@ -376,6 +403,43 @@ extern "C" uno_status uno_slab_forward(uno_slab_handle* h, double* d_send) {
   const long long rows = (long long)g.nrhs * g.c * g.H1 * h->Z;
   slab_pack_kernel<<<pack_grid(rows, h->Yc, h->nranks), pack_threads(h->Yc), 0, h->s>>>(
       h->spec, reinterpret_cast<double2*>(d_send), rows, h->Yc, g.N2);
+  SCK(cudaGetLastError());
+  return UNO_OK;
+}
+
+static bool fill_peers(const uno_slab_handle* h, double* const* hp, SlabPeers& P) {
+  if (!hp || h->nranks > kMaxRanks) return false;
+  for (int q = 0; q < kMaxRanks; ++q) P.p[q] = nullptr;
+  for (int q = 0; q < h->nranks; ++q) {
+    if (!hp[q]) return false;
+    P.p[q] = reinterpret_cast<double2*>(hp[q]);
+  }
+  return true;
+}
+
+extern "C" uno_status uno_slab_forward_peer(uno_slab_handle* h, double* const* h_peer_recv) {
+  SlabPeers P;
+  if (!h || !fill_peers(h, h_peer_recv, P)) return sfail(UNO_ERR_ARG, "null handle / peer pointer array");
+  SKL(launch_xfwd(h->cxy, CG, h->r, h->s));
+  SKL(launch_ypass(h->cxy, CG, false, h->s));
+  const Geo& g = h->gxy;
+  const long long rows = (long long)g.nrhs * g.c * g.H1 * h->Z;
+  slab_pack_peer_kernel<<<pack_grid(rows, h->Yc, h->nranks), pack_threads(h->Yc), 0, h->s>>>(h->spec, P, h->rank, rows,
+                                                                                             h->Yc, g.N2);
+  SCK(cudaGetLastError());
+  return UNO_OK;
+}
+
+extern "C" uno_status uno_slab_green_peer(uno_slab_handle* h, const double* d_recv, double* const* h_peer_recv) {
+  SlabPeers P;
+  if (!h || !d_recv || !fill_peers(h, h_peer_recv, P)) return sfail(UNO_ERR_ARG, "null argument / peer pointer array");
+  const Geo& g = h->gxy;
+  const long long nlckx = (long long)g.nrhs * g.c * g.H1;
+  const dim3 gb(1, (unsigned)std::min<long long>(nlckx, 4096), h->nranks);
+  slab_pencil_kernel<<<gb, 256, 0, h->s>>>(const_cast<double2*>(reinterpret_cast<const double2*>(d_recv)), h->pencil,
+                                          nlckx, h->Z, h->Yc, h->gz.N3, 0);
+  SKL(launch_gpass(h->cz, CG, h->s));
+  slab_pencil_peer_kernel<<<gb, 256, 0, h->s>>>(P, h->rank, h->pencil, nlckx, h->Z, h->Yc, h->gz.N3);
   SCK(cudaGetLastError());
   return UNO_OK;
 }

@@ -47,6 +47,16 @@ class LocalComm:
             recvs[(r - 1) % n][1].copy_(sends[r][0])
             recvs[(r + 1) % n][0].copy_(sends[r][1])
 
+    def peer_buffers(self, numel: int, device):
+        """Receive buffers for the peer-memory exchange: one per rank, each rank's pointer list
+        holds every rank's buffer (all in this process)."""
+        bufs = [torch.empty(numel, dtype=torch.float64, device=device) for _ in self.ranks]
+        ptrs = [[b.data_ptr() for b in bufs] for _ in self.ranks]
+        return bufs, ptrs
+
+    def peer_barrier(self):
+        pass  # one stream: the emulated ranks' kernels are already ordered
+
     def allreduce(self, vals, op: str):
         tot = vals[0].clone()
         for v in vals[1:]:
@@ -92,6 +102,21 @@ class DistComm:
         for w in self.dist.batch_isend_irecv(ops):
             w.wait()
 
+    def peer_buffers(self, numel: int, device):
+        """Receive buffers in symmetric memory (torch.distributed._symmetric_memory): every rank's
+        buffer is mapped into every process over NVLink; `buffer_ptrs` are the peer addresses."""
+        import torch.distributed._symmetric_memory as symm_mem
+
+        buf = symm_mem.empty(numel, dtype=torch.float64, device=device)
+        hdl = symm_mem.rendezvous(buf, self.dist.group.WORLD)
+        self._symm = getattr(self, "_symm", []) + [hdl]
+        return [buf], [list(hdl.buffer_ptrs)]
+
+    def peer_barrier(self):
+        # device-side barrier over the symmetric-memory signal pads (stream-ordered): every
+        # rank's peer stores of the stage have landed before anyone reads its receive buffer
+        self._symm[0].barrier()
+
     def allreduce(self, vals, op: str):
         self.dist.all_reduce(vals[0], op=self.dist.ReduceOp.SUM if op == SUM else self.dist.ReduceOp.MAX)
 
@@ -108,7 +133,7 @@ class SlabSolver:
     this process's device (every rank keeps all of it: 1 byte per voxel)."""
 
     def __init__(self, phase: torch.Tensor, physics: str, mat, comm, nrhs: int = 1, seed: int = 0, amp: float = 0.0,
-                 h: float = 0.0, ref=None):
+                 h: float = 0.0, ref=None, peer: bool = False):
         assert phase.dim() == 3 and phase.dtype == torch.uint8 and phase.is_cuda
         self.phase = phase.contiguous()
         self.comm = comm
@@ -143,6 +168,14 @@ class SlabSolver:
         self.hsend = [torch.empty((2, hs), **f64) for _ in comm.ranks]
         self.hrecv = [torch.empty((2, hs), **f64) for _ in comm.ranks]
         self.red = [torch.empty(nrhs, **f64) for _ in comm.ranks]
+        # peer-memory exchange: the pack kernels store straight into the receivers' buffers (A for
+        # the forward transpose, B for the way back); no send buffers, no all-to-all call
+        self.peer = peer
+        if peer:
+            ra, self.ptrA = comm.peer_buffers(R * 2 * blk, dev)
+            rb, self.ptrB = comm.peer_buffers(R * 2 * blk, dev)
+            self.recvA = [t.view(R, 2 * blk) for t in ra]
+            self.recvB = [t.view(R, 2 * blk) for t in rb]
 
     def close(self):
         for h in self.handles:
@@ -159,6 +192,22 @@ class SlabSolver:
     def iterate(self):
         """One PCG iteration (Alg 2 l.3-12) on every local rank."""
         c, H = self.comm, self.handles
+        if self.peer:
+            for h, pa in zip(H, self.ptrA):
+                B.uno_slab_forward_peer(h, pa)    # x, y transforms; blocks stored into the peers' A
+            c.peer_barrier()
+            self._scalar(0, MAX)
+            for h, ra, pb in zip(H, self.recvA, self.ptrB):
+                B.uno_slab_green_peer(h, ra, pb)  # z . G . z^-1; blocks stored into the peers' B
+            c.peer_barrier()
+            self._scalar(1, SUM)
+            for h, rb, hs in zip(H, self.recvB, self.hsend):
+                B.uno_slab_inverse(h, rb, hs)
+            c.halo(self.hsend, self.hrecv)
+            for h, hr in zip(H, self.hrecv):
+                B.uno_slab_kapply(h, hr)
+            self._scalar(2, SUM)
+            return
         for h, s in zip(H, self.send):
             B.uno_slab_forward(h, s)
         self._scalar(0, MAX)                      # ||r||_inf: stop test (l.3)

@@ -30,10 +30,11 @@ def whole(ph, physics, mat, nrhs, seed, amp, loads, fixed):
     return r.u.cpu().numpy(), r.reports
 
 
-def slab(ph, physics, mat, nrhs, seed, amp, loads, fixed, nranks):
+def slab(ph, physics, mat, nrhs, seed, amp, loads, fixed, nranks, peer=False):
     from paper_2508_02681_b200.slab import LocalComm, SlabSolver
 
-    sv = SlabSolver(torch.from_numpy(ph).to(dev()), physics, mat, LocalComm(nranks), nrhs=nrhs, seed=seed, amp=amp)
+    sv = SlabSolver(torch.from_numpy(ph).to(dev()), physics, mat, LocalComm(nranks), nrhs=nrhs, seed=seed, amp=amp,
+                    peer=peer)
     res = sv.solve(loads, fixed_iters=fixed) if fixed else sv.solve(loads)
     sv.close()
     return np.concatenate([u.cpu().numpy() for u in res.u], axis=2), res.reports
@@ -75,3 +76,21 @@ def test_slab_against_oracle():
     ref = homog.solve_problem(g, "thermal", ph, mat, load, 77, 0.1, fixed_iters=7)
     us, _ = slab(ph, "thermal", mat, 1, 77, 0.1, load, 7, 2)
     assert rel(us[0], ref["U"][0]) <= 1e-9
+
+
+@pytest.mark.parametrize("nranks,physics", [(2, "thermal"), (4, "thermal"), (4, "elastic")])
+def test_peer_memory_exchange_equals_all_to_all(nranks, physics):
+    # uno_slab_forward_peer / uno_slab_green_peer: the pack kernels store every block straight
+    # into the receiving rank's buffer (here: the other emulated ranks' buffers on this device);
+    # only data movement changes, so the iterates equal the all-to-all path bit for bit
+    if physics == "thermal":
+        P = synth.config1()
+        ph, mat, seed, amp, loads = P.phase, P.mat, P.seed, P.amp, np.eye(3)[:2]
+    else:
+        ph = synth.spheres_rsa(32, 0.25, 3.0, 5.0, seed=2)
+        mat = (synth.lame_from_E_nu(1.0, 0.3), synth.lame_from_E_nu(10.0, 0.2))
+        seed, amp, loads = 1002, 0.05, np.eye(6)[:2]
+    ua, ra = slab(ph, physics, mat, 2, seed, amp, loads, 5, nranks)
+    up, rp = slab(ph, physics, mat, 2, seed, amp, loads, 5, nranks, peer=True)
+    assert np.array_equal(ua, up)
+    assert [r["iterations"] for r in ra] == [r["iterations"] for r in rp] == [5, 5]
