@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(fft_threads(L), L == 256 ? UNO_YMINB : 1) ypas
 // shared-memory transpose, then DFT16 over n1 and stores X[k1 + 16 k2] straight from
 // registers.  One shared-memory round trip per element instead of four.
 constexpr int YR_R = 16, YR_ROWS = 8, YR_RS = YR_R * (YR_R + 1);
-template <bool INV, int MODE>
+template <bool INV, int MODE, bool PEER = false>
 __global__ void __launch_bounds__(YR_ROWS * YR_R) ypass256_kernel(Ctx cx, int z0, int zc) {
   constexpr int L = 256;
   const Geo g = cx.g;
@@ -429,10 +429,30 @@ __global__ void __launch_bounds__(YR_ROWS * YR_R) ypass256_kernel(Ctx cx, int z0
     for (int n1 = 0; n1 < YR_R; ++n1) v[n1] = buf[r * YR_RS + k1 * (YR_R + 1) + n1];
     dft_reg<YR_R, INV>(v);
     if (ok) {
+      if constexpr (PEER) {  // slab: the all-to-all block of each bin goes straight to its owner
+        const long long grow = (long long)load * nrows + row0 + r;
+        const int yc = cx.peer_yc;
 #pragma unroll
-      for (int k2 = 0; k2 < YR_R; ++k2) __stcg(rowp + k1 + YR_R * k2, v[k2]);
+        for (int k2 = 0; k2 < YR_R; ++k2) {
+          const int k = k1 + YR_R * k2;
+          __stcg(cx.peer[k / yc] + cx.peer_off + grow * yc + (k & (yc - 1)), v[k2]);
+        }
+      } else {
+#pragma unroll
+        for (int k2 = 0; k2 < YR_R; ++k2) __stcg(rowp + k1 + YR_R * k2, v[k2]);
+      }
     }
   }
+  if constexpr (PEER) __threadfence_system();
+}
+
+int launch_ypass_peer(const Ctx& cx, cudaStream_t s) {
+  const Geo& g = cx.g;
+  if (g.N2 != 256) return -1;
+  const long long nrows = (long long)g.c * g.H1 * g.N3;
+  const dim3 grid((unsigned)((nrows + YR_ROWS - 1) / YR_ROWS), g.nrhs);
+  ypass256_kernel<false, CG, true><<<grid, YR_ROWS * YR_R, 0, s>>>(cx, 0, 0);
+  return 1;
 }
 
 // y pass for N2 = 512: 512 = 32 x 16 (y = n1 + 32 n2, k = k1 + 16 k2).  32 threads per row: each

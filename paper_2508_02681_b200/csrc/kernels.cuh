@@ -33,6 +33,11 @@ struct Ctx {
   int hist_stride;
   const double* hlo;        // slab mode (g.halo): node plane zlo-1 of d, [nrhs][c][N2][N1]
   const double* hhi;        // slab mode: node plane zlo+P3 of d
+  // slab peer-memory forward (ypass256 PEER instance): bin k of row `row` goes to
+  // peer[k / peer_yc] + peer_off + row * peer_yc + k % peer_yc (receivers' a2a buffers)
+  double2* peer[8];
+  long long peer_off;
+  int peer_yc;
 };
 
 struct LoadParams {         // macroscopic loads for the RHS / effective-property kernels
@@ -48,6 +53,8 @@ int launch_xfwd(const Ctx& cx, int mode, const double* src, cudaStream_t s, int 
 int launch_xinv(const Ctx& cx, int mode, double* dst, cudaStream_t s, int b0 = 0, int nb = 0);
 // z0/zc: only z in [z0, z0+zc) of every (comp, kx) plane (zc = 0: all; multiples of 8)
 int launch_ypass(const Ctx& cx, int mode, bool inverse, cudaStream_t s, int z0 = 0, int zc = 0);
+// slab forward y pass storing straight into the peers' receive buffers (N2 = 256 only; -1 otherwise)
+int launch_ypass_peer(const Ctx& cx, cudaStream_t s);
 int launch_gpass(const Ctx& cx, int mode, cudaStream_t s);
 int gpass_nblk(const Geo& g);  // CTAs (gamma partials per load) of the CG-mode G pass
 // zc0/nzl: 3D thermal only, z-chunks [zc0, zc0+nzl) of g.KZC planes (nzl = 0: all)

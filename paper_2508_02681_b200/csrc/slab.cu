@@ -421,11 +421,19 @@ extern "C" uno_status uno_slab_forward_peer(uno_slab_handle* h, double* const* h
   SlabPeers P;
   if (!h || !fill_peers(h, h_peer_recv, P)) return sfail(UNO_ERR_ARG, "null handle / peer pointer array");
   SKL(launch_xfwd(h->cxy, CG, h->r, h->s));
-  SKL(launch_ypass(h->cxy, CG, false, h->s));
   const Geo& g = h->gxy;
   const long long rows = (long long)g.nrhs * g.c * g.H1 * h->Z;
-  slab_pack_peer_kernel<<<pack_grid(rows, h->Yc, h->nranks), pack_threads(h->Yc), 0, h->s>>>(h->spec, P, h->rank, rows,
-                                                                                             h->Yc, g.N2);
+  if (g.N2 == 256) {  // the y pass itself stores every bin into its owner's receive buffer
+    Ctx cp = h->cxy;
+    for (int q = 0; q < 8; ++q) cp.peer[q] = P.p[q];
+    cp.peer_off = (long long)h->rank * rows * h->Yc;
+    cp.peer_yc = h->Yc;
+    SKL(launch_ypass_peer(cp, h->s));
+  } else {
+    SKL(launch_ypass(h->cxy, CG, false, h->s));
+    slab_pack_peer_kernel<<<pack_grid(rows, h->Yc, h->nranks), pack_threads(h->Yc), 0, h->s>>>(h->spec, P, h->rank,
+                                                                                               rows, h->Yc, g.N2);
+  }
   SCK(cudaGetLastError());
   return UNO_OK;
 }
