@@ -446,21 +446,13 @@ __global__ void __launch_bounds__(YR_ROWS * YR_R) ypass256_kernel(Ctx cx, int z0
   if constexpr (PEER) __threadfence_system();
 }
 
-int launch_ypass_peer(const Ctx& cx, cudaStream_t s) {
-  const Geo& g = cx.g;
-  if (g.N2 != 256) return -1;
-  const long long nrows = (long long)g.c * g.H1 * g.N3;
-  const dim3 grid((unsigned)((nrows + YR_ROWS - 1) / YR_ROWS), g.nrhs);
-  ypass256_kernel<false, CG, true><<<grid, YR_ROWS * YR_R, 0, s>>>(cx, 0, 0);
-  return 1;
-}
 
 // y pass for N2 = 512: 512 = 32 x 16 (y = n1 + 32 n2, k = k1 + 16 k2).  32 threads per row: each
 // loads 16 elements, DFT16 over n2, twiddle w_512^{n1 k1}, padded transpose; then the 32-point
 // DFTs over n1 (one per k1) are split between thread pairs (dft_half, outputs k2 = 2m + h) and
 // stored straight from registers.  4 rows per 128-thread CTA.
 constexpr int Y5_ROWS = 4, Y5_RS = 16 * 33;
-template <bool INV, int MODE>
+template <bool INV, int MODE, bool PEER = false>
 __global__ void __launch_bounds__(128) ypass512_kernel(Ctx cx, int z0, int zc) {
   constexpr int L = 512;
   const Geo g = cx.g;
@@ -505,10 +497,37 @@ __global__ void __launch_bounds__(128) ypass512_kernel(Ctx cx, int z0, int zc) {
     for (int n1 = 0; n1 < 32; ++n1) a[n1] = Tr[k1 * 33 + n1];
     dft_half<32, INV>(a, h, tw32, o);
     if (ok) {
+      if constexpr (PEER) {  // slab: each bin straight to the owner of its k_y chunk
+        const long long grow = (long long)load * nrows + row0 + r;
+        const int yc = cx.peer_yc;
 #pragma unroll
-      for (int m = 0; m < 16; ++m) __stcg(rowp + k1 + 16 * (2 * m + h), o[m]);
+        for (int m = 0; m < 16; ++m) {
+          const int k = k1 + 16 * (2 * m + h);
+          __stcg(cx.peer[k / yc] + cx.peer_off + grow * yc + (k & (yc - 1)), o[m]);
+        }
+      } else {
+#pragma unroll
+        for (int m = 0; m < 16; ++m) __stcg(rowp + k1 + 16 * (2 * m + h), o[m]);
+      }
     }
   }
+  if constexpr (PEER) __threadfence_system();
+}
+
+int launch_ypass_peer(const Ctx& cx, cudaStream_t s) {
+  const Geo& g = cx.g;
+  const long long nrows = (long long)g.c * g.H1 * g.N3;
+  if (g.N2 == 256) {
+    const dim3 grid((unsigned)((nrows + YR_ROWS - 1) / YR_ROWS), g.nrhs);
+    ypass256_kernel<false, CG, true><<<grid, YR_ROWS * YR_R, 0, s>>>(cx, 0, 0);
+    return 1;
+  }
+  if (g.N2 == 512) {
+    const dim3 grid((unsigned)((nrows + Y5_ROWS - 1) / Y5_ROWS), g.nrhs);
+    ypass512_kernel<false, CG, true><<<grid, 128, 0, s>>>(cx, 0, 0);
+    return 1;
+  }
+  return -1;
 }
 
 template <int L, int NC>
@@ -526,7 +545,7 @@ __host__ __device__ constexpr int gsmem_bytes() {
 }
 
 // 3D G pass: sequences along z (stride N2), tile = 8 consecutive y of one kx plane.
-template <int L, int NC, int MODE>
+template <int L, int NC, int MODE, bool PEER = false>
 __global__ void __launch_bounds__(fft_threads(L), L == 256 ? UNO_GMINB : 1) gpass_z_kernel(Ctx cx) {
   constexpr int T = fft_threads(L);
   constexpr int NCC = NC == 1 ? 1 : (NC == 2 ? 3 : 6);  // unique symbol entries per bin
@@ -610,13 +629,27 @@ __global__ void __launch_bounds__(fft_threads(L), L == 256 ? UNO_GMINB : 1) gpas
   }
 #pragma unroll
   for (int q = 0; q < NC; ++q) {
-    double2* base = cx.spec + ((long long)load * g.c + q) * g.nspec + boff;
+    if constexpr (PEER) {  // slab: z plane zz belongs to rank zz / peer_z -> its receive buffer
+      const long long lk = ((long long)load * g.c + q) * g.H1 + kx;
 #pragma unroll
-    for (int i = 0; i < (8 * L + T - 1) / T; ++i) {
-      const int e = t + i * T;
-      if (e < 8 * L) base[(long long)(e >> 3) * g.N2 + (e & 7)] = tiles[q][tidx(e >> 3, e & 7)];
+      for (int i = 0; i < (8 * L + T - 1) / T; ++i) {
+        const int e = t + i * T;
+        if (e < 8 * L) {
+          const int zz = e >> 3, qd = zz / cx.peer_z, zq = zz - qd * cx.peer_z;
+          cx.peer[qd][((cx.peer_rank * cx.peer_nlckx + lk) * cx.peer_z + zq) * g.N2 + y0 + (e & 7)] =
+              tiles[q][tidx(zz, e & 7)];
+        }
+      }
+    } else {
+      double2* base = cx.spec + ((long long)load * g.c + q) * g.nspec + boff;
+#pragma unroll
+      for (int i = 0; i < (8 * L + T - 1) / T; ++i) {
+        const int e = t + i * T;
+        if (e < 8 * L) base[(long long)(e >> 3) * g.N2 + (e & 7)] = tiles[q][tidx(e >> 3, e & 7)];
+      }
     }
   }
+  if constexpr (PEER) __threadfence_system();
   gamma_finish(cx, load, part, red_sh, MODE);
 }
 
@@ -2461,6 +2494,26 @@ int gpass_nblk(const Geo& g) {
   if (g.NB > 0) return g.H1 * g.NB;
   if (g.dim == 3 && !g.dirz) return g.H1 * (g.N2 / (gpass_512(g) ? G5_C : (gpass_e256(g) ? GE_COLS : 8)));
   return (int)(((long long)g.H1 * g.P3 + 7) / 8);
+}
+
+int launch_gpass_peer(const Ctx& cx, cudaStream_t s) {
+  const Geo& g = cx.g;
+  if (g.dim != 3 || g.dirz || gpass_512(g) || gpass_e256(g) || (gpass_rd() && g.c == 1 && g.N3 == 256)) return -1;
+  return dispatch_pow2(g.N3, [&](auto Lc) {
+    constexpr int L = decltype(Lc)::value;
+    const dim3 grid((unsigned)(g.H1 * (g.N2 / 8)), g.nrhs);
+    auto go = [&](auto k, int sm) {
+      set_smem(k, sm);
+      k<<<grid, fft_threads(L), sm, s>>>(cx);
+      return 1;
+    };
+    if (g.c == 1) return go(gpass_z_kernel<L, 1, CG, true>, gsmem_bytes<L, 1>());
+    if constexpr (gsmem_bytes<L, 3>() <= 220 * 1024) {
+      return go(gpass_z_kernel<L, 3, CG, true>, gsmem_bytes<L, 3>());
+    } else {
+      return -1;
+    }
+  });
 }
 
 int launch_gpass(const Ctx& cx, int mode, cudaStream_t s) {

@@ -38,6 +38,10 @@ struct Ctx {
   double2* peer[8];
   long long peer_off;
   int peer_yc;
+  // slab peer-memory green (gpass_z PEER instance): pencil element (lk, z, y) goes to
+  // peer[z / peer_z] + ((peer_rank * peer_nlckx + lk) * peer_z + z % peer_z) * N2 + y
+  int peer_rank, peer_z;
+  long long peer_nlckx;
 };
 
 struct LoadParams {         // macroscopic loads for the RHS / effective-property kernels
@@ -55,6 +59,9 @@ int launch_xinv(const Ctx& cx, int mode, double* dst, cudaStream_t s, int b0 = 0
 int launch_ypass(const Ctx& cx, int mode, bool inverse, cudaStream_t s, int z0 = 0, int zc = 0);
 // slab forward y pass storing straight into the peers' receive buffers (N2 = 256 only; -1 otherwise)
 int launch_ypass_peer(const Ctx& cx, cudaStream_t s);
+// slab green stage storing the z^-1 output straight into the peers' receive buffers (generic
+// tiled z pass; -1 where a specialised G pass is the production kernel)
+int launch_gpass_peer(const Ctx& cx, cudaStream_t s);
 int launch_gpass(const Ctx& cx, int mode, cudaStream_t s);
 int gpass_nblk(const Geo& g);  // CTAs (gamma partials per load) of the CG-mode G pass
 // zc0/nzl: 3D thermal only, z-chunks [zc0, zc0+nzl) of g.KZC planes (nzl = 0: all)

@@ -423,7 +423,7 @@ extern "C" uno_status uno_slab_forward_peer(uno_slab_handle* h, double* const* h
   SKL(launch_xfwd(h->cxy, CG, h->r, h->s));
   const Geo& g = h->gxy;
   const long long rows = (long long)g.nrhs * g.c * g.H1 * h->Z;
-  if (g.N2 == 256) {  // the y pass itself stores every bin into its owner's receive buffer
+  if (g.N2 == 256 || g.N2 == 512) {  // the y pass itself stores every bin into its owner's receive buffer
     Ctx cp = h->cxy;
     for (int q = 0; q < 8; ++q) cp.peer[q] = P.p[q];
     cp.peer_off = (long long)h->rank * rows * h->Yc;
@@ -446,8 +446,17 @@ extern "C" uno_status uno_slab_green_peer(uno_slab_handle* h, const double* d_re
   const dim3 gb(1, (unsigned)std::min<long long>(nlckx, 4096), h->nranks);
   slab_pencil_kernel<<<gb, 256, 0, h->s>>>(const_cast<double2*>(reinterpret_cast<const double2*>(d_recv)), h->pencil,
                                           nlckx, h->Z, h->Yc, h->gz.N3, 0);
-  SKL(launch_gpass(h->cz, CG, h->s));
-  slab_pencil_peer_kernel<<<gb, 256, 0, h->s>>>(P, h->rank, h->pencil, nlckx, h->Z, h->Yc, h->gz.N3);
+  // the z pass itself stores every plane into its owner's receive buffer where the tiled z pass
+  // is the production kernel (config 4: 512^3 elastic); otherwise G pass + peer pack
+  Ctx cp = h->cz;
+  for (int q = 0; q < 8; ++q) cp.peer[q] = P.p[q];
+  cp.peer_rank = h->rank;
+  cp.peer_z = h->Z;
+  cp.peer_nlckx = nlckx;
+  if (launch_gpass_peer(cp, h->s) < 0) {
+    SKL(launch_gpass(h->cz, CG, h->s));
+    slab_pencil_peer_kernel<<<gb, 256, 0, h->s>>>(P, h->rank, h->pencil, nlckx, h->Z, h->Yc, h->gz.N3);
+  }
   SCK(cudaGetLastError());
   return UNO_OK;
 }

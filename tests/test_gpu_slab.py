@@ -96,12 +96,14 @@ def test_peer_memory_exchange_equals_all_to_all(nranks, physics):
     assert [r["iterations"] for r in ra] == [r["iterations"] for r in rp] == [5, 5]
 
 
-@pytest.mark.parametrize("nranks", [2, 4])
-def test_peer_exchange_fused_in_y_pass(nranks):
-    # N2 = 256: the forward y pass (ypass256 PEER instance) stores each bin straight into the
-    # receive buffer of the rank that owns its k_y chunk — FFT and transpose in one kernel
+@pytest.mark.parametrize("nranks,n2", [(2, 256), (4, 256), (2, 512)])
+def test_peer_exchange_fused_in_y_pass(nranks, n2):
+    # N2 = 256 / 512: the forward y pass (ypass256 / ypass512 PEER instances) stores each bin
+    # straight into the receive buffer of the rank that owns its k_y chunk, and the tiled z pass
+    # (gpass_z PEER instance, N3 = 16) stores each plane into its owner's — FFT and transpose in
+    # one kernel both ways
     rng = np.random.default_rng(5)
-    ph = (rng.random((16, 256, 32)) < 0.3).astype(np.uint8)  # [N3][N2][N1]
+    ph = (rng.random((16, n2, 32)) < 0.3).astype(np.uint8)  # [N3][N2][N1]
     mat, loads = (1.0, 15.0), np.eye(3)[:2]
     ua, _ = slab(ph, "thermal", mat, 2, 77, 0.1, loads, 5, nranks)
     up, rp = slab(ph, "thermal", mat, 2, 77, 0.1, loads, 5, nranks, peer=True)
