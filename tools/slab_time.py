@@ -19,6 +19,7 @@ ap.add_argument("--grid", type=int, default=256)
 ap.add_argument("--physics", default="thermal")
 ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--ranks", type=int, nargs="+", default=[1, 2, 4])
+ap.add_argument("--peer", type=int, nargs="+", default=[0], help="0: all-to-all copies, 1: peer-memory exchange")
 a = ap.parse_args()
 n = a.grid
 dev = torch.device("cuda:0")
@@ -33,8 +34,8 @@ s = UnoCG(ph, a.physics, mat, nrhs=nrhs, seed=seed, amp=amp)
 s.solve(loads, fixed_iters=2)
 r = s.solve(loads, fixed_iters=a.iters)
 print(f"whole grid: {r.ms / a.iters * 1e3:.0f} us/iteration")
-for R in a.ranks:
-    sv = SlabSolver(ph, a.physics, mat, LocalComm(R), nrhs=nrhs, seed=seed, amp=amp)
+for R, peer in [(R, p) for R in a.ranks for p in a.peer]:
+    sv = SlabSolver(ph, a.physics, mat, LocalComm(R), nrhs=nrhs, seed=seed, amp=amp, peer=bool(peer))
     sv.solve(loads, fixed_iters=2)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -43,6 +44,6 @@ for R in a.ranks:
     sv.solve(loads, fixed_iters=a.iters, check_every=a.iters + 5)
     e1.record()
     torch.cuda.synchronize()
-    print(f"slab x{R} (emulated in one process): {e0.elapsed_time(e1) / a.iters * 1e3:.0f} us/iteration device "
+    print(f"slab x{R} {'peer' if peer else 'a2a '} (emulated in one process): {e0.elapsed_time(e1) / a.iters * 1e3:.0f} us/iteration device "
           f"(all ranks' work), host {1e6 * (time.time() - t0) / a.iters:.0f} us/iteration")
     sv.close()
