@@ -81,6 +81,11 @@ UNO_API uno_status uno_slab_kapply(uno_slab_handle* h, const double* d_halo_recv
  * ends with a system-scope fence.  UNO_ERR_ARG: null arrays / entries.                    */
 UNO_API uno_status uno_slab_forward_peer(uno_slab_handle* h, double* const* h_peer_recv);
 UNO_API uno_status uno_slab_green_peer(uno_slab_handle* h, const double* d_recv, double* const* h_peer_recv);
+/* Peer variant of inverse: the two boundary node planes of d go straight into the neighbours'
+ * halo receive buffers (h_peer_halo_recv: HOST array [nranks] of DEVICE pointers to every rank's
+ * halo receive buffer; my first plane -> recv[1] of rank-1, my last plane -> recv[0] of rank+1).
+ * Ordering as above (barrier before the neighbours' uno_slab_kapply).                      */
+UNO_API uno_status uno_slab_inverse_peer(uno_slab_handle* h, const double* d_recv, double* const* h_peer_halo_recv);
 
 /* Per-rank partial of a CG scalar (slot UNO_SLAB_*), written to d_out[nrhs] (device);
  * uno_slab_apply takes the cross-rank totals d_in[nrhs] and updates the CG state.       */

@@ -30,7 +30,7 @@ UNO_PRECOND = {"uno": 0, "identity": 1, "jacobi": 2}
 SLAB_EXPORTS = ("uno_slab_create", "uno_slab_destroy", "uno_slab_sizes", "uno_slab_begin", "uno_slab_forward",
                 "uno_slab_green", "uno_slab_inverse", "uno_slab_kapply", "uno_slab_reduce", "uno_slab_apply",
                 "uno_slab_state", "uno_slab_finish", "uno_slab_local_means", "uno_slab_subtract_means",
-                "uno_slab_forward_peer", "uno_slab_green_peer")
+                "uno_slab_forward_peer", "uno_slab_green_peer", "uno_slab_inverse_peer")
 
 
 class UnoCgDesc(C.Structure):
@@ -88,6 +88,7 @@ def _load():
     lib.uno_slab_subtract_means.argtypes = [P, P, P]
     lib.uno_slab_forward_peer.argtypes = [P, P]
     lib.uno_slab_green_peer.argtypes = [P, P, P]
+    lib.uno_slab_inverse_peer.argtypes = [P, P, P]
     for f in EXPORTS[:-2] + SLAB_EXPORTS:
         getattr(lib, f).restype = C.c_int
     lib.uno_cg_last_error.restype = C.c_char_p
@@ -284,6 +285,10 @@ def uno_slab_forward_peer(h: int, peer_recv_ptrs):
 
 def uno_slab_green_peer(h: int, d_recv, peer_recv_ptrs):
     _check(_lib.uno_slab_green_peer(h, _ptr(d_recv), _ptr_array(peer_recv_ptrs)), "uno_slab_green_peer")
+
+
+def uno_slab_inverse_peer(h: int, d_recv, peer_halo_recv_ptrs):
+    _check(_lib.uno_slab_inverse_peer(h, _ptr(d_recv), _ptr_array(peer_halo_recv_ptrs)), "uno_slab_inverse_peer")
 
 
 def uno_slab_inverse(h: int, d_recv, d_halo_send):

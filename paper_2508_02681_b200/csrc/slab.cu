@@ -121,6 +121,17 @@ __global__ void slab_pencil_peer_kernel(SlabPeers peers, int rank, const double2
   __threadfence_system();
 }
 // halo send: plane 0 and plane Z-1 of every (load, comp) slab of d -> out[2][lc][plane]
+// peer variant: my first plane -> recv[1] of rank-1, my last plane -> recv[0] of rank+1
+__global__ void slab_halo_peer_kernel(const double* __restrict__ d, double* lo_dst, double* hi_dst, int nlc, int Z,
+                                      long long plane) {
+  const long long tot = 2LL * nlc * plane;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    const long long side = e / ((long long)nlc * plane), rem = e - side * nlc * plane;
+    const long long lc = rem / plane, xy = rem - lc * plane;
+    (side ? hi_dst : lo_dst)[rem] = d[(lc * Z + (side ? Z - 1 : 0)) * plane + xy];
+  }
+  __threadfence_system();
+}
 __global__ void slab_halo_kernel(const double* __restrict__ d, double* __restrict__ out, int nlc, int Z, long long plane) {
   const long long tot = 2LL * nlc * plane;
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
@@ -486,6 +497,24 @@ extern "C" uno_status uno_slab_inverse(uno_slab_handle* h, const double* d_recv,
   const long long plane = (long long)g.N1 * g.N2;
   const int nlc = g.nrhs * g.c;
   slab_halo_kernel<<<grid_for(2LL * nlc * plane), 256, 0, h->s>>>(h->d, d_halo_send, nlc, h->Z, plane);
+  SCK(cudaGetLastError());
+  return UNO_OK;
+}
+
+extern "C" uno_status uno_slab_inverse_peer(uno_slab_handle* h, const double* d_recv, double* const* h_peer_halo_recv) {
+  if (!h || !d_recv || !h_peer_halo_recv || h->nranks > kMaxRanks) return sfail(UNO_ERR_ARG, "null argument");
+  const int n = h->nranks, lo = (h->rank + n - 1) % n, hi = (h->rank + 1) % n;
+  if (!h_peer_halo_recv[lo] || !h_peer_halo_recv[hi]) return sfail(UNO_ERR_ARG, "null peer halo pointer");
+  const Geo& g = h->gxy;
+  const long long rows = (long long)g.nrhs * g.c * g.H1 * h->Z;
+  slab_unpack_kernel<<<pack_grid(rows, h->Yc, h->nranks), pack_threads(h->Yc), 0, h->s>>>(
+      reinterpret_cast<const double2*>(d_recv), h->spec, rows, h->Yc, g.N2);
+  SKL(launch_ypass(h->cxy, CG, true, h->s));
+  SKL(launch_xinv(h->cxy, CG, nullptr, h->s));
+  const long long plane = (long long)g.N1 * g.N2;
+  const int nlc = g.nrhs * g.c;
+  slab_halo_peer_kernel<<<grid_for(2LL * nlc * plane), 256, 0, h->s>>>(h->d, h_peer_halo_recv[lo] + nlc * plane,
+                                                                       h_peer_halo_recv[hi], nlc, h->Z, plane);
   SCK(cudaGetLastError());
   return UNO_OK;
 }

@@ -176,6 +176,8 @@ class SlabSolver:
             rb, self.ptrB = comm.peer_buffers(R * 2 * blk, dev)
             self.recvA = [t.view(R, 2 * blk) for t in ra]
             self.recvB = [t.view(R, 2 * blk) for t in rb]
+            hr, self.ptrH = comm.peer_buffers(2 * hs, dev)
+            self.hrecv = [t.view(2, hs) for t in hr]
 
     def close(self):
         for h in self.handles:
@@ -201,9 +203,9 @@ class SlabSolver:
                 B.uno_slab_green_peer(h, ra, pb)  # z . G . z^-1; blocks stored into the peers' B
             c.peer_barrier()
             self._scalar(1, SUM)
-            for h, rb, hs in zip(H, self.recvB, self.hsend):
-                B.uno_slab_inverse(h, rb, hs)
-            c.halo(self.hsend, self.hrecv)
+            for h, rb, ph in zip(H, self.recvB, self.ptrH):
+                B.uno_slab_inverse_peer(h, rb, ph)  # boundary planes into the neighbours' halos
+            c.peer_barrier()
             for h, hr in zip(H, self.hrecv):
                 B.uno_slab_kapply(h, hr)
             self._scalar(2, SUM)
