@@ -1,0 +1,76 @@
+"""Seeded shape fuzz of the CUDA operators against the oracle: random power-of-two grids (within
+the library's limits, up to 2^17 nodes so the oracle stays fast), both physics, periodic /
+mixed (Dirichlet z) / all-Dirichlet boundaries and 1-3 load cases.  Every draw reaches a
+different combination of the size-specialised kernels (256/512-point passes, elastic G pass,
+adaptive K chunking, DST passes) and their tile tails.  Tolerances as in test_gpu_parity.py,
+with the bound for P growing as N_max^2 (the oracle's probed-symbol accuracy, see below)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import fem, greens  # noqa: E402
+from paper_2508_02681_b200 import synth  # noqa: E402
+
+
+def rel(a, b):
+    return float(np.linalg.norm((a - b).ravel()) / max(np.linalg.norm(b.ravel()), 1e-300))
+
+
+def _draw(seed):
+    rng = np.random.default_rng(1000 + seed)
+    physics = "thermal" if rng.random() < 0.5 else "elastic"
+    bc = [(0, 0, 0), (0, 0, 1), (1, 1, 1)][rng.integers(0, 3)]
+    while True:
+        lo1 = 32 if (physics == "thermal" and bc != (0, 0, 0)) or physics == "thermal" else 16
+        N1 = int(2 ** rng.integers(int(np.log2(lo1)), 9))
+        N2 = int(2 ** rng.integers(4 if bc == (1, 1, 1) else 3, 10))
+        N3 = int(2 ** rng.integers(3, 10))
+        if N1 * N2 * N3 <= 1 << 17:
+            break
+    return physics, bc, (N1, N2, N3), int(rng.integers(1, 4)), int(rng.integers(0, 2 ** 31))
+
+
+def _pad_dir(u):  # all-Dirichlet oracle interior field -> library padded storage
+    out = np.zeros((u.shape[0],) + tuple(s + 1 for s in u.shape[1:]))
+    out[:, 1:, 1:, 1:] = u
+    return out
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_operators_random_shapes(seed):
+    from paper_2508_02681_b200.api import UnoCG
+
+    physics, bc, N, nrhs, pseed = _draw(seed)
+    rng = np.random.default_rng(pseed)
+    ph = (rng.random(tuple(reversed(N))) < 0.35).astype(np.uint8)
+    c = 1 if physics == "thermal" else 3
+    if physics == "thermal":
+        mat, amp = (1.0, float(rng.uniform(2, 50))), 0.1
+    else:
+        mat, amp = (synth.lame_from_E_nu(1.0, 0.3), synth.lame_from_E_nu(float(rng.uniform(2, 20)), 0.2)), 0.05
+    g = fem.Grid(N, bc=bc, c=c, h=1.0 / N[0])
+    s = UnoCG(torch.from_numpy(ph).cuda(), physics, mat, nrhs=nrhs, seed=7 + seed, amp=amp, bc=bc)
+    u = np.stack([synth.test_vector(50 + l, g.field_shape()) for l in range(nrhs)])
+    pad = _pad_dir if bc == (1, 1, 1) else (lambda v: v)
+    ud = torch.from_numpy(np.stack([pad(v) for v in u])).cuda()
+    Ku = s.apply_K(ud).cpu().numpy()
+    z = s.apply_precond(ud).cpu().numpy()
+    if bc == (0, 0, 0):
+        G = greens.ghat(g, physics, mat, 7 + seed, amp)
+        P = lambda r: greens.apply_precond(G, r)  # noqa: E731
+    elif bc == (0, 0, 1):
+        G = greens.ghat_mixed(g, physics, mat, 7 + seed, amp)
+        P = lambda r: greens.apply_precond_mixed(G, r)  # noqa: E731
+    else:
+        G = greens.ghat_dirichlet(g, physics, mat, 7 + seed, amp)
+        P = lambda r: greens.apply_precond_dirichlet(G, r)  # noqa: E731
+    # the oracle probes the symbol numerically; at the lowest frequency (theta = 2 pi / N, symbol
+    # ~ theta^2) the probe cancels to ~ eps / theta^2 relative, so the bound grows as N_max^2
+    # (the library evaluates the symbol in closed form; cf. test_maximum_axis_lengths)
+    tol_p = max(1e-12, 2e-16 * max(N) ** 2)
+    for l in range(nrhs):
+        assert rel(Ku[l], pad(fem.apply_K(g, physics, ph, mat, u[l]))) <= 1e-13, (physics, bc, N, nrhs)
+        assert rel(z[l], pad(P(u[l]))) <= tol_p, (physics, bc, N, nrhs)
+    s.close()
