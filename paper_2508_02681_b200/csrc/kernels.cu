@@ -2781,6 +2781,10 @@ int blocks_needed_max(const Geo& g) {
   } else {
     kb = (g.n + 255) / 256;
   }
+  // grid-stride passes of the baseline preconditioners and the Dirichlet dot (precond.cu,
+  // dirichlet.cu: up to 148 x 8 CTAs): a preconditioner can be switched on any handle
+  const long long jb = jacobi_nblk(g);
+  kb = kb > jb ? kb : jb;
   return (int)(m > kb ? m : kb);
 }
 

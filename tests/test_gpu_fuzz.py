@@ -74,3 +74,32 @@ def test_operators_random_shapes(seed):
         assert rel(Ku[l], pad(fem.apply_K(g, physics, ph, mat, u[l]))) <= 1e-13, (physics, bc, N, nrhs)
         assert rel(z[l], pad(P(u[l]))) <= tol_p, (physics, bc, N, nrhs)
     s.close()
+
+
+@pytest.mark.parametrize("seed", range(100, 116))
+def test_fixed_iteration_solves_random_shapes(seed):
+    # the CG-fused passes (r update + ||r||_inf in the x pass, d / u updates in the inverse pass,
+    # device-side scalars, graph loop) on random shapes: 3 fixed iterations against the oracle
+    from oracle import homog
+    from paper_2508_02681_b200.api import UnoCG
+
+    physics, bc, N, nrhs, pseed = _draw(seed)
+    rng = np.random.default_rng(pseed)
+    ph = (rng.random(tuple(reversed(N))) < 0.35).astype(np.uint8)
+    c = 1 if physics == "thermal" else 3
+    mat = (1.0, 12.0) if physics == "thermal" else (synth.lame_from_E_nu(1.0, 0.3), synth.lame_from_E_nu(8.0, 0.2))
+    amp = 0.1 if physics == "thermal" else 0.05
+    g = fem.Grid(N, bc=bc, c=c, h=1.0 / N[0])
+    nv = 3 if physics == "thermal" else 6
+    loads = np.zeros((nrhs, nv))
+    for l in range(nrhs):
+        loads[l, l % nv] = 1.0
+        loads[l, (l + 2) % nv] += 0.3
+    s = UnoCG(torch.from_numpy(ph).cuda(), physics, mat, nrhs=nrhs, seed=11, amp=amp, bc=bc)
+    u = s.solve(loads, fixed_iters=3).u.cpu().numpy()
+    ref = homog.solve_problem(g, physics, ph, mat, loads, 11, amp, fixed_iters=3)
+    pad = _pad_dir if bc == (1, 1, 1) else (lambda v: v)
+    tol = max(1e-10, 10 * 2e-16 * max(N) ** 2)
+    for l in range(nrhs):
+        assert rel(u[l], pad(ref["U"][l])) <= tol, (physics, bc, N, nrhs)
+    s.close()

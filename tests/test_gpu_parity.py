@@ -714,3 +714,23 @@ def test_all_dirichlet_256_point_dst(N, physics):
     # the register-direct DST-I pass (N = 256 on the x, y or z axis; odd extension of length 512,
     # the scalar symbol fused into the last forward pass for c = 1) against the oracle
     test_all_dirichlet_operators(N, physics)
+
+
+@pytest.mark.parametrize("bc,precond", [((0, 0, 0), "jacobi"), ((0, 0, 0), "identity"), ((1, 1, 1), "uno")])
+def test_multi_load_partials_do_not_overlap(bc, precond):
+    # regression (found by tests/test_gpu_fuzz.py): the grid-stride baseline / Dirichlet-dot passes
+    # write up to 148 x 8 CTA partials per load; with fewer reserved per load, load 0's tail landed
+    # in load 1's slots.  Each load of a 2-load solve must reproduce its 1-load solve.
+    from paper_2508_02681_b200.api import UnoCG
+
+    N = (64, 64, 32)
+    rng = np.random.default_rng(5)
+    ph = torch.from_numpy((rng.random(tuple(reversed(N))) < 0.35).astype(np.uint8)).to(dev())
+    mat = (synth.lame_from_E_nu(1.0, 0.3), synth.lame_from_E_nu(8.0, 0.2))
+    loads = np.eye(6)[:2]
+    s2 = UnoCG(ph, "elastic", mat, nrhs=2, seed=11, amp=0.05, bc=bc, precond=precond)
+    u2 = s2.solve(loads, fixed_iters=3).u.cpu().numpy()
+    for l in range(2):
+        s1 = UnoCG(ph, "elastic", mat, nrhs=1, seed=11, amp=0.05, bc=bc, precond=precond)
+        u1 = s1.solve(loads[l:l + 1], fixed_iters=3).u.cpu().numpy()[0]
+        assert rel(u2[l], u1) <= 1e-13, (bc, precond, l, rel(u2[l], u1))
