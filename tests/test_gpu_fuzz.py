@@ -103,3 +103,43 @@ def test_fixed_iteration_solves_random_shapes(seed):
     for l in range(nrhs):
         assert rel(u[l], pad(ref["U"][l])) <= tol, (physics, bc, N, nrhs)
     s.close()
+
+
+@pytest.mark.parametrize("seed", range(200, 224))
+def test_fixed_iteration_solves_random_loads_and_preconditioners(seed):
+    # 2D and 3D periodic grids, 1-8 load cases, P in {UNO, Jacobi, identity}: 2 fixed iterations
+    # of every load against the oracle (per-load reductions, the baselines' fused passes)
+    from oracle import baselines, homog
+    from paper_2508_02681_b200.api import UnoCG
+
+    rng = np.random.default_rng(seed)
+    d = int(rng.integers(2, 4))
+    physics = "thermal" if rng.random() < 0.5 else "elastic"
+    precond = ["uno", "jacobi", "identity"][rng.integers(0, 3)]
+    nrhs = int(rng.integers(1, 9))
+    while True:
+        N = tuple(int(2 ** rng.integers(4 if (i == 0 and physics == "elastic") else 3, 9 if d == 3 else 10)) for i in range(d))
+        if np.prod(N) <= (1 << 16):
+            break
+    ph = (rng.random(tuple(reversed(N))) < 0.4).astype(np.uint8)
+    c = 1 if physics == "thermal" else d
+    mat = (1.0, 9.0) if physics == "thermal" else (synth.lame_from_E_nu(1.0, 0.3), synth.lame_from_E_nu(6.0, 0.2))
+    amp = 0.1 if physics == "thermal" else 0.05
+    g = fem.Grid(N, c=c, h=1.0 / N[0])
+    nv = d if physics == "thermal" else d * (d + 1) // 2
+    loads = rng.standard_normal((nrhs, nv))
+    s = UnoCG(torch.from_numpy(ph).cuda(), physics, mat, nrhs=nrhs, seed=13, amp=amp, precond=precond)
+    u = s.solve(loads, fixed_iters=2).u.cpu().numpy()
+    for l in range(nrhs):
+        if precond == "uno":
+            ref = homog.solve_problem(g, physics, ph, mat, loads[l:l + 1], 13, amp, fixed_iters=2)["U"][0]
+        else:
+            ref = pcg_mean_free(baselines.solve(g, physics, ph, mat, loads[l], precond, fixed_iters=2).u)
+        assert rel(u[l], ref) <= 1e-10, (d, physics, precond, N, nrhs, l)
+    s.close()
+
+
+def pcg_mean_free(u):
+    from oracle import pcg
+
+    return pcg.remove_mean(u)
