@@ -110,3 +110,29 @@ def test_peer_exchange_fused_in_y_pass(nranks, n2):
     assert np.array_equal(ua, up) and [r["iterations"] for r in rp] == [5, 5]
     uw, _ = whole(ph, "thermal", mat, 2, 77, 0.1, loads, 5)
     assert rel(up, uw) <= 1e-11
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_slab_random_shapes(seed):
+    # random grids, 1/2/4 emulated ranks, both exchange paths: the slab iterates equal the
+    # whole-grid solver's (3 fixed iterations)
+    rng = np.random.default_rng(700 + seed)
+    physics = "thermal" if rng.random() < 0.6 else "elastic"
+    R = int([1, 2, 4][rng.integers(0, 3)])
+    while True:
+        N1 = int(2 ** rng.integers(5 if physics == "thermal" else 4, 8))
+        N2 = int(2 ** rng.integers(max(4, int(np.log2(8 * R))), 9))
+        N3 = int(2 ** rng.integers(max(3, int(np.log2(2 * R))), 8))
+        if N1 * N2 * N3 <= 1 << 18 and N2 // R >= 8 and N3 // R >= 2:
+            break
+    nrhs = int(rng.integers(1, 4))
+    ph = (rng.random((N3, N2, N1)) < 0.3).astype(np.uint8)
+    if physics == "thermal":
+        mat, loads = (1.0, 7.0), np.eye(3)[:nrhs]
+    else:
+        mat, loads = (synth.lame_from_E_nu(1.0, 0.3), synth.lame_from_E_nu(5.0, 0.2)), np.eye(6)[:nrhs]
+    peer = bool(rng.integers(0, 2))
+    us, reps = slab(ph, physics, mat, nrhs, 21, 0.05, loads, 3, R, peer=peer)
+    uw, _ = whole(ph, physics, mat, nrhs, 21, 0.05, loads, 3)
+    assert [r["iterations"] for r in reps] == [3] * nrhs
+    assert rel(us, uw) <= 1e-11, (physics, R, (N1, N2, N3), nrhs, peer)
