@@ -23,12 +23,12 @@ namespace uno {
 constexpr int KM_TX = 16, KM_TY = 8, KM_T = 160;
 constexpr int KM_DW = KM_TX + 2, KM_DH = KM_TY + 2, KM_DP = KM_DW * KM_DH;  // 18 x 10 node tile
 constexpr int KM_EW = KM_TX + 1, KM_EH = KM_TY + 1, KM_NE = KM_EW * KM_EH;  // 17 x 9 elements
-constexpr int KM_RING = 4;
+constexpr int KM_RING = 8, KM_LA = 4;  // ring slots; planes prefetched ahead
 constexpr int KM_PLANE = 3 * KM_DP;                 // doubles per ring slot (3 components)
 constexpr int KM_NCP = (KM_PLANE + KM_T - 1) / KM_T;  // cp.async per thread per plane
 
 __host__ __device__ constexpr int km_smem_bytes() {
-  return (KM_RING * KM_PLANE + 12 * KM_NE) * (int)sizeof(double);
+  return (KM_RING * KM_PLANE + 2 * 12 * KM_NE) * (int)sizeof(double);
 }
 
 __global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int mode, const double* __restrict__ src,
@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int
   const int dz = g.dirz;
   extern __shared__ double kms[];
   double* D = kms;                           // [RING][3][10][18]
-  double* Lb = D + KM_RING * KM_PLANE;       // [12][NE] node-plane outputs of the current layer
+  double* Lb0 = D + KM_RING * KM_PLANE;      // [2][12][NE] node-plane outputs, double-buffered by layer parity
   __shared__ double red_sh[32];
   const int t = threadIdx.x;
   const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
@@ -142,16 +142,16 @@ __global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int
 #pragma unroll
       for (int al = 0; al < 3; ++al) modal::wht4(o + al);
 #pragma unroll
-      for (int i = 0; i < 12; ++i) Lb[i * KM_NE + t] = o[i];
+      for (int i = 0; i < 12; ++i) Lb0[((k & 1) * 12 + i) * KM_NE + t] = o[i];
     }
   };
-  // prologue: planes zs-1 .. zs+2 in flight; element layer zs-1 (its upper faces feed plane zs)
+  // prologue: planes zs-1 .. zs+3 in flight; element layer zs-1 (its upper faces feed plane zs)
 #pragma unroll 1
-  for (int p = zs - 1; p <= zs + 2; ++p) {
+  for (int p = zs - 1; p <= zs - 1 + KM_LA; ++p) {
     if (p <= ze) issue_plane(p);
     cp_commit();
   }
-  cp_wait<2>();  // planes zs-1, zs
+  cp_wait<KM_LA - 1>();  // planes zs-1, zs
   __syncthreads();
   if (eth) {
     read_corners(zs - 1, uc);
@@ -161,19 +161,23 @@ __global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int
 #pragma unroll
   for (int i = 0; i < 12; ++i) vc[i] = 0.0;
   element_layer(zs - 1, false);
+  cp_wait<KM_LA - 2>();  // plane zs+1 (read by the first layer of the loop)
+  __syncthreads();
   const bool nth = t < KM_TX * KM_TY;
   const int tx = t % KM_TX, ty = t / KM_TX;
   double part = 0.0;
+  // One barrier per layer: it publishes this layer's outputs (Lb, double-buffered by parity so the
+  // next layer may be written while slow threads still gather this one), makes plane k+2 visible
+  // for the next layer, and frees the slot refilled with plane k+4 (last read four layers ago).
 #pragma unroll 1
   for (int k = zs; k < ze; ++k) {
-    cp_wait<1>();  // planes k, k+1 landed (plane k+2 may still be in flight)
-    __syncthreads();
-    // refill the slot of plane k-1 only now: every thread has left step k-1 (its node phase read it)
-    if (k + 3 <= ze) issue_plane(k + 3);
-    cp_commit();
     element_layer(k, true);
+    cp_wait<KM_LA - 3>();  // plane k+2 landed (k+3 may still be in flight)
     __syncthreads();
+    if (k + KM_LA <= ze) issue_plane(k + KM_LA);
+    cp_commit();
     if (nth) {
+      const double* Lb = Lb0 + (k & 1) * 12 * KM_NE;
       double p[3] = {0.0, 0.0, 0.0};
 #pragma unroll
       for (int o = 0; o < 4; ++o) {
