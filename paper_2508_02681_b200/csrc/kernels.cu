@@ -574,6 +574,14 @@ __global__ void __launch_bounds__(fft_threads(L), L == 256 ? UNO_GMINB : 1) gpas
     }
   }
   constexpr bool STG = gstaged<L, NC>() && MODE != FWDZ;
+  if constexpr (!STG && MODE != FWDZ) {
+    // symbol too large to stage with the tile (L = 512, c = 3): pull its rows (8 bins, 64 bytes
+    // each) into L2 now so the reads inside the fused butterfly hit L2 rather than DRAM
+    for (int r = t; r < NCC * L; r += T) {
+      const int ent = r / L, kz = r - ent * L;
+      asm volatile("prefetch.global.L2 [%0];\n" ::"l"(cx.gtab + ent * g.nspec + boff + (long long)kz * g.N2));
+    }
+  }
   if (STG) {
 #pragma unroll
     for (int q = 0; q < NCC; ++q) {
