@@ -217,6 +217,91 @@ __global__ void __launch_bounds__(128) xfwd256_kernel(Ctx cx, const double* __re
   if (MODE == CG) partial_write<true>(cx, RED_RNORM, load, bx, mx, red_sh);
 }
 
+// F1 for N1 = 512 (config 4), register-direct: the complex FFT of length M = 256 (z_j = r_2j +
+// i r_2j+1) as DFT16 over n2 (j = n1 + 16 n2, thread = n1, 16 threads per row) -> twiddle
+// w_256^{n1 k1} -> padded transpose -> DFT16 over n1 (thread = k1) -> X[k1 + 16 k2] into a row
+// buffer (stride 257, odd: conflict-free both ways; it reuses the transpose buffer) -> R2C
+// post-processing straight to the half spectrum.  CG: r -= alpha p, ||r||_inf, r write-back on
+// the loaded registers, as in xfwd256_kernel.
+constexpr int X5_RS = 16 * 17, X5_XS = 257;
+template <int MODE>
+__global__ void __launch_bounds__(128) xfwd512_kernel(Ctx cx, const double* __restrict__ src, int bofs) {
+  constexpr int M = 256;
+  const Geo g = cx.g;
+  const int load = blockIdx.y;
+  LoadState* st = cx.st + load;
+  if (MODE != STANDALONE && !st->active) return;
+  __shared__ double2 tb[8 * X5_RS];  // transpose buffer, then the X rows (8 x 257 <= 8 x 272)
+  __shared__ double2 tw[M];
+  __shared__ double2 twp[M + 1];
+  __shared__ double red_sh[32];
+  const int t = threadIdx.x;
+  const int r = t >> 4, l16 = t & 15;
+  const int bx = bofs + blockIdx.x;
+  const long long row0 = (long long)bx * 8;  // row = (comp, z, y)
+  const long long voff = (long long)load * g.c * g.n + (row0 + r) * g.N1;
+  const double2* s2 = reinterpret_cast<const double2*>(src + voff);
+  double2 v[16];
+#pragma unroll
+  for (int n2 = 0; n2 < 16; ++n2) v[n2] = __ldcg(s2 + l16 + 16 * n2);
+  double mx = 0.0;
+  if (MODE == CG) {
+    if (st->iters > 0) {  // r <- r - alpha p   (Alg 2 l.11)
+      const double alpha = st->alpha;
+      const double2* p2 = reinterpret_cast<const double2*>(cx.p + voff);
+      double2* r2 = reinterpret_cast<double2*>(cx.r + voff);
+#pragma unroll
+      for (int h8 = 0; h8 < 16; h8 += 8) {
+        double2 pv[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) pv[i] = __ldcs(p2 + l16 + 16 * (h8 + i));
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          v[h8 + i].x = fma(-alpha, pv[i].x, v[h8 + i].x);
+          v[h8 + i].y = fma(-alpha, pv[i].y, v[h8 + i].y);
+          __stcg(r2 + l16 + 16 * (h8 + i), v[h8 + i]);
+        }
+      }
+    }
+#pragma unroll
+    for (int n2 = 0; n2 < 16; ++n2) mx = fmax(mx, fmax(fabs(v[n2].x), fabs(v[n2].y)));
+  }
+  for (int i = t; i < M; i += 128) tw[i] = cx.tw.x[((i & 15) * (i >> 4)) & (M - 1)];  // [k1][n1]
+  for (int i = t; i <= M; i += 128) twp[i] = cx.tw.xpost[i];
+  __syncthreads();
+  dft_reg<16, false>(v);  // thread = n1: over n2 -> k1
+#pragma unroll
+  for (int k1 = 1; k1 < 16; ++k1) v[k1] = cmul(v[k1], tw[k1 * 16 + l16]);
+#pragma unroll
+  for (int k1 = 0; k1 < 16; ++k1) tb[r * X5_RS + k1 * 17 + l16] = v[k1];
+  __syncthreads();
+#pragma unroll
+  for (int n1 = 0; n1 < 16; ++n1) v[n1] = tb[r * X5_RS + l16 * 17 + n1];
+  dft_reg<16, false>(v);  // thread = k1: v[k2] = X[k1 + 16 k2]
+  __syncthreads();        // every transpose read done: the buffer becomes the X rows
+  double2* xs = tb;
+#pragma unroll
+  for (int k2 = 0; k2 < 16; ++k2) xs[r * X5_XS + l16 + 16 * k2] = v[k2];
+  __syncthreads();
+  // R2C post-processing: bins k and M - k of row c
+  const int y0 = (int)(row0 % g.N2);
+  const long long zc = row0 / g.N2;
+  const int z = (int)(zc % g.P3);
+  const int comp = (int)(zc / g.P3);
+  double2* out = cx.spec + ((long long)load * g.c + comp) * g.nspec + (long long)z * g.N2 + y0;
+  const long long plane = (long long)g.P3 * g.N2;
+  for (int it = t; it < (M / 2 + 1) * 8; it += 128) {
+    const int c = it & 7, k = it >> 3;
+    const double2 a = xs[c * X5_XS + k];
+    const double2 b = cconj(xs[c * X5_XS + ((M - k) & (M - 1))]);
+    const double2 E = make_double2(0.5 * (a.x + b.x), 0.5 * (a.y + b.y));
+    const double2 O = mul_mi(make_double2(0.5 * (a.x - b.x), 0.5 * (a.y - b.y)));
+    __stcg(out + (long long)k * plane + c, cadd(E, cmul(twp[k], O)));
+    if (k != M - k) __stcg(out + (long long)(M - k) * plane + c, cadd(cconj(E), cmul(twp[M - k], cconj(O))));
+  }
+  if (MODE == CG) partial_write<true>(cx, RED_RNORM, load, bx, mx, red_sh);
+}
+
 // F5 / standalone inverse: half spectrum -> real rows; CG epilogue d = s + beta d, u += alpha d_old.
 template <int M, int MODE>
 __global__ void __launch_bounds__(fft_threads(M)) xinv_kernel(Ctx cx, double* __restrict__ dst, int bofs) {
@@ -2389,6 +2474,12 @@ int launch_xfwd(const Ctx& cx, int mode, const double* src, cudaStream_t s, int 
     const dim3 grid(nb > 0 ? (unsigned)nb : (unsigned)((long long)g.c * g.P3 * g.N2 / 8), g.nrhs);
     if (mode == CG) xfwd256_kernel<CG><<<grid, 128, 0, s>>>(cx, src, b0);
     else xfwd256_kernel<STANDALONE><<<grid, 128, 0, s>>>(cx, src, b0);
+    return 1;
+  }
+  if (rd && g.N1 == 512 && mode != PLAIN) {
+    const dim3 grid(nb > 0 ? (unsigned)nb : (unsigned)((long long)g.c * g.P3 * g.N2 / 8), g.nrhs);
+    if (mode == CG) xfwd512_kernel<CG><<<grid, 128, 0, s>>>(cx, src, b0);
+    else xfwd512_kernel<STANDALONE><<<grid, 128, 0, s>>>(cx, src, b0);
     return 1;
   }
   return dispatch_pow2(g.M, [&](auto Lc) {

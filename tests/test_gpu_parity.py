@@ -734,3 +734,21 @@ def test_multi_load_partials_do_not_overlap(bc, precond):
         s1 = UnoCG(ph, "elastic", mat, nrhs=1, seed=11, amp=0.05, bc=bc, precond=precond)
         u1 = s1.solve(loads[l:l + 1], fixed_iters=3).u.cpu().numpy()[0]
         assert rel(u2[l], u1) <= 1e-13, (bc, precond, l, rel(u2[l], u1))
+
+
+@pytest.mark.parametrize("N,physics", [((512, 16, 8), "thermal"), ((512, 16, 8), "elastic"), ((512, 8, 16), "thermal")])
+def test_512_point_x_pass(N, physics):
+    # the register-direct x pass for N1 = 512 (config 4's N1: complex length 256 = 16 x 16, R2C
+    # post-processing, fused r -= alpha p and ||r||_inf) in the preconditioner and a short solve
+    g, ph, mat, amp, seed = make_case(N, physics)
+    s = solver(ph, physics, mat, 2, seed, amp)
+    G = greens.ghat(g, physics, mat, seed, amp)
+    r = np.stack([synth.test_vector(101 + l, g.field_shape()) for l in range(2)])
+    z = s.apply_precond(torch.from_numpy(r).to(dev())).cpu().numpy()
+    for l in range(2):
+        assert rel(z[l], greens.apply_precond(G, r[l])) <= 2e-16 * 512 ** 2  # long axis
+    load = loads_for(physics, 3, 2)
+    fx = homog.solve_problem(g, physics, ph, mat, load, seed, amp, fixed_iters=4)
+    u = solver(ph, physics, mat, 2, seed, amp).solve(load, fixed_iters=4).u.cpu().numpy()
+    for l in range(2):
+        assert rel(u[l], fx["U"][l]) <= 1e-9
