@@ -2470,15 +2470,17 @@ int launch_xfwd(const Ctx& cx, int mode, const double* src, cudaStream_t s, int 
     const char* e = getenv("UNO_XRD");
     return !(e && e[0] == '0');
   }();
-  if (rd && g.N1 == 256 && mode != PLAIN) {
+  if (rd && g.N1 == 256) {
     const dim3 grid(nb > 0 ? (unsigned)nb : (unsigned)((long long)g.c * g.P3 * g.N2 / 8), g.nrhs);
     if (mode == CG) xfwd256_kernel<CG><<<grid, 128, 0, s>>>(cx, src, b0);
+    else if (mode == PLAIN) xfwd256_kernel<PLAIN><<<grid, 128, 0, s>>>(cx, src, b0);
     else xfwd256_kernel<STANDALONE><<<grid, 128, 0, s>>>(cx, src, b0);
     return 1;
   }
-  if (rd && g.N1 == 512 && mode != PLAIN) {
+  if (rd && g.N1 == 512) {
     const dim3 grid(nb > 0 ? (unsigned)nb : (unsigned)((long long)g.c * g.P3 * g.N2 / 8), g.nrhs);
     if (mode == CG) xfwd512_kernel<CG><<<grid, 128, 0, s>>>(cx, src, b0);
+    else if (mode == PLAIN) xfwd512_kernel<PLAIN><<<grid, 128, 0, s>>>(cx, src, b0);
     else xfwd512_kernel<STANDALONE><<<grid, 128, 0, s>>>(cx, src, b0);
     return 1;
   }

@@ -752,3 +752,21 @@ def test_512_point_x_pass(N, physics):
     u = solver(ph, physics, mat, 2, seed, amp).solve(load, fixed_iters=4).u.cpu().numpy()
     for l in range(2):
         assert rel(u[l], fx["U"][l]) <= 1e-9
+
+
+@pytest.mark.parametrize("N,physics", [((256, 16, 16), "thermal"), ((512, 16, 8), "elastic")])
+def test_mixed_register_direct_x_pass(N, physics):
+    # the mixed schedule runs the x pass in PLAIN mode (rt -> spectrum, no CG fusion): the
+    # register-direct 256 / 512 instances against the oracle (operators and a short solve)
+    g, ph, mat, amp, seed = mixed_case(N, physics)
+    s = msolver(ph, physics, mat, 2, seed, amp)
+    u = np.stack([synth.test_vector(60 + l, g.field_shape()) for l in range(2)])
+    G = greens.ghat_mixed(g, physics, mat, seed, amp)
+    z = s.apply_precond(torch.from_numpy(u).to(dev())).cpu().numpy()
+    for l in range(2):
+        assert rel(z[l], greens.apply_precond_mixed(G, u[l])) <= 2e-16 * max(N) ** 2
+    loads = np.eye(3 if physics == "thermal" else 6)[[0, 1]]
+    fx = homog.solve_problem(g, physics, ph, mat, loads, seed, amp, fixed_iters=4)
+    us = msolver(ph, physics, mat, 2, seed, amp).solve(loads, fixed_iters=4).u.cpu().numpy()
+    for l in range(2):
+        assert rel(us[l], fx["U"][l]) <= 1e-9
