@@ -143,3 +143,32 @@ def pcg_mean_free(u):
     from oracle import pcg
 
     return pcg.remove_mean(u)
+
+
+@pytest.mark.parametrize("seed", range(300, 316))
+def test_eight_load_solves_equal_single_load_solves(seed):
+    # per-load reductions / state at larger random grids (no oracle needed): each load of an
+    # 8-load solve reproduces its 1-load solve (guards the per-load partial stride, state and
+    # early-exit logic of every pass; cf. test_multi_load_partials_do_not_overlap)
+    from paper_2508_02681_b200.api import UnoCG
+
+    rng = np.random.default_rng(seed)
+    physics = "thermal" if rng.random() < 0.5 else "elastic"
+    bc = [(0, 0, 0), (0, 0, 1), (1, 1, 1)][rng.integers(0, 3)]
+    precond = "uno" if bc != (0, 0, 0) else ["uno", "jacobi", "identity"][rng.integers(0, 3)]
+    while True:
+        N = (int(2 ** rng.integers(5, 9)), int(2 ** rng.integers(4, 9)), int(2 ** rng.integers(3, 9)))
+        if np.prod(N) <= (1 << 21) and (physics == "thermal" or np.prod(N) <= (1 << 19)):
+            break
+    ph = torch.from_numpy((rng.random(tuple(reversed(N))) < 0.3).astype(np.uint8)).cuda()
+    mat = (1.0, 10.0) if physics == "thermal" else (synth.lame_from_E_nu(1.0, 0.3), synth.lame_from_E_nu(7.0, 0.2))
+    nv = 3 if physics == "thermal" else 6
+    loads = rng.standard_normal((8, nv))
+    s8 = UnoCG(ph, physics, mat, nrhs=8, seed=3, amp=0.05, bc=bc, precond=precond)
+    u8 = s8.solve(loads, fixed_iters=3).u.cpu().numpy()
+    s8.close()
+    s1 = UnoCG(ph, physics, mat, nrhs=1, seed=3, amp=0.05, bc=bc, precond=precond)
+    for l in range(8):
+        u1 = s1.solve(loads[l:l + 1], fixed_iters=3).u.cpu().numpy()[0]
+        assert rel(u8[l], u1) <= 1e-12, (physics, bc, precond, N, l, rel(u8[l], u1))
+    s1.close()
