@@ -409,6 +409,112 @@ __global__ void __launch_bounds__(fft_threads(M)) xinv_kernel(Ctx cx, double* __
   }
 }
 
+// F5 for N1 = 512 (config 4), register-direct: the 257 half-spectrum bins of 8 rows land in
+// shared memory (row-major, stride 257: conflict-free); thread (row, k1) forms its 16 C2R
+// inputs Z[k1 + 16 k2] = (X_k + conj X_{M-k}) + i (X_k - conj X_{M-k}) conj(w^k_post) directly,
+// runs the inverse four-step (DFT16 over k2 -> twiddle conj w_256^{n1 k1} -> transpose -> DFT16
+// over k1) and holds x[n1 + 16 n2] = (s_2j, s_2j+1) in registers for the CG epilogue
+// d = s + beta d_old, u += alpha d_old (Alg 2 l.8, l.12).  Same arithmetic as xinv_kernel<256>.
+constexpr int XI5_SS = 257, XI5_RS = 16 * 17;
+template <int MODE>
+__global__ void __launch_bounds__(128) xinv512_kernel(Ctx cx, double* __restrict__ dst, int bofs) {
+  constexpr int M = 256;
+  const Geo g = cx.g;
+  const int load = blockIdx.y;
+  LoadState* st = cx.st + load;
+  if (MODE != STANDALONE && !st->active) return;
+  __shared__ double2 sb[8 * XI5_RS];  // spectrum rows [8][257], then the transpose buffer [8][16][17]
+  __shared__ double2 tw[M];
+  __shared__ double2 twp[M + 1];
+  const int t = threadIdx.x;
+  const int r = t >> 4, l16 = t & 15;
+  const long long row0 = (long long)(bofs + blockIdx.x) * 8;
+  const int y0 = (int)(row0 % g.N2);
+  const long long zc = row0 / g.N2;
+  const int z = (int)(zc % g.P3);
+  const int comp = (int)(zc / g.P3);
+  const double2* in = cx.spec + ((long long)load * g.c + comp) * g.nspec + (long long)z * g.N2 + y0;
+  const long long plane = (long long)g.P3 * g.N2;
+#pragma unroll
+  for (int i = 0; i < ((M + 1) * 8 + 127) / 128; ++i) {  // bin k of row c -> sb[c][k]
+    const int e = t + i * 128;
+    if (e < (M + 1) * 8) cp_async16(&sb[(e & 7) * XI5_SS + (e >> 3)], in + (long long)(e >> 3) * plane + (e & 7));
+  }
+  cp_commit();
+  if (MODE == CG && st->iters > 0) {  // the 8 rows of d_old and u (2 x 32 KB) into L2 for the epilogue
+    const char* db = reinterpret_cast<const char*>(cx.d + (long long)load * g.c * g.n + row0 * g.N1);
+    const char* ub = reinterpret_cast<const char*>(cx.u + (long long)load * g.c * g.n + row0 * g.N1);
+    for (int i = t; i < 8 * 512 * 8 / 128; i += 128) {
+      asm volatile("prefetch.global.L2 [%0];\n" ::"l"(db + 128LL * i));
+      asm volatile("prefetch.global.L2 [%0];\n" ::"l"(ub + 128LL * i));
+    }
+  }
+  for (int i = t; i < M; i += 128) tw[i] = cx.tw.x[((i & 15) * (i >> 4)) & (M - 1)];  // [k1][n1]
+  for (int i = t; i <= M; i += 128) twp[i] = cx.tw.xpost[i];
+  cp_wait<0>();
+  __syncthreads();
+  double2 v[16];
+  {
+    const double2* row = sb + r * XI5_SS;
+    const int k1 = l16;
+#pragma unroll
+    for (int k2 = 0; k2 < 16; ++k2) {
+      const int k = k1 + 16 * k2;
+      if (k == 0) {
+        const double X0 = row[0].x, XM = row[M].x;
+        v[0] = make_double2(X0 + XM, X0 - XM);
+      } else {
+        const double2 a = row[k], b = cconj(row[M - k]);
+        const double2 E = cadd(a, b);
+        const double2 O = cmul(csub(a, b), cconj(twp[k]));
+        v[k2] = cadd(E, mul_pi(O));
+      }
+    }
+  }
+  dft_reg<16, true>(v);  // thread = k1: inverse over k2 -> n1
+#pragma unroll
+  for (int n1 = 1; n1 < 16; ++n1) v[n1] = cmul(v[n1], cconj(tw[n1 * 16 + l16]));
+  __syncthreads();  // every read of the spectrum rows done: sb becomes the transpose buffer
+#pragma unroll
+  for (int n1 = 0; n1 < 16; ++n1) sb[r * XI5_RS + n1 * 17 + l16] = v[n1];
+  __syncthreads();
+#pragma unroll
+  for (int k1 = 0; k1 < 16; ++k1) v[k1] = sb[r * XI5_RS + l16 * 17 + k1];
+  dft_reg<16, true>(v);  // thread = n1: inverse over k1 -> n2 ; v[n2] = x[n1 + 16 n2]
+  const long long voff = (long long)load * g.c * g.n + (row0 + r) * g.N1;
+  if (MODE != CG) {
+    double2* o2 = reinterpret_cast<double2*>(dst + voff);
+#pragma unroll
+    for (int n2 = 0; n2 < 16; ++n2) __stcg(o2 + l16 + 16 * n2, v[n2]);
+  } else {
+    double2* d2 = reinterpret_cast<double2*>(cx.d + voff);
+    double2* u2 = reinterpret_cast<double2*>(cx.u + voff);
+    if (st->iters == 0) {
+#pragma unroll
+      for (int n2 = 0; n2 < 16; ++n2) __stcg(d2 + l16 + 16 * n2, v[n2]);  // d = s (Alg 2 l.2, l.8)
+    } else {
+      const double beta = st->beta, alpha = st->alpha;
+#pragma unroll
+      for (int h8 = 0; h8 < 16; h8 += 8) {
+        double2 dold[8], uu[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          dold[i] = __ldcs(d2 + l16 + 16 * (h8 + i));
+          uu[i] = __ldcs(u2 + l16 + 16 * (h8 + i));
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          uu[i].x = fma(alpha, dold[i].x, uu[i].x);  // deferred u += alpha_{m-1} d_{m-1} (l.12)
+          uu[i].y = fma(alpha, dold[i].y, uu[i].y);
+          __stcg(u2 + l16 + 16 * (h8 + i), uu[i]);
+          const double2 s = v[h8 + i];
+          __stcg(d2 + l16 + 16 * (h8 + i), make_double2(fma(beta, dold[i].x, s.x), fma(beta, dold[i].y, s.y)));
+        }
+      }
+    }
+  }
+}
+
 // ============================================================================== y pass (3D)
 template <int L>
 __host__ __device__ constexpr int ysmem_bytes() {
@@ -2507,6 +2613,17 @@ int launch_xfwd(const Ctx& cx, int mode, const double* src, cudaStream_t s, int 
 
 int launch_xinv(const Ctx& cx, int mode, double* dst, cudaStream_t s, int b0, int nb) {
   const Geo& g = cx.g;
+  static const bool rd5 = [] {
+    const char* e = getenv("UNO_XIRD");
+    return !(e && e[0] == '0');
+  }();
+  if (rd5 && g.N1 == 512) {
+    const dim3 grid(nb > 0 ? (unsigned)nb : (unsigned)((long long)g.c * g.P3 * g.N2 / 8), g.nrhs);
+    if (mode == CG) xinv512_kernel<CG><<<grid, 128, 0, s>>>(cx, dst, b0);
+    else if (mode == PLAIN) xinv512_kernel<PLAIN><<<grid, 128, 0, s>>>(cx, dst, b0);
+    else xinv512_kernel<STANDALONE><<<grid, 128, 0, s>>>(cx, dst, b0);
+    return 1;
+  }
   return dispatch_pow2(g.M, [&](auto Lc) {
     constexpr int M = decltype(Lc)::value;
     const dim3 grid(nb > 0 ? (unsigned)nb : (unsigned)((long long)g.c * g.P3 * g.N2 / 8), g.nrhs);
