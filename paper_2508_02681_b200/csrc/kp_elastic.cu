@@ -108,9 +108,10 @@ __global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int
   };
   // phase of element layer k (1 byte, read one layer ahead so its latency hides behind a layer)
   auto phase_of = [&](int k) -> bool {
-    const int layer = dz ? k : ((k + N3) & (N3 - 1));
-    // Dirichlet z: the prefetch one layer past the last one (layer N3) does not exist
-    return eth && layer >= 0 && layer < N3 && __ldg(cx.phase + (long long)layer * plane + pbase) != 0;
+    // Dirichlet z: the prefetch one layer past the last one (layer N3) does not exist — clamp the
+    // address (its value is never used); a predicated load would cost the prefetch its early issue
+    const int layer = dz ? min(k, N3 - 1) : ((k + N3) & (N3 - 1));
+    return eth && __ldg(cx.phase + (long long)layer * plane + pbase) != 0;
   };
   bool phc = phase_of(zs - 1);
   auto element_layer = [&](int k, bool want_lower) {  // element layer between node planes k, k+1
