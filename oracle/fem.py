@@ -255,6 +255,46 @@ def apply_K(g: Grid, physics: str, phase, mat, u):
     return apply_K_thermal(g, phase, mat, u) if physics == "thermal" else apply_K_elastic(g, phase, mat, u)
 
 
+def apply_K_chunked(g: Grid, physics: str, phase, mat, u: np.ndarray, zchunk: int = 32, workers: int = 1):
+    """p = K u (3D) evaluated in slabs of `zchunk` node planes along z for grids too large for
+    apply_K's temporaries (memory and threads only; the arithmetic is apply_K's).  The output at
+    node planes [a, b) depends on node planes a-1 .. b and element layers a-1 .. b-1 (Eq 22: a node
+    couples only to the 2^d elements around it), so each slab is apply_K on a z-periodic sub-grid of
+    L = b - a + 2 node planes and element layers whose output planes 1 .. L-2 are exact (the extra
+    wrap-around element layer L-1 only touches the discarded planes 0 and L-1).  Dirichlet z: the
+    fixed node planes 0 and N3 enter as zeros (Fig 4)."""
+    assert g.d == 3
+    c = g.c
+    dirz = g.bc[2] == 1
+    n3 = g.N[2]
+    ufull = np.pad(u, [(0, 0), (1, 1), (0, 0), (0, 0)]) if dirz else u  # node planes 0..N3 (Dirichlet)
+    nplanes = ufull.shape[1]
+    out = np.empty_like(u)
+    lo, hi = (1, n3) if dirz else (0, n3)  # full-grid node planes that are unknowns
+
+    def slab(a):
+        b = min(hi, a + zchunk)
+        L = b - a + 2
+        nodes = np.arange(a - 1, b + 1) % nplanes
+        layers = np.arange(a - 1, b) % n3
+        sub = Grid((g.N[0], g.N[1], L), bc=(g.bc[0], g.bc[1], 0), c=c)
+        sub.h = tuple(g.h)
+        ph = np.zeros((L,) + phase.shape[1:], dtype=phase.dtype)
+        ph[: L - 1] = phase[layers]
+        ks = apply_K(sub, physics, ph, mat, np.ascontiguousarray(ufull[:, nodes]))
+        out[:, a - lo:b - lo] = ks[:, 1:L - 1]
+
+    starts = list(range(lo, hi, zchunk))
+    if workers > 1:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(workers) as ex:
+            list(ex.map(slab, starts))
+    else:
+        for a in starts:
+            slab(a)
+    return out
+
+
 def rhs_thermal(g: Grid, phase: np.ndarray, kappa, gbar) -> np.ndarray:
     """f_i = l(phi_i) = -int grad(phi_i) . kappa gbar (decomposition Eq 76, Galerkin Eq 22;
     SURVEY A4)."""

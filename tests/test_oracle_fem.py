@@ -197,3 +197,18 @@ def test_apply_K_at_equals_full_apply(physics):
     nodes = [(0, 0, 0), (9, 5, 7), (4, 2, 3), (9, 0, 7)]
     got = fem.apply_K_at(g, physics, ph, mat, u, nodes)
     assert np.max(np.abs(got - np.array([K[(slice(None),) + n] for n in nodes]))) < 1e-14
+
+
+@pytest.mark.parametrize("physics", ["thermal", "elastic"])
+@pytest.mark.parametrize("bc", [(0, 0, 0), (0, 0, 1), (1, 1, 1)])
+@pytest.mark.parametrize("zchunk,workers", [(1, 1), (3, 2), (64, 1)])
+def test_chunked_K_equals_K(physics, bc, zchunk, workers):
+    # the slab evaluation used for the 256^3 / 512^3 goldens is apply_K exactly
+    g = fem.Grid((6, 4, 8), bc=bc, c=1 if physics == "thermal" else 3, h=0.125)
+    rng = np.random.default_rng(5)
+    ph = (rng.random(g.elem_shape) < 0.4).astype(np.uint8)
+    mat = (1.0, 7.0) if physics == "thermal" else ((0.6, 0.4), (2.8, 4.2))
+    u = rng.standard_normal(g.field_shape())
+    ref = fem.apply_K(g, physics, ph, mat, u)
+    got = fem.apply_K_chunked(g, physics, ph, mat, u, zchunk=zchunk, workers=workers)
+    assert np.max(np.abs(got - ref)) <= 1e-13 * np.max(np.abs(ref))

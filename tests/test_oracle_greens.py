@@ -201,3 +201,62 @@ def test_fans_spectrum_table4_bounds():
     Gp = greens.ghat(g, "thermal", mat, 9, 0.1)
     evp = np.sort(np.linalg.eigvals(greens.dense_P(Gp, N) @ A).real)[1:]
     assert evp.min() >= 0.9 / 3 - 1e-10 and evp.max() <= 1.1 * 5 / 3 + 1e-10
+
+
+# ----------------------------------------------------------------------------- long axes
+def _closed_form_symbol_stable(N, h, physics, ref):
+    """SURVEY App. A3 closed forms with 1 - cos(t) written as 2 sin^2(t/2) (no cancellation at low
+    frequency), signed frequencies; an independent route to the symbol on 512-1024-point axes."""
+    d = len(N)
+    grids = np.meshgrid(*[2 * np.pi * np.fft.fftfreq(N[i]) for i in reversed(range(d))], indexing="ij")
+    th = list(reversed(grids))
+    mass = [(h[i] / 3) * (2 + np.cos(th[i])) for i in range(d)]
+    S = np.zeros((d, d) + grids[0].shape)
+    for i in range(d):
+        v = (4 / h[i]) * np.sin(th[i] / 2) ** 2
+        for j in range(d):
+            if j != i:
+                v = v * mass[j]
+        S[i, i] = v
+        for j in range(d):
+            if j != i:
+                w = np.sin(th[i]) * np.sin(th[j])
+                for l in range(d):
+                    if l not in (i, j):
+                        w = w * mass[l]
+                S[i, j] = w
+    if physics == "thermal":
+        return ref * np.trace(S)[None, None]
+    lam, mu = ref
+    return (lam + mu) * S + mu * np.einsum("ij,...->ij...", np.eye(d), np.trace(S))
+
+
+@pytest.mark.parametrize("N,physics", [((1024, 8, 4), "thermal"), ((4, 1024, 8), "elastic"),
+                                       ((8, 4, 512), "elastic"), ((1024, 512), "thermal")])
+def test_symbol_relative_accuracy_on_long_axes(N, physics):
+    # the stencil DFT is evaluated without cancellation: every bin, including the lowest
+    # frequencies of a 512-1024-point axis (symbol ~ theta^2 ~ 4e-5), to ~1e-15 relative
+    d = len(N)
+    g = fem.Grid(N, c=1 if physics == "thermal" else d, h=1.0 / max(N))
+    ref = 1.7 if physics == "thermal" else (1.6774, 2.2756)
+    A = greens.symbol_probe(g, physics, ref)
+    C = _closed_form_symbol_stable(N, g.h, physics, ref)
+    nrm = np.sqrt(np.sum(C ** 2, axis=(0, 1)))
+    err = np.sqrt(np.sum((A - C) ** 2, axis=(0, 1)))
+    nz = nrm > 0
+    assert np.count_nonzero(~nz) == 1 and np.all(A[(slice(None), slice(None)) + (0,) * d] == 0)
+    assert np.max(err[nz] / nrm[nz]) < 1e-14
+
+
+@pytest.mark.parametrize("physics,N", [("thermal", (16, 8, 6)), ("elastic", (8, 6, 10)), ("elastic", (12, 8))])
+def test_half_spectrum_and_chunked_symbol_equal_full(physics, N):
+    # ghat(half=True) is the R2C restriction of the full table, chunking changes nothing
+    d = len(N)
+    g = fem.Grid(N, c=1 if physics == "thermal" else d)
+    mat = (1.0, 10.0) if physics == "thermal" else ((0.58, 0.38), (2.78, 4.17))
+    G = greens.ghat(g, physics, mat, 77, 0.1)
+    Gh = greens.ghat(g, physics, mat, 77, 0.1, half=True, zchunk=3)
+    assert np.array_equal(Gh, greens.half(G))
+    assert np.array_equal(greens.ghat(g, physics, mat, 77, 0.1, zchunk=1), G)
+    r = RNG.standard_normal(g.field_shape())
+    assert np.max(np.abs(greens.apply_precond(Gh, r) - greens.apply_precond(G, r))) == 0.0
