@@ -1,12 +1,14 @@
 #!/usr/bin/env python
 """UNO-CG hot-path benchmark (BASELINE.json metric: PCG DOF-iterations/s at 256^3).
 
-One *step* = the whole hot path over one batch of synthetic
-config-3 input: for each of the rank's 48 problems (8 Boolean-sphere microstructures at
-vf 0.1..0.4 x contrasts {2,5,10,20,50,100}, 256^3 thermal, periodic) create the solver
-(reference medium, tabulated G_hat, Eq 55 check), solve its 3 load cases with Alg 2 to
-rel. ||r||_inf 1e-8, remove the mean and compute the effective conductivity.
-value = sum over ranks/solves of (DOF x iterations) / max-over-ranks device time.
+One *step* = the whole hot path over the fixed config-3 batch: 48
+problems (8 Boolean-sphere microstructures at vf 0.1..0.4 x contrasts {2,5,10,20,50,100},
+256^3 thermal, periodic), sharded over the ranks (Latin square at 8 GPUs, LPT on
+the Eq 27 cost at 2/4; no data-path collective).  For each of its problems a rank re-targets its
+solver (reference medium, tabulated G_hat, Eq 55 check), solves the 3 load cases with Alg 2 to
+rel. ||r||_inf 1e-8, removes the mean and computes the effective conductivity.
+value = sum over ranks/solves of (DOF x iterations) / max-over-ranks device time (strong
+scaling: the batch is fixed; --weak gives every rank its own 48-problem batch instead).
 
 Launch: python bench.py --gpus N --steps K --warmup W   (N > 1 under torchrun, NCCL).
         python bench.py --impl reference ...              (the CPU oracle arm)
@@ -43,7 +45,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--grid", type=int, default=N_GRID, help="grid edge (256 = config 3; smaller only for debugging)")
-    ap.add_argument("--problems", type=int, default=48, help="problems per rank (48 = config 3)")
+    ap.add_argument("--weak", action="store_true", help="every rank solves its own 48-problem batch (weak scaling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -56,19 +58,20 @@ def dist_env():
     return ws, rank, local
 
 
-def problem_list(rank: int, nprob: int):
-    """Rank-local problems (weak scaling): microstructure m of this rank x contrast j."""
-    out = []
-    for i in range(nprob):
-        m, j = i % N_MICRO, (i // N_MICRO) % len(CONTRASTS)
-        out.append((m, CONTRASTS[j]))
-    return out
+def problem_list(ws: int, rank: int, weak: bool):
+    """This rank's (microstructure, contrast) problems: its shard of the fixed 48-problem batch
+    (dist.config3_shard), or with --weak the whole batch (own microstructure seeds per rank)."""
+    from paper_2508_02681_b200 import dist as D
+
+    if weak:
+        return D.config3_problems(CONTRASTS, N_MICRO)
+    return D.config3_shard(ws, rank, CONTRASTS, N_MICRO)
 
 
-def make_microstructures(rank: int, n: int):
+def make_microstructures(ms, n: int, seed_base: int):
     from paper_2508_02681_b200 import synth
 
-    return [synth.config3_microstructure(j, n=n, seed_base=300 + 8 * rank) for j in range(N_MICRO)]
+    return {m: synth.config3_microstructure(m, n=n, seed_base=seed_base) for m in sorted(ms)}
 
 
 class ClockSampler:
@@ -152,25 +155,34 @@ def run_ours(args):
     import torch.distributed as dist
 
     ws, rank, local = dist_env()
-    if ws > 1:
-        dist.init_process_group("nccl", init_method="env://")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", init_method="env://", device_id=dev)
+        t = torch.ones(1, device=dev)
+        dist.all_reduce(t)  # forces communicator creation; logged so the driver can check the ranks
+        torch.cuda.synchronize()
+        nv = ".".join(str(x) for x in torch.cuda.nccl.version())
+        print(f"[bench rank {rank}/{ws}] NCCL {nv} communicator ready on cuda:{local} "
+              f"({torch.cuda.get_device_name(local)}), all_reduce check {int(t.item())} == {ws}",
+              file=sys.stderr, flush=True)
     from paper_2508_02681_b200 import dist as D
     from paper_2508_02681_b200.api import UnoCG
 
     n = args.grid
     t0 = time.time()
-    micro = make_microstructures(rank, n)
-    probs = problem_list(rank, args.problems)
-    phases = [torch.from_numpy(m).to(dev) for m in micro]
+    probs = problem_list(ws, rank, args.weak)
+    seed_base = 300 + 8 * rank if args.weak else 300
+    micro = make_microstructures({m for m, _ in probs}, n, seed_base)
+    phases = {m: torch.from_numpy(v).to(dev) for m, v in micro.items()}
     loads = np.eye(3)
     u = torch.empty((3, 1, n, n, n), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream()
     gen_s = time.time() - t0
     # one solver per rank: its workspace is allocated once (like model memory); every problem
     # of a step re-runs the a0 setup (reference medium, G_hat table, Eq 55) via uno_cg_update.
-    solver = UnoCG(phases[0], "thermal", (1.0, CONTRASTS[0]), nrhs=3, seed=3000, amp=0.1, stream=stream)
+    m0, R0 = probs[0]
+    solver = UnoCG(phases[m0], "thermal", (1.0, R0), nrhs=3, seed=3000 + m0, amp=0.1, stream=stream)
 
     def one_step(timing: bool):
         dofit = 0
@@ -232,7 +244,9 @@ def run_ours(args):
                 a[1] += c
         kt1.record(stream)
         barrier()
-    ms = D.reduce_max(ev0.elapsed_time(ev1))      # max over ranks of the device time
+    my_ms = ev0.elapsed_time(ev1)
+    ms = D.reduce_max(my_ms)                      # max over ranks of the device time
+    rank_ms = D.gather_results([my_ms])
     all_dofit = D.reduce_sum(float(tot_dofit))    # units processed by all ranks
     value = all_dofit / (ms / 1e3)
     kt_ms = D.reduce_max(kt0.elapsed_time(kt1))
@@ -276,17 +290,17 @@ def run_ours(args):
     # ---- e2e: host buffers in, host results out, through the public API ----
     e2e = None
     if not args.no_e2e:
-        host_ph = [torch.from_numpy(m).pin_memory() for m in micro]
-        dph = [torch.empty_like(p, device=dev) for p in host_ph]
-        h2d = sum(p.numel() for p in host_ph)
+        host_ph = {m: torch.from_numpy(v).pin_memory() for m, v in micro.items()}
+        dph = {m: torch.empty_like(p, device=dev) for m, p in host_ph.items()}
+        h2d = sum(p.numel() for p in host_ph.values())
         d2h = 0
 
         def e2e_step():
             nonlocal d2h
             d2h = 0
             dofit = 0
-            for i, p in enumerate(host_ph):
-                dph[i].copy_(p, non_blocking=True)
+            for m, p in host_ph.items():
+                dph[m].copy_(p, non_blocking=True)
             out = []
             s = solver
             for (m, R) in probs:
@@ -313,18 +327,25 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:  # the oracle baseline is an N = 1 figure
-        cpu = cpu_baseline(micro[3], 20.0, n)
+        cpu = cpu_baseline(n)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak" if args.weak else "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"cfg3: {args.problems} problems/rank (8 Boolean-sphere microstructures vf 0.1-0.4 x "
-                                   f"6 contrasts 2-100) x 3 loads, {n}^3 thermal periodic Q1, rel ||r||_inf 1e-8",
-                       "global_batch": args.problems * ws, "grid": n, "loads": 3, "dof_per_solve": n ** 3,
+            "config": {"workload": f"cfg3: fixed batch of 48 problems (8 Boolean-sphere microstructures vf 0.1-0.4 x "
+                                   f"6 contrasts 2-100) x 3 loads, {n}^3 thermal periodic Q1, rel ||r||_inf 1e-8"
+                                   + (" (--weak: 48 per rank)" if args.weak else f", sharded over {ws} rank(s)"),
+                       "global_batch": 48 * ws if args.weak else 48, "grid": n, "loads": 3, "dof_per_solve": n ** 3,
                        "l2": "inputs larger than L2 (~1.7 GB working set per solve vs 126 MB L2)",
-                       "parallelism": f"batch-shard x{ws} (no data-path collective)",
+                       "parallelism": (f"batch-shard x{ws}: " + ("Latin square" if ws == 8 else "LPT on Eq 27 cost"
+                                                                  if ws > 1 else "single GPU")
+                                       + " (no data-path collective)"),
+                       "problems_per_rank": len(probs),
+                       "rank_ms": [round(x, 1) for x in rank_ms],
+                       "imbalance_max_over_mean": round(max(rank_ms) / (sum(rank_ms) / len(rank_ms)), 4),
                        "input_generation_s": round(gen_s, 1)},
             "roofline": roof, "iteration_roofline": iter_roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(tot_launch),
@@ -336,52 +357,82 @@ def run_ours(args):
 
 
 # ----------------------------------------------------------------------------- CPU oracle
-def _oracle_sample(phase, R, n, iters):
-    """One load case of one config-3 problem, `iters` PCG iterations with the oracle (setup
-    outside the timer).  Returns (DOF-iterations, seconds)."""
-    from oracle import fem, greens, pcg
-
-    g = fem.Grid((n, n, n), h=1.0 / n)
-    mat = (1.0, R)
-    G = greens.ghat(g, "thermal", mat, 3003, 0.1)
-    f = fem.rhs(g, "thermal", phase, mat, np.eye(3)[0])
-    t = time.perf_counter()
-    pcg.pcg(lambda v: fem.apply_K(g, "thermal", phase, mat, v), lambda v: greens.apply_precond(G, v), f,
-            fixed_iters=iters)
-    dt = time.perf_counter() - t
-    return n ** 3 * iters, dt
+def _host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
 
 
-def cpu_baseline(phase, R, n, iters=2):
-    dofit, dt = _oracle_sample(phase, R, n, iters)
-    return {"value": dofit / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"1 problem (ms 3, R={R:g}), 1 load, {iters} PCG iterations at {n}^3, NumPy single thread; "
-                      f"{dt:.1f} s"}
+class _OracleSample:
+    """The CPU oracle on one config-3 problem (microstructure 3, R = 20, seed 3003) and load e_1:
+    Alg 2 with the oracle's K (fem.apply_K_chunked: threads over z-slabs) and UNO apply (scipy.fft
+    with `workers`), on the box's host cores.  Setup (G_hat, f) is outside the
+    timer; `run(k)` times k PCG iterations and returns (DOF-iterations, seconds)."""
+
+    def __init__(self, n: int):
+        from oracle import fem, greens, transform
+        from paper_2508_02681_b200 import synth
+
+        self.cores = _host_cores()
+        self.n = n
+        self.zchunk = max(4, -(-n // self.cores))
+        self.threads = min(self.cores, -(-n // self.zchunk))
+        transform.set_workers(self.cores)
+        self.phase = synth.config3_microstructure(3, n=n)
+        self.g = fem.Grid((n, n, n), h=1.0 / n)
+        self.mat = (1.0, 20.0)
+        self.G = greens.ghat(self.g, "thermal", self.mat, 3003, 0.1, half=True)
+        self.f = fem.rhs(self.g, "thermal", self.phase, self.mat, np.eye(3)[0])
+
+    def run(self, iters: int):
+        from oracle import fem, greens, pcg
+
+        t = time.perf_counter()
+        pcg.pcg(lambda v: fem.apply_K_chunked(self.g, "thermal", self.phase, self.mat, v, zchunk=self.zchunk,
+                                              workers=self.threads),
+                lambda v: greens.apply_precond(self.G, v), self.f, fixed_iters=iters)
+        return self.n ** 3 * iters, time.perf_counter() - t
+
+    def describe(self, iters: int, secs: float) -> str:
+        return (f"1 problem (ms 3, R=20), 1 load, {iters} PCG iteration(s) at {self.n}^3: oracle K over "
+                f"{self.threads} z-slab threads, scipy.fft workers={self.cores}; {secs:.1f} s")
+
+
+def cpu_baseline(n, target_s: float = 15.0):
+    o = _OracleSample(n)
+    d1, t1 = o.run(1)
+    k = int(min(20, max(1, round(target_s / max(t1, 1e-3)))))
+    dofit, dt = o.run(k)
+    return {"value": dofit / dt, "unit": UNIT, "cores": o.cores, "threads": o.threads, "kind": "oracle",
+            "sample": o.describe(k, dt)}
 
 
 def run_reference(args):
+    """The CPU oracle arm (tier reading of the reference arm): the oracle as it stands on the box's
+    host cores, each step a bounded sample of the config-3 workload (2 PCG iterations of one
+    problem/load at 256^3), same metric/unit as our arm.  Rank 0 only."""
     ws, rank, local = dist_env()
     if rank != 0:
         return
     n = args.grid
-    from paper_2508_02681_b200 import synth
-
-    phase = synth.config3_microstructure(3, n=n)
+    o = _OracleSample(n)
     for _ in range(args.warmup):
-        _oracle_sample(phase, 20.0, n, 1)
+        o.run(1)
     tot, tsum = 0, 0.0
     for _ in range(args.steps):
-        d, t = _oracle_sample(phase, 20.0, n, 1)
+        d, t = o.run(2)
         tot += d
         tsum += t
     value = tot / tsum
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": tsum / args.steps * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "ms_per_step": tsum / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak" if args.weak else "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": f"cfg3 sample: 1 problem (ms 3, R=20), 1 load, 1 PCG iteration per step at {n}^3 "
+            "config": {"workload": f"cfg3 sample: 1 problem (ms 3, R=20), 1 load, 2 PCG iterations per step at {n}^3 "
                                    "(CPU oracle; bounded sample of the config-3 workload)", "grid": n},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": "1 load x 1 iteration per step at 256^3, NumPy single thread"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": o.cores, "threads": o.threads, "kind": "oracle",
+                             "sample": o.describe(2, tsum / max(args.steps, 1)) + " per step"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

@@ -43,8 +43,13 @@
  *    the caller, e.g. torch.cuda.current_stream().cuda_stream); calls that return
  *    host scalars synchronise that stream.
  *  - Ownership: all field buffers (phase, u, f, r, z, ...) are caller-owned device
- *    memory.  The handle owns its workspace (CG vectors r,d,p, one spectrum buffer,
- *    the tabulated symbol, reduction scratch) and frees it in uno_cg_destroy.
+ *    memory.  The handle's workspace (CG vectors r, d, p, u, one spectrum buffer, the
+ *    tabulated symbol, twiddle tables, reduction scratch; uno_cg_workspace_size bytes) is
+ *    either caller-provided (borrowed, never freed by the library) or allocated by
+ *    uno_cg_create and freed in uno_cg_destroy.  Outside it the library allocates only
+ *    on demand: the per-solve coefficient record (3 x 8 x (cap+1) doubles, grown on the
+ *    first solve with a larger cap), the Jacobi diagonal (uno_cg_set_preconditioner) and
+ *    the training spectrum (uno_cg_train_features).
  *  - Errors: every call returns uno_status; on error nothing is written to the
  *    outputs unless stated, and uno_cg_last_error() returns a thread-local message.
  *    No C++ exception crosses the ABI.  Calls on one handle are not thread-safe.
@@ -72,10 +77,13 @@ typedef enum {
   UNO_ERR_ARG = 1,         /* NULL pointer or invalid scalar argument                    */
   UNO_ERR_SHAPE = 2,       /* grid size not supported (see Conventions)                   */
   UNO_ERR_CUDA = 3,        /* a CUDA runtime call failed (message in uno_cg_last_error)   */
-  UNO_ERR_UNSUPPORTED = 4, /* valid per the paper but not built yet (non-periodic bc)     */
+  UNO_ERR_UNSUPPORTED = 4, /* valid per the paper but not built (boundary-condition pattern,
+                              see Conventions; slab-mode restrictions in uno_cg_slab.h)   */
   UNO_ERR_NOT_SPD = 5,     /* Eq 55 safety check failed at create            */
   UNO_ERR_BREAKDOWN = 6,   /* d.p <= 0 or gamma_1 <= 0 during solve           */
-  UNO_ERR_NONFINITE = 7    /* NaN/Inf residual during solve                               */
+  UNO_ERR_NONFINITE = 7,   /* NaN/Inf residual during solve                               */
+  UNO_ERR_NCCL = 8         /* slab mode (uno_cg_slab.h): a peer/communicator exchange could
+                              not be set up (peer buffer table, peer access)               */
 } uno_status;
 
 enum { UNO_THERMAL = 0, UNO_ELASTIC = 1 };
@@ -85,7 +93,7 @@ typedef struct {
   int32_t n[3];       /* voxel counts N1, N2, N3 (N3 = 1 when dim == 2)                  */
   double h;           /* voxel edge; <= 0 means 1/N1 (unit cell)              */
   int32_t physics;    /* UNO_THERMAL (c = 1) or UNO_ELASTIC (c = dim)                    */
-  int32_t bc[3];      /* per axis: 0 periodic, 1 Dirichlet ({0,0,0} or {0,0,1} accepted)   */
+  int32_t bc[3];      /* per axis: 0 periodic, 1 Dirichlet; accepted patterns in Conventions */
   double mat[2][2];   /* phase 0 / phase 1: thermal {kappa, unused}; elastic {lambda, mu} */
   double ref[2];      /* reference medium (kappa_r | lambda_r, mu_r); ref[0] <= 0 means the
                          arithmetic mean of the phases          */
@@ -106,13 +114,23 @@ typedef struct {
   double gamma_last;   /* last gamma_1 = r.s (Alg 2 l.7)                                   */
 } uno_cg_report;
 
-/* Create a solver for one microstructure.  Computes the reference medium, tabulates
- * G_hat(k)/n on the R2C half spectrum (Eq 46/49/51: the unique entries v, C = c(c+1)/2
- * planes) and runs the Eq 55 check (every block with k != 0 SPD with lambda_min > 1e-14;
- * G_hat(0) = 0 shares the periodic null space).
+/* Device workspace a handle for `desc` needs (bytes): every buffer of Alg 2's state (r, d, p,
+ * u), the spectrum, the G_hat table (Eq 51), twiddles and reduction scratch.  Validates desc
+ * exactly as uno_cg_create does (same status codes); desc.stream is not used.            */
+UNO_API uno_status uno_cg_workspace_size(const uno_cg_desc* desc, size_t* bytes);
+
+/* Create a solver for one microstructure (the problem of Eq 22 / §5 on this grid).  Computes the
+ * reference medium, tabulates G_hat(k)/n on the R2C half spectrum (Eq 46/49/51: the unique
+ * entries v, C = c(c+1)/2 planes) and runs the Eq 55 check (every block with k != 0 SPD with
+ * lambda_min > 1e-14; G_hat(0) = 0 shares the periodic null space).
  *   d_phase: device uint8 [N3][N2][N1], caller-owned, must outlive the handle.
- * Returns UNO_ERR_NOT_SPD (and no handle) if Eq 55 fails.                             */
-UNO_API uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_phase, uno_cg_handle** out);
+ *   d_workspace: device memory of uno_cg_workspace_size(desc) bytes, 256-byte aligned,
+ *     caller-owned and not touched by anyone else while the handle lives; NULL = the library
+ *     allocates it (stream-ordered pool on desc.stream) and frees it in uno_cg_destroy.
+ * Returns UNO_ERR_NOT_SPD (and no handle) if Eq 55 fails; UNO_ERR_ARG for a misaligned
+ * workspace; UNO_ERR_CUDA if an allocation fails.                                        */
+UNO_API uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_phase, void* d_workspace,
+                                 uno_cg_handle** out);
 
 UNO_API uno_status uno_cg_destroy(uno_cg_handle* h);
 
@@ -147,8 +165,9 @@ UNO_API uno_status uno_cg_apply_precond(uno_cg_handle* h, const double* d_r, dou
  * h^(d-1) * ||load||_inf is a zero RHS: 0 iterations, u = 0.  On return u holds the
  * per-component mean-free solution.
  *   h_loads: as uno_cg_rhs.  d_u: device [nrhs][c][N3][N2][N1] (output).
- *   rep: host [nrhs] reports (may be NULL).  h_hist: host [nrhs][max_iter+1] residual
- *   history ||r_m||_inf/||r0||_inf or NULL.
+ *   rep: host [nrhs] reports (may be NULL).  h_hist: host [nrhs][cap+1] residual history
+ *   ||r_m||_inf/||r0||_inf, m = 0..cap with cap = fixed_iters > 0 ? fixed_iters : max_iter
+ *   (entries past a load's last iteration are unspecified), or NULL.
  * Returns UNO_ERR_BREAKDOWN / UNO_ERR_NONFINITE if any load broke down (rep says which). */
 UNO_API uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, double rel_tol, int32_t max_iter,
                         int32_t fixed_iters, double* d_u, uno_cg_report* rep, double* h_hist);

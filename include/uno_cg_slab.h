@@ -78,7 +78,8 @@ UNO_API uno_status uno_slab_kapply(uno_slab_handle* h, const double* d_halo_recv
  * uno_slab_inverse then reads the local B.  Ordering (caller): every rank's forward_peer /
  * green_peer must complete before any rank reads the written buffers — the ||r||_inf and gamma
  * all-reduces that follow these stages (stream-ordered) provide exactly that; each pack kernel
- * ends with a system-scope fence.  UNO_ERR_ARG: null arrays / entries.                    */
+ * ends with a system-scope fence.  UNO_ERR_NCCL: the peer table is NULL, has a NULL entry or
+ * nranks exceeds the supported 8 peers.                                                   */
 UNO_API uno_status uno_slab_forward_peer(uno_slab_handle* h, double* const* h_peer_recv);
 UNO_API uno_status uno_slab_green_peer(uno_slab_handle* h, const double* d_recv, double* const* h_peer_recv);
 /* Peer variant of inverse: the two boundary node planes of d go straight into the neighbours'

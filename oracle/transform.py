@@ -8,6 +8,16 @@ last axis) as in §2.2.2 ("one-dimensional real FFT along the last").
 from __future__ import annotations
 
 import numpy as np
+import scipy.fft as sfft
+
+# threads for the FFT library calls (scipy.fft `workers`); 1 = single-threaded.  Only the
+# bench's timed oracle baseline and the golden generator raise it.
+WORKERS = 1
+
+
+def set_workers(n: int) -> None:
+    global WORKERS
+    WORKERS = max(1, int(n))
 
 
 def spatial_axes(ndim_field: int):
@@ -16,12 +26,12 @@ def spatial_axes(ndim_field: int):
 
 def forward(r: np.ndarray) -> np.ndarray:
     """r_hat = T r per component; field (c, ...) -> half spectrum (c, ..., N1//2+1)."""
-    return np.fft.rfftn(r, axes=spatial_axes(r.ndim), norm="ortho")
+    return sfft.rfftn(r, axes=spatial_axes(r.ndim), norm="ortho", workers=WORKERS)
 
 
 def inverse(rh: np.ndarray, spatial_shape) -> np.ndarray:
     """r = T^H r_hat (Eq 47)."""
-    return np.fft.irfftn(rh, s=spatial_shape, axes=spatial_axes(rh.ndim), norm="ortho")
+    return sfft.irfftn(rh, s=spatial_shape, axes=spatial_axes(rh.ndim), norm="ortho", workers=WORKERS)
 
 
 def dft_matrix(n: int) -> np.ndarray:
@@ -69,14 +79,14 @@ def forward_mixed(r: np.ndarray) -> np.ndarray:
     """r_hat = (F_x (x) F_y (x) S_z) r for fields (c, N3-1, N2, N1): DST-I along z (numpy axis 1),
     then the orthonormal R2C DFT over (y, x)."""
     from scipy.fft import dst
-    rz = dst(r, type=1, axis=1, norm="ortho")
-    return np.fft.rfftn(rz, axes=(2, 3), norm="ortho")
+    rz = dst(r, type=1, axis=1, norm="ortho", workers=WORKERS)
+    return sfft.rfftn(rz, axes=(2, 3), norm="ortho", workers=WORKERS)
 
 
 def inverse_mixed(rh: np.ndarray, spatial_shape) -> np.ndarray:
     from scipy.fft import idst
-    r = np.fft.irfftn(rh, s=spatial_shape[1:], axes=(2, 3), norm="ortho")
-    return idst(r, type=1, axis=1, norm="ortho")
+    r = sfft.irfftn(rh, s=spatial_shape[1:], axes=(2, 3), norm="ortho", workers=WORKERS)
+    return idst(r, type=1, axis=1, norm="ortho", workers=WORKERS)
 
 
 def dense_T_mixed(spatial_shape) -> np.ndarray:

@@ -17,10 +17,10 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("UNO_LIB_PATH") or os.path.join(_HERE, "lib", "libunocg.so")  # override: A/B builds
 
 UNO_OK, UNO_ERR_ARG, UNO_ERR_SHAPE, UNO_ERR_CUDA, UNO_ERR_UNSUPPORTED, UNO_ERR_NOT_SPD, UNO_ERR_BREAKDOWN, \
-    UNO_ERR_NONFINITE = range(8)
+    UNO_ERR_NONFINITE, UNO_ERR_NCCL = range(9)
 UNO_THERMAL, UNO_ELASTIC = 0, 1
 
-EXPORTS = ("uno_cg_create", "uno_cg_destroy", "uno_cg_update", "uno_cg_rhs", "uno_cg_apply_K", "uno_cg_apply_precond",
+EXPORTS = ("uno_cg_workspace_size", "uno_cg_create", "uno_cg_destroy", "uno_cg_update", "uno_cg_rhs", "uno_cg_apply_K", "uno_cg_apply_precond",
            "uno_cg_solve", "uno_cg_effective_property", "uno_cg_set_preconditioner", "uno_cg_train_features",
            "uno_cg_train_pairs", "uno_cg_train_newton", "uno_cg_train_install", "uno_cg_last_solve_stats",
            "uno_cg_last_coefficients", "uno_cg_spectrum",
@@ -55,7 +55,8 @@ def _load():
         raise ImportError(f"libunocg.so not built ({LIB_PATH}); run __graft_entry__.build() — no CPU fallback exists")
     lib = C.CDLL(LIB_PATH)
     P, D, I32, I64 = C.c_void_p, C.c_double, C.c_int32, C.c_int64
-    lib.uno_cg_create.argtypes = [C.POINTER(UnoCgDesc), P, C.POINTER(P)]
+    lib.uno_cg_workspace_size.argtypes = [C.POINTER(UnoCgDesc), C.POINTER(C.c_size_t)]
+    lib.uno_cg_create.argtypes = [C.POINTER(UnoCgDesc), P, P, C.POINTER(P)]
     lib.uno_cg_destroy.argtypes = [P]
     lib.uno_cg_update.argtypes = [P, C.POINTER(UnoCgDesc), P]
     lib.uno_cg_rhs.argtypes = [P, P, P]
@@ -123,9 +124,15 @@ def _host_f64(a) -> np.ndarray:
     return np.ascontiguousarray(np.asarray(a, dtype=np.float64))
 
 
-def uno_cg_create(desc: UnoCgDesc, d_phase) -> int:
+def uno_cg_workspace_size(desc: UnoCgDesc) -> int:
+    n = C.c_size_t()
+    _check(_lib.uno_cg_workspace_size(C.byref(desc), C.byref(n)), "uno_cg_workspace_size")
+    return n.value
+
+
+def uno_cg_create(desc: UnoCgDesc, d_phase, d_workspace=None) -> int:
     h = C.c_void_p()
-    _check(_lib.uno_cg_create(C.byref(desc), _ptr(d_phase), C.byref(h)), "uno_cg_create")
+    _check(_lib.uno_cg_create(C.byref(desc), _ptr(d_phase), _ptr(d_workspace), C.byref(h)), "uno_cg_create")
     return h.value
 
 

@@ -18,11 +18,9 @@ struct Geo {
   long long nspec;      // H1*N2*N3 complex bins per component
   double h;             // voxel edge
   int C;                // unique symbol entries per bin: c(c+1)/2 (Eq 51)
-  int NA, NB;           // 3-pass (four-step) schedule: N2 = NA*NB, y = y_a + NA*y_b; NB = 0 -> 5-pass
   int dirz;             // 1: Dirichlet on z (mixed BC; DST-I along z), node planes 1..N3-1 stored
   int P3;               // stored node planes along z: N3 (periodic) or N3 - 1 (dirz); 1 in 2D
   int KZC;              // z planes per CTA of the 3D thermal K kernel
-  int ZP;               // z-chunk of the L2-pipelined 5-pass schedule (0: off), DESIGN.md §5
   // z-slab decomposition (slab.cu; all 0 for a whole-grid handle):
   int zlo;              // global z of the first stored node plane of this slab
   int halo;             // 1: K reads node planes zlo-1 / zlo+P3 from Ctx::hlo / Ctx::hhi

@@ -428,11 +428,7 @@ static int launch_dst3(const Ctx& cx, const double* src, double* dst, int axis, 
   const int N = axis == 0 ? g.N1 : (axis == 1 ? g.N2 : g.N3);
   const long long nlc = (long long)g.nrhs * g.c;
   const long long nb = axis == 0 ? nlc * g.N3 * (g.N2 / 16) : nlc * (axis == 1 ? g.N3 : g.N2) * (g.N1 / 16);
-  static const bool rd = [] {
-    const char* e = getenv("UNO_DRD");
-    return !(e && e[0] == '0');
-  }();
-  if (rd && N == 256 && (axis == 0 ? g.N2 % 8 == 0 : g.N1 % 8 == 0)) {
+  if (N == 256 && (axis == 0 ? g.N2 % 8 == 0 : g.N1 % 8 == 0)) {
     const long long nb8 = axis == 0 ? nlc * g.N3 * (g.N2 / 8) : nlc * (axis == 1 ? g.N3 : g.N2) * (g.N1 / 8);
     dst512r_kernel<<<(unsigned)nb8, D5_T, dst512r_smem, s>>>(cx, src, dst, axis, twl, gmul);
     return 1;

@@ -1812,14 +1812,8 @@ __global__ void __launch_bounds__(128, 2) kp_thermal3d_rn_kernel(Ctx cx, int mod
   dp_finish(cx, load, nblk, my, part, red_sh, mode);
 }
 
-// rows per thread of the production thermal 3D K kernel (UNO_KNR = 2 or 4)
-static int k_nr(const Geo& g) {
-  static const int nr = [] {
-    const char* e = getenv("UNO_KNR");
-    return e && e[0] == '2' ? 2 : 4;
-  }();
-  return (nr == 4 && g.N2 >= 16) ? 4 : 2;
-}
+// rows per thread of the production thermal 3D K kernel (4; 2 when N2 < 16)
+static int k_nr(const Geo& g) { return g.N2 >= 16 ? 4 : 2; }
 
 
 // Thermal 2D: element row (App. A1: {2/3, -1/6, -1/3}) ->
@@ -1859,96 +1853,6 @@ __global__ void __launch_bounds__(256) kp_thermal2d_kernel(Ctx cx, int mode, con
   dp_finish(cx, load, gridDim.x, blockIdx.x, part, red_sh, mode);
 }
 
-// Elastic (c = dim): node-centric gather with the two phase element matrices
-// K^(ph) = lambda_ph K_lambda + mu_ph K_mu (Eq 80) resident in shared memory.
-//   p_(i,alpha) = sum_o sum_(b,beta) K^(ph_o)[(a_o,alpha),(b,beta)] d_(i-1+o+b, beta),  a_o = 1 - o.
-// (v1: direct 576-FMA gather; the Walsh-Hadamard modal form is the planned faster variant.)
-
-constexpr int KE_TX = 16, KE_TY = 8;
-__global__ void __launch_bounds__(128) kp_elastic3d_kernel(Ctx cx, int mode, const double* __restrict__ src,
-                                                           double* __restrict__ dst, int ZC) {
-  const Geo g = cx.g;
-  const int nzc = (g.P3 + ZC - 1) / ZC;
-  const int load = blockIdx.z / nzc;
-  const int zcI = blockIdx.z - load * nzc;
-  const int dz = g.dirz;
-  if (mode == CG && !cx.st[load].active) return;
-  constexpr int DW = KE_TX + 2, DH = KE_TY + 2, EW = KE_TX + 1, EH = KE_TY + 1;
-  __shared__ double D[3][3][DH * DW];        // [slot][comp][...]
-  __shared__ unsigned char P[2][EH * EW];     // phase of element layers
-  __shared__ double Ks[2][24 * 24];
-  __shared__ double red_sh[32];
-  const int t = threadIdx.x, T = blockDim.x;
-  for (int i = t; i < 2 * 576; i += T) Ks[i / 576][i % 576] = __ldg(cx.kel + i);
-  const int tx = t % KE_TX, ty = t / KE_TX;
-  const int x0 = blockIdx.x * KE_TX, y0 = blockIdx.y * KE_TY, zs = zcI * ZC + dz;
-  const int ze = min(zs + ZC, g.P3 + dz);
-  const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
-  const long long n = g.n;
-  const double* dv = src + (long long)load * 3 * n;
-  auto load_plane = [&](int zz, int slot) {
-    const bool zero = dz && (zz <= 0 || zz >= N3);  // fixed Dirichlet node plane
-    const int zw = dz ? zz - 1 : (zz + N3) % N3;
-    for (int i = t; i < 3 * DH * DW; i += T) {
-      const int comp = i / (DH * DW), r = i - comp * DH * DW;
-      const int ly = r / DW, lx = r - ly * DW;
-      const int gx = (x0 - 1 + lx + N1) & (N1 - 1), gy = (y0 - 1 + ly + N2) & (N2 - 1);
-      D[slot][comp][r] = zero ? 0.0 : __ldg(dv + comp * n + ((long long)zw * N2 + gy) * N1 + gx);
-    }
-  };
-  auto load_phase = [&](int layer, int slot) {
-    const int zw = (layer + N3) % N3;
-    for (int i = t; i < EH * EW; i += T) {
-      const int ly = i / EW, lx = i - ly * EW;
-      const int gx = (x0 - 1 + lx + N1) & (N1 - 1), gy = (y0 - 1 + ly + N2) & (N2 - 1);
-      P[slot][i] = __ldg(cx.phase + ((long long)zw * N2 + gy) * N1 + gx) ? 1 : 0;
-    }
-  };
-  load_plane(zs - 1, 0);
-  load_plane(zs, 1);
-  load_phase(zs - 1, 0);
-  double part = 0.0;
-  for (int k = zs; k < ze; ++k) {
-    const int q = k - zs;
-    const int sl[3] = {q % 3, (q + 1) % 3, (q + 2) % 3};  // planes k-1, k, k+1
-    const int pl[2] = {q & 1, (q + 1) & 1};                // layers k-1, k
-    load_plane(k + 1, sl[2]);
-    load_phase(k, pl[1]);
-    __syncthreads();
-    double acc[3] = {0.0, 0.0, 0.0};
-#pragma unroll 1
-    for (int o = 0; o < 8; ++o) {
-      const int ox = o & 1, oy = (o >> 1) & 1, oz = o >> 2;
-      const int a = (1 - ox) + 2 * (1 - oy) + 4 * (1 - oz);
-      const int ph = P[pl[oz]][(ty + oy) * EW + tx + ox];
-      const double* Km = &Ks[ph][0];
-#pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        const int bx = b & 1, by = (b >> 1) & 1, bz = b >> 2;
-        const int slot = sl[oz + bz];
-        const int off = (ty + oy + by) * DW + (tx + ox + bx);
-        const double u0 = D[slot][0][off], u1 = D[slot][1][off], u2 = D[slot][2][off];
-#pragma unroll
-        for (int al = 0; al < 3; ++al) {
-          const double* row = Km + (3 * a + al) * 24 + 3 * b;
-          acc[al] = fma(row[0], u0, fma(row[1], u1, fma(row[2], u2, acc[al])));
-        }
-      }
-    }
-    const int gx = x0 + tx, gy = y0 + ty;
-    const int offc = (ty + 1) * DW + tx + 1;
-    const long long gi = ((long long)(k - dz) * N2 + gy) * N1 + gx;
-#pragma unroll
-    for (int al = 0; al < 3; ++al) {
-      dst[(long long)load * 3 * n + al * n + gi] = acc[al];
-      part = fma(D[sl[1]][al][offc], acc[al], part);
-    }
-    __syncthreads();
-  }
-  const int nblk = gridDim.x * gridDim.y * nzc;
-  const int my = (zcI * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-  dp_finish(cx, load, nblk, my, part, red_sh, mode);
-}
 
 __global__ void __launch_bounds__(256) kp_elastic2d_kernel(Ctx cx, int mode, const double* __restrict__ src,
                                                            double* __restrict__ dst) {
@@ -2242,13 +2146,7 @@ __global__ void build_symbol_kernel(Ctx cx, double* gtab, double ref0, double re
   // N2l: stored k_y extent of this table (a y-chunk in slab mode); N2: the grid's N2 (frequencies)
   const int N1 = g.N1, N2l = g.N2, N2 = g.Ny ? g.Ny : g.N2, N3 = g.N3, d = g.dim;
   int kx, ky, kz;
-  if (g.NB > 0) {  // 3-pass layout [kx][k_b][kz][k_a], k_y = k_b + NB k_a (fft3.cu)
-    const int ka = (int)(b % g.NA);
-    kz = (int)((b / g.NA) % N3);
-    const int kb = (int)((b / ((long long)g.NA * N3)) % g.NB);
-    kx = (int)(b / ((long long)g.NA * N3 * g.NB));
-    ky = kb + g.NB * ka;
-  } else if (!g.dirz) {  // 5-pass layout [kx][kz][ky]: powers of two, shifts only
+  if (!g.dirz) {  // 5-pass layout [kx][kz][ky]: powers of two, shifts only
     const int s2 = __ffs(N2l) - 1, s3 = __ffs(N3) - 1;
     ky = (int)(b & (N2l - 1)) + g.ky0;  // y-chunk pencil (slab mode): global k_y
     kz = (int)((b >> s2) & (N3 - 1));
@@ -2495,7 +2393,7 @@ int launch_scalar(const Ctx& cx, int slot, int mode, cudaStream_t s) {
   const Geo& g = cx.g;
   int nblk;
   if (slot == RED_RNORM) {
-    nblk = g.NB > 0 ? g.NA * g.N3 * g.c : (g.dirz ? g.c * g.N2 * (g.N1 / 16) : g.c * g.P3 * g.N2 / 8);
+    nblk = g.dirz ? g.c * g.N2 * (g.N1 / 16) : g.c * g.P3 * g.N2 / 8;
   } else if (slot == RED_GAMMA) {
     nblk = gpass_nblk(g);
   } else {
@@ -2504,13 +2402,7 @@ int launch_scalar(const Ctx& cx, int slot, int mode, cudaStream_t s) {
       const int TY = (TX == 32 && k_nr(g) == 4) ? 16 : KT_TY;
       nblk = (g.N1 / TX) * (g.N2 / TY) * ((g.P3 + ZC - 1) / ZC);
     } else if (g.dim == 3) {
-      const char* e = getenv("UNO_ELASTIC_DENSE");
-      if (!(e && e[0] == '1')) {
-        nblk = kp_elastic_modal_nblk(g);
-      } else {
-        const int ZC = g.N3 < 16 ? g.N3 : 16;
-        nblk = (g.N1 / KE_TX) * (g.N2 / KE_TY) * ((g.P3 + ZC - 1) / ZC);
-      }
+      nblk = kp_elastic_modal_nblk(g);
     } else {
       nblk = (int)((g.n + 255) / 256);
     }
@@ -2572,18 +2464,14 @@ static void set_smem(K kernel, int bytes) {
 
 int launch_xfwd(const Ctx& cx, int mode, const double* src, cudaStream_t s, int b0, int nb) {
   const Geo& g = cx.g;
-  static const bool rd = [] {
-    const char* e = getenv("UNO_XRD");
-    return !(e && e[0] == '0');
-  }();
-  if (rd && g.N1 == 256) {
+  if (g.N1 == 256) {
     const dim3 grid(nb > 0 ? (unsigned)nb : (unsigned)((long long)g.c * g.P3 * g.N2 / 8), g.nrhs);
     if (mode == CG) xfwd256_kernel<CG><<<grid, 128, 0, s>>>(cx, src, b0);
     else if (mode == PLAIN) xfwd256_kernel<PLAIN><<<grid, 128, 0, s>>>(cx, src, b0);
     else xfwd256_kernel<STANDALONE><<<grid, 128, 0, s>>>(cx, src, b0);
     return 1;
   }
-  if (rd && g.N1 == 512) {
+  if (g.N1 == 512) {
     const dim3 grid(nb > 0 ? (unsigned)nb : (unsigned)((long long)g.c * g.P3 * g.N2 / 8), g.nrhs);
     if (mode == CG) xfwd512_kernel<CG><<<grid, 128, 0, s>>>(cx, src, b0);
     else if (mode == PLAIN) xfwd512_kernel<PLAIN><<<grid, 128, 0, s>>>(cx, src, b0);
@@ -2613,11 +2501,7 @@ int launch_xfwd(const Ctx& cx, int mode, const double* src, cudaStream_t s, int 
 
 int launch_xinv(const Ctx& cx, int mode, double* dst, cudaStream_t s, int b0, int nb) {
   const Geo& g = cx.g;
-  static const bool rd5 = [] {
-    const char* e = getenv("UNO_XIRD");
-    return !(e && e[0] == '0');
-  }();
-  if (rd5 && g.N1 == 512) {
+  if (g.N1 == 512) {
     const dim3 grid(nb > 0 ? (unsigned)nb : (unsigned)((long long)g.c * g.P3 * g.N2 / 8), g.nrhs);
     if (mode == CG) xinv512_kernel<CG><<<grid, 128, 0, s>>>(cx, dst, b0);
     else if (mode == PLAIN) xinv512_kernel<PLAIN><<<grid, 128, 0, s>>>(cx, dst, b0);
@@ -2648,11 +2532,7 @@ int launch_xinv(const Ctx& cx, int mode, double* dst, cudaStream_t s, int b0, in
 int launch_ypass(const Ctx& cx, int mode, bool inverse, cudaStream_t s, int z0, int zc) {
   const Geo& g = cx.g;
   if (zc > 0 && ((zc | z0) & 7)) return -1;
-  static const bool rd = [] {
-    const char* e = getenv("UNO_YRD");
-    return !(e && e[0] == '0');
-  }();
-  if (rd && g.N2 == 512 && !(zc > 0 && (zc % Y5_ROWS))) {
+  if (g.N2 == 512 && !(zc > 0 && (zc % Y5_ROWS))) {
     const long long nrows = zc > 0 ? (long long)g.c * g.H1 * zc : (long long)g.c * g.H1 * g.N3;
     const dim3 grid((unsigned)((nrows + Y5_ROWS - 1) / Y5_ROWS), g.nrhs);
     if (mode == CG) {
@@ -2664,7 +2544,7 @@ int launch_ypass(const Ctx& cx, int mode, bool inverse, cudaStream_t s, int z0, 
     }
     return 1;
   }
-  if (rd && g.N2 == 256) {
+  if (g.N2 == 256) {
     const long long nrows = zc > 0 ? (long long)g.c * g.H1 * zc : (long long)g.c * g.H1 * g.N3;
     const dim3 grid((unsigned)((nrows + YR_ROWS - 1) / YR_ROWS), g.nrhs);
     if (mode == CG) {
@@ -2694,29 +2574,21 @@ int launch_ypass(const Ctx& cx, int mode, bool inverse, cudaStream_t s, int z0, 
   });
 }
 
-static bool gpass_rd() {
-  static const bool rd = [] {
-    const char* e = getenv("UNO_GRD");
-    return !(e && e[0] == '0');
-  }();
-  return rd;
-}
 static bool gpass_e256(const Geo& g) {
-  return gpass_rd() && g.dim == 3 && !g.dirz && g.c == 3 && g.N3 == 256 && g.N2 % GE_COLS == 0;
+  return g.dim == 3 && !g.dirz && g.c == 3 && g.N3 == 256 && g.N2 % GE_COLS == 0;
 }
 static bool gpass_512(const Geo& g) {
-  return gpass_rd() && g.dim == 3 && !g.dirz && g.c == 1 && g.N3 == 512 && g.N2 % G5_C == 0;
+  return g.dim == 3 && !g.dirz && g.c == 1 && g.N3 == 512 && g.N2 % G5_C == 0;
 }
 // CTAs of the CG-mode G pass = gamma partials per load
 int gpass_nblk(const Geo& g) {
-  if (g.NB > 0) return g.H1 * g.NB;
   if (g.dim == 3 && !g.dirz) return g.H1 * (g.N2 / (gpass_512(g) ? G5_C : (gpass_e256(g) ? GE_COLS : 8)));
   return (int)(((long long)g.H1 * g.P3 + 7) / 8);
 }
 
 int launch_gpass_peer(const Ctx& cx, cudaStream_t s) {
   const Geo& g = cx.g;
-  if (g.dim != 3 || g.dirz || gpass_512(g) || gpass_e256(g) || (gpass_rd() && g.c == 1 && g.N3 == 256)) return -1;
+  if (g.dim != 3 || g.dirz || gpass_512(g) || gpass_e256(g) || (g.c == 1 && g.N3 == 256)) return -1;
   return dispatch_pow2(g.N3, [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
     const dim3 grid((unsigned)(g.H1 * (g.N2 / 8)), g.nrhs);
@@ -2736,7 +2608,6 @@ int launch_gpass_peer(const Ctx& cx, cudaStream_t s) {
 
 int launch_gpass(const Ctx& cx, int mode, cudaStream_t s) {
   const Geo& g = cx.g;
-  const bool rd = gpass_rd();
   if (mode == FWDZ) {  // forward z FFT of the half spectrum (3D periodic; training features)
     if (g.dim != 3 || g.dirz || g.dir3) return -1;
     return dispatch_pow2(g.N3, [&](auto Lc) {
@@ -2755,7 +2626,7 @@ int launch_gpass(const Ctx& cx, int mode, cudaStream_t s) {
       }
     });
   }
-  if (rd && g.dim == 3 && !g.dirz && g.c == 1 && g.N3 == 256) {
+  if (g.dim == 3 && !g.dirz && g.c == 1 && g.N3 == 256) {
     const dim3 grid((unsigned)(g.H1 * (g.N2 / 8)), g.nrhs);
     constexpr int sm = (8 * GR_CS + 256) * 16 + 256 * 8 * 8;
     if (mode == CG) {
@@ -2863,12 +2734,7 @@ int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaS
       k4<<<grid4, 128, sm4, s>>>(cx, mode, src, dst, ZC, zc0, nzl);
     } else if (TX == 32) {
       const int sm2 = KT_RING * (KR2_DPL * (int)sizeof(double) + KR2_PHS);
-      static const int la = [] {
-        const char* e = getenv("UNO_KLA");
-        return e ? atoi(e) : 4;
-      }();
-      auto k2 = la >= 7 ? kp_thermal3d_r2_kernel<32, 7> : la == 6 ? kp_thermal3d_r2_kernel<32, 6>
-                                                                   : kp_thermal3d_r2_kernel<32, 4>;
+      auto k2 = kp_thermal3d_r2_kernel<32, 4>;
       set_smem(k2, sm2);
       k2<<<grid, 128, sm2, s>>>(cx, mode, src, dst, ZC, zc0, nzl);
     }
@@ -2882,16 +2748,7 @@ int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaS
     return 1;
   }
   if (g.dim == 3) {
-    static const bool dense = [] {
-      const char* e = getenv("UNO_ELASTIC_DENSE");
-      return e && e[0] == '1';
-    }();
-    if (!dense) return launch_kp_elastic_modal(cx, mode, src, dst, s);
-    if (g.N1 < KE_TX) return -1;
-    const int ZC = g.N3 < 16 ? g.N3 : 16;
-    const dim3 grid(g.N1 / KE_TX, g.N2 / KE_TY, ((g.P3 + ZC - 1) / ZC) * g.nrhs);
-    kp_elastic3d_kernel<<<grid, KE_TX * KE_TY, 0, s>>>(cx, mode, src, dst, ZC);
-    return 1;
+    return launch_kp_elastic_modal(cx, mode, src, dst, s);
   }
   const dim3 grid((unsigned)((g.n + 255) / 256), g.nrhs);
   kp_elastic2d_kernel<<<grid, 256, 0, s>>>(cx, mode, src, dst);
@@ -2982,20 +2839,12 @@ int blocks_needed_max(const Geo& g) {
     const long long b2 = ((long long)g.H1 * g.P3 + 7) / 8;
     m = m > b2 ? m : b2;
   }
-  if (g.NB > 0) {  // 3-pass schedule: F1/F3 grids NA*N3*c, F2 grid H1*NB
-    const long long a = (long long)g.NA * g.N3 * g.c, b = (long long)g.H1 * g.NB;
-    m = m > a ? m : a;
-    m = m > b ? m : b;
-  }
   long long kb;
   if (g.dim == 3 && g.c == 1) {
     const int TX = g.N1 < 32 ? g.N1 : 32, ZC = g.KZC;
     kb = (long long)(g.N1 / TX) * (g.N2 / KT_TY) * ((g.P3 + ZC - 1) / ZC);
   } else if (g.dim == 3) {
-    const int ZC = g.N3 < 16 ? g.N3 : 16;
-    kb = (long long)(g.N1 / KE_TX) * (g.N2 / KE_TY) * ((g.P3 + ZC - 1) / ZC);
-    const long long km = kp_elastic_modal_nblk(g);
-    kb = kb > km ? kb : km;
+    kb = kp_elastic_modal_nblk(g);
   } else {
     kb = (g.n + 255) / 256;
   }

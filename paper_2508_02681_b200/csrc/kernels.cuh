@@ -80,12 +80,6 @@ int launch_loop_ctl(cudaGraphConditionalHandle h, const LoadState* st, int nrhs,
 int blocks_needed_max(const Geo& g);
 int launch_scalar(const Ctx& cx, int slot, int mode, cudaStream_t s);  // combine partials + CG scalars  // max CTAs per load of any reducing kernel
 
-// 3-pass (four-step) schedule, fft3.cu
-bool schedule3_supported(const Geo& g);
-int launch_f1(const Ctx& cx, int mode, const double* src, cudaStream_t s);
-int launch_f2(const Ctx& cx, int mode, cudaStream_t s);
-int launch_f3(const Ctx& cx, int mode, double* dst, cudaStream_t s);
-
 // elastic K.u in the Walsh-Hadamard modal basis, kp_elastic.cu
 int launch_kp_elastic_modal(const Ctx& cx, int mode, const double* src, double* dst, cudaStream_t s);
 int kp_elastic_modal_nblk(const Geo& g);

@@ -211,11 +211,8 @@ int launch_kp_elastic_modal(const Ctx& cx, int mode, const double* src, double* 
   const int ZC = g.KZC;
   const dim3 grid(g.N1 / KM_TX, g.N2 / KM_TY, ((g.P3 + ZC - 1) / ZC) * g.nrhs);
   const int sm = km_smem_bytes();
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kp_elastic3d_modal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    attr = true;
-  }
+  // the attribute is per device: set it on every launch (cheap), like set_smem in kernels.cu
+  cudaFuncSetAttribute(kp_elastic3d_modal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   kp_elastic3d_modal_kernel<<<grid, KM_T, sm, s>>>(cx, mode, src, dst, ZC);
   return 1;
 }

@@ -430,7 +430,8 @@ static bool fill_peers(const uno_slab_handle* h, double* const* hp, SlabPeers& P
 
 extern "C" uno_status uno_slab_forward_peer(uno_slab_handle* h, double* const* h_peer_recv) {
   SlabPeers P;
-  if (!h || !fill_peers(h, h_peer_recv, P)) return sfail(UNO_ERR_ARG, "null handle / peer pointer array");
+  if (!h) return sfail(UNO_ERR_ARG, "null handle");
+  if (!fill_peers(h, h_peer_recv, P)) return sfail(UNO_ERR_NCCL, "peer receive-buffer table incomplete");
   SKL(launch_xfwd(h->cxy, CG, h->r, h->s));
   const Geo& g = h->gxy;
   const long long rows = (long long)g.nrhs * g.c * g.H1 * h->Z;
@@ -451,7 +452,8 @@ extern "C" uno_status uno_slab_forward_peer(uno_slab_handle* h, double* const* h
 
 extern "C" uno_status uno_slab_green_peer(uno_slab_handle* h, const double* d_recv, double* const* h_peer_recv) {
   SlabPeers P;
-  if (!h || !d_recv || !fill_peers(h, h_peer_recv, P)) return sfail(UNO_ERR_ARG, "null argument / peer pointer array");
+  if (!h || !d_recv) return sfail(UNO_ERR_ARG, "null argument");
+  if (!fill_peers(h, h_peer_recv, P)) return sfail(UNO_ERR_NCCL, "peer receive-buffer table incomplete");
   const Geo& g = h->gxy;
   const long long nlckx = (long long)g.nrhs * g.c * g.H1;
   const dim3 gb(1, (unsigned)std::min<long long>(nlckx, 4096), h->nranks);
@@ -502,9 +504,10 @@ extern "C" uno_status uno_slab_inverse(uno_slab_handle* h, const double* d_recv,
 }
 
 extern "C" uno_status uno_slab_inverse_peer(uno_slab_handle* h, const double* d_recv, double* const* h_peer_halo_recv) {
-  if (!h || !d_recv || !h_peer_halo_recv || h->nranks > kMaxRanks) return sfail(UNO_ERR_ARG, "null argument");
+  if (!h || !d_recv) return sfail(UNO_ERR_ARG, "null argument");
+  if (!h_peer_halo_recv || h->nranks > kMaxRanks) return sfail(UNO_ERR_NCCL, "peer halo table missing / > 8 ranks");
   const int n = h->nranks, lo = (h->rank + n - 1) % n, hi = (h->rank + 1) % n;
-  if (!h_peer_halo_recv[lo] || !h_peer_halo_recv[hi]) return sfail(UNO_ERR_ARG, "null peer halo pointer");
+  if (!h_peer_halo_recv[lo] || !h_peer_halo_recv[hi]) return sfail(UNO_ERR_NCCL, "null peer halo pointer");
   const Geo& g = h->gxy;
   const long long rows = (long long)g.nrhs * g.c * g.H1 * h->Z;
   slab_unpack_kernel<<<pack_grid(rows, h->Yc, h->nranks), pack_threads(h->Yc), 0, h->s>>>(

@@ -56,6 +56,8 @@ struct uno_cg_handle {
   double2 *twx, *twxp, *twy, *twz, *twz2;
   double2 *twx2, *twy2;    // all-Dirichlet: length-2N1 / 2N2 tables of the odd-extension FFTs
   double* rt;             // mixed BC: z-sine-space intermediate vector [nrhs][c][n]
+  char* arena;            // device workspace (uno_cg_workspace_size bytes), see ws_layout
+  bool own_arena;         // allocated by the library (else borrowed from the caller)
   LoadState* st;
   double* partials;
   unsigned* counters;
@@ -83,9 +85,6 @@ struct uno_cg_handle {
   long long last_launches;
   cudaEvent_t e0, e1;
   double lam_min, lam_max;
-  // pipelined schedule: fork/join streams and dependency events used during graph capture
-  cudaStream_t aux[2];
-  cudaEvent_t pev[4];
   // preconditioner kind (0 UNO, 1 identity, 2 Jacobi) and the Jacobi inverse diagonal [n]
   int precond;
   double* dinv;
@@ -137,6 +136,7 @@ static void elastic_element(int d, double h, std::vector<double>& Kl, std::vecto
 }
 
 static bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
+static bool g_pool_cfg[64];  // default memory pool configured, per device ordinal
 
 static Ctx make_ctx(uno_cg_handle* h) {
   Ctx cx;
@@ -171,19 +171,14 @@ static void free_all(uno_cg_handle* h) {
   if (!h) return;
   if (h->gexec) cudaGraphExecDestroy(h->gexec);
   for (auto e : h->tev) cudaEventDestroy(e);
-  void* bufs[] = {h->r, h->d, h->p, h->u, h->spec, h->gtab, h->kel, h->twx, h->twxp, h->twy, h->twz, h->twz2, h->rt,
-                  h->twx2, h->twy2, h->tspec,
-                  h->st, h->partials, h->counters, h->results, h->scratch, h->hist, h->loopctr, h->dinv};
+  if (h->arena && h->own_arena) cudaFreeAsync(h->arena, h->stream);
+  void* bufs[] = {h->tspec, h->hist, h->dinv};  // allocated on demand, outside the workspace
   for (void* b : bufs)
     if (b) cudaFreeAsync(b, h->stream);
   if (h->h_st) cudaFreeHost(h->h_st);
   if (h->h_small) cudaFreeHost(h->h_small);
   if (h->e0) cudaEventDestroy(h->e0);
   if (h->e1) cudaEventDestroy(h->e1);
-  for (auto st : h->aux)
-    if (st) cudaStreamDestroy(st);
-  for (auto e : h->pev)
-    if (e) cudaEventDestroy(e);
   delete h;
 }
 
@@ -251,11 +246,9 @@ static uno_status setup_problem(uno_cg_handle* h) {
   return UNO_OK;
 }
 
-// ------------------------------------------------------------------------------ create/destroy
-extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_phase, uno_cg_handle** out) {
-  if (!desc || !d_phase || !out) return fail(UNO_ERR_ARG, "null argument");
-  *out = nullptr;
-  const uno_cg_desc& D = *desc;
+// Validate a descriptor and derive the handle's geometry (shared by uno_cg_workspace_size and
+// uno_cg_create, so both see the same grid).
+static uno_status make_geo(const uno_cg_desc& D, Geo& g) {
   if (D.dim != 2 && D.dim != 3) return fail(UNO_ERR_ARG, "dim must be 2 or 3");
   if (D.physics != UNO_THERMAL && D.physics != UNO_ELASTIC) return fail(UNO_ERR_ARG, "physics must be 0 or 1");
   // boundary conditions: all periodic, or (3D) periodic x, y with Dirichlet z (mixed)
@@ -287,12 +280,7 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
   if (dmask2 && (N1 < 16 || N2 < 16 || N1 > 512 || N2 > 512))
     return fail(UNO_ERR_SHAPE, "2D Dirichlet / mixed needs 16 <= N1, N2 <= 512");
   if (D.seed != 0 && !(D.amp >= 0 && D.amp < 1)) return fail(UNO_ERR_ARG, "amp must be in [0, 1)");
-
-  uno_cg_handle* h = new uno_cg_handle();  // value-initialised: all members zero
-  h->desc = D;
-  h->stream = (cudaStream_t)D.stream;
-  h->phase = d_phase;
-  Geo& g = h->g;
+  std::memset(&g, 0, sizeof(g));
   g.dim = D.dim;
   g.c = c;
   g.nrhs = D.nrhs;
@@ -310,19 +298,6 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
   g.nspec = (dir3 || dmask2 == 3) ? g.n : (long long)g.H1 * N2 * g.P3;
   g.h = D.h > 0 ? D.h : 1.0 / N1;
   g.C = c * (c + 1) / 2;
-  g.NA = g.NB = 0;
-  {  // transform schedule: 5-pass by default (faster on B200 so far);
-     // UNO_SCHEDULE=3 selects the 3-pass four-step schedule where it applies
-    const char* ev = getenv("UNO_SCHEDULE");
-    const bool want3 = ev && ev[0] == '3';
-    Geo t3 = g;
-    t3.NB = N2 >= 128 ? 16 : 8;
-    t3.NA = N2 / t3.NB;
-    if (want3 && !dirz && !dir3 && schedule3_supported(t3)) {
-      g.NB = t3.NB;
-      g.NA = t3.NA;
-    }
-  }
   // z planes per K CTA: 32, halved (down to 4) while the K grid is under two waves of 2 CTAs per
   // SM (small grids such as configs 1 and 2 would otherwise leave most SMs idle)
   g.KZC = g.N3 < 32 ? g.N3 : 32;
@@ -332,90 +307,139 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
     auto kblocks = [&](int zc) { return per * ((g.P3 + zc - 1) / zc) * g.nrhs; };
     while (g.KZC > 4 && kblocks(g.KZC) < 2LL * 148 * 2) g.KZC /= 2;
   }
-  g.ZP = 0;
-  {  // L2-pipelined 5-pass schedule (z-chunks), UNO_ZPIPE=<planes per chunk>
-    const char* ev = getenv("UNO_ZPIPE");
-    const int Z = ev ? atoi(ev) : 0;
-    if (Z > 0 && g.dim == 3 && c == 1 && !dirz && !dir3 && g.NB == 0 && N1 >= 32 && Z % 8 == 0 && N3 % Z == 0 && N3 / Z >= 2) {
-      g.ZP = Z;
-      g.KZC = Z;
-    }
+  return UNO_OK;
+}
+
+// Device workspace of a handle: every buffer the library owns, carved from one arena (caller-
+// provided or allocated here) at 256-byte aligned offsets.  Order = WS_* below.
+enum { WS_R, WS_D, WS_P, WS_U, WS_SPEC, WS_GTAB, WS_KEL, WS_TWX, WS_TWXP, WS_TWY, WS_TWZ, WS_TWZ2, WS_RT, WS_TWX2,
+       WS_TWY2, WS_ST, WS_PART, WS_CNT, WS_RES, WS_SCR, WS_LOOP, WS_N };
+
+static size_t scratch_doubles(const Geo& g) {
+  return (size_t)std::max<long long>((long long)(kMaxRhs * kMaxRhs + 1) * (148 * 4 + 1) * 2 + 64,
+                                     (long long)g.nrhs * g.c * 148 * 2 + g.nrhs * g.c + 64);
+}
+
+static size_t ws_layout(const Geo& g, size_t off[WS_N]) {
+  const size_t vec = (size_t)g.nrhs * g.c * g.n * 8;
+  const size_t sz[WS_N] = {
+      vec, vec, vec, vec, (size_t)g.nrhs * g.c * g.nspec * 16, (size_t)g.C * g.nspec * 8, 2 * 576 * 8,
+      (size_t)g.M * 16, (size_t)(g.M + 1) * 16, (size_t)g.N2 * 16, (size_t)g.N3 * 16, (size_t)2 * g.N3 * 16,
+      (g.dirz || g.dmask) ? vec : 8, g.dmask ? (size_t)2 * g.N1 * 16 : 16, g.dmask ? (size_t)2 * g.N2 * 16 : 16,
+      kMaxRhs * sizeof(LoadState), (size_t)RED_NSLOT * kMaxRhs * blocks_needed_max(g) * 8,
+      RED_NSLOT * kMaxRhs * sizeof(unsigned), RED_NSLOT * kMaxRhs * 8, scratch_doubles(g) * 8, 64};
+  size_t t = 0;
+  for (int i = 0; i < WS_N; ++i) {
+    if (off) off[i] = t;
+    t += (sz[i] + 255) & ~(size_t)255;
   }
+  return t;
+}
+
+extern "C" uno_status uno_cg_workspace_size(const uno_cg_desc* desc, size_t* bytes) {
+  if (!desc || !bytes) return fail(UNO_ERR_ARG, "null argument");
+  Geo g;
+  const uno_status st = make_geo(*desc, g);
+  if (st != UNO_OK) return st;
+  *bytes = ws_layout(g, nullptr);
+  return UNO_OK;
+}
+
+// ------------------------------------------------------------------------------ create/destroy
+extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_phase, void* d_workspace,
+                                    uno_cg_handle** out) {
+  if (!desc || !d_phase || !out) return fail(UNO_ERR_ARG, "null argument");
+  *out = nullptr;
+  if (((uintptr_t)d_workspace & 255) != 0) return fail(UNO_ERR_ARG, "d_workspace must be 256-byte aligned");
+  const uno_cg_desc& D = *desc;
+  Geo g0;
+  const uno_status gs = make_geo(D, g0);
+  if (gs != UNO_OK) return gs;
+
+  uno_cg_handle* h = new uno_cg_handle();  // value-initialised: all members zero
+  h->desc = D;
+  h->stream = (cudaStream_t)D.stream;
+  h->phase = d_phase;
+  h->g = g0;
+  const Geo& g = h->g;
   cudaStream_t s = h->stream;
-  const long long vec = (long long)g.nrhs * c * g.n;
-  static bool pool_cfg = false;
-  if (!pool_cfg) {  // keep freed workspace in the stream-ordered pool (cheap create/destroy)
-    int dev = 0;
-    cudaGetDevice(&dev);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !g_pool_cfg[dev]) {  // keep freed pool memory cached on this device
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
       uint64_t thr = ~0ULL;
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
-    pool_cfg = true;
+    g_pool_cfg[dev] = true;
   }
-  auto al = [&](void** p, size_t bytes) -> cudaError_t { return cudaMallocAsync(p, bytes ? bytes : 8, s); };
-  cudaError_t e = cudaSuccess;
-  const int maxb = blocks_needed_max(g);
+  size_t off[WS_N];
+  const size_t total = ws_layout(g, off);
+  h->scratch_len = scratch_doubles(g);
   h->hist_stride = 0;
-  h->scratch_len = (size_t)std::max<long long>(
-      (long long)(kMaxRhs * kMaxRhs + 1) * (148 * 4 + 1) * 2 + 64,
-      (long long)g.nrhs * c * 148 * 2 + g.nrhs * c + 64);
-  if ((e = al((void**)&h->r, vec * 8)) || (e = al((void**)&h->d, vec * 8)) || (e = al((void**)&h->p, vec * 8)) ||
-      (e = al((void**)&h->u, vec * 8)) || (e = al((void**)&h->spec, (size_t)g.nrhs * c * g.nspec * 16)) ||
-      (e = al((void**)&h->gtab, (size_t)g.C * g.nspec * 8)) || (e = al((void**)&h->kel, 2 * 576 * 8)) ||
-      (e = al((void**)&h->twx, g.M * 16)) || (e = al((void**)&h->twxp, (g.M + 1) * 16)) ||
-      (e = al((void**)&h->twy, N2 * 16)) || (e = al((void**)&h->twz, N3 * 16)) ||
-      (e = al((void**)&h->twz2, 2 * N3 * 16)) || (e = al((void**)&h->rt, (dirz || g.dmask) ? vec * 8 : 8)) ||
-      (e = al((void**)&h->twx2, g.dmask ? 2 * N1 * 16 : 16)) || (e = al((void**)&h->twy2, g.dmask ? 2 * N2 * 16 : 16)) ||
-      (e = al((void**)&h->st, kMaxRhs * sizeof(LoadState))) ||
-      (e = al((void**)&h->partials, (size_t)RED_NSLOT * kMaxRhs * maxb * 8)) ||
-      (e = al((void**)&h->counters, RED_NSLOT * kMaxRhs * sizeof(unsigned))) ||
-      (e = al((void**)&h->results, RED_NSLOT * kMaxRhs * 8)) || (e = al((void**)&h->scratch, h->scratch_len * 8)) ||
-      (e = al((void**)&h->loopctr, 64)) ||
-      (e = cudaMallocHost((void**)&h->h_st, kMaxRhs * sizeof(LoadState))) ||
+  cudaError_t e = cudaSuccess;
+  if (d_workspace) {
+    h->arena = (char*)d_workspace;
+    h->own_arena = false;
+  } else if ((e = cudaMallocAsync((void**)&h->arena, total, s)) != cudaSuccess) {
+    h->arena = nullptr;
+    free_all(h);
+    return fail(UNO_ERR_CUDA, std::string("workspace allocation: ") + cudaGetErrorString(e));
+  } else {
+    h->own_arena = true;
+  }
+  char* A = h->arena;
+  h->r = (double*)(A + off[WS_R]);
+  h->d = (double*)(A + off[WS_D]);
+  h->p = (double*)(A + off[WS_P]);
+  h->u = (double*)(A + off[WS_U]);
+  h->spec = (double2*)(A + off[WS_SPEC]);
+  h->gtab = (double*)(A + off[WS_GTAB]);
+  h->kel = (double*)(A + off[WS_KEL]);
+  h->twx = (double2*)(A + off[WS_TWX]);
+  h->twxp = (double2*)(A + off[WS_TWXP]);
+  h->twy = (double2*)(A + off[WS_TWY]);
+  h->twz = (double2*)(A + off[WS_TWZ]);
+  h->twz2 = (double2*)(A + off[WS_TWZ2]);
+  h->rt = (double*)(A + off[WS_RT]);
+  h->twx2 = (double2*)(A + off[WS_TWX2]);
+  h->twy2 = (double2*)(A + off[WS_TWY2]);
+  h->st = (LoadState*)(A + off[WS_ST]);
+  h->partials = (double*)(A + off[WS_PART]);
+  h->counters = (unsigned*)(A + off[WS_CNT]);
+  h->results = (double*)(A + off[WS_RES]);
+  h->scratch = (double*)(A + off[WS_SCR]);
+  h->loopctr = (int*)(A + off[WS_LOOP]);
+  if ((e = cudaMallocHost((void**)&h->h_st, kMaxRhs * sizeof(LoadState))) ||
       (e = cudaMallocHost((void**)&h->h_small, 4096 * 8)) || (e = cudaEventCreate(&h->e0)) ||
       (e = cudaEventCreate(&h->e1))) {
     free_all(h);
     return fail(UNO_ERR_CUDA, std::string("allocation: ") + cudaGetErrorString(e));
   }
-  if (g.ZP > 0) {
-    for (auto& st : h->aux)
-      if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking))) break;
-    for (auto& ev : h->pev)
-      if (!e) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
-    if (e) {
-      free_all(h);
-      return fail(UNO_ERR_CUDA, std::string("stream/event creation: ") + cudaGetErrorString(e));
-    }
-  }
   cudaMemsetAsync(h->counters, 0, RED_NSLOT * kMaxRhs * sizeof(unsigned), s);
   cudaMemsetAsync(h->st, 0, kMaxRhs * sizeof(LoadState), s);
   cudaMemsetAsync(h->loopctr, 0, 64, s);
   // twiddles (long double on the host)
+  const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
   std::vector<double2> t;
-  twiddles(g.M, g.M, t);
-  cudaMemcpyAsync(h->twx, t.data(), g.M * 16, cudaMemcpyHostToDevice, s);
-  cudaStreamSynchronize(s);
-  twiddles(g.M + 1, N1, t);
-  cudaMemcpyAsync(h->twxp, t.data(), (g.M + 1) * 16, cudaMemcpyHostToDevice, s);
-  cudaStreamSynchronize(s);
-  twiddles(N2, N2, t);
-  cudaMemcpyAsync(h->twy, t.data(), N2 * 16, cudaMemcpyHostToDevice, s);
-  cudaStreamSynchronize(s);
-  twiddles(N3, N3, t);
-  cudaMemcpyAsync(h->twz, t.data(), N3 * 16, cudaMemcpyHostToDevice, s);
-  cudaStreamSynchronize(s);
-  twiddles(2 * N3, 2 * N3, t);
-  cudaMemcpyAsync(h->twz2, t.data(), 2 * N3 * 16, cudaMemcpyHostToDevice, s);
-  cudaStreamSynchronize(s);
+  auto up = [&](double2* dst, int L, int denom) {
+    twiddles(L, denom, t);
+    cudaMemcpyAsync(dst, t.data(), (size_t)L * 16, cudaMemcpyHostToDevice, s);
+    cudaStreamSynchronize(s);
+  };
+  up(h->twx, g.M, g.M);
+  up(h->twxp, g.M + 1, N1);
+  up(h->twy, N2, N2);
+  up(h->twz, N3, N3);
+  up(h->twz2, 2 * N3, 2 * N3);
   if (g.dmask) {
-    twiddles(2 * N1, 2 * N1, t);
-    cudaMemcpyAsync(h->twx2, t.data(), 2 * N1 * 16, cudaMemcpyHostToDevice, s);
-    cudaStreamSynchronize(s);
-    twiddles(2 * N2, 2 * N2, t);
-    cudaMemcpyAsync(h->twy2, t.data(), 2 * N2 * 16, cudaMemcpyHostToDevice, s);
-    cudaStreamSynchronize(s);
+    up(h->twx2, 2 * N1, 2 * N1);
+    up(h->twy2, 2 * N2, 2 * N2);
+  }
+  e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    free_all(h);
+    return fail(UNO_ERR_CUDA, std::string("create: ") + cudaGetErrorString(e));
   }
   const uno_status st0 = setup_problem(h);
   if (st0 != UNO_OK) {
@@ -473,7 +497,7 @@ extern "C" uno_status uno_cg_set_preconditioner(uno_cg_handle* h, int32_t kind) 
 // ------------------------------------------------------------------------------ training (Alg 4)
 static uno_status train_check(const uno_cg_handle* h) {
   const Geo& g = h->g;
-  if (g.dim != 3 || g.dirz || g.dmask || g.NB != 0 || g.ZP != 0)
+  if (g.dim != 3 || g.dirz || g.dmask)
     return fail(UNO_ERR_UNSUPPORTED, "training: 3D periodic grids with the 5-pass transforms");
   return UNO_OK;
 }
@@ -601,11 +625,6 @@ extern "C" uno_status uno_cg_apply_precond(uno_cg_handle* h, const double* d_r, 
     KL(launch_xinv(h->cx, STANDALONE, h->rt, s), KC_XI);
     KL(launch_dstz(h->cx, STANDALONE, true, h->rt, d_z, s), KC_XI);
     KL(launch_scalar(h->cx, RED_GAMMA, STANDALONE, s), KC_OTHER);
-  } else if (h->g.NB > 0) {  // 3-pass four-step schedule
-    KL(launch_f1(h->cx, STANDALONE, d_r, s), KC_XF);
-    KL(launch_f2(h->cx, STANDALONE, s), KC_G);
-    KL(launch_f3(h->cx, STANDALONE, d_z, s), KC_XI);
-    KL(launch_scalar(h->cx, RED_GAMMA, STANDALONE, s), KC_OTHER);
   } else {
     KL(launch_xfwd(h->cx, STANDALONE, d_r, s), KC_XF);
     if (h->g.dim == 3) KL(launch_ypass(h->cx, STANDALONE, false, s), KC_Y);
@@ -661,58 +680,6 @@ static int enqueue_iteration(uno_cg_handle* h, cudaStream_t s, cudaEvent_t* ev /
     n += launch_scalar(cx, RED_GAMMA, CG, s);
     if (!run(3, [&] { return launch_xinv(cx, PLAIN, h->rt, s); })) return -1;
     if (!run(4, [&] { return launch_dstz(cx, CG, true, h->rt, nullptr, s); })) return -1;
-  } else if (h->g.NB > 0) {  // 3-pass four-step schedule (fft3.cu)
-    if (!run(0, [&] { return launch_f1(cx, CG, cx.r, s); })) return -1;
-    n += launch_scalar(cx, RED_RNORM, CG, s);
-    if (!run(2, [&] { return launch_f2(cx, CG, s); })) return -1;
-    n += launch_scalar(cx, RED_GAMMA, CG, s);
-    if (!run(4, [&] { return launch_f3(cx, CG, nullptr, s); })) return -1;
-  } else if (h->g.ZP > 0) {
-    // L2-pipelined 5-pass schedule over C = N3/Z z-chunks: the y pass of chunk c
-    // reads the x-pass output of chunk c while it is still L2 resident, likewise x^-1 after y^-1
-    // and K after x^-1 (K of chunk c waits for x^-1 of chunk c+1: its z+1 halo plane).
-    const Geo& g = h->g;
-    const int Z = g.ZP, C = g.N3 / Z, nbx = Z * g.N2 / 8;
-    cudaStream_t s1 = h->aux[0], s2 = h->aux[1];
-    cudaEvent_t ea = h->pev[0], eb = h->pev[1], ec = h->pev[2], ej = h->pev[3];
-    auto fork = [&](cudaStream_t from, cudaStream_t to, cudaEvent_t e) {
-      cudaEventRecord(e, from);
-      cudaStreamWaitEvent(to, e, 0);
-    };
-    if (ev) cudaEventRecordWithFlags(ev[0], s, cudaEventRecordExternal);
-    for (int c = 0; c < C; ++c) {  // phase A: x pass (s) -> y pass (s1)
-      if (launch_xfwd(cx, CG, cx.r, s, c * nbx, nbx) < 0) return -1;
-      fork(s, s1, ea);
-      if (launch_ypass(cx, CG, false, s1, c * Z, Z) < 0) return -1;
-      n += 2;
-    }
-    n += launch_scalar(cx, RED_RNORM, CG, s);
-    fork(s1, s, ej);
-    if (ev) cudaEventRecordWithFlags(ev[1], s, cudaEventRecordExternal);
-    if (!run(2, [&] { return launch_gpass(cx, CG, s); })) return -1;
-    n += launch_scalar(cx, RED_GAMMA, CG, s);
-    if (ev) cudaEventRecordWithFlags(ev[8], s, cudaEventRecordExternal);
-    fork(s, s1, ea);  // s1: x^-1 chain; s2: K chain
-    fork(s, s2, eb);
-    for (int c = 0; c < C; ++c) {  // phase C: y^-1 (s) -> x^-1 (s1) -> K (s2, one chunk behind)
-      if (launch_ypass(cx, CG, true, s, c * Z, Z) < 0) return -1;
-      fork(s, s1, ea);
-      if (launch_xinv(cx, CG, nullptr, s1, c * nbx, nbx) < 0) return -1;
-      n += 2;
-      if (c >= 2) {
-        fork(s1, s2, ec);
-        if (launch_kapply(cx, CG, cx.d, cx.p, s2, c - 1, 1) < 0) return -1;
-        ++n;
-      }
-    }
-    fork(s1, s2, ec);
-    if (C >= 2 && launch_kapply(cx, CG, cx.d, cx.p, s2, C - 1, 1) < 0) return -1;
-    if (launch_kapply(cx, CG, cx.d, cx.p, s2, 0, 1) < 0) return -1;
-    n += 2;
-    fork(s2, s, ej);
-    if (ev) cudaEventRecordWithFlags(ev[9], s, cudaEventRecordExternal);
-    n += launch_scalar(cx, RED_DP, CG, s);
-    return n;
   } else {
     const bool d3 = h->g.dim == 3;
     if (!run(0, [&] { return launch_xfwd(cx, CG, cx.r, s); })) return -1;
@@ -842,8 +809,8 @@ extern "C" uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, doub
   }
   CK(cudaMemcpyAsync(h->st, h->h_st, g.nrhs * sizeof(LoadState), cudaMemcpyHostToDevice, s));
   const long long work = (long long)g.nrhs * g.c * g.n;
-  // passes + 3 scalar kernels (mixed: 6 too); pipelined: 2C + 1 + 3C over C z-chunks
-  const int per_iter = h->precond != 0 ? 6 : g.dmask ? 15 : (g.ZP > 0 ? 5 * (g.N3 / g.ZP) + 4 : ((g.dim == 3 && g.NB == 0) ? 6 : 4) + 3);
+  // passes + 3 scalar kernels (mixed: 6 too)
+  const int per_iter = h->precond != 0 ? 6 : g.dmask ? 15 : (g.dim == 3 ? 6 : 4) + 3;
   if (!h->timing) {
     // whole solve device-side: WHILE node over bodies of `chunk` iterations
     const int chunk = work >= (1LL << 22) ? 2 : 4;
@@ -880,7 +847,7 @@ extern "C" uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, doub
       const int worked = std::min(chunk, std::max(0, after - before));
       for (int i = 0; i < worked; ++i)
         for (int slot = 0; slot < 6; ++slot) {
-          if ((g.dim == 2 || g.NB > 0) && (slot == 1 || slot == 3)) continue;
+          if (g.dim == 2 && (slot == 1 || slot == 3)) continue;
           float ms = 0.f;
           if (cudaEventElapsedTime(&ms, h->tev[((size_t)i * 6 + slot) * 2], h->tev[((size_t)i * 6 + slot) * 2 + 1]) ==
               cudaSuccess) {
@@ -919,8 +886,10 @@ extern "C" uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, doub
     }
     if (st.status != 0 && worst == UNO_OK) worst = (uno_status)st.status;
   }
-  if (h_hist && h->hist) {
-    CK(cudaMemcpy(h_hist, h->hist, (size_t)g.nrhs * h->hist_stride * 8, cudaMemcpyDeviceToHost));
+  if (h_hist && h->hist) {  // rows of this solve's cap + 1 entries (the device stride may be longer)
+    CK(cudaMemcpy2DAsync(h_hist, (size_t)(cap + 1) * 8, h->hist, (size_t)h->hist_stride * 8, (size_t)(cap + 1) * 8,
+                         g.nrhs, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
   }
   if (worst != UNO_OK) return fail(worst, "PCG breakdown or non-finite residual (see per-load report)");
   return UNO_OK;
@@ -974,10 +943,11 @@ static uno_status read_coefficients(uno_cg_handle* h, int load, std::vector<doub
   gam.assign(m, 0.0);
   alp.assign(m, 0.0);
   if (m > 0) {
-    CK(cudaMemcpy(gam.data(), h->hist + ((long long)1 * kMaxRhs + load) * h->hist_stride, (size_t)m * 8,
-                  cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(alp.data(), h->hist + ((long long)2 * kMaxRhs + load) * h->hist_stride, (size_t)m * 8,
-                  cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(gam.data(), h->hist + ((long long)1 * kMaxRhs + load) * h->hist_stride, (size_t)m * 8,
+                       cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaMemcpyAsync(alp.data(), h->hist + ((long long)2 * kMaxRhs + load) * h->hist_stride, (size_t)m * 8,
+                       cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
   }
   return UNO_OK;
 }

@@ -68,10 +68,39 @@ def test_library_loads_and_validates_without_gpu():
         B.uno_cg_create(d, 1)
     assert e.value.status == B.UNO_ERR_SHAPE
     d.n[0] = 16
-    d.bc[0] = 1  # Dirichlet on x: only all-periodic or periodic x,y + Dirichlet z are built
+    d.bc[0] = 1  # Dirichlet on x only: not one of the built boundary patterns
     with pytest.raises(B.UnoError) as e:
         B.uno_cg_create(d, 1)
     assert e.value.status == B.UNO_ERR_UNSUPPORTED
+    with pytest.raises(B.UnoError) as e:
+        B.uno_cg_workspace_size(d)
+    assert e.value.status == B.UNO_ERR_UNSUPPORTED
+    d.bc[0] = 0
+    with pytest.raises(B.UnoError) as e:  # misaligned caller workspace, rejected before any device work
+        B.uno_cg_create(d, 1, 8)
+    assert e.value.status == B.UNO_ERR_ARG
+
+
+def test_workspace_size_accounts_for_the_cg_state():
+    _ensure_built()
+    import torch  # noqa: F401
+
+    from paper_2508_02681_b200 import binding as B
+
+    d = B.UnoCgDesc()
+    d.dim, d.n[0], d.n[1], d.n[2], d.nrhs = 3, 256, 256, 256, 3
+    d.mat[0][0], d.mat[1][0] = 1.0, 100.0
+    n = 256 ** 3
+    ws = B.uno_cg_workspace_size(d)
+    vec = 3 * n * 8
+    spec = 3 * 129 * 256 * 256 * 16
+    gtab = 129 * 256 * 256 * 8
+    assert 4 * vec + spec + gtab <= ws <= 4 * vec + spec + gtab + (64 << 20)  # r, d, p, u + spectrum + G_hat + small
+    assert ws % 256 == 0
+    d.physics, d.nrhs = 1, 1  # elastic: 3 components, 6 symbol planes
+    d.mat[0][1] = d.mat[1][1] = 1.0
+    ws_e = B.uno_cg_workspace_size(d)
+    assert ws_e >= 4 * 3 * n * 8 + 3 * 129 * 256 * 256 * 16 + 6 * 129 * 256 * 256 * 8
 
 
 def test_slab_create_validates_without_gpu():

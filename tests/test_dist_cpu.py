@@ -34,7 +34,7 @@ def _worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     probs = [(m, R) for R in synth.CFG3_CONTRASTS for m in range(8)]
-    mine = D.shard(probs, world, rank, cost=_eq27_cost)
+    mine = D.config3_shard(world, rank)  # bench.py's assignment of the fixed 48-problem batch
     rr = D.shard(probs, world, rank)
     t = D.reduce_max(10.0 + rank)
     s = D.reduce_sum(len(mine))
@@ -67,6 +67,26 @@ def test_gloo_world2_sharding_and_reductions(world):
         assert t == 10.0 + world - 1                                # max over ranks
         assert s == len(probs)                                      # sum over ranks
         assert [r["p"] for r in res] == [p for _, m, _, _, _, _ in outs for p in m]  # rank-ordered gather
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_config3_shard_partitions_the_fixed_batch(world):
+    # every (microstructure, contrast) pair of the 48-problem batch is solved by exactly one rank;
+    # 8 ranks: Latin square (every rank all six contrasts, six distinct microstructures);
+    # 2/4 ranks: LPT on the Eq 27 cost, balanced to 2 %
+    probs = [(m, R) for R in synth.CFG3_CONTRASTS for m in range(8)]
+    parts = [D.config3_shard(world, r) for r in range(world)]
+    assert sorted(p for part in parts for p in part) == sorted(probs)
+    assert D.config3_problems() == probs
+    if world == 8:
+        for part in parts:
+            assert sorted(R for _, R in part) == sorted(synth.CFG3_CONTRASTS)
+            assert len({m for m, _ in part}) == 6
+            assert [(m, j) for (m, _), j in zip(part, range(6))] == \
+                [a for a in synth.config3_assignment(8, parts.index(part))]
+    cost = [sum(D.eq27_cost(p) for p in part) for part in parts]
+    assert max(cost) / min(cost) < 1.02
+    assert abs(D.eq27_cost((0, 100.0)) - _eq27_cost((0, 100.0))) < 1e-9
 
 
 def test_shard_single_rank_is_identity():

@@ -60,18 +60,8 @@ def loads_for(physics, d, nrhs):
 
 SHAPES = [((16, 8, 32), "thermal"), ((32, 16, 8), "thermal"), ((64, 64, 64), "thermal"), ((32, 32), "thermal"),
           ((8, 64), "thermal"), ((16, 8, 16), "elastic"), ((32, 16, 8), "elastic"), ((16, 32), "elastic"),
-          # 3-pass (four-step) schedule shapes: N2 in {64, 128, 256}, N3 >= 16
+          # long y axes with short z
           ((32, 64, 16), "thermal"), ((16, 128, 32), "thermal"), ((32, 256, 16), "thermal"), ((16, 64, 16), "elastic")]
-
-
-@pytest.fixture(params=["3", "5", "5p"])
-def schedule(request, monkeypatch):
-    """Every transform schedule (UNO_SCHEDULE / UNO_ZPIPE are read at handle creation);
-    "5p" = 5-pass with the z-chunk pipelined CG iteration (16-plane chunks)."""
-    monkeypatch.setenv("UNO_SCHEDULE", request.param[0])
-    if request.param == "5p":
-        monkeypatch.setenv("UNO_ZPIPE", "16")
-    return request.param
 
 
 @pytest.mark.parametrize("N,physics", SHAPES)
@@ -89,7 +79,7 @@ def test_apply_K_parity(N, physics):
 
 
 @pytest.mark.parametrize("N,physics", SHAPES)
-def test_apply_precond_parity(N, physics, schedule):
+def test_apply_precond_parity(N, physics):
     g, ph, mat, amp, seed = make_case(N, physics)
     nrhs = 2
     s = solver(ph, physics, mat, nrhs, seed, amp)
@@ -171,7 +161,7 @@ def test_solve_config0():
     _solve_parity(g, "thermal", P.phase, P.mat, np.eye(2), P.seed, P.amp)
 
 
-def test_solve_config1_64cubed(schedule):
+def test_solve_config1_64cubed():
     P = synth.config1()
     g = fem.Grid((64, 64, 64), h=1 / 64)
     _solve_parity(g, "thermal", P.phase, P.mat, P.loads, P.seed, P.amp)
@@ -251,9 +241,9 @@ def _full_size_reference():
     return _FULL_REF
 
 
-def test_full_size_every_schedule(schedule):
-    # 256^3 in every schedule: the size-specialised register-direct kernels (x/y/z passes and the
-    # 3-pass F1/F2/F3 at N = 256) only run at this size.
+def test_full_size_256():
+    # 256^3: the size-specialised register-direct kernels (x/y/z passes at N = 256) only run at
+    # this size.
     ref = _full_size_reference()
     s = solver(ref["ph"], "thermal", (1.0, 50.0), 1, 3005, 0.1)
     z = s.apply_precond(torch.from_numpy(ref["r"][None]).to(dev())).cpu().numpy()[0]
@@ -770,3 +760,52 @@ def test_mixed_register_direct_x_pass(N, physics):
     us = msolver(ph, physics, mat, 2, seed, amp).solve(loads, fixed_iters=4).u.cpu().numpy()
     for l in range(2):
         assert rel(us[l], fx["U"][l]) <= 1e-9
+
+
+# ----------------------------------------------------------------------------- boundary (§8(b))
+def test_caller_workspace_equals_library_workspace():
+    # uno_cg_create with a caller-owned workspace (uno_cg_workspace_size bytes) is bitwise the
+    # library-allocated handle; the buffer is not freed by destroy
+    UnoCG = _api()
+    P = synth.config1()
+    ph = torch.from_numpy(P.phase).to(dev())
+    nbytes = UnoCG.workspace_bytes(P.phase.shape, "thermal", 3)
+    ws = torch.full((nbytes + 256,), 0xAB, dtype=torch.uint8, device=dev())
+    off = (-ws.data_ptr()) % 256
+    wsa = ws[off:off + nbytes]
+    a = UnoCG(ph, "thermal", P.mat, nrhs=3, seed=P.seed, amp=P.amp, workspace=wsa)
+    ua = a.solve(P.loads).u.clone()
+    a.close()
+    b = UnoCG(ph, "thermal", P.mat, nrhs=3, seed=P.seed, amp=P.amp)
+    ub = b.solve(P.loads).u
+    assert torch.equal(ua, ub)
+    ws.zero_()  # still valid memory after destroy
+    torch.cuda.synchronize()
+
+
+def test_history_after_a_longer_cap():
+    # the device record only grows; a later solve with a smaller cap must copy
+    # exactly (nrhs, cap + 1) entries per load, row by row
+    P = synth.config1()
+    s = solver(P.phase, "thermal", P.mat, 3, P.seed, P.amp)
+    long = s.solve(P.loads, max_iter=1000, hist=True)
+    short = s.solve(P.loads, max_iter=50, hist=True)
+    assert short.hist.shape == (3, 51)
+    for l in range(3):
+        m = min(50, short.reports[l]["iterations"])
+        assert np.array_equal(short.hist[l, :m + 1], long.hist[l, :m + 1])
+    fx = s.solve(P.loads, fixed_iters=7, max_iter=3, hist=True)  # cap = fixed_iters
+    assert fx.hist.shape == (3, 8) and np.array_equal(fx.hist[:, :8], long.hist[:, :8])
+
+
+def test_api_rejects_wrong_shapes():
+    P = synth.config1()
+    s = solver(P.phase, "thermal", P.mat, 3, P.seed, P.amp)
+    with pytest.raises(ValueError):
+        s.solve(P.loads[:2])  # 2 loads for a 3-load handle
+    with pytest.raises(ValueError):
+        s.apply_K(torch.zeros(s.field_shape, dtype=torch.float32, device=dev()))
+    with pytest.raises(ValueError):
+        s.apply_precond(torch.zeros((2,) + s.field_shape[1:], dtype=torch.float64, device=dev()))
+    with pytest.raises(ValueError):
+        s.solve(P.loads, out=torch.zeros(s.field_shape, dtype=torch.float64))  # host tensor
