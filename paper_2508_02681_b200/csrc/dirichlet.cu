@@ -302,15 +302,18 @@ __global__ void d3_symbol_kernel(Ctx cx, double* gtab, double ref0, double ref1,
     for (int q = 0; q < g.C; ++q) gtab[q * n + b] = 0.0;
     return;
   }
-  double cs[3];
-  cs[0] = cospi((double)m1 / N1);
-  cs[1] = cospi((double)m2 / N2);
-  cs[2] = cospi((double)m3 / N3);
+  double cs[3], omc[3];  // cos theta_i and 1 - cos theta_i = 2 sin^2(theta_i / 2), theta_i = pi m_i / N_i
+  const int mm[3] = {m1, m2, m3}, NN[3] = {N1, N2, N3};
+  for (int i = 0; i < 3; ++i) {
+    cs[i] = cospi((double)mm[i] / NN[i]);
+    const double sh = sinpi((double)mm[i] / (2.0 * NN[i]));
+    omc[i] = 2.0 * sh * sh;
+  }
   const double h = g.h;
   double mass[3], S[3];
   for (int i = 0; i < 3; ++i) mass[i] = (h / 3.0) * (2.0 + cs[i]);
   for (int i = 0; i < 3; ++i) {
-    double v = (2.0 / h) * (1.0 - cs[i]);
+    double v = (2.0 / h) * omc[i];
     for (int j = 0; j < 3; ++j)
       if (j != i) v *= mass[j];
     S[i] = v;
@@ -361,7 +364,7 @@ __global__ void d2_symbol_kernel(Ctx cx, double* gtab, double ref0, double ref1,
   if (b >= ns) return;
   const int N1 = g.N1, N2 = g.N2;
   int kx, m;
-  double cx_, cy, scale;
+  double cx_, cy, scale, omx, omy;  // cosines and 1 - cos = 2 sin^2(half angle)
   unsigned long long canon;
   bool zero;
   if (g.dmask == 3) {
@@ -369,6 +372,8 @@ __global__ void d2_symbol_kernel(Ctx cx, double* gtab, double ref0, double ref1,
     m = (int)(b / N1);
     zero = kx == 0 || m == 0;
     cx_ = cospi((double)kx / N1);
+    const double sh = sinpi((double)kx / (2.0 * N1));
+    omx = 2.0 * sh * sh;
     scale = 4.0 / ((double)N1 * N2);
     canon = zero ? 0 : (unsigned long long)(m - 1) * (N1 - 1) + (kx - 1);
   } else {
@@ -377,6 +382,8 @@ __global__ void d2_symbol_kernel(Ctx cx, double* gtab, double ref0, double ref1,
     zero = m == 0;
     const int ka = 2 * kx <= N1 ? kx : N1 - kx;
     cx_ = cospi(2.0 * ka / N1);
+    const double sh = sinpi((double)ka / N1);
+    omx = 2.0 * sh * sh;
     scale = 2.0 / ((double)N1 * N2);
     const unsigned long long p = zero ? 0 : (unsigned long long)(m - 1);
     const unsigned long long f1 = p * N1 + kx, f2 = p * N1 + (unsigned long long)((N1 - kx) % N1);
@@ -387,7 +394,11 @@ __global__ void d2_symbol_kernel(Ctx cx, double* gtab, double ref0, double ref1,
     return;
   }
   cy = cospi((double)m / N2);
-  const double Sxx = (2.0 / 3.0) * (1.0 - cx_) * (2.0 + cy), Syy = (2.0 / 3.0) * (1.0 - cy) * (2.0 + cx_);
+  {
+    const double sh = sinpi((double)m / (2.0 * N2));
+    omy = 2.0 * sh * sh;
+  }
+  const double Sxx = (2.0 / 3.0) * omx * (2.0 + cy), Syy = (2.0 / 3.0) * omy * (2.0 + cx_);
   const double tr = Sxx + Syy;
   if (g.c == 1) {
     const double rho = seed ? (1.0 - amp + 2.0 * amp * u01(seed, 2, canon)) : 1.0;

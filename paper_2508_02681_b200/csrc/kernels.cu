@@ -2130,13 +2130,17 @@ __global__ void combine_rows_kernel(const double* partials, int nblk, double* ou
 // Perturbation: c=1 rho = 1-amp+2 amp u01(seed,2,canon(k));
 //   c=3 G = Phi + amp tr(Phi)/3 psi(theta), theta_t = u01(seed,2,8 canon(k)+t) (Eq B5);
 //   c=2 analogous with Eq 45.  canon(k) = min(flat(k), flat(-k)).  G(0) = 0.
-__device__ __forceinline__ void axis_trig(int k, int N, double& cs, double& sn) {
+// cos, sin and 1 - cos of theta = 2 pi k / N; 1 - cos is evaluated as 2 sin^2(theta / 2) (no
+// cancellation at low frequency, where the symbol ~ theta^2: relative accuracy ~eps on every bin)
+__device__ __forceinline__ void axis_trig(int k, int N, double& cs, double& sn, double& omc) {
   const int ks = (2 * k <= N) ? k : k - N;  // signed frequency: cos even, sin odd -> G(-k)=G(k) bitwise
   const int ka = ks < 0 ? -ks : ks;
   double s, c;
   sincospi(2.0 * (double)ka / (double)N, &s, &c);
   cs = c;
   sn = ks < 0 ? -s : s;
+  const double sh = sinpi((double)ka / (double)N);
+  omc = 2.0 * sh * sh;
 }
 
 __global__ void build_symbol_kernel(Ctx cx, double* gtab, double ref0, double ref1, unsigned long long seed, double amp) {
@@ -2156,9 +2160,9 @@ __global__ void build_symbol_kernel(Ctx cx, double* gtab, double ref0, double re
     kz = (int)((b / N2l) % g.P3);
     kx = (int)(b / ((long long)N2l * g.P3));
   }
-  double cs[3], sn[3];
-  axis_trig(kx, N1, cs[0], sn[0]);
-  axis_trig(ky, N2, cs[1], sn[1]);
+  double cs[3], sn[3], omc[3];
+  axis_trig(kx, N1, cs[0], sn[0], omc[0]);
+  axis_trig(ky, N2, cs[1], sn[1], omc[1]);
   double inv_n;
   unsigned long long flat, flatm;
   bool zero;
@@ -2169,12 +2173,14 @@ __global__ void build_symbol_kernel(Ctx cx, double* gtab, double ref0, double re
     sincospi((double)(kz + 1) / (double)N3, &sz, &cz);
     cs[2] = cz;
     sn[2] = 0.0;
+    const double shz = sinpi((double)(kz + 1) / (2.0 * N3));
+    omc[2] = 2.0 * shz * shz;
     inv_n = 2.0 / ((double)N1 * N2 * N3);  // F_x F_y unnormalised (N1 N2) x sine sums (N3/2)
     flat = ((unsigned long long)kz * N2 + ky) * N1 + kx;
     flatm = ((unsigned long long)kz * N2 + (unsigned long long)((N2 - ky) % N2)) * N1 + (unsigned long long)((N1 - kx) % N1);
     zero = false;
   } else {
-    axis_trig(kz, N3, cs[2], sn[2]);
+    axis_trig(kz, N3, cs[2], sn[2], omc[2]);
     inv_n = 1.0 / ((double)N1 * N2 * N3);  // = 1/n (N2: the whole grid, also for a y-chunk pencil)
     flat = ((unsigned long long)kz * N2 + ky) * N1 + kx;
     flatm = ((unsigned long long)((N3 - kz) & (N3 - 1)) * N2 + (unsigned long long)((N2 - ky) & (N2 - 1))) * N1 +
@@ -2186,9 +2192,9 @@ __global__ void build_symbol_kernel(Ctx cx, double* gtab, double ref0, double re
   const unsigned long long canon = flat < flatm ? flat : flatm;
   if (g.c == 1 && d == 3) {  // thermal 3D in scalars (same operation order as the general path)
     const double m0 = (h / 3.0) * (2.0 + cs[0]), m1 = (h / 3.0) * (2.0 + cs[1]), m2 = (h / 3.0) * (2.0 + cs[2]);
-    const double S00 = (2.0 / h) * (1.0 - cs[0]) * m1 * m2;
-    const double S11 = (2.0 / h) * (1.0 - cs[1]) * m0 * m2;
-    const double S22 = (2.0 / h) * (1.0 - cs[2]) * m0 * m1;
+    const double S00 = (2.0 / h) * omc[0] * m1 * m2;
+    const double S11 = (2.0 / h) * omc[1] * m0 * m2;
+    const double S22 = (2.0 / h) * omc[2] * m0 * m1;
     const double a = (((0.0 + S00) + S11) + S22) * ref0;
     double gv = 0.0;
     if (!zero) {
@@ -2201,7 +2207,7 @@ __global__ void build_symbol_kernel(Ctx cx, double* gtab, double ref0, double re
   double mass[3], S[3][3];
   for (int i = 0; i < d; ++i) mass[i] = (h / 3.0) * (2.0 + cs[i]);
   for (int i = 0; i < d; ++i) {
-    double v = (2.0 / h) * (1.0 - cs[i]);
+    double v = (2.0 / h) * omc[i];
     for (int j = 0; j < d; ++j)
       if (j != i) v *= mass[j];
     S[i][i] = v;

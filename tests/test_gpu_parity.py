@@ -137,6 +137,7 @@ def _solve_parity(g, physics, ph, mat, loads, seed, amp, max_iter=500):
     assert all(r["converged"] for r in res.reports)
     # common-iteration protocol for every load
     U = np.zeros_like(ref["U"])
+    Uref = np.zeros_like(ref["U"])
     for l in range(nrhs):
         m = ref["iterations"][l]
         fx = homog.solve_problem(g, physics, ph, mat, loads[l:l + 1], seed, amp, fixed_iters=max(m, 1))
@@ -145,9 +146,11 @@ def _solve_parity(g, physics, ph, mat, loads, seed, amp, max_iter=500):
         if np.linalg.norm(fx["U"][0]) > 0:
             assert rel(gu, fx["U"][0]) <= 1e-9, (l, rel(gu, fx["U"][0]))
         U[l] = gu
-    # effective property from the common-iteration solutions
+        Uref[l] = fx["U"][0]
+    # effective property: the GPU's (kernel a9 on the GPU's solutions at the common counts) against
+    # the oracle's (its formula on the oracle's solutions at the same counts), SURVEY C6 step 4
     keff_gpu = s.effective_property(torch.from_numpy(U).to(dev()), loads)
-    keff_ref = homog.effective_from_solutions(g, physics, ph, mat, ref["F"], U, loads)
+    keff_ref = homog.effective_from_solutions(g, physics, ph, mat, ref["F"], Uref, loads)
     assert np.max(np.abs(keff_gpu - keff_ref)) <= 1e-10 * np.max(np.abs(keff_ref))
     # and the converged solutions' effective property against the oracle's converged one
     keff_conv = s.effective_property(res.u, loads)
@@ -469,12 +472,10 @@ def test_maximum_axis_lengths(N, physics):
     assert rel(Ku, fem.apply_K(g, physics, ph, mat, u)) <= 1e-13
     G = greens.ghat(g, physics, mat, seed, amp)
     z = s.apply_precond(torch.from_numpy(u[None]).to(dev())).cpu().numpy()[0]
-    # at N = 1024 the lowest frequencies carry |A(k)| ~ (2 pi / N)^2 ~ 4e-5 of max|A|: the oracle's
-    # probed symbol (an FFT of the stencil response, then inverted) has relative error ~ eps (N / 2pi)^2
-    # ~ 3e-12 there (x the 3x3 block condition ~ 5 for elastic), and those modes dominate z; the
-    # tolerance of the moderate sizes (1e-12) therefore becomes 5e-11 (measured 1.4e-12 thermal,
-    # 1.7e-11 elastic)
-    assert rel(z, greens.apply_precond(G, u)) <= 5e-11
+    # at N = 1024 the lowest frequencies carry |A(k)| ~ (2 pi / N)^2 ~ 4e-5 of max|A| and dominate z:
+    # both sides evaluate 1 - cos(theta) as 2 sin^2(theta / 2) (oracle: stencil DFT; library: closed
+    # form), so the SURVEY C6 tolerance holds on the longest axes too
+    assert rel(z, greens.apply_precond(G, u)) <= 1e-12
 
 
 def test_maximum_load_cases():
@@ -597,7 +598,7 @@ def test_512_point_y_pass(N, physics):
     G = greens.ghat(g, physics, mat, seed, amp)
     r = np.stack([synth.test_vector(91 + l, g.field_shape()) for l in range(2)])
     z = s.apply_precond(torch.from_numpy(r).to(dev())).cpu().numpy()
-    tol = 1e-11 if physics == "thermal" else 5e-11  # long axis: see test_maximum_axis_lengths
+    tol = 1e-12  # long axis: see test_maximum_axis_lengths
     for l in range(2):
         assert rel(z[l], greens.apply_precond(G, r[l])) <= tol
     load = loads_for(physics, 3, 1)
@@ -616,7 +617,7 @@ def test_elastic_256_point_g_pass(N):
     r = np.stack([synth.test_vector(93 + l, g.field_shape()) for l in range(2)])
     z = s.apply_precond(torch.from_numpy(r).to(dev())).cpu().numpy()
     for l in range(2):
-        assert rel(z[l], greens.apply_precond(G, r[l])) <= 5e-11  # long axis: see test_maximum_axis_lengths
+        assert rel(z[l], greens.apply_precond(G, r[l])) <= 1e-12  # long axis: see test_maximum_axis_lengths
     load = loads_for("elastic", 3, 2)
     fx = homog.solve_problem(g, "elastic", ph, mat, load, seed, amp, fixed_iters=4)
     u = solver(ph, "elastic", mat, 2, seed, amp).solve(load, fixed_iters=4).u.cpu().numpy()
@@ -635,7 +636,7 @@ def test_512_point_g_pass(N, physics):
     r = np.stack([synth.test_vector(95 + l, g.field_shape()) for l in range(2)])
     z, rz = s.apply_precond(torch.from_numpy(r).to(dev()), want_dot=True)
     z = z.cpu().numpy()
-    tol = 1e-11 if physics == "thermal" else 5e-11  # long axis: see test_maximum_axis_lengths
+    tol = 1e-12  # long axis: see test_maximum_axis_lengths
     for l in range(2):
         ref = greens.apply_precond(G, r[l])
         assert rel(z[l], ref) <= tol
@@ -736,7 +737,7 @@ def test_512_point_x_pass(N, physics):
     r = np.stack([synth.test_vector(101 + l, g.field_shape()) for l in range(2)])
     z = s.apply_precond(torch.from_numpy(r).to(dev())).cpu().numpy()
     for l in range(2):
-        assert rel(z[l], greens.apply_precond(G, r[l])) <= 2e-16 * 512 ** 2  # long axis
+        assert rel(z[l], greens.apply_precond(G, r[l])) <= 1e-12
     load = loads_for(physics, 3, 2)
     fx = homog.solve_problem(g, physics, ph, mat, load, seed, amp, fixed_iters=4)
     u = solver(ph, physics, mat, 2, seed, amp).solve(load, fixed_iters=4).u.cpu().numpy()
@@ -754,7 +755,7 @@ def test_mixed_register_direct_x_pass(N, physics):
     G = greens.ghat_mixed(g, physics, mat, seed, amp)
     z = s.apply_precond(torch.from_numpy(u).to(dev())).cpu().numpy()
     for l in range(2):
-        assert rel(z[l], greens.apply_precond_mixed(G, u[l])) <= 2e-16 * max(N) ** 2
+        assert rel(z[l], greens.apply_precond_mixed(G, u[l])) <= 1e-12
     loads = np.eye(3 if physics == "thermal" else 6)[[0, 1]]
     fx = homog.solve_problem(g, physics, ph, mat, loads, seed, amp, fixed_iters=4)
     us = msolver(ph, physics, mat, 2, seed, amp).solve(loads, fixed_iters=4).u.cpu().numpy()
