@@ -863,7 +863,10 @@ template <int MODE>
 __global__ void __launch_bounds__(8 * YR_R, 3) gpass256_kernel(Ctx cx) {  // smem: gpass256_smem
   constexpr int L = 256, R = YR_R, RP = R + 1;
   const Geo g = cx.g;
-  const int load = blockIdx.y;
+  // load fastest in the launch order: the nrhs CTAs of one tile read the same symbol rows back to
+  // back, so the repeats are served from L2 (the table is read from HBM once per pass, not nrhs times)
+  const int load = blockIdx.x % g.nrhs;
+  const int tile = blockIdx.x / g.nrhs;
   if (MODE == CG && !cx.st[load].active) return;
   extern __shared__ double2 gsm[];
   double2* buf = gsm;                                          // [8][GR_CS]
@@ -872,8 +875,8 @@ __global__ void __launch_bounds__(8 * YR_R, 3) gpass256_kernel(Ctx cx) {  // sme
   __shared__ double red_sh[32];
   const int t = threadIdx.x, c = t & 7, ln = t >> 3;
   const int ntile_y = g.N2 >> 3;
-  const int kx = blockIdx.x / ntile_y;
-  const int y0 = (blockIdx.x - kx * ntile_y) * 8;
+  const int kx = tile / ntile_y;
+  const int y0 = (tile - kx * ntile_y) * 8;
   const long long boff = (long long)kx * g.N3 * g.N2 + y0;
   double2* col = cx.spec + (long long)load * g.nspec + boff + c;
   const long long zs = g.N2;
@@ -917,7 +920,7 @@ __global__ void __launch_bounds__(8 * YR_R, 3) gpass256_kernel(Ctx cx) {  // sme
   dft_reg<R, true>(v);  // thread = n1: inverse over k1 -> n2
 #pragma unroll
   for (int n2 = 0; n2 < R; ++n2) __stcg(col + (ln + R * n2) * zs, v[n2]);
-  gamma_finish(cx, load, part, red_sh, MODE);
+  partial_write<false>(cx, RED_GAMMA, load, tile, part, red_sh);
 }
 
 // Elastic G pass for N3 = 256 (c = 3), register-direct: tile = 4 consecutive y columns of one kx
@@ -1616,8 +1619,10 @@ __global__ void __launch_bounds__(128, 2) kp_thermal3d_rn_kernel(Ctx cx, int mod
   constexpr int NPCT = (NPC + T - 1) / T;
   const Geo g = cx.g;
   const int nzc = (g.P3 + ZC - 1) / ZC;
-  const int load = blockIdx.z / nzl;
-  const int zcI = zc0 + (blockIdx.z - load * nzl);
+  // load fastest along grid z: the nrhs CTAs of a tile read the same phase bytes close together
+  // in time (L2 hits instead of one HBM read of the phase field per load)
+  const int load = blockIdx.z % g.nrhs;
+  const int zcI = zc0 + blockIdx.z / g.nrhs;
   const int dz = g.dirz;
   if (mode == CG && !cx.st[load].active) return;
   extern __shared__ double ksm[];
@@ -2633,7 +2638,7 @@ int launch_gpass(const Ctx& cx, int mode, cudaStream_t s) {
     });
   }
   if (g.dim == 3 && !g.dirz && g.c == 1 && g.N3 == 256) {
-    const dim3 grid((unsigned)(g.H1 * (g.N2 / 8)), g.nrhs);
+    const dim3 grid((unsigned)(g.H1 * (g.N2 / 8) * g.nrhs));
     constexpr int sm = (8 * GR_CS + 256) * 16 + 256 * 8 * 8;
     if (mode == CG) {
       set_smem(gpass256_kernel<CG>, sm);
