@@ -54,6 +54,11 @@ UNO_API uno_status uno_slab_create(const uno_cg_desc* desc, int32_t rank, int32_
                                    uno_slab_handle** out);
 UNO_API uno_status uno_slab_destroy(uno_slab_handle* h);
 
+/* Re-target the handle's launches to another stream (e.g. the capture stream of a CUDA graph
+ * that records a chunk of iterations, exchanges included, so the iteration loop runs without a
+ * host synchronisation per iteration).  The caller orders it against earlier work.          */
+UNO_API uno_status uno_slab_set_stream(uno_slab_handle* h, void* stream);
+
 /* out[0] = slab vector elements (nrhs*c*Z*N2*N1), out[1] = complex elements per a2a block
  * (nrhs*c*H1*Z*Yc), out[2] = fp64 elements per halo side (nrhs*c*N2*N1), out[3] = Z.    */
 UNO_API uno_status uno_slab_sizes(uno_slab_handle* h, int64_t out[4]);

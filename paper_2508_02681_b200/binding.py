@@ -27,7 +27,7 @@ EXPORTS = ("uno_cg_workspace_size", "uno_cg_create", "uno_cg_destroy", "uno_cg_u
            "uno_cg_kernel_timing", "uno_cg_last_error", "uno_cg_version")
 UNO_PRECOND = {"uno": 0, "identity": 1, "jacobi": 2}
 # include/uno_cg_slab.h (z-slab decomposition)
-SLAB_EXPORTS = ("uno_slab_create", "uno_slab_destroy", "uno_slab_sizes", "uno_slab_begin", "uno_slab_forward",
+SLAB_EXPORTS = ("uno_slab_create", "uno_slab_destroy", "uno_slab_set_stream", "uno_slab_sizes", "uno_slab_begin", "uno_slab_forward",
                 "uno_slab_green", "uno_slab_inverse", "uno_slab_kapply", "uno_slab_reduce", "uno_slab_apply",
                 "uno_slab_state", "uno_slab_finish", "uno_slab_local_means", "uno_slab_subtract_means",
                 "uno_slab_forward_peer", "uno_slab_green_peer", "uno_slab_inverse_peer")
@@ -76,6 +76,7 @@ def _load():
     lib.uno_slab_create.argtypes = [C.POINTER(UnoCgDesc), I32, I32, P, C.POINTER(P)]
     lib.uno_slab_destroy.argtypes = [P]
     lib.uno_slab_sizes.argtypes = [P, P]
+    lib.uno_slab_set_stream.argtypes = [P, P]
     lib.uno_slab_begin.argtypes = [P, P, D, I32, I32]
     lib.uno_slab_forward.argtypes = [P, P]
     lib.uno_slab_green.argtypes = [P, P, P]
@@ -259,6 +260,10 @@ def uno_slab_create(desc: UnoCgDesc, rank: int, nranks: int, d_phase) -> int:
 
 def uno_slab_destroy(h: int):
     _check(_lib.uno_slab_destroy(h), "uno_slab_destroy")
+
+
+def uno_slab_set_stream(h: int, stream: int):
+    _check(_lib.uno_slab_set_stream(h, stream), "uno_slab_set_stream")
 
 
 def uno_slab_sizes(h: int):

@@ -364,6 +364,13 @@ extern "C" uno_status uno_slab_destroy(uno_slab_handle* h) {
   return UNO_OK;
 }
 
+extern "C" uno_status uno_slab_set_stream(uno_slab_handle* h, void* stream) {
+  if (!h) return sfail(UNO_ERR_ARG, "null handle");
+  h->s = (cudaStream_t)stream;
+  h->desc.stream = stream;
+  return UNO_OK;
+}
+
 extern "C" uno_status uno_slab_sizes(uno_slab_handle* h, int64_t out[4]) {
   if (!h || !out) return sfail(UNO_ERR_ARG, "null argument");
   const Geo& g = h->gxy;

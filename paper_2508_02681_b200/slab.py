@@ -8,12 +8,22 @@ and sequences the stages of one iteration:
     forward -> [||r|| all-reduce] -> all-to-all -> green -> [gamma all-reduce] -> all-to-all
     -> inverse -> halo exchange -> kapply -> [d.p all-reduce]
 
-Two transports implement the exchanges with identical buffer semantics:
+Three transports implement the exchanges with identical buffer semantics:
   * DistComm  — one rank per process/GPU, torch.distributed (NCCL on GPUs; gloo in the CPU
-                tests), point-to-point batches for the all-to-all and the halo planes;
+                tests), point-to-point batches for the all-to-all and the halo planes; the
+                peer-memory receive buffers live in torch symmetric memory;
+  * IpcComm   — one rank per process, receive buffers exported with CUDA IPC handles (every
+                rank maps every peer's buffer; the library's pack kernels store straight into
+                them), scalars and stage ordering over a torch.distributed group (gloo or
+                NCCL) with a stream synchronisation per stage: no kernel ever waits on another
+                process, so it also runs two ranks on ONE GPU (the multi-process test);
   * LocalComm — all ranks emulated in this process (one device), plain copies.  Used by the
                 single-GPU parity tests: the per-rank kernels and the data movement pattern
                 are exactly those of the multi-GPU run.
+
+The iteration loop checks convergence on the host only once per chunk of `check_every`
+iterations (converged loads freeze themselves on the device, so the extra bodies are no-ops);
+with graph=True the chunk is captured once as a CUDA graph (exchanges included) and replayed.
 """
 from __future__ import annotations
 
@@ -49,12 +59,12 @@ class LocalComm:
 
     def peer_buffers(self, numel: int, device):
         """Receive buffers for the peer-memory exchange: one per rank, each rank's pointer list
-        holds every rank's buffer (all in this process)."""
+        holds every rank's buffer (all in this process).  Returns (buffers, pointer lists, token)."""
         bufs = [torch.empty(numel, dtype=torch.float64, device=device) for _ in self.ranks]
         ptrs = [[b.data_ptr() for b in bufs] for _ in self.ranks]
-        return bufs, ptrs
+        return bufs, ptrs, None
 
-    def peer_barrier(self):
+    def peer_barrier(self, token):
         pass  # one stream: the emulated ranks' kernels are already ordered
 
     def allreduce(self, vals, op: str):
@@ -104,21 +114,75 @@ class DistComm:
 
     def peer_buffers(self, numel: int, device):
         """Receive buffers in symmetric memory (torch.distributed._symmetric_memory): every rank's
-        buffer is mapped into every process over NVLink; `buffer_ptrs` are the peer addresses."""
+        buffer is mapped into every process over NVLink; `buffer_ptrs` are the peer addresses.
+        The rendezvous handle is the token its barrier is taken on (one per buffer / solver)."""
         import torch.distributed._symmetric_memory as symm_mem
 
         buf = symm_mem.empty(numel, dtype=torch.float64, device=device)
         hdl = symm_mem.rendezvous(buf, self.dist.group.WORLD)
-        self._symm = getattr(self, "_symm", []) + [hdl]
-        return [buf], [list(hdl.buffer_ptrs)]
+        return [buf], [list(hdl.buffer_ptrs)], hdl
 
-    def peer_barrier(self):
-        # device-side barrier over the symmetric-memory signal pads (stream-ordered): every
-        # rank's peer stores of the stage have landed before anyone reads its receive buffer
-        self._symm[0].barrier()
+    def peer_barrier(self, token):
+        # device-side barrier over the symmetric-memory signal pads (stream-ordered on the current
+        # stream, which SlabSolver makes the library's stream): every rank's peer stores of the
+        # stage have landed before anyone reads its receive buffer
+        token.barrier()
 
     def allreduce(self, vals, op: str):
         self.dist.all_reduce(vals[0], op=self.dist.ReduceOp.SUM if op == SUM else self.dist.ReduceOp.MAX)
+
+
+class IpcComm:
+    """One rank per process; peer receive buffers shared with CUDA IPC handles, control over a
+    torch.distributed group (gloo in the single-GPU multi-process test).  A stage's peer stores
+    are ordered before the peers' reads by a stream synchronisation and a group barrier on the
+    host (peer_barrier), never by a kernel waiting on another process."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.nranks = dist.get_world_size(group)
+        self.ranks = [self.rank]
+        self._keep = []  # peers' mapped storages stay alive with the communicator
+
+    def _cpu(self, x):
+        return x.detach().to("cpu")
+
+    def peer_buffers(self, numel: int, device):
+        from torch.multiprocessing.reductions import reduce_tensor
+
+        buf = torch.zeros(numel, dtype=torch.float64, device=device)
+        torch.cuda.synchronize()
+        mine = reduce_tensor(buf)  # (rebuild function, args): a picklable CUDA IPC handle
+        allh = [None] * self.nranks
+        self.dist.all_gather_object(allh, mine, group=self.group)
+        ptrs = []
+        for q, (fn, args) in enumerate(allh):
+            if q == self.rank:
+                ptrs.append(buf.data_ptr())
+            else:
+                t = fn(*args)  # maps rank q's buffer into this process (cudaIpcOpenMemHandle)
+                self._keep.append(t)
+                ptrs.append(t.data_ptr())
+        return [buf], [ptrs], None
+
+    def peer_barrier(self, token):
+        torch.cuda.current_stream().synchronize()  # this rank's peer stores are complete
+        self.dist.barrier(group=self.group)        # ... and so are everyone else's
+
+    def allreduce(self, vals, op: str):
+        t = self._cpu(vals[0])
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM if op == SUM else self.dist.ReduceOp.MAX, group=self.group)
+        vals[0].copy_(t)
+
+    def all_to_all(self, sends, recvs):
+        raise NotImplementedError("IpcComm carries the peer-memory exchange only (SlabSolver(peer=True))")
+
+    def halo(self, sends, recvs):
+        raise NotImplementedError("IpcComm carries the peer-memory exchange only (SlabSolver(peer=True))")
 
 
 @dataclass
@@ -133,7 +197,9 @@ class SlabSolver:
     this process's device (every rank keeps all of it: 1 byte per voxel)."""
 
     def __init__(self, phase: torch.Tensor, physics: str, mat, comm, nrhs: int = 1, seed: int = 0, amp: float = 0.0,
-                 h: float = 0.0, ref=None, peer: bool = False):
+                 h: float = 0.0, ref=None, peer: bool = False, graph: bool | None = None):
+        """graph: capture a chunk of iterations as one CUDA graph (default: only for LocalComm,
+        whose exchanges are device copies; IpcComm orders stages on the host and cannot be)."""
         assert phase.dim() == 3 and phase.dtype == torch.uint8 and phase.is_cuda
         self.phase = phase.contiguous()
         self.comm = comm
@@ -172,12 +238,14 @@ class SlabSolver:
         # the forward transpose, B for the way back); no send buffers, no all-to-all call
         self.peer = peer
         if peer:
-            ra, self.ptrA = comm.peer_buffers(R * 2 * blk, dev)
-            rb, self.ptrB = comm.peer_buffers(R * 2 * blk, dev)
+            ra, self.ptrA, self.tokA = comm.peer_buffers(R * 2 * blk, dev)
+            rb, self.ptrB, self.tokB = comm.peer_buffers(R * 2 * blk, dev)
             self.recvA = [t.view(R, 2 * blk) for t in ra]
             self.recvB = [t.view(R, 2 * blk) for t in rb]
-            hr, self.ptrH = comm.peer_buffers(2 * hs, dev)
+            hr, self.ptrH, self.tokH = comm.peer_buffers(2 * hs, dev)
             self.hrecv = [t.view(2, hs) for t in hr]
+        self.graph = isinstance(comm, LocalComm) if graph is None else bool(graph)
+        self._graphs = {}
 
     def close(self):
         for h in self.handles:
@@ -197,15 +265,15 @@ class SlabSolver:
         if self.peer:
             for h, pa in zip(H, self.ptrA):
                 B.uno_slab_forward_peer(h, pa)    # x, y transforms; blocks stored into the peers' A
-            c.peer_barrier()
+            c.peer_barrier(self.tokA)
             self._scalar(0, MAX)
             for h, ra, pb in zip(H, self.recvA, self.ptrB):
                 B.uno_slab_green_peer(h, ra, pb)  # z . G . z^-1; blocks stored into the peers' B
-            c.peer_barrier()
+            c.peer_barrier(self.tokB)
             self._scalar(1, SUM)
             for h, rb, ph in zip(H, self.recvB, self.ptrH):
                 B.uno_slab_inverse_peer(h, rb, ph)  # boundary planes into the neighbours' halos
-            c.peer_barrier()
+            c.peer_barrier(self.tokH)
             for h, hr in zip(H, self.hrecv):
                 B.uno_slab_kapply(h, hr)
             self._scalar(2, SUM)
@@ -225,19 +293,44 @@ class SlabSolver:
             B.uno_slab_kapply(h, hr)
         self._scalar(2, SUM)                      # d.p -> alpha (l.10)
 
+    def _use_stream(self):
+        st = torch.cuda.current_stream().cuda_stream
+        for h in self.handles:
+            B.uno_slab_set_stream(h, st)
+
+    def _chunk(self, n: int):
+        """n iterations; with graph=True a CUDA graph of them, captured on first use and replayed
+        (the handles' launches go to the capture stream while recording)."""
+        if not self.graph:
+            for _ in range(n):
+                self.iterate()
+            return
+        g = self._graphs.get(n)
+        if g is None:
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                self._use_stream()
+                for _ in range(n):
+                    self.iterate()
+            self._use_stream()  # back to the eager stream
+            self._graphs[n] = g
+        g.replay()
+
     def solve(self, loads, rel_tol: float = 1e-8, max_iter: int = 1000, fixed_iters: int = 0,
-              check_every: int = 1) -> SlabResult:
+              check_every: int = 4) -> SlabResult:
+        self._use_stream()  # launches follow the caller's current stream (ADVICE r01)
         for h in self.handles:
             B.uno_slab_begin(h, loads, rel_tol, max_iter, fixed_iters)
         cap = (fixed_iters if fixed_iters > 0 else max_iter) + 2
         bodies = 0
         while bodies < cap:
-            self.iterate()
-            bodies += 1
-            if bodies % check_every == 0:
-                active, _ = B.uno_slab_state(self.handles[0], self.nrhs)  # identical on every rank
-                if not active:
-                    break
+            n = min(check_every, cap - bodies)
+            self._chunk(n)
+            bodies += n
+            active, _ = B.uno_slab_state(self.handles[0], self.nrhs)  # one host sync per chunk
+            if not active:
+                break
         _, reps = B.uno_slab_state(self.handles[0], self.nrhs)
         us = [torch.empty(self.shape, dtype=torch.float64, device=self.phase.device) for _ in self.handles]
         for h, u in zip(self.handles, us):
