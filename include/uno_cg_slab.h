@@ -30,8 +30,13 @@
  *   halo send/recv: fp64 [2][nrhs][c][N2][N1]; send[0] = my first plane (to rank-1),
  *     send[1] = my last plane (to rank+1); recv[0] = plane zlo-1 (from rank-1),
  *     recv[1] = plane zlo+Z (from rank+1).
- * Scope: 3D, periodic, thermal (N1 >= 32, N2 >= 16 * nranks... see create) and elastic,
- * the 5-pass transforms; N3 % nranks == 0 and N2 % nranks == 0 with Yc >= 8.
+ * Scope: 3D, thermal (N1 >= 32, N2 >= 16) and elastic (N1 >= 16), the 5-pass transforms;
+ * N3 % nranks == 0 and N2 % nranks == 0 with Yc = N2 / nranks >= 8.  Boundary conditions:
+ * periodic, or the mixed case of Eq 82 / §6.4 (bc = {0,0,1}: periodic x, y, Dirichlet faces on
+ * z, U = F_x F_y DST-I_z).  Dirichlet z uses PADDED slab storage: the vectors keep
+ * N3 node planes, plane z = 0 is the fixed Dirichlet face (held at 0 on input and output; rank
+ * 0's first plane), planes 1..N3-1 are the unknowns (the whole-grid handle stores only those
+ * N3-1), so the slabs stay equal; the pencil stage applies the z DST-I after the all-to-all.
  * Errors as in uno_cg.h (uno_cg_last_error()).
  */
 #ifndef UNO_CG_SLAB_H

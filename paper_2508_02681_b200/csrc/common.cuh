@@ -28,6 +28,8 @@ struct Geo {
   int dir3;             // 1: Dirichlet on every axis (dirichlet.cu): periodic storage, index-0 nodes held at 0
   int dmask;            // Dirichlet axes kept in that padded periodic storage (bit i = axis i): 7 (3D
                         // all-Dirichlet), 3 (2D Dirichlet), 2 (2D mixed: periodic x, Dirichlet y)
+  int zpad;             // slab mode, Dirichlet z on padded storage: node plane z = 0 (and sine mode 0
+                        // of the pencil) held at 0, planes 1..N3-1 the unknowns (wrap = plane N3 = 0)
 };
 
 // Per-load CG state (device resident; Alg 2 scalars).

@@ -120,6 +120,93 @@ __global__ void __launch_bounds__(fft_threads(L2)) dstz_kernel(Ctx cx, const dou
   }
 }
 
+// ---------------------------------------------------------------------- slab pencils, Dirichlet z
+// In slab mode the z transform runs on the complex pencil [lc][kx][z][yc] (after the x/y FFTs and
+// the all-to-all; the transforms commute, U is the same).  Storage is padded: node plane 0 is the
+// fixed Dirichlet face (always 0) and sine mode m = 1..N3-1 is kept at index m, index 0 = 0.  The
+// DST-I of a complex column is the same odd-extension FFT: (i/2) Y_m gives S(a) + i S(b).
+template <int L2>
+__global__ void __launch_bounds__(fft_threads(L2)) pencil_dst_kernel(Ctx cx, double2* __restrict__ P) {
+  constexpr int T = fft_threads(L2);
+  constexpr int N = L2 / 2;  // = N3
+  const Geo g = cx.g;        // pencil view: N2 := Yc, N3 global
+  const int load = blockIdx.y;
+  if (!cx.st[load].active) return;
+  extern __shared__ double2 smem[];
+  double2* tile = smem;
+  double2* tw = smem + 8 * L2;
+  const int t = threadIdx.x;
+  const int Yc = g.N2, nyc = Yc / 8;
+  const int yq = blockIdx.x % nyc;
+  const long long lk = blockIdx.x / nyc;  // (component, kx) row of this load
+  const long long col0 = ((long long)load * g.c * g.H1 + lk) * N * Yc + yq * 8;
+  for (int i = t; i < L2; i += T) tw[i] = cx.tw.z2[i];
+  for (int e = t; e < 8 * (N - 1); e += T) {
+    const int pz = (e >> 3) + 1, c = e & 7;
+    const double2 v = P[col0 + (long long)pz * Yc + c];
+    tile[tidx(pz, c)] = v;
+    tile[tidx(L2 - pz, c)] = make_double2(-v.x, -v.y);
+  }
+  if (t < 8) {
+    tile[tidx(0, t)] = make_double2(0.0, 0.0);
+    tile[tidx(N, t)] = make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  fft_tile<L2, false>(tile, tw);
+  for (int e = t; e < 8 * N; e += T) {
+    const int m = e >> 3, c = e & 7;
+    const double2 Y = tile[tidx(m, c)];
+    P[col0 + (long long)m * Yc + c] = m == 0 ? make_double2(0.0, 0.0) : make_double2(-0.5 * Y.y, 0.5 * Y.x);
+  }
+}
+
+// s_hat = G_hat r_hat on every bin of the pencil (all c components of a bin together) and the
+// Parseval partial of gamma (weights of the R2C kx planes), grid-stride over the bins.
+constexpr int PG_NBLK = 148 * 4;
+template <int NC>
+__global__ void __launch_bounds__(256) pencil_gmul_kernel(Ctx cx, double2* __restrict__ P) {
+  const Geo g = cx.g;
+  const int load = blockIdx.y;
+  if (!cx.st[load].active) return;
+  __shared__ double red_sh[32];
+  const long long ns = g.nspec, zy = (long long)g.N3 * g.N2;
+  double2* base = P + (long long)load * g.c * ns;
+  double part = 0.0;
+  for (long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x; b < ns; b += (long long)gridDim.x * blockDim.x) {
+    double2 x[NC];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) x[q] = base[q * ns + b];
+    part += gmul_vals<NC>(x, cx.gtab, ns, b, parseval_w((int)(b / zy), g.M));
+#pragma unroll
+    for (int q = 0; q < NC; ++q) base[q * ns + b] = x[q];
+  }
+  partial_write<false>(cx, RED_GAMMA, load, blockIdx.x, part, red_sh);
+}
+
+int pencil_gmul_nblk() { return PG_NBLK; }
+
+template <class F>
+static int dispatch_l2(int L, F&& f);
+
+// z . G . z^-1 of a Dirichlet-z slab pencil (in place): DST-I, symbol multiply + gamma partial, DST-I.
+int launch_pencil_dst_green(const Ctx& cx, double2* pencil, cudaStream_t s) {
+  const Geo& g = cx.g;
+  if (!g.zpad || g.N2 % 8) return -1;
+  const int r = dispatch_l2(2 * g.N3, [&](auto Lc) {
+    constexpr int L2 = decltype(Lc)::value;
+    const dim3 grid((unsigned)((long long)g.c * g.H1 * (g.N2 / 8)), g.nrhs);
+    const int sm = dst_smem_bytes<L2>();
+    if (sm > 48 * 1024) cudaFuncSetAttribute(pencil_dst_kernel<L2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    pencil_dst_kernel<L2><<<grid, fft_threads(L2), sm, s>>>(cx, pencil);
+    const dim3 gg(PG_NBLK, g.nrhs);
+    if (g.c == 1) pencil_gmul_kernel<1><<<gg, 256, 0, s>>>(cx, pencil);
+    else pencil_gmul_kernel<3><<<gg, 256, 0, s>>>(cx, pencil);
+    pencil_dst_kernel<L2><<<grid, fft_threads(L2), sm, s>>>(cx, pencil);
+    return 3;
+  });
+  return r;
+}
+
 template <class F>
 static int dispatch_l2(int L, F&& f) {
   switch (L) {

@@ -1787,6 +1787,7 @@ __global__ void __launch_bounds__(128, 2) kp_thermal3d_rn_kernel(Ctx cx, int mod
       EE = fma(I.Klo[m], I.dzm[m], EE);
       double pv = hc * (fma(5.0 * di, Ksum, EE) - (I.KSlo[m] + KShi));
       if (D3 && (((fixed_xy >> m) & 1u) || k == 0)) pv = 0.0;  // Dirichlet nodes
+      if (HALO && g.zpad && k == 0) pv = 0.0;                    // slab Dirichlet-z face (padded)
       orow[m * N1] = pv;
       part = fma(di, pv, part);
       O.KSlo[m] = KShi;
@@ -2171,19 +2172,23 @@ __global__ void build_symbol_kernel(Ctx cx, double* gtab, double ref0, double re
   double inv_n;
   unsigned long long flat, flatm;
   bool zero;
-  if (g.dirz) {
-    // mixed BC: sine mode m = kz+1 along z, theta_z = pi m / N3; the odd x-z / y-z
-    // couplings leave the diagonal block (S_xz = S_yz = 0); sine modes are self-conjugate.
+  if (g.dirz || g.zpad) {
+    // mixed BC: sine mode m along z (m = kz + 1 on the N3-1 stored sine planes; the
+    // slab pencil's padded layout keeps mode m at index kz = m, index 0 held at 0), theta_z = pi m / N3;
+    // the odd x-z / y-z couplings leave the diagonal block (S_xz = S_yz = 0); sine modes are
+    // self-conjugate, the perturbation is drawn at the sine-plane index p = m - 1.
+    const int m = g.zpad ? kz : kz + 1;
+    const unsigned long long pz = (unsigned long long)(m > 0 ? m - 1 : 0);
     double sz, cz;
-    sincospi((double)(kz + 1) / (double)N3, &sz, &cz);
+    sincospi((double)m / (double)N3, &sz, &cz);
     cs[2] = cz;
     sn[2] = 0.0;
-    const double shz = sinpi((double)(kz + 1) / (2.0 * N3));
+    const double shz = sinpi((double)m / (2.0 * N3));
     omc[2] = 2.0 * shz * shz;
     inv_n = 2.0 / ((double)N1 * N2 * N3);  // F_x F_y unnormalised (N1 N2) x sine sums (N3/2)
-    flat = ((unsigned long long)kz * N2 + ky) * N1 + kx;
-    flatm = ((unsigned long long)kz * N2 + (unsigned long long)((N2 - ky) % N2)) * N1 + (unsigned long long)((N1 - kx) % N1);
-    zero = false;
+    flat = (pz * N2 + ky) * N1 + kx;
+    flatm = (pz * N2 + (unsigned long long)((N2 - ky) % N2)) * N1 + (unsigned long long)((N1 - kx) % N1);
+    zero = m == 0;
   } else {
     axis_trig(kz, N3, cs[2], sn[2], omc[2]);
     inv_n = 1.0 / ((double)N1 * N2 * N3);  // = 1/n (N2: the whole grid, also for a y-chunk pencil)
@@ -2334,9 +2339,11 @@ __global__ void eq55_kernel(Ctx cx, const double* gtab, double* partials) {
   __shared__ double sh[32];
   double mn = 1e300, mx = -1e300;
   const long long ns = g.nspec;
-  const double nn = g.dirz ? (double)g.n : (double)g.N1 * (g.Ny ? g.Ny : g.N2) * g.N3;
+  const double nn = g.dirz ? (double)g.n
+                           : (g.zpad ? 0.5 * g.N1 * (g.Ny ? g.Ny : g.N2) * g.N3 : (double)g.N1 * (g.Ny ? g.Ny : g.N2) * g.N3);
   for (long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x; b < ns; b += (long long)gridDim.x * blockDim.x) {
-    if (b == 0 && !g.dirz && g.ky0 == 0 && !g.dmask) continue;  // periodic: G_hat(0) = 0 shares the null space
+    if (b == 0 && !g.dirz && !g.zpad && g.ky0 == 0 && !g.dmask) continue;  // periodic: G_hat(0) = 0 shares the null space
+    if (g.zpad && ((b / g.N2) & (g.N3 - 1)) == 0) continue;  // slab Dirichlet z: index 0 is not a sine mode
     if (g.dir3 && ((b & (g.N1 - 1)) == 0 || ((b / g.N1) & (g.N2 - 1)) == 0 || b / ((long long)g.N1 * g.N2) == 0))
       continue;  // all-Dirichlet: index-0 entries are not modes
     if (g.dim == 2 && g.dmask == 3 && ((b % g.N1) == 0 || (b / g.N1) == 0)) continue;
@@ -2593,6 +2600,7 @@ static bool gpass_512(const Geo& g) {
 }
 // CTAs of the CG-mode G pass = gamma partials per load
 int gpass_nblk(const Geo& g) {
+  if (g.zpad) return pencil_gmul_nblk();
   if (g.dim == 3 && !g.dirz) return g.H1 * (g.N2 / (gpass_512(g) ? G5_C : (gpass_e256(g) ? GE_COLS : 8)));
   return (int)(((long long)g.H1 * g.P3 + 7) / 8);
 }

@@ -80,6 +80,10 @@ int launch_loop_ctl(cudaGraphConditionalHandle h, const LoadState* st, int nrhs,
 int blocks_needed_max(const Geo& g);
 int launch_scalar(const Ctx& cx, int slot, int mode, cudaStream_t s);  // combine partials + CG scalars  // max CTAs per load of any reducing kernel
 
+// slab pencils with Dirichlet z (padded storage, Geo::zpad): DST-I . G . DST-I in place (dst.cu)
+int launch_pencil_dst_green(const Ctx& cx, double2* pencil, cudaStream_t s);
+int pencil_gmul_nblk();
+
 // elastic K.u in the Walsh-Hadamard modal basis, kp_elastic.cu
 int launch_kp_elastic_modal(const Ctx& cx, int mode, const double* src, double* dst, cudaStream_t s);
 int kp_elastic_modal_nblk(const Geo& g);

@@ -191,7 +191,8 @@ __global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int
       }
       const double* Dc = D + slot_of(k) * KM_PLANE + (ty + 1) * KM_DW + tx + 1;
       const long long gi = (long long)(k - dz - g.zlo) * plane + (long long)(y0 + ty) * N1 + x0 + tx;
-      if (g.dir3 && (x0 + tx == 0 || y0 + ty == 0 || k == 0)) p[0] = p[1] = p[2] = 0.0;  // Dirichlet nodes
+      if ((g.dir3 && (x0 + tx == 0 || y0 + ty == 0 || k == 0)) || (g.zpad && k == 0))
+        p[0] = p[1] = p[2] = 0.0;  // Dirichlet nodes (all-Dirichlet storage / slab Dirichlet-z face)
 #pragma unroll
       for (int al = 0; al < 3; ++al) {
         dst[(long long)load * 3 * n + al * n + gi] = p[al];

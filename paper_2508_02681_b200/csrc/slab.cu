@@ -202,8 +202,9 @@ extern "C" uno_status uno_slab_create(const uno_cg_desc* desc, int32_t rank, int
   *out = nullptr;
   const uno_cg_desc& D = *desc;
   if (D.dim != 3) return sfail(UNO_ERR_UNSUPPORTED, "slab mode: 3D grids only");
-  for (int i = 0; i < 3; ++i)
-    if (D.bc[i] != 0) return sfail(UNO_ERR_UNSUPPORTED, "slab mode: periodic boundaries only");
+  const bool dirz = D.bc[0] == 0 && D.bc[1] == 0 && D.bc[2] == 1;  // mixed BC of config 4 (Eq 82)
+  if (!dirz && (D.bc[0] || D.bc[1] || D.bc[2]))
+    return sfail(UNO_ERR_UNSUPPORTED, "slab mode: periodic, or periodic x, y with Dirichlet z");
   if (nranks < 1 || rank < 0 || rank >= nranks) return sfail(UNO_ERR_ARG, "rank / nranks");
   const int N1 = D.n[0], N2 = D.n[1], N3 = D.n[2];
   const int c = D.physics == UNO_THERMAL ? 1 : 3;
@@ -270,6 +271,11 @@ extern "C" uno_status uno_slab_create(const uno_cg_desc* desc, int32_t rank, int
   gk.zlo = rank * Z;
   gk.halo = 1;
   gk.Ny = N2;
+  if (dirz) {  // padded storage: node plane 0 is the Dirichlet face, held at 0 (K, RHS, pencil mode 0)
+    gk.zpad = 1;
+    gk.dmask = 4;
+    gz.zpad = 1;
+  }
   cudaStream_t s = h->s;
   const long long vec = (long long)D.nrhs * c * gxy.n;
   int maxb = blocks_needed_max(gxy);
@@ -473,7 +479,10 @@ extern "C" uno_status uno_slab_green_peer(uno_slab_handle* h, const double* d_re
   cp.peer_rank = h->rank;
   cp.peer_z = h->Z;
   cp.peer_nlckx = nlckx;
-  if (launch_gpass_peer(cp, h->s) < 0) {
+  if (h->gz.zpad) {
+    SKL(launch_pencil_dst_green(h->cz, h->pencil, h->s));
+    slab_pencil_peer_kernel<<<gb, 256, 0, h->s>>>(P, h->rank, h->pencil, nlckx, h->Z, h->Yc, h->gz.N3);
+  } else if (launch_gpass_peer(cp, h->s) < 0) {
     SKL(launch_gpass(h->cz, CG, h->s));
     slab_pencil_peer_kernel<<<gb, 256, 0, h->s>>>(P, h->rank, h->pencil, nlckx, h->Z, h->Yc, h->gz.N3);
   }
@@ -488,7 +497,10 @@ extern "C" uno_status uno_slab_green(uno_slab_handle* h, const double* d_recv, d
   const dim3 gb(1, (unsigned)std::min<long long>(nlckx, 4096), h->nranks);
   slab_pencil_kernel<<<gb, 256, 0, h->s>>>(const_cast<double2*>(reinterpret_cast<const double2*>(d_recv)), h->pencil,
                                           nlckx, h->Z, h->Yc, h->gz.N3, 0);
-  SKL(launch_gpass(h->cz, CG, h->s));
+  if (h->gz.zpad)
+    SKL(launch_pencil_dst_green(h->cz, h->pencil, h->s));  // Dirichlet z: DST-I . G . DST-I
+  else
+    SKL(launch_gpass(h->cz, CG, h->s));
   slab_pencil_kernel<<<gb, 256, 0, h->s>>>(reinterpret_cast<double2*>(d_send), h->pencil, nlckx, h->Z, h->Yc, h->gz.N3,
                                           1);
   SCK(cudaGetLastError());

@@ -194,10 +194,12 @@ class SlabResult:
 
 class SlabSolver:
     """UNO-CG on a z-slab decomposed grid.  `phase` is the whole [N3][N2][N1] uint8 field on
-    this process's device (every rank keeps all of it: 1 byte per voxel)."""
+    this process's device (every rank keeps all of it: 1 byte per voxel).  bc = (0, 0, 1): Dirichlet
+    faces on z (config 4's mixed variant); vectors then keep N3 node planes with plane 0 (the fixed
+    face, rank 0's first plane) held at 0 — the whole-grid handle's planes 1..N3-1."""
 
     def __init__(self, phase: torch.Tensor, physics: str, mat, comm, nrhs: int = 1, seed: int = 0, amp: float = 0.0,
-                 h: float = 0.0, ref=None, peer: bool = False, graph: bool | None = None):
+                 h: float = 0.0, ref=None, peer: bool = False, graph: bool | None = None, bc=(0, 0, 0)):
         """graph: capture a chunk of iterations as one CUDA graph (default: only for LocalComm,
         whose exchanges are device copies; IpcComm orders stages on the host and cannot be)."""
         assert phase.dim() == 3 and phase.dtype == torch.uint8 and phase.is_cuda
@@ -221,6 +223,9 @@ class SlabSolver:
             else:
                 d.ref[0], d.ref[1] = ref
         d.seed, d.amp, d.nrhs = seed, amp, nrhs
+        self.bc = tuple(int(b) for b in bc)
+        for i, b in enumerate(self.bc):
+            d.bc[i] = b
         d.stream = torch.cuda.current_stream().cuda_stream
         self.desc = d
         self.handles = [B.uno_slab_create(d, r, comm.nranks, self.phase) for r in comm.ranks]
@@ -335,6 +340,8 @@ class SlabSolver:
         us = [torch.empty(self.shape, dtype=torch.float64, device=self.phase.device) for _ in self.handles]
         for h, u in zip(self.handles, us):
             B.uno_slab_finish(h, u)
+        if self.bc[2]:  # Dirichlet faces on z: no null space, the fluctuation is not mean-free
+            return SlabResult(us, reps, bodies)
         # per-component mean over the whole grid: equal slabs -> mean of the slab means
         means = [torch.empty(self.nrhs * self.c, dtype=torch.float64, device=self.phase.device) for _ in self.handles]
         for h, u, m in zip(self.handles, us, means):

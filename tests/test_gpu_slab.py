@@ -22,19 +22,19 @@ def rel(a, b):
     return float(np.linalg.norm((a - b).ravel()) / max(np.linalg.norm(b.ravel()), 1e-300))
 
 
-def whole(ph, physics, mat, nrhs, seed, amp, loads, fixed):
+def whole(ph, physics, mat, nrhs, seed, amp, loads, fixed, bc=(0, 0, 0)):
     from paper_2508_02681_b200.api import UnoCG
 
-    s = UnoCG(torch.from_numpy(ph).to(dev()), physics, mat, nrhs=nrhs, seed=seed, amp=amp)
+    s = UnoCG(torch.from_numpy(ph).to(dev()), physics, mat, nrhs=nrhs, seed=seed, amp=amp, bc=bc)
     r = s.solve(loads, fixed_iters=fixed) if fixed else s.solve(loads)
     return r.u.cpu().numpy(), r.reports
 
 
-def slab(ph, physics, mat, nrhs, seed, amp, loads, fixed, nranks, peer=False):
+def slab(ph, physics, mat, nrhs, seed, amp, loads, fixed, nranks, peer=False, bc=(0, 0, 0)):
     from paper_2508_02681_b200.slab import LocalComm, SlabSolver
 
     sv = SlabSolver(torch.from_numpy(ph).to(dev()), physics, mat, LocalComm(nranks), nrhs=nrhs, seed=seed, amp=amp,
-                    peer=peer)
+                    peer=peer, bc=bc)
     res = sv.solve(loads, fixed_iters=fixed) if fixed else sv.solve(loads)
     sv.close()
     return np.concatenate([u.cpu().numpy() for u in res.u], axis=2), res.reports
@@ -210,3 +210,46 @@ def test_two_process_peer_exchange_on_one_gpu():
     us = np.concatenate([o[1] for o in outs], axis=2)
     assert all(o[2] == [fixed, fixed] for o in outs)
     assert rel(us, uw) <= 1e-11
+
+
+# ----------------------------------------------------------------------------- Dirichlet z (mixed BC)
+@pytest.mark.parametrize("nranks,peer", [(1, False), (2, False), (2, True), (4, False), (4, True)])
+def test_mixed_thermal_slab_equals_whole_grid(nranks, peer):
+    # config 4's mixed variant (Eq 82, Dirichlet faces on z) decomposed in z: padded slabs (plane 0
+    # = the fixed face), DST-I along z in the pencil stage; equals the whole-grid mixed solver
+    P = synth.config1()
+    loads = np.eye(3)[:2]
+    bc = (0, 0, 1)
+    uw, _ = whole(P.phase, "thermal", P.mat, 2, P.seed, P.amp, loads, 6, bc)
+    us, reps = slab(P.phase, "thermal", P.mat, 2, P.seed, P.amp, loads, 6, nranks, peer, bc)
+    assert [r["iterations"] for r in reps] == [6, 6]
+    assert np.all(us[:, :, 0] == 0.0)
+    assert rel(us[:, :, 1:], uw) <= 1e-11
+    uw, rw = whole(P.phase, "thermal", P.mat, 2, P.seed, P.amp, loads, 0, bc)
+    us, rs = slab(P.phase, "thermal", P.mat, 2, P.seed, P.amp, loads, 0, nranks, peer, bc)
+    for a, b in zip(rw, rs):
+        assert abs(a["iterations"] - b["iterations"]) <= 1 and b["converged"]
+    assert rel(us[:, :, 1:], uw) <= 1e-7
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_mixed_elastic_slab_equals_whole_grid(nranks):
+    ph = np.ascontiguousarray(synth.spheres_rsa(32, 0.25, 3.0, 5.0, seed=2))
+    mat = (synth.lame_from_E_nu(1.0, 0.3), synth.lame_from_E_nu(20.0, 0.2))
+    loads = np.eye(6)[[0, 5]]
+    bc = (0, 0, 1)
+    uw, _ = whole(ph, "elastic", mat, 2, 1004, 0.05, loads, 5, bc)
+    us, reps = slab(ph, "elastic", mat, 2, 1004, 0.05, loads, 5, nranks, True, bc)
+    assert [r["iterations"] for r in reps] == [5, 5]
+    assert np.all(us[:, :, 0] == 0.0)
+    assert rel(us[:, :, 1:], uw) <= 1e-11
+
+
+def test_mixed_slab_against_oracle():
+    ph = np.ascontiguousarray(synth.spheres_rsa(32, 0.3, 3.0, 5.0, seed=1))
+    mat = (1.0, 30.0)
+    g = fem.Grid((32, 32, 32), bc=(0, 0, 1), h=1 / 32)
+    load = np.eye(3)[1:2]
+    ref = homog.solve_problem(g, "thermal", ph, mat, load, 77, 0.1, fixed_iters=7)
+    us, _ = slab(ph, "thermal", mat, 1, 77, 0.1, load, 7, 2, True, (0, 0, 1))
+    assert rel(us[0][:, 1:], ref["U"][0]) <= 1e-9
