@@ -2850,6 +2850,7 @@ int launch_zero(double* x, long long n, cudaStream_t s) {
 
 int blocks_needed_max(const Geo& g) {
   long long m = (long long)g.c * g.N3 * g.N2 / 8;                // x passes
+  if (g.zpad) m = m > pencil_gmul_nblk() ? m : pencil_gmul_nblk();  // slab Dirichlet-z pencil gamma partials
   if (g.dim == 3) m = m > (long long)g.H1 * (g.N2 / 4) ? m : (long long)g.H1 * (g.N2 / 4);  // G pass
   else m = m > (g.H1 + 7) / 8 ? m : (g.H1 + 7) / 8;
   if (g.dirz) {  // DST pass grid
