@@ -322,9 +322,10 @@ def ghat_mixed(g: fem.Grid, physics: str, mat, seed: int, amp: float, ref=None) 
 
 
 def apply_precond_mixed(G: np.ndarray, r: np.ndarray) -> np.ndarray:
-    """s = U^H Q U r with U = F_x (x) F_y (x) DST-I_z (Eq 48 with the mixed transform)."""
+    """s = U^H Q U r with U = F_x (x) F_y (x) DST-I_z (Eq 48 with the mixed transform).
+    G: full (kx over N1) or R2C half (kx <= N1/2) symbol."""
     rh = transform.forward_mixed(r)
-    Gh = half(G)
+    Gh = _half_for(G, r.shape[-1])
     sh = np.einsum("ab...,b...->a...", Gh, rh)
     return transform.inverse_mixed(sh, r.shape[1:])
 

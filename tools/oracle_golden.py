@@ -45,8 +45,10 @@ def _solve_load(g, physics, phase, mat, load, G, fixed_iters, threads, tol=1e-8)
     from oracle import fem, greens, homog, pcg
 
     f = fem.rhs(g, physics, phase, mat, load)
+    # U per boundary condition (Table 1): DFT on every axis, or DFT_x DFT_y DST-I_z (mixed)
+    applyP = greens.apply_precond_mixed if g.bc == (0, 0, 1) else greens.apply_precond
     res = pcg.pcg(lambda v: fem.apply_K_chunked(g, physics, phase, mat, v, zchunk=16, workers=threads),
-                  lambda v: greens.apply_precond(G, v), f, tol=tol, max_iter=2000, fixed_iters=fixed_iters,
+                  lambda v: applyP(G, v), f, tol=tol, max_iter=2000, fixed_iters=fixed_iters,
                   zero_floor=homog.zero_rhs_floor(g, physics, mat, load))
     u = pcg.remove_mean(res.u) if all(b == 0 for b in g.bc) else res.u
     return f, u, res
