@@ -267,7 +267,7 @@ def run_ours(args):
     roof = None
     if dom:
         traffic = None
-        tf = os.path.join(ROOT, "profiles", "traffic_r01.json")
+        tf = os.path.join(ROOT, "profiles", "traffic_r02.json")
         if os.path.exists(tf):
             traffic = json.load(open(tf)).get(dom)
         roof = {"bound": "hbm", "kernel": dom, "achieved": round(per[dom]["GBps"], 1), "peak": peak, "unit": "GB/s",

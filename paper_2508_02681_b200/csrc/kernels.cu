@@ -859,8 +859,11 @@ __global__ void __launch_bounds__(fft_threads(L), L == 256 ? UNO_GMINB : 1) gpas
 // partial of gamma (Eq 46/49) are formed; the inverse mirrors the forward.  Column stride 273
 // (odd in 16-byte units) keeps every quarter-warp access bank-conflict free.
 constexpr int GR_CS = YR_R * (YR_R + 1) + 1;
+#ifndef UNO_G256_MINB
+#define UNO_G256_MINB 3  // resident CTAs per SM of the thermal 256-point G pass (A/B builds only)
+#endif
 template <int MODE>
-__global__ void __launch_bounds__(8 * YR_R, 3) gpass256_kernel(Ctx cx) {  // smem: gpass256_smem
+__global__ void __launch_bounds__(8 * YR_R, UNO_G256_MINB) gpass256_kernel(Ctx cx) {  // smem: gpass256_smem
   constexpr int L = 256, R = YR_R, RP = R + 1;
   const Geo g = cx.g;
   // load fastest in the launch order: the nrhs CTAs of one tile read the same symbol rows back to

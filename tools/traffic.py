@@ -10,9 +10,9 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 from ncu_summary import load  # noqa: E402
 
 CLASSES = [("kp_thermal3d", "K"), ("kp_elastic3d", "K"), ("xfwd_kernel", "xfwd"), ("xfwd256", "xfwd"),
-           ("ypass_kernel", "ypass"), ("ypass256", "ypass"), ("gpass_z_kernel", "gpass"), ("gpass256", "gpass"),
-           ("gpass_y2d", "gpass"), ("xinv_kernel", "xinv"), ("scalar_kernel", "scalar"),
-           ("dstz_kernel", "dstz"), ("f1_kernel", "f1"), ("f2_kernel", "f2"), ("f3_kernel", "f3")]
+           ("xfwd512", "xfwd"), ("ypass_kernel", "ypass"), ("ypass256", "ypass"), ("ypass512", "ypass"),
+           ("gpass_z_kernel", "gpass"), ("gpass256", "gpass"), ("gpass512", "gpass"), ("gpass_y2d", "gpass"),
+           ("xinv_kernel", "xinv"), ("xinv512", "xinv"), ("scalar_kernel", "scalar"), ("dstz_kernel", "dstz")]
 
 
 def main(rep, out):
