@@ -531,12 +531,12 @@ __global__ void __launch_bounds__(fft_threads(L), L == 256 ? UNO_YMINB : 1) ypas
   double2* tile = smem;
   double2* tw = smem + 8 * L;
   const int t = threadIdx.x;
-  const long long nrows = (long long)g.c * g.H1 * g.N3;
+  const long long nrows = (long long)g.c * g.H1 * g.P3;
   long long row0 = (long long)blockIdx.x * 8;  // row = (comp, kx, z)
   if (zc > 0) {  // z-chunk [z0, z0+zc) of every (comp, kx) plane (zc, z0 multiples of 8)
     const int nb = zc >> 3;
     const int q = blockIdx.x / nb;
-    row0 = (long long)q * g.N3 + z0 + (blockIdx.x - q * nb) * 8;
+    row0 = (long long)q * g.P3 + z0 + (blockIdx.x - q * nb) * 8;
   }
   double2* base = cx.spec + (long long)load * g.c * g.nspec + row0 * L;
   const bool full = row0 + 8 <= nrows;
@@ -582,12 +582,12 @@ __global__ void __launch_bounds__(YR_ROWS * YR_R) ypass256_kernel(Ctx cx, int z0
   __shared__ double2 tw[L];
   const int t = threadIdx.x;
   const int r = t >> 4, lane16 = t & 15;
-  const long long nrows = (long long)g.c * g.H1 * g.N3;
+  const long long nrows = (long long)g.c * g.H1 * g.P3;
   long long row0 = (long long)blockIdx.x * YR_ROWS;  // row = (comp, kx, z)
   if (zc > 0) {
     const int nb = zc >> 3;
     const int q = blockIdx.x / nb;
-    row0 = (long long)q * g.N3 + z0 + (blockIdx.x - q * nb) * 8;
+    row0 = (long long)q * g.P3 + z0 + (blockIdx.x - q * nb) * 8;
   }
   const bool ok = row0 + r < nrows;
   double2* rowp = cx.spec + (long long)load * g.c * g.nspec + (row0 + r) * L;
@@ -654,12 +654,12 @@ __global__ void __launch_bounds__(128) ypass512_kernel(Ctx cx, int z0, int zc) {
   __shared__ double2 tw32[16];     // w_32^r
   const int t = threadIdx.x;
   const int r = t >> 5, l32 = t & 31;
-  const long long nrows = (long long)g.c * g.H1 * g.N3;
+  const long long nrows = (long long)g.c * g.H1 * g.P3;
   long long row0 = (long long)blockIdx.x * Y5_ROWS;
   if (zc > 0) {
     const int nb = zc / Y5_ROWS;
     const int q = blockIdx.x / nb;
-    row0 = (long long)q * g.N3 + z0 + (blockIdx.x - q * nb) * Y5_ROWS;
+    row0 = (long long)q * g.P3 + z0 + (blockIdx.x - q * nb) * Y5_ROWS;
   }
   const bool ok = row0 + r < nrows;
   double2* rowp = cx.spec + (long long)load * g.c * g.nspec + (row0 + r) * L;
@@ -707,7 +707,7 @@ __global__ void __launch_bounds__(128) ypass512_kernel(Ctx cx, int z0, int zc) {
 
 int launch_ypass_peer(const Ctx& cx, cudaStream_t s) {
   const Geo& g = cx.g;
-  const long long nrows = (long long)g.c * g.H1 * g.N3;
+  const long long nrows = (long long)g.c * g.H1 * g.P3;
   if (g.N2 == 256) {
     const dim3 grid((unsigned)((nrows + YR_ROWS - 1) / YR_ROWS), g.nrhs);
     ypass256_kernel<false, CG, true><<<grid, YR_ROWS * YR_R, 0, s>>>(cx, 0, 0);
@@ -2414,7 +2414,7 @@ int launch_scalar(const Ctx& cx, int slot, int mode, cudaStream_t s) {
   const Geo& g = cx.g;
   int nblk;
   if (slot == RED_RNORM) {
-    nblk = g.dirz ? g.c * g.N2 * (g.N1 / 16) : g.c * g.P3 * g.N2 / 8;
+    nblk = g.c * g.P3 * g.N2 / 8;
   } else if (slot == RED_GAMMA) {
     nblk = gpass_nblk(g);
   } else {
@@ -2554,7 +2554,7 @@ int launch_ypass(const Ctx& cx, int mode, bool inverse, cudaStream_t s, int z0, 
   const Geo& g = cx.g;
   if (zc > 0 && ((zc | z0) & 7)) return -1;
   if (g.N2 == 512 && !(zc > 0 && (zc % Y5_ROWS))) {
-    const long long nrows = zc > 0 ? (long long)g.c * g.H1 * zc : (long long)g.c * g.H1 * g.N3;
+    const long long nrows = zc > 0 ? (long long)g.c * g.H1 * zc : (long long)g.c * g.H1 * g.P3;
     const dim3 grid((unsigned)((nrows + Y5_ROWS - 1) / Y5_ROWS), g.nrhs);
     if (mode == CG) {
       if (inverse) ypass512_kernel<true, CG><<<grid, 128, 0, s>>>(cx, z0, zc);
@@ -2566,7 +2566,7 @@ int launch_ypass(const Ctx& cx, int mode, bool inverse, cudaStream_t s, int z0, 
     return 1;
   }
   if (g.N2 == 256) {
-    const long long nrows = zc > 0 ? (long long)g.c * g.H1 * zc : (long long)g.c * g.H1 * g.N3;
+    const long long nrows = zc > 0 ? (long long)g.c * g.H1 * zc : (long long)g.c * g.H1 * g.P3;
     const dim3 grid((unsigned)((nrows + YR_ROWS - 1) / YR_ROWS), g.nrhs);
     if (mode == CG) {
       if (inverse) ypass256_kernel<true, CG><<<grid, YR_ROWS * YR_R, 0, s>>>(cx, z0, zc);
@@ -2579,7 +2579,7 @@ int launch_ypass(const Ctx& cx, int mode, bool inverse, cudaStream_t s, int z0, 
   }
   return dispatch_pow2(g.N2, [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
-    const long long nrows = zc > 0 ? (long long)g.c * g.H1 * zc : (long long)g.c * g.H1 * g.N3;
+    const long long nrows = zc > 0 ? (long long)g.c * g.H1 * zc : (long long)g.c * g.H1 * g.P3;
     const dim3 grid((unsigned)((nrows + 7) / 8), g.nrhs);
     const int sm = ysmem_bytes<L>();
     auto pick = [&](auto k) {
@@ -2603,7 +2603,7 @@ static bool gpass_512(const Geo& g) {
 }
 // CTAs of the CG-mode G pass = gamma partials per load
 int gpass_nblk(const Geo& g) {
-  if (g.zpad) return pencil_gmul_nblk();
+  if (g.zpad || (g.dirz && g.dim == 3)) return pencil_gmul_nblk();  // Dirichlet z: spectrum DST stage
   if (g.dim == 3 && !g.dirz) return g.H1 * (g.N2 / (gpass_512(g) ? G5_C : (gpass_e256(g) ? GE_COLS : 8)));
   return (int)(((long long)g.H1 * g.P3 + 7) / 8);
 }
@@ -2853,7 +2853,7 @@ int launch_zero(double* x, long long n, cudaStream_t s) {
 
 int blocks_needed_max(const Geo& g) {
   long long m = (long long)g.c * g.N3 * g.N2 / 8;                // x passes
-  if (g.zpad) m = m > pencil_gmul_nblk() ? m : pencil_gmul_nblk();  // slab Dirichlet-z pencil gamma partials
+  if (g.zpad || g.dirz) m = m > pencil_gmul_nblk() ? m : pencil_gmul_nblk();  // Dirichlet-z gamma partials
   if (g.dim == 3) m = m > (long long)g.H1 * (g.N2 / 4) ? m : (long long)g.H1 * (g.N2 / 4);  // G pass
   else m = m > (g.H1 + 7) / 8 ? m : (g.H1 + 7) / 8;
   if (g.dirz) {  // DST pass grid

@@ -80,9 +80,14 @@ int launch_loop_ctl(cudaGraphConditionalHandle h, const LoadState* st, int nrhs,
 int blocks_needed_max(const Geo& g);
 int launch_scalar(const Ctx& cx, int slot, int mode, cudaStream_t s);  // combine partials + CG scalars  // max CTAs per load of any reducing kernel
 
-// slab pencils with Dirichlet z (padded storage, Geo::zpad): DST-I . G . DST-I in place (dst.cu)
-int launch_pencil_dst_green(const Ctx& cx, double2* pencil, cudaStream_t s);
+// Dirichlet z (whole-grid mixed BC, or slab pencils on padded storage Geo::zpad): DST-I . G . DST-I
+// on the spectrum in place, 3 launches (dst.cu)
+int launch_pencil_dst_green(const Ctx& cx, double2* spec, int mode, cudaStream_t s);
 int pencil_gmul_nblk();
+
+// whole Alg 2 in one CTA per load for small 2D periodic thermal grids (tiny.cu)
+bool tiny_supported(const Geo& g);
+int launch_tiny_pcg(const Ctx& cx, cudaStream_t s);
 
 // elastic K.u in the Walsh-Hadamard modal basis, kp_elastic.cu
 int launch_kp_elastic_modal(const Ctx& cx, int mode, const double* src, double* dst, cudaStream_t s);
@@ -111,6 +116,5 @@ int train_install_run(const Ctx& cx, const std::vector<int>& pbin, const std::ve
                       const double* th0_host, const double* d_ths, double* gtab, cudaStream_t s);
 
 // mixed BC (Dirichlet on z), dst.cu
-int launch_dstz(const Ctx& cx, int mode, bool inverse, const double* src, double* dst, cudaStream_t s);
 
 }  // namespace uno

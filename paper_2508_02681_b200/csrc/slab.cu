@@ -480,7 +480,7 @@ extern "C" uno_status uno_slab_green_peer(uno_slab_handle* h, const double* d_re
   cp.peer_z = h->Z;
   cp.peer_nlckx = nlckx;
   if (h->gz.zpad) {
-    SKL(launch_pencil_dst_green(h->cz, h->pencil, h->s));
+    SKL(launch_pencil_dst_green(h->cz, h->pencil, CG, h->s));
     slab_pencil_peer_kernel<<<gb, 256, 0, h->s>>>(P, h->rank, h->pencil, nlckx, h->Z, h->Yc, h->gz.N3);
   } else if (launch_gpass_peer(cp, h->s) < 0) {
     SKL(launch_gpass(h->cz, CG, h->s));
@@ -498,7 +498,7 @@ extern "C" uno_status uno_slab_green(uno_slab_handle* h, const double* d_recv, d
   slab_pencil_kernel<<<gb, 256, 0, h->s>>>(const_cast<double2*>(reinterpret_cast<const double2*>(d_recv)), h->pencil,
                                           nlckx, h->Z, h->Yc, h->gz.N3, 0);
   if (h->gz.zpad)
-    SKL(launch_pencil_dst_green(h->cz, h->pencil, h->s));  // Dirichlet z: DST-I . G . DST-I
+    SKL(launch_pencil_dst_green(h->cz, h->pencil, CG, h->s));  // Dirichlet z: DST-I . G . DST-I
   else
     SKL(launch_gpass(h->cz, CG, h->s));
   slab_pencil_kernel<<<gb, 256, 0, h->s>>>(reinterpret_cast<double2*>(d_send), h->pencil, nlckx, h->Z, h->Yc, h->gz.N3,

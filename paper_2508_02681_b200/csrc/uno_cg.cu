@@ -55,7 +55,7 @@ struct uno_cg_handle {
   double* kel;
   double2 *twx, *twxp, *twy, *twz, *twz2;
   double2 *twx2, *twy2;    // all-Dirichlet: length-2N1 / 2N2 tables of the odd-extension FFTs
-  double* rt;             // mixed BC: z-sine-space intermediate vector [nrhs][c][n]
+  double* rt;             // all-Dirichlet / 2D mixed: intermediate vector [nrhs][c][n]
   char* arena;            // device workspace (uno_cg_workspace_size bytes), see ws_layout
   bool own_arena;         // allocated by the library (else borrowed from the caller)
   LoadState* st;
@@ -325,7 +325,7 @@ static size_t ws_layout(const Geo& g, size_t off[WS_N]) {
   const size_t sz[WS_N] = {
       vec, vec, vec, vec, (size_t)g.nrhs * g.c * g.nspec * 16, (size_t)g.C * g.nspec * 8, 2 * 576 * 8,
       (size_t)g.M * 16, (size_t)(g.M + 1) * 16, (size_t)g.N2 * 16, (size_t)g.N3 * 16, (size_t)2 * g.N3 * 16,
-      (g.dirz || g.dmask) ? vec : 8, g.dmask ? (size_t)2 * g.N1 * 16 : 16, g.dmask ? (size_t)2 * g.N2 * 16 : 16,
+      g.dmask ? vec : 8, g.dmask ? (size_t)2 * g.N1 * 16 : 16, g.dmask ? (size_t)2 * g.N2 * 16 : 16,
       kMaxRhs * sizeof(LoadState), (size_t)RED_NSLOT * kMaxRhs * blocks_needed_max(g) * 8,
       RED_NSLOT * kMaxRhs * sizeof(unsigned), RED_NSLOT * kMaxRhs * 8, scratch_doubles(g) * 8, 64};
   size_t t = 0;
@@ -618,17 +618,13 @@ extern "C" uno_status uno_cg_apply_precond(uno_cg_handle* h, const double* d_r, 
     KL(launch_d3_precond(h->cx, d_r, d_z, tw2, s), KC_G);
     KL(launch_d3_dot(h->cx, d_r, d_z, STANDALONE, s), KC_OTHER);
     KL(launch_scalar_n(h->cx, RED_GAMMA, STANDALONE, jacobi_nblk(h->g), s), KC_OTHER);
-  } else if (h->g.dirz) {  // mixed BC: DST-I along z first, then the periodic x/y machinery
-    KL(launch_dstz(h->cx, STANDALONE, false, d_r, h->rt, s), KC_XF);
-    KL(launch_xfwd(h->cx, STANDALONE, h->rt, s), KC_XF);
-    KL(launch_gpass(h->cx, STANDALONE, s), KC_G);
-    KL(launch_xinv(h->cx, STANDALONE, h->rt, s), KC_XI);
-    KL(launch_dstz(h->cx, STANDALONE, true, h->rt, d_z, s), KC_XI);
-    KL(launch_scalar(h->cx, RED_GAMMA, STANDALONE, s), KC_OTHER);
-  } else {
+  } else {  // periodic, or mixed BC (Dirichlet z: the z DST-I . G . DST-I stage on the spectrum)
     KL(launch_xfwd(h->cx, STANDALONE, d_r, s), KC_XF);
     if (h->g.dim == 3) KL(launch_ypass(h->cx, STANDALONE, false, s), KC_Y);
-    KL(launch_gpass(h->cx, STANDALONE, s), KC_G);
+    if (h->g.dirz)
+      KL(launch_pencil_dst_green(h->cx, h->spec, STANDALONE, s), KC_G);
+    else
+      KL(launch_gpass(h->cx, STANDALONE, s), KC_G);
     if (h->g.dim == 3) KL(launch_ypass(h->cx, STANDALONE, true, s), KC_Y);
     KL(launch_xinv(h->cx, STANDALONE, d_z, s), KC_XI);
     KL(launch_scalar(h->cx, RED_GAMMA, STANDALONE, s), KC_OTHER);
@@ -672,20 +668,13 @@ static int enqueue_iteration(uno_cg_handle* h, cudaStream_t s, cudaEvent_t* ev /
     n += launch_d3_dot(cx, cx.r, h->rt, CG, s);
     n += launch_scalar_n(cx, RED_GAMMA, CG, nb, s);
     if (!run(4, [&] { return launch_jac_d_ext(cx, h->rt, s); })) return -1;
-  } else if (h->g.dirz) {  // mixed BC (dst.cu): DST_z (+CG r update) | x | y.G.y^-1 | x^-1 | DST_z^-1 (+d, u)
-    if (!run(0, [&] { return launch_dstz(cx, CG, false, cx.r, h->rt, s); })) return -1;
-    n += launch_scalar(cx, RED_RNORM, CG, s);
-    if (!run(1, [&] { return launch_xfwd(cx, PLAIN, h->rt, s); })) return -1;
-    if (!run(2, [&] { return launch_gpass(cx, CG, s); })) return -1;
-    n += launch_scalar(cx, RED_GAMMA, CG, s);
-    if (!run(3, [&] { return launch_xinv(cx, PLAIN, h->rt, s); })) return -1;
-    if (!run(4, [&] { return launch_dstz(cx, CG, true, h->rt, nullptr, s); })) return -1;
-  } else {
+  } else {  // 5-pass: x | y | z.G.z^-1 (mixed BC: DST_z . G . DST_z on the spectrum) | y^-1 | x^-1, K
     const bool d3 = h->g.dim == 3;
     if (!run(0, [&] { return launch_xfwd(cx, CG, cx.r, s); })) return -1;
     n += launch_scalar(cx, RED_RNORM, CG, s);
     if (d3 && !run(1, [&] { return launch_ypass(cx, CG, false, s); })) return -1;
-    if (!run(2, [&] { return launch_gpass(cx, CG, s); })) return -1;
+    if (!run(2, [&] { return h->g.dirz ? launch_pencil_dst_green(cx, cx.spec, CG, s) : launch_gpass(cx, CG, s); }))
+      return -1;
     n += launch_scalar(cx, RED_GAMMA, CG, s);
     if (d3 && !run(3, [&] { return launch_ypass(cx, CG, true, s); })) return -1;
     if (!run(4, [&] { return launch_xinv(cx, CG, nullptr, s); })) return -1;
@@ -810,8 +799,11 @@ extern "C" uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, doub
   CK(cudaMemcpyAsync(h->st, h->h_st, g.nrhs * sizeof(LoadState), cudaMemcpyHostToDevice, s));
   const long long work = (long long)g.nrhs * g.c * g.n;
   // passes + 3 scalar kernels (mixed: 6 too)
-  const int per_iter = h->precond != 0 ? 6 : g.dmask ? 15 : (g.dim == 3 ? 6 : 4) + 3;
-  if (!h->timing) {
+  const int per_iter = h->precond != 0 ? 6 : g.dmask ? 15 : (g.dim == 3 ? (g.dirz ? 8 : 6) : 4) + 3;
+  if (!h->timing && h->precond == 0 && tiny_supported(g)) {
+    // small 2D grid (config 0): the whole of Alg 2 in one persistent CTA per load (tiny.cu)
+    KL(launch_tiny_pcg(h->cx, s), KC_OTHER);
+  } else if (!h->timing) {
     // whole solve device-side: WHILE node over bodies of `chunk` iterations
     const int chunk = work >= (1LL << 22) ? 2 : 4;
     const int cap_body = (cap + 1 + chunk - 1) / chunk + 1;

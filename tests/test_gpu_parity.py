@@ -810,3 +810,29 @@ def test_api_rejects_wrong_shapes():
         s.apply_precond(torch.zeros((2,) + s.field_shape[1:], dtype=torch.float64, device=dev()))
     with pytest.raises(ValueError):
         s.solve(P.loads, out=torch.zeros(s.field_shape, dtype=torch.float64))  # host tensor
+
+
+@pytest.mark.parametrize("N", [(32, 32), (64, 32), (16, 8)])
+def test_tiny_one_cta_solve_equals_graph_loop(N):
+    # small 2D thermal grids run the whole Alg 2 in one CTA per load (tiny.cu);
+    # the kernel-timing mode keeps the multi-kernel loop: same iterations, reports, coefficients,
+    # solutions to round-off; and both against the oracle at the common count
+    g, ph, mat, amp, seed = make_case(N, "thermal")
+    s = solver(ph, "thermal", mat, 2, seed, amp)
+    loads = np.eye(2)
+    a = s.solve(loads, hist=True)
+    ga = [s.coefficients(l) for l in range(2)]
+    assert a.launches < 20  # rhs, zero, tiny, finalize, means
+    s.kernel_timing(enable=1, reset=1)
+    b = s.solve(loads, hist=True)
+    s.kernel_timing(enable=0)
+    assert [r["iterations"] for r in a.reports] == [r["iterations"] for r in b.reports]
+    assert all(r["converged"] for r in a.reports)
+    assert rel(a.u.cpu().numpy(), b.u.cpu().numpy()) <= 1e-12
+    for l in range(2):
+        m = a.reports[l]["iterations"]
+        assert np.allclose(a.hist[l, :m + 1], b.hist[l, :m + 1], rtol=1e-9, atol=0)
+        gb = s.coefficients(l)
+        assert np.allclose(ga[l][0], gb[0], rtol=1e-10) and np.allclose(ga[l][1], gb[1], rtol=1e-10)
+    ref = homog.solve_problem(g, "thermal", ph, mat, loads[:1], seed, amp, tol=1e-8)
+    assert abs(a.reports[0]["iterations"] - ref["iterations"][0]) <= 1
