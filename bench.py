@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--weak", action="store_true", help="every rank solves its own 48-problem batch (weak scaling)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--problems", type=int, default=0,
+                    help="profiling only: the first P problems of this rank's shard (0 = all; not a bench value)")
     return ap.parse_args()
 
 
@@ -172,6 +174,8 @@ def run_ours(args):
     n = args.grid
     t0 = time.time()
     probs = problem_list(ws, rank, args.weak)
+    if args.problems > 0:
+        probs = probs[:args.problems]
     seed_base = 300 + 8 * rank if args.weak else 300
     micro = make_microstructures({m for m, _ in probs}, n, seed_base)
     phases = {m: torch.from_numpy(v).to(dev) for m, v in micro.items()}
