@@ -267,14 +267,23 @@ struct FftStagesNTUntil {
 
 // op(int tile, int col, int kbin, double2* x /*NC values of that bin*/) -> Parseval term;
 // modifies x in place.  Returns the thread's sum of op results.  Caller syncs before.
-template <int L, int NT, int NC, class Op>
-__device__ __forceinline__ double fft_gconv(double2* const* tiles, const double2* __restrict__ tw, Op op) {
+struct GconvNoHook {
+  __device__ __forceinline__ void operator()(int) const {}
+};
+// pre(q): called before component q's forward stages (e.g. wait for its copy group + barrier);
+// post(q): after its inverse stages (the tile is complete: e.g. store it while the next one runs).
+template <int L, int NT, int NC, class Op, class Pre = GconvNoHook, class Post = GconvNoHook>
+__device__ __forceinline__ double fft_gconv(double2* const* tiles, const double2* __restrict__ tw, Op op,
+                                            Pre pre = Pre(), Post post = Post()) {
   constexpr int S = plan_stages(L);
   constexpr int RL = plan_radix(L, S - 1);
   constexpr int NJ = L / RL;
   static_assert(gconv_fusable(L), "first and last radix must agree");
 #pragma unroll
-  for (int q = 0; q < NC; ++q) FftStagesNTUntil<L, NT, 1, NJ, false>::run(tiles[q], tw);
+  for (int q = 0; q < NC; ++q) {
+    pre(q);
+    FftStagesNTUntil<L, NT, 1, NJ, false>::run(tiles[q], tw);
+  }
   constexpr int ITEMS = NJ * kTile * NT;
   const int t = threadIdx.x;
   const bool act = t < ITEMS;
@@ -315,7 +324,10 @@ __device__ __forceinline__ double fft_gconv(double2* const* tiles, const double2
   }
   __syncthreads();
 #pragma unroll
-  for (int q = 0; q < NC; ++q) FftStagesNT<L, NT, plan_radix(L, 0), true>::run(tiles[q], tw);
+  for (int q = 0; q < NC; ++q) {
+    FftStagesNT<L, NT, plan_radix(L, 0), true>::run(tiles[q], tw);
+    post(q);
+  }
   return part;
 }
 

@@ -755,6 +755,11 @@ __global__ void __launch_bounds__(fft_threads(L), L == 256 ? UNO_GMINB : 1) gpas
   const int kx = blockIdx.x / ntile_y;
   const int y0 = (blockIdx.x - kx * ntile_y) * 8;
   const long long boff = (long long)kx * g.N3 * g.N2 + y0;
+  constexpr bool STG = gstaged<L, NC>() && MODE != FWDZ;
+  // unstaged symbol (L = 512, c = 3: one CTA per SM): one copy group per component, so the forward
+  // stages of component 0 run while 1 and 2 land, and each component is stored as soon as its
+  // inverse is done (load / compute / store overlap inside the CTA)
+  constexpr bool PIPE = !STG && NC == 3 && MODE != FWDZ && gconv_fusable(L) && NC * plan_radix(L, plan_stages(L) - 1) <= 32;
 #pragma unroll
   for (int q = 0; q < NC; ++q) {
     const double2* base = cx.spec + ((long long)load * g.c + q) * g.nspec + boff;
@@ -763,8 +768,8 @@ __global__ void __launch_bounds__(fft_threads(L), L == 256 ? UNO_GMINB : 1) gpas
       const int e = t + i * T;
       if (e < 8 * L) cp_async16(&tiles[q][tidx(e >> 3, e & 7)], base + (long long)(e >> 3) * g.N2 + (e & 7));
     }
+    if (PIPE) cp_commit();
   }
-  constexpr bool STG = gstaged<L, NC>() && MODE != FWDZ;
   if constexpr (!STG && MODE != FWDZ) {
     // symbol too large to stage with the tile (L = 512, c = 3): pull its rows (8 bins, 64 bytes
     // each) into L2 now so the reads inside the fused butterfly hit L2 rather than DRAM
@@ -783,10 +788,12 @@ __global__ void __launch_bounds__(fft_threads(L), L == 256 ? UNO_GMINB : 1) gpas
       }
     }
   }
-  cp_commit();
+  if (!PIPE) cp_commit();
   for (int i = t; i < L; i += T) tw[i] = cx.tw.z[i];
-  cp_wait<0>();
-  __syncthreads();
+  if (!PIPE) {
+    cp_wait<0>();
+    __syncthreads();
+  }
   if constexpr (MODE == FWDZ) {  // forward z transform only (training features, train.cu)
 #pragma unroll
     for (int q = 0; q < NC; ++q) fft_tile<L, false>(tiles[q], tw);
@@ -801,33 +808,7 @@ __global__ void __launch_bounds__(fft_threads(L), L == 256 ? UNO_GMINB : 1) gpas
     }
     return;
   }
-  const double w = parseval_w(kx, g.M);
-  double part = 0.0;
-  if constexpr (gconv_fusable(L) && NC * plan_radix(L, plan_stages(L) - 1) <= 32) {
-    // symbol multiply fused into the middle butterfly (fft.cuh fft_gconv)
-    part = fft_gconv<L, 1, NC>(tiles, tw, [&](int, int c, int kz, double2* x) {
-      return STG ? gmul_vals<NC>(x, gs, 8 * L, (long long)kz * 8 + c, w)
-                 : gmul_vals<NC>(x, cx.gtab, g.nspec, boff + (long long)kz * g.N2 + c, w);
-    });
-  } else {
-#pragma unroll
-    for (int q = 0; q < NC; ++q) fft_tile<L, false>(tiles[q], tw);
-#pragma unroll
-    for (int i = 0; i < (8 * L + T - 1) / T; ++i) {
-      const int e = t + i * T;
-      if (e < 8 * L) {
-        if (STG)
-          part += gmul_bin<NC>(tiles, tidx(e >> 3, e & 7), gs, 8 * L, e, w);
-        else
-          part += gmul_bin<NC>(tiles, tidx(e >> 3, e & 7), cx.gtab, g.nspec, boff + (long long)(e >> 3) * g.N2 + (e & 7), w);
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < NC; ++q) fft_tile<L, true>(tiles[q], tw);
-  }
-#pragma unroll
-  for (int q = 0; q < NC; ++q) {
+  auto store_comp = [&](int q) {
     if constexpr (PEER) {  // slab: z plane zz belongs to rank zz / peer_z -> its receive buffer
       const long long lk = ((long long)load * g.c + q) * g.H1 + kx;
 #pragma unroll
@@ -847,6 +828,46 @@ __global__ void __launch_bounds__(fft_threads(L), L == 256 ? UNO_GMINB : 1) gpas
         if (e < 8 * L) base[(long long)(e >> 3) * g.N2 + (e & 7)] = tiles[q][tidx(e >> 3, e & 7)];
       }
     }
+  };
+  const double w = parseval_w(kx, g.M);
+  double part = 0.0;
+  if constexpr (gconv_fusable(L) && NC * plan_radix(L, plan_stages(L) - 1) <= 32) {
+    // symbol multiply fused into the middle butterfly (fft.cuh fft_gconv)
+    auto mul = [&](int, int c, int kz, double2* x) {
+      return STG ? gmul_vals<NC>(x, gs, 8 * L, (long long)kz * 8 + c, w)
+                 : gmul_vals<NC>(x, cx.gtab, g.nspec, boff + (long long)kz * g.N2 + c, w);
+    };
+    if constexpr (PIPE) {
+      auto pre = [&](int q) {
+        if (q == 0) cp_wait<2>();
+        else if (q == 1) cp_wait<1>();
+        else cp_wait<0>();
+        __syncthreads();
+      };
+      part = fft_gconv<L, 1, NC>(tiles, tw, mul, pre, store_comp);
+    } else {
+      part = fft_gconv<L, 1, NC>(tiles, tw, mul);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < NC; ++q) fft_tile<L, false>(tiles[q], tw);
+#pragma unroll
+    for (int i = 0; i < (8 * L + T - 1) / T; ++i) {
+      const int e = t + i * T;
+      if (e < 8 * L) {
+        if (STG)
+          part += gmul_bin<NC>(tiles, tidx(e >> 3, e & 7), gs, 8 * L, e, w);
+        else
+          part += gmul_bin<NC>(tiles, tidx(e >> 3, e & 7), cx.gtab, g.nspec, boff + (long long)(e >> 3) * g.N2 + (e & 7), w);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < NC; ++q) fft_tile<L, true>(tiles[q], tw);
+  }
+  if constexpr (!PIPE) {
+#pragma unroll
+    for (int q = 0; q < NC; ++q) store_comp(q);
   }
   if constexpr (PEER) __threadfence_system();
   gamma_finish(cx, load, part, red_sh, MODE);

@@ -21,11 +21,13 @@
 namespace uno {
 
 constexpr int KM_TX = 16, KM_TY = 8, KM_T = 160;
-constexpr int KM_DW = KM_TX + 2, KM_DH = KM_TY + 2, KM_DP = KM_DW * KM_DH;  // 18 x 10 node tile
+// node tile x0-2 .. x0+17 (20 wide: 16-byte aligned pairs; x0-2 is unused) by y0-1 .. y0+8
+constexpr int KM_DW = KM_TX + 4, KM_DH = KM_TY + 2, KM_DP = KM_DW * KM_DH;
 constexpr int KM_EW = KM_TX + 1, KM_EH = KM_TY + 1, KM_NE = KM_EW * KM_EH;  // 17 x 9 elements
 constexpr int KM_RING = 8, KM_LA = 4;  // ring slots; planes prefetched ahead
 constexpr int KM_PLANE = 3 * KM_DP;                 // doubles per ring slot (3 components)
-constexpr int KM_NCP = (KM_PLANE + KM_T - 1) / KM_T;  // cp.async per thread per plane
+constexpr int KM_NCH = KM_PLANE / 2;                 // 16-byte chunks per ring slot
+constexpr int KM_NCP = (KM_NCH + KM_T - 1) / KM_T;    // cp.async per thread per plane
 
 __host__ __device__ constexpr int km_smem_bytes() {
   return (KM_RING * KM_PLANE + 2 * 12 * KM_NE) * (int)sizeof(double);
@@ -40,7 +42,7 @@ __global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int
   if (mode == CG && !cx.st[load].active) return;
   const int dz = g.dirz;
   extern __shared__ double kms[];
-  double* D = kms;                           // [RING][3][10][18]
+  double* D = kms;                           // [RING][3][10][20]
   double* Lb0 = D + KM_RING * KM_PLANE;      // [2][12][NE] node-plane outputs, double-buffered by layer parity
   __shared__ double red_sh[32];
   const int t = threadIdx.x;
@@ -52,18 +54,18 @@ __global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int
   const double* dv = src + (long long)load * 3 * n;
   const double hs = g.h / (72.0 * 64.0);
   const double l0 = cx.mat[0][0] * hs, m0 = cx.mat[0][1] * hs, l1 = cx.mat[1][0] * hs, m1 = cx.mat[1][1] * hs;
-  // copy assignment of the 3 x 10 x 18 plane tile (clamped: harmless duplicate copies)
+  // copy assignment of the 3 x 10 x 20 plane tile in 16-byte pairs (clamped: harmless duplicates)
   long long goff[KM_NCP];  // in-plane offset
   int gcomp[KM_NCP];
   unsigned sdst[KM_NCP];
 #pragma unroll
   for (int m = 0; m < KM_NCP; ++m) {
-    const int j = min(t + m * KM_T, KM_PLANE - 1);
-    const int comp = j / KM_DP, r = j - comp * KM_DP;
-    const int ly = r / KM_DW, lx = r - ly * KM_DW;
+    const int j = min(t + m * KM_T, KM_NCH - 1);
+    const int comp = j / (KM_DP / 2), r = j - comp * (KM_DP / 2);
+    const int ly = r / (KM_DW / 2), lx = 2 * (r - ly * (KM_DW / 2));
     gcomp[m] = comp;
-    goff[m] = (long long)((y0 - 1 + ly + N2) & (N2 - 1)) * N1 + ((x0 - 1 + lx + N1) & (N1 - 1));
-    sdst[m] = (unsigned)__cvta_generic_to_shared(D + j);  // clamped copies rewrite entry PLANE-1
+    goff[m] = (long long)((y0 - 1 + ly + N2) & (N2 - 1)) * N1 + ((x0 - 2 + lx + N1) & (N1 - 1));
+    sdst[m] = (unsigned)__cvta_generic_to_shared(D + comp * KM_DP + ly * KM_DW + lx);
   }
   auto slot_of = [&](int p) { return (p - zs + 1) & (KM_RING - 1); };
   auto issue_plane = [&](int p) {
@@ -71,7 +73,8 @@ __global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int
     if (dz && (p <= 0 || p >= N3)) {
 #pragma unroll
       for (int m = 0; m < KM_NCP; ++m)
-        asm volatile("st.shared.f64 [%0], 0d0000000000000000;\n" ::"r"(sdst[m] + so) : "memory");
+        asm volatile("st.shared.v2.f64 [%0], {0d0000000000000000, 0d0000000000000000};\n" ::"r"(sdst[m] + so)
+                     : "memory");
     } else {
       // component c of plane p starts at base + c * cst (slab halo buffers: [nrhs][3][N2][N1])
       const double* base;
@@ -84,7 +87,8 @@ __global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int
       }
 #pragma unroll
       for (int m = 0; m < KM_NCP; ++m)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sdst[m] + so), "l"(base + gcomp[m] * cst + goff[m])
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sdst[m] + so),
+                     "l"(base + gcomp[m] * cst + goff[m])
                      : "memory");
     }
   };
@@ -100,23 +104,26 @@ __global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int
   // 2D inverse of (lower-face modes of layer k + upper-face modes of layer k-1).
   double uc[12], vc[12];
   auto read_corners = [&](int p, double* dstv) {  // the 4 (x, y) corners of node plane p
-    const double* Dp = D + slot_of(p) * KM_PLANE + eyl * KM_DW + exl;
+    const double* Dp = D + slot_of(p) * KM_PLANE + eyl * KM_DW + exl + 1;
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int al = 0; al < 3; ++al) dstv[3 * a + al] = Dp[al * KM_DP + ((a >> 1) & 1) * KM_DW + (a & 1)];
   };
-  // phase of element layer k (1 byte, read one layer ahead so its latency hides behind a layer)
-  auto phase_of = [&](int k) -> bool {
-    // Dirichlet z: the prefetch one layer past the last one (layer N3) does not exist — clamp the
-    // address (its value is never used); a predicated load would cost the prefetch its early issue
+  // phase byte of element layer k, loaded three layers ahead (a queue of 3 registers): one layer
+  // ahead left 13 % of the stall samples on the load (ncu round 2)
+  auto phase_raw = [&](int k) -> unsigned {
+    // Dirichlet z: the prefetches past the last layer (N3 ...) do not exist — clamp the address
+    // (their values are never used); a predicated load would cost the prefetch its early issue
     const int layer = dz ? min(k, N3 - 1) : ((k + N3) & (N3 - 1));
-    return eth && __ldg(cx.phase + (long long)layer * plane + pbase) != 0;
+    return __ldg(cx.phase + (long long)layer * plane + pbase);
   };
-  bool phc = phase_of(zs - 1);
+  unsigned ph0 = phase_raw(zs - 1), ph1 = phase_raw(zs), ph2 = phase_raw(zs + 1);
   auto element_layer = [&](int k, bool want_lower) {  // element layer between node planes k, k+1
-    const bool ph = phc;
-    phc = phase_of(k + 1);
+    const bool ph = ph0 != 0;
+    ph0 = ph1;
+    ph1 = ph2;
+    ph2 = phase_raw(k + 3);
     if (!eth) return;
     const double ls = ph ? l1 : l0, ms = ph ? m1 : m0;
     double w[12];
@@ -131,9 +138,7 @@ __global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int
       uc[i] = w[i];
     }
     double v[24];
-#pragma unroll
-    for (int i = 0; i < 24; ++i) v[i] = 0.0;
-    modal::modal_apply<3>(v, u, ls, ms);  // rows of mode 0 are zero
+    modal::apply_blocked(v, u, ls, ms);  // rows of mode 0 are zero
     double o[12];
 #pragma unroll
     for (int i = 0; i < 12; ++i) {
@@ -189,7 +194,7 @@ __global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int
 #pragma unroll
         for (int al = 0; al < 3; ++al) p[al] += Lb[(3 * a + al) * KM_NE + e];
       }
-      const double* Dc = D + slot_of(k) * KM_PLANE + (ty + 1) * KM_DW + tx + 1;
+      const double* Dc = D + slot_of(k) * KM_PLANE + (ty + 1) * KM_DW + tx + 2;
       const long long gi = (long long)(k - dz - g.zlo) * plane + (long long)(y0 + ty) * N1 + x0 + tx;
       if ((g.dir3 && (x0 + tx == 0 || y0 + ty == 0 || k == 0)) || (g.zpad && k == 0))
         p[0] = p[1] = p[2] = 0.0;  // Dirichlet nodes (all-Dirichlet storage / slab Dirichlet-z face)
