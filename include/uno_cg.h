@@ -43,7 +43,8 @@
  *    the caller, e.g. torch.cuda.current_stream().cuda_stream); calls that return
  *    host scalars synchronise that stream.
  *  - Ownership: all field buffers (phase, u, f, r, z, ...) are caller-owned device
- *    memory.  The handle's workspace (CG vectors r, d, p, u, one spectrum buffer, the
+ *    memory.  The handle's workspace (CG vectors r, d, p, u, a second direction buffer for the
+ *    paired u updates of 3D grids, one spectrum buffer, the
  *    tabulated symbol, twiddle tables, reduction scratch; uno_cg_workspace_size bytes) is
  *    either caller-provided (borrowed, never freed by the library) or allocated by
  *    uno_cg_create and freed in uno_cg_destroy.  Outside it the library allocates only

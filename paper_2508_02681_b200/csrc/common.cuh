@@ -43,8 +43,10 @@ struct LoadState {
   int status;        // 0 ok, 6 breakdown, 7 nonfinite
   int converged;
   int pending_u;     // u += alpha d still owed (deferred to the x-inverse pass / finalize)
-  int fixed_iters, max_iter, pad_;
+  int fixed_iters, max_iter;
+  int u_done;        // paired u updates (Ctx::d2): direction terms 0 .. u_done-1 are in u
   double rel_tol;
+  double alpha_prev; // alpha of the K step before the last one (paired u updates)
 };
 
 // Reduction slots: one per (kernel class, load).

@@ -93,6 +93,7 @@ static __device__ void scalar_after_dp(LoadState* st, double dp, double* hist = 
     st->pending_u = 0;
     return;
   }
+  st->alpha_prev = st->alpha;
   st->alpha = st->gamma1 / dp;
   record_coef(hist, hist_stride, 2, load, st->iters, st->alpha);
   st->iters += 1;

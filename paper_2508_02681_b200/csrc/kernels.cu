@@ -360,8 +360,16 @@ __global__ void __launch_bounds__(fft_threads(M)) xinv_kernel(Ctx cx, double* __
   __syncthreads();
   const long long voff = (long long)load * g.c * g.n + row0 * g.N1;
   const int it0 = MODE == CG ? st->iters : 0;
+  // paired u updates (cx.d2): direction j = it0 is written to (j & 1) ? d2 : d and d_{j-1} read
+  // from the other buffer; u is touched only for even j >= 2, where u += alpha_{j-2} d_{j-2} +
+  // alpha_{j-1} d_{j-1} (d_{j-2} = the rows about to be overwritten): 28 instead of 32 B/DOF of
+  // vector traffic on average.  Without d2: u += alpha_{j-1} d_{j-1} every iteration.
+  const bool pair = MODE == CG && cx.d2 != nullptr;
+  double* dnew = pair && (it0 & 1) ? cx.d2 : cx.d;
+  const double* dold = pair && !(it0 & 1) ? cx.d2 : cx.d;
+  const bool do_u = pair ? (it0 >= 2 && !(it0 & 1)) : it0 > 0;
   if (MODE == CG) {  // d_old and u rows land while the inverse FFT runs
-    const double2* d2g = reinterpret_cast<const double2*>(cx.d + voff);
+    const double2* d2g = reinterpret_cast<const double2*>(dold + voff);
     const double2* u2g = reinterpret_cast<const double2*>(cx.u + voff);
     if (it0 > 0) {
 #pragma unroll
@@ -369,11 +377,16 @@ __global__ void __launch_bounds__(fft_threads(M)) xinv_kernel(Ctx cx, double* __
         const int e = t + i * T;
         if (e < 8 * M) {
           cp_async16(&stage[e], d2g + e);
-          cp_async16(&stage[8 * M + e], u2g + e);
+          if (do_u) cp_async16(&stage[8 * M + e], u2g + e);
         }
+      }
+      if (pair && do_u) {  // d_{j-2} rows: read in the epilogue straight from L2
+        const char* pb = reinterpret_cast<const char*>(dnew + voff);
+        for (int o = t * 128; o < 8 * M * 16; o += T * 128) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(pb + o));
       }
     }
     cp_commit();
+    if (pair && do_u && blockIdx.x == 0 && t == 0) st->u_done = it0;  // terms 0 .. it0-1 are in u
   }
   fft_tile<M, true>(tile, tw);
   if (MODE != CG) {
@@ -386,9 +399,9 @@ __global__ void __launch_bounds__(fft_threads(M)) xinv_kernel(Ctx cx, double* __
   } else {
     cp_wait<0>();
     __syncthreads();
-    double2* d2 = reinterpret_cast<double2*>(cx.d + voff);
+    double2* d2 = reinterpret_cast<double2*>(dnew + voff);
     double2* u2 = reinterpret_cast<double2*>(cx.u + voff);
-    const double beta = st->beta, alpha = st->alpha;
+    const double beta = st->beta, alpha = st->alpha, alpha2 = st->alpha_prev;
 #pragma unroll
     for (int i = 0; i < (8 * M + T - 1) / T; ++i) {
       const int e = t + i * T;
@@ -398,10 +411,17 @@ __global__ void __launch_bounds__(fft_threads(M)) xinv_kernel(Ctx cx, double* __
           d2[e] = s;  // d = s + (gamma1/gamma0) * 0   (Alg 2 l.2, l.8)
         } else {
           const double2 dold = stage[e];
-          double2 uu = stage[8 * M + e];  // deferred u += alpha_{m-1} d_{m-1}  (Alg 2 l.12)
-          uu.x = fma(alpha, dold.x, uu.x);
-          uu.y = fma(alpha, dold.y, uu.y);
-          u2[e] = uu;
+          if (do_u) {  // deferred u += [alpha_{m-2} d_{m-2} +] alpha_{m-1} d_{m-1}  (Alg 2 l.12)
+            double2 uu = stage[8 * M + e];
+            if (pair) {
+              const double2 dm2 = __ldcg(d2 + e);
+              uu.x = fma(alpha2, dm2.x, uu.x);
+              uu.y = fma(alpha2, dm2.y, uu.y);
+            }
+            uu.x = fma(alpha, dold.x, uu.x);
+            uu.y = fma(alpha, dold.y, uu.y);
+            u2[e] = uu;
+          }
           d2[e] = make_double2(fma(beta, dold.x, s.x), fma(beta, dold.y, s.y));
         }
       }
@@ -441,13 +461,24 @@ __global__ void __launch_bounds__(128) xinv512_kernel(Ctx cx, double* __restrict
     if (e < (M + 1) * 8) cp_async16(&sb[(e & 7) * XI5_SS + (e >> 3)], in + (long long)(e >> 3) * plane + (e & 7));
   }
   cp_commit();
-  if (MODE == CG && st->iters > 0) {  // the 8 rows of d_old and u (2 x 32 KB) into L2 for the epilogue
-    const char* db = reinterpret_cast<const char*>(cx.d + (long long)load * g.c * g.n + row0 * g.N1);
-    const char* ub = reinterpret_cast<const char*>(cx.u + (long long)load * g.c * g.n + row0 * g.N1);
+  // paired u updates (cx.d2; see xinv_kernel): direction j = iters goes to (j & 1) ? d2 : d, u is
+  // updated with two terms for even j >= 2 only
+  const int it0 = MODE == CG ? st->iters : 0;
+  const bool pair = MODE == CG && cx.d2 != nullptr;
+  double* dnew = pair && (it0 & 1) ? cx.d2 : cx.d;
+  double* dold = pair && !(it0 & 1) ? cx.d2 : cx.d;
+  const bool do_u = pair ? (it0 >= 2 && !(it0 & 1)) : it0 > 0;
+  if (MODE == CG && it0 > 0) {  // the 8 rows of d_old (and u, d_{j-2}) into L2 for the epilogue
+    const long long o = (long long)load * g.c * g.n + row0 * g.N1;
+    const char* db = reinterpret_cast<const char*>(dold + o);
+    const char* ub = reinterpret_cast<const char*>(cx.u + o);
+    const char* nb = reinterpret_cast<const char*>(dnew + o);
     for (int i = t; i < 8 * 512 * 8 / 128; i += 128) {
       asm volatile("prefetch.global.L2 [%0];\n" ::"l"(db + 128LL * i));
-      asm volatile("prefetch.global.L2 [%0];\n" ::"l"(ub + 128LL * i));
+      if (do_u) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(ub + 128LL * i));
+      if (pair && do_u) asm volatile("prefetch.global.L2 [%0];\n" ::"l"(nb + 128LL * i));
     }
+    if (pair && do_u && blockIdx.x == 0 && t == 0) st->u_done = it0;  // terms 0 .. it0-1 are in u
   }
   for (int i = t; i < M; i += 128) tw[i] = cx.tw.x[((i & 15) * (i >> 4)) & (M - 1)];  // [k1][n1]
   for (int i = t; i <= M; i += 128) twp[i] = cx.tw.xpost[i];
@@ -487,28 +518,39 @@ __global__ void __launch_bounds__(128) xinv512_kernel(Ctx cx, double* __restrict
 #pragma unroll
     for (int n2 = 0; n2 < 16; ++n2) __stcg(o2 + l16 + 16 * n2, v[n2]);
   } else {
-    double2* d2 = reinterpret_cast<double2*>(cx.d + voff);
+    double2* d2 = reinterpret_cast<double2*>(dnew + voff);
+    const double2* o2 = reinterpret_cast<const double2*>(dold + voff);
     double2* u2 = reinterpret_cast<double2*>(cx.u + voff);
-    if (st->iters == 0) {
+    if (it0 == 0) {
 #pragma unroll
       for (int n2 = 0; n2 < 16; ++n2) __stcg(d2 + l16 + 16 * n2, v[n2]);  // d = s (Alg 2 l.2, l.8)
     } else {
-      const double beta = st->beta, alpha = st->alpha;
+      const double beta = st->beta, alpha = st->alpha, alpha2 = st->alpha_prev;
 #pragma unroll
       for (int h8 = 0; h8 < 16; h8 += 8) {
-        double2 dold[8], uu[8];
+        double2 dold8[8], uu[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          dold[i] = __ldcs(d2 + l16 + 16 * (h8 + i));
-          uu[i] = __ldcs(u2 + l16 + 16 * (h8 + i));
+          dold8[i] = __ldcs(o2 + l16 + 16 * (h8 + i));
+          if (do_u) uu[i] = __ldcs(u2 + l16 + 16 * (h8 + i));
+        }
+        if (do_u && pair) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {  // + alpha_{m-2} d_{m-2} (the rows about to be overwritten)
+            const double2 dm2 = __ldcs(d2 + l16 + 16 * (h8 + i));
+            uu[i].x = fma(alpha2, dm2.x, uu[i].x);
+            uu[i].y = fma(alpha2, dm2.y, uu[i].y);
+          }
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          uu[i].x = fma(alpha, dold[i].x, uu[i].x);  // deferred u += alpha_{m-1} d_{m-1} (l.12)
-          uu[i].y = fma(alpha, dold[i].y, uu[i].y);
-          __stcg(u2 + l16 + 16 * (h8 + i), uu[i]);
+          if (do_u) {
+            uu[i].x = fma(alpha, dold8[i].x, uu[i].x);  // deferred u += alpha_{m-1} d_{m-1} (l.12)
+            uu[i].y = fma(alpha, dold8[i].y, uu[i].y);
+            __stcg(u2 + l16 + 16 * (h8 + i), uu[i]);
+          }
           const double2 s = v[h8 + i];
-          __stcg(d2 + l16 + 16 * (h8 + i), make_double2(fma(beta, dold[i].x, s.x), fma(beta, dold[i].y, s.y)));
+          __stcg(d2 + l16 + 16 * (h8 + i), make_double2(fma(beta, dold8[i].x, s.x), fma(beta, dold8[i].y, s.y)));
         }
       }
     }
@@ -1246,7 +1288,7 @@ __global__ void __launch_bounds__(TX * KT_TY, 3) kp_thermal3d_kernel(Ctx cx, int
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * KT_TY, zs = zcI * ZC;
   const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
   const long long plane = (long long)N1 * N2;
-  const double* dv = src + (long long)load * g.n;
+  const double* dv = cg_dir(cx, mode, src, load) + (long long)load * g.n;
   const double k0 = cx.mat[0][0], k1 = cx.mat[1][0];
 
   int goffD[ND], goffE[NE];
@@ -1440,7 +1482,7 @@ __global__ void __launch_bounds__(TX * KT_TY / 2, 4) kp_thermal3d_r2_kernel(Ctx 
   const int ze = min(zs + ZC, g.P3 + dz);  // node planes [zs, ze)
   const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
   const long long plane = (long long)N1 * N2;
-  const double* dv = src + (long long)load * g.n;
+  const double* dv = cg_dir(cx, mode, src, load) + (long long)load * g.n;
   const double k0 = cx.mat[0][0], k1 = cx.mat[1][0];
   // per-thread 16-byte copy assignment (indices past the tile are clamped: harmless duplicates);
   // x pairs start at even x so every chunk stays contiguous across the periodic wrap
@@ -1659,7 +1701,7 @@ __global__ void __launch_bounds__(128, 2) kp_thermal3d_rn_kernel(Ctx cx, int mod
   const int ze = min(zs + ZC, g.P3 + dz + g.zlo);  // slab mode: global node planes [zlo, zlo + P3)
   const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
   const long long plane = (long long)N1 * N2;
-  const double* dv = src + (long long)load * g.n;
+  const double* dv = cg_dir(cx, mode, src, load) + (long long)load * g.n;
   const double k0 = cx.mat[0][0], k1 = cx.mat[1][0];
   int goffD[NDC];
   unsigned sD[NDC];
@@ -1859,7 +1901,7 @@ __global__ void __launch_bounds__(256) kp_thermal2d_kernel(Ctx cx, int mode, con
   double part = 0.0;
   if (i < g.n) {
     const int x = (int)(i % N1), y = (int)(i / N1);
-    const double* dv = src + (long long)load * g.n;
+    const double* dv = cg_dir(cx, mode, src, load) + (long long)load * g.n;
     const int xm = (x - 1 + N1) & (N1 - 1), xp = (x + 1) & (N1 - 1), ym = (y - 1 + N2) & (N2 - 1), yp = (y + 1) & (N2 - 1);
     auto D = [&](int xx, int yy) { return __ldg(dv + (long long)yy * N1 + xx); };
     auto KAP = [&](int xx, int yy) { return __ldg(cx.phase + (long long)yy * N1 + xx) ? cx.mat[1][0] : cx.mat[0][0]; };
@@ -1896,7 +1938,7 @@ __global__ void __launch_bounds__(256) kp_elastic2d_kernel(Ctx cx, int mode, con
   double part = 0.0;
   if (i < n) {
     const int x = (int)(i % N1), y = (int)(i / N1);
-    const double* dv = src + (long long)load * 2 * n;
+    const double* dv = cg_dir(cx, mode, src, load) + (long long)load * 2 * n;
     double acc[2] = {0.0, 0.0};
     for (int o = 0; o < 4; ++o) {
       const int ox = o & 1, oy = o >> 1;
@@ -2050,13 +2092,27 @@ __global__ void finalize_kernel(Ctx cx) {
   const Geo g = cx.g;
   const int load = blockIdx.y;
   const LoadState* st = cx.st + load;
-  if (!st->pending_u || st->iters < 1) return;
-  const double a = st->alpha;
   const long long cnt = (long long)g.c * g.n;
   double* u = cx.u + (long long)load * cnt;
+  const double a = st->alpha;
+  const long long i0 = (long long)blockIdx.x * blockDim.x + threadIdx.x, stp = (long long)gridDim.x * blockDim.x;
+  if (cx.d2) {  // paired u updates: the terms u_done .. iters-1 (one or two) are still owed
+    const int I = st->iters, owed = I - st->u_done;
+    if (I < 1 || owed <= 0) return;
+    auto dir = [&](int j) { return ((j & 1) ? cx.d2 : cx.d) + (long long)load * cnt; };
+    const double* dl = dir(I - 1);
+    if (owed >= 2) {
+      const double* dp = dir(I - 2);
+      const double a2 = st->alpha_prev;
+      for (long long i = i0; i < cnt; i += stp) u[i] = fma(a, dl[i], fma(a2, dp[i], u[i]));
+    } else {
+      for (long long i = i0; i < cnt; i += stp) u[i] = fma(a, dl[i], u[i]);
+    }
+    return;
+  }
+  if (!st->pending_u || st->iters < 1) return;
   const double* d = cx.d + (long long)load * cnt;
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (long long)gridDim.x * blockDim.x)
-    u[i] = fma(a, d[i], u[i]);
+  for (long long i = i0; i < cnt; i += stp) u[i] = fma(a, d[i], u[i]);
 }
 
 // per (load, comp) partial sums over fixed chunks, then a fixed-order combine + subtract

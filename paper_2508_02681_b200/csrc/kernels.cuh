@@ -27,6 +27,9 @@ struct Ctx {
   double2* spec;            // [nrhs][c][H1][N3][N2]
   double* r;                // [nrhs][c][n]
   double* d;
+  double* d2;               // paired u updates: direction j lives in (j & 1) ? d2 : d, and the x^-1
+                            // pass adds two terms to u every other iteration (null: one buffer,
+                            // u += alpha d_old every iteration)
   double* p;
   double* u;
   double* hist;             // [nrhs][hist_stride] residual history (device) or null
@@ -68,6 +71,10 @@ int gpass_nblk(const Geo& g);  // CTAs (gamma partials per load) of the CG-mode 
 int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaStream_t s, int zc0 = 0, int nzl = 0);
 int launch_rhs(const Ctx& cx, const LoadParams& lp, double* f, cudaStream_t s);
 int launch_finalize(const Ctx& cx, cudaStream_t s);
+// CG-mode direction vector of `load` for the K pass (paired u updates: the buffer of direction iters)
+__device__ __forceinline__ const double* cg_dir(const Ctx& cx, int mode, const double* src, int load) {
+  return (mode == CG && cx.d2) ? ((cx.st[load].iters & 1) ? cx.d2 : cx.d) : src;
+}
 int launch_mean_removal(const Ctx& cx, const double* u, double* out, double* scratch_means, cudaStream_t s);
 int launch_effective(const Ctx& cx, const LoadParams& lp, const double* u, double* partials, int* nblocks_out,
                      cudaStream_t s);

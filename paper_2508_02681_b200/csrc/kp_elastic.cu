@@ -51,7 +51,7 @@ __global__ void __launch_bounds__(KM_T, 3) kp_elastic3d_modal_kernel(Ctx cx, int
   const long long plane = (long long)N1 * N2;
   const int x0 = blockIdx.x * KM_TX, y0 = blockIdx.y * KM_TY;
   const int zs = zcI * ZC + dz + g.zlo, ze = min(zs + ZC, g.P3 + dz + g.zlo);  // slab: global planes
-  const double* dv = src + (long long)load * 3 * n;
+  const double* dv = cg_dir(cx, mode, src, load) + (long long)load * 3 * n;
   const double hs = g.h / (72.0 * 64.0);
   const double l0 = cx.mat[0][0] * hs, m0 = cx.mat[0][1] * hs, l1 = cx.mat[1][0] * hs, m1 = cx.mat[1][1] * hs;
   // copy assignment of the 3 x 10 x 20 plane tile in 16-byte pairs (clamped: harmless duplicates)

@@ -50,6 +50,7 @@ struct uno_cg_handle {
   double ref0, ref1;
   // device buffers
   double *r, *d, *p, *u;
+  double* d2;             // second direction buffer of the paired u updates (null: not used)
   double2* spec;
   double* gtab;
   double* kel;
@@ -158,6 +159,7 @@ static Ctx make_ctx(uno_cg_handle* h) {
   cx.gtab = h->gtab;
   cx.kel = h->kel;
   cx.spec = h->spec;
+  cx.d2 = h->precond == 0 ? h->d2 : nullptr;  // the baseline preconditioners keep one buffer
   cx.r = h->r;
   cx.d = h->d;
   cx.p = h->p;
@@ -313,7 +315,15 @@ static uno_status make_geo(const uno_cg_desc& D, Geo& g) {
 // Device workspace of a handle: every buffer the library owns, carved from one arena (caller-
 // provided or allocated here) at 256-byte aligned offsets.  Order = WS_* below.
 enum { WS_R, WS_D, WS_P, WS_U, WS_SPEC, WS_GTAB, WS_KEL, WS_TWX, WS_TWXP, WS_TWY, WS_TWZ, WS_TWZ2, WS_RT, WS_TWX2,
-       WS_TWY2, WS_ST, WS_PART, WS_CNT, WS_RES, WS_SCR, WS_LOOP, WS_N };
+       WS_TWY2, WS_ST, WS_PARTS, WS_CNT, WS_RES, WS_SCR, WS_LOOP, WS_D2, WS_N };
+
+// Paired u updates (kernels.cuh Ctx::d2): 3D whole-grid handles with the UNO preconditioner (set per
+// handle), periodic or Dirichlet-z storage; the x^-1 passes (xinv_kernel, xinv512_kernel) and the
+// 3D K kernels follow the two direction buffers.
+#ifndef UNO_PAIRED_U
+#define UNO_PAIRED_U 1  // 0: one direction buffer, u updated every iteration (A/B builds only)
+#endif
+static bool paired_u_ok(const Geo& g) { return UNO_PAIRED_U && g.dim == 3 && !g.dmask && !g.halo; }
 
 static size_t scratch_doubles(const Geo& g) {
   return (size_t)std::max<long long>((long long)(kMaxRhs * kMaxRhs + 1) * (148 * 4 + 1) * 2 + 64,
@@ -327,7 +337,8 @@ static size_t ws_layout(const Geo& g, size_t off[WS_N]) {
       (size_t)g.M * 16, (size_t)(g.M + 1) * 16, (size_t)g.N2 * 16, (size_t)g.N3 * 16, (size_t)2 * g.N3 * 16,
       g.dmask ? vec : 8, g.dmask ? (size_t)2 * g.N1 * 16 : 16, g.dmask ? (size_t)2 * g.N2 * 16 : 16,
       kMaxRhs * sizeof(LoadState), (size_t)RED_NSLOT * kMaxRhs * blocks_needed_max(g) * 8,
-      RED_NSLOT * kMaxRhs * sizeof(unsigned), RED_NSLOT * kMaxRhs * 8, scratch_doubles(g) * 8, 64};
+      RED_NSLOT * kMaxRhs * sizeof(unsigned), RED_NSLOT * kMaxRhs * 8, scratch_doubles(g) * 8, 64,
+      paired_u_ok(g) ? vec : 8};
   size_t t = 0;
   for (int i = 0; i < WS_N; ++i) {
     if (off) off[i] = t;
@@ -405,11 +416,12 @@ extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_ph
   h->twx2 = (double2*)(A + off[WS_TWX2]);
   h->twy2 = (double2*)(A + off[WS_TWY2]);
   h->st = (LoadState*)(A + off[WS_ST]);
-  h->partials = (double*)(A + off[WS_PART]);
+  h->partials = (double*)(A + off[WS_PARTS]);
   h->counters = (unsigned*)(A + off[WS_CNT]);
   h->results = (double*)(A + off[WS_RES]);
   h->scratch = (double*)(A + off[WS_SCR]);
   h->loopctr = (int*)(A + off[WS_LOOP]);
+  h->d2 = paired_u_ok(g) ? (double*)(A + off[WS_D2]) : nullptr;
   if ((e = cudaMallocHost((void**)&h->h_st, kMaxRhs * sizeof(LoadState))) ||
       (e = cudaMallocHost((void**)&h->h_small, 4096 * 8)) || (e = cudaEventCreate(&h->e0)) ||
       (e = cudaEventCreate(&h->e1))) {
@@ -485,6 +497,7 @@ extern "C" uno_status uno_cg_set_preconditioner(uno_cg_handle* h, int32_t kind) 
   if (kind < UNO_PRECOND_UNO || kind > UNO_PRECOND_JACOBI) return fail(UNO_ERR_ARG, "kind must be 0, 1 or 2");
   if (kind == UNO_PRECOND_JACOBI && !h->dinv) CK(cudaMallocAsync((void**)&h->dinv, (size_t)h->g.n * 8, h->stream));
   h->precond = kind;
+  h->cx = make_ctx(h);  // the paired u updates apply to the UNO preconditioner only
   if (kind == UNO_PRECOND_JACOBI) launch_jacobi_dinv(h->cx, h->dinv, h->stream);
   if (h->gexec) {  // the iteration body changes: re-capture on the next solve
     cudaGraphExecDestroy(h->gexec);

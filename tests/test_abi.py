@@ -95,7 +95,8 @@ def test_workspace_size_accounts_for_the_cg_state():
     vec = 3 * n * 8
     spec = 3 * 129 * 256 * 256 * 16
     gtab = 129 * 256 * 256 * 8
-    assert 4 * vec + spec + gtab <= ws <= 4 * vec + spec + gtab + (64 << 20)  # r, d, p, u + spectrum + G_hat + small
+    # r, d, d2 (second direction buffer of the paired u updates), p, u + spectrum + G_hat + small
+    assert 5 * vec + spec + gtab <= ws <= 5 * vec + spec + gtab + (64 << 20)
     assert ws % 256 == 0
     d.physics, d.nrhs = 1, 1  # elastic: 3 components, 6 symbol planes
     d.mat[0][1] = d.mat[1][1] = 1.0

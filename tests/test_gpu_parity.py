@@ -838,3 +838,17 @@ def test_tiny_one_cta_solve_equals_graph_loop(N):
     ref = homog.solve_problem(g, "thermal", ph, mat, loads[:1], seed, amp, tol=1e-8)
     assert abs(a.reports[0]["iterations"] - ref["iterations"][0]) <= 1
 
+
+
+@pytest.mark.parametrize("N,physics", [((32, 16, 8), "thermal"), ((16, 8, 8), "elastic")])
+def test_paired_u_updates_every_stop_parity(N, physics):
+    # 3D handles keep two direction buffers and fold u += alpha d into every other x^-1 pass (two
+    # terms at a time); a solve can stop after an odd or an even number of K steps, leaving one or
+    # two terms for the finalize kernel: u after m = 1..6 fixed iterations equals the oracle's
+    g, ph, mat, amp, seed = make_case(N, physics)
+    s = solver(ph, physics, mat, 1, seed, amp)
+    L = loads_for(physics, 3, 1)
+    for m in range(1, 7):
+        u = s.solve(L, fixed_iters=m).u.cpu().numpy()[0]
+        ref = homog.solve_problem(g, physics, ph, mat, L, seed, amp, fixed_iters=m)["U"][0]
+        assert rel(u, ref) <= 1e-11, (m, rel(u, ref))
