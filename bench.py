@@ -146,7 +146,9 @@ def kernel_bytes(n: int, N1: int, nrhs: int):
         "xfwd": 8 + 8 + 8 + spec,         # read r, p; write r; write r_hat
         "ypass": 2 * spec,               # read + write spectrum (per launch; 2 launches/iter)
         "gpass": 2 * spec + spec / 2,    # read + write spectrum + 8 B G_hat per bin
-        "xinv": spec + 8 * 4,            # read s_hat; read d, u; write d, u
+        "xinv": spec + 8 * 3.5,          # read s_hat; paired u updates (3D handles): odd iterations
+                                         # read d_old, write d (16 B), even ones read d_old, d_{j-2},
+                                         # u, write d, u (40 B): 28 B/DOF on average
     }
     return {k: v * n * nrhs for k, v in per_dof.items()}
 

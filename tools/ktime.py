@@ -24,13 +24,13 @@ if a.physics == "thermal":
     ph = torch.from_numpy(synth.config3_microstructure(3, n=n)).to(dev)
     s = UnoCG(ph, "thermal", (1.0, 20.0), nrhs=a.nrhs, seed=3003, amp=0.1, bc=tuple(int(v) for v in a.bc.split(",")))
     loads = np.eye(3)[: a.nrhs]
-    nb = {"K": 17, "xfwd": 24 + 8.06, "ypass": 16.1, "gpass": 20.1, "xinv": 40.06}
+    nb = {"K": 17, "xfwd": 24 + 8.06, "ypass": 16.1, "gpass": 20.1, "xinv": 36.06}
 else:
     ph = torch.from_numpy(synth.spheres_rsa(n, 0.25, 6.0 * n / 64, 10.0 * n / 64, seed=2)).to(dev)
     mat = (synth.lame_from_E_nu(1.0, 0.3), synth.lame_from_E_nu(10.0, 0.2))
     s = UnoCG(ph, "elastic", mat, nrhs=a.nrhs, seed=1002, amp=0.05, bc=tuple(int(v) for v in a.bc.split(",")))
     loads = np.eye(6)[: a.nrhs]
-    nb = {"K": 16.33, "xfwd": 24 + 8.06, "ypass": 16.1, "gpass": 24.1, "xinv": 40.06}
+    nb = {"K": 16.33, "xfwd": 24 + 8.06, "ypass": 16.1, "gpass": 24.1, "xinv": 36.06}
 s.solve(loads, fixed_iters=3)
 s.kernel_timing(enable=1, reset=1)
 r = s.solve(loads, fixed_iters=a.iters)
