@@ -190,13 +190,15 @@ def run_ours(args):
     m0, R0 = probs[0]
     solver = UnoCG(phases[m0], "thermal", (1.0, R0), nrhs=3, seed=3000 + m0, amp=0.1, stream=stream)
 
-    def one_step(timing: bool):
+    def one_step(timing: bool, pev=None):
         dofit = 0
         launches = 0
         kt = {}
         effs = []
         s = solver
-        for (m, R) in probs:
+        for i, (m, R) in enumerate(probs):
+            if pev is not None:
+                pev[i][0].record(stream)
             s.update(phases[m], (1.0, R), seed=3000 + m, amp=0.1)
             launches += 2  # symbol build + Eq 55
             if timing:
@@ -206,6 +208,9 @@ def run_ours(args):
             dofit += sum(r["iterations"] for r in res.reports) * n ** 3
             effs.append(s.effective_property(res.u, loads))
             launches += 2
+            if pev is not None:
+                pev[i][1].record(stream)
+                pits.append([r["iterations"] for r in res.reports])
             if timing:
                 for k, (ms, c) in s.kernel_timing().items():
                     a = kt.setdefault(k, [0.0, 0])
@@ -223,13 +228,16 @@ def run_ours(args):
         one_step(False)
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # per-problem device time of the first timed step (events between problems: negligible cost)
+    pev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in probs]
+    pits = []
     tot_dofit, tot_launch, ktimes = 0, 0, {}
     with ClockSampler(local) as clk:
         # timed region: the production path (each solve one CUDA graph with a device-side WHILE loop)
         barrier()
         ev0.record(stream)
-        for _ in range(args.steps):
-            d_, l_, _, effs = one_step(False)
+        for k_ in range(args.steps):
+            d_, l_, _, effs = one_step(False, pev if k_ == 0 else None)
             tot_dofit += d_
             tot_launch += l_
         ev1.record(stream)
@@ -251,6 +259,7 @@ def run_ours(args):
         kt1.record(stream)
         barrier()
     my_ms = ev0.elapsed_time(ev1)
+    prob_ms = [round(a.elapsed_time(b), 2) for a, b in pev]
     ms = D.reduce_max(my_ms)                      # max over ranks of the device time
     rank_ms = D.gather_results([my_ms])
     all_dofit = D.reduce_sum(float(tot_dofit))    # units processed by all ranks
@@ -352,6 +361,9 @@ def run_ours(args):
                        "problems_per_rank": len(probs),
                        "rank_ms": [round(x, 1) for x in rank_ms],
                        "imbalance_max_over_mean": round(max(rank_ms) / (sum(rank_ms) / len(rank_ms)), 4),
+                       "problems": [f"m{m}R{R:g}" for m, R in probs] if ws == 1 else None,
+                       "problem_ms_step1": prob_ms if ws == 1 else None,
+                       "problem_iterations": pits if ws == 1 else None,
                        "input_generation_s": round(gen_s, 1)},
             "roofline": roof, "iteration_roofline": iter_roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(tot_launch),

@@ -17,6 +17,7 @@
 #include "../../include/uno_cg.h"
 #include "common.cuh"
 #include "kernels.cuh"
+#include <nvtx3/nvToolsExt.h>  // header-only: ranges are no-ops unless a profiler (nsys) is attached
 
 using namespace uno;
 
@@ -41,6 +42,13 @@ uno_status set_last_error(uno_status s, const char* msg) {  // shared with slab.
   } while (0)
 
 enum { KC_K = 0, KC_XF = 1, KC_Y = 2, KC_G = 3, KC_XI = 4, KC_OTHER = 5, KC_N = 6 };
+
+
+// NVTX range around each public call (visible in an nsys / ncu --nvtx timeline)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 struct uno_cg_handle {
   uno_cg_desc desc;
@@ -359,6 +367,7 @@ extern "C" uno_status uno_cg_workspace_size(const uno_cg_desc* desc, size_t* byt
 // ------------------------------------------------------------------------------ create/destroy
 extern "C" uno_status uno_cg_create(const uno_cg_desc* desc, const uint8_t* d_phase, void* d_workspace,
                                     uno_cg_handle** out) {
+  NvtxRange nvtx_("uno_cg_create");
   if (!desc || !d_phase || !out) return fail(UNO_ERR_ARG, "null argument");
   *out = nullptr;
   if (((uintptr_t)d_workspace & 255) != 0) return fail(UNO_ERR_ARG, "d_workspace must be 256-byte aligned");
@@ -470,6 +479,7 @@ extern "C" uno_status uno_cg_destroy(uno_cg_handle* h) {
 }
 
 extern "C" uno_status uno_cg_update(uno_cg_handle* h, const uno_cg_desc* desc, const uint8_t* d_phase) {
+  NvtxRange nvtx_("uno_cg_update");
   if (!h || !desc || !d_phase) return fail(UNO_ERR_ARG, "null argument");
   const uno_cg_desc& D = *desc;
   const uno_cg_desc& O = h->desc;
@@ -596,6 +606,7 @@ static void fill_loads(const uno_cg_handle* h, const double* h_loads, LoadParams
 }
 
 extern "C" uno_status uno_cg_rhs(uno_cg_handle* h, const double* h_loads, double* d_f) {
+  NvtxRange nvtx_("uno_cg_rhs");
   if (!h || !h_loads || !d_f) return fail(UNO_ERR_ARG, "null argument");
   LoadParams lp;
   fill_loads(h, h_loads, lp);
@@ -605,6 +616,7 @@ extern "C" uno_status uno_cg_rhs(uno_cg_handle* h, const double* h_loads, double
 }
 
 extern "C" uno_status uno_cg_apply_K(uno_cg_handle* h, const double* d_u, double* d_Au, double* h_uAu) {
+  NvtxRange nvtx_("uno_cg_apply_K");
   if (!h || !d_u || !d_Au) return fail(UNO_ERR_ARG, "null argument");
   if (d_u == d_Au) return fail(UNO_ERR_ARG, "apply_K: input and output must not alias");
   long long launches = 0;
@@ -620,6 +632,7 @@ extern "C" uno_status uno_cg_apply_K(uno_cg_handle* h, const double* d_u, double
 }
 
 extern "C" uno_status uno_cg_apply_precond(uno_cg_handle* h, const double* d_r, double* d_z, double* h_rz) {
+  NvtxRange nvtx_("uno_cg_apply_precond");
   if (!h || !d_r || !d_z) return fail(UNO_ERR_ARG, "null argument");
   long long launches = 0;
   cudaStream_t s = h->stream;
@@ -774,6 +787,7 @@ static double zero_floor(const uno_cg_handle* h, const double* load, int nv) {
 
 extern "C" uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, double rel_tol, int32_t max_iter,
                                    int32_t fixed_iters, double* d_u, uno_cg_report* rep, double* h_hist) {
+  NvtxRange nvtx_("uno_cg_solve");
   if (!h || !h_loads || !d_u) return fail(UNO_ERR_ARG, "null argument");
   if (!(rel_tol >= 0) || max_iter < 0) return fail(UNO_ERR_ARG, "rel_tol >= 0, max_iter >= 0 required");
   const Geo& g = h->g;
@@ -902,6 +916,7 @@ extern "C" uno_status uno_cg_solve(uno_cg_handle* h, const double* h_loads, doub
 
 extern "C" uno_status uno_cg_effective_property(uno_cg_handle* h, const double* d_u, const double* h_loads,
                                                 double* h_out) {
+  NvtxRange nvtx_("uno_cg_effective_property");
   if (!h || !d_u || !h_loads || !h_out) return fail(UNO_ERR_ARG, "null argument");
   const Geo& g = h->g;
   LoadParams lp;
