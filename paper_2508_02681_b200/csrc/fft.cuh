@@ -146,6 +146,62 @@ __device__ __forceinline__ void fft_stage(double2* s, const double2* __restrict_
   __syncthreads();
 }
 
+// ---- the same Stockham stages on a tile of W (power of two <= 8) columns: idx_w(j, c) =
+// W j + (c ^ (j & (W-1))).  Narrow tiles let a long transform (L = 1024) keep two CTAs per SM.
+template <int W>
+__device__ __forceinline__ int tidx_w(int j, int c) { return j * W + (c ^ (j & (W - 1))); }
+
+template <int L, int R, int NS, bool INV, int W>
+__device__ __forceinline__ void fft_stage_w(double2* s, const double2* __restrict__ tw) {
+  constexpr int NJ = L / R;
+  constexpr int ITEMS = NJ * W;
+  const int t = threadIdx.x;
+  const bool act = t < ITEMS;
+  const int c = t & (W - 1), j = t / W;
+  const int k = j % NS;
+  double2 v[R];
+  if (act) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = s[tidx_w<W>(j + r * NJ, c)];
+    if (NS > 1) {
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        double2 w = tw[r * k * (L / (NS * R))];
+        if (INV) w.y = -w.y;
+        v[r] = cmul(v[r], w);
+      }
+    }
+    if (INV) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r].y = -v[r].y;
+    }
+    Dft<R>::run(v);
+    if (INV) {
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[r].y = -v[r].y;
+    }
+  }
+  __syncthreads();
+  if (act) {
+    const int base = (j / NS) * NS * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) s[tidx_w<W>(base + r * NS, c)] = v[r];
+  }
+  __syncthreads();
+}
+template <int L, int NS, bool INV, int W>
+struct FftStagesW {
+  static __device__ __forceinline__ void run(double2* s, const double2* tw) {
+    constexpr int R = pick_radix(L / NS);
+    fft_stage_w<L, R, NS, INV, W>(s, tw);
+    FftStagesW<L, NS * R, INV, W>::run(s, tw);
+  }
+};
+template <int L, bool INV, int W>
+struct FftStagesW<L, L, INV, W> {
+  static __device__ __forceinline__ void run(double2*, const double2*) {}
+};
+
 template <int L, int NS, bool INV>
 struct FftStages {
   static __device__ __forceinline__ void run(double2* s, const double2* tw) {
@@ -163,6 +219,14 @@ struct FftStages<L, L, INV> {
 template <int L, bool INV>
 __device__ __forceinline__ void fft_tile(double2* s, const double2* tw) {
   FftStages<L, 1, INV>::run(s, tw);
+}
+
+template <int L, bool INV, int W>
+__device__ __forceinline__ void fft_tile_w(double2* s, const double2* tw) {
+  FftStagesW<L, 1, INV, W>::run(s, tw);
+}
+__host__ __device__ constexpr int fft_threads_w(int L, int W) {
+  return (W * L / min_radix(L)) < 64 ? 64 : W * L / min_radix(L);
 }
 
 // ---- NT tiles at once (tile q at s + q*8L): more butterflies per stage for bigger CTAs ----
