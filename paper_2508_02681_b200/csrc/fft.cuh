@@ -230,12 +230,15 @@ __host__ __device__ constexpr int fft_threads_w(int L, int W) {
 }
 
 // ---- NT tiles at once (tile q at s + q*8L): more butterflies per stage for bigger CTAs ----
-template <int L, int NT, int R, int NS, bool INV>
+// ALL: the CTA has exactly ITEMS threads (no inactive thread).  Inside a loop over tiles the
+// `if (act)` form would keep v[] live around the loop (undefined on the inactive path = the
+// previous iteration's value), i.e. R complex registers pinned through every other stage.
+template <int L, int NT, int R, int NS, bool INV, bool ALL = false>
 __device__ __forceinline__ void fft_stage_nt(double2* s, const double2* __restrict__ tw) {
   constexpr int NJ = L / R;
   constexpr int ITEMS = NJ * kTile * NT;
   const int t = threadIdx.x;
-  const bool act = t < ITEMS;
+  const bool act = ALL || t < ITEMS;
   const int q = t / (NJ * kTile), rem = t - q * (NJ * kTile);
   const int c = rem & 7, j = rem >> 3;
   const int k = j % NS;
@@ -271,16 +274,16 @@ __device__ __forceinline__ void fft_stage_nt(double2* s, const double2* __restri
   __syncthreads();
 }
 
-template <int L, int NT, int NS, bool INV>
+template <int L, int NT, int NS, bool INV, bool ALL = false>
 struct FftStagesNT {
   static __device__ __forceinline__ void run(double2* s, const double2* tw) {
     constexpr int R = pick_radix(L / NS);
-    fft_stage_nt<L, NT, R, NS, INV>(s, tw);
-    FftStagesNT<L, NT, NS * R, INV>::run(s, tw);
+    fft_stage_nt<L, NT, R, NS, INV, ALL>(s, tw);
+    FftStagesNT<L, NT, NS * R, INV, ALL>::run(s, tw);
   }
 };
-template <int L, int NT, bool INV>
-struct FftStagesNT<L, NT, L, INV> {
+template <int L, int NT, bool INV, bool ALL>
+struct FftStagesNT<L, NT, L, INV, ALL> {
   static __device__ __forceinline__ void run(double2*, const double2*) {}
 };
 
@@ -318,13 +321,13 @@ __host__ __device__ constexpr bool gconv_fusable(int L) {
   return plan_stages(L) >= 2 && plan_radix(L, 0) == plan_radix(L, plan_stages(L) - 1);
 }
 
-template <int L, int NT, int NS, int STOP, bool INV>
+template <int L, int NT, int NS, int STOP, bool INV, bool ALL = false>
 struct FftStagesNTUntil {
   static __device__ __forceinline__ void run(double2* s, const double2* tw) {
     if constexpr (NS < STOP) {
       constexpr int R = pick_radix(L / NS);
-      fft_stage_nt<L, NT, R, NS, INV>(s, tw);
-      FftStagesNTUntil<L, NT, NS * R, STOP, INV>::run(s, tw);
+      fft_stage_nt<L, NT, R, NS, INV, ALL>(s, tw);
+      FftStagesNTUntil<L, NT, NS * R, STOP, INV, ALL>::run(s, tw);
     }
   }
 };
@@ -336,7 +339,7 @@ struct GconvNoHook {
 };
 // pre(q): called before component q's forward stages (e.g. wait for its copy group + barrier);
 // post(q): after its inverse stages (the tile is complete: e.g. store it while the next one runs).
-template <int L, int NT, int NC, class Op, class Pre = GconvNoHook, class Post = GconvNoHook>
+template <int L, int NT, int NC, bool ALL = false, class Op, class Pre = GconvNoHook, class Post = GconvNoHook>
 __device__ __forceinline__ double fft_gconv(double2* const* tiles, const double2* __restrict__ tw, Op op,
                                             Pre pre = Pre(), Post post = Post()) {
   constexpr int S = plan_stages(L);
@@ -346,11 +349,11 @@ __device__ __forceinline__ double fft_gconv(double2* const* tiles, const double2
 #pragma unroll
   for (int q = 0; q < NC; ++q) {
     pre(q);
-    FftStagesNTUntil<L, NT, 1, NJ, false>::run(tiles[q], tw);
+    FftStagesNTUntil<L, NT, 1, NJ, false, ALL>::run(tiles[q], tw);
   }
   constexpr int ITEMS = NJ * kTile * NT;
   const int t = threadIdx.x;
-  const bool act = t < ITEMS;
+  const bool act = ALL || t < ITEMS;
   const int tq = t / (NJ * kTile), rem = t - tq * (NJ * kTile);
   const int c = rem & 7, j = rem >> 3;
   double part = 0.0;
@@ -389,7 +392,7 @@ __device__ __forceinline__ double fft_gconv(double2* const* tiles, const double2
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < NC; ++q) {
-    FftStagesNT<L, NT, plan_radix(L, 0), true>::run(tiles[q], tw);
+    FftStagesNT<L, NT, plan_radix(L, 0), true, ALL>::run(tiles[q], tw);
     post(q);
   }
   return part;

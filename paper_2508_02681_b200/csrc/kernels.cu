@@ -2759,6 +2759,7 @@ int launch_gpass(const Ctx& cx, int mode, cudaStream_t s) {
     }
     return 1;
   }
+  if (mode != FWDZ && gpass512e_supported(g)) return launch_gpass512e(cx, mode, s);
   if (g.dim == 3 && !g.dirz) {
     return dispatch_pow2(g.N3, [&](auto Lc) {
       constexpr int L = decltype(Lc)::value;

@@ -1,0 +1,6 @@
+# persistent elastic 512-point G pass: parity (config-4 goldens, elastic tests), then A/B against the one-tile-per-CTA kernel
+python -m pytest tests -m gpu -q -p no:cacheprovider -x -k "config4 or golden or elastic or 512" > gpurun_out/t24.log 2>&1; echo rc=$? >> gpurun_out/t24.log; tail -3 gpurun_out/t24.log
+for rep in 1 2; do for lib in "" build_ab/libunocg_g0.so; do
+  echo "== lib ${lib:-persist}"
+  UNO_LIB_PATH=$lib python tools/ktime.py --grid 512 --iters 4 --physics elastic --nrhs 1 | grep "^gpass\|sum"
+done; done 2>&1 | tee gpurun_out/kt24.log
