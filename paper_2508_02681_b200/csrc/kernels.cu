@@ -2681,13 +2681,14 @@ static bool gpass_512(const Geo& g) {
 // CTAs of the CG-mode G pass = gamma partials per load
 int gpass_nblk(const Geo& g) {
   if (g.zpad || (g.dirz && g.dim == 3)) return pencil_gmul_nblk();  // Dirichlet z: spectrum DST stage
+  if (gpass512e_supported(g)) return gpass512e_nblk(g);
   if (g.dim == 3 && !g.dirz) return g.H1 * (g.N2 / (gpass_512(g) ? G5_C : (gpass_e256(g) ? GE_COLS : 8)));
   return (int)(((long long)g.H1 * g.P3 + 7) / 8);
 }
 
 int launch_gpass_peer(const Ctx& cx, cudaStream_t s) {
   const Geo& g = cx.g;
-  if (g.dim != 3 || g.dirz || gpass_512(g) || gpass_e256(g) || (g.c == 1 && g.N3 == 256)) return -1;
+  if (g.dim != 3 || g.dirz || gpass_512(g) || gpass_e256(g) || gpass512e_supported(g) || (g.c == 1 && g.N3 == 256)) return -1;
   return dispatch_pow2(g.N3, [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
     const dim3 grid((unsigned)(g.H1 * (g.N2 / 8)), g.nrhs);

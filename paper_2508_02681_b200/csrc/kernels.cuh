@@ -68,6 +68,7 @@ int launch_gpass_peer(const Ctx& cx, cudaStream_t s);
 int launch_gpass(const Ctx& cx, int mode, cudaStream_t s);
 // persistent elastic G pass at N3 = 512 (gpass512e.cu); same per-tile gamma partials as the tiled z pass
 bool gpass512e_supported(const Geo& g);
+int gpass512e_nblk(const Geo& g);
 int launch_gpass512e(const Ctx& cx, int mode, cudaStream_t s);
 int gpass_nblk(const Geo& g);  // CTAs (gamma partials per load) of the CG-mode G pass
 // zc0/nzl: 3D thermal only, z-chunks [zc0, zc0+nzl) of g.KZC planes (nzl = 0: all)

@@ -1,0 +1,5 @@
+timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -x -k "config4 or golden or (elastic and 512)" > gpurun_out/t32.log 2>&1; echo rc=$? >> gpurun_out/t32.log; tail -3 gpurun_out/t32.log
+for rep in 1 2; do for lib in "" build_ab/libunocg_notma.so; do
+  echo "== lib ${lib:-tma}"
+  UNO_LIB_PATH=$lib timeout 300 python tools/ktime.py --grid 512 --iters 4 --physics elastic --nrhs 1 | grep "^gpass\|sum"
+done; done 2>&1 | tee gpurun_out/kt32.log
