@@ -40,9 +40,17 @@ __host__ __device__ constexpr int dst_smem_bytes() {
 // W: columns per CTA (8; 4 for the 1024-point transform of N3 = 512: two CTAs share an SM, so one's
 // loads / stores overlap the other's FFT stages — 9.70 -> 8.24 ms for the DST . G . DST stage of the
 // 512^3 elastic mixed grid, despite 168 bytes of spills at the 64-register cap).
+#ifndef UNO_DST_T256
+#define UNO_DST_T256 1  // 1024-point transform on 256 threads (1-2 butterflies each, no spills); 0: 512 threads (A/B)
+#endif
+template <int L2, int W>
+__host__ __device__ constexpr int dst_threads() {
+  return (L2 == 1024 && W == 4 && UNO_DST_T256) ? 256 : fft_threads_w(L2, W);
+}
 template <int L2, bool PAD, int MODE, int W = 8>
-__global__ void __launch_bounds__(fft_threads_w(L2, W), (W == 4 || L2 <= 512) ? 2 : 1) spec_dst_kernel(Ctx cx, double2* __restrict__ P) {
-  constexpr int T = fft_threads_w(L2, W);
+__global__ void __launch_bounds__(dst_threads<L2, W>(), (W == 4 || L2 <= 512) ? 2 : 1) spec_dst_kernel(Ctx cx, double2* __restrict__ P) {
+  constexpr int T = dst_threads<L2, W>();
+  constexpr int TT = T == fft_threads_w(L2, W) ? 0 : T;  // threads < butterflies: several per thread
   constexpr int N = L2 / 2;           // = N3
   constexpr int NP = PAD ? N : N - 1;  // stored planes
   constexpr int OFF = PAD ? 0 : 1;     // node / mode j lives at index j - OFF
@@ -85,7 +93,7 @@ __global__ void __launch_bounds__(fft_threads_w(L2, W), (W == 4 || L2 <= 512) ? 
     tile[tidx_w<W>(N, t)] = make_double2(0.0, 0.0);
   }
   __syncthreads();
-  fft_tile_w<L2, false, W>(tile, tw);
+  fft_tile_w<L2, false, W, TT>(tile, tw);
   for (int e = t; e < W * NP; e += T) {
     const int i = e / W, c = e & (W - 1), m = i + OFF;
     const double2 Y = tile[tidx_w<W>(m, c)];
@@ -136,7 +144,7 @@ int launch_pencil_dst_green(const Ctx& cx, double2* spec, int mode, cudaStream_t
     constexpr int sm = (W * L2 + L2) * (int)sizeof(double2);
     auto dst = [&](auto k) {
       if (sm > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-      k<<<grid, fft_threads_w(L2, W), sm, s>>>(cx, spec);
+      k<<<grid, dst_threads<L2, W>(), sm, s>>>(cx, spec);
     };
     auto run_dst = [&] {
       if (pad) cg ? dst(spec_dst_kernel<L2, true, CG, W>) : dst(spec_dst_kernel<L2, true, STANDALONE, W>);

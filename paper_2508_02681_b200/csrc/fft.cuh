@@ -151,54 +151,66 @@ __device__ __forceinline__ void fft_stage(double2* s, const double2* __restrict_
 template <int W>
 __device__ __forceinline__ int tidx_w(int j, int c) { return j * W + (c ^ (j & (W - 1))); }
 
-template <int L, int R, int NS, bool INV, int W>
+// TT: threads of the CTA when fewer than one per butterfly (0: one butterfly per thread, inactive
+// threads allowed).  With TT > 0 a thread runs ITEMS / TT butterflies of the stage, which is how a
+// radix-16 plan stays under its register budget without spills (1024-point DST: 256 threads at
+// 128 registers instead of 512 at 64).
+template <int L, int R, int NS, bool INV, int W, int TT = 0>
 __device__ __forceinline__ void fft_stage_w(double2* s, const double2* __restrict__ tw) {
   constexpr int NJ = L / R;
   constexpr int ITEMS = NJ * W;
+  constexpr int NH = TT > 0 ? ITEMS / TT : 1;
+  static_assert(TT == 0 || (ITEMS % TT == 0 && TT % W == 0), "whole butterflies per thread");
   const int t = threadIdx.x;
-  const bool act = t < ITEMS;
-  const int c = t & (W - 1), j = t / W;
-  const int k = j % NS;
-  double2 v[R];
+  const bool act = TT > 0 || t < ITEMS;
+  const int c = t & (W - 1), j0 = t / W;
+  double2 v[NH][R];
   if (act) {
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = s[tidx_w<W>(j + r * NJ, c)];
-    if (NS > 1) {
+    for (int h = 0; h < NH; ++h) {
+      const int j = j0 + h * (TT > 0 ? TT / W : 0), k = j % NS;
 #pragma unroll
-      for (int r = 1; r < R; ++r) {
-        double2 w = tw[r * k * (L / (NS * R))];
-        if (INV) w.y = -w.y;
-        v[r] = cmul(v[r], w);
+      for (int r = 0; r < R; ++r) v[h][r] = s[tidx_w<W>(j + r * NJ, c)];
+      if (NS > 1) {
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+          double2 w = tw[r * k * (L / (NS * R))];
+          if (INV) w.y = -w.y;
+          v[h][r] = cmul(v[h][r], w);
+        }
       }
-    }
-    if (INV) {
+      if (INV) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[r].y = -v[r].y;
-    }
-    Dft<R>::run(v);
-    if (INV) {
+        for (int r = 0; r < R; ++r) v[h][r].y = -v[h][r].y;
+      }
+      Dft<R>::run(v[h]);
+      if (INV) {
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[r].y = -v[r].y;
+        for (int r = 0; r < R; ++r) v[h][r].y = -v[h][r].y;
+      }
     }
   }
   __syncthreads();
   if (act) {
-    const int base = (j / NS) * NS * R + k;
 #pragma unroll
-    for (int r = 0; r < R; ++r) s[tidx_w<W>(base + r * NS, c)] = v[r];
+    for (int h = 0; h < NH; ++h) {
+      const int j = j0 + h * (TT > 0 ? TT / W : 0), k = j % NS, base = (j / NS) * NS * R + k;
+#pragma unroll
+      for (int r = 0; r < R; ++r) s[tidx_w<W>(base + r * NS, c)] = v[h][r];
+    }
   }
   __syncthreads();
 }
-template <int L, int NS, bool INV, int W>
+template <int L, int NS, bool INV, int W, int TT = 0>
 struct FftStagesW {
   static __device__ __forceinline__ void run(double2* s, const double2* tw) {
     constexpr int R = pick_radix(L / NS);
-    fft_stage_w<L, R, NS, INV, W>(s, tw);
-    FftStagesW<L, NS * R, INV, W>::run(s, tw);
+    fft_stage_w<L, R, NS, INV, W, TT>(s, tw);
+    FftStagesW<L, NS * R, INV, W, TT>::run(s, tw);
   }
 };
-template <int L, bool INV, int W>
-struct FftStagesW<L, L, INV, W> {
+template <int L, bool INV, int W, int TT>
+struct FftStagesW<L, L, INV, W, TT> {
   static __device__ __forceinline__ void run(double2*, const double2*) {}
 };
 
@@ -221,9 +233,9 @@ __device__ __forceinline__ void fft_tile(double2* s, const double2* tw) {
   FftStages<L, 1, INV>::run(s, tw);
 }
 
-template <int L, bool INV, int W>
+template <int L, bool INV, int W, int TT = 0>
 __device__ __forceinline__ void fft_tile_w(double2* s, const double2* tw) {
-  FftStagesW<L, 1, INV, W>::run(s, tw);
+  FftStagesW<L, 1, INV, W, TT>::run(s, tw);
 }
 __host__ __device__ constexpr int fft_threads_w(int L, int W) {
   return (W * L / min_radix(L)) < 64 ? 64 : W * L / min_radix(L);

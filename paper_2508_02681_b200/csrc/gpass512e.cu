@@ -40,7 +40,7 @@ namespace g5e {
 constexpr int W = UNO_G5E_W;  // y columns per tile (8: one CTA per SM; 4: two)
 constexpr int L = 512, NC = 3, T = 32 * W, R = 8, NJ = L / R, NH = NJ * W / T;  // NH = 2 items per thread
 constexpr int TJ = T / W;        // items j0 .. j0 + TJ - 1 per round
-__device__ __forceinline__ int tix(int j, int c) { return W == 8 ? tix(j, c) : tidx_w<W>(j, c); }
+__device__ __forceinline__ int tix(int j, int c) { return W == 8 ? tidx(j, c) : tidx_w<W>(j, c); }
 static_assert(NH == 2 && pick_radix(512) == 8 && pick_radix(64) == 8 && pick_radix(8) == 8, "512 = 8.8.8");
 
 struct Args {
