@@ -2727,6 +2727,7 @@ int launch_gpass(const Ctx& cx, int mode, cudaStream_t s) {
     });
   }
   if (g.dim == 3 && !g.dirz && g.c == 1 && g.N3 == 256) {
+    if (gpass256t_supported(g) && launch_gpass256t(cx, mode, s) > 0) return 1;  // TMA-streamed persistent kernel
     const dim3 grid((unsigned)(g.H1 * (g.N2 / 8) * g.nrhs));
     constexpr int sm = (8 * GR_CS + 256) * 16 + 256 * 8 * 8;
     if (mode == CG) {

@@ -70,6 +70,9 @@ int launch_gpass(const Ctx& cx, int mode, cudaStream_t s);
 bool gpass512e_supported(const Geo& g);
 int gpass512e_nblk(const Geo& g);
 int launch_gpass512e(const Ctx& cx, int mode, cudaStream_t s);
+// TMA-streamed thermal G pass at N3 = 256 (gpass256t.cu); -1 if the tensor maps cannot be encoded
+bool gpass256t_supported(const Geo& g);
+int launch_gpass256t(const Ctx& cx, int mode, cudaStream_t s);
 int gpass_nblk(const Geo& g);  // CTAs (gamma partials per load) of the CG-mode G pass
 // zc0/nzl: 3D thermal only, z-chunks [zc0, zc0+nzl) of g.KZC planes (nzl = 0: all)
 int launch_kapply(const Ctx& cx, int mode, const double* src, double* dst, cudaStream_t s, int zc0 = 0, int nzl = 0);
