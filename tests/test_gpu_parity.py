@@ -648,6 +648,49 @@ def test_512_point_g_pass(N, physics):
         assert rel(u[l], fx["U"][l]) <= 1e-10
 
 
+def test_persistent_elastic_g512_pass():
+    # the persistent TMA elastic G pass (gpass512e.cu: N3 = 512 with full N2 = 512 planes, config 4's
+    # kernel) on a thin grid: 576 tiles over 148 CTAs = several tiles per CTA with a ragged last
+    # round (cross-tile buffer reloads, mbarrier phases), two load cases (grid y), Parseval gamma
+    N = (16, 512, 512)
+    g, ph, mat, amp, seed = make_case(N, "elastic")
+    s = solver(ph, "elastic", mat, 2, seed, amp)
+    G = greens.ghat(g, "elastic", mat, seed, amp)
+    r = np.stack([synth.test_vector(97 + l, g.field_shape()) for l in range(2)])
+    z, rz = s.apply_precond(torch.from_numpy(r).to(dev()), want_dot=True)
+    z = z.cpu().numpy()
+    for l in range(2):
+        ref = greens.apply_precond(G, r[l])
+        assert rel(z[l], ref) <= 1e-12
+        assert abs(rz[l] - np.sum(r[l] * ref)) <= 1e-12 * abs(np.sum(r[l] * ref))
+    z2 = s.apply_precond(torch.from_numpy(r).to(dev())).cpu().numpy()
+    assert np.array_equal(z, z2)  # bitwise repeatable (a race in the ring would not be)
+
+
+@pytest.mark.parametrize("N,nrhs", [((16, 8, 256), 1), ((32, 64, 256), 3), ((64, 16, 256), 2)])
+def test_tma_thermal_g256_pass(N, nrhs):
+    # the TMA-streamed thermal G pass (gpass256t.cu: N3 = 256, config 3's kernel): fewer tiles than
+    # CTAs (prologue-only ring), several units per CTA; the symbol kept in
+    # registers across the loads of a tile; and a solve to tolerance in which the loads stop at
+    # different iterations (inactive loads drop out of the unit list)
+    g, ph, mat, amp, seed = make_case(N, "thermal")
+    s = solver(ph, "thermal", mat, nrhs, seed, amp)
+    G = greens.ghat(g, "thermal", mat, seed, amp)
+    r = np.stack([synth.test_vector(99 + l, g.field_shape()) for l in range(nrhs)])
+    z, rz = s.apply_precond(torch.from_numpy(r).to(dev()), want_dot=True)
+    z = z.cpu().numpy()
+    for l in range(nrhs):
+        ref = greens.apply_precond(G, r[l])
+        assert rel(z[l], ref) <= 1e-12
+        assert abs(rz[l] - np.sum(r[l] * ref)) <= 1e-12 * abs(np.sum(r[l] * ref))
+    assert np.array_equal(z, s.apply_precond(torch.from_numpy(r).to(dev())).cpu().numpy())
+    load = loads_for("thermal", 3, nrhs)
+    ref = homog.solve_problem(g, "thermal", ph, mat, load, seed, amp, tol=1e-8)
+    res = s.solve(load, rel_tol=1e-8)
+    for l in range(nrhs):
+        assert abs(res.reports[l]["iterations"] - ref["iterations"][l]) <= 1
+
+
 @pytest.mark.parametrize("N,physics", [((64, 64, 256), "elastic"), ((32, 32, 512), "thermal"), ((32, 512, 16), "thermal"),
                                        ((128, 64, 64), "elastic"), ((256, 64, 64), "thermal")])
 def test_repeat_bitwise_deterministic(N, physics):
