@@ -515,7 +515,8 @@ __global__ void __launch_bounds__(g5::T, 8 / g5::W) gpass512e_kernel(Ctx cx) {
 int gpass512e_nblk(const Geo& g) { return g.H1 * (g.N2 / g5e::W); }
 
 bool gpass512e_supported(const Geo& g) {
-  return UNO_G512E_PERSIST && g.dim == 3 && !g.dirz && !g.zpad && g.c == 3 && g.N3 == 512 && g.N2 == 512;
+  return UNO_G512E_PERSIST && g.dim == 3 && !g.dirz && !g.zpad && g.c == 3 && g.N3 == 512 && g.N2 % g5e::W == 0 &&
+         (g5e::W == 8 || g.N2 == 512);  // W = 8: same tiles and gamma partial layout as gpass_z_kernel<512, 3>
 }
 
 #ifndef UNO_G5E_TMA

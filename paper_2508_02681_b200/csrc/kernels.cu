@@ -2688,7 +2688,7 @@ int gpass_nblk(const Geo& g) {
 
 int launch_gpass_peer(const Ctx& cx, cudaStream_t s) {
   const Geo& g = cx.g;
-  if (g.dim != 3 || g.dirz || gpass_512(g) || gpass_e256(g) || gpass512e_supported(g) || (g.c == 1 && g.N3 == 256)) return -1;
+  if (g.dim != 3 || g.dirz || gpass_512(g) || gpass_e256(g) || (g.c == 1 && g.N3 == 256)) return -1;
   return dispatch_pow2(g.N3, [&](auto Lc) {
     constexpr int L = decltype(Lc)::value;
     const dim3 grid((unsigned)(g.H1 * (g.N2 / 8)), g.nrhs);

@@ -648,11 +648,12 @@ def test_512_point_g_pass(N, physics):
         assert rel(u[l], fx["U"][l]) <= 1e-10
 
 
-def test_persistent_elastic_g512_pass():
-    # the persistent TMA elastic G pass (gpass512e.cu: N3 = 512 with full N2 = 512 planes, config 4's
-    # kernel) on a thin grid: 576 tiles over 148 CTAs = several tiles per CTA with a ragged last
-    # round (cross-tile buffer reloads, mbarrier phases), two load cases (grid y), Parseval gamma
-    N = (16, 512, 512)
+@pytest.mark.parametrize("N", [(16, 512, 512), (16, 8, 512), (32, 16, 512)])
+def test_persistent_elastic_g512_pass(N):
+    # the persistent TMA elastic G pass (gpass512e.cu: N3 = 512, config 4's kernel) on thin grids:
+    # 576 tiles over 148 CTAs = several tiles per CTA with a ragged last round (cross-tile buffer
+    # reloads, mbarrier phases); a single y tile per plane (fewer tiles than CTAs); two load cases
+    # (grid y), Parseval gamma
     g, ph, mat, amp, seed = make_case(N, "elastic")
     s = solver(ph, "elastic", mat, 2, seed, amp)
     G = greens.ghat(g, "elastic", mat, seed, amp)

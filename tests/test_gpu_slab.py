@@ -176,6 +176,16 @@ def _ipc_rank(rank, world, port, q, phase, mat, seed, amp, loads, fixed):
         q.put((rank, res.u[0].cpu().numpy(), [r["iterations"] for r in res.reports]))
         dist.barrier()
         sv.close()
+        # ordered teardown: drop this process's mappings of the peer's buffers (torch CUDA IPC is
+        # reference counted across processes) before anyone exits — a producer that terminated
+        # with its tensors still mapped elsewhere made this test fail once in a full-suite run
+        del sv, res
+        import gc
+
+        gc.collect()
+        torch.cuda.ipc_collect()
+        torch.cuda.synchronize()
+        dist.barrier()
     finally:
         dist.destroy_process_group()
 
