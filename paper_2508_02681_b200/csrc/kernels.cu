@@ -25,6 +25,16 @@
 #include "dev_common.cuh"
 
 // minimum resident CTAs per SM requested from ptxas for the 256-point passes (occupancy experiments)
+// first-stage twiddles of the register-direct y passes read through L1 instead of a per-CTA smem copy:
+// faster for the 512-point pass (8 KB table per 4-row CTA: 1204 vs 1238 us at 512^3 elastic), slower for
+// the 256-point pass (147 vs 127 us at 256^3 x 3 loads: 15 more LDG per thread in the LSU pipe of a pass
+// that runs at 6.3 TB/s)
+#ifndef UNO_TWLDG_256
+#define UNO_TWLDG_256 0
+#endif
+#ifndef UNO_TWLDG_512
+#define UNO_TWLDG_512 1
+#endif
 #ifndef UNO_YMINB
 #define UNO_YMINB 1
 #endif
@@ -621,7 +631,9 @@ __global__ void __launch_bounds__(YR_ROWS * YR_R) ypass256_kernel(Ctx cx, int z0
   const int load = blockIdx.y;
   if (MODE == CG && !cx.st[load].active) return;
   __shared__ double2 buf[YR_ROWS * YR_RS];
+#if !UNO_TWLDG_256
   __shared__ double2 tw[L];
+#endif
   const int t = threadIdx.x;
   const int r = t >> 4, lane16 = t & 15;
   const long long nrows = (long long)g.c * g.H1 * g.P3;
@@ -640,15 +652,22 @@ __global__ void __launch_bounds__(YR_ROWS * YR_R) ypass256_kernel(Ctx cx, int z0
   }
   // twiddle table tw[k1][n1] = w_256^{n1 k1}: a quarter-warp (8 consecutive n1) reads 8
   // consecutive entries (conflict-free)
+#if !UNO_TWLDG_256
   for (int i = t; i < L; i += YR_ROWS * YR_R) tw[i] = cx.tw.y[((i & 15) * (i >> 4)) & (L - 1)];
   __syncthreads();
+#endif
   // stage 1 (thread = n1): DFT16 over n2 -> k1, twiddle w_256^{n1 k1}
   dft_reg<YR_R, INV>(v);
   {
     const int n1 = lane16;
 #pragma unroll
     for (int k1 = 1; k1 < YR_R; ++k1) {
+#if UNO_TWLDG_256
+      // straight from the 4 KB table through L1: no staging copy and no barrier before stage 1
+      const double2 w = __ldg(cx.tw.y + ((k1 * n1) & (L - 1)));
+#else
       const double2 w = tw[k1 * YR_R + n1];
+#endif
       v[k1] = cmul(v[k1], INV ? cconj(w) : w);
     }
 #pragma unroll
@@ -692,7 +711,9 @@ __global__ void __launch_bounds__(128) ypass512_kernel(Ctx cx, int z0, int zc) {
   const int load = blockIdx.y;
   if (MODE == CG && !cx.st[load].active) return;
   __shared__ double2 buf[Y5_ROWS * Y5_RS];
+#if !UNO_TWLDG_512
   __shared__ double2 tw[16 * 32];  // [k1][n1] = w_512^{n1 k1}
+#endif
   __shared__ double2 tw32[16];     // w_32^r
   const int t = threadIdx.x;
   const int r = t >> 5, l32 = t & 31;
@@ -710,13 +731,21 @@ __global__ void __launch_bounds__(128) ypass512_kernel(Ctx cx, int z0, int zc) {
 #pragma unroll
     for (int n2 = 0; n2 < 16; ++n2) v[n2] = __ldcg(rowp + l32 + 32 * n2);
   }
+#if !UNO_TWLDG_512
   for (int i = t; i < 16 * 32; i += 128) tw[i] = cx.tw.y[((i & 31) * (i >> 5)) & (L - 1)];
+#endif
   if (t < 16) tw32[t] = cx.tw.y[16 * t];
+#if !UNO_TWLDG_512
   __syncthreads();
+#endif
   dft_reg<16, INV>(v);  // thread = n1: over n2 -> k1
 #pragma unroll
   for (int k1 = 1; k1 < 16; ++k1) {
+#if UNO_TWLDG_512
+    const double2 w = __ldg(cx.tw.y + ((k1 * l32) & (L - 1)));  // 8 KB table through L1 (see ypass256_kernel)
+#else
     const double2 w = tw[k1 * 32 + l32];
+#endif
     v[k1] = cmul(v[k1], INV ? cconj(w) : w);
   }
   double2* Tr = buf + r * Y5_RS;
