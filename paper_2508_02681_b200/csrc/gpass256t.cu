@@ -29,6 +29,9 @@
 
 namespace uno {
 
+#ifndef UNO_SERP
+#define UNO_SERP 1  // reversed tile order (see ypass256_kernel); 0: A/B
+#endif
 #ifndef UNO_G256T_NB
 #define UNO_G256T_NB 2  // ring buffers per CTA: 2 (three CTAs per SM, 168 registers) or 3 (two CTAs per SM)
 #endif
@@ -90,7 +93,7 @@ struct Args {
   const CUtensorMap* sym;   // doubles [1][kx][z][y], box 8 x 256 (L2 prefetch only)
   const double* gtab;
   unsigned tiles, mbar;     // shared-memory addresses of buffer 0 and of the NB mbarriers
-  int N2, N3, M, ntile_y;
+  int N2, N3, M, ntile_y, ntiles;
   int nact;                 // active load cases
   int act[kMaxRhs];         // their indices
 };
@@ -99,6 +102,9 @@ struct Args {
 __device__ __forceinline__ void unit_of(const Args& a, long long u, int& tile, int& load) {
   const long long gt = u / a.nact;
   tile = (int)(blockIdx.x + gt * gridDim.x);
+#if UNO_SERP
+  tile = a.ntiles - 1 - tile;  // last k_x planes first: they are what the forward y pass left in L2
+#endif
   load = a.act[(int)(u - gt * a.nact)];
 }
 // thread 0: load unit (tile, load) into ring buffer b; the first load of a tile also pulls the
@@ -140,6 +146,7 @@ __global__ void __launch_bounds__(g2t::T, g2t::kCtasPerSm) gpass256t_kernel(Ctx 
   }
   if (a.nact == 0) return;
   const int ntiles = g.H1 * a.ntile_y;
+  a.ntiles = ntiles;
   const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   const long long nunits = (long long)my_tiles * a.nact;
   for (int i = t; i < L; i += T) tw[i] = cx.tw.z[i];

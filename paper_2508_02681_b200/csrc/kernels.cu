@@ -29,6 +29,9 @@
 // faster for the 512-point pass (8 KB table per 4-row CTA: 1204 vs 1238 us at 512^3 elastic), slower for
 // the 256-point pass (147 vs 127 us at 256^3 x 3 loads: 15 more LDG per thread in the LSU pipe of a pass
 // that runs at 6.3 TB/s)
+#ifndef UNO_SERP
+#define UNO_SERP 1  // L2-aware launch order of the y / G passes (0: A/B)
+#endif
 #ifndef UNO_TWLDG_256
 #define UNO_TWLDG_256 0
 #endif
@@ -628,7 +631,17 @@ template <bool INV, int MODE, bool PEER = false>
 __global__ void __launch_bounds__(YR_ROWS * YR_R) ypass256_kernel(Ctx cx, int z0, int zc) {
   constexpr int L = 256;
   const Geo g = cx.g;
+#if UNO_SERP
+  // load fastest in the launch order (the hardware issues CTAs x-fastest): the row blocks of all load
+  // cases advance together through the k_x planes, so the tail this pass leaves in L2 holds the last
+  // planes of every load — where the reversed G pass starts (and where the inverse y pass follows it)
+  const unsigned lin = blockIdx.y * gridDim.x + blockIdx.x;
+  const int load = (int)(lin % gridDim.y);
+  const unsigned bxl = lin / gridDim.y;
+#else
   const int load = blockIdx.y;
+  const unsigned bxl = blockIdx.x;
+#endif
   if (MODE == CG && !cx.st[load].active) return;
   __shared__ double2 buf[YR_ROWS * YR_RS];
 #if !UNO_TWLDG_256
@@ -637,11 +650,11 @@ __global__ void __launch_bounds__(YR_ROWS * YR_R) ypass256_kernel(Ctx cx, int z0
   const int t = threadIdx.x;
   const int r = t >> 4, lane16 = t & 15;
   const long long nrows = (long long)g.c * g.H1 * g.P3;
-  long long row0 = (long long)blockIdx.x * YR_ROWS;  // row = (comp, kx, z)
+  long long row0 = (long long)bxl * YR_ROWS;  // row = (comp, kx, z)
   if (zc > 0) {
     const int nb = zc >> 3;
-    const int q = blockIdx.x / nb;
-    row0 = (long long)q * g.P3 + z0 + (blockIdx.x - q * nb) * 8;
+    const int q = bxl / nb;
+    row0 = (long long)q * g.P3 + z0 + (bxl - q * nb) * 8;
   }
   const bool ok = row0 + r < nrows;
   double2* rowp = cx.spec + (long long)load * g.c * g.nspec + (row0 + r) * L;
