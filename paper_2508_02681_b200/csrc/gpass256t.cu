@@ -42,7 +42,7 @@ namespace uno {
 namespace g2t {
 constexpr int L = 256, T = 128, R = 16, NJ = L / R, NB = UNO_G256T_NB;  // NB ring buffers
 constexpr unsigned kTileBytes = 8 * L * 16;
-constexpr int kCtasPerSm = NB == 2 ? 3 : 2, kCtas = 148 * kCtasPerSm;
+constexpr int kCtasPerSm = NB == 1 ? 4 : (NB == 2 ? 3 : 2), kCtas = 148 * kCtasPerSm;
 static_assert(NJ * kTile == T, "one butterfly per thread in every pass");
 
 __device__ __forceinline__ unsigned sm_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
@@ -225,6 +225,12 @@ __global__ void __launch_bounds__(g2t::T, g2t::kCtasPerSm) gpass256t_kernel(Ctx 
     if (t == 0) {
       tma_store(a.spec, 2 * y0, 0, kx, load, a.tiles + b * kTileBytes);
       bulk_commit();
+      if (NB == 1 && u + 1 < nunits) {  // single buffer (four CTAs per SM cover each other's waits)
+        bulk_wait_read<0>();
+        int tile2, load2;
+        unit_of(a, u + 1, tile2, load2);
+        load_unit(a, 0, tile2, load2, (u + 1) % a.nact == 0);
+      }
       if (NB == 3 && u >= 1 && u + 2 < nunits) {  // the store of unit u - 1 has read its buffer: reload it for unit u + 2
         bulk_wait_read<1>();
         int tile2, load2;
