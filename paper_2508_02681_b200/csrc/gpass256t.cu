@@ -43,7 +43,7 @@ namespace g2t {
 constexpr int L = 256, T = 128, R = 16, NJ = L / R, NB = UNO_G256T_NB;  // NB ring buffers
 constexpr unsigned kTileBytes = 8 * L * 16;
 constexpr int kCtasPerSm = NB == 1 ? 4 : (NB == 2 ? 3 : 2), kCtas = 148 * kCtasPerSm;
-static_assert(NJ * kTile == T, "one butterfly per thread in every pass");
+static_assert(NJ * kTile == T && T == 128, "one butterfly per thread in every pass; four warps (gamma partial)");
 
 __device__ __forceinline__ unsigned sm_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned mb, unsigned count) {
@@ -210,7 +210,13 @@ __global__ void __launch_bounds__(g2t::T, g2t::kCtasPerSm) gpass256t_kernel(Ctx 
     dft_reg_inv_inline<R>(v);
 #pragma unroll
     for (int r = 0; r < R; ++r) s[tidx(j + r * NJ, c)] = v[r];  // canonical row 16 j + r, parked
+    // gamma partial of the unit (same tree and order as block_reduce), riding on the barrier the
+    // stages need anyway instead of two barriers of its own
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_down_sync(0xffffffffu, part, o);
+    if ((t & 31) == 0) red_sh[t >> 5] = part;
     __syncthreads();
+    if (t == 0) red_partials(cx.sc, RED_GAMMA, load)[tile] = ((red_sh[0] + red_sh[1]) + red_sh[2]) + red_sh[3];
     // P3: last inverse stage (span 16): canonical rows j + 16 r are parked at rows 16 j + r
 #pragma unroll
     for (int r = 0; r < R; ++r) v[r] = s[tidx(j * R + r, c)];
@@ -238,7 +244,6 @@ __global__ void __launch_bounds__(g2t::T, g2t::kCtasPerSm) gpass256t_kernel(Ctx 
         load_unit(a, (int)((u + 2) % NB), tile2, load2, (u + 2) % a.nact == 0);
       }
     }
-    partial_write<false>(cx, RED_GAMMA, load, tile, part, red_sh);  // same partial layout as gpass256_kernel
   }
   if (t == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
